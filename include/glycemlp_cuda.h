@@ -1,0 +1,134 @@
+/*
+ * glycemlp_cuda.h -- C ABI of libglycemlp_cuda.so, the B200 (sm_100a)
+ * replacement for the glycemlp training hot path.
+ *
+ * Reference boundary (all paths relative to /root/reference/pkg/src/glycemlp):
+ *   backend.run_train_segment(w_ih2d, w_ho2d, feats2d, targets, epochs, lr, kind)
+ *                                                         backend.py:208-234
+ *   kernels.train_segment_seq / train_segment_par        kernels.py:264-349
+ *   kernels.eval_counts(w_ih2d, w_ho2d, feats2d, labels) kernels.py:352-375
+ *   trainer._confusion                                    trainer.py:94-97
+ *
+ * Conventions
+ *   - Weight layout is the reference's (network.py:84-90): w_ih is
+ *     hidden x (input+1) row-major with the bias in the trailing slot, w_ho is
+ *     outputs x (hidden+1). Both are float32 and updated IN PLACE.
+ *   - Return 0 on success, a negative GLX_ERR_* code otherwise; the message
+ *     is in glx_last_error() (thread-local). Codes map onto the reference's
+ *     exception types (errors.py:16-25).
+ *   - "host" entry points take host pointers, copy in, run, copy out and
+ *     synchronise (the reference's synchronous in-place contract).
+ *   - "device" entry points take device pointers owned by the caller and a
+ *     cudaStream_t (NULL = legacy default stream); they are asynchronous.
+ *   - numerics: GLX_FP32 (packed-FP32 FMA, fast sigmoid; within 1e-4
+ *     max(1,|w|)-relative of the reference) or GLX_REF64 (the reference's
+ *     f64 op order, f32 stores).
+ */
+#ifndef GLYCEMLP_CUDA_H
+#define GLYCEMLP_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GLX_OK 0
+#define GLX_ERR_SHAPE (-1)   /* ShapeError       (errors.py:20) */
+#define GLX_ERR_INVALID (-2) /* ValidationError  (errors.py:16) */
+#define GLX_ERR_NUMERIC (-3) /* NumericError     (errors.py:24) */
+#define GLX_ERR_CUDA (-4)    /* RuntimeError: CUDA / NCCL failure */
+#define GLX_ERR_NOMEM (-5)   /* MemoryError */
+
+#define GLX_FP32 0
+#define GLX_REF64 1
+
+#define GLX_FLAG_CACHE_INPUTS 1 /* host API: keep feats/targets resident keyed by host pointer */
+
+const char* glx_last_error(void);
+int glx_version(void);
+int glx_device_count(void);
+int glx_sm_count(int device);
+
+/* ------------------------------------------------------------------ host API */
+
+/* Drop-in for backend.run_train_segment (backend.py:208-234) /
+ * kernels.train_segment_seq|par (kernels.py:264-349): `epochs` passes of
+ * per-instance online SGD in dataset order, weights updated in place.
+ * feats: rows x input_dim f32, targets: rows f32 in {0,1}. */
+int glx_run_train_segment(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
+                          int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr, int32_t numerics,
+                          int32_t device, int32_t flags);
+
+/* Full-batch gradient descent: every
+ * epoch computes the mean gradient over all rows at the epoch-start weights
+ * and applies W <- W - lr * grad. FP32 numerics. stats_hist (host, may be
+ * NULL) receives 5 doubles per epoch: loss sum, tp, tn, fp, fn at the
+ * epoch-start weights. */
+int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
+                                int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr,
+                                double* stats_hist, int32_t device, int32_t flags);
+
+/* Drop-in for kernels.eval_counts (kernels.py:352-375) plus the loss sum.
+ * counts4 = (tp, tn, fp, fn) for output_dim 1, (correct, wrong, 0, 0) for
+ * output_dim > 1 (argmax). labels: rows u8. */
+int glx_eval_counts(const float* w_ih, const float* w_ho, const float* feats, const uint8_t* labels, int64_t rows,
+                    int32_t input_dim, int32_t hidden_dim, int32_t output_dim, int32_t numerics, int64_t* counts4,
+                    double* loss_sum, int32_t device, int32_t flags);
+
+/* Drop the resident-input cache of GLX_FLAG_CACHE_INPUTS (all devices). */
+void glx_cache_clear(void);
+
+/* ---------------------------------------------------------------- device API */
+
+/* Online SGD on device buffers (single network). X: N x D, T: N. */
+int glx_train_online(float* w_ih, float* w_ho, const float* X, const float* T, int64_t N, int32_t D, int32_t H,
+                     int64_t epochs, double lr, int32_t numerics, void* stream);
+
+/* n_nets independent online networks on one dataset (config 3): network n
+ * owns w_pool[w_off[n] ...] = [w_ih (H_n x (D+1)) | w_ho (H_n + 1)].
+ * H_per_net and w_off are HOST arrays; w_pool, X, T are device pointers. */
+int glx_train_sweep(int64_t n_nets, const int32_t* H_per_net, const int64_t* w_off, float* w_pool, const float* X,
+                    const float* T, int64_t N, int32_t D, int64_t epochs, double lr, int32_t numerics, void* stream);
+
+/* Packed row layout of the streaming kernels: row r at Xp + r*ld with
+ * ld = glx_packed_ld(D), holding [x_0..x_{D-1}, 1.0, target, 0...]. */
+int32_t glx_packed_ld(int32_t D);
+int glx_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int32_t D, float* Xp,
+                  void* stream);
+
+/* Full-batch GD on packed rows. stats_hist: device double[5*epochs] or NULL.
+ * nonfinite: device int32 set to 1 if any updated weight is non-finite. */
+int glx_train_batch(float* w_ih, float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H, int64_t epochs,
+                    double lr, double* stats_hist, int32_t* nonfinite, void* stream);
+
+/* Data-parallel split of one epoch (config 4): glx_batch_grad writes this
+ * rank's gradient SUM over its N rows (not divided by N) into grad (device
+ * double[glx_batch_grad_len]), laid out as [dW1 (H(D+1)) | dW2 (H+1) | loss,
+ * tp, tn, fp, fn]; after an all-reduce(sum) across ranks, glx_batch_apply
+ * performs W <- f32(f64(W) - lr_over_n * grad) with n the global row count. */
+int64_t glx_batch_grad_len(int32_t D, int32_t H);
+int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
+                   double* grad, void* stream);
+int glx_batch_apply(float* w_ih, float* w_ho, const double* grad, int32_t D, int32_t H, double lr_over_n,
+                    int32_t* nonfinite, void* stream);
+
+/* Evaluation on device buffers; results land in device memory
+ * (counts4: uint64[4] accumulated, so zero it first; loss: double[1]). */
+int glx_eval(const float* w_ih, const float* w_ho, const float* X, const uint8_t* labels, int64_t N, int32_t D,
+             int32_t H, int32_t K, uint64_t* counts4, double* loss, void* stream);
+/* Fast FP32 evaluation on packed rows (fused streaming forward);
+ * stats: device double[5] = loss, tp, tn, fp, fn. */
+int glx_eval_packed(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
+                    double* stats, void* stream);
+
+/* ------------------------------------------------------------ diagnostics */
+/* Number of CUDA kernels this library has launched (for launch accounting). */
+uint64_t glx_launch_count(void);
+/* FFMA2 throughput microbenchmark on `device`: returns TFLOP/s. */
+int glx_fp32_peak(int32_t device, int32_t iters, double* tflops, double* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GLYCEMLP_CUDA_H */

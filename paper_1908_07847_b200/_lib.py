@@ -1,0 +1,107 @@
+"""ctypes binding of libglycemlp_cuda.so (declarations: include/glycemlp_cuda.h).
+
+The product path has no CPU fallback: if the library is missing, fails to
+load, or no CUDA device is visible, every compute call raises RuntimeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from pathlib import Path
+
+import numpy as np
+
+from .errors import NumericError, ShapeError, ValidationError
+
+LIB_PATH = Path(__file__).resolve().parent / "libglycemlp_cuda.so"
+
+GLX_OK = 0
+GLX_ERR_SHAPE = -1
+GLX_ERR_INVALID = -2
+GLX_ERR_NUMERIC = -3
+GLX_ERR_CUDA = -4
+GLX_ERR_NOMEM = -5
+
+GLX_FP32 = 0
+GLX_REF64 = 1
+GLX_FLAG_CACHE_INPUTS = 1
+
+NUMERICS = {"fp32": GLX_FP32, "ref64": GLX_REF64}
+
+# every exported symbol of include/glycemlp_cuda.h with (restype, argtypes)
+_vp = ctypes.c_void_p
+_i32 = ctypes.c_int32
+_i64 = ctypes.c_int64
+_u64 = ctypes.c_uint64
+_dbl = ctypes.c_double
+_int = ctypes.c_int
+SIGNATURES = {
+    "glx_last_error": (ctypes.c_char_p, []),
+    "glx_version": (_int, []),
+    "glx_device_count": (_int, []),
+    "glx_sm_count": (_int, [_int]),
+    "glx_run_train_segment": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _i32, _i32, _i32]),
+    "glx_run_train_segment_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _vp, _i32, _i32]),
+    "glx_eval_counts": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32]),
+    "glx_cache_clear": (None, []),
+    "glx_train_online": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _i32, _vp]),
+    "glx_train_sweep": (_int, [_i64, _vp, _vp, _vp, _vp, _vp, _i64, _i32, _i64, _dbl, _i32, _vp]),
+    "glx_packed_ld": (_i32, [_i32]),
+    "glx_pack_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
+    "glx_train_batch": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _vp, _vp, _vp]),
+    "glx_batch_grad_len": (_i64, [_i32, _i32]),
+    "glx_batch_grad": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "glx_batch_apply": (_int, [_vp, _vp, _vp, _i32, _i32, _dbl, _vp, _vp]),
+    "glx_eval": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "glx_eval_packed": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "glx_launch_count": (_u64, []),
+    "glx_fp32_peak": (_int, [_i32, _i32, _vp, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load(require_device: bool = True):
+    """Load the library (once). Raises RuntimeError if it cannot run here."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            L = ctypes.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(L, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = L
+    if require_device and _lib.glx_device_count() < 1:
+        raise RuntimeError("no CUDA device visible: the glycemlp B200 engine has no CPU fallback")
+    return _lib
+
+
+def check(rc: int) -> None:
+    """Map a GLX_ERR_* return code onto the reference's exception types."""
+    if rc == GLX_OK:
+        return
+    msg = (_lib.glx_last_error() or b"").decode(errors="replace")
+    if rc == GLX_ERR_SHAPE:
+        raise ShapeError(msg)
+    if rc == GLX_ERR_INVALID:
+        raise ValidationError(msg)
+    if rc == GLX_ERR_NUMERIC:
+        raise NumericError(msg)
+    if rc == GLX_ERR_NOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"glycemlp CUDA error: {msg}")
+
+
+def ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+def launch_count() -> int:
+    return int(load(require_device=False).glx_launch_count())

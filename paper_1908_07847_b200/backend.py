@@ -1,0 +1,177 @@
+"""Execution backend: the drop-in for the reference's engine selection and
+training-segment entry point, running on the B200 through the C ABI.
+
+Reference counterparts (/root/reference/pkg/src/glycemlp/):
+  BackendKind / sequential() / parallel()      backend.py:44-70
+  run_train_segment(w_ih2d, w_ho2d, feats2d, targets, epochs, lr, kind)
+                                               backend.py:208-234
+  kernels.eval_counts(w_ih2d, w_ho2d, feats2d, labels)
+                                               kernels.py:352-375
+
+The engine name is "cuda" (the reference rejects any other name than its two
+CPU engines, test_backend.py:24-25, so the device engine has its own name).
+numerics="ref64" reproduces the reference's float64 operation order (the
+result the reference's sequential and parallel engines both produce);
+numerics="fp32" runs packed-FP32 FMA with a MUFU sigmoid, within the
+1e-4 max(1,|w|)-relative tolerance of SURVEY.md 8(c). sequential() and
+parallel() return the "ref64" device engine so reference call sites keep
+their exact semantics; there is no CPU engine in this package.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .errors import ShapeError, ValidationError
+
+CUDA = "cuda"
+ONLINE = "online"
+BATCH = "batch"
+
+
+@dataclass(frozen=True)
+class BackendKind:
+    """Device engine selector.
+
+    name      always "cuda"
+    workers   GPUs used by the sharded entry points (sweep, data parallel);
+              a single training segment runs on `device`
+    numerics  "fp32" (default) or "ref64"
+    device    CUDA device ordinal for the host-pointer entry points
+    """
+
+    name: str = CUDA
+    workers: int = 1
+    numerics: str = "fp32"
+    device: int = 0
+
+    def __post_init__(self) -> None:
+        if self.name != CUDA:
+            raise ValidationError(f"backend must be {CUDA!r}, got {self.name!r}")
+        if self.workers < 1:
+            raise ValidationError(f"worker_count must be >= 1, got {self.workers}")
+        if self.numerics not in _lib.NUMERICS:
+            raise ValidationError(f"numerics must be one of {tuple(_lib.NUMERICS)}, got {self.numerics!r}")
+        if self.device < 0:
+            raise ValidationError(f"device must be >= 0, got {self.device}")
+
+    @property
+    def effective_workers(self) -> int:
+        return self.workers
+
+
+def cuda(device: int = 0, numerics: str = "fp32", workers: int = 1) -> BackendKind:
+    return BackendKind(CUDA, workers, numerics, device)
+
+
+def sequential() -> BackendKind:
+    """Reference-exact numerics on the device (replaces the CPU sequential engine)."""
+    return BackendKind(CUDA, 1, "ref64", 0)
+
+
+def parallel(workers: int | None = None) -> BackendKind:
+    """Reference-exact numerics on the device (replaces the CPU neuron-parallel engine)."""
+    return BackendKind(CUDA, 1, "ref64", 0)
+
+
+def _f32c(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _check_weights(w_ih2d: np.ndarray, w_ho2d: np.ndarray) -> tuple[int, int]:
+    for name, w in (("w_ih2d", w_ih2d), ("w_ho2d", w_ho2d)):
+        if w.dtype != np.float32 or w.ndim != 2 or not w.flags.c_contiguous or not w.flags.writeable:
+            raise ShapeError(f"{name} must be a writeable C-contiguous 2-D float32 array (updated in place)")
+    H, d1 = w_ih2d.shape
+    if w_ho2d.shape != (1, H + 1):
+        raise ShapeError(f"w_ho2d shape {w_ho2d.shape} != (1, {H + 1})")
+    return d1 - 1, H
+
+
+def _check_inputs(w_ih2d, feats2d, targets):
+    if feats2d.ndim != 2 or feats2d.shape[1] != w_ih2d.shape[1] - 1:
+        raise ShapeError(f"feature count {feats2d.shape[-1]} != input_dim {w_ih2d.shape[1] - 1}")
+    if targets.shape[0] != feats2d.shape[0]:
+        raise ShapeError("targets length must match feature rows")
+
+
+def _cache_flag(enabled: bool, *arrays: np.ndarray) -> int:
+    # resident-input reuse keys on host pointers: only safe for read-only
+    # arrays that outlive the caller's sequence of calls (trainer.train)
+    return _lib.GLX_FLAG_CACHE_INPUTS if enabled and all(not a.flags.writeable for a in arrays) else 0
+
+
+def clear_input_cache() -> None:
+    _lib.load(require_device=False).glx_cache_clear()
+
+
+def run_train_segment(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, targets: np.ndarray,
+                      epochs: int, lr: float, kind: BackendKind, *, cache_inputs: bool = False) -> None:
+    """`epochs` passes of per-instance SGD in dataset order, weights updated in place.
+
+    Same contract as backend.py:208-234: ShapeError on a feature-count or
+    target-length mismatch, synchronous, non-finite weights are left for the
+    caller to detect.
+    """
+    _check_inputs(w_ih2d, feats2d, targets)
+    D, H = _check_weights(w_ih2d, w_ho2d)
+    L = _lib.load()
+    X = feats2d if (feats2d.dtype == np.float32 and feats2d.flags.c_contiguous) else _f32c(feats2d)
+    T = targets if (targets.dtype == np.float32 and targets.flags.c_contiguous) else _f32c(targets)
+    _lib.check(L.glx_run_train_segment(
+        _lib.ptr(w_ih2d), _lib.ptr(w_ho2d), _lib.ptr(X), _lib.ptr(T), X.shape[0], D, H, int(epochs), float(lr),
+        _lib.NUMERICS[kind.numerics], kind.device, _cache_flag(cache_inputs, X, T)))
+
+
+def run_train_segment_batch(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, targets: np.ndarray,
+                            epochs: int, lr: float, kind: BackendKind, stats: np.ndarray | None = None, *,
+                            cache_inputs: bool = False) -> None:
+    """`epochs` of full-batch gradient descent (mean gradient over all rows), in place.
+
+    SURVEY.md 8(a) a13 (no reference implementation; parity against the
+    oracle restatement). `stats`, if given, is a float64 (epochs, 5) array
+    receiving loss sum, tp, tn, fp, fn at each epoch's starting weights.
+    """
+    _check_inputs(w_ih2d, feats2d, targets)
+    D, H = _check_weights(w_ih2d, w_ho2d)
+    L = _lib.load()
+    X = feats2d if (feats2d.dtype == np.float32 and feats2d.flags.c_contiguous) else _f32c(feats2d)
+    T = targets if (targets.dtype == np.float32 and targets.flags.c_contiguous) else _f32c(targets)
+    sp = None
+    if stats is not None:
+        if stats.dtype != np.float64 or stats.shape != (int(epochs), 5) or not stats.flags.c_contiguous:
+            raise ShapeError(f"stats must be a C-contiguous float64 array of shape ({int(epochs)}, 5)")
+        sp = _lib.ptr(stats)
+    _lib.check(L.glx_run_train_segment_batch(
+        _lib.ptr(w_ih2d), _lib.ptr(w_ho2d), _lib.ptr(X), _lib.ptr(T), X.shape[0], D, H, int(epochs), float(lr),
+        sp, kind.device, _cache_flag(cache_inputs, X, T)))
+
+
+def eval_counts_loss(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, labels: np.ndarray,
+                     kind: BackendKind | None = None) -> tuple[tuple[int, int, int, int], float]:
+    """((tp, tn, fp, fn), sum of 0.5*(t-o)^2) with poor (label 1) as the positive class."""
+    kind = kind or sequential()
+    if feats2d.ndim != 2 or feats2d.shape[1] != w_ih2d.shape[1] - 1:
+        raise ShapeError(f"feature count {feats2d.shape[-1]} != input_dim {w_ih2d.shape[1] - 1}")
+    if labels.shape[0] != feats2d.shape[0]:
+        raise ShapeError("labels length must match feature rows")
+    H, d1 = w_ih2d.shape
+    K = w_ho2d.shape[0]
+    L = _lib.load()
+    W1, W2 = _f32c(w_ih2d), _f32c(w_ho2d)
+    X = _f32c(feats2d)
+    Y = np.ascontiguousarray(labels, dtype=np.uint8)
+    counts = np.zeros(4, dtype=np.int64)
+    loss = np.zeros(1, dtype=np.float64)
+    _lib.check(L.glx_eval_counts(_lib.ptr(W1), _lib.ptr(W2), _lib.ptr(X), _lib.ptr(Y), X.shape[0], d1 - 1, H, K,
+                                 _lib.NUMERICS[kind.numerics], _lib.ptr(counts), _lib.ptr(loss), kind.device, 0))
+    return (int(counts[0]), int(counts[1]), int(counts[2]), int(counts[3])), float(loss[0])
+
+
+def eval_counts(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, labels: np.ndarray,
+                kind: BackendKind | None = None) -> tuple[int, int, int, int]:
+    """Drop-in for kernels.eval_counts (kernels.py:352-375)."""
+    return eval_counts_loss(w_ih2d, w_ho2d, feats2d, labels, kind)[0]

@@ -1,0 +1,579 @@
+// glx_abi.cu -- the extern "C" boundary of libglycemlp_cuda.so (include/glycemlp_cuda.h).
+//
+// Host entry points mirror the reference's synchronous in-place contract of
+// backend.run_train_segment (/root/reference/pkg/src/glycemlp/backend.py:208-234)
+// and kernels.eval_counts (kernels.py:352-375); device entry points take
+// caller-owned device buffers and a stream. Library-owned scratch (per-CTA
+// gradient partials, kernel weight copies, descriptors) is cached per
+// (device, stream) and only ever grows.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "glx_kernels.h"
+#include "glycemlp_cuda.h"
+
+using namespace glx;
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<uint64_t> g_launches{0};
+
+int set_err(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define GLX_CK(expr)                                                                                       \
+    do {                                                                                                   \
+        cudaError_t e_ = (expr);                                                                           \
+        if (e_ != cudaSuccess)                                                                             \
+            return set_err(GLX_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, \
+                           __LINE__);                                                                      \
+    } while (0)
+
+#define GLX_LAUNCH(expr)          \
+    do {                          \
+        GLX_CK(expr);             \
+        g_launches.fetch_add(1);  \
+    } while (0)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes <= cap && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes < 256 ? 256 : bytes);
+        if (e == cudaSuccess) cap = bytes < 256 ? 256 : bytes;
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return reinterpret_cast<T*>(p);
+    }
+};
+
+// scratch tied to one (device, stream): stream order serialises its reuse
+struct Workspace {
+    DevBuf part, wk, desc, ctan, losspart, grad;
+};
+
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace*> g_ws;
+
+Workspace* workspace(cudaStream_t st) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_ws_mu);
+    auto key = std::make_pair(dev, st);
+    auto it = g_ws.find(key);
+    if (it != g_ws.end()) return it->second;
+    Workspace* w = new Workspace();
+    g_ws[key] = w;
+    return w;
+}
+
+int sm_count_current() {
+    int dev = 0, n = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+
+// host-API state per device: own stream, staging buffers, optional input cache
+struct HostState {
+    std::mutex mu;
+    cudaStream_t stream = nullptr;
+    DevBuf w1, w2, x, t, lab, xp, stats, cnt, loss, flag, ex, exp_;
+    const void* key_x = nullptr;
+    size_t bytes_x = 0;
+    const void* key_t = nullptr;
+    size_t bytes_t = 0;
+    const void* key_xp = nullptr;  // packed rows built from (key_x, key_t)
+};
+HostState g_host[64];
+
+// ------------------------------------------------------------ online launch
+struct NetReq {
+    float* w_ih;
+    float* w_ho;
+    int H;
+    int idx;
+};
+
+int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t N, int D, int64_t epochs, double lr,
+               bool ref64, cudaStream_t st) {
+    const int dp = online_dp_for(D);
+    if (dp < 0) return set_err(GLX_ERR_INVALID, "online kernel supports input_dim <= 63, got %d", D);
+    for (auto& n : nets)
+        if (n.H < 1 || n.H > 512) return set_err(GLX_ERR_INVALID, "online kernel supports 1 <= hidden_dim <= 512, got %d", n.H);
+    const size_t xbytes = ((size_t)N * dp * 4 + (size_t)N * 4 + 15) / 16 * 16;
+    const bool x_in_smem = xbytes <= 160 * 1024;
+    // first-fit decreasing packing of networks into CTAs of <= 16 warps / 15 networks
+    std::stable_sort(nets.begin(), nets.end(), [](const NetReq& a, const NetReq& b) { return a.H > b.H; });
+    struct Cta {
+        int warps = 0;
+        size_t scratch = 0;
+        std::vector<int> members;
+    };
+    std::vector<Cta> ctas;
+    std::vector<OnlineNetDesc> desc(nets.size());
+    size_t open_from = 0;  // CTAs before this index are full
+    for (size_t n = 0; n < nets.size(); n++) {
+        const int nw = (nets[n].H + 31) / 32;
+        const size_t scr = (online_scratch_bytes(nets[n].H, ref64) + 15) / 16 * 16;
+        size_t c = open_from;
+        for (; c < ctas.size(); c++)
+            if (ctas[c].warps + nw <= 16 && ctas[c].members.size() < 15) break;
+        if (c == ctas.size()) ctas.emplace_back();
+        Cta& C = ctas[c];
+        OnlineNetDesc& d = desc[n];
+        d.w_ih = nets[n].w_ih;
+        d.w_ho = nets[n].w_ho;
+        d.H = nets[n].H;
+        d.warp0 = C.warps;
+        d.nwarps = nw;
+        d.bar_id = 1 + (int)C.members.size();
+        d.scratch_off = (int)((x_in_smem ? xbytes : 0) + C.scratch);
+        d.pad = 0;
+        C.warps += nw;
+        C.scratch += scr;
+        C.members.push_back((int)n);
+        while (open_from < ctas.size() && ctas[open_from].warps >= 16) open_from++;
+    }
+    // descriptors grouped per CTA
+    std::vector<OnlineNetDesc> ordered;
+    std::vector<int2> cta_nets;
+    int max_warps = 0;
+    size_t max_scratch = 0;
+    for (auto& C : ctas) {
+        cta_nets.push_back(make_int2((int)ordered.size(), (int)C.members.size()));
+        for (int m : C.members) ordered.push_back(desc[m]);
+        max_warps = std::max(max_warps, C.warps);
+        max_scratch = std::max(max_scratch, C.scratch);
+    }
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->desc.ensure(ordered.size() * sizeof(OnlineNetDesc)));
+    GLX_CK(ws->ctan.ensure(cta_nets.size() * sizeof(int2)));
+    GLX_CK(cudaMemcpyAsync(ws->desc.p, ordered.data(), ordered.size() * sizeof(OnlineNetDesc),
+                           cudaMemcpyHostToDevice, st));
+    GLX_CK(cudaMemcpyAsync(ws->ctan.p, cta_nets.data(), cta_nets.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
+    OnlineLaunch L;
+    L.nets = ws->desc.as<OnlineNetDesc>();
+    L.cta_nets = ws->ctan.as<int2>();
+    L.n_ctas = (int)ctas.size();
+    L.threads = max_warps * 32;
+    L.smem_bytes = (x_in_smem ? xbytes : 0) + max_scratch;
+    L.x_in_smem = x_in_smem;
+    L.ref64 = ref64;
+    L.X = X;
+    L.T = T;
+    L.N = N;
+    L.D = D;
+    L.epochs = epochs;
+    L.lr = lr;
+    GLX_LAUNCH(launch_online(L, st));
+    // the copies above read pageable host memory that dies with this frame:
+    // cudaMemcpyAsync from pageable memory has finished staging on return.
+    return GLX_OK;
+}
+
+int check_dims(int64_t rows, int D, int H) {
+    if (rows < 0) return set_err(GLX_ERR_SHAPE, "rows must be >= 0, got %lld", (long long)rows);
+    if (D < 1) return set_err(GLX_ERR_SHAPE, "input_dim must be >= 1, got %d", D);
+    if (H < 1) return set_err(GLX_ERR_SHAPE, "hidden_dim must be >= 1, got %d", H);
+    return GLX_OK;
+}
+
+int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, int H, int64_t epochs, double lr,
+                     double* stats_hist, int32_t* nonfinite, cudaStream_t st) {
+    BatchGeom g;
+    if (!batch_geometry(N, D, H, sm_count_current(), true, &g))
+        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d N=%lld (needs D<=33, H<=512)", D,
+                       H, (long long)N);
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
+    GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
+    float* wk0 = ws->wk.as<float>();
+    float* wk1 = wk0 + g.WKS;
+    GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk1, st));
+    const double lr_over_n = lr / (double)N;
+    for (int64_t e = 0; e < epochs; e++) {
+        float* cur = (e & 1) ? wk1 : wk0;
+        float* nxt = (e & 1) ? wk0 : wk1;
+        GLX_LAUNCH(launch_batch_epoch(g, Xp, cur, ws->part.as<float>(), true, st));
+        GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), w_ih, w_ho, cur, nxt, lr_over_n, true,
+                                       stats_hist ? stats_hist + 5 * e : nullptr, nonfinite, st));
+    }
+    return GLX_OK;
+}
+
+}  // namespace
+
+namespace glx {
+size_t online_scratch_bytes(int H, bool ref64) {
+    if (!ref64) return 2 * 16 * sizeof(float);
+    const int nb = (H + 15) / 16;
+    return (size_t)(nb * 17 + 2) * sizeof(double);
+}
+// defined in glx_batch.cu
+cudaError_t launch_batch_grad(const BatchGeom& g, const float* part, const float* Wk, double* grad, cudaStream_t st);
+cudaError_t launch_batch_apply(int D, int H, float* W1, float* W2, const double* grad, double lr_over_n,
+                               int* nonfinite, cudaStream_t st);
+}  // namespace glx
+
+extern "C" {
+
+const char* glx_last_error(void) { return g_err.c_str(); }
+int glx_version(void) { return 100; }
+uint64_t glx_launch_count(void) { return g_launches.load(); }
+
+int glx_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+int glx_sm_count(int device) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return 0;
+    return n;
+}
+
+void glx_cache_clear(void) {
+    for (auto& h : g_host) {
+        std::lock_guard<std::mutex> lk(h.mu);
+        h.key_x = h.key_t = h.key_xp = nullptr;
+        h.bytes_x = h.bytes_t = 0;
+    }
+}
+
+// --------------------------------------------------------------- device API
+
+int glx_train_online(float* w_ih, float* w_ho, const float* X, const float* T, int64_t N, int32_t D, int32_t H,
+                     int64_t epochs, double lr, int32_t numerics, void* stream) {
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0");
+    if (N == 0 || epochs == 0) return GLX_OK;
+    std::vector<NetReq> nets{{w_ih, w_ho, H, 0}};
+    return run_online(nets, X, T, N, D, epochs, lr, numerics == GLX_REF64, (cudaStream_t)stream);
+}
+
+int glx_train_sweep(int64_t n_nets, const int32_t* H_per_net, const int64_t* w_off, float* w_pool, const float* X,
+                    const float* T, int64_t N, int32_t D, int64_t epochs, double lr, int32_t numerics, void* stream) {
+    if (n_nets < 0) return set_err(GLX_ERR_INVALID, "n_nets must be >= 0");
+    if (n_nets == 0 || N == 0 || epochs == 0) return GLX_OK;
+    std::vector<NetReq> nets;
+    nets.reserve((size_t)n_nets);
+    for (int64_t n = 0; n < n_nets; n++) {
+        const int H = H_per_net[n];
+        int rc = check_dims(N, D, H);
+        if (rc) return rc;
+        float* wi = w_pool + w_off[n];
+        nets.push_back({wi, wi + (int64_t)H * (D + 1), H, (int)n});
+    }
+    return run_online(nets, X, T, N, D, epochs, lr, numerics == GLX_REF64, (cudaStream_t)stream);
+}
+
+int32_t glx_packed_ld(int32_t D) {
+    const int dp = D + 1 <= 8 ? 8 : D + 1 <= 16 ? 16 : D + 1 <= 34 ? 34 : D + 1;
+    return ((std::max(D + 2, dp)) + 3) / 4 * 4;
+}
+
+int glx_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int32_t D, float* Xp,
+                  void* stream) {
+    if (N < 0 || D < 1) return set_err(GLX_ERR_SHAPE, "bad pack shape");
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_pack_rows(X, T, labels, N, D, glx_packed_ld(D), Xp, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_train_batch(float* w_ih, float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H, int64_t epochs,
+                    double lr, double* stats_hist, int32_t* nonfinite, void* stream) {
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    if (N == 0 || epochs <= 0) return GLX_OK;
+    return batch_train_impl(w_ih, w_ho, Xp, N, D, H, epochs, lr, stats_hist, nonfinite, (cudaStream_t)stream);
+}
+
+int64_t glx_batch_grad_len(int32_t D, int32_t H) { return (int64_t)H * (D + 1) + H + 1 + 5; }
+
+int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
+                   double* grad, void* stream) {
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (N == 0) {
+        GLX_CK(cudaMemsetAsync(grad, 0, sizeof(double) * glx_batch_grad_len(D, H), st));
+        return GLX_OK;
+    }
+    BatchGeom g;
+    if (!batch_geometry(N, D, H, sm_count_current(), true, &g))
+        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d", D, H);
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
+    GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
+    float* wk0 = ws->wk.as<float>();
+    GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk0 + g.WKS, st));
+    GLX_LAUNCH(launch_batch_epoch(g, Xp, wk0, ws->part.as<float>(), true, st));
+    GLX_LAUNCH(launch_batch_grad(g, ws->part.as<float>(), wk0, grad, st));
+    return GLX_OK;
+}
+
+int glx_batch_apply(float* w_ih, float* w_ho, const double* grad, int32_t D, int32_t H, double lr_over_n,
+                    int32_t* nonfinite, void* stream) {
+    if (D < 1 || H < 1) return set_err(GLX_ERR_SHAPE, "bad shape");
+    GLX_LAUNCH(launch_batch_apply(D, H, w_ih, w_ho, grad, lr_over_n, nonfinite, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_eval(const float* w_ih, const float* w_ho, const float* X, const uint8_t* labels, int64_t N, int32_t D,
+             int32_t H, int32_t K, uint64_t* counts4, double* loss, void* stream) {
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    if (K < 1 || K > 16) return set_err(GLX_ERR_INVALID, "output_dim must be in [1, 16], got %d", K);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (N == 0) {
+        GLX_CK(cudaMemsetAsync(loss, 0, sizeof(double), st));
+        return GLX_OK;
+    }
+    const int nparts = (int)((N + 127) / 128);
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->losspart.ensure((size_t)nparts * sizeof(double)));
+    GLX_LAUNCH(launch_eval_ref64(w_ih, w_ho, X, labels, N, D, H, K, reinterpret_cast<unsigned long long*>(counts4),
+                                 ws->losspart.as<double>(), nparts, st));
+    GLX_LAUNCH(launch_eval_finish(ws->losspart.as<double>(), nparts, loss, st));
+    return GLX_OK;
+}
+
+int glx_eval_packed(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
+                    double* stats, void* stream) {
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (N == 0) {
+        GLX_CK(cudaMemsetAsync(stats, 0, 5 * sizeof(double), st));
+        return GLX_OK;
+    }
+    BatchGeom g;
+    if (!batch_geometry(N, D, H, sm_count_current(), false, &g))
+        return set_err(GLX_ERR_INVALID, "eval kernel: unsupported shape D=%d H=%d", D, H);
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
+    GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
+    float* wk0 = ws->wk.as<float>();
+    GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk0 + g.WKS, st));
+    GLX_LAUNCH(launch_batch_epoch(g, Xp, wk0, ws->part.as<float>(), false, st));
+    GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), nullptr, nullptr, wk0, nullptr, 0.0, false, stats,
+                                   nullptr, st));
+    return GLX_OK;
+}
+
+// ----------------------------------------------------------------- host API
+
+static HostState* host_state(int32_t device, int* rc) {
+    if (device < 0 || device >= 64) {
+        *rc = set_err(GLX_ERR_INVALID, "device %d out of range", device);
+        return nullptr;
+    }
+    HostState* h = &g_host[device];
+    return h;
+}
+
+#define HOST_PROLOGUE(device)                                                              \
+    int rc_ = GLX_OK;                                                                      \
+    HostState* hs = host_state(device, &rc_);                                              \
+    if (!hs) return rc_;                                                                   \
+    std::lock_guard<std::mutex> lk_(hs->mu);                                               \
+    GLX_CK(cudaSetDevice(device));                                                         \
+    if (!hs->stream) GLX_CK(cudaStreamCreateWithFlags(&hs->stream, cudaStreamNonBlocking)); \
+    cudaStream_t st = hs->stream;
+
+// upload feats/targets unless the cache says they are already resident
+static int stage_inputs(HostState* hs, const float* feats, size_t xbytes, const float* targets, size_t tbytes,
+                        bool cache, cudaStream_t st) {
+    const bool hit = cache && hs->key_x == feats && hs->bytes_x == xbytes && hs->key_t == targets &&
+                     hs->bytes_t == tbytes && hs->x.p && hs->t.p;
+    if (hit) return GLX_OK;
+    hs->key_x = hs->key_t = hs->key_xp = nullptr;
+    GLX_CK(hs->x.ensure(xbytes));
+    GLX_CK(hs->t.ensure(tbytes));
+    if (xbytes) GLX_CK(cudaMemcpyAsync(hs->x.p, feats, xbytes, cudaMemcpyHostToDevice, st));
+    if (tbytes) GLX_CK(cudaMemcpyAsync(hs->t.p, targets, tbytes, cudaMemcpyHostToDevice, st));
+    if (cache) {
+        hs->key_x = feats;
+        hs->bytes_x = xbytes;
+        hs->key_t = targets;
+        hs->bytes_t = tbytes;
+    }
+    return GLX_OK;
+}
+
+int glx_run_train_segment(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
+                          int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr, int32_t numerics,
+                          int32_t device, int32_t flags) {
+    int rc = check_dims(rows, input_dim, hidden_dim);
+    if (rc) return rc;
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0, got %lld", (long long)epochs);
+    if (rows == 0 || epochs == 0) return GLX_OK;
+    HOST_PROLOGUE(device);
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
+    GLX_CK(hs->w1.ensure(n1 * 4));
+    GLX_CK(hs->w2.ensure(n2 * 4));
+    rc = stage_inputs(hs, feats, (size_t)rows * input_dim * 4, targets, (size_t)rows * 4,
+                      (flags & GLX_FLAG_CACHE_INPUTS) != 0, st);
+    if (rc) return rc;
+    GLX_CK(cudaMemcpyAsync(hs->w1.p, w_ih, n1 * 4, cudaMemcpyHostToDevice, st));
+    GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
+    std::vector<NetReq> nets{{hs->w1.as<float>(), hs->w2.as<float>(), hidden_dim, 0}};
+    rc = run_online(nets, hs->x.as<float>(), hs->t.as<float>(), rows, input_dim, epochs, lr, numerics == GLX_REF64,
+                    st);
+    if (rc) return rc;
+    GLX_CK(cudaMemcpyAsync(w_ih, hs->w1.p, n1 * 4, cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(w_ho, hs->w2.p, n2 * 4, cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaStreamSynchronize(st));
+    return GLX_OK;
+}
+
+int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
+                                int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr,
+                                double* stats_hist, int32_t device, int32_t flags) {
+    int rc = check_dims(rows, input_dim, hidden_dim);
+    if (rc) return rc;
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0, got %lld", (long long)epochs);
+    if (rows == 0 || epochs == 0) return GLX_OK;
+    HOST_PROLOGUE(device);
+    const int ld = glx_packed_ld(input_dim);
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
+    GLX_CK(hs->w1.ensure(n1 * 4));
+    GLX_CK(hs->w2.ensure(n2 * 4));
+    const bool cache = (flags & GLX_FLAG_CACHE_INPUTS) != 0;
+    const bool packed_hit = cache && hs->key_xp == feats && hs->key_x == feats && hs->key_t == targets &&
+                            hs->bytes_x == (size_t)rows * input_dim * 4;
+    if (!packed_hit) {
+        rc = stage_inputs(hs, feats, (size_t)rows * input_dim * 4, targets, (size_t)rows * 4, cache, st);
+        if (rc) return rc;
+        GLX_CK(hs->xp.ensure((size_t)rows * ld * 4));
+        GLX_LAUNCH(launch_pack_rows(hs->x.as<float>(), hs->t.as<float>(), nullptr, rows, input_dim, ld,
+                                    hs->xp.as<float>(), st));
+        if (cache) hs->key_xp = feats;
+    }
+    GLX_CK(hs->stats.ensure((size_t)5 * epochs * sizeof(double)));
+    GLX_CK(hs->flag.ensure(sizeof(int)));
+    GLX_CK(cudaMemsetAsync(hs->flag.p, 0, sizeof(int), st));
+    GLX_CK(cudaMemcpyAsync(hs->w1.p, w_ih, n1 * 4, cudaMemcpyHostToDevice, st));
+    GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
+    rc = batch_train_impl(hs->w1.as<float>(), hs->w2.as<float>(), hs->xp.as<float>(), rows, input_dim, hidden_dim,
+                          epochs, lr, stats_hist ? hs->stats.as<double>() : nullptr, hs->flag.as<int>(), st);
+    if (rc) return rc;
+    GLX_CK(cudaMemcpyAsync(w_ih, hs->w1.p, n1 * 4, cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(w_ho, hs->w2.p, n2 * 4, cudaMemcpyDeviceToHost, st));
+    if (stats_hist)
+        GLX_CK(cudaMemcpyAsync(stats_hist, hs->stats.p, (size_t)5 * epochs * sizeof(double), cudaMemcpyDeviceToHost,
+                               st));
+    GLX_CK(cudaStreamSynchronize(st));
+    return GLX_OK;
+}
+
+int glx_eval_counts(const float* w_ih, const float* w_ho, const float* feats, const uint8_t* labels, int64_t rows,
+                    int32_t input_dim, int32_t hidden_dim, int32_t output_dim, int32_t numerics, int64_t* counts4,
+                    double* loss_sum, int32_t device, int32_t flags) {
+    int rc = check_dims(rows, input_dim, hidden_dim);
+    if (rc) return rc;
+    if (output_dim < 1 || output_dim > 16)
+        return set_err(GLX_ERR_INVALID, "output_dim must be in [1, 16], got %d", output_dim);
+    for (int q = 0; q < 4; q++) counts4[q] = 0;
+    if (loss_sum) *loss_sum = 0.0;
+    if (rows == 0) return GLX_OK;
+    HOST_PROLOGUE(device);
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)output_dim * (hidden_dim + 1);
+    GLX_CK(hs->w1.ensure(n1 * 4));
+    GLX_CK(hs->w2.ensure(n2 * 4));
+    GLX_CK(hs->cnt.ensure(4 * sizeof(uint64_t)));
+    GLX_CK(hs->loss.ensure(8 * sizeof(double)));
+    GLX_CK(cudaMemcpyAsync(hs->w1.p, w_ih, n1 * 4, cudaMemcpyHostToDevice, st));
+    GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
+    // evaluation inputs use their own buffers (train and test splits alternate;
+    // the training-input cache stays intact)
+    (void)flags;
+    const size_t xbytes = (size_t)rows * input_dim * 4;
+    GLX_CK(hs->lab.ensure((size_t)rows));
+    GLX_CK(cudaMemcpyAsync(hs->lab.p, labels, (size_t)rows, cudaMemcpyHostToDevice, st));
+    DevBuf* xb = &hs->ex;
+    GLX_CK(xb->ensure(xbytes));
+    GLX_CK(cudaMemcpyAsync(xb->p, feats, xbytes, cudaMemcpyHostToDevice, st));
+    uint64_t hc[4] = {0, 0, 0, 0};
+    double hl[5] = {0, 0, 0, 0, 0};
+    if (numerics == GLX_REF64 || output_dim > 1) {
+        GLX_CK(cudaMemsetAsync(hs->cnt.p, 0, 4 * sizeof(uint64_t), st));
+        rc = glx_eval(hs->w1.as<float>(), hs->w2.as<float>(), xb->as<float>(), hs->lab.as<uint8_t>(), rows, input_dim,
+                      hidden_dim, output_dim, hs->cnt.as<uint64_t>(), hs->loss.as<double>(), st);
+        if (rc) return rc;
+        GLX_CK(cudaMemcpyAsync(hc, hs->cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+        GLX_CK(cudaMemcpyAsync(hl, hs->loss.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+        GLX_CK(cudaStreamSynchronize(st));
+        for (int q = 0; q < 4; q++) counts4[q] = (int64_t)hc[q];
+        if (loss_sum) *loss_sum = hl[0];
+        return GLX_OK;
+    }
+    // fast FP32 path: pack rows (labels as targets) then the fused streaming forward
+    const int ld = glx_packed_ld(input_dim);
+    GLX_CK(hs->exp_.ensure((size_t)rows * ld * 4));
+    GLX_LAUNCH(launch_pack_rows(xb->as<float>(), nullptr, hs->lab.as<uint8_t>(), rows, input_dim, ld,
+                                hs->exp_.as<float>(), st));
+    rc = glx_eval_packed(hs->w1.as<float>(), hs->w2.as<float>(), hs->exp_.as<float>(), rows, input_dim, hidden_dim,
+                         hs->loss.as<double>(), st);
+    if (rc) return rc;
+    GLX_CK(cudaMemcpyAsync(hl, hs->loss.p, 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaStreamSynchronize(st));
+    if (loss_sum) *loss_sum = hl[0];
+    for (int q = 0; q < 4; q++) counts4[q] = (int64_t)llround(hl[1 + q]);
+    return GLX_OK;
+}
+
+int glx_fp32_peak(int32_t device, int32_t iters, double* tflops, double* ms) {
+    GLX_CK(cudaSetDevice(device));
+    const int sms = glx_sm_count(device);
+    const int blocks = sms * 8;
+    float* out = nullptr;
+    GLX_CK(cudaMalloc(&out, (size_t)blocks * 256 * 4));
+    cudaEvent_t e0, e1;
+    GLX_CK(cudaEventCreate(&e0));
+    GLX_CK(cudaEventCreate(&e1));
+    GLX_LAUNCH(launch_fp32_peak(out, 16, blocks, nullptr));  // warm-up
+    GLX_CK(cudaEventRecord(e0, nullptr));
+    GLX_LAUNCH(launch_fp32_peak(out, iters, blocks, nullptr));
+    GLX_CK(cudaEventRecord(e1, nullptr));
+    GLX_CK(cudaEventSynchronize(e1));
+    float t = 0.f;
+    GLX_CK(cudaEventElapsedTime(&t, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    const double flops = (double)blocks * 256 * (double)iters * 16 * 8 * 4;
+    if (ms) *ms = t;
+    if (tflops) *tflops = flops / ((double)t * 1e-3) / 1e12;
+    return GLX_OK;
+}
+
+}  // extern "C"

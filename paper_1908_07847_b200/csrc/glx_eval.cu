@@ -1,0 +1,165 @@
+// glx_eval.cu -- exact accuracy evaluation and the FP32 peak microbenchmark.
+//
+// eval_ref64_kernel replaces kernels.eval_counts
+// (/root/reference/pkg/src/glycemlp/kernels.py:352-375): one thread per row,
+// the reference's f64 16-blocked dot order for both layers, pred = o >= 0.5f,
+// confusion counts with label 1 ("poor") as the positive class. Counts are
+// reduced with warp ballots + integer atomics (order independent, so exact);
+// the loss partials are per block and summed in block order (deterministic).
+// K > 1 extension: counts = (correct, wrong, 0, 0) with argmax prediction.
+#include "glx_common.cuh"
+#include "glx_kernels.h"
+
+namespace glx {
+
+constexpr int kEvalThreads = 128;
+constexpr int kMaxK = 16;
+
+__global__ void __launch_bounds__(kEvalThreads) eval_ref64_kernel(const float* __restrict__ W1g,
+                                                                   const float* __restrict__ W2g,
+                                                                   const float* __restrict__ X,
+                                                                   const uint8_t* __restrict__ labels, int64_t N,
+                                                                   int D, int H, int K, int w_in_smem,
+                                                                   unsigned long long* __restrict__ counts4,
+                                                                   double* __restrict__ loss_part) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const float* W1 = W1g;
+    const float* W2 = W2g;
+    const int64_t n1 = (int64_t)H * (D + 1), n2 = (int64_t)K * (H + 1);
+    if (w_in_smem) {
+        float* s1 = reinterpret_cast<float*>(sm);
+        for (int64_t e = threadIdx.x; e < n1 + n2; e += blockDim.x) s1[e] = e < n1 ? W1g[e] : W2g[e - n1];
+        __syncthreads();
+        W1 = s1;
+        W2 = s1 + n1;
+    }
+    __shared__ double lsum[kEvalThreads / 32];
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const bool valid = r < N;
+    double loss = 0.0;
+    int pred = 0, lab = 0;
+    if (valid) {
+        const float* x = X + r * D;
+        double zo[kMaxK];
+        for (int k = 0; k < K; k++) zo[k] = 0.0;
+        for (int jb = 0; jb < H; jb += 16) {
+            double po[kMaxK];
+            for (int k = 0; k < K; k++) po[k] = 0.0;
+            const int je = jb + 16 < H ? jb + 16 : H;
+            for (int j = jb; j < je; j++) {
+                const float* wr = W1 + (int64_t)j * (D + 1);
+                double acc = 0.0;
+                for (int b0 = 0; b0 < D; b0 += 16) {
+                    const int b1 = b0 + 16 < D ? b0 + 16 : D;
+                    double part = 0.0;
+                    for (int i = b0; i < b1; i++) part = fma((double)wr[i], (double)__ldg(x + i), part);
+                    acc = __dadd_rn(acc, part);
+                }
+                const double z = __dadd_rn(acc, (double)wr[D]);
+                const float h = __double2float_rn(1.0 / (1.0 + exp(-z)));
+                for (int k = 0; k < K; k++) po[k] = fma((double)W2[(int64_t)k * (H + 1) + j], (double)h, po[k]);
+            }
+            for (int k = 0; k < K; k++) zo[k] = __dadd_rn(zo[k], po[k]);
+        }
+        lab = labels[r];
+        float best = -1.0f;
+        for (int k = 0; k < K; k++) {
+            const double z = __dadd_rn(zo[k], (double)W2[(int64_t)k * (H + 1) + H]);
+            const float o = __double2float_rn(1.0 / (1.0 + exp(-z)));
+            const double t = K == 1 ? (double)lab : (lab == k ? 1.0 : 0.0);
+            const double d = t - (double)o;
+            loss += 0.5 * d * d;
+            if (K == 1) pred = o >= 0.5f ? 1 : 0;
+            else if (o > best) { best = o; pred = k; }
+        }
+    }
+    // counts: (tp, tn, fp, fn) for K == 1, (correct, wrong, 0, 0) for K > 1
+    unsigned c[4];
+    if (K == 1) {
+        c[0] = __popc(__ballot_sync(0xffffffffu, valid && pred == 1 && lab == 1));
+        c[1] = __popc(__ballot_sync(0xffffffffu, valid && pred == 0 && lab != 1));
+        c[2] = __popc(__ballot_sync(0xffffffffu, valid && pred == 1 && lab != 1));
+        c[3] = __popc(__ballot_sync(0xffffffffu, valid && pred == 0 && lab == 1));
+    } else {
+        c[0] = __popc(__ballot_sync(0xffffffffu, valid && pred == lab));
+        c[1] = __popc(__ballot_sync(0xffffffffu, valid && pred != lab));
+        c[2] = c[3] = 0;
+    }
+    if ((threadIdx.x & 31) == 0)
+        for (int q = 0; q < 4; q++)
+            if (c[q]) atomicAdd(counts4 + q, (unsigned long long)c[q]);
+    // loss: fixed-order warp tree then block order
+    for (int o = 16; o > 0; o >>= 1) loss += __shfl_down_sync(0xffffffffu, loss, o);
+    if ((threadIdx.x & 31) == 0) lsum[threadIdx.x >> 5] = loss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kEvalThreads / 32; w++) s += lsum[w];
+        loss_part[blockIdx.x] = s;
+    }
+}
+
+__global__ void eval_finish_kernel(const double* __restrict__ loss_part, int nparts, double* __restrict__ out) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    const int per = (nparts + blockDim.x - 1) / blockDim.x;
+    const int b = threadIdx.x * per, e = min(nparts, b + per);
+    for (int i = b; i < e; i++) s += loss_part[i];  // contiguous chunks, fixed order
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int i = 0; i < (int)blockDim.x; i++) t += sh[i];
+        *out = t;
+    }
+}
+
+cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,
+                              int D, int H, int K, unsigned long long* counts4, double* loss_part, int nparts,
+                              cudaStream_t st) {
+    if (K < 1 || K > kMaxK) return cudaErrorInvalidValue;
+    const size_t wbytes = 4 * ((size_t)H * (D + 1) + (size_t)K * (H + 1));
+    const int w_in_smem = wbytes <= 160 * 1024;
+    const size_t smem = w_in_smem ? wbytes : 0;
+    if (smem > 48 * 1024) {
+        cudaError_t e =
+            cudaFuncSetAttribute(eval_ref64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    eval_ref64_kernel<<<nparts, kEvalThreads, smem, st>>>(W1, W2, X, labels, N, D, H, K, w_in_smem, counts4,
+                                                           loss_part);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss_out, cudaStream_t st) {
+    eval_finish_kernel<<<1, 256, 0, st>>>(loss_part, nparts, loss_out);
+    return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- FP32 peak
+// 8 independent FFMA2 chains per thread: measures the packed-FP32 FMA
+// throughput the batch kernels are bounded by (roofline denominator).
+__global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters) {
+    float2 a[8];
+    const float2 m = make_float2(1.0000001f, 0.9999999f), c = make_float2(1e-7f, -1e-7f);
+#pragma unroll
+    for (int k = 0; k < 8; k++) a[k] = make_float2(threadIdx.x * 1e-3f + k, blockIdx.x * 1e-3f - k);
+    for (int it = 0; it < iters; it++) {
+#pragma unroll
+        for (int u = 0; u < 16; u++) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) a[k] = ffma2(a[k], m, c);
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 8; k++) s += a[k].x + a[k].y;
+    if (s == 1.2345f) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st) {
+    fp32_peak_kernel<<<blocks, 256, 0, st>>>(out, iters);
+    return cudaGetLastError();
+}
+
+}  // namespace glx

@@ -1,0 +1,85 @@
+// glx_kernels.h -- internal launch descriptors shared by the .cu files and the C-ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace glx {
+
+// --------------------------------------------------------------- online SGD
+struct OnlineNetDesc {
+    float* w_ih;      // H x (D+1), reference layout (network.py:84-90)
+    float* w_ho;      // H + 1
+    int H;
+    int warp0;        // first warp of this network inside its CTA
+    int nwarps;
+    int bar_id;       // named barrier id (1..15)
+    int scratch_off;  // byte offset of this network's scratch in dynamic smem
+    int pad;
+};
+
+struct OnlineLaunch {
+    const OnlineNetDesc* nets;  // device
+    const int2* cta_nets;       // device: (first net, count) per CTA
+    int n_ctas;
+    int threads;
+    size_t smem_bytes;
+    bool x_in_smem;
+    bool ref64;
+    const float* X;  // device, (N, D)
+    const float* T;  // device, (N,)
+    int64_t N;
+    int D;
+    int64_t epochs;
+    double lr;
+};
+
+int online_dp_for(int D);
+cudaError_t launch_online(const OnlineLaunch& L, cudaStream_t st);
+size_t online_scratch_bytes(int H, bool ref64);
+
+// -------------------------------------------------------------- batch epoch
+struct BatchGeom {
+    int D, H, DP, LD, MT, TPG, G, R, RPG, HP;
+    int64_t N, ntiles;
+    int grid;
+    int P1;   // H*(D+1)
+    int PS;   // per-CTA partial record stride (floats)
+    int WKS;  // kernel weight-copy stride (floats)
+    size_t smem;
+};
+
+// kernel weight copy layout (floats): W1s[H][DP] (scaled by -log2 e, bias at
+// slot D, zero beyond), w2s[H] (scaled), b2s (scaled), w2r[H] (raw)
+inline int wk_w2s(const BatchGeom& g) { return g.H * g.DP; }
+inline int wk_b2s(const BatchGeom& g) { return g.H * g.DP + g.H; }
+inline int wk_w2r(const BatchGeom& g) { return g.H * g.DP + g.H + 1; }
+
+// per-CTA partial record: [dW1acc (P1) | dW2acc (H) | dsum | loss | c0 c1 c2 c3]
+inline int ps_acc2(const BatchGeom& g) { return g.P1; }
+inline int ps_dsum(const BatchGeom& g) { return g.P1 + g.H; }
+inline int ps_loss(const BatchGeom& g) { return g.P1 + g.H + 1; }
+inline int ps_cnt(const BatchGeom& g) { return g.P1 + g.H + 2; }
+
+bool batch_geometry(int64_t N, int D, int H, int n_sms, bool train, BatchGeom* g);
+cudaError_t launch_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
+                             float* Xp, cudaStream_t st);
+cudaError_t launch_batch_prep(const BatchGeom& g, const float* W1, const float* W2, float* Wk0, float* Wk1,
+                              cudaStream_t st);
+cudaError_t launch_batch_epoch(const BatchGeom& g, const float* Xp, const float* Wk, float* part, bool train,
+                               cudaStream_t st);
+// reduce the per-CTA partials; if train, apply the SGD update to W1/W2 and
+// write the next kernel weight copy. stats (may be null): [loss, c0, c1, c2, c3]
+cudaError_t launch_batch_update(const BatchGeom& g, const float* part, float* W1, float* W2, const float* Wk_cur,
+                                float* Wk_next, double lr_over_n, bool train, double* stats, int* nonfinite,
+                                cudaStream_t st);
+
+// ------------------------------------------------------------ exact eval
+cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,
+                              int D, int H, int K, unsigned long long* counts4, double* loss_part, int nparts,
+                              cudaStream_t st);
+cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss_out, cudaStream_t st);
+
+// ------------------------------------------------------------ diagnostics
+cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st);
+
+}  // namespace glx

@@ -1,0 +1,247 @@
+// glx_online.cu -- per-instance online SGD (the reference's training semantics).
+//
+// Replaces kernels.train_segment_seq / train_segment_par
+// (/root/reference/pkg/src/glycemlp/kernels.py:264-349). The reference's
+// "neuron-parallel" engine gives each worker a block of hidden neurons and
+// meets at a spin barrier twice per training row; here each hidden neuron is
+// one CUDA thread that keeps its weight row in REGISTERS, the training rows
+// sit in shared memory, and the network's warps meet at one named barrier
+// per row (fp32) or two (ref64). Several independent networks (hidden-width x
+// seed sweeps) are packed into one CTA, each on its own
+// warp range and named barrier, sharing the CTA's copy of the rows.
+//
+// Numerics (template Real):
+//   double -- "ref64": the reference's exact op order: f64 products of f32
+//             operands accumulated over 16-wide blocks in index order, bias
+//             last, f64 sigmoid, unfused w - step*x, one f32 rounding per
+//             store (kernels.py:102-139). Differs from the CPU only where
+//             CUDA's f64 exp and glibc's differ in the last ulp.
+//   float  -- "fp32": FFMA2 (packed f32x2) dot and update, MUFU sigmoid,
+//             tree reduction. Within the 1e-4 max(1,|w|) tolerance.
+#include "glx_common.cuh"
+#include "glx_kernels.h"
+
+namespace glx {
+
+template <typename Real, int DP, bool XS>
+__device__ __forceinline__ void load_row(float (&x)[DP], const float* __restrict__ xs, const float* __restrict__ X,
+                                         int64_t r, int D) {
+    if (XS) {  // shared: rows pre-padded to DP floats as [x_0..x_{D-1}, 1, 0...]
+        const float2* p = reinterpret_cast<const float2*>(xs + r * DP);
+#pragma unroll
+        for (int q = 0; q < DP / 2; q++) {
+            float2 v = p[q];
+            x[2 * q] = v.x;
+            x[2 * q + 1] = v.y;
+        }
+    } else {  // global, caller layout (N, D)
+        const float* p = X + r * D;
+#pragma unroll
+        for (int i = 0; i < DP; i++) x[i] = i < D ? __ldg(p + i) : (i == D ? 1.0f : 0.0f);
+    }
+}
+
+template <typename Real, int DP, bool XS>
+__global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __restrict__ nets,
+                                                          const int2* __restrict__ cta_nets, const float* __restrict__ X,
+                                                          const float* __restrict__ T, int64_t N, int D,
+                                                          int64_t epochs, double lr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* xs = reinterpret_cast<float*>(smem_raw);  // N x DP (if XS)
+    float* ts = xs + (XS ? N * DP : 0);              // N targets (if XS)
+
+    const int2 cn = cta_nets[blockIdx.x];
+    const int warp = threadIdx.x >> 5;
+
+    // stage the training rows once per CTA (shared by every packed network)
+    if (XS) {
+        for (int64_t e = threadIdx.x; e < N * DP; e += blockDim.x) {
+            int64_t r = e / DP;
+            int i = (int)(e - r * DP);
+            xs[e] = i < D ? X[r * D + i] : (i == D ? 1.0f : 0.0f);
+        }
+        for (int64_t r = threadIdx.x; r < N; r += blockDim.x) ts[r] = T[r];
+        __syncthreads();
+    }
+
+    // find my network
+    int my = -1;
+    for (int k = 0; k < cn.y; k++) {
+        const OnlineNetDesc& nd = nets[cn.x + k];
+        if (warp >= nd.warp0 && warp < nd.warp0 + nd.nwarps) my = cn.x + k;
+    }
+    if (my < 0) return;
+    const OnlineNetDesc nd = nets[my];
+    const int H = nd.H;
+    const int nthr = nd.nwarps * 32;
+    const int j = threadIdx.x - nd.warp0 * 32;
+    const bool active = j < H;
+    float* w_ih = nd.w_ih;
+    float* w_ho = nd.w_ho;
+    unsigned char* scratch = smem_raw + nd.scratch_off;
+
+    // weight row j in registers; slot D is the bias (x_D == 1)
+    float w[DP];
+#pragma unroll
+    for (int i = 0; i < DP; i++) w[i] = (active && i <= D) ? w_ih[(int64_t)j * (D + 1) + i] : 0.0f;
+    float w2 = active ? w_ho[j] : 0.0f;
+    float b2 = w_ho[H];  // only thread j == 0 updates / writes it back
+
+    float x[DP];
+    if constexpr (sizeof(Real) == 4) {
+        // ---------------------------------------------------------------- fp32
+        float* red = reinterpret_cast<float*>(scratch);  // [2][16] warp partials
+        const float kScale = (float)(-GLX_LOG2E);
+        int buf = 0;
+        for (int64_t ep = 0; ep < epochs; ep++) {
+            for (int64_t r = 0; r < N; r++) {
+                load_row<Real, DP, XS>(x, xs, X, r, D);
+                const float t = XS ? ts[r] : __ldg(T + r);
+                float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < DP / 2; q++)
+                    p = ffma2(make_float2(w[2 * q], w[2 * q + 1]), make_float2(x[2 * q], x[2 * q + 1]), p);
+                const float h = active ? sigmoid_scaled(kScale * (p.x + p.y)) : 0.0f;
+                float prod = active ? w2 * h : 0.0f;
+                if (j == 0) prod += b2;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+                if ((threadIdx.x & 31) == 0) red[buf * 16 + (j >> 5)] = prod;
+                bar_sync(nd.bar_id, nthr);
+                float zo = 0.0f;
+                for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
+                buf ^= 1;
+                const float o = sigmoid_scaled(kScale * zo);
+                const float d_o = (o - t) * o * (1.0f - o);
+                const float step_o = (float)lr * d_o;
+                if (active) {
+                    const float d_h = w2 * d_o * h * (1.0f - h);
+                    const float ns = -(float)lr * d_h;
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) {
+                        float2 wp = ffma2(bcast2(ns), make_float2(x[2 * q], x[2 * q + 1]),
+                                          make_float2(w[2 * q], w[2 * q + 1]));
+                        w[2 * q] = wp.x;
+                        w[2 * q + 1] = wp.y;
+                    }
+                    w2 = fmaf(-step_o, h, w2);
+                }
+                if (j == 0) b2 -= step_o;
+            }
+        }
+    } else {
+        // ---------------------------------------------------------------- ref64
+        const int nb = (H + 15) >> 4;
+        double* prods = reinterpret_cast<double*>(scratch);  // nb blocks x 17 (padded against bank conflicts)
+        double* bc = prods + nb * 17;                        // [0] = d_o, [1] = step_o
+        for (int64_t ep = 0; ep < epochs; ep++) {
+            for (int64_t r = 0; r < N; r++) {
+                load_row<Real, DP, XS>(x, xs, X, r, D);
+                float h = 0.0f;
+                if (active) {
+                    // kernels.py:102-122: blocked f64 dot, bias last, f64 sigmoid, f32 round
+                    double acc = 0.0;
+#pragma unroll
+                    for (int b0 = 0; b0 < DP; b0 += 16) {
+                        double part = 0.0;
+#pragma unroll
+                        for (int i = b0; i < (b0 + 16 < DP ? b0 + 16 : DP); i++)
+                            if (i < D) part = fma((double)w[i], (double)x[i], part);  // exact product
+                        if (b0 < D) acc = __dadd_rn(acc, part);
+                    }
+                    double z = __dadd_rn(acc, (double)w[D < DP ? D : DP - 1]);
+                    h = __double2float_rn(1.0 / (1.0 + exp(-z)));
+                    prods[(j >> 4) * 17 + (j & 15)] = (double)w2 * (double)h;  // exact product
+                }
+                bar_sync(nd.bar_id, nthr);
+                if (j < 32) {  // leader warp: the output neuron (kernels.py:277-289)
+                    double part = 0.0;
+                    if (j < nb) {
+                        const int jn = min(16, H - j * 16);
+                        for (int k = 0; k < jn; k++) part = __dadd_rn(part, prods[j * 17 + k]);
+                    }
+                    double z = 0.0;
+                    for (int b = 0; b < nb; b++) z = __dadd_rn(z, __shfl_sync(0xffffffffu, part, b));
+                    if (j == 0) {
+                        z = __dadd_rn(z, (double)b2);
+                        const float o = __double2float_rn(1.0 / (1.0 + exp(-z)));
+                        const double od = (double)o;
+                        const double td = (double)(XS ? ts[r] : __ldg(T + r));
+                        const double d_o = __dmul_rn(__dmul_rn(__dsub_rn(od, td), od), __dsub_rn(1.0, od));
+                        bc[0] = d_o;
+                        bc[1] = __dmul_rn(lr, d_o);
+                    }
+                }
+                bar_sync(nd.bar_id, nthr);
+                const double d_o = bc[0], step_o = bc[1];
+                if (active) {
+                    // hidden first, from the pre-update w_ho (kernels.py:290-292)
+                    const double hd = (double)h;
+                    const double d_h = __dmul_rn(__dmul_rn(__dmul_rn((double)w2, d_o), hd), __dsub_rn(1.0, hd));
+                    const double s = __dmul_rn(lr, d_h);
+#pragma unroll
+                    for (int i = 0; i < DP; i++)
+                        if (i < D) w[i] = __double2float_rn(__dsub_rn((double)w[i], __dmul_rn(s, (double)x[i])));
+                    if (D < DP) w[D < DP ? D : DP - 1] = __double2float_rn(__dsub_rn((double)w[D < DP ? D : DP - 1], s));
+                    w2 = __double2float_rn(__dsub_rn((double)w2, __dmul_rn(step_o, hd)));
+                }
+                if (j == 0) b2 = __double2float_rn(__dsub_rn((double)b2, step_o));
+            }
+        }
+    }
+    if (active) {
+#pragma unroll
+        for (int i = 0; i < DP; i++)
+            if (i <= D) w_ih[(int64_t)j * (D + 1) + i] = w[i];
+        w_ho[j] = w2;
+    }
+    if (j == 0) w_ho[H] = b2;
+}
+
+// ------------------------------------------------------------------ launcher
+template <typename Real, int DP>
+static cudaError_t launch_online_dp(const OnlineLaunch& L, cudaStream_t st) {
+    const size_t smem = L.smem_bytes;
+    if (L.x_in_smem) {
+        auto k = online_sgd_kernel<Real, DP, true>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k<<<L.n_ctas, L.threads, smem, st>>>(L.nets, L.cta_nets, L.X, L.T, L.N, L.D, L.epochs, L.lr);
+    } else {
+        auto k = online_sgd_kernel<Real, DP, false>;
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        k<<<L.n_ctas, L.threads, smem, st>>>(L.nets, L.cta_nets, L.X, L.T, L.N, L.D, L.epochs, L.lr);
+    }
+    return cudaGetLastError();
+}
+
+int online_dp_for(int D) {
+    if (D + 1 <= 8) return 8;
+    if (D + 1 <= 16) return 16;
+    if (D + 1 <= 34) return 34;
+    if (D + 1 <= 64) return 64;
+    return -1;
+}
+
+cudaError_t launch_online(const OnlineLaunch& L, cudaStream_t st) {
+    const int dp = online_dp_for(L.D);
+    if (L.ref64) {
+        switch (dp) {
+            case 8: return launch_online_dp<double, 8>(L, st);
+            case 16: return launch_online_dp<double, 16>(L, st);
+            case 34: return launch_online_dp<double, 34>(L, st);
+            case 64: return launch_online_dp<double, 64>(L, st);
+        }
+    } else {
+        switch (dp) {
+            case 8: return launch_online_dp<float, 8>(L, st);
+            case 16: return launch_online_dp<float, 16>(L, st);
+            case 34: return launch_online_dp<float, 34>(L, st);
+            case 64: return launch_online_dp<float, 64>(L, st);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace glx

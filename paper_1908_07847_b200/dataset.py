@@ -1,0 +1,163 @@
+"""Dataset containers and the synthetic sample generator of the benchmark configs.
+
+Mirrors the parts of the reference's dataset module that the training path
+reads (/root/reference/pkg/src/glycemlp/dataset.py): the immutable
+row-major float32 + uint8 Dataset (:77-111), SplitPair (:114-120),
+NormStats (:61-74) and synthetic_matrix (:260-289), which defines every
+benchmark configuration's input. CSV ingestion, record derivation, splitting
+and min-max normalisation are host plumbing outside the accelerated path
+(SURVEY.md 2.1); a reference-built SplitPair can be passed straight to
+trainer.train.
+
+For cohorts too large for per-row string ids (configs 2/4: 1M and 64M rows),
+synthetic_arrays / iter_synthetic_chunks produce the same bytes as
+synthetic_matrix without the Dataset wrapper, optionally chunk by chunk.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Iterator
+
+import numpy as np
+
+from .errors import ShapeError, ValidationError
+
+SUBSET_TAGS = ("male", "female", "all", "synthetic")
+LABEL_GOOD = 0
+LABEL_POOR = 1
+
+
+@dataclass(frozen=True)
+class NormStats:
+    col_min: np.ndarray
+    col_max: np.ndarray
+
+    def __post_init__(self) -> None:
+        if self.col_min.shape != self.col_max.shape or self.col_min.ndim != 1:
+            raise ShapeError("col_min and col_max must be 1-D arrays of equal length")
+
+    @property
+    def columns(self) -> int:
+        return int(self.col_min.shape[0])
+
+
+@dataclass(frozen=True)
+class Dataset:
+    """Immutable flat row-major float32 features + uint8 labels (dataset.py:77-111)."""
+
+    features: np.ndarray
+    labels: np.ndarray
+    rows: int
+    columns: int
+    subset_tag: str
+    row_ids: tuple
+    norm_stats: NormStats | None = None
+
+    def __post_init__(self) -> None:
+        if self.subset_tag not in SUBSET_TAGS:
+            raise ValidationError(f"subset_tag must be one of {SUBSET_TAGS}, got {self.subset_tag!r}")
+        if self.features.dtype != np.float32 or self.features.ndim != 1:
+            raise ShapeError("features must be a flat float32 array")
+        if self.features.shape[0] != self.rows * self.columns:
+            raise ShapeError(f"features length {self.features.shape[0]} != rows*columns ({self.rows}*{self.columns})")
+        if self.labels.shape[0] != self.rows:
+            raise ShapeError(f"labels length {self.labels.shape[0]} != rows {self.rows}")
+        if len(self.row_ids) != self.rows:
+            raise ShapeError(f"row_ids length {len(self.row_ids)} != rows {self.rows}")
+        self.features.setflags(write=False)
+        self.labels.setflags(write=False)
+
+    def matrix(self) -> np.ndarray:
+        return self.features.reshape(self.rows, self.columns)
+
+
+@dataclass(frozen=True)
+class SplitPair:
+    train: Dataset
+    test: Dataset
+    seed: int
+    fraction: float
+    stratified: bool = True
+
+
+def _check_synth_args(rows: int, columns: int, signal: str) -> None:
+    if rows < 2:
+        raise ValueError(f"rows must be >= 2, got {rows}")
+    if columns < 1:
+        raise ValueError(f"columns must be >= 1, got {columns}")
+    if signal not in ("planted-linear", "random"):
+        raise ValueError(f"signal must be planted-linear or random, got {signal!r}")
+
+
+def synthetic_arrays(rows: int, columns: int, seed: int, signal: str = "random") -> tuple[np.ndarray, np.ndarray]:
+    """(features (rows, columns) f32, labels (rows,) u8), byte-identical to synthetic_matrix.
+
+    The generator call order is the reference's (dataset.py:272-281): all
+    U[0,1) float32 features first, then either the planted hyperplane
+    (5 distinct columns, N(0,1) weights, label = score >= median score) or
+    independent fair-coin labels.
+    """
+    _check_synth_args(rows, columns, signal)
+    gen = np.random.default_rng(seed)
+    feats = gen.random((rows, columns), dtype=np.float32)
+    if signal == "random":
+        return feats, (gen.random(rows) < 0.5).astype(np.uint8)
+    pick = gen.choice(columns, size=min(5, columns), replace=False)
+    coef = gen.normal(0.0, 1.0, size=pick.shape[0])
+    score = feats[:, pick].astype(np.float64) @ coef
+    return feats, (score >= np.median(score)).astype(np.uint8)
+
+
+def synthetic_matrix(rows: int, columns: int, seed: int, signal: str = "random") -> Dataset:
+    """Benchmark / shape-test Dataset (dataset.py:260-289)."""
+    feats, labels = synthetic_arrays(rows, columns, seed, signal)
+    return Dataset(
+        features=feats.reshape(-1),
+        labels=labels,
+        rows=rows,
+        columns=columns,
+        subset_tag="synthetic",
+        row_ids=tuple(f"m{i:05d}" for i in range(rows)),
+    )
+
+
+def iter_synthetic_chunks(rows: int, columns: int, seed: int, signal: str = "random",
+                          chunk_rows: int = 1 << 20) -> Iterator[tuple[int, np.ndarray, np.ndarray]]:
+    """Yield (row0, features chunk, labels chunk) equal to synthetic_arrays' rows.
+
+    PCG64 float32 draws are sequential, so drawing the feature matrix in row
+    chunks gives the same bytes as one draw. The planted labels depend on the
+    median over ALL rows and the hyperplane is drawn after the features, so
+    planted-linear runs two passes: one to draw the hyperplane and the scores,
+    then a replay of the saved generator state for the features.
+    """
+    _check_synth_args(rows, columns, signal)
+    gen = np.random.default_rng(seed)
+    start_state = gen.bit_generator.state
+    if signal == "random":
+        for r0 in range(0, rows, chunk_rows):
+            gen.random((min(chunk_rows, rows - r0), columns), dtype=np.float32)
+        labels = (gen.random(rows) < 0.5).astype(np.uint8)
+        gen.bit_generator.state = start_state
+        for r0 in range(0, rows, chunk_rows):
+            n = min(chunk_rows, rows - r0)
+            yield r0, gen.random((n, columns), dtype=np.float32), labels[r0:r0 + n]
+        return
+    # pass 1: advance past the features, draw the hyperplane, then score chunk by chunk
+    for r0 in range(0, rows, chunk_rows):
+        gen.random((min(chunk_rows, rows - r0), columns), dtype=np.float32)
+    pick = gen.choice(columns, size=min(5, columns), replace=False)
+    coef = gen.normal(0.0, 1.0, size=pick.shape[0])
+    gen.bit_generator.state = start_state
+    score = np.empty(rows, dtype=np.float64)
+    for r0 in range(0, rows, chunk_rows):
+        n = min(chunk_rows, rows - r0)
+        f = gen.random((n, columns), dtype=np.float32)
+        score[r0:r0 + n] = f[:, pick].astype(np.float64) @ coef
+    labels = (score >= np.median(score)).astype(np.uint8)
+    del score
+    gen.bit_generator.state = start_state
+    for r0 in range(0, rows, chunk_rows):
+        n = min(chunk_rows, rows - r0)
+        yield r0, gen.random((n, columns), dtype=np.float32), labels[r0:r0 + n]

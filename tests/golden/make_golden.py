@@ -1,0 +1,141 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE.
+
+Run here (the only place /root/reference exists), never on the GPU box:
+
+    NUMBA_CACHE_DIR=/tmp/numba_cache PYTHONDONTWRITEBYTECODE=1 \
+        python tests/golden/make_golden.py
+
+It imports the unmodified reference package from /root/reference/pkg/src and
+records, for small fixed-seed cases, the reference's own outputs:
+
+* online SGD weights after N epochs via backend.run_train_segment
+  (kernels.train_segment_seq, kernels.py:264-295) and the parallel engine;
+* eval_counts (kernels.py:352-375) at each checkpoint;
+* trainer.train checkpoint rows (trainer.py:123-199);
+* synthetic_matrix (dataset.py:260-289) and init_weights (network.py:110-116)
+  digests, so the product's own generators can be pinned byte-for-byte.
+
+The committed .npz/.json files are what tests/ read; this script is only
+re-run when a case is added.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+import sys
+from pathlib import Path
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache")
+sys.dont_write_bytecode = True
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import numpy as np  # noqa: E402
+
+import glycemlp as g  # noqa: E402
+from glycemlp import backend as B  # noqa: E402
+from glycemlp import kernels as Kr  # noqa: E402
+from glycemlp.trainer import TrainSpec  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+
+
+def digest(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def matrix_split(rows, cols, seed, signal="planted-linear"):
+    data = g.synthetic_matrix(rows, cols, seed, signal)
+    return g.normalize_split(g.train_test_split(data, 0.75, seed))
+
+
+def record_split(rows, seed, signal, sex=None):
+    records = g.synth_dataset(rows, seed, signal)
+    if sex is not None:
+        male, female = g.split_by_sex(records)
+        records = male if sex == "male" else female
+    data = g.build_dataset(records, "synthetic")
+    return g.normalize_split(g.train_test_split(data, 0.75, seed))
+
+
+def online_case(name, pair, hidden, seed, checkpoints, lr=0.1):
+    cfg = g.NetworkConfig(input_dim=pair.train.columns, hidden_dim=hidden, seed=seed, learning_rate=lr)
+    net = g.init_weights(cfg)
+    feats = pair.train.matrix()
+    targets = pair.train.labels.astype(np.float32)
+    out = {
+        "train_x": np.ascontiguousarray(feats), "train_y": pair.train.labels.copy(),
+        "test_x": np.ascontiguousarray(pair.test.matrix()), "test_y": pair.test.labels.copy(),
+        "w_ih0": net.w_ih.copy(), "w_ho0": net.w_ho.copy(),
+        "checkpoints": np.array(checkpoints, dtype=np.int64),
+        "meta": np.array([pair.train.columns, hidden, 1, seed], dtype=np.int64),
+        "lr": np.array([lr]),
+    }
+    prev = 0
+    for cp in checkpoints:
+        B.run_train_segment(net.w_ih2d, net.w_ho2d, feats, targets, cp - prev, lr, g.sequential())
+        prev = cp
+        out[f"w_ih_{cp}"] = net.w_ih.copy()
+        out[f"w_ho_{cp}"] = net.w_ho.copy()
+        out[f"train_counts_{cp}"] = np.array(Kr.eval_counts(net.w_ih2d, net.w_ho2d, feats, pair.train.labels), np.int64)
+        out[f"test_counts_{cp}"] = np.array(Kr.eval_counts(net.w_ih2d, net.w_ho2d, pair.test.matrix(), pair.test.labels), np.int64)
+    # the parallel engine must agree byte-for-byte; record it too
+    par = g.init_weights(cfg)
+    B.run_train_segment(par.w_ih2d, par.w_ho2d, feats, targets, checkpoints[-1], lr, g.parallel(2))
+    assert par.w_ih.tobytes() == net.w_ih.tobytes() and par.w_ho.tobytes() == net.w_ho.tobytes()
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+    print(f"{name}: D={pair.train.columns} H={hidden} rows={pair.train.rows}/{pair.test.rows} cps={checkpoints}")
+
+
+def trainer_case():
+    pair = matrix_split(120, 33, 7)
+    cfg = g.NetworkConfig(input_dim=33, hidden_dim=33, seed=7)
+    rep = g.train(TrainSpec(config=cfg, epochs=1000, backend=g.sequential()), pair)
+    rows = [{"epoch": r.epoch, "train_accuracy": r.train_accuracy, "test_accuracy": r.test_accuracy,
+             "train_confusion": r.train_confusion, "test_confusion": r.test_confusion} for r in rep.rows]
+    (OUT / "trainer_paper_1000.json").write_text(json.dumps({
+        "rows": rows, "w_ih_sha256": digest(rep.network.w_ih), "w_ho_sha256": digest(rep.network.w_ho),
+        "diverged": rep.diverged}, indent=1))
+    print("trainer_paper_1000: rows", [r["epoch"] for r in rows])
+
+
+def generator_digests():
+    cases = []
+    for rows, cols, seed, signal in ((120, 33, 7, "planted-linear"), (1000, 33, 0, "planted-linear"),
+                                     (257, 5, 3, "random"), (10_000, 33, 0, "random"),
+                                     (5000, 1024, 1, "planted-linear")):
+        d = g.synthetic_matrix(rows, cols, seed, signal)
+        cases.append({"rows": rows, "columns": cols, "seed": seed, "signal": signal,
+                      "features_sha256": digest(d.features), "labels_sha256": digest(d.labels)})
+    inits = []
+    for D, H, seed in ((33, 33, 7), (30, 17, 13), (33, 256, 0), (33, 512, 63), (1024, 1024, 0)):
+        net = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=seed))
+        inits.append({"input_dim": D, "hidden_dim": H, "seed": seed,
+                      "w_ih_sha256": digest(net.w_ih), "w_ho_sha256": digest(net.w_ho)})
+    (OUT / "generators.json").write_text(json.dumps({"synthetic_matrix": cases, "init_weights": inits}, indent=1))
+    print("generators: ok")
+
+
+def small_backend_case():
+    # test_backend.py:143-152 shape: 7-19-1 on 25 random rows, 40 epochs
+    rng = np.random.default_rng(11)
+    feats = rng.random((25, 7), dtype=np.float32)
+    targets = (rng.random(25) < 0.5).astype(np.float32)
+    cfg = g.NetworkConfig(input_dim=7, hidden_dim=19, seed=3)
+    net = g.init_weights(cfg)
+    w_ih0, w_ho0 = net.w_ih.copy(), net.w_ho.copy()
+    B.run_train_segment(net.w_ih2d, net.w_ho2d, feats, targets, 40, 0.1, g.sequential())
+    np.savez_compressed(OUT / "small_7_19_1.npz", x=feats, t=targets, w_ih0=w_ih0, w_ho0=w_ho0,
+                        w_ih=net.w_ih, w_ho=net.w_ho, epochs=np.array([40]))
+    print("small_7_19_1: ok")
+
+
+if __name__ == "__main__":
+    online_case("paper_33_33_1", matrix_split(120, 33, 7), 33, 7, [1, 10, 100, 1000])
+    online_case("cohort_male_30_30_1", record_split(120, 7, "planted-linear", "male"), 30, 7, [1, 10, 100, 1000])
+    online_case("cohort_female_30_30_1", record_split(120, 7, "random", "female"), 30, 7, [1, 10, 100, 1000])
+    online_case("wide_33_256_1", matrix_split(200, 33, 3), 256, 5, [1, 10, 50])
+    small_backend_case()
+    trainer_case()
+    generator_digests()

@@ -1,0 +1,123 @@
+"""Data-parallel orchestration (paper_1908_07847_b200/dp.py) on CPU: gloo, world_size 2.
+
+The product's epoch loop (shard -> per-rank gradient sum -> all-reduce(sum)
+-> identical update) is run with a numpy test engine standing in for the
+device kernels; the result must equal single-process full-batch GD (the
+oracle restatement) to f64 rounding, and every rank must hold identical
+weights and statistics.
+"""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1908_07847_b200 import dp
+
+
+class NumpyEngine:
+    """Test stand-in for dp.DeviceEngine: f64 gradient sums of one row shard."""
+
+    def __init__(self, x, t, w_ih, w_ho):
+        self.x = x.astype(np.float64)
+        self.t = t.astype(np.float64)
+        self.N, self.D = x.shape
+        self.H = w_ih.size // (self.D + 1)
+        self.w1 = w_ih.copy().reshape(self.H, self.D + 1)
+        self.w2 = w_ho.copy().reshape(-1)
+
+    def grad_sum(self):
+        W1 = self.w1.astype(np.float64)
+        w2 = self.w2.astype(np.float64)
+        xa = np.hstack([self.x, np.ones((self.N, 1))])
+        h = 1.0 / (1.0 + np.exp(-(xa @ W1.T)))
+        o = 1.0 / (1.0 + np.exp(-(h @ w2[:-1] + w2[-1])))
+        d_o = (o - self.t) * o * (1.0 - o)
+        d_h = (d_o[:, None] * w2[None, :-1]) * h * (1.0 - h)
+        g1 = d_h.T @ xa
+        g2 = np.concatenate([d_o @ h, [d_o.sum()]])
+        pred, pos = o >= 0.5, self.t >= 0.5
+        stats = [0.5 * np.sum((self.t - o) ** 2), np.sum(pred & pos), np.sum(~pred & ~pos), np.sum(pred & ~pos),
+                 np.sum(~pred & pos)]
+        return torch.from_numpy(np.concatenate([g1.reshape(-1), g2, np.array(stats, np.float64)]))
+
+    def apply(self, grad, lr_over_n):
+        g = grad.numpy()
+        P1 = self.H * (self.D + 1)
+        self.w1 = (self.w1.astype(np.float64) - lr_over_n * g[:P1].reshape(self.w1.shape)).astype(np.float32)
+        self.w2 = (self.w2.astype(np.float64) - lr_over_n * g[P1:P1 + self.H + 1]).astype(np.float32)
+
+
+def _data():
+    rng = np.random.default_rng(17)
+    x = rng.random((203, 6), dtype=np.float32)
+    t = (x[:, 0] + 0.3 * x[:, 3] > 0.65).astype(np.float32)
+    w1 = rng.uniform(-0.5, 0.5, 5 * 7).astype(np.float32)
+    w2 = rng.uniform(-0.5, 0.5, 6).astype(np.float32)
+    return x, t, w1, w2
+
+
+def _worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    x, t, w1, w2 = _data()
+    r0, r1 = dp.shard_bounds(x.shape[0], world, rank)
+    eng = NumpyEngine(x[r0:r1], t[r0:r1], w1, w2)
+    stats = dp.train_data_parallel(eng, 25, 2.0, x.shape[0], dp.nccl_all_reduce())
+    out_q.put((rank, eng.w1.copy(), eng.w2.copy(), [(s.loss_sum, s.counts) for s in stats]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.timeout(240)
+def test_gloo_world2_equals_single_process_full_batch():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=200) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, a1, a2, sa), (_, b1, b2, sb) = res
+    # every rank holds identical weights and statistics
+    assert a1.tobytes() == b1.tobytes() and a2.tobytes() == b2.tobytes()
+    assert [c for _, c in sa] == [c for _, c in sb]
+    # ... equal to single-process full-batch GD (oracle restatement, B = N)
+    from oracle import oracle as O
+
+    x, t, w1, w2 = _data()
+    r1 = w1.copy().reshape(5, 7)
+    r2 = w2.copy().reshape(1, 6)
+    O.train_batch(r1, r2, x, t, 25, 2.0, x.shape[0])
+    assert np.max(np.abs(a1.reshape(-1) - r1.reshape(-1))) <= 1e-6
+    assert np.max(np.abs(a2.reshape(-1) - r2.reshape(-1))) <= 1e-6
+    # statistics cover all rows: counts sum to N every epoch
+    assert all(sum(c) == x.shape[0] for _, c in sa)
+
+
+def test_world1_no_allreduce_matches():
+    x, t, w1, w2 = _data()
+    eng = NumpyEngine(x, t, w1, w2)
+    dp.train_data_parallel(eng, 5, 2.0, x.shape[0], None)
+    from oracle import oracle as O
+
+    r1 = w1.copy().reshape(5, 7)
+    r2 = w2.copy().reshape(1, 6)
+    O.train_batch(r1, r2, x, t, 5, 2.0, x.shape[0])
+    assert np.max(np.abs(eng.w1.reshape(-1) - r1.reshape(-1))) <= 1e-6

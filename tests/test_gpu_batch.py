@@ -1,0 +1,100 @@
+"""Full-batch GD kernel (configs 2/4) vs the oracle batch restatement, plus
+size-independent properties at the full 1M-row benchmark size."""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+import paper_1908_07847_b200 as g
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _case(N, D, H, seed, signal="planted-linear"):
+    x, l = g.synthetic_arrays(N, D, seed, signal)
+    return x, l, l.astype(np.float32), g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=seed))
+
+
+@pytest.mark.parametrize("N,D,H", [
+    (2, 33, 33), (65, 33, 33), (1000, 33, 33), (1000, 33, 256), (777, 33, 512), (500, 33, 19),
+    (300, 7, 5), (301, 15, 16), (250, 30, 30), (4099, 33, 64), (130, 1, 1), (513, 32, 36),
+])
+def test_batch_vs_oracle(gpu, N, D, H):
+    x, l, t, net0 = _case(N, D, H, seed=N % 97)
+    epochs, lr = 6, 0.5
+    ref = net0.copy()
+    O.train_batch(ref.w_ih2d, ref.w_ho2d, x, t, epochs, lr, N)
+    net = net0.copy()
+    stats = np.zeros((epochs, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, epochs, lr, g.cuda(), stats)
+    err = max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho))
+    assert err <= 1e-5, f"N={N} D={D} H={H}: {err:.3e}"
+    # epoch-0 statistics are the evaluation of the initial weights
+    (tp, tn, fp, fn), loss = O.eval_counts(net0.w_ih2d, net0.w_ho2d, x, l)
+    assert stats[0, 1:].sum() == N
+    assert abs(stats[0, 0] - loss) <= 1e-4 * max(1.0, loss)
+    assert np.abs(stats[0, 1:] - np.array([tp, tn, fp, fn])).sum() <= 2  # |o-0.5| < 1e-6 rows may flip
+
+
+def test_batch_is_deterministic(gpu):
+    x, l, t, net0 = _case(100_003, 33, 256, seed=4)
+    a, b = net0.copy(), net0.copy()
+    g.run_train_segment_batch(a.w_ih2d, a.w_ho2d, x, t, 3, 0.1, g.cuda())
+    g.run_train_segment_batch(b.w_ih2d, b.w_ho2d, x, t, 3, 0.1, g.cuda())
+    assert a.w_ih.tobytes() == b.w_ih.tobytes() and a.w_ho.tobytes() == b.w_ho.tobytes()
+
+
+@pytest.mark.parametrize("H", [33, 256])
+def test_full_size_1M_properties(gpu, H):
+    # config 2 at full size: 1M rows; the oracle checks a bounded 2-epoch run on the same data
+    x, l, t, net0 = _case(1_000_000, 33, H, seed=0)
+    net = net0.copy()
+    stats = np.zeros((2, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 2, 0.1, g.cuda(), stats)
+    assert net.weights_finite()
+    assert (stats[:, 1:].sum(axis=1) == 1_000_000).all()
+    ref = net0.copy()
+    O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, t, 2, 0.1)
+    assert max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho)) <= 1e-5
+
+
+def test_loss_decreases_over_epochs(gpu):
+    x, l, t, net0 = _case(200_000, 33, 33, seed=1)
+    stats = np.zeros((40, 5))
+    net = net0.copy()
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 40, 2.0, g.cuda(), stats)
+    assert stats[-1, 0] < stats[0, 0]
+
+
+def test_dp_split_equals_fused_single_gpu(gpu):
+    """glx_batch_grad + glx_batch_apply over 2 row shards (summed on the host, as the
+    all-reduce would) == the fused single-GPU epoch loop."""
+    import torch
+
+    from paper_1908_07847_b200 import dp
+
+    x, l, t, net0 = _case(20_001, 33, 64, seed=9)
+    fused = net0.copy()
+    g.run_train_segment_batch(fused.w_ih2d, fused.w_ho2d, x, t, 4, 0.5, g.cuda())
+    engines = []
+    for r in range(2):
+        r0, r1 = dp.shard_bounds(x.shape[0], 2, r)
+        engines.append(dp.DeviceEngine(x[r0:r1], t[r0:r1], net0.w_ih, net0.w_ho))
+    for _ in range(4):
+        total = engines[0].grad_sum().clone() + engines[1].grad_sum().clone()
+        for e in engines:
+            e.apply(total, 0.5 / x.shape[0])
+    torch.cuda.synchronize()
+    w1, w2 = engines[0].weights()
+    assert rel_err(w1, fused.w_ih) <= 1e-6 and rel_err(w2, fused.w_ho) <= 1e-6
+    v1, v2 = engines[1].weights()
+    assert w1.tobytes() == v1.tobytes() and w2.tobytes() == v2.tobytes()
+
+
+def test_unsupported_shape_raises(gpu):
+    net = g.init_weights(g.NetworkConfig(input_dim=40, hidden_dim=8, seed=0))
+    x = np.zeros((10, 40), np.float32)
+    with pytest.raises(g.ValidationError):
+        g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, np.zeros(10, np.float32), 1, 0.1, g.cuda())
