@@ -125,6 +125,12 @@ int glx_eval_packed(const float* w_ih, const float* w_ho, const float* Xp, int64
 /* ------------------------------------------------------------ diagnostics */
 /* Number of CUDA kernels this library has launched (for launch accounting). */
 uint64_t glx_launch_count(void);
+/* Per-launch timing of the streaming epoch kernel (batch_epoch_kernel): when
+ * enabled, an event pair is recorded on the launching stream around every
+ * launch; glx_profile_read synchronises, returns the summed kernel time and
+ * launch count since the last read, and resets. */
+void glx_profile_enable(int32_t on);
+int glx_profile_read(double* total_ms, int64_t* launches);
 /* FFMA2 throughput microbenchmark on `device`: returns TFLOP/s. */
 int glx_fp32_peak(int32_t device, int32_t iters, double* tflops, double* ms);
 

@@ -56,6 +56,8 @@ SIGNATURES = {
     "glx_eval": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
     "glx_eval_packed": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp]),
     "glx_launch_count": (_u64, []),
+    "glx_profile_enable": (None, [_i32]),
+    "glx_profile_read": (_int, [_vp, _vp]),
     "glx_fp32_peak": (_int, [_i32, _i32, _vp, _vp]),
 }
 

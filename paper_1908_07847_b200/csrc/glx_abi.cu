@@ -92,6 +92,34 @@ Workspace* workspace(cudaStream_t st) {
     return w;
 }
 
+// optional per-launch timing of the streaming epoch kernel (roofline evidence):
+// an event pair recorded on the launching stream around every launch
+struct Profiler {
+    std::mutex mu;
+    bool on = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pairs;
+    size_t used = 0;
+} g_prof;
+
+cudaError_t prof_begin(cudaStream_t st, cudaEvent_t* e1) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    if (!g_prof.on) {
+        *e1 = nullptr;
+        return cudaSuccess;
+    }
+    if (g_prof.used == g_prof.pairs.size()) {
+        cudaEvent_t a, b;
+        cudaError_t e = cudaEventCreate(&a);
+        if (e != cudaSuccess) return e;
+        e = cudaEventCreate(&b);
+        if (e != cudaSuccess) return e;
+        g_prof.pairs.emplace_back(a, b);
+    }
+    auto& pr = g_prof.pairs[g_prof.used++];
+    *e1 = pr.second;
+    return cudaEventRecord(pr.first, st);
+}
+
 int sm_count_current() {
     int dev = 0, n = 0;
     cudaGetDevice(&dev);
@@ -220,7 +248,10 @@ int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D
     for (int64_t e = 0; e < epochs; e++) {
         float* cur = (e & 1) ? wk1 : wk0;
         float* nxt = (e & 1) ? wk0 : wk1;
+        cudaEvent_t pe = nullptr;
+        GLX_CK(prof_begin(st, &pe));
         GLX_LAUNCH(launch_batch_epoch(g, Xp, cur, ws->part.as<float>(), true, st));
+        if (pe) GLX_CK(cudaEventRecord(pe, st));
         GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), w_ih, w_ho, cur, nxt, lr_over_n, true,
                                        stats_hist ? stats_hist + 5 * e : nullptr, nonfinite, st));
     }
@@ -335,7 +366,10 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
     GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
     float* wk0 = ws->wk.as<float>();
     GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk0 + g.WKS, st));
+    cudaEvent_t pe = nullptr;
+    GLX_CK(prof_begin(st, &pe));
     GLX_LAUNCH(launch_batch_epoch(g, Xp, wk0, ws->part.as<float>(), true, st));
+    if (pe) GLX_CK(cudaEventRecord(pe, st));
     GLX_LAUNCH(launch_batch_grad(g, ws->part.as<float>(), wk0, grad, st));
     return GLX_OK;
 }
@@ -548,6 +582,27 @@ int glx_eval_counts(const float* w_ih, const float* w_ho, const float* feats, co
     GLX_CK(cudaStreamSynchronize(st));
     if (loss_sum) *loss_sum = hl[0];
     for (int q = 0; q < 4; q++) counts4[q] = (int64_t)llround(hl[1 + q]);
+    return GLX_OK;
+}
+
+void glx_profile_enable(int32_t on) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = on != 0;
+    g_prof.used = 0;
+}
+
+int glx_profile_read(double* total_ms, int64_t* launches) {
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    double tot = 0.0;
+    for (size_t i = 0; i < g_prof.used; i++) {
+        GLX_CK(cudaEventSynchronize(g_prof.pairs[i].second));
+        float ms = 0.f;
+        GLX_CK(cudaEventElapsedTime(&ms, g_prof.pairs[i].first, g_prof.pairs[i].second));
+        tot += ms;
+    }
+    if (total_ms) *total_ms = tot;
+    if (launches) *launches = (int64_t)g_prof.used;
+    g_prof.used = 0;
     return GLX_OK;
 }
 

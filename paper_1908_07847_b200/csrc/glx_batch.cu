@@ -34,6 +34,7 @@
 #include "glx_kernels.h"
 
 #include <algorithm>
+#include <cstdio>
 
 namespace glx {
 
@@ -503,9 +504,17 @@ template <int DP, int MT, bool TRAIN>
 static cudaError_t launch_t(const BatchGeom& g, const BatchArgs& a, cudaStream_t st) {
     auto k = batch_epoch_kernel<DP, MT, TRAIN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
-    if (e != cudaSuccess) return e;
-    k<<<g.grid, kFT + (TRAIN ? kBT : 0) + 32, g.smem, st>>>(a);
-    return cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "glx: batch_epoch_kernel<%d,%d,%d> cudaFuncSetAttribute(smem=%zu): %s\n", DP, MT,
+                (int)TRAIN, g.smem, cudaGetErrorString(e));
+        return e;
+    }
+    k<<<g.grid, kFT + (TRAIN ? kBT : 0), g.smem, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess)
+        fprintf(stderr, "glx: batch_epoch_kernel<%d,%d,%d> launch grid=%d smem=%zu: %s\n", DP, MT, (int)TRAIN,
+                g.grid, g.smem, cudaGetErrorString(e));
+    return e;
 }
 
 template <int DP, bool TRAIN>
