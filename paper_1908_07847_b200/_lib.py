@@ -7,6 +7,7 @@ load, or no CUDA device is visible, every compute call raises RuntimeError.
 from __future__ import annotations
 
 import ctypes
+import os
 import threading
 from pathlib import Path
 
@@ -14,7 +15,7 @@ import numpy as np
 
 from .errors import NumericError, ShapeError, ValidationError
 
-LIB_PATH = Path(__file__).resolve().parent / "libglycemlp_cuda.so"
+LIB_PATH = Path(os.environ.get("GLX_LIB", Path(__file__).resolve().parent / "libglycemlp_cuda.so"))
 
 GLX_OK = 0
 GLX_ERR_SHAPE = -1

@@ -38,12 +38,57 @@
 
 namespace glx {
 
-constexpr int kNF = 4;  // forward warps
-constexpr int kNB = 4;  // backward warps
+#ifndef GLX_NW
+#define GLX_NW 4
+#endif
+#ifndef GLX_FROWS
+#define GLX_FROWS 2
+#endif
+#ifndef GLX_BROWS
+#define GLX_BROWS 2
+#endif
+#ifndef GLX_MAXMT
+#define GLX_MAXMT 4  // max hidden units per thread (register tile)
+#endif
+#ifndef GLX_TILE_ROWS
+#define GLX_TILE_ROWS 256  // target rows per tile (shared memory permitting)
+#endif
+constexpr int kNF = GLX_NW;  // forward warps
+constexpr int kNB = GLX_NW;  // backward warps
 constexpr int kNX = 4;  // x tile stages
 constexpr int kFT = kNF * 32;
 constexpr int kBT = kNB * 32;
 constexpr int kBarF = 1, kBarHFull = 2, kBarHEmpty = 4, kBarEpi = 6;
+
+template <int MT>
+__device__ __forceinline__ void store_units(float* p, const float (&v)[MT]) {
+    if constexpr (MT == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (MT == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < MT; u++) p[u] = v[u];
+    }
+}
+
+template <int MT>
+__device__ __forceinline__ void load_units(const float* p, float (&v)[MT]) {
+    if constexpr (MT == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    } else if constexpr (MT == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+#pragma unroll
+        for (int u = 0; u < MT; u++) v[u] = p[u];
+    }
+}
 
 struct BatchArgs {
     const float* Xp;
@@ -124,67 +169,126 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
             float* op = opart + hb * a.R * (a.TPG + 1);
             float* hrow = hbuf + hb * a.R * a.HP;
             if (fv) {
-                for (int rr = 0; rr < a.RPG; rr++) {
-                    const int r = g + rr * a.G;
-                    const float* xr = xt + r * a.LD;
-                    float2 xv[DP / 2];
+                // FR rows per step, software-pipelined: the FFMA2 chains of step i+1
+                // are issued in the same basic block as the sigmoid / output-partial
+                // tail of step i, so MUFU latency hides under FMA work
+                constexpr int FR = GLX_FROWS;
+                auto chains = [&](int rr, float2 (&p)[FR][MT]) {
+                    const float* xr[FR];
 #pragma unroll
-                    for (int q = 0; q < DP / 4; q++) {
-                        const float4 v = reinterpret_cast<const float4*>(xr)[q];
-                        xv[2 * q] = make_float2(v.x, v.y);
-                        xv[2 * q + 1] = make_float2(v.z, v.w);
-                    }
-                    if (DP % 4) xv[DP / 2 - 1] = reinterpret_cast<const float2*>(xr)[DP / 2 - 1];
-                    float osum = 0.f;
-                    float hv[MT];
+                    for (int f2 = 0; f2 < FR; f2++) xr[f2] = xt + (g + (rr + f2) * a.G) * a.LD;
 #pragma unroll
-                    for (int u = 0; u < MT; u++) {
-                        float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+                    for (int f2 = 0; f2 < FR; f2++)
 #pragma unroll
-                        for (int q = 0; q < DP / 2; q += 2) {
-                            acc0 = ffma2(w[u][q], xv[q], acc0);
-                            if (q + 1 < DP / 2) acc1 = ffma2(w[u][q + 1], xv[q + 1], acc1);
+                        for (int u = 0; u < MT; u++) p[f2][u] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q4 = 0; q4 < DP / 4; q4++) {
+                        float4 v[FR];
+#pragma unroll
+                        for (int f2 = 0; f2 < FR; f2++) v[f2] = reinterpret_cast<const float4*>(xr[f2])[q4];
+#pragma unroll
+                        for (int u = 0; u < MT; u++) {
+#pragma unroll
+                            for (int f2 = 0; f2 < FR; f2++)
+                                p[f2][u] = ffma2(w[u][2 * q4], make_float2(v[f2].x, v[f2].y), p[f2][u]);
+#pragma unroll
+                            for (int f2 = 0; f2 < FR; f2++)
+                                p[f2][u] = ffma2(w[u][2 * q4 + 1], make_float2(v[f2].z, v[f2].w), p[f2][u]);
                         }
-                        const float z = (acc0.x + acc1.x) + (acc0.y + acc1.y);
-                        hv[u] = sigmoid_scaled(z);
-                        osum = fmaf(w2s[u], hv[u], osum);
                     }
-                    if (TRAIN) {
-                        float* hp = hrow + r * a.HP + jq * MT;
-                        if (MT == 4) {
-                            *reinterpret_cast<float4*>(hp) = make_float4(hv[0], hv[MT > 1 ? 1 : 0],
-                                                                         hv[MT > 2 ? 2 : 0], hv[MT > 3 ? 3 : 0]);
-                        } else if (MT == 2) {
-                            *reinterpret_cast<float2*>(hp) = make_float2(hv[0], hv[MT > 1 ? 1 : 0]);
+                    if (DP % 4) {
+#pragma unroll
+                        for (int f2 = 0; f2 < FR; f2++) {
+                            const float2 v = reinterpret_cast<const float2*>(xr[f2])[DP / 2 - 1];
+#pragma unroll
+                            for (int u = 0; u < MT; u++) p[f2][u] = ffma2(w[u][DP / 2 - 1], v, p[f2][u]);
+                        }
+                    }
+                };
+                auto finish = [&](int rr, const float2 (&p)[FR][MT]) {
+#pragma unroll
+                    for (int f2 = 0; f2 < FR; f2++) {
+                        const int row = g + (rr + f2) * a.G;
+                        float h[MT];
+                        float osum;
+                        if constexpr (MT % 2 == 0) {
+                            // unit pairs share packed f32x2 adds / FMAs
+                            float2 os = make_float2(0.f, 0.f);
+#pragma unroll
+                            for (int u = 0; u < MT; u += 2) {
+                                const float2 z = __fadd2_rn(make_float2(p[f2][u].x, p[f2][u + 1].x),
+                                                            make_float2(p[f2][u].y, p[f2][u + 1].y));
+                                const float2 e1 = __fadd2_rn(make_float2(ex2_approx(z.x), ex2_approx(z.y)),
+                                                             make_float2(1.f, 1.f));
+                                h[u] = rcp_approx(e1.x);
+                                h[u + 1] = rcp_approx(e1.y);
+                                os = ffma2(make_float2(w2s[u], w2s[u + 1]), make_float2(h[u], h[u + 1]), os);
+                            }
+                            osum = os.x + os.y;
                         } else {
+                            osum = 0.f;
 #pragma unroll
-                            for (int u = 0; u < MT; u++) hp[u] = hv[u];
+                            for (int u = 0; u < MT; u++) {
+                                h[u] = sigmoid_scaled(p[f2][u].x + p[f2][u].y);
+                                osum = fmaf(w2s[u], h[u], osum);
+                            }
                         }
+                        if (TRAIN) store_units<MT>(hrow + row * a.HP + jq * MT, h);
+                        op[row * (a.TPG + 1) + jq] = osum;
                     }
-                    op[r * (a.TPG + 1) + jq] = osum;
+                };
+                float2 pc[FR][MT];
+                chains(0, pc);
+                for (int rr = FR; rr < a.RPG; rr += FR) {
+                    float2 pn[FR][MT];
+                    chains(rr, pn);
+                    finish(rr - FR, pc);
+#pragma unroll
+                    for (int f2 = 0; f2 < FR; f2++)
+#pragma unroll
+                        for (int u = 0; u < MT; u++) pc[f2][u] = pn[f2][u];
                 }
+                finish(a.RPG - FR, pc);
             }
             bar_sync(kBarF, kFT);
-            // per-row output neuron: o, delta_o, loss, confusion (kernels.py:352-375)
-            if (f < a.R) {
-                const int r = f;
-                const int64_t grow = t * a.R + r;
-                float d = 0.f;
-                if (grow < a.N) {
-                    float zo = b2s;
-                    const float* opr = op + r * (a.TPG + 1);
-                    for (int q = 0; q < a.TPG; q++) zo += opr[q];
-                    const float o = sigmoid_scaled(zo);
-                    const float tt = xt[r * a.LD + a.D + 1];
-                    d = (o - tt) * o * (1.0f - o);
-                    loss = fmaf(0.5f * (tt - o), (tt - o), loss);
-                    const bool pred = o >= 0.5f, pos = tt >= 0.5f;
-                    c0 += (pred && pos) ? 1.f : 0.f;    // tp
-                    c1 += (!pred && !pos) ? 1.f : 0.f;  // tn
-                    c2 += (pred && !pos) ? 1.f : 0.f;   // fp
-                    c3 += (!pred && pos) ? 1.f : 0.f;   // fn
+            // per-row output neuron: o, delta_o, loss, confusion (kernels.py:352-375);
+            // TPR threads per row split the partial sums, 4 accumulators each
+            {
+                const int tpr = (2 * a.R <= kFT) ? 2 : 1;
+                const int part = f - (f / tpr) * tpr;
+                for (int r = f / tpr; r - f / tpr < a.R; r += kFT / tpr) {  // warp-uniform trip count
+                    const bool rv = r < a.R;
+                    float z0 = 0.f, z1 = 0.f, z2 = 0.f, z3 = 0.f;
+                    if (rv) {
+                        const float* opr = op + r * (a.TPG + 1);
+                        int q = part;
+                        for (; q + 3 * tpr < a.TPG; q += 4 * tpr) {
+                            z0 += opr[q];
+                            z1 += opr[q + tpr];
+                            z2 += opr[q + 2 * tpr];
+                            z3 += opr[q + 3 * tpr];
+                        }
+                        for (; q < a.TPG; q += tpr) z0 += opr[q];
+                    }
+                    float zo = (z0 + z1) + (z2 + z3);
+                    if (tpr == 2) zo += __shfl_xor_sync(0xffffffffu, zo, 1);
+                    const int64_t grow = t * a.R + r;
+                    if (rv && part == 0) {
+                        float d = 0.f;
+                        if (grow < a.N) {
+                            const float o = sigmoid_scaled(zo + b2s);
+                            const float tt = xt[r * a.LD + a.D + 1];
+                            d = (o - tt) * o * (1.0f - o);
+                            loss = fmaf(0.5f * (tt - o), (tt - o), loss);
+                            const bool pred = o >= 0.5f, pos = tt >= 0.5f;
+                            c0 += (pred && pos) ? 1.f : 0.f;    // tp
+                            c1 += (!pred && !pos) ? 1.f : 0.f;  // tn
+                            c2 += (pred && !pos) ? 1.f : 0.f;   // fp
+                            c3 += (!pred && pos) ? 1.f : 0.f;   // fn
+                        }
+                        if (TRAIN) dobuf[hb * a.R + r] = d;
+                    }
                 }
-                if (TRAIN) dobuf[hb * a.R + r] = d;
             }
             if (TRAIN) {
                 bar_arrive(kBarHFull + hb, kFT + NBT);
@@ -224,44 +328,75 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
             const float* hrow = hbuf + hb * a.R * a.HP;
             const float* dr = dobuf + hb * a.R;
             if (bv) {
-                for (int rr = 0; rr < a.RPG; rr++) {
-                    const int r = gb + rr * a.G;
-                    const float d = dr[r];
-                    const float* xr = xt + r * a.LD;
-                    float hv[MT];
-                    const float* hp = hrow + r * a.HP + jq * MT;
-                    if (MT == 4) {
-                        const float4 v = *reinterpret_cast<const float4*>(hp);
-                        hv[0] = v.x;
-                        hv[MT > 1 ? 1 : 0] = v.y;
-                        hv[MT > 2 ? 2 : 0] = v.z;
-                        hv[MT > 3 ? 3 : 0] = v.w;
-                    } else if (MT == 2) {
-                        const float2 v = *reinterpret_cast<const float2*>(hp);
-                        hv[0] = v.x;
-                        hv[MT > 1 ? 1 : 0] = v.y;
-                    } else {
+                // BR rows per iteration; the next rows' delta_o and h are prefetched
+                constexpr int BR = GLX_BROWS;
+                float dn[BR], hn[BR][MT];
 #pragma unroll
-                        for (int u = 0; u < MT; u++) hv[u] = hp[u];
+                for (int b2 = 0; b2 < BR; b2++) {
+                    dn[b2] = dr[gb + b2 * a.G];
+                    load_units<MT>(hrow + (gb + b2 * a.G) * a.HP + jq * MT, hn[b2]);
+                }
+                for (int rr = 0; rr < a.RPG; rr += BR) {
+                    float sv[BR][MT];
+                    const float* xr[BR];
+#pragma unroll
+                    for (int b2 = 0; b2 < BR; b2++) {
+                        xr[b2] = xt + (gb + (rr + b2) * a.G) * a.LD;
+                        const float d = dn[b2];
+                        if constexpr (MT % 2 == 0) {
+#pragma unroll
+                            for (int u = 0; u < MT; u += 2) {
+                                const float2 hh = make_float2(hn[b2][u], hn[b2][u + 1]);
+                                const float2 v = __fmul2_rn(bcast2(d), hh);
+                                const float2 t = ffma2(make_float2(-v.x, -v.y), hh, v);
+                                sv[b2][u] = t.x;
+                                sv[b2][u + 1] = t.y;
+                                const float2 a2 = __fadd2_rn(make_float2(acc2[u], acc2[u + 1]), v);
+                                acc2[u] = a2.x;
+                                acc2[u + 1] = a2.y;
+                            }
+                        } else {
+#pragma unroll
+                            for (int u = 0; u < MT; u++) {
+                                const float v = d * hn[b2][u];
+                                sv[b2][u] = fmaf(-v, hn[b2][u], v);
+                                acc2[u] += v;
+                            }
+                        }
+                        if (jq == 0) dsum += d;
                     }
-                    float2 xv[DP / 2];
+                    if (rr + BR < a.RPG) {
 #pragma unroll
-                    for (int q = 0; q < DP / 4; q++) {
-                        const float4 v = reinterpret_cast<const float4*>(xr)[q];
-                        xv[2 * q] = make_float2(v.x, v.y);
-                        xv[2 * q + 1] = make_float2(v.z, v.w);
+                        for (int b2 = 0; b2 < BR; b2++) {
+                            const int rn = gb + (rr + BR + b2) * a.G;
+                            dn[b2] = dr[rn];
+                            load_units<MT>(hrow + rn * a.HP + jq * MT, hn[b2]);
+                        }
                     }
-                    if (DP % 4) xv[DP / 2 - 1] = reinterpret_cast<const float2*>(xr)[DP / 2 - 1];
 #pragma unroll
-                    for (int u = 0; u < MT; u++) {
-                        const float v = d * hv[u];
-                        const float sv = fmaf(-v, hv[u], v);
-                        acc2[u] += v;
-                        const float2 sb = bcast2(sv);
+                    for (int q4 = 0; q4 < DP / 4; q4++) {
+                        float4 v[BR];
 #pragma unroll
-                        for (int q = 0; q < DP / 2; q++) acc[u][q] = ffma2(sb, xv[q], acc[u][q]);
+                        for (int b2 = 0; b2 < BR; b2++) v[b2] = reinterpret_cast<const float4*>(xr[b2])[q4];
+#pragma unroll
+                        for (int u = 0; u < MT; u++) {
+#pragma unroll
+                            for (int b2 = 0; b2 < BR; b2++) {
+                                acc[u][2 * q4] = ffma2(bcast2(sv[b2][u]), make_float2(v[b2].x, v[b2].y), acc[u][2 * q4]);
+                                acc[u][2 * q4 + 1] =
+                                    ffma2(bcast2(sv[b2][u]), make_float2(v[b2].z, v[b2].w), acc[u][2 * q4 + 1]);
+                            }
+                        }
                     }
-                    if (jq == 0) dsum += d;
+                    if (DP % 4) {
+#pragma unroll
+                        for (int b2 = 0; b2 < BR; b2++) {
+                            const float2 v = reinterpret_cast<const float2*>(xr[b2])[DP / 2 - 1];
+#pragma unroll
+                            for (int u = 0; u < MT; u++)
+                                acc[u][DP / 2 - 1] = ffma2(bcast2(sv[b2][u]), v, acc[u][DP / 2 - 1]);
+                        }
+                    }
                 }
             }
             bar_arrive(kBarHEmpty + hb, kFT + NBT);
@@ -472,25 +607,26 @@ bool batch_geometry(int64_t N, int D, int H, int n_sms, bool train, BatchGeom* g
     q.LD = ((std::max(D + 2, q.DP)) + 3) / 4 * 4;
     q.MT = 0;
     for (int mt : {4, 3, 2, 1})
-        if (H % mt == 0 && H / mt <= kFT) {
+        if (mt <= GLX_MAXMT && H % mt == 0 && H / mt <= kFT) {
             q.MT = mt;
             break;
         }
     if (!q.MT) return false;
     q.TPG = H / q.MT;
-    q.G = kFT / q.TPG;
+    q.G = std::min(kFT / q.TPG, kFT / 2);  // rows come in pairs, <= kFT rows per tile
     q.HP = (H + 3) / 4 * 4;
     q.P1 = H * (D + 1);
     q.PS = (q.P1 + H + 6 + 3) / 4 * 4;
     q.WKS = (H * q.DP + 2 * H + 1 + 3) / 4 * 4;
     // rows per tile: a multiple of G, <= 128 (one finalising thread per row), as
     // large as the shared-memory budget allows (target 64)
-    int rpg = (64 + q.G - 1) / q.G;
-    for (;; rpg--) {
-        if (rpg < 1) return false;
+    int rpg = (GLX_TILE_ROWS + q.G - 1) / q.G;
+    rpg += rpg & 1;  // the row loops take rows in pairs
+    for (;; rpg -= 2) {
+        if (rpg < 2) return false;
         q.RPG = rpg;
         q.R = q.G * rpg;
-        if (q.R > kFT) continue;
+        if (q.R > 4 * kFT) continue;
         q.smem = batch_smem(q, train);
         if (q.smem <= 227 * 1024) break;
     }
