@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -232,10 +233,33 @@ int check_dims(int64_t rows, int D, int H) {
     return GLX_OK;
 }
 
+// epoch-kernel selection: the three-role kernel (glx_batch3.cu) when its
+// geometry fits, else the two-role kernel; GLX_BATCH_KERNEL=2 forces the latter
+bool use_three_role() {
+    static int v = [] {
+        const char* e = getenv("GLX_BATCH_KERNEL");
+        return (e && e[0] == '2') ? 0 : 1;
+    }();
+    return v != 0;
+}
+
+bool train_geometry(int64_t N, int D, int H, BatchGeom* g, bool* three) {
+    // the three-role kernel wins where its forward/backward tiles are 4 units wide
+    // (H % 4 == 0); narrower tiles stay on the two-role kernel (profiles/r01_summary.md)
+    *three = use_three_role() && batch3_geometry(N, D, H, sm_count_current(), g) && g->MT == 4;
+    return *three || batch_geometry(N, D, H, sm_count_current(), true, g);
+}
+
+cudaError_t launch_train_epoch(const BatchGeom& g, bool three, const float* Xp, const float* Wk, float* part,
+                               cudaStream_t st) {
+    return three ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
+}
+
 int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, int H, int64_t epochs, double lr,
                      double* stats_hist, int32_t* nonfinite, cudaStream_t st) {
     BatchGeom g;
-    if (!batch_geometry(N, D, H, sm_count_current(), true, &g))
+    bool three = false;
+    if (!train_geometry(N, D, H, &g, &three))
         return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d N=%lld (needs D<=33, H<=512)", D,
                        H, (long long)N);
     Workspace* ws = workspace(st);
@@ -250,7 +274,7 @@ int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D
         float* nxt = (e & 1) ? wk0 : wk1;
         cudaEvent_t pe = nullptr;
         GLX_CK(prof_begin(st, &pe));
-        GLX_LAUNCH(launch_batch_epoch(g, Xp, cur, ws->part.as<float>(), true, st));
+        GLX_LAUNCH(launch_train_epoch(g, three, Xp, cur, ws->part.as<float>(), st));
         if (pe) GLX_CK(cudaEventRecord(pe, st));
         GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), w_ih, w_ho, cur, nxt, lr_over_n, true,
                                        stats_hist ? stats_hist + 5 * e : nullptr, nonfinite, st));
@@ -359,7 +383,8 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
         return GLX_OK;
     }
     BatchGeom g;
-    if (!batch_geometry(N, D, H, sm_count_current(), true, &g))
+    bool three = false;
+    if (!train_geometry(N, D, H, &g, &three))
         return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d", D, H);
     Workspace* ws = workspace(st);
     GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
@@ -368,7 +393,7 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
     GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk0 + g.WKS, st));
     cudaEvent_t pe = nullptr;
     GLX_CK(prof_begin(st, &pe));
-    GLX_LAUNCH(launch_batch_epoch(g, Xp, wk0, ws->part.as<float>(), true, st));
+    GLX_LAUNCH(launch_train_epoch(g, three, Xp, wk0, ws->part.as<float>(), st));
     if (pe) GLX_CK(cudaEventRecord(pe, st));
     GLX_LAUNCH(launch_batch_grad(g, ws->part.as<float>(), wk0, grad, st));
     return GLX_OK;

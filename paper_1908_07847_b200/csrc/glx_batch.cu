@@ -47,6 +47,9 @@ namespace glx {
 #ifndef GLX_BROWS
 #define GLX_BROWS 2
 #endif
+#ifndef GLX_PACK_SCALARS
+#define GLX_PACK_SCALARS 0  // packed f32x2 for the per-unit scalar math (runs on fmaheavy like FFMA2)
+#endif
 #ifndef GLX_MAXMT
 #define GLX_MAXMT 4  // max hidden units per thread (register tile)
 #endif
@@ -59,36 +62,6 @@ constexpr int kNX = 4;  // x tile stages
 constexpr int kFT = kNF * 32;
 constexpr int kBT = kNB * 32;
 constexpr int kBarF = 1, kBarHFull = 2, kBarHEmpty = 4, kBarEpi = 6;
-
-template <int MT>
-__device__ __forceinline__ void store_units(float* p, const float (&v)[MT]) {
-    if constexpr (MT == 4) {
-        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-    } else if constexpr (MT == 2) {
-        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
-    } else {
-#pragma unroll
-        for (int u = 0; u < MT; u++) p[u] = v[u];
-    }
-}
-
-template <int MT>
-__device__ __forceinline__ void load_units(const float* p, float (&v)[MT]) {
-    if constexpr (MT == 4) {
-        const float4 t = *reinterpret_cast<const float4*>(p);
-        v[0] = t.x;
-        v[1] = t.y;
-        v[2] = t.z;
-        v[3] = t.w;
-    } else if constexpr (MT == 2) {
-        const float2 t = *reinterpret_cast<const float2*>(p);
-        v[0] = t.x;
-        v[1] = t.y;
-    } else {
-#pragma unroll
-        for (int u = 0; u < MT; u++) v[u] = p[u];
-    }
-}
 
 struct BatchArgs {
     const float* Xp;
@@ -211,17 +184,22 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
                         const int row = g + (rr + f2) * a.G;
                         float h[MT];
                         float osum;
-                        if constexpr (MT % 2 == 0) {
+                        if constexpr (MT % 2 == 0 && GLX_PACK_SCALARS) {
                             // unit pairs share packed f32x2 adds / FMAs
                             float2 os = make_float2(0.f, 0.f);
 #pragma unroll
                             for (int u = 0; u < MT; u += 2) {
                                 const float2 z = __fadd2_rn(make_float2(p[f2][u].x, p[f2][u + 1].x),
                                                             make_float2(p[f2][u].y, p[f2][u + 1].y));
+#ifdef GLX_DEBUG_NOSIGMOID
+                                h[u] = z.x;
+                                h[u + 1] = z.y;
+#else
                                 const float2 e1 = __fadd2_rn(make_float2(ex2_approx(z.x), ex2_approx(z.y)),
                                                              make_float2(1.f, 1.f));
                                 h[u] = rcp_approx(e1.x);
                                 h[u + 1] = rcp_approx(e1.y);
+#endif
                                 os = ffma2(make_float2(w2s[u], w2s[u + 1]), make_float2(h[u], h[u + 1]), os);
                             }
                             osum = os.x + os.y;
@@ -237,18 +215,23 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
                         op[row * (a.TPG + 1) + jq] = osum;
                     }
                 };
-                float2 pc[FR][MT];
-                chains(0, pc);
-                for (int rr = FR; rr < a.RPG; rr += FR) {
-                    float2 pn[FR][MT];
-                    chains(rr, pn);
-                    finish(rr - FR, pc);
-#pragma unroll
-                    for (int f2 = 0; f2 < FR; f2++)
-#pragma unroll
-                        for (int u = 0; u < MT; u++) pc[f2][u] = pn[f2][u];
+                // two accumulator sets alternate (no register copies between steps)
+                float2 pA[FR][MT], pB[FR][MT];
+                chains(0, pA);
+                int rr = FR;
+                for (; rr + FR < a.RPG; rr += 2 * FR) {
+                    chains(rr, pB);
+                    finish(rr - FR, pA);
+                    chains(rr + FR, pA);
+                    finish(rr, pB);
                 }
-                finish(a.RPG - FR, pc);
+                if (rr < a.RPG) {
+                    chains(rr, pB);
+                    finish(rr - FR, pA);
+                    finish(rr, pB);
+                } else {
+                    finish(rr - FR, pA);
+                }
             }
             bar_sync(kBarF, kFT);
             // per-row output neuron: o, delta_o, loss, confusion (kernels.py:352-375);
@@ -336,6 +319,9 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
                     dn[b2] = dr[gb + b2 * a.G];
                     load_units<MT>(hrow + (gb + b2 * a.G) * a.HP + jq * MT, hn[b2]);
                 }
+#ifdef GLX_DEBUG_NOB
+                if (a.N > 0) {} else
+#endif
                 for (int rr = 0; rr < a.RPG; rr += BR) {
                     float sv[BR][MT];
                     const float* xr[BR];
@@ -343,7 +329,7 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
                     for (int b2 = 0; b2 < BR; b2++) {
                         xr[b2] = xt + (gb + (rr + b2) * a.G) * a.LD;
                         const float d = dn[b2];
-                        if constexpr (MT % 2 == 0) {
+                        if constexpr (MT % 2 == 0 && GLX_PACK_SCALARS) {
 #pragma unroll
                             for (int u = 0; u < MT; u += 2) {
                                 const float2 hh = make_float2(hn[b2][u], hn[b2][u + 1]);

@@ -79,4 +79,36 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
+// MT consecutive floats <-> registers (vectorised when MT is 2 or 4)
+template <int MT>
+__device__ __forceinline__ void store_units(float* p, const float (&v)[MT]) {
+    if constexpr (MT == 4) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    } else if constexpr (MT == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
+    } else {
+#pragma unroll
+        for (int u = 0; u < MT; u++) p[u] = v[u];
+    }
+}
+
+template <int MT>
+__device__ __forceinline__ void load_units(const float* p, float (&v)[MT]) {
+    if constexpr (MT == 4) {
+        const float4 t = *reinterpret_cast<const float4*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    } else if constexpr (MT == 2) {
+        const float2 t = *reinterpret_cast<const float2*>(p);
+        v[0] = t.x;
+        v[1] = t.y;
+    } else {
+#pragma unroll
+        for (int u = 0; u < MT; u++) v[u] = p[u];
+    }
+}
+
+
 }  // namespace glx

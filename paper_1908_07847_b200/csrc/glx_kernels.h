@@ -46,7 +46,11 @@ struct BatchGeom {
     int PS;   // per-CTA partial record stride (floats)
     int WKS;  // kernel weight-copy stride (floats)
     size_t smem;
+    // three-role kernel (glx_batch3.cu) only
+    int UA, QR, AG;
+    int off_dob, off_opart, off_z, off_x;
 };
+using Batch3Geom = BatchGeom;
 
 // kernel weight copy layout (floats): W1s[H][DP] (scaled by -log2 e, bias at
 // slot D, zero beyond), w2s[H] (scaled), b2s (scaled), w2r[H] (raw)
@@ -72,6 +76,13 @@ cudaError_t launch_batch_epoch(const BatchGeom& g, const float* Xp, const float*
 cudaError_t launch_batch_update(const BatchGeom& g, const float* part, float* W1, float* W2, const float* Wk_cur,
                                 float* Wk_next, double lr_over_n, bool train, double* stats, int* nonfinite,
                                 cudaStream_t st);
+
+#ifndef GLX3_TILE_ROWS
+#define GLX3_TILE_ROWS 256
+#endif
+// three-role (forward / activation / backward) epoch kernel; same partial record
+bool batch3_geometry(int64_t N, int D, int H, int n_sms, Batch3Geom* g);
+cudaError_t launch_batch3_epoch(const Batch3Geom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st);
 
 // ------------------------------------------------------------ exact eval
 cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,

@@ -27,6 +27,8 @@ for H in [int(h) for h in os.environ.get("KB_H", "256,33").split(",")]:
     kms = np.zeros(1); kn = np.zeros(1, np.int64); L.glx_profile_read(_lib.ptr(kms), _lib.ptr(kn)); L.glx_profile_enable(0)
     k = kms[0] / kn[0]
     flops = N * (4 * H * (D + 1) + 4 * (H + 1) + 2 * H)
+    if hasattr(L, "glx3_timing_dump"):
+        L.glx3_timing_dump()
     res[f"H{H}"] = {"kernel_ms": k, "step_ms": e0.elapsed_time(e1) / 50, "frac": flops / (k * 1e-3) / 1e12 / res["peak"]}
     # correctness vs oracle on a small case
     from oracle import oracle as O
