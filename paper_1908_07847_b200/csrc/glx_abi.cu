@@ -149,6 +149,18 @@ struct NetReq {
     int idx;
 };
 
+// hidden units per thread for the fp32 online kernel: 1 for a single network
+// (shortest per-row critical path); for sweeps an MT-unit register tile
+// (GLX_ONLINE_MT overrides) amortises the per-row reduction and barrier
+int online_mt(size_t n_nets, bool ref64, int dp) {
+    if (ref64) return 1;
+    const char* e = getenv("GLX_ONLINE_MT");
+    int mt = e ? atoi(e) : (n_nets > 1 ? 4 : 1);
+    if (mt != 1 && mt != 2 && mt != 4) mt = 1;
+    if (dp > 34) mt = 1;  // 64-wide rows: the MT tile would spill
+    return mt;
+}
+
 int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t N, int D, int64_t epochs, double lr,
                bool ref64, cudaStream_t st) {
     const int dp = online_dp_for(D);
@@ -157,7 +169,9 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
         if (n.H < 1 || n.H > 512) return set_err(GLX_ERR_INVALID, "online kernel supports 1 <= hidden_dim <= 512, got %d", n.H);
     const size_t xbytes = ((size_t)N * dp * 4 + (size_t)N * 4 + 15) / 16 * 16;
     const bool x_in_smem = xbytes <= 160 * 1024;
-    // first-fit decreasing packing of networks into CTAs of <= 16 warps / 15 networks
+    const int mt = online_mt(nets.size(), ref64, dp);
+    const int cap = mt == 1 ? 16 : 8;  // warps per CTA (register budget of the MT-unit tile)
+    // first-fit decreasing packing of networks into CTAs of <= cap warps / 15 networks
     std::stable_sort(nets.begin(), nets.end(), [](const NetReq& a, const NetReq& b) { return a.H > b.H; });
     struct Cta {
         int warps = 0;
@@ -168,11 +182,11 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     std::vector<OnlineNetDesc> desc(nets.size());
     size_t open_from = 0;  // CTAs before this index are full
     for (size_t n = 0; n < nets.size(); n++) {
-        const int nw = (nets[n].H + 31) / 32;
+        const int nw = (nets[n].H + 32 * mt - 1) / (32 * mt);
         const size_t scr = (online_scratch_bytes(nets[n].H, ref64) + 15) / 16 * 16;
         size_t c = open_from;
         for (; c < ctas.size(); c++)
-            if (ctas[c].warps + nw <= 16 && ctas[c].members.size() < 15) break;
+            if (ctas[c].warps + nw <= cap && ctas[c].members.size() < 15) break;
         if (c == ctas.size()) ctas.emplace_back();
         Cta& C = ctas[c];
         OnlineNetDesc& d = desc[n];
@@ -187,7 +201,7 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
         C.warps += nw;
         C.scratch += scr;
         C.members.push_back((int)n);
-        while (open_from < ctas.size() && ctas[open_from].warps >= 16) open_from++;
+        while (open_from < ctas.size() && ctas[open_from].warps >= cap) open_from++;
     }
     // descriptors grouped per CTA
     std::vector<OnlineNetDesc> ordered;
@@ -214,6 +228,7 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     L.smem_bytes = (x_in_smem ? xbytes : 0) + max_scratch;
     L.x_in_smem = x_in_smem;
     L.ref64 = ref64;
+    L.mt = mt;
     L.X = X;
     L.T = T;
     L.N = N;

@@ -25,6 +25,7 @@ struct OnlineLaunch {
     size_t smem_bytes;
     bool x_in_smem;
     bool ref64;
+    int mt;  // fp32 hidden units per thread (1, 2 or 4)
     const float* X;  // device, (N, D)
     const float* T;  // device, (N,)
     int64_t N;

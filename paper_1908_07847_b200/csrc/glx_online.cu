@@ -198,9 +198,127 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
     if (j == 0) w_ho[H] = b2;
 }
 
+
+// fp32 online SGD with an MT-unit register tile per thread (sweeps): the
+// per-row reduction, barrier and output-neuron work are paid once per MT
+// hidden units instead of once per unit.
+template <int DP, int MT, bool XS>
+__global__ void __launch_bounds__(256) online_sgd_mt_kernel(const OnlineNetDesc* __restrict__ nets,
+                                                             const int2* __restrict__ cta_nets,
+                                                             const float* __restrict__ X, const float* __restrict__ T,
+                                                             int64_t N, int D, int64_t epochs, double lr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    float* xs = reinterpret_cast<float*>(smem_raw);
+    float* ts = xs + (XS ? N * DP : 0);
+    const int2 cn = cta_nets[blockIdx.x];
+    const int warp = threadIdx.x >> 5;
+    if (XS) {
+        for (int64_t e = threadIdx.x; e < N * DP; e += blockDim.x) {
+            int64_t r = e / DP;
+            int i = (int)(e - r * DP);
+            xs[e] = i < D ? X[r * D + i] : (i == D ? 1.0f : 0.0f);
+        }
+        for (int64_t r = threadIdx.x; r < N; r += blockDim.x) ts[r] = T[r];
+        __syncthreads();
+    }
+    int my = -1;
+    for (int k = 0; k < cn.y; k++) {
+        const OnlineNetDesc& nd = nets[cn.x + k];
+        if (warp >= nd.warp0 && warp < nd.warp0 + nd.nwarps) my = cn.x + k;
+    }
+    if (my < 0) return;
+    const OnlineNetDesc nd = nets[my];
+    const int H = nd.H;
+    const int nthr = nd.nwarps * 32;
+    const int t = threadIdx.x - nd.warp0 * 32;
+    float* w_ih = nd.w_ih;
+    float* w_ho = nd.w_ho;
+    float* red = reinterpret_cast<float*>(smem_raw + nd.scratch_off);  // [2][16]
+    float2 w[MT][DP / 2];
+    float w2[MT];
+    bool act[MT];
+#pragma unroll
+    for (int u = 0; u < MT; u++) {
+        const int j = t * MT + u;
+        act[u] = j < H;
+#pragma unroll
+        for (int q = 0; q < DP / 2; q++) {
+            const int i0 = 2 * q, i1 = 2 * q + 1;
+            w[u][q] = make_float2((act[u] && i0 <= D) ? w_ih[(int64_t)j * (D + 1) + i0] : 0.f,
+                                  (act[u] && i1 <= D) ? w_ih[(int64_t)j * (D + 1) + i1] : 0.f);
+        }
+        w2[u] = act[u] ? w_ho[j] : 0.f;
+    }
+    float b2 = w_ho[H];
+    const float kScale = (float)(-GLX_LOG2E);
+    const float flr = (float)lr;
+    int buf = 0;
+    float x[DP];
+    for (int64_t ep = 0; ep < epochs; ep++) {
+        for (int64_t r = 0; r < N; r++) {
+            load_row<float, DP, XS>(x, xs, X, r, D);
+            const float tt = XS ? ts[r] : __ldg(T + r);
+            float h[MT];
+            float prod = (t == 0) ? b2 : 0.f;
+#pragma unroll
+            for (int u = 0; u < MT; u++) {
+                float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < DP / 2; q++) p = ffma2(w[u][q], make_float2(x[2 * q], x[2 * q + 1]), p);
+                h[u] = act[u] ? sigmoid_scaled(kScale * (p.x + p.y)) : 0.f;
+                prod = fmaf(w2[u], h[u], prod);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+            if ((threadIdx.x & 31) == 0) red[buf * 16 + (t >> 5)] = prod;
+            bar_sync(nd.bar_id, nthr);
+            float zo = 0.f;
+            for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
+            buf ^= 1;
+            const float o = sigmoid_scaled(kScale * zo);
+            const float d_o = (o - tt) * o * (1.0f - o);
+            const float step_o = flr * d_o;
+#pragma unroll
+            for (int u = 0; u < MT; u++) {
+                const float ns = -flr * (w2[u] * d_o * h[u] * (1.0f - h[u]));
+#pragma unroll
+                for (int q = 0; q < DP / 2; q++) w[u][q] = ffma2(bcast2(ns), make_float2(x[2 * q], x[2 * q + 1]), w[u][q]);
+                w2[u] = fmaf(-step_o, h[u], w2[u]);
+            }
+            if (t == 0) b2 -= step_o;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < MT; u++) {
+        const int j = t * MT + u;
+        if (!act[u]) continue;
+#pragma unroll
+        for (int q = 0; q < DP / 2; q++) {
+            if (2 * q <= D) w_ih[(int64_t)j * (D + 1) + 2 * q] = w[u][q].x;
+            if (2 * q + 1 <= D) w_ih[(int64_t)j * (D + 1) + 2 * q + 1] = w[u][q].y;
+        }
+        w_ho[j] = w2[u];
+    }
+    if (t == 0) w_ho[H] = b2;
+}
+
 // ------------------------------------------------------------------ launcher
+template <int DP, int MT>
+static cudaError_t launch_online_mt(const OnlineLaunch& L, cudaStream_t st) {
+    const size_t smem = L.smem_bytes;
+    auto k = L.x_in_smem ? online_sgd_mt_kernel<DP, MT, true> : online_sgd_mt_kernel<DP, MT, false>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k<<<L.n_ctas, L.threads, smem, st>>>(L.nets, L.cta_nets, L.X, L.T, L.N, L.D, L.epochs, L.lr);
+    return cudaGetLastError();
+}
+
 template <typename Real, int DP>
 static cudaError_t launch_online_dp(const OnlineLaunch& L, cudaStream_t st) {
+    if constexpr (sizeof(Real) == 4) {
+        if (L.mt == 2) return launch_online_mt<DP, 2>(L, st);
+        if (L.mt == 4) return launch_online_mt<DP, 4>(L, st);
+    }
     const size_t smem = L.smem_bytes;
     if (L.x_in_smem) {
         auto k = online_sgd_kernel<Real, DP, true>;

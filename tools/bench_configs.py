@@ -1,0 +1,225 @@
+"""Per-config measurements beyond bench.py's headline (eval).
+
+Prints one JSON object per config; writes them to profiles/ when --out is given.
+Device timings use CUDA events on the launching stream; CPU reference timings use
+the C ports of the reference engines (oracle/, pinned byte-identical).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+import torch  # noqa: E402
+
+import paper_1908_07847_b200 as g  # noqa: E402
+from paper_1908_07847_b200 import _lib, dp  # noqa: E402
+from paper_1908_07847_b200.sweep import pack_pool  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+
+
+def f_train(d, h, k=1):
+    return 4 * h * (d + 1) + 4 * k * (h + 1) + 2 * h * k
+
+
+def fp32_peak(L):
+    tfl = np.zeros(1)
+    ms = np.zeros(1)
+    _lib.check(L.glx_fp32_peak(0, 50_000, _lib.ptr(tfl), _lib.ptr(ms)))
+    return float(tfl[0])
+
+
+def timed(fn, reps=1):
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def cpu_rate(fn, rows, budget_s=5.0):
+    t0 = time.perf_counter()
+    fn(1)
+    dt = time.perf_counter() - t0
+    ep = max(1, int(budget_s / max(dt, 1e-6)))
+    t0 = time.perf_counter()
+    fn(ep)
+    return rows * ep / (time.perf_counter() - t0)
+
+
+def config1(L, peak):
+    """Paper shape online SGD, one network (33-33-1, 90 rows) + both 30-30-1 cohorts."""
+    from conftest import load_case  # fixture data produced by the reference
+
+    out = []
+    for name in ("paper_33_33_1", "cohort_male_30_30_1", "cohort_female_30_30_1"):
+        c = load_case(name)
+        D, H = int(c["meta"][0]), int(c["meta"][1])
+        x, t = c["train_x"], c["train_y"].astype(np.float32)
+        N = x.shape[0]
+        dev = torch.device("cuda")
+        X = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        T = torch.from_numpy(t).to(dev)
+        res = {"config": f"1: {name} online SGD, {N} rows, {D}-{H}-1"}
+        for numerics in ("fp32", "ref64"):
+            net = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=7))
+            w1 = torch.from_numpy(net.w_ih).to(dev)
+            w2 = torch.from_numpy(net.w_ho).to(dev)
+            E = 2000
+            st = torch.cuda.current_stream().cuda_stream
+            run = lambda: _lib.check(L.glx_train_online(w1.data_ptr(), w2.data_ptr(), X.data_ptr(), T.data_ptr(), N,
+                                                        D, H, E, 0.1, _lib.NUMERICS[numerics], st))
+            run()
+            ms = timed(run)
+            res[f"gpu_{numerics}_sample_epochs_per_s"] = N * E / (ms * 1e-3)
+        w1 = net.w_ih2d.copy()
+        w2 = net.w_ho2d.copy()
+        res["cpu_seq_sample_epochs_per_s"] = cpu_rate(lambda e: O.train_online_seq(w1, w2, x, t, e, 0.1), N)
+        res["cpu_par_sample_epochs_per_s"] = cpu_rate(lambda e: O.train_online_par(w1, w2, x, t, e, 0.1), N)
+        res["cpu_cores"] = os.cpu_count()
+        res["note"] = "latency-bound: rows are serial in online SGD; one network uses one CTA"
+        out.append(res)
+    return out
+
+
+def config3(L, peak, epochs=200):
+    """4096 networks (64 widths 8..512 x 64 seeds), paper 90-row split, online fp32."""
+    from conftest import load_case
+
+    c = load_case("paper_33_33_1")
+    x, t = c["train_x"], c["train_y"].astype(np.float32)
+    N, D = x.shape
+    hs, ss = g.sweep_grid(range(8, 513, 8), range(64))
+    nets = [g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=h, seed=s)) for h, s in zip(hs, ss)]
+    pool, H, off = pack_pool(nets)
+    dev = torch.device("cuda")
+    wp = torch.from_numpy(pool).to(dev)
+    X = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    T = torch.from_numpy(t).to(dev)
+    st = torch.cuda.current_stream().cuda_stream
+    res = {"config": f"3: sweep 4096 nets 33->{{8..512}}->1, {N} rows, online", "epochs": epochs}
+    for numerics in ("fp32", "ref64"):
+        ep = epochs if numerics == "fp32" else max(1, epochs // 10)
+        run = lambda: _lib.check(L.glx_train_sweep(len(nets), _lib.ptr(H), _lib.ptr(off), wp.data_ptr(),
+                                                   X.data_ptr(), T.data_ptr(), N, D, ep, 0.1,
+                                                   _lib.NUMERICS[numerics], st))
+        run()
+        ms = timed(run)
+        flops = sum(f_train(D, h) for h in hs) * N * ep
+        res[f"gpu_{numerics}_net_sample_epochs_per_s"] = len(nets) * N * ep / (ms * 1e-3)
+        res[f"gpu_{numerics}_tflops"] = flops / (ms * 1e-3) / 1e12
+        res[f"gpu_{numerics}_frac_fp32_peak"] = flops / (ms * 1e-3) / 1e12 / peak
+        res[f"gpu_{numerics}_ms"] = ms
+    # CPU: the reference engine on a cost-stratified sample of networks, extrapolated by flops
+    idx = list(range(0, 4096, 128))
+    sub = [nets[i].copy() for i in idx]
+    spool, sH, soff = pack_pool(sub)
+    t0 = time.perf_counter()
+    O.train_sweep(sH, soff, spool, x, t, 20, 0.1, os.cpu_count())
+    dt = time.perf_counter() - t0
+    sub_flops = sum(f_train(D, int(h)) for h in sH) * N * 20
+    cpu_tflops = sub_flops / dt / 1e12
+    all_flops = sum(f_train(D, h) for h in hs) * N
+    res["cpu_net_sample_epochs_per_s"] = 4096 * N * (cpu_tflops * 1e12 / all_flops)
+    res["cpu_cores"] = os.cpu_count()
+    res["cpu_sample"] = f"{len(sub)} stratified networks x 20 epochs, train_segment_seq per network, OpenMP over nets"
+    return res
+
+
+def config4_1gpu(L, peak, rows=67_108_864, epochs=5):
+    """64Mi rows, 33->256->1, full batch, on one GPU (the DP config's per-run total)."""
+    dev = torch.device("cuda")
+    D, H = 33, 256
+    ld = int(L.glx_packed_ld(D))
+    Xp = torch.empty((rows, ld), dtype=torch.float32, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    t0 = time.perf_counter()
+    for r0, f, l in g.iter_synthetic_chunks(rows, D, 0, "planted-linear", chunk_rows=1 << 22):
+        Xc = torch.from_numpy(f).to(dev)
+        Tc = torch.from_numpy(l.astype(np.float32)).to(dev)
+        _lib.check(L.glx_pack_rows(Xc.data_ptr(), Tc.data_ptr(), None, f.shape[0], D,
+                                   Xp[r0:r0 + f.shape[0]].data_ptr(), st))
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - t0
+    net = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=0))
+    w1 = torch.from_numpy(net.w_ih).to(dev)
+    w2 = torch.from_numpy(net.w_ho).to(dev)
+    run = lambda: _lib.check(L.glx_train_batch(w1.data_ptr(), w2.data_ptr(), Xp.data_ptr(), rows, D, H, epochs, 0.1,
+                                               None, None, st))
+    run()
+    ms = timed(run) / epochs
+    flops = rows * f_train(D, H)
+    return {"config": "4 (1 GPU): 64Mi rows synthetic_matrix(...,33,0,planted-linear), 33->256->1 full batch",
+            "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
+            "tflops": flops / (ms * 1e-3) / 1e12, "frac_fp32_peak": flops / (ms * 1e-3) / 1e12 / peak,
+            "data_gen_and_pack_s": gen_s}
+
+
+def eval_rate(L, peak):
+    x, l = g.synthetic_arrays(1_000_000, 33, 0, "planted-linear")
+    out = {}
+    dev = torch.device("cuda")
+    for H in (33, 256):
+        net = g.init_weights(g.NetworkConfig(input_dim=33, hidden_dim=H, seed=0))
+        w1 = torch.from_numpy(net.w_ih).to(dev)
+        w2 = torch.from_numpy(net.w_ho).to(dev)
+        X = torch.from_numpy(x).to(dev)
+        Y = torch.from_numpy(l).to(dev)
+        cnt = torch.zeros(4, dtype=torch.int64, device=dev)
+        loss = torch.zeros(1, dtype=torch.float64, device=dev)
+        st = torch.cuda.current_stream().cuda_stream
+        run = lambda: _lib.check(L.glx_eval(w1.data_ptr(), w2.data_ptr(), X.data_ptr(), Y.data_ptr(), x.shape[0], 33,
+                                            H, 1, cnt.data_ptr(), loss.data_ptr(), st))
+        run()
+        ms = timed(run)
+        Xp = torch.empty((x.shape[0], int(L.glx_packed_ld(33))), dtype=torch.float32, device=dev)
+        T = torch.from_numpy(l.astype(np.float32)).to(dev)
+        _lib.check(L.glx_pack_rows(X.data_ptr(), T.data_ptr(), None, x.shape[0], 33, Xp.data_ptr(), st))
+        stats = torch.zeros(5, dtype=torch.float64, device=dev)
+        run2 = lambda: _lib.check(L.glx_eval_packed(w1.data_ptr(), w2.data_ptr(), Xp.data_ptr(), x.shape[0], 33, H,
+                                                    stats.data_ptr(), st))
+        run2()
+        ms2 = timed(run2)
+        f_eval = 2 * H * 34 + 2 * (H + 1)
+        out[f"H{H}"] = {"ref64_rows_per_s": x.shape[0] / (ms * 1e-3), "fp32_rows_per_s": x.shape[0] / (ms2 * 1e-3),
+                        "fp32_frac_fp32_peak": x.shape[0] * f_eval / (ms2 * 1e-3) / 1e12 / peak}
+        w1h, w2h = net.w_ih2d.copy(), net.w_ho2d.copy()
+        t0 = time.perf_counter()
+        O.eval_counts(w1h, w2h, x[:100_000], l[:100_000])
+        out[f"H{H}"]["cpu_rows_per_s_1core"] = 100_000 / (time.perf_counter() - t0)
+    return {"config": "eval_counts, 1M rows x 33", **out}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--which", default="1,3,4,eval")
+    ap.add_argument("--out", default=None)
+    args = ap.parse_args()
+    L = _lib.load()
+    peak = fp32_peak(L)
+    results = {"fp32_peak_tflops": peak}
+    for w in args.which.split(","):
+        fn = {"1": config1, "3": config3, "4": config4_1gpu, "eval": eval_rate}[w]
+        r = fn(L, peak)
+        results[f"config_{w}"] = r
+        print(json.dumps({w: r}), flush=True)
+    if args.out:
+        Path(args.out).write_text(json.dumps(results, indent=1))
+
+
+if __name__ == "__main__":
+    main()
