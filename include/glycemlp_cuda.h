@@ -122,6 +122,13 @@ int glx_eval(const float* w_ih, const float* w_ho, const float* X, const uint8_t
 int glx_eval_packed(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
                     double* stats, void* stream);
 
+/* tcgen05 tensor-core GEMM used by the wide configuration:
+ * D[M x N] = A[M x K] . B[N x K]^T with bf16 row-major A, B (device) and f32
+ * accumulation in TMEM. epilogue 0 writes D as f32 (row stride ldd); epilogue 1
+ * writes bf16 sigmoid(D + bias[col]) to d_bf16. K % 64 == 0, N % 32 == 0. */
+int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue, float* d_f32,
+                     void* d_bf16, const float* bias, int32_t ldd, void* stream);
+
 /* ------------------------------------------------------------ diagnostics */
 /* Number of CUDA kernels this library has launched (for launch accounting). */
 uint64_t glx_launch_count(void);

@@ -625,6 +625,14 @@ int glx_eval_counts(const float* w_ih, const float* w_ho, const float* feats, co
     return GLX_OK;
 }
 
+int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue, float* d_f32,
+                     void* d_bf16, const float* bias, int32_t ldd, void* stream) {
+    if (M < 1 || N < 1 || K < 1 || K % 64 || N % 32)
+        return set_err(GLX_ERR_SHAPE, "tc gemm needs K %% 64 == 0 and N %% 32 == 0 (M=%d N=%d K=%d)", M, N, K);
+    GLX_LAUNCH(launch_tc_gemm(A, B, M, N, K, epilogue, d_f32, d_bf16, bias, ldd, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
 void glx_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof.mu);
     g_prof.on = on != 0;

@@ -91,6 +91,12 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
                               cudaStream_t st);
 cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss_out, cudaStream_t st);
 
+// ------------------------------------------------------------ tcgen05 GEMM
+// D[M x N] = A[M x K] . B[N x K]^T, bf16 row-major operands, f32 accumulation in
+// TMEM. epi 0: D f32 (ldd); epi 1: bf16 sigmoid(D + bias[col]) into d_bf16 (ldd).
+cudaError_t launch_tc_gemm(const void* A, const void* B, int M, int N, int K, int epi, float* d_f32, void* d_bf16,
+                           const float* bias, int ldd, cudaStream_t st);
+
 // ------------------------------------------------------------ diagnostics
 cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st);
 
