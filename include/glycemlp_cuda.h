@@ -129,6 +129,18 @@ int glx_eval_packed(const float* w_ih, const float* w_ho, const float* Xp, int64
 int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t K, int32_t epilogue, float* d_f32,
                      void* d_bf16, const float* bias, int32_t ldd, void* stream);
 
+/* Wide configuration: 1024 inputs -> 1024 hidden -> 16
+ * sigmoid outputs, full-batch GD with every large contraction on tcgen05
+ * (BF16 operands, FP32 accumulation in TMEM). glx_wide_make_data fills the
+ * device buffers Xb (N x 1024 bf16, U[0,1)), XT (1025 x N bf16: X^T plus a
+ * ones row) and labels (N u8 class ids in [0,16)); N % 64 == 0.
+ * glx_wide_train runs `epochs` epochs on f32 master weights in the reference
+ * layout (w_ih 1024 x 1025, w_ho 16 x 1025); stats_hist (device, may be NULL)
+ * gets [loss, correct, wrong] per epoch at the epoch-start weights. */
+int glx_wide_make_data(int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream);
+int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
+                   int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream);
+
 /* ------------------------------------------------------------ diagnostics */
 /* Number of CUDA kernels this library has launched (for launch accounting). */
 uint64_t glx_launch_count(void);

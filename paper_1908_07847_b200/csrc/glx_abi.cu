@@ -75,7 +75,7 @@ struct DevBuf {
 
 // scratch tied to one (device, stream): stream order serialises its reuse
 struct Workspace {
-    DevBuf part, wk, desc, ctan, losspart, grad;
+    DevBuf part, wk, desc, ctan, losspart, grad, wide;
 };
 
 std::mutex g_ws_mu;
@@ -630,6 +630,44 @@ int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t
     if (M < 1 || N < 1 || K < 1 || K % 64 || N % 32)
         return set_err(GLX_ERR_SHAPE, "tc gemm needs K %% 64 == 0 and N %% 32 == 0 (M=%d N=%d K=%d)", M, N, K);
     GLX_LAUNCH(launch_tc_gemm(A, B, M, N, K, epilogue, d_f32, d_bf16, bias, ldd, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_wide_make_data(int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream) {
+    if (N < 64 || N % 64) return set_err(GLX_ERR_SHAPE, "wide data needs N %% 64 == 0 (got %lld)", (long long)N);
+    GLX_LAUNCH(launch_wide_gen(Xb, XT, labels, N, seed, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
+                   int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream) {
+    if (N < 64 || N % 64) return set_err(GLX_ERR_SHAPE, "wide training needs N %% 64 == 0 (got %lld)", (long long)N);
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t C = std::min<int64_t>(N, (int64_t)1 << 20);  // rows per chunk (multiple of 64)
+    const int splits = 8;
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->wide.ensure(wide_work_bytes(C, splits)));
+    for (int64_t e = 0; e < epochs; e++) {
+        double* stats = stats_hist ? stats_hist + 3 * e : nullptr;
+        if (stats) GLX_CK(cudaMemsetAsync(stats, 0, 3 * sizeof(double), st));
+        cudaEvent_t pe = nullptr;
+        cudaError_t perr = cudaSuccess;
+        auto prof = [&](bool begin) {
+            if (begin) {
+                cudaError_t r = prof_begin(st, &pe);
+                if (r != cudaSuccess) perr = r;
+            } else if (pe) {
+                cudaError_t r = cudaEventRecord(pe, st);
+                if (r != cudaSuccess) perr = r;
+                pe = nullptr;
+            }
+        };
+        GLX_CK(wide_epoch(w_ih, w_ho, Xb, XT, labels, N, lr, ws->wide.as<unsigned char>(), C, splits, stats,
+                          nonfinite, st, prof));
+        GLX_CK(perr);
+        g_launches.fetch_add(3 + 5 * (uint64_t)((N + C - 1) / C));
+    }
     return GLX_OK;
 }
 

@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <functional>
+
 namespace glx {
 
 // --------------------------------------------------------------- online SGD
@@ -96,6 +98,13 @@ cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss
 // TMEM. epi 0: D f32 (ldd); epi 1: bf16 sigmoid(D + bias[col]) into d_bf16 (ldd).
 cudaError_t launch_tc_gemm(const void* A, const void* B, int M, int N, int K, int epi, float* d_f32, void* d_bf16,
                            const float* bias, int ldd, cudaStream_t st);
+
+// wide configuration (1024 -> 1024 -> 16) on the tcgen05 GEMM
+cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, cudaStream_t st);
+size_t wide_work_bytes(int64_t C, int splits);
+cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
+                       double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
+                       cudaStream_t st, const std::function<void(bool)>& prof);
 
 // ------------------------------------------------------------ diagnostics
 cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st);

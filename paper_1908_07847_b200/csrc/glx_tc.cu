@@ -18,7 +18,9 @@
 #include "glx_common.cuh"
 #include "glx_kernels.h"
 
+#include <algorithm>
 #include <cstdio>
+#include <functional>
 
 namespace glx {
 
@@ -79,17 +81,37 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
 }
 
 struct TcEpilogue {
-    int kind;            // 0: D f32 store; 1: bias + sigmoid -> bf16 store
-    float* d_f32;        // kind 0
-    __nv_bfloat16* d_bf16;  // kind 1
-    const float* bias;   // kind 1: per column (length N)
-    int ldd;             // leading dimension of D (elements)
+    int kind;               // 0: f32 store; 1: bias+sigmoid -> bf16; 2: output layer; 3: delta_h^T; 4: f32 accumulate
+    float* d_f32;           // 0, 4 (4: + blockIdx.z * zstride)
+    __nv_bfloat16* d_bf16;  // 1
+    const float* bias;      // 1, 2
+    int ldd;
+    int64_t zstride;
+    // 2: output neuron per row (wide config): K sigmoid outputs, one-hot targets from labels
+    const uint8_t* labels;
+    int K;
+    __nv_bfloat16* do_b;  // [M][64] bf16, columns >= K stay zero
+    float* do_f;          // [M][K] f32
+    double* stats;        // [loss, correct, wrong]
+    // 3: delta_h = v * h (1 - h), written transposed
+    const __nv_bfloat16* h;
+    int ldh;
+    __nv_bfloat16* dht;
+    int64_t ldt;
+};
+
+struct TcGemm {
+    const void* A;  // [M x K] bf16, row stride lda
+    const void* B;  // [N x K] bf16, row stride ldb
+    int M, N, K;
+    int64_t lda, ldb;
+    int splits;  // split-K: blockIdx.z takes K / splits
 };
 
 template <int BN>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                                                                   const __grid_constant__ CUtensorMap map_b, int M,
-                                                                  int N, int K, TcEpilogue ep) {
+                                                                  int N, int K, int kb_per_split, TcEpilogue ep) {
     constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
     constexpr uint32_t kBBytes = BN * kTcBK * 2;
     constexpr uint32_t kStage = kABytes + kBBytes;
@@ -104,7 +126,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * BN;
-    const int nk = K / kTcBK;
+    const int kb0 = blockIdx.z * kb_per_split;
+    const int nk = min(K / kTcBK - kb0, kb_per_split);  // this CTA's K blocks (split-K over blockIdx.z)
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kTcStages; s++) {
@@ -134,8 +157,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 if (kb >= kTcStages) mbar_wait(&empty[s], ((kb / kTcStages) - 1) & 1);
                 unsigned char* st = sm + s * kStage;
                 mbar_arrive_expect_tx(&full[s], kStage);
-                tma_load_2d(st, &map_a, kb * kTcBK, m0, &full[s]);
-                tma_load_2d(st + kABytes, &map_b, kb * kTcBK, n0, &full[s]);
+                tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
+                tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
             }
         }
     } else if (warp == 1) {
@@ -162,22 +185,89 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         mbar_wait(done, 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const int row = m0 + quad * 32 + lane;
+        const bool rv = row < M;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
             float v[32];
             tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c, v);
-            if (row < M) {
-                if (ep.kind == 0) {
-                    float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (int64_t)row * ep.ldd + n0 + c);
+            if (ep.kind == 0 || ep.kind == 4) {
+                if (rv) {
+                    float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (ep.kind == 4 ? blockIdx.z * ep.zstride : 0) +
+                                                            (int64_t)row * ep.ldd + n0 + c);
 #pragma unroll
-                    for (int q = 0; q < 8; q++) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                } else {
+                    for (int q = 0; q < 8; q++) {
+                        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        if (ep.kind == 4) {
+                            const float4 p = dst[q];
+                            o.x += p.x;
+                            o.y += p.y;
+                            o.z += p.z;
+                            o.w += p.w;
+                        }
+                        dst[q] = o;
+                    }
+                }
+            } else if (ep.kind == 1) {
+                if (rv) {
                     __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(ep.d_bf16 + (int64_t)row * ep.ldd + n0 + c);
 #pragma unroll
                     for (int q = 0; q < 16; q++) {
                         const float z0 = v[2 * q] + ep.bias[n0 + c + 2 * q];
                         const float z1 = v[2 * q + 1] + ep.bias[n0 + c + 2 * q + 1];
                         dst[q] = __floats2bfloat162_rn(1.0f / (1.0f + __expf(-z0)), 1.0f / (1.0f + __expf(-z1)));
+                    }
+                }
+            } else if (ep.kind == 2) {
+                // output neuron (kernels.py:352-375 generalised to K outputs)
+                float loss = 0.f, correct = 0.f, wrong = 0.f;
+                if (rv) {
+                    const int lab = ep.labels[row];
+                    float best = -1.f;
+                    int arg = 0;
+#pragma unroll
+                    for (int k = 0; k < 32; k++) {
+                        if (k >= ep.K) break;
+                        const float o = 1.0f / (1.0f + __expf(-(v[k] + ep.bias[k])));
+                        const float t = (k == lab) ? 1.f : 0.f;
+                        const float d = (o - t) * o * (1.0f - o);
+                        loss = fmaf(0.5f * (t - o), t - o, loss);
+                        if (o > best) {
+                            best = o;
+                            arg = k;
+                        }
+                        ep.do_b[(int64_t)row * 64 + k] = __float2bfloat16_rn(d);
+                        ep.do_f[(int64_t)row * ep.K + k] = d;
+                    }
+                    correct = arg == lab ? 1.f : 0.f;
+                    wrong = 1.f - correct;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    loss += __shfl_xor_sync(0xffffffffu, loss, o);
+                    correct += __shfl_xor_sync(0xffffffffu, correct, o);
+                    wrong += __shfl_xor_sync(0xffffffffu, wrong, o);
+                }
+                if (lane == 0) {
+                    atomicAdd(ep.stats + 0, (double)loss);
+                    atomicAdd(ep.stats + 1, (double)correct);
+                    atomicAdd(ep.stats + 2, (double)wrong);
+                }
+            } else {
+                // delta_h = (delta_o W2)_j * h (1 - h), stored transposed for the dW1 GEMM
+                if (rv) {
+                    const uint4* hp = reinterpret_cast<const uint4*>(ep.h + (int64_t)row * ep.ldh + n0 + c);
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; q4++) {
+                        const uint4 hv = hp[q4];
+                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv);
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const float2 hf = __bfloat1622float2(h2[e]);
+                            const int col = n0 + c + q4 * 8 + 2 * e;
+                            ep.dht[(int64_t)col * ep.ldt + row] = __float2bfloat16_rn(v[q4 * 8 + 2 * e] * hf.x * (1.f - hf.x));
+                            ep.dht[(int64_t)(col + 1) * ep.ldt + row] =
+                                __float2bfloat16_rn(v[q4 * 8 + 2 * e + 1] * hf.y * (1.f - hf.y));
+                        }
                     }
                 }
             }
@@ -208,12 +298,13 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// row-major [rows x cols] bf16 matrix, box [box_rows x 64 cols], 128-byte swizzle
-static bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int box_rows) {
+// row-major [rows x cols] bf16 matrix with row stride ld (elements), box
+// [box_rows x 64 cols], 128-byte swizzle; rows beyond `rows` read as zero
+static bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
     cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
@@ -222,28 +313,312 @@ static bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int6
 }
 
 template <int BN>
-static cudaError_t tc_launch(const void* A, const void* B, int M, int N, int K, const TcEpilogue& ep,
-                             cudaStream_t st) {
+static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
     CUtensorMap ma, mb;
-    if (!make_map_bf16(&ma, A, M, K, kTcBM) || !make_map_bf16(&mb, B, N, K, BN)) return cudaErrorInvalidValue;
+    if (!make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM) || !make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN))
+        return cudaErrorInvalidValue;
     const size_t smem = 1024 + (size_t)kTcStages * (kTcBM + BN) * kTcBK * 2 + 256;
     auto k = tc_gemm_kernel<BN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    dim3 grid(N / BN, (M + kTcBM - 1) / kTcBM);
-    k<<<grid, kTcThreads, smem, st>>>(ma, mb, M, N, K, ep);
+    const int nk = g.K / kTcBK;
+    const int splits = g.splits < 1 ? 1 : g.splits;
+    const int kps = (nk + splits - 1) / splits;
+    dim3 grid(g.N / BN, (g.M + kTcBM - 1) / kTcBM, (nk + kps - 1) / kps);
+    k<<<grid, kTcThreads, smem, st>>>(ma, mb, g.M, g.N, g.K, kps, ep);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tc(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
+    if (g.K % kTcBK != 0) return cudaErrorInvalidValue;
+    if (g.N % 256 == 0 && ep.kind != 2) return tc_launch<256>(g, ep, st);
+    if (g.N % 128 == 0 && ep.kind != 2) return tc_launch<128>(g, ep, st);
+    if (g.N % 64 == 0 && ep.kind != 2) return tc_launch<64>(g, ep, st);
+    if (g.N % 32 == 0) return tc_launch<32>(g, ep, st);
+    return cudaErrorInvalidValue;
+}
+
+
+// =========================================================== wide config
+// D = 1024 inputs, H = 1024 hidden, K = 16 sigmoid outputs,
+// full-batch GD. Per epoch, in row chunks of C rows:
+//   1. H     = sigmoid(X W1^T + b1)                 tcgen05, epilogue 1 -> bf16
+//   2. delta_o per row (one-hot targets, K outputs)  tcgen05 (N=32 padded), epilogue 2
+//   3. dH^T  = ((delta_o W2) * h(1-h))^T              tcgen05 (K=64 padded), epilogue 3
+//   4. dW1^T += [X,1]^T dH                            tcgen05 split-K, epilogue 4 (f32 accumulate)
+//   5. dW2   += delta_o^T [H,1]                       CUDA cores
+// then W <- f32(W - lr/N grad) on the f32 master weights (reference layout).
+constexpr int kWD = 1024, kWH = 1024, kWK = 16;
+constexpr int kWMi = 1152;  // [X,1]^T rows padded to a multiple of 128 (rows > 1024 read as zero)
+
+__device__ __forceinline__ uint32_t mix32(uint64_t x) {
+    x ^= x >> 33;
+    x *= 0xff51afd7ed558ccdULL;
+    x ^= x >> 33;
+    x *= 0xc4ceb9fe1a85ec53ULL;
+    x ^= x >> 33;
+    return (uint32_t)x;
+}
+__device__ __forceinline__ float unit_u01(uint64_t seed, uint64_t idx) {
+    return (mix32(seed * 0x9E3779B97F4A7C15ULL + idx) >> 8) * (1.0f / 16777216.0f);
+}
+
+// X[r][i] ~ U[0,1) (counter-based hash), bf16; labels = argmax_k of 16 planted
+// linear scores over 32 fixed columns (a K-class analogue of synthetic_matrix's
+// planted-linear labels)
+__global__ void wide_gen_kernel(__nv_bfloat16* __restrict__ X, uint8_t* __restrict__ labels, int64_t N,
+                                uint64_t seed) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
+    if (r >= N) return;
+    float score[kWK];
+#pragma unroll
+    for (int k = 0; k < kWK; k++) score[k] = 0.f;
+    for (int i = threadIdx.x; i < kWD; i += 32) {
+        const float v = unit_u01(seed, (uint64_t)r * kWD + i);
+        const __nv_bfloat16 b = __float2bfloat16_rn(v);
+        X[r * kWD + i] = b;
+        if ((i & 31) == 7) {  // 32 planted columns
+            const float vb = __bfloat162float(b) - 0.5f;  // centred: classes come out balanced
+#pragma unroll
+            for (int k = 0; k < kWK; k++) score[k] += (unit_u01(seed ^ 0xABCDEFULL, (uint64_t)k * kWD + i) - 0.5f) * vb;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < kWK; k++)
+        for (int o = 16; o > 0; o >>= 1) score[k] += __shfl_xor_sync(0xffffffffu, score[k], o);
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int k = 1; k < kWK; k++)
+            if (score[k] > score[best]) best = k;
+        labels[r] = (uint8_t)best;
+    }
+}
+
+// XT[i][r] = X[r][i] for i < 1024, XT[1024][r] = 1 (bias input)
+__global__ void wide_transpose_kernel(const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ XT, int64_t N) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int i0 = blockIdx.y * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t r = r0 + dy;
+        tile[dy][threadIdx.x] = r < N ? X[r * kWD + i0 + threadIdx.x] : __float2bfloat16_rn(0.f);
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t r = r0 + threadIdx.x;
+        if (r < N) XT[(int64_t)(i0 + dy) * N + r] = tile[threadIdx.x][dy];
+    }
+    if (blockIdx.y == 0 && threadIdx.y == 0) {
+        const int64_t r = r0 + threadIdx.x;
+        if (r < N) XT[(int64_t)kWD * N + r] = __float2bfloat16_rn(1.f);
+    }
+}
+
+// bf16 operand copies of the f32 master weights for this epoch
+__global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __restrict__ W2,
+                                   __nv_bfloat16* __restrict__ W1b, float* __restrict__ b1,
+                                   __nv_bfloat16* __restrict__ W2b, float* __restrict__ b2,
+                                   __nv_bfloat16* __restrict__ W2T) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < kWH * kWD) {
+        const int j = e / kWD, i = e % kWD;
+        W1b[e] = __float2bfloat16_rn(W1[(int64_t)j * (kWD + 1) + i]);
+    }
+    if (e < kWH) b1[e] = W1[(int64_t)e * (kWD + 1) + kWD];
+    if (e < 32 * kWH) {
+        const int k = e / kWH, j = e % kWH;
+        W2b[e] = __float2bfloat16_rn(k < kWK ? W2[k * (kWH + 1) + j] : 0.f);
+    }
+    if (e < kWH * 64) {
+        const int j = e / 64, k = e % 64;
+        W2T[e] = __float2bfloat16_rn(k < kWK ? W2[k * (kWH + 1) + j] : 0.f);
+    }
+    if (e < kWK) b2[e] = W2[e * (kWH + 1) + kWH];
+}
+
+// dW2[k][j] += sum_r delta_o[r][k] h[r][j]; column kWH is the bias (h = 1)
+__global__ void __launch_bounds__(256) wide_dw2_kernel(const float* __restrict__ dof, const __nv_bfloat16* __restrict__ H,
+                                                       int64_t rows, double* __restrict__ dW2) {
+    const int j = blockIdx.x * 64 + (threadIdx.x & 63);
+    const int sub = threadIdx.x >> 6;  // 4 row phases
+    float acc[kWK];
+#pragma unroll
+    for (int k = 0; k < kWK; k++) acc[k] = 0.f;
+    if (j <= kWH) {
+        for (int64_t r = (int64_t)blockIdx.y * 4 + sub; r < rows; r += (int64_t)gridDim.y * 4) {
+            const float h = j < kWH ? __bfloat162float(H[r * kWH + j]) : 1.f;
+            const float4* d4 = reinterpret_cast<const float4*>(dof + r * kWK);
+#pragma unroll
+            for (int q = 0; q < kWK / 4; q++) {
+                const float4 d = d4[q];
+                acc[4 * q] = fmaf(d.x, h, acc[4 * q]);
+                acc[4 * q + 1] = fmaf(d.y, h, acc[4 * q + 1]);
+                acc[4 * q + 2] = fmaf(d.z, h, acc[4 * q + 2]);
+                acc[4 * q + 3] = fmaf(d.w, h, acc[4 * q + 3]);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kWK; k++) atomicAdd(dW2 + k * (kWH + 1) + j, (double)acc[k]);
+    }
+}
+
+__global__ void wide_update_kernel(float* __restrict__ W1, float* __restrict__ W2, const float* __restrict__ dW1T,
+                                   int splits, int64_t zstride, const double* __restrict__ dW2, double lr_over_n,
+                                   int* __restrict__ nonfinite) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < kWH * (kWD + 1)) {
+        const int j = e / (kWD + 1), i = e % (kWD + 1);
+        double g = 0.0;
+        for (int z = 0; z < splits; z++) g += (double)dW1T[z * zstride + (int64_t)i * kWH + j];
+        const float w = __double2float_rn((double)W1[e] - lr_over_n * g);
+        W1[e] = w;
+        if (!isfinite(w) && nonfinite) atomicOr(nonfinite, 1);
+    }
+    if (e < kWK * (kWH + 1)) {
+        const float w = __double2float_rn((double)W2[e] - lr_over_n * dW2[e]);
+        W2[e] = w;
+        if (!isfinite(w) && nonfinite) atomicOr(nonfinite, 1);
+    }
+}
+
+cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, cudaStream_t st) {
+    dim3 blk(32, 8);
+    wide_gen_kernel<<<(unsigned)((N + 7) / 8), blk, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(Xb), labels, N, seed);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((N + 31) / 32), kWD / 32);
+    wide_transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(reinterpret_cast<const __nv_bfloat16*>(Xb),
+                                                       reinterpret_cast<__nv_bfloat16*>(XT), N);
+    return cudaGetLastError();
+}
+
+struct WideWork {
+    void* W1b;
+    float* b1;
+    void* W2b;
+    float* b2;
+    void* W2T;
+    void* Hb;
+    void* dob;
+    float* dof;
+    void* dht;
+    float* dW1T;
+    double* dW2;
+    int64_t C;
+    int splits;
+};
+
+size_t wide_work_bytes(int64_t C, int splits) {
+    return (size_t)kWH * kWD * 2 + kWH * 4 + 32 * kWH * 2 + 64 + (size_t)kWH * 64 * 2 + (size_t)C * kWH * 2 +
+           (size_t)C * 64 * 2 + (size_t)C * kWK * 4 + (size_t)kWH * C * 2 + (size_t)splits * kWMi * kWH * 4 +
+           (size_t)kWK * (kWH + 1) * 8 + 64 * 16;
+}
+
+static void carve(WideWork& w, unsigned char* base, int64_t C, int splits) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        void* p = base + o;
+        o += (bytes + 255) / 256 * 256;
+        return p;
+    };
+    w.W1b = take((size_t)kWH * kWD * 2);
+    w.b1 = (float*)take(kWH * 4);
+    w.W2b = take(32 * kWH * 2);
+    w.b2 = (float*)take(64);
+    w.W2T = take((size_t)kWH * 64 * 2);
+    w.Hb = take((size_t)C * kWH * 2);
+    w.dob = take((size_t)C * 64 * 2);
+    w.dof = (float*)take((size_t)C * kWK * 4);
+    w.dht = take((size_t)kWH * C * 2);
+    w.dW1T = (float*)take((size_t)splits * kWMi * kWH * 4);
+    w.dW2 = (double*)take((size_t)kWK * (kWH + 1) * 8);
+    w.C = C;
+    w.splits = splits;
+}
+
+// one epoch; stats (device, may be null): [loss, correct, wrong] accumulated
+cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
+                       double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
+                       cudaStream_t st, const std::function<void(bool)>& prof) {
+    WideWork w;
+    carve(w, work, C, splits);
+    cudaError_t e;
+    const int n_derive = kWH * kWD;
+    wide_derive_kernel<<<(n_derive + 255) / 256, 256, 0, st>>>(W1, W2, (__nv_bfloat16*)w.W1b, w.b1,
+                                                               (__nv_bfloat16*)w.W2b, w.b2, (__nv_bfloat16*)w.W2T);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int64_t zstride = (int64_t)kWMi * kWH;
+    if ((e = cudaMemsetAsync(w.dW1T, 0, (size_t)splits * zstride * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.dW2, 0, (size_t)kWK * (kWH + 1) * 8, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 64 * 2, st)) != cudaSuccess) return e;
+    for (int64_t r0 = 0; r0 < N; r0 += C) {
+        const int Cc = (int)std::min<int64_t>(C, N - r0);
+        const __nv_bfloat16* Xc = reinterpret_cast<const __nv_bfloat16*>(Xb) + r0 * kWD;
+        prof(true);
+        {  // 1. hidden layer
+            TcGemm g{Xc, w.W1b, Cc, kWH, kWD, kWD, kWD, 1};
+            TcEpilogue ep{};
+            ep.kind = 1;
+            ep.d_bf16 = (__nv_bfloat16*)w.Hb;
+            ep.bias = w.b1;
+            ep.ldd = kWH;
+            if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 2. output layer -> delta_o, loss, accuracy
+            TcGemm g{w.Hb, w.W2b, Cc, 32, kWH, kWH, kWH, 1};
+            TcEpilogue ep{};
+            ep.kind = 2;
+            ep.bias = w.b2;
+            ep.labels = labels + r0;
+            ep.K = kWK;
+            ep.do_b = (__nv_bfloat16*)w.dob;
+            ep.do_f = w.dof;
+            ep.stats = stats;
+            if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 3. hidden deltas, transposed
+            TcGemm g{w.dob, w.W2T, Cc, kWH, 64, 64, 64, 1};
+            TcEpilogue ep{};
+            ep.kind = 3;
+            ep.h = (const __nv_bfloat16*)w.Hb;
+            ep.ldh = kWH;
+            ep.dht = (__nv_bfloat16*)w.dht;
+            ep.ldt = C;
+            if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 4. dW1^T += [X,1]^T dH (split-K over the chunk's rows)
+            const __nv_bfloat16* XTc = reinterpret_cast<const __nv_bfloat16*>(XT) + r0;
+            TcGemm g{XTc, w.dht, kWD + 1, kWH, Cc, N, C, splits};
+            TcEpilogue ep{};
+            ep.kind = 4;
+            ep.d_f32 = w.dW1T;
+            ep.ldd = kWH;
+            ep.zstride = zstride;
+            if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
+        }
+        prof(false);
+        {  // 5. dW2
+            dim3 grid((kWH + 1 + 63) / 64, 148);
+            wide_dw2_kernel<<<grid, 256, 0, st>>>(w.dof, (const __nv_bfloat16*)w.Hb, Cc, w.dW2);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+    }
+    const int nu = kWH * (kWD + 1);
+    wide_update_kernel<<<(nu + 255) / 256, 256, 0, st>>>(W1, W2, w.dW1T, splits, zstride, w.dW2, lr / (double)N,
+                                                         nonfinite);
     return cudaGetLastError();
 }
 
 cudaError_t launch_tc_gemm(const void* A, const void* B, int M, int N, int K, int epi, float* d_f32,
                            void* d_bf16, const float* bias, int ldd, cudaStream_t st) {
-    if (K % kTcBK != 0) return cudaErrorInvalidValue;
-    TcEpilogue ep{epi, d_f32, reinterpret_cast<__nv_bfloat16*>(d_bf16), bias, ldd};
-    if (N % 256 == 0) return tc_launch<256>(A, B, M, N, K, ep, st);
-    if (N % 128 == 0) return tc_launch<128>(A, B, M, N, K, ep, st);
-    if (N % 64 == 0) return tc_launch<64>(A, B, M, N, K, ep, st);
-    if (N % 32 == 0) return tc_launch<32>(A, B, M, N, K, ep, st);
-    return cudaErrorInvalidValue;
+    TcGemm g{A, B, M, N, K, K, K, 1};
+    TcEpilogue ep{};
+    ep.kind = epi;
+    ep.d_f32 = d_f32;
+    ep.d_bf16 = reinterpret_cast<__nv_bfloat16*>(d_bf16);
+    ep.bias = bias;
+    ep.ldd = ldd;
+    return launch_tc(g, ep, st);
 }
 
 }  // namespace glx

@@ -1,0 +1,77 @@
+"""Wide configuration: 1024 -> 1024 -> 16, full-batch GD on tcgen05.
+
+Every large contraction of the epoch (hidden layer, hidden deltas, dW1) runs on
+the hand-written tcgen05 GEMM of csrc/glx_tc.cu with BF16 operands and FP32
+TMEM accumulation; the f32 master weights keep the reference layout
+(w_ih 1024 x 1025, w_ho 16 x 1025) and take the update in f64. The rows are
+generated on the device (16M x 1024 does not fit host RAM as f32): U[0,1)
+features from a counter-based hash and K=16 labels = argmax of 16 planted
+linear scores (a build decision; parity for K>1 is against the
+oracle restatement, not the reference).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import ShapeError
+
+D, H, K = 1024, 1024, 16
+
+
+class WideData:
+    """Device-resident rows: Xb (N x 1024 bf16), XT (1025 x N bf16), labels (N u8)."""
+
+    def __init__(self, n_rows: int, seed: int = 0, device: int = 0):
+        import torch
+
+        if n_rows < 64 or n_rows % 64:
+            raise ShapeError(f"wide data needs a positive multiple of 64 rows, got {n_rows}")
+        self.N = n_rows
+        self.dev = torch.device("cuda", device)
+        L = _lib.load()
+        with torch.cuda.device(self.dev):
+            self.Xb = torch.empty((n_rows, D), dtype=torch.bfloat16, device=self.dev)
+            self.XT = torch.empty((D + 1, n_rows), dtype=torch.bfloat16, device=self.dev)
+            self.labels = torch.empty(n_rows, dtype=torch.uint8, device=self.dev)
+            _lib.check(L.glx_wide_make_data(n_rows, seed, self.Xb.data_ptr(), self.XT.data_ptr(),
+                                            self.labels.data_ptr(), torch.cuda.current_stream().cuda_stream))
+
+    def host_rows(self) -> tuple[np.ndarray, np.ndarray]:
+        """(features f32 = the exact bf16 values, labels u8) for CPU checking."""
+        return self.Xb.float().cpu().numpy(), self.labels.cpu().numpy()
+
+
+def init_wide_weights(seed: int = 0, init_range: float = 0.5) -> tuple[np.ndarray, np.ndarray]:
+    """Reference-style init (network.py:110-116) for the 1024-1024-16 shape."""
+    gen = np.random.default_rng(seed)
+    w_ih = gen.uniform(-init_range, init_range, H * (D + 1)).astype(np.float32)
+    w_ho = gen.uniform(-init_range, init_range, K * (H + 1)).astype(np.float32)
+    return w_ih, w_ho
+
+
+def train_wide(data: WideData, w_ih: np.ndarray, w_ho: np.ndarray, epochs: int, lr: float,
+               stats: np.ndarray | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Run `epochs` full-batch epochs; returns the updated (w_ih, w_ho) copies.
+
+    stats, if given, is a float64 (epochs, 3) array: loss sum, correct, wrong
+    at each epoch's starting weights.
+    """
+    import torch
+
+    if w_ih.size != H * (D + 1) or w_ho.size != K * (H + 1):
+        raise ShapeError("wide weights must be 1024 x 1025 and 16 x 1025")
+    L = _lib.load()
+    with torch.cuda.device(data.dev):
+        st = torch.cuda.current_stream()
+        w1 = torch.from_numpy(np.ascontiguousarray(w_ih, dtype=np.float32)).to(data.dev)
+        w2 = torch.from_numpy(np.ascontiguousarray(w_ho, dtype=np.float32)).to(data.dev)
+        sd = torch.zeros((max(epochs, 1), 3), dtype=torch.float64, device=data.dev)
+        flag = torch.zeros(1, dtype=torch.int32, device=data.dev)
+        _lib.check(L.glx_wide_train(w1.data_ptr(), w2.data_ptr(), data.Xb.data_ptr(), data.XT.data_ptr(),
+                                    data.labels.data_ptr(), data.N, int(epochs), float(lr), sd.data_ptr(),
+                                    flag.data_ptr(), st.cuda_stream))
+        if stats is not None:
+            stats[:] = sd[:epochs].cpu().numpy()
+        return w1.cpu().numpy(), w2.cpu().numpy()

@@ -42,3 +42,36 @@ def test_tc_gemm_sigmoid_epilogue(gpu):
     ref = torch.sigmoid(A.float() @ B.float().T + bias)
     torch.cuda.synchronize()
     assert (H.float() - ref).abs().max().item() < 4e-3  # bf16 rounding of values in (0, 1)
+
+
+@pytest.mark.parametrize("init_range,lr,tol", [
+    (0.5, 0.1, 1e-4),   # reference defaults (init 0.5, lr 0.1; network.py:31-57): within SURVEY.md 8(c)'s 1e-4
+    (0.5, 0.5, 5e-4),   # 5x the default step: BF16 rounding of h / W2 in the output GEMM shows in W2
+    (0.05, 4.0, 1e-3),  # stress: weights move ~100x more per epoch than at the defaults
+])
+def test_wide_config_vs_oracle(gpu, init_range, lr, tol):
+    """Config 5 shape 1024-1024-16 on tcgen05 (BF16 operands) vs the oracle's f64 K=16
+    full-batch restatement on the same (bf16-valued) rows."""
+    import numpy as np
+
+    from conftest import rel_err
+    from oracle import oracle as O
+    from paper_1908_07847_b200 import wide
+
+    data = wide.WideData(2048, seed=5)
+    x, y = data.host_rows()
+    counts = np.bincount(y, minlength=16)
+    assert counts.min() > 0 and counts.max() < 4 * 2048 / 16, counts  # balanced classes
+    w1, w2 = wide.init_wide_weights(seed=3, init_range=init_range)
+    stats = np.zeros((3, 3))
+    g1, g2 = wide.train_wide(data, w1, w2, 3, lr, stats)
+    r1, r2 = w1.copy().reshape(1024, 1025), w2.copy().reshape(16, 1025)
+    T = np.eye(16, dtype=np.float32)[y]
+    O.train_batch_par(r1, r2, x, T, 3, lr)
+    e1, e2 = rel_err(g1, r1.reshape(-1)), rel_err(g2, r2.reshape(-1))
+    assert e1 <= tol and e2 <= tol, (e1, e2)
+    # epoch-0 statistics = evaluation of the initial weights
+    (correct, wrong, _, _), loss = O.eval_counts(w1.reshape(1024, 1025), w2.reshape(16, 1025), x, y)
+    assert stats[0, 1] + stats[0, 2] == 2048
+    assert abs(stats[0, 0] - loss) <= 5e-3 * loss
+    assert abs(stats[0, 1] - correct) <= 20
