@@ -26,7 +26,13 @@ namespace glx {
 
 constexpr int kTcBM = 128;
 constexpr int kTcBK = 64;  // bf16 elements per 128-byte swizzled row
-constexpr int kTcStages = 4;
+#ifndef GLX_TC_MAXBN
+#define GLX_TC_MAXBN 256  // widest N tile (TMEM columns) per CTA
+#endif
+#ifndef GLX_TC_STAGES
+#define GLX_TC_STAGES 2  // 2 stages -> 2 CTAs per SM: one tile's epilogue overlaps the other's MMAs
+#endif
+constexpr int kTcStages = GLX_TC_STAGES;
 constexpr int kTcThreads = 192;
 
 // ------------------------------------------------------------- descriptors
@@ -209,12 +215,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 }
             } else if (ep.kind == 1) {
                 if (rv) {
-                    __nv_bfloat162* dst = reinterpret_cast<__nv_bfloat162*>(ep.d_bf16 + (int64_t)row * ep.ldd + n0 + c);
+                    // 16-byte stores: 8 bf16 per store, 4 per 32-column chunk
+                    uint4* dst = reinterpret_cast<uint4*>(ep.d_bf16 + (int64_t)row * ep.ldd + n0 + c);
+                    const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c);
 #pragma unroll
-                    for (int q = 0; q < 16; q++) {
-                        const float z0 = v[2 * q] + ep.bias[n0 + c + 2 * q];
-                        const float z1 = v[2 * q + 1] + ep.bias[n0 + c + 2 * q + 1];
-                        dst[q] = __floats2bfloat162_rn(1.0f / (1.0f + __expf(-z0)), 1.0f / (1.0f + __expf(-z1)));
+                    for (int q = 0; q < 4; q++) {
+                        uint32_t pk[4];
+#pragma unroll
+                        for (int e = 0; e < 4; e++) {
+                            const float4 bb = b4[(8 * q + 2 * e) / 4];
+                            const float b0 = ((2 * e) & 3) == 0 ? bb.x : bb.z;
+                            const float b1 = ((2 * e) & 3) == 0 ? bb.y : bb.w;
+                            const float z0 = v[8 * q + 2 * e] + b0;
+                            const float z1 = v[8 * q + 2 * e + 1] + b1;
+                            const __nv_bfloat162 h2 = __floats2bfloat162_rn(__frcp_rn(1.0f + __expf(-z0)),
+                                                                            __frcp_rn(1.0f + __expf(-z1)));
+                            pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+                        }
+                        dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
                     }
                 }
             } else if (ep.kind == 2) {
@@ -247,7 +265,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     correct += __shfl_xor_sync(0xffffffffu, correct, o);
                     wrong += __shfl_xor_sync(0xffffffffu, wrong, o);
                 }
-                if (lane == 0) {
+                if (lane == 0 && ep.stats) {
                     atomicAdd(ep.stats + 0, (double)loss);
                     atomicAdd(ep.stats + 1, (double)correct);
                     atomicAdd(ep.stats + 2, (double)wrong);
@@ -331,8 +349,8 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
 
 cudaError_t launch_tc(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
     if (g.K % kTcBK != 0) return cudaErrorInvalidValue;
-    if (g.N % 256 == 0 && ep.kind != 2) return tc_launch<256>(g, ep, st);
-    if (g.N % 128 == 0 && ep.kind != 2) return tc_launch<128>(g, ep, st);
+    if (GLX_TC_MAXBN >= 256 && g.N % 256 == 0 && ep.kind != 2) return tc_launch<256>(g, ep, st);
+    if (GLX_TC_MAXBN >= 128 && g.N % 128 == 0 && ep.kind != 2) return tc_launch<128>(g, ep, st);
     if (g.N % 64 == 0 && ep.kind != 2) return tc_launch<64>(g, ep, st);
     if (g.N % 32 == 0) return tc_launch<32>(g, ep, st);
     return cudaErrorInvalidValue;
@@ -436,29 +454,59 @@ __global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __
     if (e < kWK) b2[e] = W2[e * (kWH + 1) + kWH];
 }
 
-// dW2[k][j] += sum_r delta_o[r][k] h[r][j]; column kWH is the bias (h = 1)
-__global__ void __launch_bounds__(256) wide_dw2_kernel(const float* __restrict__ dof, const __nv_bfloat16* __restrict__ H,
-                                                       int64_t rows, double* __restrict__ dW2) {
-    const int j = blockIdx.x * 64 + (threadIdx.x & 63);
-    const int sub = threadIdx.x >> 6;  // 4 row phases
-    float acc[kWK];
+// dW2[k][j] += sum_r delta_o[r][k] h[r][j]; column kWH is the bias (h = 1).
+// Block = 64 threads x 4 hidden columns each (256 columns) + one row slice;
+// delta_o rows are staged in shared memory and read as broadcasts.
+__global__ void __launch_bounds__(64) wide_dw2_kernel(const float* __restrict__ dof, const __nv_bfloat16* __restrict__ H,
+                                                      int64_t rows, double* __restrict__ dW2) {
+    constexpr int RT = 64;  // rows per smem stage
+    __shared__ float4 sd[RT][kWK / 4];
+    const int j0 = blockIdx.x * 256 + threadIdx.x * 4;  // 4 columns; block 4 also covers the bias column
+    const bool bias_blk = blockIdx.x == kWH / 256;
+    float acc[4][kWK];
 #pragma unroll
-    for (int k = 0; k < kWK; k++) acc[k] = 0.f;
-    if (j <= kWH) {
-        for (int64_t r = (int64_t)blockIdx.y * 4 + sub; r < rows; r += (int64_t)gridDim.y * 4) {
-            const float h = j < kWH ? __bfloat162float(H[r * kWH + j]) : 1.f;
-            const float4* d4 = reinterpret_cast<const float4*>(dof + r * kWK);
+    for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int k = 0; k < kWK; k++) acc[u][k] = 0.f;
+    const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
+    const int64_t rb = (int64_t)blockIdx.y * per, re = min(rows, rb + per);
+    for (int64_t r0 = rb; r0 < re; r0 += RT) {
+        const int n = (int)min((int64_t)RT, re - r0);
+        __syncthreads();
+        for (int e = threadIdx.x; e < n * (kWK / 4); e += 64)
+            sd[e / (kWK / 4)][e % (kWK / 4)] = reinterpret_cast<const float4*>(dof + r0 * kWK)[e];
+        __syncthreads();
+        for (int rr = 0; rr < n; rr++) {
+            float h[4];
+            if (!bias_blk) {
+                const uint2 hv = *reinterpret_cast<const uint2*>(H + (r0 + rr) * kWH + j0);
+                const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv.x));
+                const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv.y));
+                h[0] = a.x; h[1] = a.y; h[2] = b.x; h[3] = b.y;
+            } else {
+                h[0] = threadIdx.x == 0 ? 1.f : 0.f; h[1] = h[2] = h[3] = 0.f;
+            }
 #pragma unroll
             for (int q = 0; q < kWK / 4; q++) {
-                const float4 d = d4[q];
-                acc[4 * q] = fmaf(d.x, h, acc[4 * q]);
-                acc[4 * q + 1] = fmaf(d.y, h, acc[4 * q + 1]);
-                acc[4 * q + 2] = fmaf(d.z, h, acc[4 * q + 2]);
-                acc[4 * q + 3] = fmaf(d.w, h, acc[4 * q + 3]);
+                const float4 d = sd[rr][q];
+#pragma unroll
+                for (int u = 0; u < 4; u++) {
+                    acc[u][4 * q] = fmaf(d.x, h[u], acc[u][4 * q]);
+                    acc[u][4 * q + 1] = fmaf(d.y, h[u], acc[u][4 * q + 1]);
+                    acc[u][4 * q + 2] = fmaf(d.z, h[u], acc[u][4 * q + 2]);
+                    acc[u][4 * q + 3] = fmaf(d.w, h[u], acc[u][4 * q + 3]);
+                }
             }
         }
+    }
+    if (!bias_blk) {
 #pragma unroll
-        for (int k = 0; k < kWK; k++) atomicAdd(dW2 + k * (kWH + 1) + j, (double)acc[k]);
+        for (int u = 0; u < 4; u++)
+#pragma unroll
+            for (int k = 0; k < kWK; k++) atomicAdd(dW2 + k * (kWH + 1) + j0 + u, (double)acc[u][k]);
+    } else if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < kWK; k++) atomicAdd(dW2 + k * (kWH + 1) + kWH, (double)acc[0][k]);
     }
 }
 
@@ -598,8 +646,8 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
         }
         prof(false);
         {  // 5. dW2
-            dim3 grid((kWH + 1 + 63) / 64, 148);
-            wide_dw2_kernel<<<grid, 256, 0, st>>>(w.dof, (const __nv_bfloat16*)w.Hb, Cc, w.dW2);
+            dim3 grid(kWH / 256 + 1, 296);
+            wide_dw2_kernel<<<grid, 64, 0, st>>>(w.dof, (const __nv_bfloat16*)w.Hb, Cc, w.dW2);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
