@@ -155,7 +155,7 @@ struct NetReq {
 int online_mt(size_t n_nets, bool ref64, int dp) {
     if (ref64) return 1;
     const char* e = getenv("GLX_ONLINE_MT");
-    int mt = e ? atoi(e) : (n_nets > 1 ? 4 : 1);
+    int mt = e ? atoi(e) : (n_nets > 1 ? 2 : 1);
     if (mt != 1 && mt != 2 && mt != 4) mt = 1;
     if (dp > 34) mt = 1;  // 64-wide rows: the MT tile would spill
     return mt;

@@ -34,6 +34,9 @@ constexpr int k3ZFull = 1, k3SFull = 4, k3ZEmpty = 7, k3AInt = 10, k3Epi = 11;
 #ifndef GLX3_RS
 #define GLX3_RS 4  // rows per step in the forward / backward streams (RPG must be a multiple)
 #endif
+#ifndef GLX3_FWD_BCAST
+#define GLX3_FWD_BCAST 0  // forward FFMA2 in broadcast-scalar form (x_i * weight pair of two units)
+#endif
 #ifndef GLX3_REGS_F
 #define GLX3_REGS_F 216
 #endif
@@ -107,12 +110,25 @@ __global__ void __launch_bounds__(k3NT, 1) batch3_kernel(const Batch3Args a) {
         const int f = rt;
         const int g = f / a.TPG, jq = f - (f / a.TPG) * a.TPG;
         const bool fv = g < a.G;
-        float2 w[MT][DP / 2];
+        // broadcast form (MT even): wp[up][i] = (w_{2up,i}, w_{2up+1,i}); else pair-of-inputs form
+        constexpr bool kBc = GLX3_FWD_BCAST && (MT % 2 == 0);
+        float2 wp[kBc ? MT / 2 : 1][kBc ? DP : 1];
+        float2 w[kBc ? 1 : MT][kBc ? 1 : DP / 2];
+        if constexpr (kBc) {
 #pragma unroll
-        for (int u = 0; u < MT; u++) {
-            const float2* src = reinterpret_cast<const float2*>(Wk + (int64_t)(fv ? jq * MT + u : 0) * DP);
+            for (int up = 0; up < MT / 2; up++) {
+                const float* r0 = Wk + (int64_t)(fv ? jq * MT + 2 * up : 0) * DP;
+                const float* r1 = Wk + (int64_t)(fv ? jq * MT + 2 * up + 1 : 0) * DP;
 #pragma unroll
-            for (int q = 0; q < DP / 2; q++) w[u][q] = fv ? src[q] : make_float2(0.f, 0.f);
+                for (int i = 0; i < DP; i++) wp[up][i] = fv ? make_float2(r0[i], r1[i]) : make_float2(0.f, 0.f);
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < MT; u++) {
+                const float2* src = reinterpret_cast<const float2*>(Wk + (int64_t)(fv ? jq * MT + u : 0) * DP);
+#pragma unroll
+                for (int q = 0; q < DP / 2; q++) w[u][q] = fv ? src[q] : make_float2(0.f, 0.f);
+            }
         }
 #ifdef GLX3_TIMING
         long long t_comp = 0, t_wait = 0;
@@ -145,6 +161,49 @@ __global__ void __launch_bounds__(k3NT, 1) batch3_kernel(const Batch3Args a) {
                     const float* xr[RS];
 #pragma unroll
                     for (int q = 0; q < RS; q++) xr[q] = xt + (g + (rr + q) * a.G) * a.LD;
+                    if constexpr (kBc) {
+                    float2 zp[RS][MT / 2];
+#pragma unroll
+                    for (int q = 0; q < RS; q++)
+#pragma unroll
+                        for (int up = 0; up < MT / 2; up++) zp[q][up] = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q4 = 0; q4 < DP / 4; q4++) {
+                        float4 v[RS];
+#pragma unroll
+                        for (int q = 0; q < RS; q++) v[q] = ld_f4(xr[q] + 4 * q4);
+#pragma unroll
+                        for (int e = 0; e < 4; e++)
+#pragma unroll
+                            for (int up = 0; up < MT / 2; up++)
+#pragma unroll
+                                for (int q = 0; q < RS; q++) {
+                                    const float xs = e == 0 ? v[q].x : e == 1 ? v[q].y : e == 2 ? v[q].z : v[q].w;
+                                    zp[q][up] = ffma2(bcast2(xs), wp[up][(4 * q4 + e) % DP], zp[q][up]);
+                                }
+                    }
+                    if (DP % 4) {
+#pragma unroll
+                        for (int q = 0; q < RS; q++) {
+                            const float2 v = ld_f2(xr[q] + DP - 2);
+#pragma unroll
+                            for (int up = 0; up < MT / 2; up++) {
+                                zp[q][up] = ffma2(bcast2(v.x), wp[up][(DP - 2) % DP], zp[q][up]);
+                                zp[q][up] = ffma2(bcast2(v.y), wp[up][(DP - 1) % DP], zp[q][up]);
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < RS; q++) {
+                        float z[MT];
+#pragma unroll
+                        for (int up = 0; up < MT / 2; up++) {
+                            z[2 * up] = zp[q][up].x;
+                            z[2 * up + 1] = zp[q][up].y;
+                        }
+                        store_units<MT>(zt + (g + (rr + q) * a.G) * a.HP + jq * MT, z);
+                    }
+                    } else {
                     float2 p[RS][MT];
 #pragma unroll
                     for (int q = 0; q < RS; q++)
@@ -158,7 +217,7 @@ __global__ void __launch_bounds__(k3NT, 1) batch3_kernel(const Batch3Args a) {
 #pragma unroll
                         for (int u = 0; u < MT; u++) {
 #pragma unroll
-                            for (int q = 0; q < RS; q++) p[q][u] = ffma2(w[u][2 * q4], make_float2(v[q].x, v[q].y), p[q][u]);
+                            for (int q = 0; q < RS; q++) p[q][u] = ffma2(w[u % (kBc ? 1 : MT)][(2 * q4) % (kBc ? 1 : DP / 2)], make_float2(v[q].x, v[q].y), p[q][u]);
 #pragma unroll
                             for (int q = 0; q < RS; q++)
                                 p[q][u] = ffma2(w[u][2 * q4 + 1], make_float2(v[q].z, v[q].w), p[q][u]);
@@ -179,9 +238,9 @@ __global__ void __launch_bounds__(k3NT, 1) batch3_kernel(const Batch3Args a) {
                         for (int u = 0; u < MT; u++) z[u] = p[q][u].x + p[q][u].y;
                         store_units<MT>(zt + (g + (rr + q) * a.G) * a.HP + jq * MT, z);
                     }
+                    }
                 }
             }
-            T_ADD(t_comp, tc);
             bar_arrive(k3ZFull + zb, 2 * k3WG);
         }
         for (int k = (nk >= k3NZ ? nk - k3NZ : 0); k < nk; k++) bar_sync(k3ZEmpty + (k % k3NZ), 2 * k3WG);

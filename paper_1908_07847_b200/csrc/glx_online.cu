@@ -202,8 +202,14 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
 // fp32 online SGD with an MT-unit register tile per thread (sweeps): the
 // per-row reduction, barrier and output-neuron work are paid once per MT
 // hidden units instead of once per unit.
+#ifndef GLX_ONLINE_XSMEM
+#define GLX_ONLINE_XSMEM 1  // x pairs from shared memory (frees 34 registers for occupancy)
+#endif
+#ifndef GLX_ONLINE_MT2_CTAS
+#define GLX_ONLINE_MT2_CTAS 2  // resident 256-thread CTAs per SM for the 2-unit tile (<= 128 registers)
+#endif
 template <int DP, int MT, bool XS>
-__global__ void __launch_bounds__(256) online_sgd_mt_kernel(const OnlineNetDesc* __restrict__ nets,
+__global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online_sgd_mt_kernel(const OnlineNetDesc* __restrict__ nets,
                                                              const int2* __restrict__ cta_nets,
                                                              const float* __restrict__ X, const float* __restrict__ T,
                                                              int64_t N, int D, int64_t epochs, double lr) {
@@ -254,9 +260,14 @@ __global__ void __launch_bounds__(256) online_sgd_mt_kernel(const OnlineNetDesc*
     const float flr = (float)lr;
     int buf = 0;
     float x[DP];
+    // GLX_ONLINE_XSMEM: with the rows staged in shared memory, read x pairs from
+    // there in both loops instead of holding the row in 34 registers
+    constexpr bool kXs = XS && GLX_ONLINE_XSMEM;
     for (int64_t ep = 0; ep < epochs; ep++) {
         for (int64_t r = 0; r < N; r++) {
-            load_row<float, DP, XS>(x, xs, X, r, D);
+            const float2* xr2 = reinterpret_cast<const float2*>(xs + (XS ? r * DP : 0));
+            if constexpr (!kXs) load_row<float, DP, XS>(x, xs, X, r, D);
+            auto xp = [&](int q) { return kXs ? xr2[q] : make_float2(x[2 * q], x[2 * q + 1]); };
             const float tt = XS ? ts[r] : __ldg(T + r);
             float h[MT];
             float prod = (t == 0) ? b2 : 0.f;
@@ -264,7 +275,7 @@ __global__ void __launch_bounds__(256) online_sgd_mt_kernel(const OnlineNetDesc*
             for (int u = 0; u < MT; u++) {
                 float2 p = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int q = 0; q < DP / 2; q++) p = ffma2(w[u][q], make_float2(x[2 * q], x[2 * q + 1]), p);
+                for (int q = 0; q < DP / 2; q++) p = ffma2(w[u][q], xp(q), p);
                 h[u] = act[u] ? sigmoid_scaled(kScale * (p.x + p.y)) : 0.f;
                 prod = fmaf(w2[u], h[u], prod);
             }
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(256) online_sgd_mt_kernel(const OnlineNetDesc*
             for (int u = 0; u < MT; u++) {
                 const float ns = -flr * (w2[u] * d_o * h[u] * (1.0f - h[u]));
 #pragma unroll
-                for (int q = 0; q < DP / 2; q++) w[u][q] = ffma2(bcast2(ns), make_float2(x[2 * q], x[2 * q + 1]), w[u][q]);
+                for (int q = 0; q < DP / 2; q++) w[u][q] = ffma2(bcast2(ns), xp(q), w[u][q]);
                 w2[u] = fmaf(-step_o, h[u], w2[u]);
             }
             if (t == 0) b2 -= step_o;

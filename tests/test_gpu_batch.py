@@ -98,3 +98,31 @@ def test_unsupported_shape_raises(gpu):
     x = np.zeros((10, 40), np.float32)
     with pytest.raises(g.ValidationError):
         g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, np.zeros(10, np.float32), 1, 0.1, g.cuda())
+
+
+def test_dp_path_over_nccl_one_rank(gpu):
+    """The torch.distributed NCCL all-reduce path of dp.py (world size 1) matches the fused loop."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_07847_b200 import dp
+
+    x, l, t, net0 = _case(50_000, 33, 256, seed=2)
+    fused = net0.copy()
+    g.run_train_segment_batch(fused.w_ih2d, fused.w_ho2d, x, t, 5, 0.5, g.cuda())
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        eng = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
+        stats = dp.train_data_parallel(eng, 5, 0.5, x.shape[0], dp.nccl_all_reduce())
+        w1, w2 = eng.weights()
+    finally:
+        dist.destroy_process_group()
+    assert rel_err(w1, fused.w_ih) <= 1e-6 and rel_err(w2, fused.w_ho) <= 1e-6
+    assert all(sum(st.counts) == x.shape[0] for st in stats)
