@@ -30,10 +30,10 @@ constexpr int kTcBK = 64;  // bf16 elements per 128-byte swizzled row
 #define GLX_TC_MAXBN 256  // widest N tile (TMEM columns) per CTA
 #endif
 #ifndef GLX_TC_STAGES
-#define GLX_TC_STAGES 2  // 2 stages -> 2 CTAs per SM: one tile's epilogue overlaps the other's MMAs
+#define GLX_TC_STAGES 4  // persistent kernel, 1 CTA per SM: the TMEM double buffer overlaps epilogue and MMA
 #endif
 constexpr int kTcStages = GLX_TC_STAGES;
-constexpr int kTcThreads = 192;
+constexpr int kTcThreads = 320;  // TMA warp + MMA warp + 8 epilogue warps
 
 // ------------------------------------------------------------- descriptors
 // UMMA shared-memory descriptor, K-major, 128-byte swizzle (canonical layout:
@@ -115,32 +115,139 @@ struct TcGemm {
 };
 
 template <int BN>
+__device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const float (&v)[32], int M, int row, int n0,
+                                                  int c, int lane) {
+    const bool rv = row < M;
+    if (ep.kind == 0 || ep.kind == 4) {
+        if (rv) {
+            float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (int64_t)row * ep.ldd +
+                                                    n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                if (ep.kind == 4) {
+                    const float4 p = dst[q];
+                    o.x += p.x;
+                    o.y += p.y;
+                    o.z += p.z;
+                    o.w += p.w;
+                }
+                dst[q] = o;
+            }
+        }
+    } else if (ep.kind == 1) {
+        if (rv) {
+            // 16-byte stores: 8 bf16 per store, 4 per 32-column chunk
+            uint4* dst = reinterpret_cast<uint4*>(ep.d_bf16 + (int64_t)row * ep.ldd + n0 + c);
+            const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                const float4 ba = __ldg(b4 + 2 * q), bb = __ldg(b4 + 2 * q + 1);
+                const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
+                uint32_t pk[4];
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const float z0 = v[8 * q + 2 * e] + bv[2 * e];
+                    const float z1 = v[8 * q + 2 * e + 1] + bv[2 * e + 1];
+                    const __nv_bfloat162 h2 =
+                        __floats2bfloat162_rn(__frcp_rn(1.0f + __expf(-z0)), __frcp_rn(1.0f + __expf(-z1)));
+                    pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
+                }
+                dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            }
+        }
+    } else if (ep.kind == 2) {
+        // output neuron (kernels.py:352-375 generalised to K outputs)
+        float loss = 0.f, correct = 0.f, wrong = 0.f;
+        if (rv) {
+            const int lab = ep.labels[row];
+            float best = -1.f;
+            int arg = 0;
+#pragma unroll
+            for (int k = 0; k < 32; k++) {
+                if (k >= ep.K) break;
+                const float o = 1.0f / (1.0f + __expf(-(v[k] + ep.bias[k])));
+                const float t = (k == lab) ? 1.f : 0.f;
+                const float d = (o - t) * o * (1.0f - o);
+                loss = fmaf(0.5f * (t - o), t - o, loss);
+                if (o > best) {
+                    best = o;
+                    arg = k;
+                }
+                ep.do_b[(int64_t)row * 64 + k] = __float2bfloat16_rn(d);
+                ep.do_f[(int64_t)row * ep.K + k] = d;
+            }
+            correct = arg == lab ? 1.f : 0.f;
+            wrong = 1.f - correct;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            loss += __shfl_xor_sync(0xffffffffu, loss, o);
+            correct += __shfl_xor_sync(0xffffffffu, correct, o);
+            wrong += __shfl_xor_sync(0xffffffffu, wrong, o);
+        }
+        if (lane == 0 && ep.stats) {
+            atomicAdd(ep.stats + 0, (double)loss);
+            atomicAdd(ep.stats + 1, (double)correct);
+            atomicAdd(ep.stats + 2, (double)wrong);
+        }
+    } else {
+        // delta_h = (delta_o W2)_j * h (1 - h), stored transposed for the dW1 GEMM
+        if (rv) {
+            const uint4* hp = reinterpret_cast<const uint4*>(ep.h + (int64_t)row * ep.ldh + n0 + c);
+#pragma unroll
+            for (int q4 = 0; q4 < 4; q4++) {
+                const uint4 hv = hp[q4];
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv);
+#pragma unroll
+                for (int e = 0; e < 4; e++) {
+                    const float2 hf = __bfloat1622float2(h2[e]);
+                    const int col = n0 + c + q4 * 8 + 2 * e;
+                    ep.dht[(int64_t)col * ep.ldt + row] = __float2bfloat16_rn(v[q4 * 8 + 2 * e] * hf.x * (1.f - hf.x));
+                    ep.dht[(int64_t)(col + 1) * ep.ldt + row] =
+                        __float2bfloat16_rn(v[q4 * 8 + 2 * e + 1] * hf.y * (1.f - hf.y));
+                }
+            }
+        }
+    }
+}
+
+// Persistent tcgen05 GEMM: warp 0 = TMA producer, warp 1 = TMEM owner + MMA
+// issuer, warps 2..9 = epilogue. The accumulator is double-buffered in TMEM
+// (2 x BN columns), so the epilogue of tile i overlaps the MMAs of tile i+1.
+// Tiles are walked (split z, M, N) with N fastest, so concurrently running
+// CTAs share their A tile through L2.
+template <int BN>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                                                                   const __grid_constant__ CUtensorMap map_b, int M,
-                                                                  int N, int K, int kb_per_split, TcEpilogue ep) {
+                                                                  int N, int K, int kb_per_split, int n_mt, int n_nt,
+                                                                  int n_zt, TcEpilogue ep) {
     constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
     constexpr uint32_t kBBytes = BN * kTcBK * 2;
     constexpr uint32_t kStage = kABytes + kBBytes;
-    constexpr uint32_t kCols = BN < 32 ? 32 : BN;  // TMEM allocation: power of two >= 32
+    constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
+    constexpr int kEpiCols = BN >= 64 ? BN / 2 : BN;        // columns per epilogue warp
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    // 1024-byte alignment for the 128-byte swizzle atoms
     unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + kTcStages * kStage);
     uint64_t* empty = full + kTcStages;
-    uint64_t* done = empty + kTcStages;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* tfull = empty + kTcStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int m0 = blockIdx.y * kTcBM, n0 = blockIdx.x * BN;
-    const int kb0 = blockIdx.z * kb_per_split;
-    const int nk = min(K / kTcBK - kb0, kb_per_split);  // this CTA's K blocks (split-K over blockIdx.z)
+    const int nkt = K / kTcBK;
+    const int tiles = n_mt * n_nt * n_zt;
 
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < kTcStages; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(done, 1);
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 8);  // one arrival per epilogue warp
+        }
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b) : "memory");
@@ -156,139 +263,84 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
+    auto decode = [&](int t, int& z, int& m0, int& n0, int& kb0, int& nk) {
+        z = t / (n_mt * n_nt);
+        const int rem = t - z * (n_mt * n_nt);
+        m0 = (rem / n_nt) * kTcBM;
+        n0 = (rem % n_nt) * BN;
+        kb0 = z * kb_per_split;
+        nk = min(nkt - kb0, kb_per_split);
+    };
+
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % kTcStages;
-                if (kb >= kTcStages) mbar_wait(&empty[s], ((kb / kTcStages) - 1) & 1);
-                unsigned char* st = sm + s * kStage;
-                mbar_arrive_expect_tx(&full[s], kStage);
-                tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
-                tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
+            int it = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                int z, m0, n0, kb0, nk;
+                decode(t, z, m0, n0, kb0, nk);
+                for (int kb = 0; kb < nk; kb++, it++) {
+                    const int s = it % kTcStages;
+                    if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
+                    unsigned char* st = sm + s * kStage;
+                    mbar_arrive_expect_tx(&full[s], kStage);
+                    tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
+                    tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
             constexpr uint32_t idesc = umma_idesc_bf16(kTcBM, BN);
-            for (int kb = 0; kb < nk; kb++) {
-                const int s = kb % kTcStages;
-                mbar_wait(&full[s], (kb / kTcStages) & 1);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
+                int z, m0, n0, kb0, nk;
+                decode(t, z, m0, n0, kb0, nk);
+                const int acc = lt & 1;
+                if (lt >= 2) mbar_wait(&tempty[acc], ((lt / 2) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t a_addr = smem_u32(sm + s * kStage);
-                const uint32_t b_addr = a_addr + kABytes;
+                const uint32_t dcol = tmem + acc * BN;
+                for (int kb = 0; kb < nk; kb++, it++) {
+                    const int s = it % kTcStages;
+                    mbar_wait(&full[s], (it / kTcStages) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t a_addr = smem_u32(sm + s * kStage);
+                    const uint32_t b_addr = a_addr + kABytes;
 #pragma unroll
-                for (int kk = 0; kk < kTcBK / 16; kk++) {  // 32-byte K steps inside the 128-byte row
-                    umma_bf16(tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
-                              (kb | kk) != 0);
+                    for (int kk = 0; kk < kTcBK / 16; kk++)
+                        umma_bf16(dcol, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                                  (kb | kk) != 0);
+                    umma_commit(&empty[s]);
                 }
-                umma_commit(&empty[s]);  // slot free once these MMAs have read it
+                umma_commit(&tfull[acc]);
             }
-            umma_commit(done);  // accumulator complete
         }
     } else {
-        // epilogue: warp w owns TMEM lanes [32*(w%4), 32*(w%4)+32)
+        // epilogue warps 2..9: TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4
+        const int ew = warp - 2;
         const int quad = warp & 3;
-        mbar_wait(done, 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const int row = m0 + quad * 32 + lane;
-        const bool rv = row < M;
+        const int c0 = (BN >= 64) ? (ew >> 2) * kEpiCols : 0;
+        const bool work = (BN >= 64) || ew < 4;
+        int lt = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
+            int z, m0, n0, kb0, nk;
+            decode(t, z, m0, n0, kb0, nk);
+            const int acc = lt & 1;
+            mbar_wait(&tfull[acc], (lt / 2) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            if (work) {
+                TcEpilogue e2 = ep;
+                if (ep.kind == 4) e2.d_f32 = ep.d_f32 + z * ep.zstride;
+                const int row = m0 + quad * 32 + lane;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 32) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + c, v);
-            if (ep.kind == 0 || ep.kind == 4) {
-                if (rv) {
-                    float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (ep.kind == 4 ? blockIdx.z * ep.zstride : 0) +
-                                                            (int64_t)row * ep.ldd + n0 + c);
-#pragma unroll
-                    for (int q = 0; q < 8; q++) {
-                        float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                        if (ep.kind == 4) {
-                            const float4 p = dst[q];
-                            o.x += p.x;
-                            o.y += p.y;
-                            o.z += p.z;
-                            o.w += p.w;
-                        }
-                        dst[q] = o;
-                    }
-                }
-            } else if (ep.kind == 1) {
-                if (rv) {
-                    // 16-byte stores: 8 bf16 per store, 4 per 32-column chunk
-                    uint4* dst = reinterpret_cast<uint4*>(ep.d_bf16 + (int64_t)row * ep.ldd + n0 + c);
-                    const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c);
-#pragma unroll
-                    for (int q = 0; q < 4; q++) {
-                        uint32_t pk[4];
-#pragma unroll
-                        for (int e = 0; e < 4; e++) {
-                            const float4 bb = b4[(8 * q + 2 * e) / 4];
-                            const float b0 = ((2 * e) & 3) == 0 ? bb.x : bb.z;
-                            const float b1 = ((2 * e) & 3) == 0 ? bb.y : bb.w;
-                            const float z0 = v[8 * q + 2 * e] + b0;
-                            const float z1 = v[8 * q + 2 * e + 1] + b1;
-                            const __nv_bfloat162 h2 = __floats2bfloat162_rn(__frcp_rn(1.0f + __expf(-z0)),
-                                                                            __frcp_rn(1.0f + __expf(-z1)));
-                            pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
-                        }
-                        dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                    }
-                }
-            } else if (ep.kind == 2) {
-                // output neuron (kernels.py:352-375 generalised to K outputs)
-                float loss = 0.f, correct = 0.f, wrong = 0.f;
-                if (rv) {
-                    const int lab = ep.labels[row];
-                    float best = -1.f;
-                    int arg = 0;
-#pragma unroll
-                    for (int k = 0; k < 32; k++) {
-                        if (k >= ep.K) break;
-                        const float o = 1.0f / (1.0f + __expf(-(v[k] + ep.bias[k])));
-                        const float t = (k == lab) ? 1.f : 0.f;
-                        const float d = (o - t) * o * (1.0f - o);
-                        loss = fmaf(0.5f * (t - o), t - o, loss);
-                        if (o > best) {
-                            best = o;
-                            arg = k;
-                        }
-                        ep.do_b[(int64_t)row * 64 + k] = __float2bfloat16_rn(d);
-                        ep.do_f[(int64_t)row * ep.K + k] = d;
-                    }
-                    correct = arg == lab ? 1.f : 0.f;
-                    wrong = 1.f - correct;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    loss += __shfl_xor_sync(0xffffffffu, loss, o);
-                    correct += __shfl_xor_sync(0xffffffffu, correct, o);
-                    wrong += __shfl_xor_sync(0xffffffffu, wrong, o);
-                }
-                if (lane == 0 && ep.stats) {
-                    atomicAdd(ep.stats + 0, (double)loss);
-                    atomicAdd(ep.stats + 1, (double)correct);
-                    atomicAdd(ep.stats + 2, (double)wrong);
-                }
-            } else {
-                // delta_h = (delta_o W2)_j * h (1 - h), stored transposed for the dW1 GEMM
-                if (rv) {
-                    const uint4* hp = reinterpret_cast<const uint4*>(ep.h + (int64_t)row * ep.ldh + n0 + c);
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; q4++) {
-                        const uint4 hv = hp[q4];
-                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv);
-#pragma unroll
-                        for (int e = 0; e < 4; e++) {
-                            const float2 hf = __bfloat1622float2(h2[e]);
-                            const int col = n0 + c + q4 * 8 + 2 * e;
-                            ep.dht[(int64_t)col * ep.ldt + row] = __float2bfloat16_rn(v[q4 * 8 + 2 * e] * hf.x * (1.f - hf.x));
-                            ep.dht[(int64_t)(col + 1) * ep.ldt + row] =
-                                __float2bfloat16_rn(v[q4 * 8 + 2 * e + 1] * hf.y * (1.f - hf.y));
-                        }
-                    }
+                for (int c = c0; c < c0 + kEpiCols; c += 32) {
+                    float v[32];
+                    tmem_ld32(tmem + acc * BN + ((uint32_t)(quad * 32) << 16) + c, v);
+                    tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane);
                 }
             }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -342,8 +394,13 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
     const int nk = g.K / kTcBK;
     const int splits = g.splits < 1 ? 1 : g.splits;
     const int kps = (nk + splits - 1) / splits;
-    dim3 grid(g.N / BN, (g.M + kTcBM - 1) / kTcBM, (nk + kps - 1) / kps);
-    k<<<grid, kTcThreads, smem, st>>>(ma, mb, g.M, g.N, g.K, kps, ep);
+    const int n_nt = g.N / BN, n_mt = (g.M + kTcBM - 1) / kTcBM, n_zt = (nk + kps - 1) / kps;
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = n_nt * n_mt * n_zt;
+    const int grid = tiles < sms ? tiles : sms;
+    k<<<grid, kTcThreads, smem, st>>>(ma, mb, g.M, g.N, g.K, kps, n_mt, n_nt, n_zt, ep);
     return cudaGetLastError();
 }
 
@@ -455,58 +512,70 @@ __global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __
 }
 
 // dW2[k][j] += sum_r delta_o[r][k] h[r][j]; column kWH is the bias (h = 1).
-// Block = 64 threads x 4 hidden columns each (256 columns) + one row slice;
-// delta_o rows are staged in shared memory and read as broadcasts.
-__global__ void __launch_bounds__(64) wide_dw2_kernel(const float* __restrict__ dof, const __nv_bfloat16* __restrict__ H,
-                                                      int64_t rows, double* __restrict__ dW2) {
-    constexpr int RT = 64;  // rows per smem stage
-    __shared__ float4 sd[RT][kWK / 4];
-    const int j0 = blockIdx.x * 256 + threadIdx.x * 4;  // 4 columns; block 4 also covers the bias column
+// Block = 64 column groups (4 hidden columns each) x 4 row phases; delta_o rows
+// are staged in shared memory and consumed as float2 broadcasts by FFMA2 with
+// the h value as the broadcast scalar; the 4 phases are combined in shared
+// memory before one f64 atomic per (k, j) per block.
+constexpr int kDw2Rows = 64;
+__global__ void __launch_bounds__(256) wide_dw2_kernel(const float* __restrict__ dof, const __nv_bfloat16* __restrict__ H,
+                                                       int64_t rows, double* __restrict__ dW2) {
+    extern __shared__ __align__(16) float dsm[];
+    float* sd = dsm;                    // [kDw2Rows][kWK]
+    float* red = dsm + kDw2Rows * kWK;  // [4][256][kWK] phase partials
+    const int tid = threadIdx.x, cg = tid & 63, ph = tid >> 6;
     const bool bias_blk = blockIdx.x == kWH / 256;
-    float acc[4][kWK];
+    const int j0 = blockIdx.x * 256 + cg * 4;
+    float2 acc[4][kWK / 2];
 #pragma unroll
     for (int u = 0; u < 4; u++)
 #pragma unroll
-        for (int k = 0; k < kWK; k++) acc[u][k] = 0.f;
+        for (int q = 0; q < kWK / 2; q++) acc[u][q] = make_float2(0.f, 0.f);
     const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
     const int64_t rb = (int64_t)blockIdx.y * per, re = min(rows, rb + per);
-    for (int64_t r0 = rb; r0 < re; r0 += RT) {
-        const int n = (int)min((int64_t)RT, re - r0);
+    for (int64_t r0 = rb; r0 < re; r0 += kDw2Rows) {
+        const int n = (int)min((int64_t)kDw2Rows, re - r0);
         __syncthreads();
-        for (int e = threadIdx.x; e < n * (kWK / 4); e += 64)
-            sd[e / (kWK / 4)][e % (kWK / 4)] = reinterpret_cast<const float4*>(dof + r0 * kWK)[e];
+        if (tid < n * (kWK / 4))
+            reinterpret_cast<float4*>(sd)[tid] = reinterpret_cast<const float4*>(dof + r0 * kWK)[tid];
         __syncthreads();
-        for (int rr = 0; rr < n; rr++) {
+        for (int rr = ph; rr < n; rr += 4) {
             float h[4];
             if (!bias_blk) {
                 const uint2 hv = *reinterpret_cast<const uint2*>(H + (r0 + rr) * kWH + j0);
                 const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv.x));
                 const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv.y));
-                h[0] = a.x; h[1] = a.y; h[2] = b.x; h[3] = b.y;
+                h[0] = a.x;
+                h[1] = a.y;
+                h[2] = b.x;
+                h[3] = b.y;
             } else {
-                h[0] = threadIdx.x == 0 ? 1.f : 0.f; h[1] = h[2] = h[3] = 0.f;
+                h[0] = cg == 0 ? 1.f : 0.f;
+                h[1] = h[2] = h[3] = 0.f;
             }
+            const float2* d2 = reinterpret_cast<const float2*>(sd + rr * kWK);
 #pragma unroll
-            for (int q = 0; q < kWK / 4; q++) {
-                const float4 d = sd[rr][q];
+            for (int q = 0; q < kWK / 2; q++) {
+                const float2 d = d2[q];
 #pragma unroll
-                for (int u = 0; u < 4; u++) {
-                    acc[u][4 * q] = fmaf(d.x, h[u], acc[u][4 * q]);
-                    acc[u][4 * q + 1] = fmaf(d.y, h[u], acc[u][4 * q + 1]);
-                    acc[u][4 * q + 2] = fmaf(d.z, h[u], acc[u][4 * q + 2]);
-                    acc[u][4 * q + 3] = fmaf(d.w, h[u], acc[u][4 * q + 3]);
-                }
+                for (int u = 0; u < 4; u++) acc[u][q] = ffma2(bcast2(h[u]), d, acc[u][q]);
             }
         }
     }
-    if (!bias_blk) {
+    __syncthreads();
 #pragma unroll
-        for (int u = 0; u < 4; u++)
+    for (int u = 0; u < 4; u++)
 #pragma unroll
-            for (int k = 0; k < kWK; k++) atomicAdd(dW2 + k * (kWH + 1) + j0 + u, (double)acc[u][k]);
-    } else if (threadIdx.x == 0) {
-#pragma unroll
-        for (int k = 0; k < kWK; k++) atomicAdd(dW2 + k * (kWH + 1) + kWH, (double)acc[0][k]);
+        for (int q = 0; q < kWK / 2; q++) {
+            red[(ph * 256 + cg * 4 + u) * kWK + 2 * q] = acc[u][q].x;
+            red[(ph * 256 + cg * 4 + u) * kWK + 2 * q + 1] = acc[u][q].y;
+        }
+    __syncthreads();
+    for (int e = tid; e < 256 * kWK; e += 256) {
+        const int col = e / kWK, k = e % kWK;
+        const float v = red[e] + red[256 * kWK + e] + red[2 * 256 * kWK + e] + red[3 * 256 * kWK + e];
+        const int j = blockIdx.x * 256 + col;
+        if (!bias_blk) atomicAdd(dW2 + k * (kWH + 1) + j, (double)v);
+        else if (col == 0) atomicAdd(dW2 + k * (kWH + 1) + kWH, (double)v);
     }
 }
 
@@ -646,8 +715,14 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
         }
         prof(false);
         {  // 5. dW2
-            dim3 grid(kWH / 256 + 1, 296);
-            wide_dw2_kernel<<<grid, 64, 0, st>>>(w.dof, (const __nv_bfloat16*)w.Hb, Cc, w.dW2);
+            const size_t dsm = (size_t)(kDw2Rows * kWK + 4 * 256 * kWK) * sizeof(float);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(wide_dw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
+                attr = true;
+            }
+            dim3 grid(kWH / 256 + 1, 96);
+            wide_dw2_kernel<<<grid, 256, dsm, st>>>(w.dof, (const __nv_bfloat16*)w.Hb, Cc, w.dW2);
             if ((e = cudaGetLastError()) != cudaSuccess) return e;
         }
     }
