@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 #include <functional>
 
 namespace glx {
@@ -32,7 +33,20 @@ constexpr int kTcBK = 64;  // bf16 elements per 128-byte swizzled row
 #ifndef GLX_TC_STAGES
 #define GLX_TC_STAGES 4  // persistent kernel, 1 CTA per SM: the TMEM double buffer overlaps epilogue and MMA
 #endif
-constexpr int kTcStages = GLX_TC_STAGES;
+// ring depth per tile width: 4 x 48 KB stages at BN = 256, up to 8 for narrow tiles
+__host__ __device__ constexpr int tc_stages(int BN) {
+    return (GLX_TC_STAGES * (kTcBM + 256) * kTcBK * 2) / ((kTcBM + BN) * kTcBK * 2) > 8
+               ? 8
+               : (GLX_TC_STAGES * (kTcBM + 256) * kTcBK * 2) / ((kTcBM + BN) * kTcBK * 2);
+}
+// per-epilogue-warp staging for TMA stores of bf16 results: two 32 x 32 bf16
+// blocks (2 KB each) per warp, used alternately
+constexpr int kTcStgBlk = 32 * 32;  // bf16 elements per staged block
+constexpr int kTcStgBytes = 8 * 2 * kTcStgBlk * 2;
+#ifndef GLX_TC_PREFETCH
+#define GLX_TC_PREFETCH 0  // k-blocks of L2 prefetch ahead of the loads (8 measured 2x slower on the split-K GEMM)
+#endif
+constexpr int kTcPrefetch = GLX_TC_PREFETCH;
 constexpr int kTcThreads = 320;  // TMA warp + MMA warp + 8 epilogue warps
 
 // ------------------------------------------------------------- descriptors
@@ -55,6 +69,12 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
             smem_u32(dst)),
         "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
+}
+
+// L2-only prefetch of the same box (no shared memory, no barrier)
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
+                 : "memory");
 }
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -90,6 +110,7 @@ struct TcEpilogue {
     int kind;               // 0: f32 store; 1: bias+sigmoid -> bf16; 2: output layer; 3: delta_h^T; 4: f32 accumulate
     float* d_f32;           // 0, 4 (4: + blockIdx.z * zstride)
     __nv_bfloat16* d_bf16;  // 1
+    __nv_bfloat16* d_t;     // 1 (optional): transposed copy of the bf16 result, row stride ldt
     const float* bias;      // 1, 2
     int ldd;
     int64_t zstride;
@@ -97,13 +118,46 @@ struct TcEpilogue {
     const uint8_t* labels;
     int K;
     __nv_bfloat16* do_b;  // [M][64] bf16, columns >= K stay zero
-    float* do_f;          // [M][K] f32
+    __nv_bfloat16* do_t;  // [K][ldt] bf16: delta_o transposed (the dW2 GEMM operand)
     double* stats;        // [loss, correct, wrong]
     // 3: delta_h = v * h (1 - h), written transposed
     const __nv_bfloat16* h;
     int ldh;
     __nv_bfloat16* dht;
-    int64_t ldt;
+    int64_t ldt;  // row stride of the transposed outputs (d_t, do_t, dht)
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Per-warp TMA store staging: two 2 KB blocks used alternately; a block is
+// rewritten only after the bulk store issued from it two stores ago has read it.
+struct EpiStage {
+    uint16_t* buf;  // this warp's 2 x kTcStgBlk bf16
+    int next;
+    const CUtensorMap* map_d;  // row-major bf16 result (kind 1), box 32 x 32
+    const CUtensorMap* map_t;  // transposed bf16 result (kinds 1, 3), box 32 x 32
+    __device__ __forceinline__ uint16_t* acquire(int lane) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+        uint16_t* b = buf + next * kTcStgBlk;
+        next ^= 1;
+        return b;
+    }
+    // make the generic-proxy writes of this warp visible to the bulk copy, then issue it
+    __device__ __forceinline__ void release(const CUtensorMap* map, const uint16_t* b, int c0, int c1, int lane) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tma_store_2d(map, b, c0, c1);
+    }
+    __device__ __forceinline__ void drain(int lane) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        __syncwarp();
+    }
 };
 
 struct TcGemm {
@@ -114,9 +168,27 @@ struct TcGemm {
     int splits;  // split-K: blockIdx.z takes K / splits
 };
 
+// lane = row, pk[e] = columns 2e, 2e+1 of that row
+__device__ __forceinline__ void store_rows_bf16(EpiStage& sg, const uint32_t (&pk)[16], int row0, int col0, int lane) {
+    uint16_t* b = sg.acquire(lane);
+    uint4* d = reinterpret_cast<uint4*>(b + lane * 32);
+#pragma unroll
+    for (int q = 0; q < 4; q++) d[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    sg.release(sg.map_d, b, col0, row0, lane);
+}
+__device__ __forceinline__ void store_cols_bf16(EpiStage& sg, const uint32_t (&pk)[16], int row0, int col0, int lane) {
+    uint16_t* b = sg.acquire(lane);
+#pragma unroll
+    for (int e = 0; e < 16; e++) {
+        b[(2 * e) * 32 + lane] = (uint16_t)(pk[e] & 0xFFFFu);
+        b[(2 * e + 1) * 32 + lane] = (uint16_t)(pk[e] >> 16);
+    }
+    sg.release(sg.map_t, b, row0, col0, lane);
+}
+
 template <int BN>
 __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const float (&v)[32], int M, int row, int n0,
-                                                  int c, int lane) {
+                                                  int c, int lane, EpiStage& sg) {
     const bool rv = row < M;
     if (ep.kind == 0 || ep.kind == 4) {
         if (rv) {
@@ -136,26 +208,30 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
             }
         }
     } else if (ep.kind == 1) {
-        if (rv) {
-            // 16-byte stores: 8 bf16 per store, 4 per 32-column chunk
-            uint4* dst = reinterpret_cast<uint4*>(ep.d_bf16 + (int64_t)row * ep.ldd + n0 + c);
+        // 16-byte stores: 8 bf16 per store, 4 per 32-column chunk
+        uint32_t pall[16];
+        {
             const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c);
 #pragma unroll
             for (int q = 0; q < 4; q++) {
                 const float4 ba = __ldg(b4 + 2 * q), bb = __ldg(b4 + 2 * q + 1);
                 const float bv[8] = {ba.x, ba.y, ba.z, ba.w, bb.x, bb.y, bb.z, bb.w};
-                uint32_t pk[4];
+                uint32_t* pk = pall + 4 * q;
+                // sigmoid(z) = 1 / (1 + 2^(-log2e z)): MUFU ex2 + rcp, ample for a bf16 result
+                const float2 nl2e = bcast2(-1.4426950408889634f);
 #pragma unroll
                 for (int e = 0; e < 4; e++) {
-                    const float z0 = v[8 * q + 2 * e] + bv[2 * e];
-                    const float z1 = v[8 * q + 2 * e + 1] + bv[2 * e + 1];
-                    const __nv_bfloat162 h2 =
-                        __floats2bfloat162_rn(__frcp_rn(1.0f + __expf(-z0)), __frcp_rn(1.0f + __expf(-z1)));
+                    const float2 zs = __fmul2_rn(__fadd2_rn(make_float2(v[8 * q + 2 * e], v[8 * q + 2 * e + 1]),
+                                                            make_float2(bv[2 * e], bv[2 * e + 1])),
+                                                 nl2e);
+                    const __nv_bfloat162 h2 = __floats2bfloat162_rn(sigmoid_scaled(zs.x), sigmoid_scaled(zs.y));
                     pk[e] = *reinterpret_cast<const uint32_t*>(&h2);
                 }
-                dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             }
         }
+        // TMA stores clip rows >= M of a tail tile
+        store_rows_bf16(sg, pall, row - lane, n0 + c, lane);
+        if (ep.d_t) store_cols_bf16(sg, pall, row - lane, n0 + c, lane);
     } else if (ep.kind == 2) {
         // output neuron (kernels.py:352-375 generalised to K outputs)
         float loss = 0.f, correct = 0.f, wrong = 0.f;
@@ -174,8 +250,9 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
                     best = o;
                     arg = k;
                 }
-                ep.do_b[(int64_t)row * 64 + k] = __float2bfloat16_rn(d);
-                ep.do_f[(int64_t)row * ep.K + k] = d;
+                const __nv_bfloat16 db = __float2bfloat16_rn(d);
+                ep.do_b[(int64_t)row * 64 + k] = db;
+                ep.do_t[(int64_t)k * ep.ldt + row] = db;
             }
             correct = arg == lab ? 1.f : 0.f;
             wrong = 1.f - correct;
@@ -193,22 +270,25 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
         }
     } else {
         // delta_h = (delta_o W2)_j * h (1 - h), stored transposed for the dW1 GEMM
+        uint32_t pall[16];
+        uint4 hv[4] = {};
         if (rv) {
             const uint4* hp = reinterpret_cast<const uint4*>(ep.h + (int64_t)row * ep.ldh + n0 + c);
 #pragma unroll
-            for (int q4 = 0; q4 < 4; q4++) {
-                const uint4 hv = hp[q4];
-                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv);
+            for (int q4 = 0; q4 < 4; q4++) hv[q4] = hp[q4];
+        }
 #pragma unroll
-                for (int e = 0; e < 4; e++) {
-                    const float2 hf = __bfloat1622float2(h2[e]);
-                    const int col = n0 + c + q4 * 8 + 2 * e;
-                    ep.dht[(int64_t)col * ep.ldt + row] = __float2bfloat16_rn(v[q4 * 8 + 2 * e] * hf.x * (1.f - hf.x));
-                    ep.dht[(int64_t)(col + 1) * ep.ldt + row] =
-                        __float2bfloat16_rn(v[q4 * 8 + 2 * e + 1] * hf.y * (1.f - hf.y));
-                }
+        for (int q4 = 0; q4 < 4; q4++) {
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&hv[q4]);
+#pragma unroll
+            for (int e = 0; e < 4; e++) {
+                const float2 hf = __bfloat1622float2(h2[e]);
+                const __nv_bfloat162 d2 = __floats2bfloat162_rn(v[q4 * 8 + 2 * e] * hf.x * (1.f - hf.x),
+                                                                v[q4 * 8 + 2 * e + 1] * hf.y * (1.f - hf.y));
+                pall[q4 * 4 + e] = *reinterpret_cast<const uint32_t*>(&d2);
             }
         }
+        store_cols_bf16(sg, pall, row - lane, n0 + c, lane);
     }
 }
 
@@ -219,12 +299,15 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
 // CTAs share their A tile through L2.
 template <int BN>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                                                                  const __grid_constant__ CUtensorMap map_b, int M,
+                                                                  const __grid_constant__ CUtensorMap map_b,
+                                                                  const __grid_constant__ CUtensorMap map_d,
+                                                                  const __grid_constant__ CUtensorMap map_t, int M,
                                                                   int N, int K, int kb_per_split, int n_mt, int n_nt,
                                                                   int n_zt, TcEpilogue ep) {
     constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
     constexpr uint32_t kBBytes = BN * kTcBK * 2;
     constexpr uint32_t kStage = kABytes + kBBytes;
+    constexpr int kTcStages = tc_stages(BN);
     constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
     constexpr int kEpiCols = BN >= 64 ? BN / 2 : BN;        // columns per epilogue warp
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -234,6 +317,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     uint64_t* tfull = empty + kTcStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint16_t* stg_all = reinterpret_cast<uint16_t*>(sm + kTcStages * kStage + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkt = K / kTcBK;
@@ -274,11 +358,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
+            // L2 prefetch cursor kTcPrefetch k-blocks ahead of the loads: operands
+            // streamed from HBM (split-K over rows) miss L2 on every block, and the
+            // shared ring alone only covers ~4 MMA k-blocks of latency.
+            int pt = blockIdx.x, pkb = 0, pz, pm0, pn0, pkb0, pnk;
+            if (pt < tiles) decode(pt, pz, pm0, pn0, pkb0, pnk);
+            auto prefetch_next = [&]() {
+                if (pt >= tiles) return;
+                tma_prefetch_2d(&map_a, (pkb0 + pkb) * kTcBK, pm0);
+                tma_prefetch_2d(&map_b, (pkb0 + pkb) * kTcBK, pn0);
+                if (++pkb >= pnk) {
+                    pkb = 0;
+                    pt += gridDim.x;
+                    if (pt < tiles) decode(pt, pz, pm0, pn0, pkb0, pnk);
+                }
+            };
+            for (int i = 0; i < kTcPrefetch; i++) prefetch_next();
             int it = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 int z, m0, n0, kb0, nk;
                 decode(t, z, m0, n0, kb0, nk);
                 for (int kb = 0; kb < nk; kb++, it++) {
+                    if (kTcPrefetch > 0) prefetch_next();
                     const int s = it % kTcStages;
                     if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
                     unsigned char* st = sm + s * kStage;
@@ -320,6 +421,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         const int quad = warp & 3;
         const int c0 = (BN >= 64) ? (ew >> 2) * kEpiCols : 0;
         const bool work = (BN >= 64) || ew < 4;
+        EpiStage sg{stg_all + ew * 2 * kTcStgBlk, 0, &map_d, &map_t};
         int lt = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
             int z, m0, n0, kb0, nk;
@@ -335,13 +437,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 for (int c = c0; c < c0 + kEpiCols; c += 32) {
                     float v[32];
                     tmem_ld32(tmem + acc * BN + ((uint32_t)(quad * 32) << 16) + c, v);
-                    tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane);
+                    tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane, sg);
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
         }
+        sg.drain(lane);
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -369,25 +472,34 @@ static EncodeTiledFn encode_fn() {
 }
 
 // row-major [rows x cols] bf16 matrix with row stride ld (elements), box
-// [box_rows x 64 cols], 128-byte swizzle; rows beyond `rows` read as zero
-static bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+// [box_rows x box_cols]; loads: 64 cols, 128-byte swizzle, rows beyond `rows`
+// read as zero; stores: 32 x 32, no swizzle, out-of-range elements skipped
+static bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                          int box_cols = kTcBK, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kTcBK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int BN>
 static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, md, mt;
+    memset(&md, 0, sizeof(md));
+    memset(&mt, 0, sizeof(mt));
     if (!make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM) || !make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN))
         return cudaErrorInvalidValue;
-    const size_t smem = 1024 + (size_t)kTcStages * (kTcBM + BN) * kTcBK * 2 + 256;
+    if (ep.kind == 1 && !make_map_bf16(&md, ep.d_bf16, g.M, g.N, ep.ldd, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return cudaErrorInvalidValue;
+    __nv_bfloat16* tdst = ep.kind == 1 ? ep.d_t : ep.kind == 3 ? ep.dht : nullptr;
+    if (tdst && !make_map_bf16(&mt, tdst, g.N, g.M, ep.ldt, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+        return cudaErrorInvalidValue;
+    const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 256 + kTcStgBytes;
     auto k = tc_gemm_kernel<BN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -400,7 +512,7 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = n_nt * n_mt * n_zt;
     const int grid = tiles < sms ? tiles : sms;
-    k<<<grid, kTcThreads, smem, st>>>(ma, mb, g.M, g.N, g.K, kps, n_mt, n_nt, n_zt, ep);
+    k<<<grid, kTcThreads, smem, st>>>(ma, mb, md, mt, g.M, g.N, g.K, kps, n_mt, n_nt, n_zt, ep);
     return cudaGetLastError();
 }
 
@@ -421,7 +533,7 @@ cudaError_t launch_tc(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
 //   2. delta_o per row (one-hot targets, K outputs)  tcgen05 (N=32 padded), epilogue 2
 //   3. dH^T  = ((delta_o W2) * h(1-h))^T              tcgen05 (K=64 padded), epilogue 3
 //   4. dW1^T += [X,1]^T dH                            tcgen05 split-K, epilogue 4 (f32 accumulate)
-//   5. dW2   += delta_o^T [H,1]                       CUDA cores
+//   5. dW2^T += [H,1]^T delta_o                       tcgen05 split-K, epilogue 4 (H^T from epilogue 1)
 // then W <- f32(W - lr/N grad) on the f32 master weights (reference layout).
 constexpr int kWD = 1024, kWH = 1024, kWK = 16;
 constexpr int kWMi = 1152;  // [X,1]^T rows padded to a multiple of 128 (rows > 1024 read as zero)
@@ -511,77 +623,17 @@ __global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __
     if (e < kWK) b2[e] = W2[e * (kWH + 1) + kWH];
 }
 
-// dW2[k][j] += sum_r delta_o[r][k] h[r][j]; column kWH is the bias (h = 1).
-// Block = 64 column groups (4 hidden columns each) x 4 row phases; delta_o rows
-// are staged in shared memory and consumed as float2 broadcasts by FFMA2 with
-// the h value as the broadcast scalar; the 4 phases are combined in shared
-// memory before one f64 atomic per (k, j) per block.
-constexpr int kDw2Rows = 64;
-__global__ void __launch_bounds__(256) wide_dw2_kernel(const float* __restrict__ dof, const __nv_bfloat16* __restrict__ H,
-                                                       int64_t rows, double* __restrict__ dW2) {
-    extern __shared__ __align__(16) float dsm[];
-    float* sd = dsm;                    // [kDw2Rows][kWK]
-    float* red = dsm + kDw2Rows * kWK;  // [4][256][kWK] phase partials
-    const int tid = threadIdx.x, cg = tid & 63, ph = tid >> 6;
-    const bool bias_blk = blockIdx.x == kWH / 256;
-    const int j0 = blockIdx.x * 256 + cg * 4;
-    float2 acc[4][kWK / 2];
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-#pragma unroll
-        for (int q = 0; q < kWK / 2; q++) acc[u][q] = make_float2(0.f, 0.f);
-    const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
-    const int64_t rb = (int64_t)blockIdx.y * per, re = min(rows, rb + per);
-    for (int64_t r0 = rb; r0 < re; r0 += kDw2Rows) {
-        const int n = (int)min((int64_t)kDw2Rows, re - r0);
-        __syncthreads();
-        if (tid < n * (kWK / 4))
-            reinterpret_cast<float4*>(sd)[tid] = reinterpret_cast<const float4*>(dof + r0 * kWK)[tid];
-        __syncthreads();
-        for (int rr = ph; rr < n; rr += 4) {
-            float h[4];
-            if (!bias_blk) {
-                const uint2 hv = *reinterpret_cast<const uint2*>(H + (r0 + rr) * kWH + j0);
-                const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv.x));
-                const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hv.y));
-                h[0] = a.x;
-                h[1] = a.y;
-                h[2] = b.x;
-                h[3] = b.y;
-            } else {
-                h[0] = cg == 0 ? 1.f : 0.f;
-                h[1] = h[2] = h[3] = 0.f;
-            }
-            const float2* d2 = reinterpret_cast<const float2*>(sd + rr * kWK);
-#pragma unroll
-            for (int q = 0; q < kWK / 2; q++) {
-                const float2 d = d2[q];
-#pragma unroll
-                for (int u = 0; u < 4; u++) acc[u][q] = ffma2(bcast2(h[u]), d, acc[u][q]);
-            }
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 4; u++)
-#pragma unroll
-        for (int q = 0; q < kWK / 2; q++) {
-            red[(ph * 256 + cg * 4 + u) * kWK + 2 * q] = acc[u][q].x;
-            red[(ph * 256 + cg * 4 + u) * kWK + 2 * q + 1] = acc[u][q].y;
-        }
-    __syncthreads();
-    for (int e = tid; e < 256 * kWK; e += 256) {
-        const int col = e / kWK, k = e % kWK;
-        const float v = red[e] + red[256 * kWK + e] + red[2 * 256 * kWK + e] + red[3 * 256 * kWK + e];
-        const int j = blockIdx.x * 256 + col;
-        if (!bias_blk) atomicAdd(dW2 + k * (kWH + 1) + j, (double)v);
-        else if (col == 0) atomicAdd(dW2 + k * (kWH + 1) + kWH, (double)v);
-    }
+// row `row` of a [rows x ld] bf16 matrix = 1.0 (the bias row of H^T)
+__global__ void fill_ones_row_kernel(__nv_bfloat16* __restrict__ M, int64_t ld, int row, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) M[(int64_t)row * ld + i] = __float2bfloat16_rn(1.f);
 }
 
+// W <- f32(W - lr/N * grad) in f64; the split-K partial sums are reduced here
+// in f64 (dW1^T: [split][1152][1024], dW2^T: [split][1152][32], row 1024 = bias)
 __global__ void wide_update_kernel(float* __restrict__ W1, float* __restrict__ W2, const float* __restrict__ dW1T,
-                                   int splits, int64_t zstride, const double* __restrict__ dW2, double lr_over_n,
-                                   int* __restrict__ nonfinite) {
+                                   int splits, int64_t zstride, const float* __restrict__ dW2T, int splits2,
+                                   int64_t zstride2, double lr_over_n, int* __restrict__ nonfinite) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < kWH * (kWD + 1)) {
         const int j = e / (kWD + 1), i = e % (kWD + 1);
@@ -592,7 +644,10 @@ __global__ void wide_update_kernel(float* __restrict__ W1, float* __restrict__ W
         if (!isfinite(w) && nonfinite) atomicOr(nonfinite, 1);
     }
     if (e < kWK * (kWH + 1)) {
-        const float w = __double2float_rn((double)W2[e] - lr_over_n * dW2[e]);
+        const int k = e / (kWH + 1), j = e % (kWH + 1);
+        double g = 0.0;
+        for (int z = 0; z < splits2; z++) g += (double)dW2T[z * zstride2 + (int64_t)j * 32 + k];
+        const float w = __double2float_rn((double)W2[e] - lr_over_n * g);
         W2[e] = w;
         if (!isfinite(w) && nonfinite) atomicOr(nonfinite, 1);
     }
@@ -609,56 +664,59 @@ cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint
     return cudaGetLastError();
 }
 
+constexpr int kWSplits2 = 16;  // split-K of the dW2 GEMM (9 M tiles x 16 = 144 CTAs)
+
 struct WideWork {
     void* W1b;
     float* b1;
     void* W2b;
     float* b2;
     void* W2T;
-    void* Hb;
-    void* dob;
-    float* dof;
-    void* dht;
+    void* Hb;   // [C][1024] bf16
+    void* HT;   // [1025][C] bf16, row 1024 = 1 (bias input of dW2)
+    void* dob;  // [C][64] bf16
+    void* doT;  // [32][C] bf16, rows >= 16 zero
+    void* dht;  // [1024][C] bf16
     float* dW1T;
-    double* dW2;
+    float* dW2T;
     int64_t C;
     int splits;
 };
 
-size_t wide_work_bytes(int64_t C, int splits) {
-    return (size_t)kWH * kWD * 2 + kWH * 4 + 32 * kWH * 2 + 64 + (size_t)kWH * 64 * 2 + (size_t)C * kWH * 2 +
-           (size_t)C * 64 * 2 + (size_t)C * kWK * 4 + (size_t)kWH * C * 2 + (size_t)splits * kWMi * kWH * 4 +
-           (size_t)kWK * (kWH + 1) * 8 + 64 * 16;
-}
-
-static void carve(WideWork& w, unsigned char* base, int64_t C, int splits) {
+static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
     size_t o = 0;
     auto take = [&](size_t bytes) {
-        void* p = base + o;
+        void* p = base ? base + o : nullptr;
         o += (bytes + 255) / 256 * 256;
         return p;
     };
-    w.W1b = take((size_t)kWH * kWD * 2);
-    w.b1 = (float*)take(kWH * 4);
-    w.W2b = take(32 * kWH * 2);
-    w.b2 = (float*)take(64);
-    w.W2T = take((size_t)kWH * 64 * 2);
-    w.Hb = take((size_t)C * kWH * 2);
-    w.dob = take((size_t)C * 64 * 2);
-    w.dof = (float*)take((size_t)C * kWK * 4);
-    w.dht = take((size_t)kWH * C * 2);
-    w.dW1T = (float*)take((size_t)splits * kWMi * kWH * 4);
-    w.dW2 = (double*)take((size_t)kWK * (kWH + 1) * 8);
-    w.C = C;
-    w.splits = splits;
+    WideWork t;
+    t.W1b = take((size_t)kWH * kWD * 2);
+    t.b1 = (float*)take(kWH * 4);
+    t.W2b = take(32 * kWH * 2);
+    t.b2 = (float*)take(64);
+    t.W2T = take((size_t)kWH * 64 * 2);
+    t.Hb = take((size_t)C * kWH * 2);
+    t.HT = take((size_t)(kWH + 1) * C * 2);
+    t.dob = take((size_t)C * 64 * 2);
+    t.doT = take((size_t)32 * C * 2);
+    t.dht = take((size_t)kWH * C * 2);
+    t.dW1T = (float*)take((size_t)splits * kWMi * kWH * 4);
+    t.dW2T = (float*)take((size_t)kWSplits2 * kWMi * 32 * 4);
+    t.C = C;
+    t.splits = splits;
+    if (w) *w = t;
+    return o;
 }
+
+size_t wide_work_bytes(int64_t C, int splits) { return carve(nullptr, nullptr, C, splits); }
 
 // one epoch; stats (device, may be null): [loss, correct, wrong] accumulated
 cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
                        double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
                        cudaStream_t st, const std::function<void(bool)>& prof) {
     WideWork w;
-    carve(w, work, C, splits);
+    carve(&w, work, C, splits);
     cudaError_t e;
     const int n_derive = kWH * kWD;
     wide_derive_kernel<<<(n_derive + 255) / 256, 256, 0, st>>>(W1, W2, (__nv_bfloat16*)w.W1b, w.b1,
@@ -666,8 +724,12 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int64_t zstride = (int64_t)kWMi * kWH;
     if ((e = cudaMemsetAsync(w.dW1T, 0, (size_t)splits * zstride * 4, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(w.dW2, 0, (size_t)kWK * (kWH + 1) * 8, st)) != cudaSuccess) return e;
+    const int64_t zstride2 = (int64_t)kWMi * 32;
+    if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)kWSplits2 * zstride2 * 4, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 64 * 2, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.doT, 0, (size_t)32 * C * 2, st)) != cudaSuccess) return e;
+    fill_ones_row_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.HT, C, kWH, C);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     for (int64_t r0 = 0; r0 < N; r0 += C) {
         const int Cc = (int)std::min<int64_t>(C, N - r0);
         const __nv_bfloat16* Xc = reinterpret_cast<const __nv_bfloat16*>(Xb) + r0 * kWD;
@@ -677,6 +739,8 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             TcEpilogue ep{};
             ep.kind = 1;
             ep.d_bf16 = (__nv_bfloat16*)w.Hb;
+            ep.d_t = (__nv_bfloat16*)w.HT;
+            ep.ldt = C;
             ep.bias = w.b1;
             ep.ldd = kWH;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
@@ -689,7 +753,8 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             ep.labels = labels + r0;
             ep.K = kWK;
             ep.do_b = (__nv_bfloat16*)w.dob;
-            ep.do_f = w.dof;
+            ep.do_t = (__nv_bfloat16*)w.doT;
+            ep.ldt = C;
             ep.stats = stats;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
@@ -713,22 +778,20 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             ep.zstride = zstride;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
-        prof(false);
-        {  // 5. dW2
-            const size_t dsm = (size_t)(kDw2Rows * kWK + 4 * 256 * kWK) * sizeof(float);
-            static bool attr = false;
-            if (!attr) {
-                cudaFuncSetAttribute(wide_dw2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm);
-                attr = true;
-            }
-            dim3 grid(kWH / 256 + 1, 96);
-            wide_dw2_kernel<<<grid, 256, dsm, st>>>(w.dof, (const __nv_bfloat16*)w.Hb, Cc, w.dW2);
-            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32 with delta_o^T rows >= 16 zero)
+            TcGemm g{w.HT, w.doT, kWH + 1, 32, Cc, C, C, kWSplits2};
+            TcEpilogue ep{};
+            ep.kind = 4;
+            ep.d_f32 = w.dW2T;
+            ep.ldd = 32;
+            ep.zstride = zstride2;
+            if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
+        prof(false);
     }
     const int nu = kWH * (kWD + 1);
-    wide_update_kernel<<<(nu + 255) / 256, 256, 0, st>>>(W1, W2, w.dW1T, splits, zstride, w.dW2, lr / (double)N,
-                                                         nonfinite);
+    wide_update_kernel<<<(nu + 255) / 256, 256, 0, st>>>(W1, W2, w.dW1T, splits, zstride, w.dW2T, kWSplits2,
+                                                         zstride2, lr / (double)N, nonfinite);
     return cudaGetLastError();
 }
 
