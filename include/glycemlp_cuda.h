@@ -132,8 +132,10 @@ int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t
 /* Wide configuration: 1024 inputs -> 1024 hidden -> 16
  * sigmoid outputs, full-batch GD with every large contraction on tcgen05
  * (BF16 operands, FP32 accumulation in TMEM). glx_wide_make_data fills the
- * device buffers Xb (N x 1024 bf16, U[0,1)), XT (1025 x N bf16: X^T plus a
- * ones row) and labels (N u8 class ids in [0,16)); N % 64 == 0.
+ * device buffers Xb (N x 1024 bf16, U[0,1)), XT (1025 x N bf16: [X,1]^T in
+ * the K-blocked layout [N/64][1025][64], element (i, r) at
+ * ((r/64)*1025 + i)*64 + r%64) and labels (N u8 class ids in [0,16));
+ * N % 64 == 0.
  * glx_wide_train runs `epochs` epochs on f32 master weights in the reference
  * layout (w_ih 1024 x 1025, w_ho 16 x 1025); stats_hist (device, may be NULL)
  * gets [loss, correct, wrong] per epoch at the epoch-start weights. */

@@ -43,10 +43,6 @@ __host__ __device__ constexpr int tc_stages(int BN) {
 // blocks (2 KB each) per warp, used alternately
 constexpr int kTcStgBlk = 32 * 32;  // bf16 elements per staged block
 constexpr int kTcStgBytes = 8 * 2 * kTcStgBlk * 2;
-#ifndef GLX_TC_PREFETCH
-#define GLX_TC_PREFETCH 0  // k-blocks of L2 prefetch ahead of the loads (8 measured 2x slower on the split-K GEMM)
-#endif
-constexpr int kTcPrefetch = GLX_TC_PREFETCH;
 constexpr int kTcThreads = 320;  // TMA warp + MMA warp + 8 epilogue warps
 
 // ------------------------------------------------------------- descriptors
@@ -71,10 +67,13 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// L2-only prefetch of the same box (no shared memory, no barrier)
-__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0), "r"(c1)
-                 : "memory");
+// K-blocked operand ([K/64][rows][64]): box {64, rows, 1} is one contiguous span
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
 }
 
 __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -118,18 +117,25 @@ struct TcEpilogue {
     const uint8_t* labels;
     int K;
     __nv_bfloat16* do_b;  // [M][64] bf16, columns >= K stay zero
-    __nv_bfloat16* do_t;  // [K][ldt] bf16: delta_o transposed (the dW2 GEMM operand)
+    __nv_bfloat16* do_t;  // delta_o transposed, K-blocked [M/64][32][64] bf16 (the dW2 GEMM operand)
     double* stats;        // [loss, correct, wrong]
     // 3: delta_h = v * h (1 - h), written transposed
     const __nv_bfloat16* h;
     int ldh;
     __nv_bfloat16* dht;
-    int64_t ldt;  // row stride of the transposed outputs (d_t, do_t, dht)
+    int64_t ldt;  // row stride of the transposed outputs (d_t, dht) when t_blk == 0
+    int t_blk;    // R > 0: transposed outputs K-blocked [M/64][R][64]
 };
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(map),
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
@@ -140,7 +146,8 @@ struct EpiStage {
     uint16_t* buf;  // this warp's 2 x kTcStgBlk bf16
     int next;
     const CUtensorMap* map_d;  // row-major bf16 result (kind 1), box 32 x 32
-    const CUtensorMap* map_t;  // transposed bf16 result (kinds 1, 3), box 32 x 32
+    const CUtensorMap* map_t;  // transposed bf16 result (kinds 1, 3), box 32 x 32 (x 1 when K-blocked)
+    bool t_blocked;
     __device__ __forceinline__ uint16_t* acquire(int lane) {
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
         __syncwarp();
@@ -149,10 +156,14 @@ struct EpiStage {
         return b;
     }
     // make the generic-proxy writes of this warp visible to the bulk copy, then issue it
-    __device__ __forceinline__ void release(const CUtensorMap* map, const uint16_t* b, int c0, int c1, int lane) {
+    __device__ __forceinline__ void release(const CUtensorMap* map, const uint16_t* b, int c0, int c1, int lane,
+                                            bool blocked = false) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) tma_store_2d(map, b, c0, c1);
+        if (lane == 0) {
+            if (blocked) tma_store_3d(map, b, c0 & 63, c1, c0 >> 6);
+            else tma_store_2d(map, b, c0, c1);
+        }
     }
     __device__ __forceinline__ void drain(int lane) {
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -165,7 +176,8 @@ struct TcGemm {
     const void* B;  // [N x K] bf16, row stride ldb
     int M, N, K;
     int64_t lda, ldb;
-    int splits;  // split-K: blockIdx.z takes K / splits
+    int splits;         // split-K: blockIdx.z takes K / splits
+    int a_blk, b_blk;   // 0: row-major; R > 0: K-blocked [K/64][R][64] (lda/ldb unused)
 };
 
 // lane = row, pk[e] = columns 2e, 2e+1 of that row
@@ -183,7 +195,7 @@ __device__ __forceinline__ void store_cols_bf16(EpiStage& sg, const uint32_t (&p
         b[(2 * e) * 32 + lane] = (uint16_t)(pk[e] & 0xFFFFu);
         b[(2 * e + 1) * 32 + lane] = (uint16_t)(pk[e] >> 16);
     }
-    sg.release(sg.map_t, b, row0, col0, lane);
+    sg.release(sg.map_t, b, row0, col0, lane, sg.t_blocked);
 }
 
 template <int BN>
@@ -252,7 +264,7 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
                 }
                 const __nv_bfloat16 db = __float2bfloat16_rn(d);
                 ep.do_b[(int64_t)row * 64 + k] = db;
-                ep.do_t[(int64_t)k * ep.ldt + row] = db;
+                ep.do_t[((int64_t)(row >> 6) * 32 + k) * 64 + (row & 63)] = db;
             }
             correct = arg == lab ? 1.f : 0.f;
             wrong = 1.f - correct;
@@ -301,7 +313,8 @@ template <int BN>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                                                                   const __grid_constant__ CUtensorMap map_b,
                                                                   const __grid_constant__ CUtensorMap map_d,
-                                                                  const __grid_constant__ CUtensorMap map_t, int M,
+                                                                  const __grid_constant__ CUtensorMap map_t, int flags,
+                                                                  int M,
                                                                   int N, int K, int kb_per_split, int n_mt, int n_nt,
                                                                   int n_zt, TcEpilogue ep) {
     constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
@@ -358,34 +371,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer
-            // L2 prefetch cursor kTcPrefetch k-blocks ahead of the loads: operands
-            // streamed from HBM (split-K over rows) miss L2 on every block, and the
-            // shared ring alone only covers ~4 MMA k-blocks of latency.
-            int pt = blockIdx.x, pkb = 0, pz, pm0, pn0, pkb0, pnk;
-            if (pt < tiles) decode(pt, pz, pm0, pn0, pkb0, pnk);
-            auto prefetch_next = [&]() {
-                if (pt >= tiles) return;
-                tma_prefetch_2d(&map_a, (pkb0 + pkb) * kTcBK, pm0);
-                tma_prefetch_2d(&map_b, (pkb0 + pkb) * kTcBK, pn0);
-                if (++pkb >= pnk) {
-                    pkb = 0;
-                    pt += gridDim.x;
-                    if (pt < tiles) decode(pt, pz, pm0, pn0, pkb0, pnk);
-                }
-            };
-            for (int i = 0; i < kTcPrefetch; i++) prefetch_next();
             int it = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
                 int z, m0, n0, kb0, nk;
                 decode(t, z, m0, n0, kb0, nk);
                 for (int kb = 0; kb < nk; kb++, it++) {
-                    if (kTcPrefetch > 0) prefetch_next();
                     const int s = it % kTcStages;
                     if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
                     unsigned char* st = sm + s * kStage;
                     mbar_arrive_expect_tx(&full[s], kStage);
-                    tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
-                    tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
+                    if (flags & 1) tma_load_3d(st, &map_a, 0, m0, kb0 + kb, &full[s]);
+                    else tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
+                    if (flags & 2) tma_load_3d(st + kABytes, &map_b, 0, n0, kb0 + kb, &full[s]);
+                    else tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
                 }
             }
         }
@@ -421,7 +419,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         const int quad = warp & 3;
         const int c0 = (BN >= 64) ? (ew >> 2) * kEpiCols : 0;
         const bool work = (BN >= 64) || ew < 4;
-        EpiStage sg{stg_all + ew * 2 * kTcStgBlk, 0, &map_d, &map_t};
+        EpiStage sg{stg_all + ew * 2 * kTcStgBlk, 0, &map_d, &map_t, (flags & 4) != 0};
         int lt = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
             int z, m0, n0, kb0, nk;
@@ -487,18 +485,41 @@ static bool make_map_bf16(CUtensorMap* map, const void* base, int64_t rows, int6
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// K-blocked [nkb][R][64] bf16 operand: box {64 | box_k, box_rows, 1}
+static bool make_map_blk(CUtensorMap* map, const void* base, int64_t R, int64_t nkb, int box_rows, int box_k,
+                         CUtensorMapSwizzle swz) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {64, (cuuint64_t)R, (cuuint64_t)nkb};
+    cuuint64_t strides[2] = {64 * 2, (cuuint64_t)R * 64 * 2};
+    cuuint32_t box[3] = {(cuuint32_t)box_k, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN>
 static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
     CUtensorMap ma, mb, md, mt;
     memset(&md, 0, sizeof(md));
     memset(&mt, 0, sizeof(mt));
-    if (!make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM) || !make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN))
-        return cudaErrorInvalidValue;
+    const int64_t nkb = g.K / kTcBK;
+    const bool oka = g.a_blk ? make_map_blk(&ma, g.A, g.a_blk, nkb, kTcBM, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
+                             : make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM);
+    const bool okb = g.b_blk ? make_map_blk(&mb, g.B, g.b_blk, nkb, BN, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
+                             : make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN);
+    if (!oka || !okb) return cudaErrorInvalidValue;
     if (ep.kind == 1 && !make_map_bf16(&md, ep.d_bf16, g.M, g.N, ep.ldd, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
         return cudaErrorInvalidValue;
     __nv_bfloat16* tdst = ep.kind == 1 ? ep.d_t : ep.kind == 3 ? ep.dht : nullptr;
-    if (tdst && !make_map_bf16(&mt, tdst, g.N, g.M, ep.ldt, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
-        return cudaErrorInvalidValue;
+    if (tdst) {
+        const bool ok = ep.t_blk ? (g.M % 64 == 0 &&
+                                    make_map_blk(&mt, tdst, ep.t_blk, g.M / 64, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+                                 : make_map_bf16(&mt, tdst, g.N, g.M, ep.ldt, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
+        if (!ok) return cudaErrorInvalidValue;
+    }
+    const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0);
     const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 256 + kTcStgBytes;
     auto k = tc_gemm_kernel<BN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -512,7 +533,7 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
     if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int tiles = n_nt * n_mt * n_zt;
     const int grid = tiles < sms ? tiles : sms;
-    k<<<grid, kTcThreads, smem, st>>>(ma, mb, md, mt, g.M, g.N, g.K, kps, n_mt, n_nt, n_zt, ep);
+    k<<<grid, kTcThreads, smem, st>>>(ma, mb, md, mt, flags, g.M, g.N, g.K, kps, n_mt, n_nt, n_zt, ep);
     return cudaGetLastError();
 }
 
@@ -581,7 +602,10 @@ __global__ void wide_gen_kernel(__nv_bfloat16* __restrict__ X, uint8_t* __restri
     }
 }
 
-// XT[i][r] = X[r][i] for i < 1024, XT[1024][r] = 1 (bias input)
+// [X,1]^T in the K-blocked layout of the split-K operands: element (i, r) at
+// ((r / 64) * 1025 + i) * 64 + r % 64; row i = 1024 is the bias input (1)
+__device__ __forceinline__ int64_t kblk_index(int64_t r, int i, int R) { return ((r >> 6) * R + i) * 64 + (r & 63); }
+
 __global__ void wide_transpose_kernel(const __nv_bfloat16* __restrict__ X, __nv_bfloat16* __restrict__ XT, int64_t N) {
     __shared__ __nv_bfloat16 tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.x * 32;
@@ -593,11 +617,11 @@ __global__ void wide_transpose_kernel(const __nv_bfloat16* __restrict__ X, __nv_
     __syncthreads();
     for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
         const int64_t r = r0 + threadIdx.x;
-        if (r < N) XT[(int64_t)(i0 + dy) * N + r] = tile[threadIdx.x][dy];
+        if (r < N) XT[kblk_index(r, i0 + dy, kWD + 1)] = tile[threadIdx.x][dy];
     }
     if (blockIdx.y == 0 && threadIdx.y == 0) {
         const int64_t r = r0 + threadIdx.x;
-        if (r < N) XT[(int64_t)kWD * N + r] = __float2bfloat16_rn(1.f);
+        if (r < N) XT[kblk_index(r, kWD, kWD + 1)] = __float2bfloat16_rn(1.f);
     }
 }
 
@@ -623,10 +647,10 @@ __global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __
     if (e < kWK) b2[e] = W2[e * (kWH + 1) + kWH];
 }
 
-// row `row` of a [rows x ld] bf16 matrix = 1.0 (the bias row of H^T)
-__global__ void fill_ones_row_kernel(__nv_bfloat16* __restrict__ M, int64_t ld, int row, int64_t n) {
+// row `row` of a K-blocked [n/64][R][64] bf16 matrix = 1.0 (the bias row of H^T)
+__global__ void fill_ones_row_kernel(__nv_bfloat16* __restrict__ M, int R, int row, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) M[(int64_t)row * ld + i] = __float2bfloat16_rn(1.f);
+    if (i < n) M[kblk_index(i, row, R)] = __float2bfloat16_rn(1.f);
 }
 
 // W <- f32(W - lr/N * grad) in f64; the split-K partial sums are reduced here
@@ -673,10 +697,10 @@ struct WideWork {
     float* b2;
     void* W2T;
     void* Hb;   // [C][1024] bf16
-    void* HT;   // [1025][C] bf16, row 1024 = 1 (bias input of dW2)
+    void* HT;   // [H,1]^T, K-blocked [C/64][1025][64] bf16, row 1024 = 1 (bias input of dW2)
     void* dob;  // [C][64] bf16
-    void* doT;  // [32][C] bf16, rows >= 16 zero
-    void* dht;  // [1024][C] bf16
+    void* doT;  // delta_o^T, K-blocked [C/64][32][64] bf16, rows >= 16 zero
+    void* dht;  // dH^T, K-blocked [C/64][1024][64] bf16
     float* dW1T;
     float* dW2T;
     int64_t C;
@@ -728,7 +752,7 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
     if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)kWSplits2 * zstride2 * 4, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 64 * 2, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.doT, 0, (size_t)32 * C * 2, st)) != cudaSuccess) return e;
-    fill_ones_row_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.HT, C, kWH, C);
+    fill_ones_row_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.HT, kWH + 1, kWH, C);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     for (int64_t r0 = 0; r0 < N; r0 += C) {
         const int Cc = (int)std::min<int64_t>(C, N - r0);
@@ -740,7 +764,7 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             ep.kind = 1;
             ep.d_bf16 = (__nv_bfloat16*)w.Hb;
             ep.d_t = (__nv_bfloat16*)w.HT;
-            ep.ldt = C;
+            ep.t_blk = kWH + 1;
             ep.bias = w.b1;
             ep.ldd = kWH;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
@@ -754,7 +778,6 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             ep.K = kWK;
             ep.do_b = (__nv_bfloat16*)w.dob;
             ep.do_t = (__nv_bfloat16*)w.doT;
-            ep.ldt = C;
             ep.stats = stats;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
@@ -765,12 +788,12 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             ep.h = (const __nv_bfloat16*)w.Hb;
             ep.ldh = kWH;
             ep.dht = (__nv_bfloat16*)w.dht;
-            ep.ldt = C;
+            ep.t_blk = kWH;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
         {  // 4. dW1^T += [X,1]^T dH (split-K over the chunk's rows)
-            const __nv_bfloat16* XTc = reinterpret_cast<const __nv_bfloat16*>(XT) + r0;
-            TcGemm g{XTc, w.dht, kWD + 1, kWH, Cc, N, C, splits};
+            const __nv_bfloat16* XTc = reinterpret_cast<const __nv_bfloat16*>(XT) + r0 * (kWD + 1);
+            TcGemm g{XTc, w.dht, kWD + 1, kWH, Cc, 0, 0, splits, kWD + 1, kWH};
             TcEpilogue ep{};
             ep.kind = 4;
             ep.d_f32 = w.dW1T;
@@ -779,7 +802,7 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
         {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32 with delta_o^T rows >= 16 zero)
-            TcGemm g{w.HT, w.doT, kWH + 1, 32, Cc, C, C, kWSplits2};
+            TcGemm g{w.HT, w.doT, kWH + 1, 32, Cc, 0, 0, kWSplits2, kWH + 1, 32};
             TcEpilogue ep{};
             ep.kind = 4;
             ep.d_f32 = w.dW2T;

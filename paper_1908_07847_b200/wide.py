@@ -21,7 +21,8 @@ D, H, K = 1024, 1024, 16
 
 
 class WideData:
-    """Device-resident rows: Xb (N x 1024 bf16), XT (1025 x N bf16), labels (N u8)."""
+    """Device-resident rows: Xb (N x 1024 bf16), XT ([X,1]^T, 1025 x N bf16 stored
+    K-blocked as [N/64][1025][64]), labels (N u8)."""
 
     def __init__(self, n_rows: int, seed: int = 0, device: int = 0):
         import torch
@@ -33,7 +34,7 @@ class WideData:
         L = _lib.load()
         with torch.cuda.device(self.dev):
             self.Xb = torch.empty((n_rows, D), dtype=torch.bfloat16, device=self.dev)
-            self.XT = torch.empty((D + 1, n_rows), dtype=torch.bfloat16, device=self.dev)
+            self.XT = torch.empty((n_rows // 64, D + 1, 64), dtype=torch.bfloat16, device=self.dev)
             self.labels = torch.empty(n_rows, dtype=torch.uint8, device=self.dev)
             _lib.check(L.glx_wide_make_data(n_rows, seed, self.Xb.data_ptr(), self.XT.data_ptr(),
                                             self.labels.data_ptr(), torch.cuda.current_stream().cuda_stream))
