@@ -41,8 +41,12 @@ __host__ __device__ constexpr int tc_stages(int BN) {
 }
 // per-epilogue-warp staging for TMA stores of bf16 results: two 32 x 32 bf16
 // blocks (2 KB each) per warp, used alternately
+#ifndef GLX_TC_STG_SETS
+#define GLX_TC_STG_SETS 1  // staging sets of 2 blocks per epilogue warp
+#endif
+constexpr int kTcStgSets = GLX_TC_STG_SETS;
 constexpr int kTcStgBlk = 32 * 32;  // bf16 elements per staged block
-constexpr int kTcStgBytes = 8 * 2 * kTcStgBlk * 2;
+constexpr int kTcStgBytes = 8 * 2 * kTcStgSets * kTcStgBlk * 2;
 constexpr int kTcThreads = 320;  // TMA warp + MMA warp + 8 epilogue warps
 
 // ------------------------------------------------------------- descriptors
@@ -105,6 +109,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
     for (int i = 0; i < 32; i++) v[i] = __uint_as_float(r[i]);
 }
 
+// tcgen05.ld without the wait: the 32 registers are valid only after tmem_wait()
+__device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 struct TcEpilogue {
     int kind;               // 0: f32 store; 1: bias+sigmoid -> bf16; 2: output layer; 3: delta_h^T; 4: f32 accumulate
     float* d_f32;           // 0, 4 (4: + blockIdx.z * zstride)
@@ -149,10 +167,10 @@ struct EpiStage {
     const CUtensorMap* map_t;  // transposed bf16 result (kinds 1, 3), box 32 x 32 (x 1 when K-blocked)
     bool t_blocked;
     __device__ __forceinline__ uint16_t* acquire(int lane) {
-        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(2 * kTcStgSets - 1) : "memory");
         __syncwarp();
         uint16_t* b = buf + next * kTcStgBlk;
-        next ^= 1;
+        next = next + 1 == 2 * kTcStgSets ? 0 : next + 1;
         return b;
     }
     // make the generic-proxy writes of this warp visible to the bulk copy, then issue it
@@ -171,6 +189,37 @@ struct EpiStage {
     }
 };
 
+// kind 1: the row-major block and (optionally) its transpose from one staging
+// pass with a single proxy fence; both staging blocks are reused only after
+// the previous chunk's bulk stores have read them
+__device__ __forceinline__ void store_rows_cols_bf16(EpiStage& sg, const uint32_t (&pk)[16], int row0, int col0,
+                                                     int lane, bool with_t) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(2 * (kTcStgSets - 1)) : "memory");
+    __syncwarp();
+    uint16_t* br = sg.buf + sg.next * kTcStgBlk;
+    uint16_t* bt = br + kTcStgBlk;
+    sg.next = sg.next + 2 == 2 * kTcStgSets ? 0 : sg.next + 2;
+    uint4* d = reinterpret_cast<uint4*>(br + lane * 32);
+#pragma unroll
+    for (int q = 0; q < 4; q++) d[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    if (with_t) {
+#pragma unroll
+        for (int e = 0; e < 16; e++) {
+            bt[(2 * e) * 32 + lane] = (uint16_t)(pk[e] & 0xFFFFu);
+            bt[(2 * e + 1) * 32 + lane] = (uint16_t)(pk[e] >> 16);
+        }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(sg.map_d, br, col0, row0);
+        if (with_t) {
+            if (sg.t_blocked) tma_store_3d(sg.map_t, bt, row0 & 63, col0, row0 >> 6);
+            else tma_store_2d(sg.map_t, bt, row0, col0);
+        }
+    }
+}
+
 struct TcGemm {
     const void* A;  // [M x K] bf16, row stride lda
     const void* B;  // [N x K] bf16, row stride ldb
@@ -180,14 +229,7 @@ struct TcGemm {
     int a_blk, b_blk;   // 0: row-major; R > 0: K-blocked [K/64][R][64] (lda/ldb unused)
 };
 
-// lane = row, pk[e] = columns 2e, 2e+1 of that row
-__device__ __forceinline__ void store_rows_bf16(EpiStage& sg, const uint32_t (&pk)[16], int row0, int col0, int lane) {
-    uint16_t* b = sg.acquire(lane);
-    uint4* d = reinterpret_cast<uint4*>(b + lane * 32);
-#pragma unroll
-    for (int q = 0; q < 4; q++) d[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-    sg.release(sg.map_d, b, col0, row0, lane);
-}
+// lane = row, pk[e] = columns 2e, 2e+1 of that row; stored transposed
 __device__ __forceinline__ void store_cols_bf16(EpiStage& sg, const uint32_t (&pk)[16], int row0, int col0, int lane) {
     uint16_t* b = sg.acquire(lane);
 #pragma unroll
@@ -242,8 +284,7 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
             }
         }
         // TMA stores clip rows >= M of a tail tile
-        store_rows_bf16(sg, pall, row - lane, n0 + c, lane);
-        if (ep.d_t) store_cols_bf16(sg, pall, row - lane, n0 + c, lane);
+        store_rows_cols_bf16(sg, pall, row - lane, n0 + c, lane, ep.d_t != nullptr);
     } else if (ep.kind == 2) {
         // output neuron (kernels.py:352-375 generalised to K outputs)
         float loss = 0.f, correct = 0.f, wrong = 0.f;
@@ -419,7 +460,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         const int quad = warp & 3;
         const int c0 = (BN >= 64) ? (ew >> 2) * kEpiCols : 0;
         const bool work = (BN >= 64) || ew < 4;
-        EpiStage sg{stg_all + ew * 2 * kTcStgBlk, 0, &map_d, &map_t, (flags & 4) != 0};
+        EpiStage sg{stg_all + ew * 2 * kTcStgSets * kTcStgBlk, 0, &map_d, &map_t, (flags & 4) != 0};
         int lt = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
             int z, m0, n0, kb0, nk;
@@ -431,11 +472,32 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                 TcEpilogue e2 = ep;
                 if (ep.kind == 4) e2.d_f32 = ep.d_f32 + z * ep.zstride;
                 const int row = m0 + quad * 32 + lane;
+                // software pipeline: the TMEM load of chunk c + 32 is in flight
+                // while chunk c goes through the epilogue math and stores
+                const uint32_t tbase = tmem + acc * BN + ((uint32_t)(quad * 32) << 16);
+                uint32_t ra[32], rb[32];
+                tmem_ld32_async(tbase + c0, ra);
+                tmem_wait();
 #pragma unroll 1
-                for (int c = c0; c < c0 + kEpiCols; c += 32) {
-                    float v[32];
-                    tmem_ld32(tmem + acc * BN + ((uint32_t)(quad * 32) << 16) + c, v);
-                    tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane, sg);
+                for (int c = c0; c < c0 + kEpiCols; c += 64) {
+                    const bool more = c + 32 < c0 + kEpiCols;
+                    if (more) tmem_ld32_async(tbase + c + 32, rb);
+                    {
+                        float v[32];
+#pragma unroll
+                        for (int i = 0; i < 32; i++) v[i] = __uint_as_float(ra[i]);
+                        tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane, sg);
+                    }
+                    if (!more) break;
+                    tmem_wait();
+                    if (c + 64 < c0 + kEpiCols) tmem_ld32_async(tbase + c + 64, ra);
+                    {
+                        float v[32];
+#pragma unroll
+                        for (int i = 0; i < 32; i++) v[i] = __uint_as_float(rb[i]);
+                        tc_epilogue_chunk<BN>(e2, v, M, row, n0, c + 32, lane, sg);
+                    }
+                    tmem_wait();
                 }
             }
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -191,15 +191,15 @@ def config5(L, peak, rows=16_777_216, epochs=3):
     _lib.check(L.glx_profile_read(_lib.ptr(kms), _lib.ptr(kn)))
     L.glx_profile_enable(0)
     flops = rows * f_train(1024, 1024, 16)
-    tc_flops = rows * (2 * 1024 * 1024 * 2 + 2 * 1024 * 32 + 2 * 1024 * 64) + rows * 2 * 128 / 128 * 0
     pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     bf16 = pk.get("bf16_tflops", 1654.1)
     return {"config": "5: wide 1024->1024->16, 16Mi rows, full batch, tcgen05 BF16 operands / FP32 TMEM accumulation",
             "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
             "tflops_algorithmic": flops / (ms * 1e-3) / 1e12, "frac_bf16_peak": flops / (ms * 1e-3) / 1e12 / bf16,
             "tc_gemm_ms_per_epoch": float(kms[0]) / epochs, "bf16_peak_tflops": bf16,
-            "note": "tc_gemm_ms covers the four tcgen05 GEMM launches per chunk; the remainder is the CUDA-core dW2 "
-                    "reduction, derive/update kernels"}
+            "note": "tc_gemm_ms covers the five tcgen05 GEMM launches per 1Mi-row chunk (hidden layer, output layer, "
+                    "hidden deltas, split-K dW1, split-K dW2); the remainder is the per-epoch derive/update kernels. "
+                    "frac_bf16_peak is against MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"}
 
 
 def eval_rate(L, peak):
