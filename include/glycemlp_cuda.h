@@ -140,6 +140,18 @@ int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t
  * layout (w_ih 1024 x 1025, w_ho 16 x 1025); stats_hist (device, may be NULL)
  * gets [loss, correct, wrong] per epoch at the epoch-start weights. */
 int glx_wide_make_data(int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream);
+/* Rows [row0, row0 + N) of the same data set (a data-parallel shard). */
+int glx_wide_make_shard(int64_t row0, int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream);
+/* Data-parallel split of one wide epoch (SURVEY.md 8(e) for C5): glx_wide_grad
+ * writes the f64 gradient SUM over this shard's rows at the current weights
+ * into grad[0, P) (reference layout: w_ih then w_ho, P = 1,066,000) and
+ * [loss, correct, wrong] into grad[P, P+3); after an all-reduce of the
+ * glx_wide_grad_len() doubles, glx_wide_apply performs
+ * W <- f32(f64(W) - lr_over_n * grad) identically on every rank. */
+int64_t glx_wide_grad_len(void);
+int glx_wide_grad(const float* w_ih, const float* w_ho, const void* Xb, const void* XT, const uint8_t* labels,
+                  int64_t N, double* grad, void* stream);
+int glx_wide_apply(float* w_ih, float* w_ho, const double* grad, double lr_over_n, int32_t* nonfinite, void* stream);
 int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
                    int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream);
 

@@ -633,9 +633,38 @@ int glx_tc_gemm_bf16(const void* A, const void* B, int32_t M, int32_t N, int32_t
     return GLX_OK;
 }
 
-int glx_wide_make_data(int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream) {
+int glx_wide_make_shard(int64_t row0, int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream) {
     if (N < 64 || N % 64) return set_err(GLX_ERR_SHAPE, "wide data needs N %% 64 == 0 (got %lld)", (long long)N);
-    GLX_LAUNCH(launch_wide_gen(Xb, XT, labels, N, seed, (cudaStream_t)stream));
+    if (row0 < 0) return set_err(GLX_ERR_INVALID, "row0 must be >= 0");
+    GLX_LAUNCH(launch_wide_gen(Xb, XT, labels, N, seed, row0, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_wide_make_data(int64_t N, uint64_t seed, void* Xb, void* XT, uint8_t* labels, void* stream) {
+    return glx_wide_make_shard(0, N, seed, Xb, XT, labels, stream);
+}
+
+int64_t glx_wide_grad_len(void) { return kWideP + 3; }
+
+int glx_wide_grad(const float* w_ih, const float* w_ho, const void* Xb, const void* XT, const uint8_t* labels,
+                  int64_t N, double* grad, void* stream) {
+    if (N < 64 || N % 64) return set_err(GLX_ERR_SHAPE, "wide gradient needs N %% 64 == 0 (got %lld)", (long long)N);
+    if (!grad) return set_err(GLX_ERR_INVALID, "grad must be a device buffer of glx_wide_grad_len() doubles");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t C = std::min<int64_t>(N, (int64_t)1 << 20);
+    const int splits = 8;
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->wide.ensure(wide_work_bytes(C, splits)));
+    GLX_CK(wide_grad(w_ih, w_ho, Xb, XT, labels, N, ws->wide.as<unsigned char>(), C, splits, grad, st,
+                     [](bool) {}));
+    g_launches.fetch_add(3 + 5 * (uint64_t)((N + C - 1) / C));
+    return GLX_OK;
+}
+
+int glx_wide_apply(float* w_ih, float* w_ho, const double* grad, double lr_over_n, int32_t* nonfinite, void* stream) {
+    if (!grad) return set_err(GLX_ERR_INVALID, "grad must not be NULL");
+    GLX_CK(wide_apply(w_ih, w_ho, grad, lr_over_n, nonfinite, (cudaStream_t)stream));
+    g_launches.fetch_add(1);
     return GLX_OK;
 }
 
@@ -666,7 +695,7 @@ int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, con
         GLX_CK(wide_epoch(w_ih, w_ho, Xb, XT, labels, N, lr, ws->wide.as<unsigned char>(), C, splits, stats,
                           nonfinite, st, prof));
         GLX_CK(perr);
-        g_launches.fetch_add(3 + 5 * (uint64_t)((N + C - 1) / C));
+        g_launches.fetch_add(4 + 5 * (uint64_t)((N + C - 1) / C));
     }
     return GLX_OK;
 }

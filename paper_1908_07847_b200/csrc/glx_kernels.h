@@ -100,8 +100,14 @@ cudaError_t launch_tc_gemm(const void* A, const void* B, int M, int N, int K, in
                            const float* bias, int ldd, cudaStream_t st);
 
 // wide configuration (1024 -> 1024 -> 16) on the tcgen05 GEMM
-cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, cudaStream_t st);
+constexpr int64_t kWideP = 1024 * 1025 + 16 * 1025;  // weights of the wide network
+cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, int64_t row0,
+                            cudaStream_t st);
 size_t wide_work_bytes(int64_t C, int splits);
+cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const void* XT, const uint8_t* labels,
+                      int64_t N, unsigned char* work, int64_t C, int splits, double* grad, cudaStream_t st,
+                      const std::function<void(bool)>& prof);
+cudaError_t wide_apply(float* W1, float* W2, const double* grad, double lr_over_n, int* nonfinite, cudaStream_t st);
 cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
                        double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
                        cudaStream_t st, const std::function<void(bool)>& prof);

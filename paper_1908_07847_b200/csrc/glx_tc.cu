@@ -619,7 +619,8 @@ cudaError_t launch_tc(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
 //   5. dW2^T += [H,1]^T delta_o                       tcgen05 split-K, epilogue 4 (H^T from epilogue 1)
 // then W <- f32(W - lr/N grad) on the f32 master weights (reference layout).
 constexpr int kWD = 1024, kWH = 1024, kWK = 16;
-constexpr int kWMi = 1152;  // [X,1]^T rows padded to a multiple of 128 (rows > 1024 read as zero)
+constexpr int kWMi = 1152;
+constexpr int kWP = kWH * (kWD + 1) + kWK * (kWH + 1);  // 1,066,000 weights  // [X,1]^T rows padded to a multiple of 128 (rows > 1024 read as zero)
 
 __device__ __forceinline__ uint32_t mix32(uint64_t x) {
     x ^= x >> 33;
@@ -637,14 +638,15 @@ __device__ __forceinline__ float unit_u01(uint64_t seed, uint64_t idx) {
 // linear scores over 32 fixed columns (a K-class analogue of synthetic_matrix's
 // planted-linear labels)
 __global__ void wide_gen_kernel(__nv_bfloat16* __restrict__ X, uint8_t* __restrict__ labels, int64_t N,
-                                uint64_t seed) {
+                                uint64_t seed, int64_t row0) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
     if (r >= N) return;
+    const int64_t rg = row0 + r;  // global row index: a shard is a slice of the full data set
     float score[kWK];
 #pragma unroll
     for (int k = 0; k < kWK; k++) score[k] = 0.f;
     for (int i = threadIdx.x; i < kWD; i += 32) {
-        const float v = unit_u01(seed, (uint64_t)r * kWD + i);
+        const float v = unit_u01(seed, (uint64_t)rg * kWD + i);
         const __nv_bfloat16 b = __float2bfloat16_rn(v);
         X[r * kWD + i] = b;
         if ((i & 31) == 7) {  // 32 planted columns
@@ -715,33 +717,43 @@ __global__ void fill_ones_row_kernel(__nv_bfloat16* __restrict__ M, int R, int r
     if (i < n) M[kblk_index(i, row, R)] = __float2bfloat16_rn(1.f);
 }
 
-// W <- f32(W - lr/N * grad) in f64; the split-K partial sums are reduced here
-// in f64 (dW1^T: [split][1152][1024], dW2^T: [split][1152][32], row 1024 = bias)
-__global__ void wide_update_kernel(float* __restrict__ W1, float* __restrict__ W2, const float* __restrict__ dW1T,
-                                   int splits, int64_t zstride, const float* __restrict__ dW2T, int splits2,
-                                   int64_t zstride2, double lr_over_n, int* __restrict__ nonfinite) {
+// grad (f64, reference layout: dW1 [1024][1025] then dW2 [16][1025]) = the
+// split-K partial sums reduced in fixed slab order (dW1^T: [split][1152][1024],
+// dW2^T: [split][1152][32], row 1024 = bias)
+__global__ void wide_reduce_kernel(const float* __restrict__ dW1T, int splits, int64_t zstride,
+                                   const float* __restrict__ dW2T, int splits2, int64_t zstride2,
+                                   double* __restrict__ grad) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < kWH * (kWD + 1)) {
         const int j = e / (kWD + 1), i = e % (kWD + 1);
         double g = 0.0;
         for (int z = 0; z < splits; z++) g += (double)dW1T[z * zstride + (int64_t)i * kWH + j];
-        const float w = __double2float_rn((double)W1[e] - lr_over_n * g);
-        W1[e] = w;
-        if (!isfinite(w) && nonfinite) atomicOr(nonfinite, 1);
-    }
-    if (e < kWK * (kWH + 1)) {
-        const int k = e / (kWH + 1), j = e % (kWH + 1);
+        grad[e] = g;
+    } else if (e < kWP) {
+        const int e2 = e - kWH * (kWD + 1);
+        const int k = e2 / (kWH + 1), j = e2 % (kWH + 1);
         double g = 0.0;
         for (int z = 0; z < splits2; z++) g += (double)dW2T[z * zstride2 + (int64_t)j * 32 + k];
-        const float w = __double2float_rn((double)W2[e] - lr_over_n * g);
-        W2[e] = w;
-        if (!isfinite(w) && nonfinite) atomicOr(nonfinite, 1);
+        grad[e] = g;
     }
 }
 
-cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, cudaStream_t st) {
+// W <- f32(f64(W) - lr/N * grad) over both layers (the reference's unfused op order)
+__global__ void wide_apply_kernel(float* __restrict__ W1, float* __restrict__ W2, const double* __restrict__ grad,
+                                  double lr_over_n, int* __restrict__ nonfinite) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= kWP) return;
+    float* w = e < kWH * (kWD + 1) ? W1 + e : W2 + (e - kWH * (kWD + 1));
+    const float v = __double2float_rn((double)*w - lr_over_n * grad[e]);
+    *w = v;
+    if (!isfinite(v) && nonfinite) atomicOr(nonfinite, 1);
+}
+
+cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, int64_t row0,
+                            cudaStream_t st) {
     dim3 blk(32, 8);
-    wide_gen_kernel<<<(unsigned)((N + 7) / 8), blk, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(Xb), labels, N, seed);
+    wide_gen_kernel<<<(unsigned)((N + 7) / 8), blk, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(Xb), labels, N, seed,
+                                                            row0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((N + 31) / 32), kWD / 32);
@@ -765,6 +777,7 @@ struct WideWork {
     void* dht;  // dH^T, K-blocked [C/64][1024][64] bf16
     float* dW1T;
     float* dW2T;
+    double* grad;  // [kWP + 3]: gradient sums, then loss, correct, wrong
     int64_t C;
     int splits;
 };
@@ -789,6 +802,7 @@ static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
     t.dht = take((size_t)kWH * C * 2);
     t.dW1T = (float*)take((size_t)splits * kWMi * kWH * 4);
     t.dW2T = (float*)take((size_t)kWSplits2 * kWMi * 32 * 4);
+    t.grad = (double*)take((size_t)(kWP + 3) * 8);
     t.C = C;
     t.splits = splits;
     if (w) *w = t;
@@ -798,12 +812,17 @@ static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
 size_t wide_work_bytes(int64_t C, int splits) { return carve(nullptr, nullptr, C, splits); }
 
 // one epoch; stats (device, may be null): [loss, correct, wrong] accumulated
-cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
-                       double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
-                       cudaStream_t st, const std::function<void(bool)>& prof) {
+// gradient SUM over the N rows at the current weights -> grad[0, kWP) (f64),
+// grad[kWP .. kWP+3) = loss, correct, wrong (grad may be the workspace's own)
+cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const void* XT, const uint8_t* labels,
+                      int64_t N, unsigned char* work, int64_t C, int splits, double* grad, cudaStream_t st,
+                      const std::function<void(bool)>& prof) {
     WideWork w;
     carve(&w, work, C, splits);
     cudaError_t e;
+    if (!grad) grad = w.grad;
+    double* stats = grad + kWP;
+    if ((e = cudaMemsetAsync(stats, 0, 3 * sizeof(double), st)) != cudaSuccess) return e;
     const int n_derive = kWH * kWD;
     wide_derive_kernel<<<(n_derive + 255) / 256, 256, 0, st>>>(W1, W2, (__nv_bfloat16*)w.W1b, w.b1,
                                                                (__nv_bfloat16*)w.W2b, w.b2, (__nv_bfloat16*)w.W2T);
@@ -874,10 +893,29 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
         }
         prof(false);
     }
-    const int nu = kWH * (kWD + 1);
-    wide_update_kernel<<<(nu + 255) / 256, 256, 0, st>>>(W1, W2, w.dW1T, splits, zstride, w.dW2T, kWSplits2,
-                                                         zstride2, lr / (double)N, nonfinite);
+    wide_reduce_kernel<<<(kWP + 255) / 256, 256, 0, st>>>(w.dW1T, splits, zstride, w.dW2T, kWSplits2, zstride2,
+                                                         grad);
     return cudaGetLastError();
+}
+
+cudaError_t wide_apply(float* W1, float* W2, const double* grad, double lr_over_n, int* nonfinite, cudaStream_t st) {
+    wide_apply_kernel<<<(kWP + 255) / 256, 256, 0, st>>>(W1, W2, grad, lr_over_n, nonfinite);
+    return cudaGetLastError();
+}
+
+// one fused epoch (single device): gradient into the workspace, then the update;
+// stats (device, may be null) receives [loss, correct, wrong]
+cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
+                       double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
+                       cudaStream_t st, const std::function<void(bool)>& prof) {
+    WideWork w;
+    carve(&w, work, C, splits);
+    cudaError_t e = wide_grad(W1, W2, Xb, XT, labels, N, work, C, splits, w.grad, st, prof);
+    if (e != cudaSuccess) return e;
+    if (stats && (e = cudaMemcpyAsync(stats, w.grad + kWP, 3 * sizeof(double), cudaMemcpyDeviceToDevice, st)) !=
+                     cudaSuccess)
+        return e;
+    return wide_apply(W1, W2, w.grad, lr / (double)N, nonfinite, st);
 }
 
 cudaError_t launch_tc_gemm(const void* A, const void* B, int M, int N, int K, int epi, float* d_f32,

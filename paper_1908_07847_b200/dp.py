@@ -1,4 +1,4 @@
-"""Data-parallel full-batch training over torch.distributed (config 4).
+"""Data-parallel full-batch training over torch.distributed (configs 4 and 5).
 
 SURVEY.md 8(e): the rows are sharded contiguously over the ranks (one
 process per GPU), every epoch each rank computes the gradient SUM of its
@@ -31,7 +31,7 @@ def shard_bounds(n_rows: int, world_size: int, rank: int) -> tuple[int, int]:
 @dataclass
 class EpochStats:
     loss_sum: float
-    counts: tuple[int, int, int, int]
+    counts: tuple[int, ...]  # K=1: tp, tn, fp, fn; wide K=16: correct, wrong
 
 
 class DeviceEngine:
@@ -83,18 +83,21 @@ def train_data_parallel(engine, epochs: int, lr: float, n_total: int, all_reduce
     Returns per-epoch statistics (loss sum and confusion counts over ALL rows,
     at each epoch's starting weights), identical on every rank.
     """
-    P = engine.H * (engine.D + 1) + engine.H + 1
+    # gradient layout: P sums, then loss and the counts (K=1: tp, tn, fp, fn;
+    # the wide K=16 engine: correct, wrong)
+    P = getattr(engine, "P", None) or engine.H * (engine.D + 1) + engine.H + 1
+    ns = getattr(engine, "n_stats", 5)
     kept = []  # device-side copies: no host sync inside the epoch loop
     for _ in range(epochs):
         g = engine.grad_sum()
         if all_reduce is not None:
             all_reduce(g)
         engine.apply(g, lr / n_total)
-        kept.append(g[P:P + 5].clone() if hasattr(g, "clone") else g[P:P + 5].copy())
+        kept.append(g[P:P + ns].clone() if hasattr(g, "clone") else g[P:P + ns].copy())
     stats = []
     for s in kept:
         s = s.tolist()
-        stats.append(EpochStats(float(s[0]), tuple(int(round(v)) for v in s[1:5])))
+        stats.append(EpochStats(float(s[0]), tuple(int(round(v)) for v in s[1:ns])))
     return stats
 
 

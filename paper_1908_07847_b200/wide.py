@@ -24,20 +24,22 @@ class WideData:
     """Device-resident rows: Xb (N x 1024 bf16), XT ([X,1]^T, 1025 x N bf16 stored
     K-blocked as [N/64][1025][64]), labels (N u8)."""
 
-    def __init__(self, n_rows: int, seed: int = 0, device: int = 0):
+    def __init__(self, n_rows: int, seed: int = 0, device: int = 0, row0: int = 0):
+        """Rows [row0, row0 + n_rows) of the data set `seed` (row0 > 0: a data-parallel shard)."""
         import torch
 
         if n_rows < 64 or n_rows % 64:
             raise ShapeError(f"wide data needs a positive multiple of 64 rows, got {n_rows}")
         self.N = n_rows
+        self.row0 = row0
         self.dev = torch.device("cuda", device)
         L = _lib.load()
         with torch.cuda.device(self.dev):
             self.Xb = torch.empty((n_rows, D), dtype=torch.bfloat16, device=self.dev)
             self.XT = torch.empty((n_rows // 64, D + 1, 64), dtype=torch.bfloat16, device=self.dev)
             self.labels = torch.empty(n_rows, dtype=torch.uint8, device=self.dev)
-            _lib.check(L.glx_wide_make_data(n_rows, seed, self.Xb.data_ptr(), self.XT.data_ptr(),
-                                            self.labels.data_ptr(), torch.cuda.current_stream().cuda_stream))
+            _lib.check(L.glx_wide_make_shard(row0, n_rows, seed, self.Xb.data_ptr(), self.XT.data_ptr(),
+                                             self.labels.data_ptr(), torch.cuda.current_stream().cuda_stream))
 
     def host_rows(self) -> tuple[np.ndarray, np.ndarray]:
         """(features f32 = the exact bf16 values, labels u8) for CPU checking."""
@@ -76,3 +78,52 @@ def train_wide(data: WideData, w_ih: np.ndarray, w_ho: np.ndarray, epochs: int, 
         if stats is not None:
             stats[:] = sd[:epochs].cpu().numpy()
         return w1.cpu().numpy(), w2.cpu().numpy()
+
+
+def shard_rows(n_rows: int, world_size: int, rank: int) -> tuple[int, int]:
+    """Contiguous shard [r0, r1) of `rank` with both ends on 64-row boundaries."""
+    if n_rows % 64:
+        raise ShapeError(f"wide data needs a multiple of 64 rows, got {n_rows}")
+    blocks = n_rows // 64
+    return 64 * (blocks * rank // world_size), 64 * (blocks * (rank + 1) // world_size)
+
+
+class WideEngine:
+    """One rank's wide-network state for dp.train_data_parallel:
+    the shard's device rows, f32 master weights and the f64 gradient buffer
+    (P = 1,066,000 sums + loss, correct, wrong)."""
+
+    P = H * (D + 1) + K * (H + 1)
+    n_stats = 3
+
+    def __init__(self, data: WideData, w_ih: np.ndarray, w_ho: np.ndarray):
+        import torch
+
+        if w_ih.size != H * (D + 1) or w_ho.size != K * (H + 1):
+            raise ShapeError("wide weights must be 1024 x 1025 and 16 x 1025")
+        self.torch = torch
+        self.L = _lib.load()
+        self.data = data
+        self.N = data.N
+        with torch.cuda.device(data.dev):
+            self.stream = torch.cuda.current_stream(data.dev).cuda_stream
+            self.w1 = torch.from_numpy(np.ascontiguousarray(w_ih, dtype=np.float32).reshape(-1)).to(data.dev)
+            self.w2 = torch.from_numpy(np.ascontiguousarray(w_ho, dtype=np.float32).reshape(-1)).to(data.dev)
+            self.grad = torch.zeros(int(self.L.glx_wide_grad_len()), dtype=torch.float64, device=data.dev)
+            self.flag = torch.zeros(1, dtype=torch.int32, device=data.dev)
+
+    def grad_sum(self):
+        d = self.data
+        _lib.check(self.L.glx_wide_grad(self.w1.data_ptr(), self.w2.data_ptr(), d.Xb.data_ptr(), d.XT.data_ptr(),
+                                        d.labels.data_ptr(), d.N, self.grad.data_ptr(), self.stream))
+        return self.grad
+
+    def apply(self, grad, lr_over_n: float) -> None:
+        _lib.check(self.L.glx_wide_apply(self.w1.data_ptr(), self.w2.data_ptr(), grad.data_ptr(), float(lr_over_n),
+                                         self.flag.data_ptr(), self.stream))
+
+    def weights(self) -> tuple[np.ndarray, np.ndarray]:
+        return self.w1.cpu().numpy(), self.w2.cpu().numpy()
+
+    def nonfinite(self) -> bool:
+        return bool(self.flag.item())

@@ -121,3 +121,102 @@ def test_world1_no_allreduce_matches():
     r2 = w2.copy().reshape(1, 6)
     O.train_batch(r1, r2, x, t, 5, 2.0, x.shape[0])
     assert np.max(np.abs(eng.w1.reshape(-1) - r1.reshape(-1))) <= 1e-6
+
+
+class NumpyKEngine:
+    """Test stand-in for wide.WideEngine: K sigmoid outputs, one-hot targets, the
+    wide gradient layout (P sums, then loss, correct, wrong)."""
+
+    n_stats = 3
+
+    def __init__(self, x, y, w_ih, w_ho, H, K):
+        self.x = x.astype(np.float64)
+        self.y = y
+        self.N, self.D = x.shape
+        self.H, self.K = H, K
+        self.P = H * (self.D + 1) + K * (H + 1)
+        self.w1 = w_ih.copy().reshape(H, self.D + 1)
+        self.w2 = w_ho.copy().reshape(K, H + 1)
+
+    def grad_sum(self):
+        W1, W2 = self.w1.astype(np.float64), self.w2.astype(np.float64)
+        xa = np.hstack([self.x, np.ones((self.N, 1))])
+        h = 1.0 / (1.0 + np.exp(-(xa @ W1.T)))
+        ha = np.hstack([h, np.ones((self.N, 1))])
+        o = 1.0 / (1.0 + np.exp(-(ha @ W2.T)))
+        t = np.eye(self.K)[self.y]
+        d_o = (o - t) * o * (1.0 - o)
+        d_h = (d_o @ W2[:, :-1]) * h * (1.0 - h)
+        correct = np.sum(np.argmax(o, axis=1) == self.y)
+        stats = [0.5 * np.sum((t - o) ** 2), correct, self.N - correct]
+        return torch.from_numpy(np.concatenate([(d_h.T @ xa).reshape(-1), (d_o.T @ ha).reshape(-1),
+                                                np.array(stats, np.float64)]))
+
+    def apply(self, grad, lr_over_n):
+        g = grad.numpy()
+        P1 = self.w1.size
+        self.w1 = (self.w1.astype(np.float64) - lr_over_n * g[:P1].reshape(self.w1.shape)).astype(np.float32)
+        self.w2 = (self.w2.astype(np.float64) - lr_over_n * g[P1:self.P].reshape(self.w2.shape)).astype(np.float32)
+
+
+def _kdata():
+    rng = np.random.default_rng(5)
+    x = rng.random((256, 9), dtype=np.float32)
+    y = np.argmax(x[:, :4] + 0.1 * rng.random((256, 4)), axis=1).astype(np.uint8)
+    w1 = rng.uniform(-0.5, 0.5, 6 * 10).astype(np.float32)
+    w2 = rng.uniform(-0.5, 0.5, 4 * 7).astype(np.float32)
+    return x, y, w1, w2
+
+
+def _kworker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1908_07847_b200 import wide
+
+    x, y, w1, w2 = _kdata()
+    r0, r1 = wide.shard_rows(x.shape[0], world, rank)  # 64-row aligned shards, as the wide path uses
+    eng = NumpyKEngine(x[r0:r1], y[r0:r1], w1, w2, 6, 4)
+    stats = dp.train_data_parallel(eng, 10, 1.5, x.shape[0], dp.nccl_all_reduce())
+    out_q.put((rank, eng.w1.copy(), eng.w2.copy(), [(s.loss_sum, s.counts) for s in stats]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(240)
+def test_gloo_world2_k_outputs_wide_layout():
+    """The C5 data-parallel loop (K=16 engine layout: P sums + loss, correct, wrong)
+    over gloo equals the oracle's single-process K-output full-batch restatement."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_kworker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=200) for _ in range(2)], key=lambda r: r[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, a1, a2, sa), (_, b1, b2, sb) = res
+    assert a1.tobytes() == b1.tobytes() and a2.tobytes() == b2.tobytes()
+    assert [c for _, c in sa] == [c for _, c in sb]
+    from oracle import oracle as O
+
+    x, y, w1, w2 = _kdata()
+    r1, r2 = w1.copy().reshape(6, 10), w2.copy().reshape(4, 7)
+    O.train_batch_par(r1, r2, x, np.eye(4, dtype=np.float32)[y], 10, 1.5)
+    assert np.max(np.abs(a1.reshape(-1) - r1.reshape(-1))) <= 1e-6
+    assert np.max(np.abs(a2.reshape(-1) - r2.reshape(-1))) <= 1e-6
+    assert all(len(c) == 2 and sum(c) == x.shape[0] for _, c in sa)
+
+
+def test_wide_shard_rows_cover_and_align():
+    from paper_1908_07847_b200 import wide
+
+    for n, world in [(64 * 100, 8), (64 * 7, 4), (1 << 24, 8), (64, 1)]:
+        spans = [wide.shard_rows(n, world, r) for r in range(world)]
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+        assert all(r0 % 64 == 0 and r1 % 64 == 0 for r0, r1 in spans)
+    with pytest.raises(Exception):
+        wide.shard_rows(100, 2, 0)

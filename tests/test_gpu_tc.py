@@ -1,5 +1,7 @@
-"""tcgen05 BF16 GEMM (csrc/glx_tc.cu) vs a plain fp32 torch reference of the same op."""
+"""tcgen05 BF16 GEMM (csrc/glx_tc.cu) vs a plain fp32 torch reference of the same op, and the
+wide configuration (C5) built on it vs the oracle, including its data-parallel split."""
 
+import numpy as np
 import pytest
 
 pytestmark = pytest.mark.gpu
@@ -75,3 +77,71 @@ def test_wide_config_vs_oracle(gpu, init_range, lr, tol):
     assert stats[0, 1] + stats[0, 2] == 2048
     assert abs(stats[0, 0] - loss) <= 5e-3 * loss
     assert abs(stats[0, 1] - correct) <= 20
+
+
+def test_wide_shard_is_slice_of_full_data(gpu):
+    from paper_1908_07847_b200 import wide
+
+    full = wide.WideData(2048, seed=5)
+    part = wide.WideData(1024, seed=5, row0=1024)
+    import torch
+
+    bits = lambda t: t.contiguous().view(torch.int16).cpu().numpy().tobytes()
+    assert bits(full.Xb[1024:]) == bits(part.Xb)
+    assert bits(full.XT[16:]) == bits(part.XT)  # K-blocked: 64-row blocks 16.. of the full data
+    assert (full.labels[1024:].cpu() == part.labels.cpu()).all()
+
+
+def test_wide_dp_split_equals_fused(gpu):
+    """C5 data-parallel split: two row shards' f64 gradient sums,
+    added as the all-reduce would, then glx_wide_apply == the fused epoch."""
+    from conftest import rel_err
+    from paper_1908_07847_b200 import wide
+
+    N, epochs, lr = 4096, 3, 0.5
+    w1, w2 = wide.init_wide_weights(seed=11)
+    fused1, fused2 = wide.train_wide(wide.WideData(N, seed=2), w1, w2, epochs, lr)
+    engines = []
+    for r in range(2):
+        r0, r1 = wide.shard_rows(N, 2, r)
+        engines.append(wide.WideEngine(wide.WideData(r1 - r0, seed=2, row0=r0), w1, w2))
+    for _ in range(epochs):
+        total = engines[0].grad_sum().clone() + engines[1].grad_sum().clone()
+        for e in engines:
+            e.apply(total, lr / N)
+    a1, a2 = engines[0].weights()
+    b1, b2 = engines[1].weights()
+    assert a1.tobytes() == b1.tobytes() and a2.tobytes() == b2.tobytes()
+    assert rel_err(a1, fused1) <= 1e-6 and rel_err(a2, fused2) <= 1e-6
+
+
+def test_wide_dp_over_nccl_one_rank(gpu):
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from conftest import rel_err
+    from paper_1908_07847_b200 import dp, wide
+
+    N, epochs, lr = 2048, 2, 0.1
+    w1, w2 = wide.init_wide_weights(seed=4)
+    data = wide.WideData(N, seed=9)
+    st = np.zeros((epochs, 3))
+    f1, f2 = wide.train_wide(data, w1, w2, epochs, lr, st)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        eng = wide.WideEngine(data, w1, w2)
+        stats = dp.train_data_parallel(eng, epochs, lr, N, dp.nccl_all_reduce())
+        g1, g2 = eng.weights()
+    finally:
+        dist.destroy_process_group()
+    assert rel_err(g1, f1) <= 1e-7 and rel_err(g2, f2) <= 1e-7
+    for s_, row in zip(stats, st):
+        assert s_.counts == (int(row[1]), int(row[2]))
+        assert abs(s_.loss_sum - row[0]) <= 1e-9 * row[0]
