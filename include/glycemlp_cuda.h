@@ -96,6 +96,20 @@ int glx_train_sweep(int64_t n_nets, const int32_t* H_per_net, const int64_t* w_o
 int32_t glx_packed_ld(int32_t D);
 int glx_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int32_t D, float* Xp,
                   void* stream);
+/* The same packing with the reference's min-max normalisation applied to the
+ * features on the way (dataset.py:383-392; see glx_minmax_apply). */
+int glx_pack_rows_minmax(const float* X, const float* T, const uint8_t* labels, int64_t N, int32_t D,
+                         const float* col_min, const float* col_max, float* Xp, void* stream);
+
+/* Min-max normalisation, replacing dataset.normalize_fit / normalize_apply
+ * (dataset.py:369-392). glx_minmax_fit: col_min/col_max (device float[D]) =
+ * per-column min and max of the N x D row-major f32 rows (exact). glx_minmax_apply:
+ * Y = X scaled as f32((x - min) / (max - min)) with IEEE f32 ops, constant
+ * columns -> 0, clamped to [-0.5, 1.5]; Y may alias X. Inputs are finite
+ * (NaN propagation of numpy's min/max is not reproduced). */
+int glx_minmax_fit(const float* X, int64_t N, int32_t D, float* col_min, float* col_max, void* stream);
+int glx_minmax_apply(const float* X, int64_t N, int32_t D, const float* col_min, const float* col_max, float* Y,
+                     void* stream);
 
 /* Full-batch GD on packed rows. stats_hist: device double[5*epochs] or NULL.
  * nonfinite: device int32 set to 1 if any updated weight is non-finite. */

@@ -143,3 +143,26 @@ def train_sweep(H_per_net, w_off, w_pool, feats2d, targets, epochs, lr, workers=
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+# ------------------------------------------------------------- min-max normalisation
+# numpy restatement of the reference's normalize_fit / normalize_apply
+# (/root/reference/pkg/src/glycemlp/dataset.py:369-398): per-column f32 min and
+# max of the training rows; (x - min) / (max - min) with every op in f32,
+# constant columns -> 0.0, clamp to [-0.5, 1.5]. Pinned bit-exactly against the
+# reference's outputs in tests/golden/normalize_cases.npz.
+NORM_CLAMP_LO, NORM_CLAMP_HI = np.float32(-0.5), np.float32(1.5)
+
+
+def normalize_fit(m: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    m = np.asarray(m, dtype=np.float32)
+    return m.min(axis=0).copy(), m.max(axis=0).copy()
+
+
+def normalize_apply(m: np.ndarray, col_min: np.ndarray, col_max: np.ndarray) -> np.ndarray:
+    m = np.asarray(m, dtype=np.float32)
+    span = (col_max - col_min).astype(np.float32)
+    out = np.zeros_like(m)
+    nz = span != 0
+    out[:, nz] = (m[:, nz] - col_min[nz]) / span[nz]
+    return np.clip(out, NORM_CLAMP_LO, NORM_CLAMP_HI)

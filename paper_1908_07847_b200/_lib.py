@@ -59,6 +59,9 @@ SIGNATURES = {
     "glx_tc_gemm_bf16": (_int, [_vp, _vp, _i32, _i32, _i32, _i32, _vp, _vp, _vp, _i32, _vp]),
     "glx_wide_make_data": (_int, [_i64, _u64, _vp, _vp, _vp, _vp]),
     "glx_wide_train": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _dbl, _vp, _vp, _vp]),
+    "glx_pack_rows_minmax": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
+    "glx_minmax_fit": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
+    "glx_minmax_apply": (_int, [_vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "glx_wide_make_shard": (_int, [_i64, _i64, _u64, _vp, _vp, _vp, _vp]),
     "glx_wide_grad_len": (_i64, []),
     "glx_wide_grad": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),

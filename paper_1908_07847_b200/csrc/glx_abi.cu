@@ -75,7 +75,7 @@ struct DevBuf {
 
 // scratch tied to one (device, stream): stream order serialises its reuse
 struct Workspace {
-    DevBuf part, wk, desc, ctan, losspart, grad, wide;
+    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm;
 };
 
 std::mutex g_ws_mu;
@@ -375,6 +375,33 @@ int glx_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t
     if (N < 0 || D < 1) return set_err(GLX_ERR_SHAPE, "bad pack shape");
     if (N == 0) return GLX_OK;
     GLX_LAUNCH(launch_pack_rows(X, T, labels, N, D, glx_packed_ld(D), Xp, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_pack_rows_minmax(const float* X, const float* T, const uint8_t* labels, int64_t N, int32_t D,
+                         const float* col_min, const float* col_max, float* Xp, void* stream) {
+    if (N < 0 || D < 1) return set_err(GLX_ERR_SHAPE, "bad pack shape");
+    if (!col_min || !col_max) return set_err(GLX_ERR_INVALID, "col_min and col_max are required");
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_pack_rows(X, T, labels, N, D, glx_packed_ld(D), Xp, (cudaStream_t)stream, col_min, col_max));
+    return GLX_OK;
+}
+
+int glx_minmax_fit(const float* X, int64_t N, int32_t D, float* col_min, float* col_max, void* stream) {
+    if (N < 1 || D < 1) return set_err(GLX_ERR_SHAPE, "normalize_fit needs at least one row and column");
+    cudaStream_t st = (cudaStream_t)stream;
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->norm.ensure((size_t)2 * D * sizeof(int)));
+    GLX_CK(launch_minmax_fit(X, N, D, ws->norm.as<int>(), col_min, col_max, st));
+    g_launches.fetch_add(3);
+    return GLX_OK;
+}
+
+int glx_minmax_apply(const float* X, int64_t N, int32_t D, const float* col_min, const float* col_max, float* Y,
+                     void* stream) {
+    if (N < 0 || D < 1) return set_err(GLX_ERR_SHAPE, "bad normalize shape");
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_minmax_apply(X, N, D, col_min, col_max, Y, (cudaStream_t)stream));
     return GLX_OK;
 }
 

@@ -504,13 +504,14 @@ __global__ void batch_prep_kernel(const float* __restrict__ W1, const float* __r
 }
 
 __global__ void pack_rows_kernel(const float* __restrict__ X, const float* __restrict__ T,
-                                 const uint8_t* __restrict__ labels, int64_t N, int D, int LD, float* __restrict__ Xp) {
+                                 const uint8_t* __restrict__ labels, int64_t N, int D, int LD, float* __restrict__ Xp,
+                                 const float* __restrict__ col_min, const float* __restrict__ col_max) {
     const int64_t total = N * LD;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t r = e / LD;
         const int i = (int)(e - r * LD);
         float v;
-        if (i < D) v = X[r * D + i];
+        if (i < D) v = col_min ? minmax_norm(X[r * D + i], col_min[i], col_max[i]) : X[r * D + i];
         else if (i == D) v = 1.0f;
         else if (i == D + 1) v = T ? T[r] : (labels ? (float)labels[r] : 0.0f);
         else v = 0.0f;
@@ -704,11 +705,11 @@ cudaError_t launch_batch_prep(const BatchGeom& g, const float* W1, const float* 
 }
 
 cudaError_t launch_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
-                             float* Xp, cudaStream_t st) {
+                             float* Xp, cudaStream_t st, const float* col_min, const float* col_max) {
     const int64_t total = N * LD;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     if (blocks < 1) blocks = 1;
-    pack_rows_kernel<<<blocks, 256, 0, st>>>(X, T, labels, N, D, LD, Xp);
+    pack_rows_kernel<<<blocks, 256, 0, st>>>(X, T, labels, N, D, LD, Xp, col_min, col_max);
     return cudaGetLastError();
 }
 

@@ -24,6 +24,15 @@ __device__ __forceinline__ float rcp_approx(float x) {
 }
 __device__ __forceinline__ float sigmoid_scaled(float zs) { return rcp_approx(1.0f + ex2_approx(zs)); }
 
+// reference normalize_apply (dataset.py:383-392): every op a separately
+// rounded f32 op (no contraction), constant columns -> 0, clamp [-0.5, 1.5]
+__device__ __forceinline__ float minmax_norm(float x, float mn, float mx) {
+    const float span = __fsub_rn(mx, mn);
+    if (span == 0.0f) return 0.0f;
+    const float y = __fdiv_rn(__fsub_rn(x, mn), span);
+    return fminf(fmaxf(y, -0.5f), 1.5f);
+}
+
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 bcast2(float s) { return make_float2(s, s); }
 

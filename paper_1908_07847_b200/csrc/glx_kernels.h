@@ -68,8 +68,15 @@ inline int ps_loss(const BatchGeom& g) { return g.P1 + g.H + 1; }
 inline int ps_cnt(const BatchGeom& g) { return g.P1 + g.H + 2; }
 
 bool batch_geometry(int64_t N, int D, int H, int n_sms, bool train, BatchGeom* g);
+// col_min/col_max (optional): min-max normalise the features while packing
 cudaError_t launch_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
-                             float* Xp, cudaStream_t st);
+                             float* Xp, cudaStream_t st, const float* col_min = nullptr,
+                             const float* col_max = nullptr);
+// min-max normalisation (glx_data.cu); work = 2*D ints
+cudaError_t launch_minmax_fit(const float* X, int64_t N, int D, int* work, float* col_min, float* col_max,
+                              cudaStream_t st);
+cudaError_t launch_minmax_apply(const float* X, int64_t N, int D, const float* col_min, const float* col_max,
+                                float* Y, cudaStream_t st);
 cudaError_t launch_batch_prep(const BatchGeom& g, const float* W1, const float* W2, float* Wk0, float* Wk1,
                               cudaStream_t st);
 cudaError_t launch_batch_epoch(const BatchGeom& g, const float* Xp, const float* Wk, float* part, bool train,

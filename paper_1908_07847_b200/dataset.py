@@ -3,11 +3,13 @@
 Mirrors the parts of the reference's dataset module that the training path
 reads (/root/reference/pkg/src/glycemlp/dataset.py): the immutable
 row-major float32 + uint8 Dataset (:77-111), SplitPair (:114-120),
-NormStats (:61-74) and synthetic_matrix (:260-289), which defines every
-benchmark configuration's input. CSV ingestion, record derivation, splitting
-and min-max normalisation are host plumbing outside the accelerated path
-(SURVEY.md 2.1); a reference-built SplitPair can be passed straight to
-trainer.train.
+NormStats (:61-74), synthetic_matrix (:260-289), which defines every
+benchmark configuration's input, and the min-max normalisation
+normalize_fit / normalize_apply / normalize_split (:369-410), which runs on
+the device (csrc/glx_data.cu) with the reference's f32
+results bit for bit. CSV ingestion, record derivation and splitting are host
+plumbing outside the accelerated path; a reference-built
+SplitPair can be passed straight to trainer.train.
 
 For cohorts too large for per-row string ids (configs 2/4: 1M and 64M rows),
 synthetic_arrays / iter_synthetic_chunks produce the same bytes as
@@ -21,6 +23,7 @@ from typing import Iterator
 
 import numpy as np
 
+from . import _lib
 from .errors import ShapeError, ValidationError
 
 SUBSET_TAGS = ("male", "female", "all", "synthetic")
@@ -161,3 +164,52 @@ def iter_synthetic_chunks(rows: int, columns: int, seed: int, signal: str = "ran
     for r0 in range(0, rows, chunk_rows):
         n = min(chunk_rows, rows - r0)
         yield r0, gen.random((n, columns), dtype=np.float32), labels[r0:r0 + n]
+
+
+# ---------------------------------------------------------------- normalisation
+def _device_matrix(d: Dataset, device: int):
+    import torch
+
+    return torch.from_numpy(np.array(d.matrix(), dtype=np.float32, copy=True)).to(torch.device("cuda", device))
+
+
+def normalize_fit(train: Dataset, device: int = 0) -> NormStats:
+    """Per-column min/max of the training partition (dataset.py:369-372), on the device."""
+    import torch
+
+    L = _lib.load()
+    dev = torch.device("cuda", device)
+    with torch.cuda.device(dev):
+        m = _device_matrix(train, device)
+        mn = torch.empty(train.columns, dtype=torch.float32, device=dev)
+        mx = torch.empty(train.columns, dtype=torch.float32, device=dev)
+        _lib.check(L.glx_minmax_fit(m.data_ptr(), train.rows, train.columns, mn.data_ptr(), mx.data_ptr(),
+                                    torch.cuda.current_stream(dev).cuda_stream))
+        return NormStats(col_min=mn.cpu().numpy(), col_max=mx.cpu().numpy())
+
+
+def normalize_apply(d: Dataset, stats: NormStats, device: int = 0) -> Dataset:
+    """Min-max scale with train-fitted stats, clamp to [-0.5, 1.5], constant columns
+    -> 0.0 (dataset.py:375-398), on the device; same f32 bytes as the reference."""
+    import torch
+
+    if stats.columns != d.columns:
+        raise ShapeError(f"stats have {stats.columns} columns, dataset has {d.columns}")
+    L = _lib.load()
+    dev = torch.device("cuda", device)
+    with torch.cuda.device(dev):
+        m = _device_matrix(d, device)
+        mn = torch.from_numpy(np.ascontiguousarray(stats.col_min, dtype=np.float32)).to(dev)
+        mx = torch.from_numpy(np.ascontiguousarray(stats.col_max, dtype=np.float32)).to(dev)
+        _lib.check(L.glx_minmax_apply(m.data_ptr(), d.rows, d.columns, mn.data_ptr(), mx.data_ptr(), m.data_ptr(),
+                                      torch.cuda.current_stream(dev).cuda_stream))
+        out = m.cpu().numpy()
+    return Dataset(features=np.ascontiguousarray(out, dtype=np.float32).reshape(-1), labels=d.labels.copy(),
+                   rows=d.rows, columns=d.columns, subset_tag=d.subset_tag, row_ids=d.row_ids, norm_stats=stats)
+
+
+def normalize_split(pair: SplitPair, device: int = 0) -> SplitPair:
+    """Fit on the train partition, apply to both sides (dataset.py:401-410)."""
+    stats = normalize_fit(pair.train, device)
+    return SplitPair(train=normalize_apply(pair.train, stats, device), test=normalize_apply(pair.test, stats, device),
+                     seed=pair.seed, fraction=pair.fraction, stratified=pair.stratified)

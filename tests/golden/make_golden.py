@@ -131,11 +131,55 @@ def small_backend_case():
     print("small_7_19_1: ok")
 
 
+def normalize_cases():
+    """Reference normalize_fit / normalize_apply (dataset.py:369-398) on raw splits:
+    the paper matrix split, a record-built cohort (mixed column ranges), and a
+    hand-built case with a constant column, negative values and test rows
+    outside the fitted range (clamp to [-0.5, 1.5])."""
+    out = {}
+
+    def record(name, pair):
+        stats = g.normalize_fit(pair.train)
+        out[f"{name}_train_raw"] = np.ascontiguousarray(pair.train.matrix())
+        out[f"{name}_test_raw"] = np.ascontiguousarray(pair.test.matrix())
+        out[f"{name}_col_min"] = stats.col_min.copy()
+        out[f"{name}_col_max"] = stats.col_max.copy()
+        out[f"{name}_train_norm"] = np.ascontiguousarray(g.normalize_apply(pair.train, stats).matrix())
+        out[f"{name}_test_norm"] = np.ascontiguousarray(g.normalize_apply(pair.test, stats).matrix())
+
+    record("paper", g.train_test_split(g.synthetic_matrix(120, 33, 7, "planted-linear"), 0.75, 7))
+    record("cohort", g.train_test_split(g.build_dataset(g.synth_dataset(240, 3, "planted-linear"), "synthetic"),
+                                        0.75, 3))
+    rng = np.random.default_rng(21)
+    rows, cols = 300, 37
+    m = (rng.normal(0.0, 1.0, (rows, cols)) * rng.uniform(0.01, 300.0, cols)).astype(np.float32)
+    m[:, 5] = 2.5  # constant column -> 0.0
+    m[:, 9] = -m[:, 9]
+    m[250:, 11] *= 40.0  # test rows far outside the fitted range -> clamped
+
+    def ds(a):
+        return g.Dataset(features=np.ascontiguousarray(a).reshape(-1), labels=np.zeros(a.shape[0], np.uint8),
+                         rows=a.shape[0], columns=cols, subset_tag="synthetic",
+                         row_ids=tuple(f"r{i}" for i in range(a.shape[0])))
+
+    record("edge", g.SplitPair(train=ds(m[:250]), test=ds(m[250:]), seed=0, fraction=0.8))
+    np.savez_compressed(OUT / "normalize_cases.npz", **out)
+    print("normalize_cases: ok", sorted({k.split("_")[0] for k in out}))
+
+
+CASES = {
+    "online": lambda: (
+        online_case("paper_33_33_1", matrix_split(120, 33, 7), 33, 7, [1, 10, 100, 1000]),
+        online_case("cohort_male_30_30_1", record_split(120, 7, "planted-linear", "male"), 30, 7, [1, 10, 100, 1000]),
+        online_case("cohort_female_30_30_1", record_split(120, 7, "random", "female"), 30, 7, [1, 10, 100, 1000]),
+        online_case("wide_33_256_1", matrix_split(200, 33, 3), 256, 5, [1, 10, 50])),
+    "small": small_backend_case,
+    "trainer": trainer_case,
+    "generators": generator_digests,
+    "normalize": normalize_cases,
+}
+
 if __name__ == "__main__":
-    online_case("paper_33_33_1", matrix_split(120, 33, 7), 33, 7, [1, 10, 100, 1000])
-    online_case("cohort_male_30_30_1", record_split(120, 7, "planted-linear", "male"), 30, 7, [1, 10, 100, 1000])
-    online_case("cohort_female_30_30_1", record_split(120, 7, "random", "female"), 30, 7, [1, 10, 100, 1000])
-    online_case("wide_33_256_1", matrix_split(200, 33, 3), 256, 5, [1, 10, 50])
-    small_backend_case()
-    trainer_case()
-    generator_digests()
+    # no arguments: every fixture; otherwise only the named groups
+    for name in sys.argv[1:] or list(CASES):
+        CASES[name]()

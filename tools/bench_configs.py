@@ -237,6 +237,30 @@ def eval_rate(L, peak):
     return {"config": "eval_counts, 1M rows x 33", **out}
 
 
+def norm_rate(L, peak, rows=67_108_864, D=33):
+    """Device min-max normalisation at config 4's size (64Mi x 33 f32, 8.9 GB): fit
+    (reads X) and apply (reads X, writes Y) against the measured HBM copy peak."""
+    dev = torch.device("cuda")
+    X = torch.rand((rows, D), device=dev) * 100.0
+    Y = torch.empty_like(X)
+    mn = torch.empty(D, device=dev)
+    mx = torch.empty(D, device=dev)
+    st = torch.cuda.current_stream().cuda_stream
+    fit = lambda: _lib.check(L.glx_minmax_fit(X.data_ptr(), rows, D, mn.data_ptr(), mx.data_ptr(), st))
+    app = lambda: _lib.check(L.glx_minmax_apply(X.data_ptr(), rows, D, mn.data_ptr(), mx.data_ptr(), Y.data_ptr(), st))
+    fit()
+    app()
+    t_fit = timed(fit, 5)
+    t_app = timed(app, 5)
+    pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    hbm = pk.get("hbm_gbs", 6545.9)
+    b = rows * D * 4
+    return {"config": f"min-max normalisation, {rows} x {D} f32 (config 4 rows)",
+            "fit_ms": t_fit, "fit_gbs": b / (t_fit * 1e-3) / 1e9, "fit_frac_hbm": b / (t_fit * 1e-3) / 1e9 / hbm,
+            "apply_ms": t_app, "apply_gbs": 2 * b / (t_app * 1e-3) / 1e9,
+            "apply_frac_hbm": 2 * b / (t_app * 1e-3) / 1e9 / hbm, "hbm_peak_gbs": hbm}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="1,3,4,eval")
@@ -246,7 +270,7 @@ def main():
     peak = fp32_peak(L)
     results = {"fp32_peak_tflops": peak}
     for w in args.which.split(","):
-        fn = {"1": config1, "3": config3, "4": config4_1gpu, "5": config5, "eval": eval_rate}[w]
+        fn = {"1": config1, "3": config3, "4": config4_1gpu, "5": config5, "eval": eval_rate, "norm": norm_rate}[w]
         r = fn(L, peak)
         results[f"config_{w}"] = r
         print(json.dumps({w: r}), flush=True)
