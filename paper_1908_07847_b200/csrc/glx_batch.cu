@@ -706,6 +706,7 @@ cudaError_t launch_batch_prep(const BatchGeom& g, const float* W1, const float* 
 
 cudaError_t launch_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
                              float* Xp, cudaStream_t st, const float* col_min, const float* col_max) {
+    if (pack_tiled_ok(X, T, labels, Xp, D, LD)) return launch_pack_tiled(X, T, labels, N, D, LD, col_min, col_max, Xp, st);
     const int64_t total = N * LD;
     int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
     if (blocks < 1) blocks = 1;

@@ -285,6 +285,116 @@ __global__ void __launch_bounds__(256) minmax_tiled_kernel(const float* X, float
     }
 }
 
+// rows per packing tile: ~32 KB of input + output per stage, a multiple of 16
+// so the u8 label slice of a tile stays 16-byte aligned
+__host__ __device__ inline int pack_tile_rows(int D, int LD) {
+    const int r = (kNormTileFloats / (D + LD + 1)) & ~15;
+    return r < 16 ? 16 : r;
+}
+
+// Batch row packing (glx_batch.cu layout [x_0..x_{D-1}, 1, target, 0..] of LD
+// floats), optionally min-max normalising x: feature tiles arrive by bulk copy,
+// the packed tile is built in shared memory by (packed column, row phase)
+// threads and leaves by bulk store. Targets come from T (f32) or labels (u8).
+__global__ void __launch_bounds__(256) pack_tiled_kernel(const float* __restrict__ X, const float* __restrict__ T,
+                                                         const uint8_t* __restrict__ labels, int64_t N, int D, int LD,
+                                                         const float* __restrict__ col_min,
+                                                         const float* __restrict__ col_max, float* __restrict__ Xp) {
+    extern __shared__ __align__(128) unsigned char nsm[];
+    const int R = pack_tile_rows(D, LD);
+    float* in_ring = reinterpret_cast<float*>(nsm);
+    float* out_ring = in_ring + (size_t)kNormStages * R * D;
+    float* tgt_ring = out_ring + (size_t)kNormStages * R * LD;  // R floats or R label bytes per stage
+    uint64_t* full = reinterpret_cast<uint64_t*>(tgt_ring + (size_t)kNormStages * R);
+    const int t = threadIdx.x;
+    const ColMap cm(t, LD);
+    const int64_t n_tiles = N / R;
+    if (t == 0) {
+        for (int s = 0; s < kNormStages; s++) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int i = cm.c;  // packed column of this thread (LD < 256 always: D <= 250)
+    float lo = 0.f, hi = 0.f;
+    if (col_min && cm.active && i < D) {
+        lo = col_min[i];
+        hi = col_max[i];
+    }
+    // the tile's features and its slice of targets (f32) or labels (u8) arrive on one barrier
+    const uint32_t tbytes = T ? (uint32_t)R * 4 : labels ? (uint32_t)R : 0u;
+    auto issue = [&](int64_t tile, int s) {
+        const uint32_t bytes = (uint32_t)R * D * 4;
+        mbar_arrive_expect_tx(&full[s], bytes + tbytes);
+        bulk_g2s(in_ring + (size_t)s * R * D, X + tile * R * D, bytes, &full[s]);
+        if (T) bulk_g2s(tgt_ring + (size_t)s * R, T + tile * R, tbytes, &full[s]);
+        else if (labels) bulk_g2s(tgt_ring + (size_t)s * R, labels + tile * R, tbytes, &full[s]);
+    };
+    auto target = [&](const float* tg, int64_t r_local, int64_t r) -> float {  // tg: staged slice or null
+        if (T) return tg ? tg[r_local] : T[r];
+        if (labels) return tg ? (float)reinterpret_cast<const uint8_t*>(tg)[r_local] : (float)labels[r];
+        return 0.0f;
+    };
+    auto value = [&](const float* xrow, const float* tg, int64_t r_local, int64_t r) -> float {
+        if (i < D) return col_min ? minmax_norm(xrow[i], lo, hi) : xrow[i];
+        if (i == D) return 1.0f;
+        if (i == D + 1) return target(tg, r_local, r);
+        return 0.0f;
+    };
+    if (t == 0) {
+        int s = 0;
+        for (int64_t tile = blockIdx.x; tile < n_tiles && s < kNormStages; tile += gridDim.x, s++) issue(tile, s);
+    }
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, it++) {
+        const int s = it % kNormStages;
+        mbar_wait(&full[s], (it / kNormStages) & 1);
+        const float* ip = in_ring + (size_t)s * R * D;
+        const float* tg = tgt_ring + (size_t)s * R;
+        float* op = out_ring + (size_t)s * R * LD;
+        if (cm.active) {
+#pragma unroll 4
+            for (int r = cm.ph; r < R; r += cm.P) op[r * LD + i] = value(ip + r * D, tg, r, tile * R + r);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();  // tile consumed: in slot s may be refilled, out slot s is complete
+        if (t == 0) {
+            bulk_s2g(Xp + tile * R * LD, op, (uint32_t)R * LD * 4);
+            const int64_t nxt = tile + (int64_t)kNormStages * gridDim.x;
+            if (nxt < n_tiles) issue(nxt, s);
+            // the out slot written in iteration it + 2 is the one stored at it + 2 - S:
+            // leave at most S - 2 stores pending, so it is free; the next
+            // iteration's __syncthreads orders this wait before those writes
+            asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kNormStages - 2) : "memory");
+        }
+    }
+    if (blockIdx.x == gridDim.x - 1 && cm.active) {  // ragged tail from global memory
+        for (int64_t r = n_tiles * R + cm.ph; r < N; r += cm.P) Xp[r * LD + i] = value(X + r * D, nullptr, 0, r);
+    }
+    if (t == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static size_t pack_smem(int D, int LD) {
+    return (size_t)kNormStages * pack_tile_rows(D, LD) * (D + LD + 1) * 4 + 64;
+}
+
+bool pack_tiled_ok(const void* X, const void* T, const void* labels, const void* Xp, int D, int LD) {
+    return LD < 256 && pack_smem(D, LD) <= 113 * 1024 && ((uintptr_t)X & 15) == 0 && ((uintptr_t)Xp & 15) == 0 &&
+           ((uintptr_t)T & 15) == 0 && ((uintptr_t)labels & 15) == 0;
+}
+
+cudaError_t launch_pack_tiled(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
+                              const float* col_min, const float* col_max, float* Xp, cudaStream_t st) {
+    const size_t smem = pack_smem(D, LD);
+    cudaError_t e = cudaFuncSetAttribute(pack_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t tiles = N / pack_tile_rows(D, LD);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, 2 * sms));
+    pack_tiled_kernel<<<grid, 256, smem, st>>>(X, T, labels, N, D, LD, col_min, col_max, Xp);
+    return cudaGetLastError();
+}
+
 static size_t norm_smem(int D) {
     const size_t ring = (size_t)kNormStages * norm_tile_rows(D) * D * 4;
     const size_t red = (size_t)2 * 256 * kNormMaxColsPerThread * 4;

@@ -72,6 +72,10 @@ bool batch_geometry(int64_t N, int D, int H, int n_sms, bool train, BatchGeom* g
 cudaError_t launch_pack_rows(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
                              float* Xp, cudaStream_t st, const float* col_min = nullptr,
                              const float* col_max = nullptr);
+// TMA-staged packing (glx_data.cu), used by launch_pack_rows when aligned
+bool pack_tiled_ok(const void* X, const void* T, const void* labels, const void* Xp, int D, int LD);
+cudaError_t launch_pack_tiled(const float* X, const float* T, const uint8_t* labels, int64_t N, int D, int LD,
+                              const float* col_min, const float* col_max, float* Xp, cudaStream_t st);
 // min-max normalisation (glx_data.cu); work = 2*D ints
 cudaError_t launch_minmax_fit(const float* X, int64_t N, int D, int* work, float* col_min, float* col_max,
                               cudaStream_t st);

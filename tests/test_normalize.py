@@ -110,3 +110,39 @@ def test_normalize_column_mismatch_raises(gpu):
     st = g.NormStats(col_min=np.zeros(3, np.float32), col_max=np.ones(3, np.float32))
     with pytest.raises(g.ShapeError):
         g.normalize_apply(_ds(np.zeros((4, 5), np.float32)), st)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("N,D", [(1, 1), (223, 7), (1000, 33), (4099, 33), (37, 250), (100_003, 15)])
+def test_pack_rows_layout(gpu, N, D):
+    """glx_pack_rows / glx_pack_rows_minmax: row r = [x_r (normalised or not), 1, target, 0...]
+    of glx_packed_ld(D) floats, for ragged N (tile tails) and odd D."""
+    import torch
+
+    import paper_1908_07847_b200._lib as L
+
+    rng = np.random.default_rng(N + D)
+    x = (rng.normal(size=(N, D)) * 9).astype(np.float32)
+    lab = (rng.random(N) < 0.5).astype(np.uint8)
+    t = lab.astype(np.float32) * 0.75
+    lib = L.load()
+    ld = int(lib.glx_packed_ld(D))
+    st = torch.cuda.current_stream().cuda_stream
+    X, T, Lb = torch.from_numpy(x).cuda(), torch.from_numpy(t).cuda(), torch.from_numpy(lab).cuda()
+    mn, mx = O.normalize_fit(x)
+    dmn, dmx = torch.from_numpy(mn).cuda(), torch.from_numpy(mx).cuda()
+    for norm in (False, True):
+        for use_t in (True, False):
+            Xp = torch.full((N, ld), float("nan"), device="cuda")
+            if norm:
+                L.check(lib.glx_pack_rows_minmax(X.data_ptr(), T.data_ptr() if use_t else None,
+                                                 None if use_t else Lb.data_ptr(), N, D, dmn.data_ptr(),
+                                                 dmx.data_ptr(), Xp.data_ptr(), st))
+            else:
+                L.check(lib.glx_pack_rows(X.data_ptr(), T.data_ptr() if use_t else None,
+                                          None if use_t else Lb.data_ptr(), N, D, Xp.data_ptr(), st))
+            want = np.zeros((N, ld), np.float32)
+            want[:, :D] = O.normalize_apply(x, mn, mx) if norm else x
+            want[:, D] = 1.0
+            want[:, D + 1] = t if use_t else lab
+            assert Xp.cpu().numpy().tobytes() == want.tobytes(), (norm, use_t)

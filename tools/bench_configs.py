@@ -252,13 +252,26 @@ def norm_rate(L, peak, rows=67_108_864, D=33):
     app()
     t_fit = timed(fit, 5)
     t_app = timed(app, 5)
+    ld = int(L.glx_packed_ld(D))
+    T = torch.rand(rows, device=dev)
+    Xp = torch.empty((rows, ld), device=dev)
+    pack = lambda: _lib.check(L.glx_pack_rows(X.data_ptr(), T.data_ptr(), None, rows, D, Xp.data_ptr(), st))
+    packn = lambda: _lib.check(L.glx_pack_rows_minmax(X.data_ptr(), T.data_ptr(), None, rows, D, mn.data_ptr(),
+                                                     mx.data_ptr(), Xp.data_ptr(), st))
+    pack()
+    packn()
+    t_pack = timed(pack, 5)
+    t_packn = timed(packn, 5)
+    pb = rows * (D * 4 + 4 + ld * 4)
     pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     hbm = pk.get("hbm_gbs", 6545.9)
     b = rows * D * 4
     return {"config": f"min-max normalisation, {rows} x {D} f32 (config 4 rows)",
             "fit_ms": t_fit, "fit_gbs": b / (t_fit * 1e-3) / 1e9, "fit_frac_hbm": b / (t_fit * 1e-3) / 1e9 / hbm,
             "apply_ms": t_app, "apply_gbs": 2 * b / (t_app * 1e-3) / 1e9,
-            "apply_frac_hbm": 2 * b / (t_app * 1e-3) / 1e9 / hbm, "hbm_peak_gbs": hbm}
+            "apply_frac_hbm": 2 * b / (t_app * 1e-3) / 1e9 / hbm, "hbm_peak_gbs": hbm,
+            "pack_rows_ms": t_pack, "pack_rows_gbs": pb / (t_pack * 1e-3) / 1e9,
+            "pack_rows_minmax_ms": t_packn, "pack_rows_minmax_gbs": pb / (t_packn * 1e-3) / 1e9}
 
 
 def main():
