@@ -335,16 +335,52 @@ def peaks():
     return json.loads(p.read_text()) if p.exists() else {}
 
 
+class SuiteCpuLegs:
+    """CPU reference legs of the secondary-config suite (tools/bench_configs.py):
+    the C restatement of the reference engines (oracle/, pinned byte-identical to
+    kernels.train_segment_seq / _par / eval_counts), timed beside the device."""
+
+    def __init__(self):
+        from oracle import oracle as O
+
+        self.O = O
+
+    def online_seq(self, *a):
+        self.O.train_online_seq(*a)
+
+    def online_par(self, *a):
+        self.O.train_online_par(*a)
+
+    def sweep(self, *a):
+        self.O.train_sweep(*a)
+
+    def eval_counts(self, *a):
+        return self.O.eval_counts(*a)
+
+
+def run_suite(which: str, out: str | None):
+    sys.path.insert(0, str(ROOT / "tools"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import bench_configs
+
+    bench_configs.run_suite(which, out, SuiteCpuLegs())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=600)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--suite", default=None,
+                    help="secondary configurations instead of the headline, e.g. 1,3,4,5,eval,norm")
+    ap.add_argument("--out", default=None, help="with --suite: write the results JSON here")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    if args.impl == "reference":
+    if args.suite:
+        run_suite(args.suite, args.out)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_gpu(args)

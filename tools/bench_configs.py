@@ -1,8 +1,10 @@
-"""Per-config measurements beyond bench.py's headline (eval).
+"""Per-config device measurements beyond bench.py's headline (SURVEY.md 8(d)
+configs 1, 3, 4, 5, eval, normalisation).
 
-Prints one JSON object per config; writes them to profiles/ when --out is given.
-Device timings use CUDA events on the launching stream; CPU reference timings use
-the C ports of the reference engines (oracle/, pinned byte-identical).
+Device timings use CUDA events on the launching stream. The CPU reference
+numbers beside them come from `cpu` legs passed in by `python bench.py --suite`
+(bench.py owns the reference-engine timing); run directly, this module reports
+device numbers only. Prints one JSON object per config; --out writes them all.
 """
 
 from __future__ import annotations
@@ -25,7 +27,6 @@ import torch  # noqa: E402
 import paper_1908_07847_b200 as g  # noqa: E402
 from paper_1908_07847_b200 import _lib, dp  # noqa: E402
 from paper_1908_07847_b200.sweep import pack_pool  # noqa: E402
-from oracle import oracle as O  # noqa: E402
 
 
 def f_train(d, h, k=1):
@@ -61,7 +62,7 @@ def cpu_rate(fn, rows, budget_s=5.0):
     return rows * ep / (time.perf_counter() - t0)
 
 
-def config1(L, peak):
+def config1(L, peak, cpu=None):
     """Paper shape online SGD, one network (33-33-1, 90 rows) + both 30-30-1 cohorts."""
     from conftest import load_case  # fixture data produced by the reference
 
@@ -86,17 +87,18 @@ def config1(L, peak):
             run()
             ms = timed(run)
             res[f"gpu_{numerics}_sample_epochs_per_s"] = N * E / (ms * 1e-3)
-        w1 = net.w_ih2d.copy()
-        w2 = net.w_ho2d.copy()
-        res["cpu_seq_sample_epochs_per_s"] = cpu_rate(lambda e: O.train_online_seq(w1, w2, x, t, e, 0.1), N)
-        res["cpu_par_sample_epochs_per_s"] = cpu_rate(lambda e: O.train_online_par(w1, w2, x, t, e, 0.1), N)
-        res["cpu_cores"] = os.cpu_count()
+        if cpu is not None:
+            w1 = net.w_ih2d.copy()
+            w2 = net.w_ho2d.copy()
+            res["cpu_seq_sample_epochs_per_s"] = cpu_rate(lambda e: cpu.online_seq(w1, w2, x, t, e, 0.1), N)
+            res["cpu_par_sample_epochs_per_s"] = cpu_rate(lambda e: cpu.online_par(w1, w2, x, t, e, 0.1), N)
+            res["cpu_cores"] = os.cpu_count()
         res["note"] = "latency-bound: rows are serial in online SGD; one network uses one CTA"
         out.append(res)
     return out
 
 
-def config3(L, peak, epochs=200):
+def config3(L, peak, cpu=None, epochs=200):
     """4096 networks (64 widths 8..512 x 64 seeds), paper 90-row split, online fp32."""
     from conftest import load_case
 
@@ -124,12 +126,14 @@ def config3(L, peak, epochs=200):
         res[f"gpu_{numerics}_tflops"] = flops / (ms * 1e-3) / 1e12
         res[f"gpu_{numerics}_frac_fp32_peak"] = flops / (ms * 1e-3) / 1e12 / peak
         res[f"gpu_{numerics}_ms"] = ms
+    if cpu is None:
+        return res
     # CPU: the reference engine on a cost-stratified sample of networks, extrapolated by flops
     idx = list(range(0, 4096, 128))
     sub = [nets[i].copy() for i in idx]
     spool, sH, soff = pack_pool(sub)
     t0 = time.perf_counter()
-    O.train_sweep(sH, soff, spool, x, t, 20, 0.1, os.cpu_count())
+    cpu.sweep(sH, soff, spool, x, t, 20, 0.1, os.cpu_count())
     dt = time.perf_counter() - t0
     sub_flops = sum(f_train(D, int(h)) for h in sH) * N * 20
     cpu_tflops = sub_flops / dt / 1e12
@@ -140,7 +144,7 @@ def config3(L, peak, epochs=200):
     return res
 
 
-def config4_1gpu(L, peak, rows=67_108_864, epochs=5):
+def config4_1gpu(L, peak, cpu=None, rows=67_108_864, epochs=5):
     """64Mi rows, 33->256->1, full batch, on one GPU (the DP config's per-run total)."""
     dev = torch.device("cuda")
     D, H = 33, 256
@@ -169,7 +173,7 @@ def config4_1gpu(L, peak, rows=67_108_864, epochs=5):
             "data_gen_and_pack_s": gen_s}
 
 
-def config5(L, peak, rows=16_777_216, epochs=3):
+def config5(L, peak, cpu=None, rows=16_777_216, epochs=3):
     """Wide 1024 -> 1024 -> 16 on 16Mi rows, full batch, tcgen05 BF16 (device-generated rows)."""
     from paper_1908_07847_b200 import wide
 
@@ -202,7 +206,7 @@ def config5(L, peak, rows=16_777_216, epochs=3):
                     "frac_bf16_peak is against MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"}
 
 
-def eval_rate(L, peak):
+def eval_rate(L, peak, cpu=None):
     x, l = g.synthetic_arrays(1_000_000, 33, 0, "planted-linear")
     out = {}
     dev = torch.device("cuda")
@@ -230,14 +234,15 @@ def eval_rate(L, peak):
         f_eval = 2 * H * 34 + 2 * (H + 1)
         out[f"H{H}"] = {"ref64_rows_per_s": x.shape[0] / (ms * 1e-3), "fp32_rows_per_s": x.shape[0] / (ms2 * 1e-3),
                         "fp32_frac_fp32_peak": x.shape[0] * f_eval / (ms2 * 1e-3) / 1e12 / peak}
-        w1h, w2h = net.w_ih2d.copy(), net.w_ho2d.copy()
-        t0 = time.perf_counter()
-        O.eval_counts(w1h, w2h, x[:100_000], l[:100_000])
-        out[f"H{H}"]["cpu_rows_per_s_1core"] = 100_000 / (time.perf_counter() - t0)
+        if cpu is not None:
+            w1h, w2h = net.w_ih2d.copy(), net.w_ho2d.copy()
+            t0 = time.perf_counter()
+            cpu.eval_counts(w1h, w2h, x[:100_000], l[:100_000])
+            out[f"H{H}"]["cpu_rows_per_s_1core"] = 100_000 / (time.perf_counter() - t0)
     return {"config": "eval_counts, 1M rows x 33", **out}
 
 
-def norm_rate(L, peak, rows=67_108_864, D=33):
+def norm_rate(L, peak, cpu=None, rows=67_108_864, D=33):
     """Device min-max normalisation at config 4's size (64Mi x 33 f32, 8.9 GB): fit
     (reads X) and apply (reads X, writes Y) against the measured HBM copy peak."""
     dev = torch.device("cuda")
@@ -274,21 +279,28 @@ def norm_rate(L, peak, rows=67_108_864, D=33):
             "pack_rows_minmax_ms": t_packn, "pack_rows_minmax_gbs": pb / (t_packn * 1e-3) / 1e9}
 
 
+SUITE = {"1": config1, "3": config3, "4": config4_1gpu, "5": config5, "eval": eval_rate, "norm": norm_rate}
+
+
+def run_suite(which: str, out: str | None = None, cpu=None) -> dict:
+    L = _lib.load()
+    peak = fp32_peak(L)
+    results = {"fp32_peak_tflops": peak}
+    for w in which.split(","):
+        r = SUITE[w](L, peak, cpu)
+        results[f"config_{w}"] = r
+        print(json.dumps({w: r}), flush=True)
+    if out:
+        Path(out).write_text(json.dumps(results, indent=1))
+    return results
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="1,3,4,eval")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
-    L = _lib.load()
-    peak = fp32_peak(L)
-    results = {"fp32_peak_tflops": peak}
-    for w in args.which.split(","):
-        fn = {"1": config1, "3": config3, "4": config4_1gpu, "5": config5, "eval": eval_rate, "norm": norm_rate}[w]
-        r = fn(L, peak)
-        results[f"config_{w}"] = r
-        print(json.dumps({w: r}), flush=True)
-    if args.out:
-        Path(args.out).write_text(json.dumps(results, indent=1))
+    run_suite(args.which, args.out)
 
 
 if __name__ == "__main__":
