@@ -69,6 +69,24 @@ int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, co
                                 int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr,
                                 double* stats_hist, int32_t device, int32_t flags);
 
+/* One trainer checkpoint in one call (replacing the
+ * segment + 2x eval_counts + weights_finite sequence of trainer.py:152-163):
+ * train `epochs` (mode 0 online SGD as glx_run_train_segment, 1 full batch
+ * as glx_run_train_segment_batch), then on the device, on the same stream and
+ * without a weight round trip: the finiteness test of the new weights and the
+ * exact (reference-order f64) confusion counts of the train rows (labels =
+ * their u8 labels; the rows are already resident) and of the test rows.
+ * counts8 = train (tp, tn, fp, fn) then test (tp, tn, fp, fn); loss2 = the two
+ * loss sums; finite = 1 iff every weight is finite; train_seconds = the call's
+ * wall time minus the evaluation's device time. The weights are copied back
+ * as by the segment calls. With GLX_FLAG_CACHE_INPUTS the train and test rows
+ * stay resident across checkpoint calls (keyed on the host pointers). */
+int glx_run_train_segment_eval(float* w_ih, float* w_ho, const float* feats, const float* targets,
+                               const uint8_t* labels, int64_t rows, const float* test_feats,
+                               const uint8_t* test_labels, int64_t test_rows, int32_t input_dim, int32_t hidden_dim,
+                               int64_t epochs, double lr, int32_t numerics, int32_t mode, int32_t device,
+                               int32_t flags, int64_t* counts8, double* loss2, int32_t* finite, double* train_seconds);
+
 /* Drop-in for kernels.eval_counts (kernels.py:352-375) plus the loss sum.
  * counts4 = (tp, tn, fp, fn) for output_dim 1, (correct, wrong, 0, 0) for
  * output_dim > 1 (argmax). labels: rows u8. */

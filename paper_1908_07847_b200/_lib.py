@@ -44,6 +44,8 @@ SIGNATURES = {
     "glx_sm_count": (_int, [_int]),
     "glx_run_train_segment": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _i32, _i32, _i32]),
     "glx_run_train_segment_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _vp, _i32, _i32]),
+    "glx_run_train_segment_eval": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _i32,
+                                          _i32, _i32, _i32, _vp, _vp, _vp, _vp]),
     "glx_eval_counts": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _i32]),
     "glx_cache_clear": (None, []),
     "glx_train_online": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _i32, _vp]),

@@ -150,6 +150,57 @@ def run_train_segment_batch(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.
         sp, kind.device, _cache_flag(cache_inputs, X, T)))
 
 
+@dataclass(frozen=True)
+class CheckpointEval:
+    """Result of run_train_segment_eval: exact confusion counts (tp, tn, fp, fn)
+    of both splits at the segment's final weights, their loss sums, whether every
+    weight is finite, and the training part's wall time."""
+
+    train_counts: tuple[int, int, int, int]
+    test_counts: tuple[int, int, int, int]
+    train_loss: float
+    test_loss: float
+    finite: bool
+    train_seconds: float
+
+
+def run_train_segment_eval(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, targets: np.ndarray,
+                           labels: np.ndarray, test_feats2d: np.ndarray, test_labels: np.ndarray, epochs: int,
+                           lr: float, kind: BackendKind, *, mode: str = ONLINE,
+                           cache_inputs: bool = False) -> CheckpointEval:
+    """One trainer checkpoint in one device call: `epochs` of
+    training (online SGD or full batch), then the finiteness test and the exact
+    train/test confusion counts on the device, without a host round trip of the
+    weights in between. Weights are updated in place like run_train_segment."""
+    _check_inputs(w_ih2d, feats2d, targets)
+    D, H = _check_weights(w_ih2d, w_ho2d)
+    if labels.shape[0] != feats2d.shape[0]:
+        raise ShapeError("labels length must match feature rows")
+    if test_feats2d.ndim != 2 or test_feats2d.shape[1] != D or test_labels.shape[0] != test_feats2d.shape[0]:
+        raise ShapeError(f"test rows must be (n, {D}) with n labels")
+    if mode not in (ONLINE, BATCH):
+        raise ValidationError(f"mode must be {ONLINE!r} or {BATCH!r}, got {mode!r}")
+    L = _lib.load()
+    X = feats2d if (feats2d.dtype == np.float32 and feats2d.flags.c_contiguous) else _f32c(feats2d)
+    T = targets if (targets.dtype == np.float32 and targets.flags.c_contiguous) else _f32c(targets)
+    Y = labels if (labels.dtype == np.uint8 and labels.flags.c_contiguous) else np.ascontiguousarray(labels, np.uint8)
+    VX = test_feats2d if (test_feats2d.dtype == np.float32 and test_feats2d.flags.c_contiguous) else _f32c(test_feats2d)
+    VY = (test_labels if (test_labels.dtype == np.uint8 and test_labels.flags.c_contiguous)
+          else np.ascontiguousarray(test_labels, np.uint8))
+    counts = np.zeros(8, dtype=np.int64)
+    loss = np.zeros(2, dtype=np.float64)
+    finite = np.zeros(1, dtype=np.int32)
+    secs = np.zeros(1, dtype=np.float64)
+    _lib.check(L.glx_run_train_segment_eval(
+        _lib.ptr(w_ih2d), _lib.ptr(w_ho2d), _lib.ptr(X), _lib.ptr(T), _lib.ptr(Y), X.shape[0], _lib.ptr(VX),
+        _lib.ptr(VY), VX.shape[0], D, H, int(epochs), float(lr), _lib.NUMERICS[kind.numerics],
+        0 if mode == ONLINE else 1, kind.device, _cache_flag(cache_inputs, X, T, Y, VX, VY), _lib.ptr(counts),
+        _lib.ptr(loss), _lib.ptr(finite), _lib.ptr(secs)))
+    c = [int(v) for v in counts]
+    return CheckpointEval(tuple(c[:4]), tuple(c[4:]), float(loss[0]), float(loss[1]), bool(finite[0]),
+                          float(secs[0]))
+
+
 def eval_counts_loss(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, labels: np.ndarray,
                      kind: BackendKind | None = None) -> tuple[tuple[int, int, int, int], float]:
     """((tp, tn, fp, fn), sum of 0.5*(t-o)^2) with poor (label 1) as the positive class."""

@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -133,6 +134,11 @@ struct HostState {
     std::mutex mu;
     cudaStream_t stream = nullptr;
     DevBuf w1, w2, x, t, lab, xp, stats, cnt, loss, flag, ex, exp_;
+    DevBuf tlab, vx, vlab;  // checkpoint evaluation: train labels, test rows and labels
+    const void* key_tlab = nullptr;
+    const void* key_vx = nullptr;
+    const void* key_vlab = nullptr;
+    size_t bytes_vx = 0;
     const void* key_x = nullptr;
     size_t bytes_x = 0;
     const void* key_t = nullptr;
@@ -333,7 +339,8 @@ void glx_cache_clear(void) {
     for (auto& h : g_host) {
         std::lock_guard<std::mutex> lk(h.mu);
         h.key_x = h.key_t = h.key_xp = nullptr;
-        h.bytes_x = h.bytes_t = 0;
+        h.key_tlab = h.key_vx = h.key_vlab = nullptr;
+        h.bytes_x = h.bytes_t = h.bytes_vx = 0;
     }
 }
 
@@ -530,6 +537,24 @@ static int stage_inputs(HostState* hs, const float* feats, size_t xbytes, const 
     return GLX_OK;
 }
 
+// online segment on the host state's device buffers (weights uploaded, not downloaded)
+static int online_segment_dev(HostState* hs, const float* w_ih, const float* w_ho, const float* feats,
+                              const float* targets, int64_t rows, int32_t input_dim, int32_t hidden_dim,
+                              int64_t epochs, double lr, int32_t numerics, int32_t flags, cudaStream_t st) {
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
+    GLX_CK(hs->w1.ensure(n1 * 4));
+    GLX_CK(hs->w2.ensure(n2 * 4));
+    int rc = stage_inputs(hs, feats, (size_t)rows * input_dim * 4, targets, (size_t)rows * 4,
+                          (flags & GLX_FLAG_CACHE_INPUTS) != 0, st);
+    if (rc) return rc;
+    GLX_CK(cudaMemcpyAsync(hs->w1.p, w_ih, n1 * 4, cudaMemcpyHostToDevice, st));
+    GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
+    if (epochs == 0) return GLX_OK;
+    std::vector<NetReq> nets{{hs->w1.as<float>(), hs->w2.as<float>(), hidden_dim, 0}};
+    return run_online(nets, hs->x.as<float>(), hs->t.as<float>(), rows, input_dim, epochs, lr, numerics == GLX_REF64,
+                      st);
+}
+
 int glx_run_train_segment(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
                           int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr, int32_t numerics,
                           int32_t device, int32_t flags) {
@@ -539,16 +564,8 @@ int glx_run_train_segment(float* w_ih, float* w_ho, const float* feats, const fl
     if (rows == 0 || epochs == 0) return GLX_OK;
     HOST_PROLOGUE(device);
     const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
-    GLX_CK(hs->w1.ensure(n1 * 4));
-    GLX_CK(hs->w2.ensure(n2 * 4));
-    rc = stage_inputs(hs, feats, (size_t)rows * input_dim * 4, targets, (size_t)rows * 4,
-                      (flags & GLX_FLAG_CACHE_INPUTS) != 0, st);
-    if (rc) return rc;
-    GLX_CK(cudaMemcpyAsync(hs->w1.p, w_ih, n1 * 4, cudaMemcpyHostToDevice, st));
-    GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
-    std::vector<NetReq> nets{{hs->w1.as<float>(), hs->w2.as<float>(), hidden_dim, 0}};
-    rc = run_online(nets, hs->x.as<float>(), hs->t.as<float>(), rows, input_dim, epochs, lr, numerics == GLX_REF64,
-                    st);
+    rc = online_segment_dev(hs, w_ih, w_ho, feats, targets, rows, input_dim, hidden_dim, epochs, lr, numerics, flags,
+                            st);
     if (rc) return rc;
     GLX_CK(cudaMemcpyAsync(w_ih, hs->w1.p, n1 * 4, cudaMemcpyDeviceToHost, st));
     GLX_CK(cudaMemcpyAsync(w_ho, hs->w2.p, n2 * 4, cudaMemcpyDeviceToHost, st));
@@ -556,18 +573,15 @@ int glx_run_train_segment(float* w_ih, float* w_ho, const float* feats, const fl
     return GLX_OK;
 }
 
-int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
-                                int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr,
-                                double* stats_hist, int32_t device, int32_t flags) {
-    int rc = check_dims(rows, input_dim, hidden_dim);
-    if (rc) return rc;
-    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0, got %lld", (long long)epochs);
-    if (rows == 0 || epochs == 0) return GLX_OK;
-    HOST_PROLOGUE(device);
+// full-batch segment on the host state's device buffers (weights uploaded, not downloaded)
+static int batch_segment_dev(HostState* hs, const float* w_ih, const float* w_ho, const float* feats,
+                             const float* targets, int64_t rows, int32_t input_dim, int32_t hidden_dim,
+                             int64_t epochs, double lr, bool want_stats, int32_t flags, cudaStream_t st) {
     const int ld = glx_packed_ld(input_dim);
     const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
     GLX_CK(hs->w1.ensure(n1 * 4));
     GLX_CK(hs->w2.ensure(n2 * 4));
+    int rc = GLX_OK;
     const bool cache = (flags & GLX_FLAG_CACHE_INPUTS) != 0;
     const bool packed_hit = cache && hs->key_xp == feats && hs->key_x == feats && hs->key_t == targets &&
                             hs->bytes_x == (size_t)rows * input_dim * 4;
@@ -579,13 +593,27 @@ int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, co
                                     hs->xp.as<float>(), st));
         if (cache) hs->key_xp = feats;
     }
-    GLX_CK(hs->stats.ensure((size_t)5 * epochs * sizeof(double)));
+    GLX_CK(hs->stats.ensure((size_t)5 * std::max<int64_t>(epochs, 1) * sizeof(double)));
     GLX_CK(hs->flag.ensure(sizeof(int)));
     GLX_CK(cudaMemsetAsync(hs->flag.p, 0, sizeof(int), st));
     GLX_CK(cudaMemcpyAsync(hs->w1.p, w_ih, n1 * 4, cudaMemcpyHostToDevice, st));
     GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
-    rc = batch_train_impl(hs->w1.as<float>(), hs->w2.as<float>(), hs->xp.as<float>(), rows, input_dim, hidden_dim,
-                          epochs, lr, stats_hist ? hs->stats.as<double>() : nullptr, hs->flag.as<int>(), st);
+    if (epochs == 0) return GLX_OK;
+    return batch_train_impl(hs->w1.as<float>(), hs->w2.as<float>(), hs->xp.as<float>(), rows, input_dim, hidden_dim,
+                            epochs, lr, want_stats ? hs->stats.as<double>() : nullptr, hs->flag.as<int>(), st);
+}
+
+int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
+                                int32_t input_dim, int32_t hidden_dim, int64_t epochs, double lr,
+                                double* stats_hist, int32_t device, int32_t flags) {
+    int rc = check_dims(rows, input_dim, hidden_dim);
+    if (rc) return rc;
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0, got %lld", (long long)epochs);
+    if (rows == 0 || epochs == 0) return GLX_OK;
+    HOST_PROLOGUE(device);
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
+    rc = batch_segment_dev(hs, w_ih, w_ho, feats, targets, rows, input_dim, hidden_dim, epochs, lr,
+                           stats_hist != nullptr, flags, st);
     if (rc) return rc;
     GLX_CK(cudaMemcpyAsync(w_ih, hs->w1.p, n1 * 4, cudaMemcpyDeviceToHost, st));
     GLX_CK(cudaMemcpyAsync(w_ho, hs->w2.p, n2 * 4, cudaMemcpyDeviceToHost, st));
@@ -649,6 +677,95 @@ int glx_eval_counts(const float* w_ih, const float* w_ho, const float* feats, co
     GLX_CK(cudaStreamSynchronize(st));
     if (loss_sum) *loss_sum = hl[0];
     for (int q = 0; q < 4; q++) counts4[q] = (int64_t)llround(hl[1 + q]);
+    return GLX_OK;
+}
+
+// upload a host buffer into `buf` unless (key, bytes) says it is resident
+static int stage_buf(DevBuf& buf, const void*& key, size_t* key_bytes, const void* src, size_t bytes, bool cache,
+                     cudaStream_t st) {
+    if (cache && key == src && buf.p && (!key_bytes || *key_bytes == bytes)) return GLX_OK;
+    key = nullptr;
+    GLX_CK(buf.ensure(bytes));
+    if (bytes) GLX_CK(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, st));
+    if (cache) {
+        key = src;
+        if (key_bytes) *key_bytes = bytes;
+    }
+    return GLX_OK;
+}
+
+int glx_run_train_segment_eval(float* w_ih, float* w_ho, const float* feats, const float* targets,
+                               const uint8_t* labels, int64_t rows, const float* test_feats,
+                               const uint8_t* test_labels, int64_t test_rows, int32_t input_dim, int32_t hidden_dim,
+                               int64_t epochs, double lr, int32_t numerics, int32_t mode, int32_t device,
+                               int32_t flags, int64_t* counts8, double* loss2, int32_t* finite, double* train_seconds) {
+    int rc = check_dims(rows, input_dim, hidden_dim);
+    if (rc) return rc;
+    if (test_rows < 0) return set_err(GLX_ERR_SHAPE, "test_rows must be >= 0");
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0, got %lld", (long long)epochs);
+    if (mode != 0 && mode != 1) return set_err(GLX_ERR_INVALID, "mode must be 0 (online) or 1 (batch)");
+    if (rows == 0) return set_err(GLX_ERR_SHAPE, "training rows must not be empty");
+    auto t0 = std::chrono::steady_clock::now();
+    HOST_PROLOGUE(device);
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
+    rc = mode == 0 ? online_segment_dev(hs, w_ih, w_ho, feats, targets, rows, input_dim, hidden_dim, epochs, lr,
+                                        numerics, flags, st)
+                   : batch_segment_dev(hs, w_ih, w_ho, feats, targets, rows, input_dim, hidden_dim, epochs, lr, false,
+                                       flags, st);
+    if (rc) return rc;
+    // checkpoint evaluation on the device, same stream: exact (ref64) counts for the
+    // train rows (already resident) and the test rows; the eval's own device time is
+    // excluded from train_seconds
+    const bool cache = (flags & GLX_FLAG_CACHE_INPUTS) != 0;
+    cudaEvent_t e0, e1;
+    GLX_CK(cudaEventCreate(&e0));
+    GLX_CK(cudaEventCreate(&e1));
+    GLX_CK(cudaEventRecord(e0, st));
+    rc = stage_buf(hs->tlab, hs->key_tlab, nullptr, labels, (size_t)rows, cache, st);
+    if (!rc && test_rows) rc = stage_buf(hs->vx, hs->key_vx, &hs->bytes_vx, test_feats,
+                                         (size_t)test_rows * input_dim * 4, cache, st);
+    if (!rc && test_rows) rc = stage_buf(hs->vlab, hs->key_vlab, nullptr, test_labels, (size_t)test_rows, cache, st);
+    if (rc) return rc;
+    GLX_CK(hs->cnt.ensure(8 * sizeof(uint64_t)));
+    GLX_CK(hs->loss.ensure(8 * sizeof(double)));
+    GLX_CK(hs->flag.ensure(sizeof(int)));
+    GLX_CK(cudaMemsetAsync(hs->cnt.p, 0, 8 * sizeof(uint64_t), st));
+    GLX_CK(cudaMemsetAsync(hs->loss.p, 0, 2 * sizeof(double), st));
+    GLX_CK(cudaMemsetAsync(hs->flag.p, 0, sizeof(int), st));
+    GLX_LAUNCH(launch_nonfinite(hs->w1.as<float>(), (int64_t)n1, hs->w2.as<float>(), (int64_t)n2, hs->flag.as<int>(),
+                                st));
+    uint64_t* cnt = hs->cnt.as<uint64_t>();
+    double* loss = hs->loss.as<double>();
+    rc = glx_eval(hs->w1.as<float>(), hs->w2.as<float>(), hs->x.as<float>(), hs->tlab.as<uint8_t>(), rows, input_dim,
+                  hidden_dim, 1, cnt, loss, st);
+    if (!rc && test_rows)
+        rc = glx_eval(hs->w1.as<float>(), hs->w2.as<float>(), hs->vx.as<float>(), hs->vlab.as<uint8_t>(), test_rows,
+                      input_dim, hidden_dim, 1, cnt + 4, loss + 1, st);
+    if (rc) return rc;
+    GLX_CK(cudaEventRecord(e1, st));
+    uint64_t hc[8];
+    double hl[2];
+    int hf = 0;
+    GLX_CK(cudaMemcpyAsync(w_ih, hs->w1.p, n1 * 4, cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(w_ho, hs->w2.p, n2 * 4, cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(hc, hs->cnt.p, sizeof(hc), cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(hl, hs->loss.p, sizeof(hl), cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(&hf, hs->flag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaStreamSynchronize(st));
+    float eval_ms = 0.f;
+    GLX_CK(cudaEventElapsedTime(&eval_ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    for (int q = 0; q < 8; q++) counts8[q] = (int64_t)hc[q];
+    if (loss2) {
+        loss2[0] = hl[0];
+        loss2[1] = test_rows ? hl[1] : 0.0;
+    }
+    if (finite) *finite = hf ? 0 : 1;
+    if (train_seconds) {
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        *train_seconds = std::max(0.0, wall - eval_ms * 1e-3);
+    }
     return GLX_OK;
 }
 

@@ -10,6 +10,8 @@
 #include "glx_common.cuh"
 #include "glx_kernels.h"
 
+#include <algorithm>
+
 namespace glx {
 
 constexpr int kEvalThreads = 128;
@@ -155,6 +157,22 @@ __global__ void __launch_bounds__(256) fp32_peak_kernel(float* out, int iters) {
 #pragma unroll
     for (int k = 0; k < 8; k++) s += a[k].x + a[k].y;
     if (s == 1.2345f) out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+// flag |= 1 if any of a[0, na) or b[0, nb) is not finite (checkpoint divergence test)
+__global__ void nonfinite_kernel(const float* __restrict__ a, int64_t na, const float* __restrict__ b, int64_t nb,
+                                 int* __restrict__ flag) {
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < na + nb; i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(i < na ? a[i] : b[i - na]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st) {
+    const int64_t n = na + nb;
+    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 4);
+    nonfinite_kernel<<<blocks < 1 ? 1 : blocks, 256, 0, st>>>(a, na, b, nb, flag);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st) {

@@ -102,6 +102,7 @@ cudaError_t launch_batch3_epoch(const Batch3Geom& g, const float* Xp, const floa
 cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,
                               int D, int H, int K, unsigned long long* counts4, double* loss_part, int nparts,
                               cudaStream_t st);
+cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st);
 cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss_out, cudaStream_t st);
 
 // ------------------------------------------------------------ tcgen05 GEMM

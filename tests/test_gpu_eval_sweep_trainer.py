@@ -143,3 +143,40 @@ def test_batch_mode_trainer(gpu):
                   c["train_x"].shape[0])
     assert rel_err(rep.network.w_ih, ref.w_ih) <= 1e-5
     assert rep.metadata["mode"] == "batch"
+
+
+@pytest.mark.parametrize("mode", ["online", "batch"])
+def test_fused_checkpoint_equals_segment_plus_eval(gpu, mode):
+    """backend.run_train_segment_eval == the unfused sequence:
+    segment, host finiteness test, eval_counts on train and on test."""
+    from paper_1908_07847_b200.backend import run_train_segment_eval
+
+    c = load_case("paper_33_33_1")
+    x, y, vx, vy = c["train_x"], c["train_y"], c["test_x"], c["test_y"]
+    t = y.astype(np.float32)
+    kind = g.sequential() if mode == "online" else g.cuda()
+    a = g.init_weights(g.NetworkConfig(input_dim=33, hidden_dim=33, seed=7))
+    b = a.copy()
+    step = g.run_train_segment if mode == "online" else g.run_train_segment_batch
+    for n in (1, 9, 90):
+        r = run_train_segment_eval(a.w_ih2d, a.w_ho2d, x, t, y, vx, vy, n, 0.5, kind, mode=mode)
+        step(b.w_ih2d, b.w_ho2d, x, t, n, 0.5, kind)
+        assert a.w_ih.tobytes() == b.w_ih.tobytes() and a.w_ho.tobytes() == b.w_ho.tobytes()
+        assert r.finite and r.train_seconds >= 0
+        assert r.train_counts == g.eval_counts(b.w_ih2d, b.w_ho2d, x, y)
+        assert r.test_counts == g.eval_counts(b.w_ih2d, b.w_ho2d, vx, vy)
+        assert sum(r.train_counts) == x.shape[0] and sum(r.test_counts) == vx.shape[0]
+        (_, l_tr), (_, l_te) = O.eval_counts(b.w_ih2d, b.w_ho2d, x, y), O.eval_counts(b.w_ih2d, b.w_ho2d, vx, vy)
+        assert r.train_loss == pytest.approx(l_tr, rel=1e-12) and r.test_loss == pytest.approx(l_te, rel=1e-12)
+
+
+def test_fused_checkpoint_flags_nonfinite(gpu):
+    from paper_1908_07847_b200.backend import run_train_segment_eval
+
+    c = load_case("paper_33_33_1")
+    x, y = c["train_x"], c["train_y"]
+    net = g.init_weights(g.NetworkConfig(input_dim=33, hidden_dim=33, seed=7))
+    net.w_ih[5] = np.inf
+    r = run_train_segment_eval(net.w_ih2d, net.w_ho2d, x, y.astype(np.float32), y, c["test_x"], c["test_y"], 1, 0.1,
+                               g.cuda(), mode="batch")
+    assert not r.finite and not net.weights_finite()
