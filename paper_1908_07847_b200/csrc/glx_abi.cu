@@ -173,7 +173,8 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     if (dp < 0) return set_err(GLX_ERR_INVALID, "online kernel supports input_dim <= 63, got %d", D);
     for (auto& n : nets)
         if (n.H < 1 || n.H > 512) return set_err(GLX_ERR_INVALID, "online kernel supports 1 <= hidden_dim <= 512, got %d", n.H);
-    const size_t xbytes = ((size_t)N * dp * 4 + (size_t)N * 4 + 15) / 16 * 16;
+    // staged rows [N][dp], targets [N], lookahead dots [N] (glx_online.cu)
+    const size_t xbytes = ((size_t)N * dp * 4 + (size_t)N * 8 + 15) / 16 * 16;
     const bool x_in_smem = xbytes <= 160 * 1024;
     const int mt = online_mt(nets.size(), ref64, dp);
     const int cap = mt == 1 ? 16 : 8;  // warps per CTA (register budget of the MT-unit tile)

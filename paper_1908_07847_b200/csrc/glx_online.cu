@@ -21,6 +21,8 @@
 #include "glx_common.cuh"
 #include "glx_kernels.h"
 
+#include <cstdio>
+
 namespace glx {
 
 template <typename Real, int DP, bool XS>
@@ -205,6 +207,11 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
 #ifndef GLX_ONLINE_XSMEM
 #define GLX_ONLINE_XSMEM 1  // x pairs from shared memory (frees 34 registers for occupancy)
 #endif
+#ifndef GLX_ONLINE_LA
+// lookahead forward: z_{r+1} = W^(r) x_{r+1} + ns_r (x_r . x_{r+1}) lets the next
+// row's dot product run alongside this row's output reduction (fp32 only)
+#define GLX_ONLINE_LA 1
+#endif
 #ifndef GLX_ONLINE_MT2_CTAS
 #define GLX_ONLINE_MT2_CTAS 2  // resident 256-thread CTAs per SM for the 2-unit tile (<= 128 registers)
 #endif
@@ -216,6 +223,7 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* xs = reinterpret_cast<float*>(smem_raw);
     float* ts = xs + (XS ? N * DP : 0);
+    float* gd = ts + (XS ? N : 0);  // gd[r] = x_r . x_{(r+1) mod N} (lookahead correction)
     const int2 cn = cta_nets[blockIdx.x];
     const int warp = threadIdx.x >> 5;
     if (XS) {
@@ -226,6 +234,16 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
         }
         for (int64_t r = threadIdx.x; r < N; r += blockDim.x) ts[r] = T[r];
         __syncthreads();
+        if (GLX_ONLINE_LA) {
+            for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
+                const float* a0 = xs + r * DP;
+                const float* a1 = xs + (r + 1 == N ? 0 : r + 1) * DP;
+                float s = 0.f;
+                for (int i = 0; i < DP; i++) s = fmaf(a0[i], a1[i], s);
+                gd[r] = s;
+            }
+            __syncthreads();
+        }
     }
     int my = -1;
     for (int k = 0; k < cn.y; k++) {
@@ -263,6 +281,82 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
     // GLX_ONLINE_XSMEM: with the rows staged in shared memory, read x pairs from
     // there in both loops instead of holding the row in 34 registers
     constexpr bool kXs = XS && GLX_ONLINE_XSMEM;
+    if constexpr (kXs && GLX_ONLINE_LA) {
+        // Lookahead schedule. At row r the thread holds z_r (this row's dots) and
+        // the pending update (ns of row r-1, applied lazily). Off the critical
+        // path: apply that update (W becomes W^(r)) and form W^(r) x_{r+1}. On it:
+        // sigmoid, output reduction, delta_o, ns_r, then z_{r+1} = that dot +
+        // ns_r * gd[r]. Same arithmetic as the reference order up to f32 rounding.
+        const float2* x0 = reinterpret_cast<const float2*>(xs);
+        float zc[MT], nsp[MT];
+#pragma unroll
+        for (int u = 0; u < MT; u++) {
+            float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < DP / 2; q++) p = ffma2(w[u][q], x0[q], p);
+            zc[u] = p.x + p.y;
+            nsp[u] = 0.f;
+        }
+        int64_t rp = 0;  // row of the pending update (nsp = 0 before the first row)
+        for (int64_t ep = 0; ep < epochs; ep++) {
+            for (int64_t r = 0; r < N; r++) {
+                const int64_t rn = r + 1 == N ? 0 : r + 1;
+                const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
+                const float2* xn2 = reinterpret_cast<const float2*>(xs + rn * DP);
+                // (B) off the critical path
+                float zpre[MT];
+#pragma unroll
+                for (int u = 0; u < MT; u++) {
+                    float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) {
+                        w[u][q] = ffma2(bcast2(nsp[u]), xp2[q], w[u][q]);
+                        p = ffma2(w[u][q], xn2[q], p);
+                    }
+                    zpre[u] = p.x + p.y;
+                }
+                // (A) the row's critical chain
+                const float tt = ts[r];
+                float h[MT];
+                float prod = (t == 0) ? b2 : 0.f;
+#pragma unroll
+                for (int u = 0; u < MT; u++) {
+                    h[u] = act[u] ? sigmoid_scaled(kScale * zc[u]) : 0.f;
+                    prod = fmaf(w2[u], h[u], prod);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+                if ((threadIdx.x & 31) == 0) red[buf * 16 + (t >> 5)] = prod;
+                bar_sync(nd.bar_id, nthr);
+                float zo = 0.f;
+                for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
+                buf ^= 1;
+                const float o = sigmoid_scaled(kScale * zo);
+                const float d_o = (o - tt) * o * (1.0f - o);
+                const float step_o = flr * d_o;
+                const float g = gd[r];
+#ifdef GLX_LA_DEBUG
+                if (ep == 0 && r < 2 && t < 2 && blockIdx.x == 0 && nd.warp0 == 0)
+                    printf("r=%d t=%d zc0=%.7g zc1=%.7g h0=%.7g zo=%.7g o=%.7g d_o=%.7g g=%.7g zpre0=%.7g w2=%.7g b2=%.7g tt=%.3g\n",
+                           (int)r, t, zc[0], zc[1], h[0], zo, o, d_o, g, zpre[0], w2[0], b2, tt);
+#endif
+#pragma unroll
+                for (int u = 0; u < MT; u++) {
+                    const float ns = -flr * (w2[u] * d_o * h[u] * (1.0f - h[u]));
+                    w2[u] = fmaf(-step_o, h[u], w2[u]);
+                    zc[u] = fmaf(ns, g, zpre[u]);
+                    nsp[u] = ns;
+                }
+                if (t == 0) b2 -= step_o;
+                rp = r;
+            }
+        }
+        const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
+#pragma unroll
+        for (int u = 0; u < MT; u++)
+#pragma unroll
+            for (int q = 0; q < DP / 2; q++) w[u][q] = ffma2(bcast2(nsp[u]), xp2[q], w[u][q]);
+    } else {  // (braced: an unbraced discarded `else` swallowed the pragma'd write-back loop below)
     for (int64_t ep = 0; ep < epochs; ep++) {
         for (int64_t r = 0; r < N; r++) {
             const float2* xr2 = reinterpret_cast<const float2*>(xs + (XS ? r * DP : 0));
@@ -298,6 +392,7 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
             }
             if (t == 0) b2 -= step_o;
         }
+    }
     }
 #pragma unroll
     for (int u = 0; u < MT; u++) {
