@@ -23,6 +23,12 @@
 
 #include <cstdio>
 
+#ifndef GLX_ONLINE_LA
+// lookahead forward: z_{r+1} = W^(r) x_{r+1} + ns_r (x_r . x_{r+1}) lets the next
+// row's dot product run alongside this row's output reduction (fp32 only)
+#define GLX_ONLINE_LA 1
+#endif
+
 namespace glx {
 
 template <typename Real, int DP, bool XS>
@@ -51,6 +57,8 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
     extern __shared__ __align__(16) unsigned char smem_raw[];
     float* xs = reinterpret_cast<float*>(smem_raw);  // N x DP (if XS)
     float* ts = xs + (XS ? N * DP : 0);              // N targets (if XS)
+    float* gd = ts + (XS ? N : 0);                   // N lookahead dots x_r . x_{r+1} (if XS, fp32)
+    constexpr bool kLA = XS && GLX_ONLINE_LA && sizeof(Real) == 4;
 
     const int2 cn = cta_nets[blockIdx.x];
     const int warp = threadIdx.x >> 5;
@@ -64,6 +72,16 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
         }
         for (int64_t r = threadIdx.x; r < N; r += blockDim.x) ts[r] = T[r];
         __syncthreads();
+        if (kLA) {
+            for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
+                const float* a0 = xs + r * DP;
+                const float* a1 = xs + (r + 1 == N ? 0 : r + 1) * DP;
+                float s = 0.f;
+                for (int i = 0; i < DP; i++) s = fmaf(a0[i], a1[i], s);
+                gd[r] = s;
+            }
+            __syncthreads();
+        }
     }
 
     // find my network
@@ -95,6 +113,72 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
         float* red = reinterpret_cast<float*>(scratch);  // [2][16] warp partials
         const float kScale = (float)(-GLX_LOG2E);
         int buf = 0;
+        if constexpr (kLA) {
+            // lookahead schedule of online_sgd_mt_kernel, one unit per thread
+            const float2* x0 = reinterpret_cast<const float2*>(xs);
+            float2 p0 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < DP / 2; q++) p0 = ffma2(make_float2(w[2 * q], w[2 * q + 1]), x0[q], p0);
+            float zc = p0.x + p0.y, nsp = 0.f;
+            int64_t rp = 0;
+            for (int64_t ep = 0; ep < epochs; ep++) {
+                if (ep > 0) {  // epoch start: as a fresh call (see online_sgd_mt_kernel)
+                    const float2* xl2 = reinterpret_cast<const float2*>(xs + rp * DP);
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) {
+                        const float2 wq = ffma2(bcast2(nsp), xl2[q], make_float2(w[2 * q], w[2 * q + 1]));
+                        w[2 * q] = wq.x;
+                        w[2 * q + 1] = wq.y;
+                    }
+                    nsp = 0.f;
+                    float2 pz = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) pz = ffma2(make_float2(w[2 * q], w[2 * q + 1]), x0[q], pz);
+                    zc = pz.x + pz.y;
+                }
+                for (int64_t r = 0; r < N; r++) {
+                    const int64_t rn = r + 1 == N ? 0 : r + 1;
+                    const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
+                    const float2* xn2 = reinterpret_cast<const float2*>(xs + rn * DP);
+                    float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) {
+                        const float2 wq = ffma2(bcast2(nsp), xp2[q], make_float2(w[2 * q], w[2 * q + 1]));
+                        w[2 * q] = wq.x;
+                        w[2 * q + 1] = wq.y;
+                        p = ffma2(wq, xn2[q], p);
+                    }
+                    const float zpre = p.x + p.y;
+                    const float t = ts[r];
+                    const float h = active ? sigmoid_scaled(kScale * zc) : 0.0f;
+                    float prod = active ? w2 * h : 0.0f;
+                    if (j == 0) prod += b2;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
+                    if ((threadIdx.x & 31) == 0) red[buf * 16 + (j >> 5)] = prod;
+                    bar_sync(nd.bar_id, nthr);
+                    float zo = 0.0f;
+                    for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
+                    buf ^= 1;
+                    const float o = sigmoid_scaled(kScale * zo);
+                    const float d_o = (o - t) * o * (1.0f - o);
+                    const float step_o = (float)lr * d_o;
+                    const float ns = active ? -(float)lr * (w2 * d_o * h * (1.0f - h)) : 0.0f;
+                    if (active) w2 = fmaf(-step_o, h, w2);
+                    if (j == 0) b2 -= step_o;
+                    zc = fmaf(ns, gd[r], zpre);
+                    nsp = ns;
+                    rp = r;
+                }
+            }
+            const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
+#pragma unroll
+            for (int q = 0; q < DP / 2; q++) {
+                const float2 wq = ffma2(bcast2(nsp), xp2[q], make_float2(w[2 * q], w[2 * q + 1]));
+                w[2 * q] = wq.x;
+                w[2 * q + 1] = wq.y;
+            }
+        } else {
         for (int64_t ep = 0; ep < epochs; ep++) {
             for (int64_t r = 0; r < N; r++) {
                 load_row<Real, DP, XS>(x, xs, X, r, D);
@@ -130,6 +214,7 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
                 }
                 if (j == 0) b2 -= step_o;
             }
+        }
         }
     } else {
         // ---------------------------------------------------------------- ref64
@@ -206,11 +291,6 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
 // hidden units instead of once per unit.
 #ifndef GLX_ONLINE_XSMEM
 #define GLX_ONLINE_XSMEM 1  // x pairs from shared memory (frees 34 registers for occupancy)
-#endif
-#ifndef GLX_ONLINE_LA
-// lookahead forward: z_{r+1} = W^(r) x_{r+1} + ns_r (x_r . x_{r+1}) lets the next
-// row's dot product run alongside this row's output reduction (fp32 only)
-#define GLX_ONLINE_LA 1
 #endif
 #ifndef GLX_ONLINE_MT2_CTAS
 #define GLX_ONLINE_MT2_CTAS 2  // resident 256-thread CTAs per SM for the 2-unit tile (<= 128 registers)
@@ -299,6 +379,25 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
         }
         int64_t rp = 0;  // row of the pending update (nsp = 0 before the first row)
         for (int64_t ep = 0; ep < epochs; ep++) {
+            if (ep > 0) {
+                // epoch start: settle the pending update and form z_0 directly, exactly
+                // as a fresh call does, so results do not depend on how the epochs are
+                // split into calls (checkpoint segments)
+                const float2* xl2 = reinterpret_cast<const float2*>(xs + rp * DP);
+#pragma unroll
+                for (int u = 0; u < MT; u++) {
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) w[u][q] = ffma2(bcast2(nsp[u]), xl2[q], w[u][q]);
+                    nsp[u] = 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < MT; u++) {
+                    float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q = 0; q < DP / 2; q++) p = ffma2(w[u][q], x0[q], p);
+                    zc[u] = p.x + p.y;
+                }
+            }
             for (int64_t r = 0; r < N; r++) {
                 const int64_t rn = r + 1 == N ? 0 : r + 1;
                 const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
