@@ -108,6 +108,7 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
     float b2 = w_ho[H];  // only thread j == 0 updates / writes it back
 
     float x[DP];
+    float bw = 0.0f;  // ref64: the bias weight (see below); fp32 keeps it in w[D]
     if constexpr (sizeof(Real) == 4) {
         // ---------------------------------------------------------------- fp32
         float* red = reinterpret_cast<float*>(scratch);  // [2][16] warp partials
@@ -219,11 +220,17 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
     } else {
         // ---------------------------------------------------------------- ref64
         const int nb = (H + 15) >> 4;
+        // the bias weight w[D] lives in its own register here: any runtime index into
+        // w (NVVM even rebuilds one from a predicated select) moves the row to local memory
+        bw = active ? w_ih[(int64_t)j * (D + 1) + D] : 0.0f;
         double* prods = reinterpret_cast<double*>(scratch);  // nb blocks x 17 (padded against bank conflicts)
         double* bc = prods + nb * 17;                        // [0] = d_o, [1] = step_o
         for (int64_t ep = 0; ep < epochs; ep++) {
             for (int64_t r = 0; r < N; r++) {
+                // the row stays in registers: reading it from shared memory inside the
+                // f64 chains measured 2.4x slower (the kernel then drops to 64 registers)
                 load_row<Real, DP, XS>(x, xs, X, r, D);
+                auto xd = [&](int i) -> double { return (double)x[i]; };
                 float h = 0.0f;
                 if (active) {
                     // kernels.py:102-122: blocked f64 dot, bias last, f64 sigmoid, f32 round
@@ -232,11 +239,13 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
                     for (int b0 = 0; b0 < DP; b0 += 16) {
                         double part = 0.0;
 #pragma unroll
-                        for (int i = b0; i < (b0 + 16 < DP ? b0 + 16 : DP); i++)
-                            if (i < D) part = fma((double)w[i], (double)x[i], part);  // exact product
+                        for (int k = 0; k < 16; k++) {  // constant trip count: w stays in registers
+                            const int i = b0 + k;
+                            if (i < DP && i < D) part = fma((double)w[i < DP ? i : 0], xd(i < DP ? i : 0), part);
+                        }
                         if (b0 < D) acc = __dadd_rn(acc, part);
                     }
-                    double z = __dadd_rn(acc, (double)w[D < DP ? D : DP - 1]);
+                    double z = __dadd_rn(acc, (double)bw);
                     h = __double2float_rn(1.0 / (1.0 + exp(-z)));
                     prods[(j >> 4) * 17 + (j & 15)] = (double)w2 * (double)h;  // exact product
                 }
@@ -268,8 +277,8 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
                     const double s = __dmul_rn(lr, d_h);
 #pragma unroll
                     for (int i = 0; i < DP; i++)
-                        if (i < D) w[i] = __double2float_rn(__dsub_rn((double)w[i], __dmul_rn(s, (double)x[i])));
-                    if (D < DP) w[D < DP ? D : DP - 1] = __double2float_rn(__dsub_rn((double)w[D < DP ? D : DP - 1], s));
+                        if (i < D) w[i] = __double2float_rn(__dsub_rn((double)w[i], __dmul_rn(s, xd(i))));
+                    bw = __double2float_rn(__dsub_rn((double)bw, s));  // bias (x_D = 1)
                     w2 = __double2float_rn(__dsub_rn((double)w2, __dmul_rn(step_o, hd)));
                 }
                 if (j == 0) b2 = __double2float_rn(__dsub_rn((double)b2, step_o));
@@ -279,7 +288,8 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
     if (active) {
 #pragma unroll
         for (int i = 0; i < DP; i++)
-            if (i <= D) w_ih[(int64_t)j * (D + 1) + i] = w[i];
+            if (sizeof(Real) == 4 ? i <= D : i < D) w_ih[(int64_t)j * (D + 1) + i] = w[i];
+        if constexpr (sizeof(Real) == 8) w_ih[(int64_t)j * (D + 1) + D] = bw;
         w_ho[j] = w2;
     }
     if (j == 0) w_ho[H] = b2;
