@@ -17,14 +17,19 @@ namespace glx {
 constexpr int kEvalThreads = 128;
 constexpr int kMaxK = 16;
 
+// KT = 1: single output (compile-time), so the output accumulators are scalars;
+// KT = 0: runtime K <= 16 (the per-output arrays then live in local memory)
+template <int KT>
 __global__ void __launch_bounds__(kEvalThreads) eval_ref64_kernel(const float* __restrict__ W1g,
                                                                    const float* __restrict__ W2g,
                                                                    const float* __restrict__ X,
                                                                    const uint8_t* __restrict__ labels, int64_t N,
-                                                                   int D, int H, int K, int w_in_smem,
+                                                                   int D, int H, int K_, int w_in_smem,
                                                                    unsigned long long* __restrict__ counts4,
                                                                    double* __restrict__ loss_part) {
     extern __shared__ __align__(16) unsigned char sm[];
+    const int K = KT ? KT : K_;
+    constexpr int KA = KT ? KT : kMaxK;  // accumulator array extent
     const float* W1 = W1g;
     const float* W2 = W2g;
     const int64_t n1 = (int64_t)H * (D + 1), n2 = (int64_t)K * (H + 1);
@@ -42,10 +47,10 @@ __global__ void __launch_bounds__(kEvalThreads) eval_ref64_kernel(const float* _
     int pred = 0, lab = 0;
     if (valid) {
         const float* x = X + r * D;
-        double zo[kMaxK];
+        double zo[KA];
         for (int k = 0; k < K; k++) zo[k] = 0.0;
         for (int jb = 0; jb < H; jb += 16) {
-            double po[kMaxK];
+            double po[KA];
             for (int k = 0; k < K; k++) po[k] = 0.0;
             const int je = jb + 16 < H ? jb + 16 : H;
             for (int j = jb; j < je; j++) {
@@ -123,13 +128,12 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
     const size_t wbytes = 4 * ((size_t)H * (D + 1) + (size_t)K * (H + 1));
     const int w_in_smem = wbytes <= 160 * 1024;
     const size_t smem = w_in_smem ? wbytes : 0;
+    auto k = K == 1 ? eval_ref64_kernel<1> : eval_ref64_kernel<0>;
     if (smem > 48 * 1024) {
-        cudaError_t e =
-            cudaFuncSetAttribute(eval_ref64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    eval_ref64_kernel<<<nparts, kEvalThreads, smem, st>>>(W1, W2, X, labels, N, D, H, K, w_in_smem, counts4,
-                                                           loss_part);
+    k<<<nparts, kEvalThreads, smem, st>>>(W1, W2, X, labels, N, D, H, K, w_in_smem, counts4, loss_part);
     return cudaGetLastError();
 }
 
