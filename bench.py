@@ -276,7 +276,7 @@ def run_gpu(args):
         traffic = json.loads(tr_file.read_text()).get("batch_epoch_kernel_bytes_per_launch")
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic,
-                "kernel": "batch_epoch_kernel<34,4,true>", "kernel_ms_per_launch": k_ms,
+                "kernel": "batch3_kernel<34,4,4> (three warp-specialised roles)", "kernel_ms_per_launch": k_ms,
                 "kernel_share_of_step": k_ms * int(kn[0]) / elapsed if elapsed else None,
                 "algorithmic_flops_per_launch": flops_per_launch,
                 "algorithmic_hbm_bytes_per_launch": ROWS_PER_GPU * (4 * D + 1),
