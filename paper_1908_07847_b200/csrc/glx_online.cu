@@ -21,8 +21,6 @@
 #include "glx_common.cuh"
 #include "glx_kernels.h"
 
-#include <cstdio>
-
 #ifndef GLX_ONLINE_LA
 // lookahead forward: z_{r+1} = W^(r) x_{r+1} + ns_r (x_r . x_{r+1}) lets the next
 // row's dot product run alongside this row's output reduction (fp32 only)
@@ -444,11 +442,6 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
                 const float d_o = (o - tt) * o * (1.0f - o);
                 const float step_o = flr * d_o;
                 const float g = gd[r];
-#ifdef GLX_LA_DEBUG
-                if (ep == 0 && r < 2 && t < 2 && blockIdx.x == 0 && nd.warp0 == 0)
-                    printf("r=%d t=%d zc0=%.7g zc1=%.7g h0=%.7g zo=%.7g o=%.7g d_o=%.7g g=%.7g zpre0=%.7g w2=%.7g b2=%.7g tt=%.3g\n",
-                           (int)r, t, zc[0], zc[1], h[0], zo, o, d_o, g, zpre[0], w2[0], b2, tt);
-#endif
 #pragma unroll
                 for (int u = 0; u < MT; u++) {
                     const float ns = -flr * (w2[u] * d_o * h[u] * (1.0f - h[u]));
