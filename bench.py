@@ -211,7 +211,15 @@ def run_gpu(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    # GLX_BENCH_FORCE_DP=1: take the data-parallel branch even with one rank (a
+    # one-rank NCCL group), to exercise the N > 1 code path on a single GPU
+    use_dp = world > 1 or os.environ.get("GLX_BENCH_FORCE_DP") == "1"
+    if use_dp:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29517")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = _lib.load()
     feats, labels = g.synthetic_arrays(ROWS_PER_GPU, D, rank, "planted-linear")
@@ -223,13 +231,15 @@ def run_gpu(args):
     stats_dev = torch.zeros((max(args.steps, args.warmup), 5), dtype=torch.float64, device="cuda")
     flag = torch.zeros(1, dtype=torch.int32, device="cuda")
 
+    ar = dp.nccl_all_reduce() if use_dp else None
+
     def epochs(k, stats):
-        if world == 1:  # fused single-GPU loop: epoch kernel + reduce/update kernel per epoch
+        if not use_dp:  # fused single-GPU loop: epoch kernel + reduce/update kernel per epoch
             _lib.check(L.glx_train_batch(eng.w1.data_ptr(), eng.w2.data_ptr(), eng.Xp.data_ptr(), eng.N, D, H, k,
                                          LR, stats.data_ptr() if stats is not None else None, flag.data_ptr(),
                                          stream.cuda_stream))
         else:
-            dp.train_data_parallel(eng, k, LR, n_total, dp.nccl_all_reduce())
+            dp.train_data_parallel_graph(eng, k, LR, n_total, ar)
 
     # FP32 roofline denominator: packed-FFMA throughput on this GPU, now
     tfl = np.zeros(1)
@@ -241,9 +251,9 @@ def run_gpu(args):
     torch.cuda.synchronize()
     L.glx_profile_enable(1)
     L.glx_profile_read(None, None)
-    launches0 = int(L.glx_launch_count())
+    launches0 = int(L.glx_launch_count()) + dp.graph_kernel_launches
     with ClockSampler(local) as clk:
-        if world > 1:
+        if use_dp:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -251,22 +261,32 @@ def run_gpu(args):
         epochs(args.steps, stats_dev)
         e1.record(stream)
         torch.cuda.synchronize()
-        if world > 1:
+        if use_dp:
             dist.barrier()
-    launches = int(L.glx_launch_count()) - launches0
+    launches = int(L.glx_launch_count()) + dp.graph_kernel_launches - launches0
     kms = np.zeros(1)
     kn = np.zeros(1, dtype=np.int64)
     _lib.check(L.glx_profile_read(_lib.ptr(kms), _lib.ptr(kn)))
     L.glx_profile_enable(0)
     elapsed = e0.elapsed_time(e1)
-    if world > 1:
+    if use_dp:
         t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
     value = n_total * args.steps / (elapsed * 1e-3)
     assert not eng.nonfinite() and not bool(flag.item()), "non-finite weights during the benchmark"
 
-    # roofline of the dominant kernel (batch_epoch_kernel), per launch
+    # roofline of the dominant kernel (the epoch kernel), per launch
+    kernel_timing = "CUDA events around every epoch-kernel launch in the timed region"
+    if int(kn[0]) == 0 and use_dp:
+        # the timed region replayed a CUDA graph (no per-launch host events): time the
+        # same kernel on eager data-parallel epochs right after it
+        L.glx_profile_enable(1)
+        L.glx_profile_read(None, None)
+        dp.train_data_parallel(eng, 5, LR, n_total, ar)
+        _lib.check(L.glx_profile_read(_lib.ptr(kms), _lib.ptr(kn)))
+        L.glx_profile_enable(0)
+        kernel_timing = "CUDA events around 5 eager epochs right after the timed region (which replays a CUDA graph)"
     k_ms = float(kms[0]) / max(1, int(kn[0]))
     flops_per_launch = ROWS_PER_GPU * f_train()
     achieved = flops_per_launch / (k_ms * 1e-3) / 1e12
@@ -277,17 +297,17 @@ def run_gpu(args):
     roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp32_peak, "traffic": traffic,
                 "kernel": "batch3_kernel<34,4,4> (three warp-specialised roles)", "kernel_ms_per_launch": k_ms,
-                "kernel_share_of_step": k_ms * int(kn[0]) / elapsed if elapsed else None,
+                "kernel_share_of_step": k_ms / (elapsed / args.steps) if elapsed else None,
+                "kernel_timing": kernel_timing,
                 "algorithmic_flops_per_launch": flops_per_launch,
                 "algorithmic_hbm_bytes_per_launch": ROWS_PER_GPU * (4 * D + 1),
                 "hbm_frac": ROWS_PER_GPU * (4 * D + 1) / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6545.9),
                 "peak_source": "glx_fp32_peak FFMA2 microbenchmark on this GPU in this run (MEASURED_PEAKS.json "
                                "has no FP32 figure)"}
 
-    # end-to-end through the public host-pointer API, inputs in pinned host memory
-    e2e = None
-    if rank == 0 or world == 1:
-        e2e = run_e2e(g, torch, feats, targets)
+    # end-to-end through the public API, inputs in pinned host memory: the host
+    # segment API on one GPU, the data-parallel engine (every rank) on N
+    e2e = run_e2e_dp(g, torch, dp, feats, targets, n_total, world) if use_dp else run_e2e(g, torch, feats, targets)
 
     line = None
     if rank == 0:
@@ -297,9 +317,9 @@ def run_gpu(args):
                 "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
                 "config": config_dict(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk.summary(),
-                "final_loss_sum": float(stats_dev[args.steps - 1, 0].item()) if world == 1 else None}
+                "final_loss_sum": float(stats_dev[args.steps - 1, 0].item()) if not use_dp else None}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if use_dp:
         dist.barrier()
         dist.destroy_process_group()
 
@@ -328,6 +348,42 @@ def run_e2e(g, torch, feats, targets, reps=3):
             "h2d_bytes_per_step": int(feats.nbytes + targets.nbytes + w_bytes),
             "d2h_bytes_per_step": int(w_bytes + stats.nbytes), "epochs_per_step": E_E2E,
             "seconds_per_step": dt, "api": "backend.run_train_segment_batch -> glx_run_train_segment_batch"}
+
+
+def run_e2e_dp(g, torch, dp, feats, targets, n_total, world, reps=3):
+    """N-GPU public-API step: every rank builds a dp.DeviceEngine from its pinned host
+    shard (host->device copy and row packing), runs E_E2E data-parallel epochs
+    (gradient kernel, NCCL all-reduce, update) and reads the weights back; the step
+    time is the max over ranks and the value covers all ranks' rows."""
+    import torch.distributed as dist
+
+    pin_x = torch.empty(feats.shape, dtype=torch.float32, pin_memory=True)
+    pin_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
+    pin_x.numpy()[:] = feats
+    pin_t.numpy()[:] = targets
+    x, t = pin_x.numpy(), pin_t.numpy()
+    net0 = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=0))
+    times = []
+    for it in range(reps + 1):  # the first repetition is the warm-up
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        eng = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho, device=torch.cuda.current_device())
+        # eager epochs: a fresh engine per step would pay graph instantiation in-step
+        dp.train_data_parallel(eng, E_E2E, LR, n_total, dp.nccl_all_reduce())
+        w1, w2 = eng.weights()
+        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        if it:
+            times.append(float(dt.item()))
+        del eng
+    dt = statistics.median(times)
+    w_bytes = 4 * (w1.size + w2.size)
+    return {"value": n_total * E_E2E / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(feats.nbytes + targets.nbytes + w_bytes),
+            "d2h_bytes_per_step": int(w_bytes + 5 * 8 * E_E2E), "epochs_per_step": E_E2E, "seconds_per_step": dt,
+            "per_rank": True, "ranks": world,
+            "api": "dp.DeviceEngine + dp.train_data_parallel (glx_batch_grad, NCCL all-reduce, glx_batch_apply)"}
 
 
 def peaks():

@@ -101,6 +101,69 @@ def train_data_parallel(engine, epochs: int, lr: float, n_total: int, all_reduce
     return stats
 
 
+# kernels of this library launched by CUDA-graph replays (the library's own
+# glx_launch_count only sees launches issued through its C entry points)
+graph_kernel_launches = 0
+
+
+def train_data_parallel_graph(engine, epochs: int, lr: float, n_total: int, all_reduce) -> list[EpochStats]:
+    """train_data_parallel with one epoch (gradient kernels, all-reduce, update)
+    captured in a CUDA graph and replayed, removing the per-epoch host launch
+    overhead. The graph is cached on the engine (keyed on the step size), so only
+    the first call captures. NCCL collectives are graph-capturable; if capture
+    fails the eager loop runs instead. Same arithmetic and results as
+    train_data_parallel."""
+    import torch
+
+    P = getattr(engine, "P", None) or engine.H * (engine.D + 1) + engine.H + 1
+    ns = getattr(engine, "n_stats", 5)
+    key = float(lr) / n_total
+    cache = getattr(engine, "_graph_cache", None)
+    if cache is None or cache[0] != key:
+        side = torch.cuda.Stream(device=engine.grad.device)
+        saved = engine.stream
+        try:
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                engine.stream = side.cuda_stream
+                # one eager epoch on the capture stream: the library allocates its
+                # per-stream workspace on first use, which capture does not allow
+                first = train_data_parallel(engine, 1, lr, n_total, all_reduce)
+                graph = torch.cuda.CUDAGraph()
+                n0 = int(engine.L.glx_launch_count())
+                with torch.cuda.graph(graph, stream=side):
+                    g = engine.grad_sum()
+                    all_reduce(g)
+                    engine.apply(g, key)
+                per_replay = int(engine.L.glx_launch_count()) - n0
+            torch.cuda.current_stream().wait_stream(side)
+        except Exception:  # capture unsupported here: eager epochs
+            engine.stream = saved
+            torch.cuda.current_stream().wait_stream(side)
+            return first + train_data_parallel(engine, epochs - 1, lr, n_total, all_reduce) if epochs > 1 else first
+        finally:
+            engine.stream = saved
+        engine._graph_cache = (key, graph, side, per_replay)
+        done = first
+        epochs -= 1
+    else:
+        done = []
+    global graph_kernel_launches
+    _, graph, side, per_replay = engine._graph_cache
+    graph_kernel_launches += per_replay * epochs
+    hist = torch.zeros((max(epochs, 1), ns), dtype=torch.float64, device=engine.grad.device)
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for e in range(epochs):
+            graph.replay()
+            hist[e].copy_(engine.grad[P:P + ns])
+    torch.cuda.current_stream().wait_stream(side)
+    out = list(done)
+    for s in hist[:epochs].tolist():
+        out.append(EpochStats(float(s[0]), tuple(int(round(v)) for v in s[1:ns])))
+    return out
+
+
 def nccl_all_reduce(group=None):
     import torch.distributed as dist
 

@@ -126,3 +126,35 @@ def test_dp_path_over_nccl_one_rank(gpu):
         dist.destroy_process_group()
     assert rel_err(w1, fused.w_ih) <= 1e-6 and rel_err(w2, fused.w_ho) <= 1e-6
     assert all(sum(st.counts) == x.shape[0] for st in stats)
+
+
+def test_dp_graph_replay_equals_eager_over_nccl_one_rank(gpu):
+    """dp.train_data_parallel_graph (the epoch captured in a CUDA graph, NCCL all-reduce
+    inside) gives the same weights and statistics as the eager data-parallel loop."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_07847_b200 import dp
+
+    x, l, t, net0 = _case(40_000, 33, 256, seed=3)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        a = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
+        sa = dp.train_data_parallel(a, 7, 0.5, x.shape[0], dp.nccl_all_reduce())
+        b = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
+        sb = dp.train_data_parallel_graph(b, 3, 0.5, x.shape[0], dp.nccl_all_reduce())
+        sb += dp.train_data_parallel_graph(b, 4, 0.5, x.shape[0], dp.nccl_all_reduce())  # cached graph replays
+        assert getattr(b, "_graph_cache", None) is not None  # capture succeeded (no eager fallback)
+        torch.cuda.synchronize()
+        wa, wb = a.weights(), b.weights()
+    finally:
+        dist.destroy_process_group()
+    assert wa[0].tobytes() == wb[0].tobytes() and wa[1].tobytes() == wb[1].tobytes()
+    assert [(s.loss_sum, s.counts) for s in sa] == [(s.loss_sum, s.counts) for s in sb]
