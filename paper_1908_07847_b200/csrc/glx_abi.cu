@@ -155,13 +155,14 @@ struct NetReq {
     int idx;
 };
 
-// hidden units per thread for the fp32 online kernel: 1 for a single network
-// (shortest per-row critical path); for sweeps an MT-unit register tile
-// (GLX_ONLINE_MT overrides) amortises the per-row reduction and barrier
-int online_mt(size_t n_nets, bool ref64, int dp) {
+// hidden units per thread for the fp32 online kernel: for sweeps an MT-unit
+// register tile (GLX_ONLINE_MT overrides) amortises the per-row reduction and
+// barrier; a single network uses 2 units per thread when that makes it one warp
+// (no cross-warp exchange: 292 vs 337 ns per row at 33-33-1), else 1
+int online_mt(size_t n_nets, bool ref64, int dp, int max_h) {
     if (ref64) return 1;
     const char* e = getenv("GLX_ONLINE_MT");
-    int mt = e ? atoi(e) : (n_nets > 1 ? 2 : 1);
+    int mt = e ? atoi(e) : (n_nets > 1 || max_h <= 64 ? 2 : 1);
     if (mt != 1 && mt != 2 && mt != 4) mt = 1;
     if (dp > 34) mt = 1;  // 64-wide rows: the MT tile would spill
     return mt;
@@ -176,7 +177,9 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     // staged rows [N][dp], targets [N], lookahead dots [N] (glx_online.cu)
     const size_t xbytes = ((size_t)N * dp * 4 + (size_t)N * 8 + 15) / 16 * 16;
     const bool x_in_smem = xbytes <= 160 * 1024;
-    const int mt = online_mt(nets.size(), ref64, dp);
+    int max_h = 0;
+    for (auto& n : nets) max_h = std::max(max_h, n.H);
+    const int mt = online_mt(nets.size(), ref64, dp, max_h);
     const int cap = mt == 1 ? 16 : 8;  // warps per CTA (register budget of the MT-unit tile)
     // first-fit decreasing packing of networks into CTAs of <= cap warps / 15 networks
     std::stable_sort(nets.begin(), nets.end(), [](const NetReq& a, const NetReq& b) { return a.H > b.H; });
@@ -236,6 +239,7 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     L.x_in_smem = x_in_smem;
     L.ref64 = ref64;
     L.mt = mt;
+    L.one_warp = std::all_of(desc.begin(), desc.end(), [](const OnlineNetDesc& d) { return d.nwarps == 1; });
     L.X = X;
     L.T = T;
     L.N = N;

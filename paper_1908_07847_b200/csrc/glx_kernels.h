@@ -28,6 +28,7 @@ struct OnlineLaunch {
     bool x_in_smem;
     bool ref64;
     int mt;  // fp32 hidden units per thread (1, 2 or 4)
+    bool one_warp = false;  // every network fits one warp (fp32 MT kernel fast path)
     const float* X;  // device, (N, D)
     const float* T;  // device, (N,)
     int64_t N;

@@ -303,7 +303,10 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
 #ifndef GLX_ONLINE_MT2_CTAS
 #define GLX_ONLINE_MT2_CTAS 2  // resident 256-thread CTAs per SM for the 2-unit tile (<= 128 registers)
 #endif
-template <int DP, int MT, bool XS>
+// ONEW: every network of the launch is one warp (H <= 32 MT): the warp-shuffle
+// reduction already gives every lane the output sum, no shared-memory exchange
+// or named barrier (a separate instantiation: a runtime branch cost the sweep)
+template <int DP, int MT, bool XS, bool ONEW = false>
 __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online_sgd_mt_kernel(const OnlineNetDesc* __restrict__ nets,
                                                              const int2* __restrict__ cta_nets,
                                                              const float* __restrict__ X, const float* __restrict__ T,
@@ -433,11 +436,14 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
-                if ((threadIdx.x & 31) == 0) red[buf * 16 + (t >> 5)] = prod;
-                bar_sync(nd.bar_id, nthr);
-                float zo = 0.f;
-                for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
-                buf ^= 1;
+                float zo = prod;
+                if constexpr (!ONEW) {
+                    if ((threadIdx.x & 31) == 0) red[buf * 16 + (t >> 5)] = prod;
+                    bar_sync(nd.bar_id, nthr);
+                    zo = 0.f;
+                    for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
+                    buf ^= 1;
+                }
                 const float o = sigmoid_scaled(kScale * zo);
                 const float d_o = (o - tt) * o * (1.0f - o);
                 const float step_o = flr * d_o;
@@ -514,7 +520,9 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
 template <int DP, int MT>
 static cudaError_t launch_online_mt(const OnlineLaunch& L, cudaStream_t st) {
     const size_t smem = L.smem_bytes;
-    auto k = L.x_in_smem ? online_sgd_mt_kernel<DP, MT, true> : online_sgd_mt_kernel<DP, MT, false>;
+    auto k = L.x_in_smem ? (L.one_warp && MT == 2 ? online_sgd_mt_kernel<DP, MT, true, true>
+                                                  : online_sgd_mt_kernel<DP, MT, true>)
+                         : online_sgd_mt_kernel<DP, MT, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     k<<<L.n_ctas, L.threads, smem, st>>>(L.nets, L.cta_nets, L.X, L.T, L.N, L.D, L.epochs, L.lr);
