@@ -470,7 +470,7 @@ int glx_eval(const float* w_ih, const float* w_ho, const float* X, const uint8_t
         GLX_CK(cudaMemsetAsync(loss, 0, sizeof(double), st));
         return GLX_OK;
     }
-    const int nparts = (int)((N + 127) / 128);
+    const int nparts = eval_nparts(N, H, K);
     Workspace* ws = workspace(st);
     GLX_CK(ws->losspart.ensure((size_t)nparts * sizeof(double)));
     GLX_LAUNCH(launch_eval_ref64(w_ih, w_ho, X, labels, N, D, H, K, reinterpret_cast<unsigned long long*>(counts4),

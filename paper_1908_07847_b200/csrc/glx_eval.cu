@@ -106,6 +106,115 @@ __global__ void __launch_bounds__(kEvalThreads) eval_ref64_kernel(const float* _
     }
 }
 
+// K = 1, one row over kSplit lanes (a row's serial f64 work shrinks kSplit-fold):
+// lane s of a row group takes hidden blocks s, s + kSplit, ... (16 units each,
+// the reference's in-block order), then the group's lane 0 adds the block sums
+// in block order fetched by shuffles -- the reference's sequential sum, exactly.
+constexpr int kSplit = 8;
+constexpr int kSplitMaxBlocksPerLane = 8;  // H <= 16 * 8 * 8 = 1024
+constexpr int kSplitRowsPerBlock = kEvalThreads / kSplit;
+
+__global__ void __launch_bounds__(kEvalThreads) eval_ref64_split_kernel(const float* __restrict__ W1g,
+                                                                         const float* __restrict__ W2g,
+                                                                         const float* __restrict__ X,
+                                                                         const uint8_t* __restrict__ labels, int64_t N,
+                                                                         int D, int H, int w_in_smem,
+                                                                         unsigned long long* __restrict__ counts4,
+                                                                         double* __restrict__ loss_part) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const float* W1 = W1g;
+    const float* W2 = W2g;
+    const int64_t n1 = (int64_t)H * (D + 1), n2 = (int64_t)(H + 1);
+    if (w_in_smem) {
+        float* s1 = reinterpret_cast<float*>(sm);
+        for (int64_t e = threadIdx.x; e < n1 + n2; e += blockDim.x) s1[e] = e < n1 ? W1g[e] : W2g[e - n1];
+        __syncthreads();
+        W1 = s1;
+        W2 = s1 + n1;
+    }
+    __shared__ double lsum[kEvalThreads / 32];
+    const int lane = threadIdx.x & 31;
+    const int sl = lane % kSplit, base = lane - sl;
+    const int64_t r = (int64_t)blockIdx.x * kSplitRowsPerBlock + threadIdx.x / kSplit;
+    const bool valid = r < N;
+    const int nb = (H + 15) >> 4;
+    double pk[kSplitMaxBlocksPerLane];
+#pragma unroll
+    for (int k = 0; k < kSplitMaxBlocksPerLane; k++) pk[k] = 0.0;
+    if (valid) {
+        const float* x = X + r * D;
+#pragma unroll
+        for (int k = 0; k < kSplitMaxBlocksPerLane; k++) {
+            const int b = k * kSplit + sl;
+            if (b < nb) {
+                double po = 0.0;
+                const int je = min(b * 16 + 16, H);
+                for (int j = b * 16; j < je; j++) {
+                    const float* wr = W1 + (int64_t)j * (D + 1);
+                    double acc = 0.0;
+                    for (int b0 = 0; b0 < D; b0 += 16) {
+                        const int b1 = b0 + 16 < D ? b0 + 16 : D;
+                        double part = 0.0;
+                        for (int i = b0; i < b1; i++) part = fma((double)wr[i], (double)__ldg(x + i), part);
+                        acc = __dadd_rn(acc, part);
+                    }
+                    const double z = __dadd_rn(acc, (double)wr[D]);
+                    const float h = __double2float_rn(1.0 / (1.0 + exp(-z)));
+                    po = fma((double)W2[j], (double)h, po);
+                }
+                pk[k] = po;
+            }
+        }
+    }
+    // block sums in block order on the group's lane 0 (all lanes shuffle: static indices)
+    double zo = 0.0;
+#pragma unroll
+    for (int k = 0; k < kSplitMaxBlocksPerLane; k++)
+#pragma unroll
+        for (int s = 0; s < kSplit; s++) {
+            const double v = __shfl_sync(0xffffffffu, pk[k], base + s);
+            if (k * kSplit + s < nb) zo = __dadd_rn(zo, v);
+        }
+    const bool lead = valid && sl == 0;
+    double loss = 0.0;
+    int pred = 0, lab = 0;
+    if (lead) {
+        lab = labels[r];
+        const double z = __dadd_rn(zo, (double)W2[H]);
+        const float o = __double2float_rn(1.0 / (1.0 + exp(-z)));
+        const double d = (double)lab - (double)o;
+        loss = 0.5 * d * d;
+        pred = o >= 0.5f ? 1 : 0;
+    }
+    unsigned c[4];
+    c[0] = __popc(__ballot_sync(0xffffffffu, lead && pred == 1 && lab == 1));
+    c[1] = __popc(__ballot_sync(0xffffffffu, lead && pred == 0 && lab != 1));
+    c[2] = __popc(__ballot_sync(0xffffffffu, lead && pred == 1 && lab != 1));
+    c[3] = __popc(__ballot_sync(0xffffffffu, lead && pred == 0 && lab == 1));
+    if (lane == 0)
+        for (int q = 0; q < 4; q++)
+            if (c[q]) atomicAdd(counts4 + q, (unsigned long long)c[q]);
+    for (int o = 16; o > 0; o >>= 1) loss += __shfl_down_sync(0xffffffffu, loss, o);
+    if (lane == 0) lsum[threadIdx.x >> 5] = loss;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kEvalThreads / 32; w++) s += lsum[w];
+        loss_part[blockIdx.x] = s;
+    }
+}
+
+// split rows only when every lane gets a block (H = 33: 3 blocks -> 1.9x slower split)
+static bool use_split(int H, int K) {
+    const int nb = (H + 15) / 16;
+    return K == 1 && nb >= kSplit && nb <= kSplit * kSplitMaxBlocksPerLane;
+}
+
+int eval_nparts(int64_t N, int H, int K) {
+    const bool split = use_split(H, K);
+    return (int)((N + (split ? kSplitRowsPerBlock : kEvalThreads) - 1) / (split ? kSplitRowsPerBlock : kEvalThreads));
+}
+
 __global__ void eval_finish_kernel(const double* __restrict__ loss_part, int nparts, double* __restrict__ out) {
     __shared__ double sh[256];
     double s = 0.0;
@@ -128,6 +237,17 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
     const size_t wbytes = 4 * ((size_t)H * (D + 1) + (size_t)K * (H + 1));
     const int w_in_smem = wbytes <= 160 * 1024;
     const size_t smem = w_in_smem ? wbytes : 0;
+    if (use_split(H, K)) {
+        if (nparts != eval_nparts(N, H, K)) return cudaErrorInvalidValue;
+        if (smem > 48 * 1024) {
+            cudaError_t e =
+                cudaFuncSetAttribute(eval_ref64_split_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        eval_ref64_split_kernel<<<nparts, kEvalThreads, smem, st>>>(W1, W2, X, labels, N, D, H, w_in_smem, counts4,
+                                                                    loss_part);
+        return cudaGetLastError();
+    }
     auto k = K == 1 ? eval_ref64_kernel<1> : eval_ref64_kernel<0>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -104,6 +104,7 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
                               int D, int H, int K, unsigned long long* counts4, double* loss_part, int nparts,
                               cudaStream_t st);
 cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st);
+int eval_nparts(int64_t N, int H, int K);  // loss partials of launch_eval_ref64
 cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss_out, cudaStream_t st);
 
 // ------------------------------------------------------------ tcgen05 GEMM

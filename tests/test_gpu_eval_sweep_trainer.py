@@ -15,7 +15,10 @@ pytestmark = pytest.mark.gpu
 
 
 # ------------------------------------------------------------------ eval
-@pytest.mark.parametrize("N,D,H", [(1, 3, 2), (129, 33, 33), (100_000, 33, 256), (5000, 1024, 64), (77, 30, 1)])
+@pytest.mark.parametrize("N,D,H", [(1, 3, 2), (129, 33, 33), (100_000, 33, 256), (5000, 1024, 64), (77, 30, 1),
+                                   # row split over 8 lanes (H > 112): exactly 8 blocks with a partial one, uneven
+                                   # blocks per lane, 63 blocks, ragged row counts
+                                   (2003, 33, 120), (3001, 17, 513), (1501, 33, 1000), (17, 33, 128)])
 def test_eval_ref64_exact_vs_oracle(gpu, N, D, H):
     x, l = g.synthetic_arrays(max(N, 2), D, 3, "planted-linear")
     x, l = x[:N], l[:N]
