@@ -28,9 +28,14 @@ namespace glx {
 
 constexpr int k3WG = 128;
 constexpr int k3NT = 3 * k3WG;
-constexpr int k3NX = 5;  // x ring stages: B on k, A on k+1, F on k+2, 2 prefetched
-constexpr int k3NZ = 3;  // z/h/s tile slots
-constexpr int k3ZFull = 1, k3SFull = 4, k3ZEmpty = 7, k3AInt = 10, k3Epi = 11;
+#ifndef GLX3_NZ
+#define GLX3_NZ 3  // z/h/s tile slots (F on k+2, A on k+1, B on k)
+#endif
+constexpr int k3NZ = GLX3_NZ;
+constexpr int k3NX = k3NZ + 2;  // x ring stages: the z ring plus 2 prefetched
+// named barriers: per-slot z-full, s-full, z-empty, then two CTA-wide ones (<= 16)
+constexpr int k3ZFull = 1, k3SFull = 1 + k3NZ, k3ZEmpty = 1 + 2 * k3NZ, k3AInt = 1 + 3 * k3NZ, k3Epi = 2 + 3 * k3NZ;
+static_assert(k3Epi < 16, "named barrier ids");
 #ifndef GLX3_RS
 #define GLX3_RS 4  // rows per step in the forward / backward streams (RPG must be a multiple)
 #endif
