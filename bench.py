@@ -105,7 +105,7 @@ class ClockSampler:
 
 
 # --------------------------------------------------------- CPU baselines
-def cpu_baseline_batch(feats, targets, target_s=10.0):
+def cpu_baseline_batch(feats, targets, target_s=20.0):  # the 4096-row calibration overestimates ~2x
     """Oracle port of the full-batch restatement, all host cores, bounded sample."""
     from oracle import oracle as O
 
@@ -116,13 +116,15 @@ def cpu_baseline_batch(feats, targets, target_s=10.0):
     t0 = time.perf_counter()
     O.train_batch_par(w1, w2, feats[:n], targets[:n], 1, LR, nw)
     dt = max(time.perf_counter() - t0, 1e-6)
-    n = int(min(feats.shape[0], max(4096, n * target_s / dt)))
+    want = n * target_s / dt  # sample-epochs for ~target_s of CPU work
+    n = int(min(feats.shape[0], max(4096, want)))
+    epochs = max(1, int(round(want / n)))  # all rows fit: repeat epochs to fill the budget
     t0 = time.perf_counter()
-    O.train_batch_par(w1, w2, feats[:n], targets[:n], 1, LR, nw)
+    O.train_batch_par(w1, w2, feats[:n], targets[:n], epochs, LR, nw)
     dt = time.perf_counter() - t0
-    return {"value": n / dt, "unit": UNIT, "cores": nw, "kind": "port",
+    return {"value": n * epochs / dt, "unit": UNIT, "cores": nw, "kind": "port",
             "sample": f"oracle train_batch_par (full-batch restatement, f64 reference op order), "
-                      f"{n} of the rows x 1 epoch, {dt:.1f} s"}
+                      f"{n} of the rows x {epochs} epochs, {dt:.1f} s"}
 
 
 def _reference_engines(nw):
