@@ -126,6 +126,24 @@ int glx_pack_rows_minmax(const float* X, const float* T, const uint8_t* labels, 
  * columns -> 0, clamped to [-0.5, 1.5]; Y may alias X. Inputs are finite
  * (NaN propagation of numpy's min/max is not reproduced). */
 int glx_minmax_fit(const float* X, int64_t N, int32_t D, float* col_min, float* col_max, void* stream);
+
+/* Benchmark rows on the device (replacing dataset.synthetic_matrix's host
+ * generation, dataset.py:260-289): numpy's PCG64 stream
+ * reproduced bit for bit by jump-ahead. state/inc = the 128-bit PCG64 state
+ * and increment of default_rng(seed) (bit_generator.state), split hi/lo.
+ * glx_pcg64_uniform_f32: out[i] = the i-th float32 draw (Generator.random(
+ * dtype=float32)) counted from 64-bit output first_output (two floats per
+ * output, low half first). glx_pcg64_coin: labels[r] = 1 iff the float64 draw
+ * of output first_output + r is < 0.5 (Generator.random() < 0.5).
+ * glx_planted_score: score[r] = sum_q f64(X[r, pick[q]]) * coef[q] (device
+ * pick/coef); glx_label_ge: labels[r] = score[r] >= *threshold (device). */
+int glx_pcg64_uniform_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t first_output,
+                          int64_t n_floats, float* out, void* stream);
+int glx_pcg64_coin(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t first_output,
+                   int64_t n, uint8_t* labels, void* stream);
+int glx_planted_score(const float* X, int64_t N, int32_t D, const int32_t* pick, const double* coef, int32_t k,
+                      double* score, void* stream);
+int glx_label_ge(const double* score, int64_t N, const double* threshold, uint8_t* labels, void* stream);
 int glx_minmax_apply(const float* X, int64_t N, int32_t D, const float* col_min, const float* col_max, float* Y,
                      void* stream);
 

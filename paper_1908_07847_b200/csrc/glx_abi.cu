@@ -399,6 +399,37 @@ int glx_pack_rows_minmax(const float* X, const float* T, const uint8_t* labels, 
     return GLX_OK;
 }
 
+int glx_pcg64_uniform_f32(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t first_output,
+                          int64_t n_floats, float* out, void* stream) {
+    if (first_output < 0 || n_floats < 0) return set_err(GLX_ERR_INVALID, "bad pcg64 range");
+    const uint64_t st4[4] = {state_hi, state_lo, inc_hi, inc_lo};
+    GLX_LAUNCH(launch_pcg64_f32(st4, first_output, n_floats, out, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_pcg64_coin(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t first_output,
+                   int64_t n, uint8_t* labels, void* stream) {
+    if (first_output < 0 || n < 0) return set_err(GLX_ERR_INVALID, "bad pcg64 range");
+    const uint64_t st4[4] = {state_hi, state_lo, inc_hi, inc_lo};
+    GLX_LAUNCH(launch_pcg64_coin(st4, first_output, n, labels, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_planted_score(const float* X, int64_t N, int32_t D, const int32_t* pick, const double* coef, int32_t k,
+                      double* score, void* stream) {
+    if (N < 0 || D < 1 || k < 1 || k > D) return set_err(GLX_ERR_SHAPE, "bad planted-score shape");
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_planted_score(X, N, D, pick, coef, k, score, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_label_ge(const double* score, int64_t N, const double* threshold, uint8_t* labels, void* stream) {
+    if (N < 0) return set_err(GLX_ERR_SHAPE, "bad label shape");
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_label_ge(score, N, threshold, labels, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
 int glx_minmax_fit(const float* X, int64_t N, int32_t D, float* col_min, float* col_max, void* stream) {
     if (N < 1 || D < 1) return set_err(GLX_ERR_SHAPE, "normalize_fit needs at least one row and column");
     cudaStream_t st = (cudaStream_t)stream;

@@ -452,4 +452,126 @@ cudaError_t launch_minmax_apply(const float* X, int64_t N, int D, const float* c
     return cudaGetLastError();
 }
 
+
+// ============================================================ synthetic rows
+// numpy's Generator(PCG64(seed)) on the device (reference dataset.py:260-289):
+// a 128-bit LCG s <- s * M + inc whose 64-bit outputs are XSL-RR(s) of the
+// state after each step; float32 draws use the low then the high 32 bits of one
+// output as (u >> 8) * 2^-24, float64 draws use (u >> 11) * 2^-53. Jump-ahead
+// (s_{k+n} = A_n s_k + C_n) lets thread t produce outputs t, t + T, t + 2T, ...,
+// so a warp's stores are coalesced and the bytes equal numpy's sequential draws.
+namespace pcg {
+typedef unsigned __int128 u128;
+__host__ __device__ inline u128 mk(uint64_t hi, uint64_t lo) { return ((u128)hi << 64) | lo; }
+__device__ __forceinline__ uint64_t xsl_rr(u128 s) {
+    const uint64_t hi = (uint64_t)(s >> 64), lo = (uint64_t)s;
+    const uint64_t x = hi ^ lo;
+    const unsigned rot = (unsigned)(hi >> 58);
+    return (x >> rot) | (x << ((64u - rot) & 63u));
+}
+// (A, C) of n steps of s <- s * m + c
+__device__ inline void jump(u128 m, u128 c, uint64_t n, u128& A, u128& C) {
+    A = 1;
+    C = 0;
+    while (n) {
+        if (n & 1) {
+            A *= m;
+            C = C * m + c;
+        }
+        c = (m + 1) * c;
+        m *= m;
+        n >>= 1;
+    }
+}
+constexpr uint64_t kMultHi = 0x2360ed051fc65da4ULL, kMultLo = 0x4385df649fccf645ULL;
+}  // namespace pcg
+
+// out[i] for i < n_floats, float i = half (i & 1) of output first + i / 2
+__global__ void pcg64_f32_kernel(uint64_t s_hi, uint64_t s_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t first,
+                                 int64_t n_floats, float2* __restrict__ out2, float* __restrict__ out_tail) {
+    using namespace pcg;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n_out = (n_floats + 1) / 2;
+    if (t >= n_out) return;
+    u128 A, C;
+    jump(mk(kMultHi, kMultLo), mk(inc_hi, inc_lo), (uint64_t)(first + t + 1), A, C);
+    u128 s = A * mk(s_hi, s_lo) + C;
+    u128 aT, cT;  // T steps at once (thread stride)
+    jump(mk(kMultHi, kMultLo), mk(inc_hi, inc_lo), (uint64_t)T, aT, cT);
+    for (int64_t k = t; k < n_out; k += T) {
+        const uint64_t v = xsl_rr(s);
+        const float f0 = (float)((uint32_t)v >> 8) * (1.0f / 16777216.0f);
+        const float f1 = (float)((uint32_t)(v >> 32) >> 8) * (1.0f / 16777216.0f);
+        if (2 * k + 1 < n_floats) out2[k] = make_float2(f0, f1);
+        else out_tail[0] = f0;  // odd count: the last output's low half only
+        s = aT * s + cT;
+    }
+}
+
+// labels[r] = (float64 draw of output first + r) < 0.5, i.e. the output's top bit is 0
+__global__ void pcg64_coin_kernel(uint64_t s_hi, uint64_t s_lo, uint64_t inc_hi, uint64_t inc_lo, int64_t first,
+                                  int64_t n, uint8_t* __restrict__ labels) {
+    using namespace pcg;
+    const int64_t T = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    u128 A, C;
+    jump(mk(kMultHi, kMultLo), mk(inc_hi, inc_lo), (uint64_t)(first + t + 1), A, C);
+    u128 s = A * mk(s_hi, s_lo) + C;
+    u128 aT, cT;  // T steps at once (thread stride)
+    jump(mk(kMultHi, kMultLo), mk(inc_hi, inc_lo), (uint64_t)T, aT, cT);
+    for (int64_t k = t; k < n; k += T) {
+        labels[k] = (xsl_rr(s) >> 63) == 0 ? 1 : 0;
+        s = aT * s + cT;
+    }
+}
+
+// planted-linear score: f64 sum over the picked columns, in pick order
+__global__ void planted_score_kernel(const float* __restrict__ X, int64_t N, int D, const int* __restrict__ pick,
+                                     const double* __restrict__ coef, int k, double* __restrict__ score) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= N) return;
+    double s = 0.0;
+    for (int q = 0; q < k; q++) s = __dadd_rn(s, __dmul_rn((double)X[r * D + pick[q]], coef[q]));
+    score[r] = s;
+}
+
+__global__ void label_ge_kernel(const double* __restrict__ score, int64_t N, const double* __restrict__ thr,
+                                uint8_t* __restrict__ labels) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < N) labels[r] = score[r] >= *thr ? 1 : 0;
+}
+
+static int pcg_grid(int64_t n) {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, (int64_t)sms * 8));
+}
+
+cudaError_t launch_pcg64_f32(const uint64_t* st4, int64_t first, int64_t n_floats, float* out, cudaStream_t st) {
+    if (n_floats <= 0) return cudaSuccess;
+    const int64_t n_out = (n_floats + 1) / 2;
+    pcg64_f32_kernel<<<pcg_grid(n_out), 256, 0, st>>>(st4[0], st4[1], st4[2], st4[3], first, n_floats,
+                                                      reinterpret_cast<float2*>(out), out + (n_floats - 1));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pcg64_coin(const uint64_t* st4, int64_t first, int64_t n, uint8_t* labels, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    pcg64_coin_kernel<<<pcg_grid(n), 256, 0, st>>>(st4[0], st4[1], st4[2], st4[3], first, n, labels);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_planted_score(const float* X, int64_t N, int D, const int* pick, const double* coef, int k,
+                                 double* score, cudaStream_t st) {
+    planted_score_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(X, N, D, pick, coef, k, score);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_label_ge(const double* score, int64_t N, const double* thr, uint8_t* labels, cudaStream_t st) {
+    label_ge_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(score, N, thr, labels);
+    return cudaGetLastError();
+}
+
 }  // namespace glx

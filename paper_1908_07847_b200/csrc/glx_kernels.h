@@ -105,6 +105,12 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
                               cudaStream_t st);
 cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st);
 int eval_nparts(int64_t N, int H, int K);  // loss partials of launch_eval_ref64
+// numpy PCG64 streams on the device (glx_data.cu); st4 = state hi, lo, inc hi, lo
+cudaError_t launch_pcg64_f32(const uint64_t* st4, int64_t first, int64_t n_floats, float* out, cudaStream_t st);
+cudaError_t launch_pcg64_coin(const uint64_t* st4, int64_t first, int64_t n, uint8_t* labels, cudaStream_t st);
+cudaError_t launch_planted_score(const float* X, int64_t N, int D, const int* pick, const double* coef, int k,
+                                 double* score, cudaStream_t st);
+cudaError_t launch_label_ge(const double* score, int64_t N, const double* thr, uint8_t* labels, cudaStream_t st);
 cudaError_t launch_eval_finish(const double* loss_part, int nparts, double* loss_out, cudaStream_t st);
 
 // ------------------------------------------------------------ tcgen05 GEMM

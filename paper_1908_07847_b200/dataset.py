@@ -213,3 +213,70 @@ def normalize_split(pair: SplitPair, device: int = 0) -> SplitPair:
     stats = normalize_fit(pair.train, device)
     return SplitPair(train=normalize_apply(pair.train, stats, device), test=normalize_apply(pair.test, stats, device),
                      seed=pair.seed, fraction=pair.fraction, stratified=pair.stratified)
+
+
+# ------------------------------------------------------------- device generation
+def _split128(v: int) -> tuple[int, int]:
+    return (v >> 64) & 0xFFFFFFFFFFFFFFFF, v & 0xFFFFFFFFFFFFFFFF
+
+
+def _post_feature_generator(seed: int, n_floats: int) -> np.random.Generator:
+    """default_rng(seed) in the state synthetic_arrays leaves after drawing n_floats
+    float32 features (PCG64.advance over the 64-bit outputs, plus the buffered
+    32-bit half when n_floats is odd)."""
+    k0 = (n_floats + 1) // 2
+    gen = np.random.default_rng(seed)
+    gen.bit_generator.advance(k0)
+    if n_floats % 2:
+        g = np.random.default_rng(seed)
+        g.bit_generator.advance(k0 - 1)
+        v = int(g.bit_generator.random_raw(1)[0])
+        st = gen.bit_generator.state
+        st["has_uint32"] = 1
+        st["uinteger"] = v >> 32
+        gen.bit_generator.state = st
+    return gen
+
+
+def synthetic_arrays_device(rows: int, columns: int, seed: int, signal: str = "random", device: int = 0):
+    """synthetic_arrays generated on the device: (features (rows, columns) f32,
+    labels (rows,) u8) as torch tensors on cuda:device, byte-identical to the host
+    generator (dataset.py:260-289). The PCG64 stream is evaluated by jump-ahead on
+    the GPU (csrc/glx_data.cu); the planted hyperplane's 5 columns and N(0,1)
+    weights are drawn on the host from the generator advanced past the features,
+    scores and labels (score >= median, numpy's two-middle-values mean) on the
+    device."""
+    import torch
+
+    _check_synth_args(rows, columns, signal)
+    L = _lib.load()
+    dev = torch.device("cuda", device)
+    st = np.random.default_rng(seed).bit_generator.state["state"]
+    s_hi, s_lo = _split128(int(st["state"]))
+    i_hi, i_lo = _split128(int(st["inc"]))
+    n_floats = rows * columns
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        X = torch.empty((rows, columns), dtype=torch.float32, device=dev)
+        labels = torch.empty(rows, dtype=torch.uint8, device=dev)
+        _lib.check(L.glx_pcg64_uniform_f32(s_hi, s_lo, i_hi, i_lo, 0, n_floats, X.data_ptr(), stream))
+        if signal == "random":
+            _lib.check(L.glx_pcg64_coin(s_hi, s_lo, i_hi, i_lo, (n_floats + 1) // 2, rows, labels.data_ptr(), stream))
+            return X, labels
+        gen = _post_feature_generator(seed, n_floats)
+        pick = gen.choice(columns, size=min(5, columns), replace=False)
+        coef = gen.normal(0.0, 1.0, size=pick.shape[0])
+        pk = torch.from_numpy(pick.astype(np.int32)).to(dev)
+        cf = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.float64)).to(dev)
+        score = torch.empty(rows, dtype=torch.float64, device=dev)
+        _lib.check(L.glx_planted_score(X.data_ptr(), rows, columns, pk.data_ptr(), cf.data_ptr(), int(pick.shape[0]),
+                                       score.data_ptr(), stream))
+        # numpy median: the middle value, or the mean of the two middle values
+        # (a device sort: 31 ms at 64Mi rows, where torch.kthvalue took 0.75 s)
+        srt = torch.sort(score).values
+        lo = srt[(rows - 1) // 2]
+        med = lo if rows % 2 else (lo + srt[rows // 2]) / 2.0
+        del srt
+        thr = med.reshape(1).contiguous()
+        _lib.check(L.glx_label_ge(score.data_ptr(), rows, thr.data_ptr(), labels.data_ptr(), stream))
+        return X, labels
