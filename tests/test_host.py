@@ -156,3 +156,21 @@ def test_shard_bounds_partition(n, w):
     assert b[0][0] == 0 and b[-1][1] == n
     assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
     assert max(e - s for s, e in b) - min(e - s for s, e in b) <= 1
+
+
+@pytest.mark.parametrize("rows,cols,seed", [(120, 33, 7), (257, 5, 3), (11, 3, 5), (1000, 1, 2)])
+def test_post_feature_generator_matches_reference_draws(rows, cols, seed):
+    """The host half of synthetic_arrays_device: default_rng(seed) advanced past the
+    float32 features (including the buffered 32-bit half when rows*cols is odd)
+    draws the same planted columns and weights as synthetic_arrays."""
+    from paper_1908_07847_b200.dataset import _post_feature_generator, _split128
+
+    ref = np.random.default_rng(seed)
+    ref.random((rows, cols), dtype=np.float32)
+    pick = ref.choice(cols, size=min(5, cols), replace=False)
+    coef = ref.normal(0.0, 1.0, size=pick.shape[0])
+    gen = _post_feature_generator(seed, rows * cols)
+    assert (gen.choice(cols, size=min(5, cols), replace=False) == pick).all()
+    assert (gen.normal(0.0, 1.0, size=pick.shape[0]) == coef).all()
+    hi, lo = _split128((1 << 127) + 5)
+    assert hi == 1 << 63 and lo == 5
