@@ -205,6 +205,16 @@ int glx_wide_apply(float* w_ih, float* w_ho, const double* grad, double lr_over_
 int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
                    int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream);
 
+/* ---------------------------------------------------- per-instance API */
+/* network.forward (network.py:128-135) for N rows, the reference's f64 order:
+ * hidden (device, N x H f32) and out (device, N x K f32) activations. */
+int glx_forward(const float* w_ih, const float* w_ho, const float* X, int64_t N, int32_t D, int32_t H, int32_t K,
+                float* hidden, float* out, void* stream);
+/* network.loss_gradients (network.py:144-165) for one row, one output, from its
+ * forward activations: g_ih (H x (D+1) f64) and g_ho (H+1 f64), device. */
+int glx_instance_gradients(const float* w_ho, const float* x, const float* hidden, const float* out, double target,
+                           int32_t D, int32_t H, double* g_ih, double* g_ho, void* stream);
+
 /* ------------------------------------------------------------ diagnostics */
 /* Number of CUDA kernels this library has launched (for launch accounting). */
 uint64_t glx_launch_count(void);

@@ -510,6 +510,26 @@ int glx_eval(const float* w_ih, const float* w_ho, const float* X, const uint8_t
     return GLX_OK;
 }
 
+int glx_forward(const float* w_ih, const float* w_ho, const float* X, int64_t N, int32_t D, int32_t H, int32_t K,
+                float* hidden, float* out, void* stream) {
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    if (K < 1 || K > 16) return set_err(GLX_ERR_INVALID, "output_dim must be in [1, 16], got %d", K);
+    if (!hidden || !out) return set_err(GLX_ERR_INVALID, "hidden and out are required");
+    if (N == 0) return GLX_OK;
+    GLX_CK(launch_forward(w_ih, w_ho, X, N, D, H, K, hidden, out, (cudaStream_t)stream));
+    g_launches.fetch_add(2);
+    return GLX_OK;
+}
+
+int glx_instance_gradients(const float* w_ho, const float* x, const float* hidden, const float* out, double target,
+                           int32_t D, int32_t H, double* g_ih, double* g_ho, void* stream) {
+    int rc = check_dims(1, D, H);
+    if (rc) return rc;
+    GLX_LAUNCH(launch_instance_gradients(w_ho, x, hidden, out, target, D, H, g_ih, g_ho, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
 int glx_eval_packed(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
                     double* stats, void* stream) {
     int rc = check_dims(N, D, H);

@@ -210,6 +210,87 @@ static bool use_split(int H, int K) {
     return K == 1 && nb >= kSplit && nb <= kSplit * kSplitMaxBlocksPerLane;
 }
 
+// ----------------------------------------------------------- per-instance API
+// network.forward (network.py:128-135) for N rows: hidden[r][j] and out[r][k] are
+// _activation's f32 results (kernels.py:102-122), the reference's f64 order.
+__global__ void forward_hidden_kernel(const float* __restrict__ W1, const float* __restrict__ X, int64_t N, int D,
+                                      int H, float* __restrict__ hidden) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * H) return;
+    const int64_t r = e / H;
+    const int j = (int)(e - r * H);
+    const float* wr = W1 + (int64_t)j * (D + 1);
+    const float* x = X + r * D;
+    double acc = 0.0;
+    for (int b0 = 0; b0 < D; b0 += 16) {
+        const int b1 = b0 + 16 < D ? b0 + 16 : D;
+        double part = 0.0;
+        for (int i = b0; i < b1; i++) part = fma((double)wr[i], (double)x[i], part);
+        acc = __dadd_rn(acc, part);
+    }
+    const double z = __dadd_rn(acc, (double)wr[D]);
+    hidden[e] = __double2float_rn(1.0 / (1.0 + exp(-z)));
+}
+
+__global__ void forward_output_kernel(const float* __restrict__ W2, const float* __restrict__ hidden, int64_t N, int H,
+                                      int K, float* __restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= N * K) return;
+    const int64_t r = e / K;
+    const int k = (int)(e - r * K);
+    const float* wr = W2 + (int64_t)k * (H + 1);
+    const float* h = hidden + r * H;
+    double acc = 0.0;
+    for (int b0 = 0; b0 < H; b0 += 16) {
+        const int b1 = b0 + 16 < H ? b0 + 16 : H;
+        double part = 0.0;
+        for (int j = b0; j < b1; j++) part = fma((double)wr[j], (double)h[j], part);
+        acc = __dadd_rn(acc, part);
+    }
+    const double z = __dadd_rn(acc, (double)wr[H]);
+    out[e] = __double2float_rn(1.0 / (1.0 + exp(-z)));
+}
+
+// network.loss_gradients (network.py:144-165) for one row and one output, f64:
+// delta_o = ((o - t) o)(1 - o); g_ho = delta_o [h, 1]; err_h = w_ho delta_o;
+// delta_h = (err_h h)(1 - h); g_ih = delta_h [x, 1] (layer_backward_seq order)
+__global__ void instance_gradients_kernel(const float* __restrict__ W2, const float* __restrict__ x,
+                                          const float* __restrict__ hidden, const float* __restrict__ out,
+                                          double target, int D, int H, double* __restrict__ g_ih,
+                                          double* __restrict__ g_ho) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j > H) return;
+    const double o = (double)out[0];
+    const double d_o = __dmul_rn(__dmul_rn(__dsub_rn(o, target), o), __dsub_rn(1.0, o));
+    if (j == H) {
+        g_ho[H] = d_o;
+        return;
+    }
+    const double h = (double)hidden[j];
+    g_ho[j] = __dmul_rn(d_o, h);
+    const double err_h = __dadd_rn(0.0, __dadd_rn(0.0, __dmul_rn((double)W2[j], d_o)));
+    const double d_h = __dmul_rn(__dmul_rn(err_h, h), __dsub_rn(1.0, h));
+    double* gr = g_ih + (int64_t)j * (D + 1);
+    for (int i = 0; i < D; i++) gr[i] = __dmul_rn(d_h, (double)x[i]);
+    gr[D] = d_h;
+}
+
+cudaError_t launch_forward(const float* W1, const float* W2, const float* X, int64_t N, int D, int H, int K,
+                           float* hidden, float* out, cudaStream_t st) {
+    const int64_t nh = N * H, no = N * K;
+    forward_hidden_kernel<<<(unsigned)((nh + 127) / 128), 128, 0, st>>>(W1, X, N, D, H, hidden);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    forward_output_kernel<<<(unsigned)((no + 127) / 128), 128, 0, st>>>(W2, hidden, N, H, K, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_instance_gradients(const float* W2, const float* x, const float* hidden, const float* out,
+                                      double target, int D, int H, double* g_ih, double* g_ho, cudaStream_t st) {
+    instance_gradients_kernel<<<(H + 1 + 127) / 128, 128, 0, st>>>(W2, x, hidden, out, target, D, H, g_ih, g_ho);
+    return cudaGetLastError();
+}
+
 int eval_nparts(int64_t N, int H, int K) {
     const bool split = use_split(H, K);
     return (int)((N + (split ? kSplitRowsPerBlock : kEvalThreads) - 1) / (split ? kSplitRowsPerBlock : kEvalThreads));

@@ -105,6 +105,10 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
                               cudaStream_t st);
 cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st);
 int eval_nparts(int64_t N, int H, int K);  // loss partials of launch_eval_ref64
+cudaError_t launch_forward(const float* W1, const float* W2, const float* X, int64_t N, int D, int H, int K,
+                           float* hidden, float* out, cudaStream_t st);
+cudaError_t launch_instance_gradients(const float* W2, const float* x, const float* hidden, const float* out,
+                                      double target, int D, int H, double* g_ih, double* g_ho, cudaStream_t st);
 // numpy PCG64 streams on the device (glx_data.cu); st4 = state hi, lo, inc hi, lo
 cudaError_t launch_pcg64_f32(const uint64_t* st4, int64_t first, int64_t n_floats, float* out, cudaStream_t st);
 cudaError_t launch_pcg64_coin(const uint64_t* st4, int64_t first, int64_t n, uint8_t* labels, cudaStream_t st);
