@@ -210,6 +210,15 @@ int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, con
  * hidden (device, N x H f32) and out (device, N x K f32) activations. */
 int glx_forward(const float* w_ih, const float* w_ho, const float* X, int64_t N, int32_t D, int32_t H, int32_t K,
                 float* hidden, float* out, void* stream);
+/* Layer-level API (backend.py:73-205, kernels.py:163-257), device buffers, the
+ * reference's f64 order. glx_layer_forward: out[r][j] = _activation of neuron j
+ * (W: n x (m+1) f32, bias last) on input row r of X (N x m). glx_layer_backward:
+ * deltas[j] = (err[j] a_j)(1 - a_j), grads[j] = deltas[j] [x, 1] (n x (m+1) f64).
+ * glx_backprop_error: err_prev[i] = sum_j W[j][i] deltas[j], 16-blocked over j. */
+int glx_layer_forward(const float* W, const float* X, int64_t N, int32_t m, int32_t n, float* out, void* stream);
+int glx_layer_backward(const float* x, const float* acts, const double* err, int32_t n, int32_t m, double* deltas,
+                       double* grads, void* stream);
+int glx_backprop_error(const float* W, const double* deltas, int32_t n, int32_t m, double* err_prev, void* stream);
 /* network.loss_gradients (network.py:144-165) for one row, one output, from its
  * forward activations: g_ih (H x (D+1) f64) and g_ho (H+1 f64), device. */
 int glx_instance_gradients(const float* w_ho, const float* x, const float* hidden, const float* out, double target,

@@ -64,6 +64,9 @@ SIGNATURES = {
     "glx_pack_rows_minmax": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp, _vp, _vp]),
     "glx_minmax_fit": (_int, [_vp, _i64, _i32, _vp, _vp, _vp]),
     "glx_forward": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
+    "glx_layer_forward": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
+    "glx_layer_backward": (_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "glx_backprop_error": (_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
     "glx_instance_gradients": (_int, [_vp, _vp, _vp, _vp, _dbl, _i32, _i32, _vp, _vp, _vp]),
     "glx_pcg64_uniform_f32": (_int, [_u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp]),
     "glx_pcg64_coin": (_int, [_u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp]),

@@ -226,3 +226,98 @@ def eval_counts(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, lab
                 kind: BackendKind | None = None) -> tuple[int, int, int, int]:
     """Drop-in for kernels.eval_counts (kernels.py:352-375)."""
     return eval_counts_loss(w_ih2d, w_ho2d, feats2d, labels, kind)[0]
+
+
+# ------------------------------------------------------- layer-level API
+@dataclass
+class LayerJob:
+    """One dense layer pass (backend.py:73-102): weights (n_neurons x (n_inputs+1)),
+    inputs, outputs; the same validation as the reference."""
+
+    weights: np.ndarray
+    inputs: np.ndarray
+    outputs: np.ndarray
+
+    def __post_init__(self) -> None:
+        if self.weights.ndim != 2 or self.weights.dtype != np.float32:
+            raise ShapeError("weights must be a 2-D float32 array")
+        if self.inputs.ndim != 1 or self.inputs.dtype != np.float32:
+            raise ShapeError("inputs must be a 1-D float32 array")
+        if self.weights.shape[1] != self.inputs.shape[0] + 1:
+            raise ShapeError(f"weights row length {self.weights.shape[1]} != n_inputs+1 ({self.inputs.shape[0]}+1)")
+        if self.outputs.shape != (self.weights.shape[0],) or self.outputs.dtype != np.float32:
+            raise ShapeError("outputs must be a float32 array with one slot per neuron")
+
+    @classmethod
+    def create(cls, weights: np.ndarray, inputs: np.ndarray) -> "LayerJob":
+        w = np.ascontiguousarray(weights, dtype=np.float32)
+        x = np.ascontiguousarray(inputs, dtype=np.float32)
+        return cls(weights=w, inputs=x, outputs=np.empty(w.shape[0], dtype=np.float32))
+
+
+def _dev(kind: BackendKind | None):
+    import torch
+
+    return torch.device("cuda", (kind or sequential()).device)
+
+
+def run_layer_forward(job: LayerJob, kind: BackendKind | None = None, debug: bool = False) -> np.ndarray:
+    """outputs[j] = sigmoid(dot(weights row j, inputs) + bias_j), filled in place
+    (backend.py:134-144), on the device in the reference's f64 order. `debug`
+    (the reference's write-once check of its thread pool) has no device analogue:
+    each neuron is one thread's single store."""
+    import torch
+
+    L = _lib.load()
+    dev = _dev(kind)
+    n, m1 = job.weights.shape
+    W = torch.from_numpy(np.ascontiguousarray(job.weights)).to(dev)
+    x = torch.from_numpy(np.ascontiguousarray(job.inputs)).to(dev)
+    out = torch.empty(n, dtype=torch.float32, device=dev)
+    _lib.check(L.glx_layer_forward(W.data_ptr(), x.data_ptr(), 1, m1 - 1, n, out.data_ptr(),
+                                   torch.cuda.current_stream(dev).cuda_stream))
+    job.outputs[:] = out.cpu().numpy()
+    return job.outputs
+
+
+def run_layer_backward(job: LayerJob, upstream_error: np.ndarray, kind: BackendKind | None = None,
+                       debug: bool = False) -> tuple[np.ndarray, np.ndarray]:
+    """Per-neuron deltas and gradient rows for one layer (backend.py:147-189):
+    deltas[j] = (err_j a_j)(1 - a_j), grads[j] = deltas[j] [inputs, 1], f64, with
+    job.outputs holding the layer's forward activations."""
+    import torch
+
+    n, m1 = job.weights.shape
+    err = np.ascontiguousarray(upstream_error, dtype=np.float64)
+    if err.shape != (n,):
+        raise ShapeError(f"upstream_error must have shape ({n},), got {err.shape}")
+    L = _lib.load()
+    dev = _dev(kind)
+    x = torch.from_numpy(np.ascontiguousarray(job.inputs)).to(dev)
+    a = torch.from_numpy(np.ascontiguousarray(job.outputs)).to(dev)
+    e = torch.from_numpy(err).to(dev)
+    deltas = torch.empty(n, dtype=torch.float64, device=dev)
+    grads = torch.empty((n, m1), dtype=torch.float64, device=dev)
+    _lib.check(L.glx_layer_backward(x.data_ptr(), a.data_ptr(), e.data_ptr(), n, m1 - 1, deltas.data_ptr(),
+                                    grads.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    return deltas.cpu().numpy(), grads.cpu().numpy()
+
+
+def backpropagate_error(weights: np.ndarray, deltas: np.ndarray, kind: BackendKind | None = None) -> np.ndarray:
+    """Fold a layer's deltas back into upstream error terms, W^T @ delta without the
+    bias column, 16-blocked over neurons (backend.py:192-205)."""
+    import torch
+
+    w = np.ascontiguousarray(weights, dtype=np.float32)
+    d = np.ascontiguousarray(deltas, dtype=np.float64)
+    if w.ndim != 2 or d.shape != (w.shape[0],):
+        raise ShapeError("weights must be (n, m+1) and deltas length n")
+    n, m1 = w.shape
+    L = _lib.load()
+    dev = _dev(kind)
+    W = torch.from_numpy(w).to(dev)
+    D = torch.from_numpy(d).to(dev)
+    out = torch.empty(m1 - 1, dtype=torch.float64, device=dev)
+    _lib.check(L.glx_backprop_error(W.data_ptr(), D.data_ptr(), n, m1 - 1, out.data_ptr(),
+                                    torch.cuda.current_stream(dev).cuda_stream))
+    return out.cpu().numpy()

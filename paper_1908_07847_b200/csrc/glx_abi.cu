@@ -522,6 +522,26 @@ int glx_forward(const float* w_ih, const float* w_ho, const float* X, int64_t N,
     return GLX_OK;
 }
 
+int glx_layer_forward(const float* W, const float* X, int64_t N, int32_t m, int32_t n, float* out, void* stream) {
+    if (N < 0 || m < 1 || n < 1) return set_err(GLX_ERR_SHAPE, "bad layer shape (N=%lld m=%d n=%d)", (long long)N, m, n);
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_layer_forward(W, X, N, m, n, out, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_layer_backward(const float* x, const float* acts, const double* err, int32_t n, int32_t m, double* deltas,
+                       double* grads, void* stream) {
+    if (m < 0 || n < 1) return set_err(GLX_ERR_SHAPE, "bad layer shape (m=%d n=%d)", m, n);
+    GLX_LAUNCH(launch_layer_backward(x, acts, err, n, m, deltas, grads, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_backprop_error(const float* W, const double* deltas, int32_t n, int32_t m, double* err_prev, void* stream) {
+    if (m < 1 || n < 1) return set_err(GLX_ERR_SHAPE, "bad layer shape (m=%d n=%d)", m, n);
+    GLX_LAUNCH(launch_backprop_error(W, deltas, n, m, err_prev, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
 int glx_instance_gradients(const float* w_ho, const float* x, const float* hidden, const float* out, double target,
                            int32_t D, int32_t H, double* g_ih, double* g_ho, void* stream) {
     int rc = check_dims(1, D, H);

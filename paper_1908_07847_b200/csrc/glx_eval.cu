@@ -275,6 +275,55 @@ __global__ void instance_gradients_kernel(const float* __restrict__ W2, const fl
     gr[D] = d_h;
 }
 
+// backend.run_layer_backward (backend.py:147-189 -> kernels.layer_backward_seq):
+// deltas[j] = (err[j] a_j)(1 - a_j), grads[j] = deltas[j] [x, 1], f64
+__global__ void layer_backward_kernel(const float* __restrict__ x, const float* __restrict__ acts,
+                                      const double* __restrict__ err, int n, int m, double* __restrict__ deltas,
+                                      double* __restrict__ grads) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const double a = (double)acts[j];
+    const double d = __dmul_rn(__dmul_rn(err[j], a), __dsub_rn(1.0, a));
+    deltas[j] = d;
+    double* g = grads + (int64_t)j * (m + 1);
+    for (int i = 0; i < m; i++) g[i] = __dmul_rn(d, (double)x[i]);
+    g[m] = d;
+}
+
+// backend.backpropagate_error (backend.py:192-205 -> kernels.backprop_error_seq):
+// err_prev[i] = sum_j f64(W[j][i]) deltas[j], 16-blocked over j in order
+__global__ void backprop_error_kernel(const float* __restrict__ W, const double* __restrict__ deltas, int n, int m,
+                                      double* __restrict__ err_prev) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= m) return;
+    double acc = 0.0;
+    for (int b0 = 0; b0 < n; b0 += 16) {
+        const int b1 = b0 + 16 < n ? b0 + 16 : n;
+        double part = 0.0;
+        for (int j = b0; j < b1; j++) part = __dadd_rn(part, __dmul_rn((double)W[(int64_t)j * (m + 1) + i], deltas[j]));
+        acc = __dadd_rn(acc, part);
+    }
+    err_prev[i] = acc;
+}
+
+cudaError_t launch_layer_forward(const float* W, const float* X, int64_t N, int m, int n, float* out, cudaStream_t st) {
+    const int64_t e = N * n;
+    forward_hidden_kernel<<<(unsigned)((e + 127) / 128), 128, 0, st>>>(W, X, N, m, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_layer_backward(const float* x, const float* acts, const double* err, int n, int m, double* deltas,
+                                  double* grads, cudaStream_t st) {
+    layer_backward_kernel<<<(n + 127) / 128, 128, 0, st>>>(x, acts, err, n, m, deltas, grads);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_backprop_error(const float* W, const double* deltas, int n, int m, double* err_prev,
+                                  cudaStream_t st) {
+    backprop_error_kernel<<<(m + 127) / 128, 128, 0, st>>>(W, deltas, n, m, err_prev);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_forward(const float* W1, const float* W2, const float* X, int64_t N, int D, int H, int K,
                            float* hidden, float* out, cudaStream_t st) {
     const int64_t nh = N * H, no = N * K;

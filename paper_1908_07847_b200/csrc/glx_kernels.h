@@ -105,6 +105,11 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
                               cudaStream_t st);
 cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st);
 int eval_nparts(int64_t N, int H, int K);  // loss partials of launch_eval_ref64
+cudaError_t launch_layer_forward(const float* W, const float* X, int64_t N, int m, int n, float* out, cudaStream_t st);
+cudaError_t launch_layer_backward(const float* x, const float* acts, const double* err, int n, int m, double* deltas,
+                                  double* grads, cudaStream_t st);
+cudaError_t launch_backprop_error(const float* W, const double* deltas, int n, int m, double* err_prev,
+                                  cudaStream_t st);
 cudaError_t launch_forward(const float* W1, const float* W2, const float* X, int64_t N, int D, int H, int K,
                            float* hidden, float* out, cudaStream_t st);
 cudaError_t launch_instance_gradients(const float* W2, const float* x, const float* hidden, const float* out,

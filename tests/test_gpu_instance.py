@@ -97,3 +97,52 @@ def test_backprop_update_contract(gpu):
         g.backprop_update(net, [0.1, 0.2, 0.3, 0.4], 0.5)
     with pytest.raises(g.ShapeError):
         g.forward(net, [0.1, 0.2])
+
+
+# ------------------------------------------------------- layer-level API
+def _np_activation(W, x):
+    """f64 restatement of kernels._activation for every neuron (kernels.py:102-122)."""
+    from oracle import oracle as O
+
+    n, m1 = W.shape
+    out = np.empty(n, np.float32)
+    for j in range(n):
+        acc = 0.0
+        for b0 in range(0, m1 - 1, 16):
+            part = 0.0
+            for i in range(b0, min(b0 + 16, m1 - 1)):
+                part += float(W[j, i]) * float(x[i])
+            acc += part
+        out[j] = np.float32(O.sigmoid64(acc + float(W[j, m1 - 1])))
+    return out
+
+
+def test_layer_forward_backward_backprop_error(gpu):
+    rng = np.random.default_rng(9)
+    W = rng.uniform(-0.5, 0.5, (37, 34)).astype(np.float32)
+    x = rng.random(33, dtype=np.float32)
+    job = g.LayerJob.create(W, x)
+    out = g.run_layer_forward(job, g.sequential())
+    assert out is job.outputs and out.tobytes() == _np_activation(W, x).tobytes()
+    err = rng.normal(size=37)
+    deltas, grads = g.run_layer_backward(job, err, g.sequential())
+    a = out.astype(np.float64)
+    want_d = (err * a) * (1.0 - a)
+    assert deltas.tobytes() == want_d.tobytes()
+    want_g = np.hstack([want_d[:, None] * x.astype(np.float64)[None, :], want_d[:, None]])
+    assert grads.tobytes() == want_g.tobytes()
+    ep = g.backpropagate_error(W, deltas, g.sequential())
+    want_e = np.empty(33)
+    for i in range(33):
+        acc = 0.0
+        for b0 in range(0, 37, 16):
+            part = 0.0
+            for j in range(b0, min(b0 + 16, 37)):
+                part += float(W[j, i]) * deltas[j]
+            acc += part
+        want_e[i] = acc
+    assert ep.tobytes() == want_e.tobytes()
+    with pytest.raises(g.ShapeError):
+        g.LayerJob(W, x[:5], np.empty(37, np.float32))
+    with pytest.raises(g.ShapeError):
+        g.run_layer_backward(job, err[:3], g.sequential())
