@@ -80,6 +80,20 @@ def test_sweep_vs_oracle_per_network(gpu):
             assert err <= tol, f"{numerics} H={cfg.hidden_dim} seed={cfg.seed}: {err:.3e}"
 
 
+def test_sweep_of_one_warp_networks_vs_oracle(gpu):
+    """Every network fits one warp (H <= 64 at 2 units per thread): the launch takes the
+    one-warp instantiation with no shared-memory exchange."""
+    c = load_case("paper_33_33_1")
+    t = c["train_y"].astype(np.float32)
+    hs, ss = g.sweep_grid([1, 7, 33, 64], [0, 5])
+    spec = g.SweepSpec(input_dim=33, hidden_dims=hs, seeds=ss, epochs=25)
+    nets = g.train_sweep(spec, c["train_x"], t)
+    for cfg, net in zip(spec.configs(), nets):
+        ref = g.init_weights(cfg)
+        O.train_online_seq(ref.w_ih2d, ref.w_ho2d, c["train_x"], t, 25, 0.1)
+        assert max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho)) <= 1e-4, cfg
+
+
 def test_sweep_full_grid_runs_and_matches_sample(gpu):
     # config 3 shape: 64 widths x 64 seeds = 4096 networks; oracle-check a stratified sample
     c = load_case("paper_33_33_1")
