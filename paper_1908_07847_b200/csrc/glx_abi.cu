@@ -175,7 +175,7 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     for (auto& n : nets)
         if (n.H < 1 || n.H > 512) return set_err(GLX_ERR_INVALID, "online kernel supports 1 <= hidden_dim <= 512, got %d", n.H);
     // staged rows [N][dp], targets [N], lookahead dots [N] (glx_online.cu)
-    const size_t xbytes = ((size_t)N * dp * 4 + (size_t)N * 8 + 15) / 16 * 16;
+    const size_t xbytes = ((size_t)N * ((dp + 3) & ~3) * 4 + (size_t)N * 8 + 15) / 16 * 16;  // rows padded to 4
     const bool x_in_smem = xbytes <= 160 * 1024;
     int max_h = 0;
     for (auto& n : nets) max_h = std::max(max_h, n.H);

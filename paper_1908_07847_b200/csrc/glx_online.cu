@@ -307,28 +307,33 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
 // reduction already gives every lane the output sum, no shared-memory exchange
 // or named barrier (a separate instantiation: a runtime branch cost the sweep)
 template <int DP, int MT, bool XS, bool ONEW = false>
-__global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online_sgd_mt_kernel(const OnlineNetDesc* __restrict__ nets,
+#ifndef GLX_ONLINE_ONEW_CTAS
+#define GLX_ONLINE_ONEW_CTAS GLX_ONLINE_MT2_CTAS
+#endif
+__global__ void __launch_bounds__(256, MT == 2 ? (ONEW ? GLX_ONLINE_ONEW_CTAS : GLX_ONLINE_MT2_CTAS) : 1) online_sgd_mt_kernel(const OnlineNetDesc* __restrict__ nets,
                                                              const int2* __restrict__ cta_nets,
                                                              const float* __restrict__ X, const float* __restrict__ T,
                                                              int64_t N, int D, int64_t epochs, double lr) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // staged rows are padded to SP floats (16-byte aligned): x is read as float4
+    constexpr int SP = (DP + 3) & ~3;
     float* xs = reinterpret_cast<float*>(smem_raw);
-    float* ts = xs + (XS ? N * DP : 0);
+    float* ts = xs + (XS ? N * SP : 0);
     float* gd = ts + (XS ? N : 0);  // gd[r] = x_r . x_{(r+1) mod N} (lookahead correction)
     const int2 cn = cta_nets[blockIdx.x];
     const int warp = threadIdx.x >> 5;
     if (XS) {
-        for (int64_t e = threadIdx.x; e < N * DP; e += blockDim.x) {
-            int64_t r = e / DP;
-            int i = (int)(e - r * DP);
+        for (int64_t e = threadIdx.x; e < N * SP; e += blockDim.x) {
+            int64_t r = e / SP;
+            int i = (int)(e - r * SP);
             xs[e] = i < D ? X[r * D + i] : (i == D ? 1.0f : 0.0f);
         }
         for (int64_t r = threadIdx.x; r < N; r += blockDim.x) ts[r] = T[r];
         __syncthreads();
         if (GLX_ONLINE_LA) {
             for (int64_t r = threadIdx.x; r < N; r += blockDim.x) {
-                const float* a0 = xs + r * DP;
-                const float* a1 = xs + (r + 1 == N ? 0 : r + 1) * DP;
+                const float* a0 = xs + r * SP;
+                const float* a1 = xs + (r + 1 == N ? 0 : r + 1) * SP;
                 float s = 0.f;
                 for (int i = 0; i < DP; i++) s = fmaf(a0[i], a1[i], s);
                 gd[r] = s;
@@ -394,7 +399,7 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
                 // epoch start: settle the pending update and form z_0 directly, exactly
                 // as a fresh call does, so results do not depend on how the epochs are
                 // split into calls (checkpoint segments)
-                const float2* xl2 = reinterpret_cast<const float2*>(xs + rp * DP);
+                const float2* xl2 = reinterpret_cast<const float2*>(xs + rp * SP);
 #pragma unroll
                 for (int u = 0; u < MT; u++) {
 #pragma unroll
@@ -411,20 +416,28 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
             }
             for (int64_t r = 0; r < N; r++) {
                 const int64_t rn = r + 1 == N ? 0 : r + 1;
-                const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
-                const float2* xn2 = reinterpret_cast<const float2*>(xs + rn * DP);
-                // (B) off the critical path
+                const float4* xp4 = reinterpret_cast<const float4*>(xs + rp * SP);
+                const float4* xn4 = reinterpret_cast<const float4*>(xs + rn * SP);
+                // (B) off the critical path: one float4 of each row feeds every unit
+                float2 pz[MT];
+#pragma unroll
+                for (int u = 0; u < MT; u++) pz[u] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q4 = 0; q4 < (DP + 3) / 4; q4++) {
+                    const float4 a = xp4[q4], c = xn4[q4];
+#pragma unroll
+                    for (int u = 0; u < MT; u++) {
+                        w[u][2 * q4] = ffma2(bcast2(nsp[u]), make_float2(a.x, a.y), w[u][2 * q4]);
+                        pz[u] = ffma2(w[u][2 * q4], make_float2(c.x, c.y), pz[u]);
+                        if (2 * q4 + 1 < DP / 2) {
+                            w[u][2 * q4 + 1] = ffma2(bcast2(nsp[u]), make_float2(a.z, a.w), w[u][2 * q4 + 1]);
+                            pz[u] = ffma2(w[u][2 * q4 + 1], make_float2(c.z, c.w), pz[u]);
+                        }
+                    }
+                }
                 float zpre[MT];
 #pragma unroll
-                for (int u = 0; u < MT; u++) {
-                    float2 p = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int q = 0; q < DP / 2; q++) {
-                        w[u][q] = ffma2(bcast2(nsp[u]), xp2[q], w[u][q]);
-                        p = ffma2(w[u][q], xn2[q], p);
-                    }
-                    zpre[u] = p.x + p.y;
-                }
+                for (int u = 0; u < MT; u++) zpre[u] = pz[u].x + pz[u].y;
                 // (A) the row's critical chain
                 const float tt = ts[r];
                 float h[MT];
@@ -441,7 +454,9 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
                     if ((threadIdx.x & 31) == 0) red[buf * 16 + (t >> 5)] = prod;
                     bar_sync(nd.bar_id, nthr);
                     zo = 0.f;
-                    for (int k = 0; k < nd.nwarps; k++) zo += red[buf * 16 + k];
+#pragma unroll
+                    for (int k = 0; k < 8; k++)  // <= 8 warps per CTA: predicated, no loop
+                        if (k < nd.nwarps) zo += red[buf * 16 + k];
                     buf ^= 1;
                 }
                 const float o = sigmoid_scaled(kScale * zo);
@@ -459,7 +474,7 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
                 rp = r;
             }
         }
-        const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * DP);
+        const float2* xp2 = reinterpret_cast<const float2*>(xs + rp * SP);
 #pragma unroll
         for (int u = 0; u < MT; u++)
 #pragma unroll
@@ -467,7 +482,7 @@ __global__ void __launch_bounds__(256, MT == 2 ? GLX_ONLINE_MT2_CTAS : 1) online
     } else {  // (braced: an unbraced discarded `else` swallowed the pragma'd write-back loop below)
     for (int64_t ep = 0; ep < epochs; ep++) {
         for (int64_t r = 0; r < N; r++) {
-            const float2* xr2 = reinterpret_cast<const float2*>(xs + (XS ? r * DP : 0));
+            const float2* xr2 = reinterpret_cast<const float2*>(xs + (XS ? r * SP : 0));
             if constexpr (!kXs) load_row<float, DP, XS>(x, xs, X, r, D);
             auto xp = [&](int q) { return kXs ? xr2[q] : make_float2(x[2 * q], x[2 * q + 1]); };
             const float tt = XS ? ts[r] : __ldg(T + r);
