@@ -437,15 +437,29 @@ __global__ void __launch_bounds__(256, MT == 2 ? (ONEW ? GLX_ONLINE_ONEW_CTAS : 
                 }
                 float zpre[MT];
 #pragma unroll
-                for (int u = 0; u < MT; u++) zpre[u] = pz[u].x + pz[u].y;
-                // (A) the row's critical chain
+                for (int u = 0; u < MT; u++) zpre[u] = pz[u].x + pz[u].y;  // (pairs: see below)
+                // (A) the row's critical chain; unit pairs use packed FMUL2/FADD2/FFMA2
+                // (per lane the same IEEE ops as the scalar form)
                 const float tt = ts[r];
                 float h[MT];
                 float prod = (t == 0) ? b2 : 0.f;
+                if constexpr (MT % 2 == 0) {
 #pragma unroll
-                for (int u = 0; u < MT; u++) {
-                    h[u] = act[u] ? sigmoid_scaled(kScale * zc[u]) : 0.f;
-                    prod = fmaf(w2[u], h[u], prod);
+                    for (int p = 0; p < MT / 2; p++) {
+                        const float2 zz = __fmul2_rn(make_float2(zc[2 * p], zc[2 * p + 1]), bcast2(kScale));
+                        const float2 den =
+                            __fadd2_rn(make_float2(ex2_approx(zz.x), ex2_approx(zz.y)), bcast2(1.0f));
+                        h[2 * p] = act[2 * p] ? rcp_approx(den.x) : 0.f;
+                        h[2 * p + 1] = act[2 * p + 1] ? rcp_approx(den.y) : 0.f;
+                        prod = fmaf(w2[2 * p], h[2 * p], prod);
+                        prod = fmaf(w2[2 * p + 1], h[2 * p + 1], prod);
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < MT; u++) {
+                        h[u] = act[u] ? sigmoid_scaled(kScale * zc[u]) : 0.f;
+                        prod = fmaf(w2[u], h[u], prod);
+                    }
                 }
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) prod += __shfl_xor_sync(0xffffffffu, prod, o);
@@ -463,12 +477,31 @@ __global__ void __launch_bounds__(256, MT == 2 ? (ONEW ? GLX_ONLINE_ONEW_CTAS : 
                 const float d_o = (o - tt) * o * (1.0f - o);
                 const float step_o = flr * d_o;
                 const float g = gd[r];
+                if constexpr (MT % 2 == 0) {
 #pragma unroll
-                for (int u = 0; u < MT; u++) {
-                    const float ns = -flr * (w2[u] * d_o * h[u] * (1.0f - h[u]));
-                    w2[u] = fmaf(-step_o, h[u], w2[u]);
-                    zc[u] = fmaf(ns, g, zpre[u]);
-                    nsp[u] = ns;
+                    for (int p = 0; p < MT / 2; p++) {
+                        const float2 hp = make_float2(h[2 * p], h[2 * p + 1]);
+                        const float2 omh = ffma2(hp, bcast2(-1.0f), bcast2(1.0f));  // 1 - h, one rounding
+                        const float2 w2p = make_float2(w2[2 * p], w2[2 * p + 1]);
+                        const float2 ns =
+                            __fmul2_rn(__fmul2_rn(__fmul2_rn(__fmul2_rn(w2p, bcast2(d_o)), hp), omh), bcast2(-flr));
+                        const float2 w2n = ffma2(bcast2(-step_o), hp, w2p);
+                        const float2 zn = ffma2(ns, bcast2(g), make_float2(zpre[2 * p], zpre[2 * p + 1]));
+                        w2[2 * p] = w2n.x;
+                        w2[2 * p + 1] = w2n.y;
+                        zc[2 * p] = zn.x;
+                        zc[2 * p + 1] = zn.y;
+                        nsp[2 * p] = ns.x;
+                        nsp[2 * p + 1] = ns.y;
+                    }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < MT; u++) {
+                        const float ns = -flr * (w2[u] * d_o * h[u] * (1.0f - h[u]));
+                        w2[u] = fmaf(-step_o, h[u], w2[u]);
+                        zc[u] = fmaf(ns, g, zpre[u]);
+                        nsp[u] = ns;
+                    }
                 }
                 if (t == 0) b2 -= step_o;
                 rp = r;
