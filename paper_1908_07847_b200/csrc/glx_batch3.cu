@@ -290,10 +290,24 @@ __global__ void __launch_bounds__(k3NT, 1) batch3_kernel(const Batch3Args a) {
                     float hv[UA];
                     load_units<UA>(zp, hv);
                     float os = 0.f;
+                    if constexpr (UA % 2 == 0) {  // unit pairs in packed FADD2 / FFMA2
+                        float2 os2 = make_float2(0.f, 0.f);
 #pragma unroll
-                    for (int u = 0; u < UA; u++) {
-                        hv[u] = sigmoid_scaled(hv[u]);
-                        os = fmaf(w2s[u], hv[u], os);
+                        for (int p = 0; p < UA / 2; p++) {
+                            const float2 den =
+                                __fadd2_rn(make_float2(ex2_approx(hv[2 * p]), ex2_approx(hv[2 * p + 1])), bcast2(1.0f));
+                            hv[2 * p] = rcp_approx(den.x);
+                            hv[2 * p + 1] = rcp_approx(den.y);
+                            os2 = ffma2(make_float2(w2s[2 * p], w2s[2 * p + 1]), make_float2(hv[2 * p], hv[2 * p + 1]),
+                                        os2);
+                        }
+                        os = os2.x + os2.y;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < UA; u++) {
+                            hv[u] = sigmoid_scaled(hv[u]);
+                            os = fmaf(w2s[u], hv[u], os);
+                        }
                     }
                     store_units<UA>(zp, hv);
                     opart[r * (a.QR + 1) + qa] = os;
@@ -344,11 +358,25 @@ __global__ void __launch_bounds__(k3NT, 1) batch3_kernel(const Batch3Args a) {
                     const float d = dob[r];
                     float hv[UA];
                     load_units<UA>(zp, hv);
+                    if constexpr (UA % 2 == 0) {  // same IEEE ops per lane, packed
 #pragma unroll
-                    for (int u = 0; u < UA; u++) {
-                        const float v = d * hv[u];
-                        acc2[u] += v;
-                        hv[u] = fmaf(-v, hv[u], v);
+                        for (int p = 0; p < UA / 2; p++) {
+                            const float2 hp = make_float2(hv[2 * p], hv[2 * p + 1]);
+                            const float2 v = __fmul2_rn(bcast2(d), hp);
+                            const float2 ac = __fadd2_rn(make_float2(acc2[2 * p], acc2[2 * p + 1]), v);
+                            acc2[2 * p] = ac.x;
+                            acc2[2 * p + 1] = ac.y;
+                            const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
+                            hv[2 * p] = s2.x;
+                            hv[2 * p + 1] = s2.y;
+                        }
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < UA; u++) {
+                            const float v = d * hv[u];
+                            acc2[u] += v;
+                            hv[u] = fmaf(-v, hv[u], v);
+                        }
                     }
                     store_units<UA>(zp, hv);
                     if (qa == 0) dsum += d;
