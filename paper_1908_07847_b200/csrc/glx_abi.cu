@@ -174,6 +174,12 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     if (dp < 0) return set_err(GLX_ERR_INVALID, "online kernel supports input_dim <= 63, got %d", D);
     for (auto& n : nets)
         if (n.H < 1 || n.H > 512) return set_err(GLX_ERR_INVALID, "online kernel supports 1 <= hidden_dim <= 512, got %d", n.H);
+    // exact path, one paper-size network: the f64-resident small kernel
+    if (ref64 && nets.size() == 1 && nets[0].H <= 64 && dp <= 34 && online_ref64_small_smem(N, D) <= 160 * 1024 &&
+        getenv("GLX_ONLINE_REF64_SMALL") == nullptr) {
+        GLX_LAUNCH(launch_online_ref64_small(nets[0].w_ih, nets[0].w_ho, nets[0].H, X, T, N, D, epochs, lr, st));
+        return GLX_OK;
+    }
     // staged rows [N][dp], targets [N], lookahead dots [N] (glx_online.cu)
     const size_t xbytes = ((size_t)N * ((dp + 3) & ~3) * 4 + (size_t)N * 8 + 15) / 16 * 16;  // rows padded to 4
     const bool x_in_smem = xbytes <= 160 * 1024;

@@ -38,6 +38,10 @@ struct OnlineLaunch {
 };
 
 int online_dp_for(int D);
+// ref64 online SGD of one network with H <= 64 and input_dim <= 33 (f64-resident rows)
+size_t online_ref64_small_smem(int64_t N, int D);
+cudaError_t launch_online_ref64_small(float* w_ih, float* w_ho, int H, const float* X, const float* T, int64_t N,
+                                      int D, int64_t epochs, double lr, cudaStream_t st);
 cudaError_t launch_online(const OnlineLaunch& L, cudaStream_t st);
 size_t online_scratch_bytes(int H, bool ref64);
 

@@ -571,6 +571,125 @@ __global__ void __launch_bounds__(256, MT == 2 ? (ONEW ? GLX_ONLINE_ONEW_CTAS : 
     if (t == 0) w_ho[H] = b2;
 }
 
+// ref64 online SGD for ONE network of <= 64 hidden units (configs 1/cohorts with
+// sequential()): the same operation order as online_sgd_kernel<double> (the
+// reference's kernels.py:264-295), with the rows staged once as f64 and the weight
+// row held as f64 registers that always carry f32-representable values. Per row
+// that removes the f32 -> f64 conversions of x and w from the dot and the update
+// (the 512-thread kernel is capped at 128 registers and cannot hold both).
+template <int DP>
+__global__ void __launch_bounds__(64) online_ref64_small_kernel(float* __restrict__ w_ih, float* __restrict__ w_ho,
+                                                               int H, const float* __restrict__ X,
+                                                               const float* __restrict__ T, int64_t N, int D,
+                                                               int64_t epochs, double lr) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double* x64 = reinterpret_cast<double*>(smem_raw);  // N x DP, [x, 1, 0...]
+    double* t64 = x64 + N * DP;                         // N
+    double* prods = t64 + N;                            // 4 blocks x 17
+    double* bc = prods + 4 * 17;                        // d_o, step_o
+    for (int64_t e = threadIdx.x; e < N * DP; e += blockDim.x) {
+        const int64_t r = e / DP;
+        const int i = (int)(e - r * DP);
+        x64[e] = i < D ? (double)X[r * D + i] : (i == D ? 1.0 : 0.0);
+    }
+    for (int64_t r = threadIdx.x; r < N; r += blockDim.x) t64[r] = (double)T[r];
+    __syncthreads();
+    const int j = threadIdx.x;
+    const bool active = j < H;
+    double w[DP];
+#pragma unroll
+    for (int i = 0; i < DP; i++) w[i] = (active && i < D) ? (double)w_ih[(int64_t)j * (D + 1) + i] : 0.0;
+    double bw = active ? (double)w_ih[(int64_t)j * (D + 1) + D] : 0.0;
+    double w2 = active ? (double)w_ho[j] : 0.0;
+    double b2 = (double)w_ho[H];
+    const int nb = (H + 15) >> 4;
+    for (int64_t ep = 0; ep < epochs; ep++) {
+        for (int64_t r = 0; r < N; r++) {
+            const double* xr = x64 + r * DP;
+            float h = 0.0f;
+            if (active) {
+                double acc = 0.0;
+#pragma unroll
+                for (int b0 = 0; b0 < DP; b0 += 16) {
+                    double part = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 16; k++) {
+                        const int i = b0 + k;
+                        if (i < DP && i < D) part = fma(w[i < DP ? i : 0], xr[i < DP ? i : 0], part);
+                    }
+                    if (b0 < D) acc = __dadd_rn(acc, part);
+                }
+                const double z = __dadd_rn(acc, bw);
+                h = __double2float_rn(1.0 / (1.0 + exp(-z)));
+                prods[(j >> 4) * 17 + (j & 15)] = w2 * (double)h;  // exact product
+            }
+            __syncthreads();
+            if (j < 32) {  // the output neuron (kernels.py:277-289)
+                double part = 0.0;
+                if (j < nb) {
+                    const int jn = min(16, H - j * 16);
+                    for (int k = 0; k < jn; k++) part = __dadd_rn(part, prods[j * 17 + k]);
+                }
+                double z = 0.0;
+                for (int b = 0; b < nb; b++) z = __dadd_rn(z, __shfl_sync(0xffffffffu, part, b));
+                if (j == 0) {
+                    z = __dadd_rn(z, b2);
+                    const double od = (double)__double2float_rn(1.0 / (1.0 + exp(-z)));
+                    const double d_o = __dmul_rn(__dmul_rn(__dsub_rn(od, t64[r]), od), __dsub_rn(1.0, od));
+                    bc[0] = d_o;
+                    bc[1] = __dmul_rn(lr, d_o);
+                }
+            }
+            __syncthreads();
+            const double d_o = bc[0], step_o = bc[1];
+            if (active) {  // hidden first, from the pre-update w_ho (kernels.py:290-292)
+                const double hd = (double)h;
+                const double d_h = __dmul_rn(__dmul_rn(__dmul_rn(w2, d_o), hd), __dsub_rn(1.0, hd));
+                const double s = __dmul_rn(lr, d_h);
+#pragma unroll
+                for (int i = 0; i < DP; i++)
+                    if (i < D) w[i] = (double)__double2float_rn(__dsub_rn(w[i], __dmul_rn(s, xr[i])));
+                bw = (double)__double2float_rn(__dsub_rn(bw, s));
+                w2 = (double)__double2float_rn(__dsub_rn(w2, __dmul_rn(step_o, hd)));
+            }
+            if (j == 0) b2 = (double)__double2float_rn(__dsub_rn(b2, step_o));
+        }
+    }
+    if (active) {
+#pragma unroll
+        for (int i = 0; i < DP; i++)
+            if (i < D) w_ih[(int64_t)j * (D + 1) + i] = (float)w[i];
+        w_ih[(int64_t)j * (D + 1) + D] = (float)bw;
+        w_ho[j] = (float)w2;
+    }
+    if (j == 0) w_ho[H] = (float)b2;
+}
+
+size_t online_ref64_small_smem(int64_t N, int D) {
+    const int dp = online_dp_for(D);
+    return (size_t)N * dp * 8 + (size_t)N * 8 + 4 * 17 * 8 + 16;
+}
+
+cudaError_t launch_online_ref64_small(float* w_ih, float* w_ho, int H, const float* X, const float* T, int64_t N,
+                                      int D, int64_t epochs, double lr, cudaStream_t st) {
+    const size_t smem = online_ref64_small_smem(N, D);
+    const int threads = H <= 32 ? 32 : 64;
+    const int dp = online_dp_for(D);
+    cudaError_t e = cudaSuccess;
+    auto go = [&](auto kernel) {
+        e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess) kernel<<<1, threads, smem, st>>>(w_ih, w_ho, H, X, T, N, D, epochs, lr);
+    };
+    switch (dp) {
+        case 8: go(online_ref64_small_kernel<8>); break;
+        case 16: go(online_ref64_small_kernel<16>); break;
+        case 34: go(online_ref64_small_kernel<34>); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ launcher
 template <int DP, int MT>
 static cudaError_t launch_online_mt(const OnlineLaunch& L, cudaStream_t st) {
