@@ -254,7 +254,12 @@ __global__ void __launch_bounds__(512) online_sgd_kernel(const OnlineNetDesc* __
                     double part = 0.0;
                     if (j < nb) {
                         const int jn = min(16, H - j * 16);
-                        for (int k = 0; k < jn; k++) part = __dadd_rn(part, prods[j * 17 + k]);
+                        double pv[16];  // loads ahead of the sequential adds (see the small kernel)
+#pragma unroll
+                        for (int k = 0; k < 16; k++) pv[k] = k < jn ? prods[j * 17 + k] : 0.0;
+#pragma unroll
+                        for (int k = 0; k < 16; k++)
+                            if (k < jn) part = __dadd_rn(part, pv[k]);
                     }
                     double z = 0.0;
                     for (int b = 0; b < nb; b++) z = __dadd_rn(z, __shfl_sync(0xffffffffu, part, b));
@@ -628,7 +633,14 @@ __global__ void __launch_bounds__(64) online_ref64_small_kernel(float* __restric
                 double part = 0.0;
                 if (j < nb) {
                     const int jn = min(16, H - j * 16);
-                    for (int k = 0; k < jn; k++) part = __dadd_rn(part, prods[j * 17 + k]);
+                    // unrolled and predicated: the 16 loads issue ahead of the dependent
+                    // sequential adds (the reference's in-block order is kept)
+                    double pv[16];
+#pragma unroll
+                    for (int k = 0; k < 16; k++) pv[k] = k < jn ? prods[j * 17 + k] : 0.0;
+#pragma unroll
+                    for (int k = 0; k < 16; k++)
+                        if (k < jn) part = __dadd_rn(part, pv[k]);
                 }
                 double z = 0.0;
                 for (int b = 0; b < nb; b++) z = __dadd_rn(z, __shfl_sync(0xffffffffu, part, b));
