@@ -130,15 +130,18 @@ def train_nets_on_device(nets: list[Network], feats2d: np.ndarray, targets: np.n
 
 
 def train_sweep(spec: SweepSpec, feats2d: np.ndarray, targets: np.ndarray, *, rank: int = 0, world_size: int = 1,
-                device: int | None = None, group=None) -> list[Network] | None:
+                device: int | None = None, group=None, trainer=None) -> list[Network] | None:
     """Train every network of the sweep; with world_size > 1 each rank trains its
-    LPT shard on its own GPU and rank 0 returns the gathered list (others None)."""
+    LPT shard on its own GPU and rank 0 returns the gathered list (others None).
+    `trainer(nets, feats2d, targets, epochs, lr, numerics, device)` trains a list in
+    place (default: the device kernel, train_nets_on_device; tests inject a CPU
+    stand-in to exercise the sharding and gather with gloo)."""
     nets = [init_weights(c) for c in spec.configs()]
     shards = lpt_shards(spec.costs(), world_size)
     mine = shards[rank]
     dev = rank if device is None else device
-    train_nets_on_device([nets[i] for i in mine], feats2d, targets, spec.epochs, spec.learning_rate,
-                         spec.numerics, dev)
+    (trainer or train_nets_on_device)([nets[i] for i in mine], feats2d, targets, spec.epochs, spec.learning_rate,
+                                      spec.numerics, dev)
     if world_size == 1:
         return nets
     import torch.distributed as dist

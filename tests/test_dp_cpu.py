@@ -220,3 +220,52 @@ def test_wide_shard_rows_cover_and_align():
         assert all(r0 % 64 == 0 and r1 % 64 == 0 for r0, r1 in spans)
     with pytest.raises(Exception):
         wide.shard_rows(100, 2, 0)
+
+
+def _oracle_trainer(nets, feats2d, targets, epochs, lr, numerics, device):
+    """CPU stand-in for sweep.train_nets_on_device: the reference's sequential engine."""
+    from oracle import oracle as O
+
+    for n in nets:
+        O.train_online_seq(n.w_ih2d, n.w_ho2d, feats2d, targets, epochs, lr)
+
+
+def _sweep_worker(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_1908_07847_b200 as g
+
+    x, y = g.synthetic_arrays(40, 6, 2, "planted-linear")
+    hs, ss = g.sweep_grid([3, 8, 17, 30], [0, 1, 2])
+    spec = g.SweepSpec(input_dim=6, hidden_dims=hs, seeds=ss, epochs=7)
+    nets = g.train_sweep(spec, x, y.astype(np.float32), rank=rank, world_size=world, trainer=_oracle_trainer)
+    out_q.put((rank, None if nets is None else [(n.w_ih.copy(), n.w_ho.copy()) for n in nets]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(240)
+def test_gloo_world2_sweep_sharding_and_gather():
+    """Config 3 across ranks: LPT shards trained independently (no
+    data-path collective), gathered on rank 0, equal to the single-process sweep."""
+    import paper_1908_07847_b200 as g
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sweep_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=200) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert res[1] is None and res[0] is not None
+    x, y = g.synthetic_arrays(40, 6, 2, "planted-linear")
+    hs, ss = g.sweep_grid([3, 8, 17, 30], [0, 1, 2])
+    spec = g.SweepSpec(input_dim=6, hidden_dims=hs, seeds=ss, epochs=7)
+    single = g.train_sweep(spec, x, y.astype(np.float32), trainer=_oracle_trainer)
+    assert len(res[0]) == len(single) == 12
+    for (wi, wo), n in zip(res[0], single):
+        assert wi.tobytes() == n.w_ih.tobytes() and wo.tobytes() == n.w_ho.tobytes()
