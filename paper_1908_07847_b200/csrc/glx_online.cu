@@ -23,6 +23,9 @@
 
 #include <type_traits>
 
+#ifndef GLX_ONLINE_LANE_SUM
+#define GLX_ONLINE_LANE_SUM 0  // sweep output partials: lane-parallel shuffle sum (1) or predicated loop (0)
+#endif
 #ifndef GLX_ONLINE_LA
 // lookahead forward: z_{r+1} = W^(r) x_{r+1} + ns_r (x_r . x_{r+1}) lets the next
 // row's dot product run alongside this row's output reduction (fp32 only)
@@ -479,10 +482,19 @@ __global__ void __launch_bounds__(256, MT == 2 ? (ONEW ? GLX_ONLINE_ONEW_CTAS : 
                 if constexpr (!ONEW) {
                     if ((threadIdx.x & 31) == 0) red[buf * 16 + (t >> 5)] = prod;
                     bar_sync(nd.bar_id, nthr);
+#if GLX_ONLINE_LANE_SUM
+                    // each group of 8 lanes holds the <= 8 warp partials, 3 xor shuffles
+                    const int kk = threadIdx.x & 7;
+                    zo = kk < nd.nwarps ? red[buf * 16 + kk] : 0.f;
+                    zo += __shfl_xor_sync(0xffffffffu, zo, 4);
+                    zo += __shfl_xor_sync(0xffffffffu, zo, 2);
+                    zo += __shfl_xor_sync(0xffffffffu, zo, 1);
+#else
                     zo = 0.f;
 #pragma unroll
                     for (int k = 0; k < 8; k++)  // <= 8 warps per CTA: predicated, no loop
                         if (k < nd.nwarps) zo += red[buf * 16 + k];
+#endif
                     buf ^= 1;
                 }
                 const float o = sigmoid_scaled(kScale * zo);
