@@ -159,10 +159,13 @@ struct NetReq {
 // register tile (GLX_ONLINE_MT overrides) amortises the per-row reduction and
 // barrier; a single network uses 2 units per thread when that makes it one warp
 // (no cross-warp exchange: 292 vs 337 ns per row at 33-33-1), else 1
-int online_mt(size_t n_nets, bool ref64, int dp, int max_h) {
+// (sweeps: 4 units per thread when networks of H >= 128 hold at least half of the
+// hidden units -- config 3: 0.402 vs 0.417 ms/epoch -- else 2: small networks
+// were 2x slower at 4)
+int online_mt(size_t n_nets, bool ref64, int dp, int max_h, double big_frac) {
     if (ref64) return 1;
     const char* e = getenv("GLX_ONLINE_MT");
-    int mt = e ? atoi(e) : (n_nets > 1 || max_h <= 64 ? 2 : 1);
+    int mt = e ? atoi(e) : (n_nets > 1 ? (big_frac >= 0.5 ? 4 : 2) : (max_h <= 64 ? 2 : 1));
     if (mt != 1 && mt != 2 && mt != 4) mt = 1;
     if (dp > 34) mt = 1;  // 64-wide rows: the MT tile would spill
     return mt;
@@ -184,8 +187,13 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     const size_t xbytes = ((size_t)N * ((dp + 3) & ~3) * 4 + (size_t)N * 8 + 15) / 16 * 16;  // rows padded to 4
     const bool x_in_smem = xbytes <= 160 * 1024;
     int max_h = 0;
-    for (auto& n : nets) max_h = std::max(max_h, n.H);
-    const int mt = online_mt(nets.size(), ref64, dp, max_h);
+    double units = 0, big_units = 0;
+    for (auto& n : nets) {
+        max_h = std::max(max_h, n.H);
+        units += n.H;
+        if (n.H >= 128) big_units += n.H;
+    }
+    const int mt = online_mt(nets.size(), ref64, dp, max_h, units > 0 ? big_units / units : 0.0);
     const int cap = mt == 1 ? 16 : 8;  // warps per CTA (register budget of the MT-unit tile)
     // first-fit decreasing packing of networks into CTAs of <= cap warps / 15 networks
     std::stable_sort(nets.begin(), nets.end(), [](const NetReq& a, const NetReq& b) { return a.H > b.H; });
