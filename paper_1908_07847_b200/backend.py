@@ -7,6 +7,10 @@ Reference counterparts (/root/reference/pkg/src/glycemlp/):
                                                backend.py:208-234
   kernels.eval_counts(w_ih2d, w_ho2d, feats2d, labels)
                                                kernels.py:352-375
+  LayerJob / run_layer_forward / run_layer_backward / backpropagate_error
+                                               backend.py:73-205
+plus run_train_segment_batch (full-batch GD) and
+run_train_segment_eval (one trainer checkpoint in one device call, 8(f)1).
 
 The engine name is "cuda" (the reference rejects any other name than its two
 CPU engines, test_backend.py:24-25, so the device engine has its own name).
