@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 BUILD = ROOT / "build"
 LIB = PKG / "libglycemlp_cuda.so"
-SOURCES = ("glx_online.cu", "glx_batch.cu", "glx_batch3.cu", "glx_eval.cu", "glx_tc.cu", "glx_data.cu", "glx_abi.cu")
+SOURCES = ("glx_online.cu", "glx_batch.cu", "glx_batch3.cu", "glx_batchtc.cu", "glx_eval.cu", "glx_tc.cu", "glx_data.cu", "glx_abi.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 

@@ -273,33 +273,45 @@ int check_dims(int64_t rows, int D, int H) {
     return GLX_OK;
 }
 
-// epoch-kernel selection: the three-role kernel (glx_batch3.cu) when its
-// geometry fits, else the two-role kernel; GLX_BATCH_KERNEL=2 forces the latter
-bool use_three_role() {
+// epoch-kernel selection (kind 2: tcgen05 3xTF32 kernel, glx_batchtc.cu; 1: the
+// three-role FP32 kernel, glx_batch3.cu; 0: the two-role kernel). Default: the
+// first whose geometry fits. GLX_BATCH_KERNEL=3 starts at the three-role
+// kernel, GLX_BATCH_KERNEL=2 forces the two-role kernel.
+int batch_kernel_pref() {
     static int v = [] {
         const char* e = getenv("GLX_BATCH_KERNEL");
-        return (e && e[0] == '2') ? 0 : 1;
+        return (e && e[0] == '2') ? 0 : (e && e[0] == '3') ? 1 : 2;
     }();
-    return v != 0;
+    return v;
 }
 
-bool train_geometry(int64_t N, int D, int H, BatchGeom* g, bool* three) {
+bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
+    const int pref = batch_kernel_pref();
+    if (pref >= 2 && batchtc_geometry(N, D, H, sm_count_current(), g)) {
+        *kind = 2;
+        return true;
+    }
     // the three-role kernel wins where its forward/backward tiles are 4 units wide
     // (H % 4 == 0); narrower tiles stay on the two-role kernel (profiles/r01_summary.md)
-    *three = use_three_role() && batch3_geometry(N, D, H, sm_count_current(), g) && g->MT == 4;
-    return *three || batch_geometry(N, D, H, sm_count_current(), true, g);
+    if (pref >= 1 && batch3_geometry(N, D, H, sm_count_current(), g) && g->MT == 4) {
+        *kind = 1;
+        return true;
+    }
+    *kind = 0;
+    return batch_geometry(N, D, H, sm_count_current(), true, g);
 }
 
-cudaError_t launch_train_epoch(const BatchGeom& g, bool three, const float* Xp, const float* Wk, float* part,
+cudaError_t launch_train_epoch(const BatchGeom& g, int kind, const float* Xp, const float* Wk, float* part,
                                cudaStream_t st) {
-    return three ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
+    if (kind == 2) return launch_batchtc_epoch(g, Xp, Wk, part, st);
+    return kind == 1 ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
 }
 
 int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, int H, int64_t epochs, double lr,
                      double* stats_hist, int32_t* nonfinite, cudaStream_t st) {
     BatchGeom g;
-    bool three = false;
-    if (!train_geometry(N, D, H, &g, &three))
+    int kind = 0;
+    if (!train_geometry(N, D, H, &g, &kind))
         return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d N=%lld (needs D<=33, H<=512)", D,
                        H, (long long)N);
     Workspace* ws = workspace(st);
@@ -314,7 +326,7 @@ int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D
         float* nxt = (e & 1) ? wk0 : wk1;
         cudaEvent_t pe = nullptr;
         GLX_CK(prof_begin(st, &pe));
-        GLX_LAUNCH(launch_train_epoch(g, three, Xp, cur, ws->part.as<float>(), st));
+        GLX_LAUNCH(launch_train_epoch(g, kind, Xp, cur, ws->part.as<float>(), st));
         if (pe) GLX_CK(cudaEventRecord(pe, st));
         GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), w_ih, w_ho, cur, nxt, lr_over_n, true,
                                        stats_hist ? stats_hist + 5 * e : nullptr, nonfinite, st));
@@ -482,8 +494,8 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
         return GLX_OK;
     }
     BatchGeom g;
-    bool three = false;
-    if (!train_geometry(N, D, H, &g, &three))
+    int kind = 0;
+    if (!train_geometry(N, D, H, &g, &kind))
         return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d", D, H);
     Workspace* ws = workspace(st);
     GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
@@ -492,7 +504,7 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
     GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk0 + g.WKS, st));
     cudaEvent_t pe = nullptr;
     GLX_CK(prof_begin(st, &pe));
-    GLX_LAUNCH(launch_train_epoch(g, three, Xp, wk0, ws->part.as<float>(), st));
+    GLX_LAUNCH(launch_train_epoch(g, kind, Xp, wk0, ws->part.as<float>(), st));
     if (pe) GLX_CK(cudaEventRecord(pe, st));
     GLX_LAUNCH(launch_batch_grad(g, ws->part.as<float>(), wk0, grad, st));
     return GLX_OK;

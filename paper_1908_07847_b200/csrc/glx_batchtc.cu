@@ -1,0 +1,610 @@
+// glx_batchtc.cu -- full-batch gradient-descent epoch (configs 2 and 4:
+// D <= 33 inputs -> H = 128 or 256 sigmoid units -> 1 output) on the
+// 5th-generation tensor cores, fp32-accurate through 3xTF32.
+//
+// Same contract as batch3_kernel (glx_batch3.cu): one persistent CTA per SM
+// walks row tiles and writes one per-CTA partial record
+//   [dW1acc (H*(D+1)) | dW2acc (H) | dsum | loss | c0 c1 c2 c3]
+// that batch_update_kernel reduces in f64 and applies (kernels.py:264-295
+// batch semantics).
+//
+// Both GEMMs of the epoch run on tcgen05 with the hidden units on the TMEM
+// lanes (M = 128 units per half):
+//   forward   Z^T[j][r]  = W1s[j][:] . x_r            (SS: A = W1s, B = x tile, K-major)
+//   backward  dW1[j][k] += sum_r dh[j][r] x_r[k]       (TS: A = dh^T from TMEM, B = x tile, MN-major)
+// so the delta of every hidden unit stays in TMEM between the two MMAs. Both
+// shared-memory operands are K-major no-swizzle core matrices (8 rows x 16 B):
+// the forward reads the x tile as [rows x features], the backward a transposed
+// copy [features x rows] written by the converter warps (tf32 MMAs with an
+// MN-major B operand return zeros on sm_100a, tools/umma_probe.cu).
+// Each operand is split hi = tf32(v) (bit truncation), lo = v - hi and the
+// products are accumulated as lo.hi + hi.lo + hi.hi in the fp32 TMEM
+// accumulator: the dropped lo.lo term is 2^-22 relative, so results track the
+// fp32 CUDA-core kernel (tests/test_gpu_batch.py, 1e-5 against the f64 oracle).
+//
+// Per 64-row tile the epilogue warps (thread = hidden unit) read Z^T from
+// TMEM, apply the MUFU sigmoid, reduce the output partial w2s_j h_j over the
+// units with a warp reduce-scatter plus one shared-memory pass, compute
+// delta_o per row, and write dh = delta_o h (1 - h) back to TMEM as hi/lo for
+// the backward MMA. Z^T is double-buffered so the forward MMA of tile t+1
+// overlaps the epilogue of tile t, and the backward of tile t overlaps the
+// epilogue of tile t+1.
+#include "glx_common.cuh"
+#include "glx_kernels.h"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace glx {
+
+namespace {
+
+constexpr int kR = 64;                      // rows per tile (forward MMA N)
+constexpr int kFC = 10;                     // 4-feature chunks of the forward operands (K = 40)
+constexpr int kNB = 48;                     // features in the backward (MMA N, multiple of 16)
+constexpr int kXF = kR / 8 * kFC * 128;     // bytes per forward x tile copy (hi or lo): [r/8][k/4][r%8][k%4]
+constexpr int kXT = kNB / 8 * kR / 4 * 128; // bytes per transposed tile copy: [k/8][r/4][k%8][r%4]
+constexpr int kWT = 16 * kFC * 128;         // bytes per 128-unit weight copy (hi or lo)
+constexpr int kXFS = 2;                     // forward x stages (free once the forward MMA completes)
+constexpr int kXS = 3;                      // transposed x stages (free once the backward MMA completes)
+constexpr int kXR = 3;                      // raw x stages (TMA bulk targets)
+constexpr int kMaxLD = 36;
+constexpr int kRawBytes = kR * kMaxLD * 4;
+constexpr uint32_t kTf32Mask = 0xFFFFE000u;
+constexpr int kColZ = 0;     // Z^T / dh hi: buffer b at 128 b, half hf at + 64 hf
+constexpr int kColLo = 256;  // dh lo: half hf at + 64 hf
+constexpr int kColW = 384;   // dW1 accumulators: half hf at + 48 hf
+constexpr uint32_t kTmemCols = 512;
+constexpr int kEpiBar = 1;
+// the dW1 TMEM accumulator restarts every kDrain tiles after being added (round
+// to nearest) into per-thread fp32 registers: tensor-core fp32 accumulation over
+// ~10^5 rows per CTA drifted by ~1e-3 relative at 64Mi rows; short partials keep
+// the sum at the fp32 CUDA-core kernel's accuracy (tests/test_gpu_fullsize.py)
+#ifndef GLX_BTC_DRAIN
+#define GLX_BTC_DRAIN 1
+#endif
+constexpr int kDrain = GLX_BTC_DRAIN;
+constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
+
+struct BtcArgs {
+    const float* Xp;
+    const float* Wk;
+    float* part;
+    int64_t N, ntiles;
+    int D, DP, LD, H, P1, PS;
+};
+
+struct BtcSmem {  // byte offsets
+    int w, xf, xc, raw, tgt, opart, dob, stat, bars;
+    int total;
+};
+
+__host__ __device__ constexpr int btc_threads(int NH) { return (4 + 4 * NH) * 32; }
+
+__host__ __device__ constexpr BtcSmem btc_smem(int NH) {
+    BtcSmem s{};
+    s.w = 0;
+    s.xf = s.w + 2 * NH * kWT;
+    s.xc = s.xf + kXFS * 2 * kXF;
+    s.raw = s.xc + kXS * 2 * kXT;
+    s.tgt = s.raw + kXR * kRawBytes;
+    s.opart = s.tgt + kXS * kR * 4;
+    s.dob = s.opart + 4 * NH * kR * 4;
+    s.stat = s.dob + kR * 4;
+    s.bars = s.stat + kR * 6 * 4;
+    s.total = s.bars + 256;
+    return s;
+}
+
+// UMMA shared-memory descriptor, no swizzle (canonical core matrices of
+// 8 rows x 16 B): start | LBO (K-direction stride) | SBO (M/N-direction
+// stride) | version 1 (sm100) | layout type 0
+__device__ __forceinline__ uint64_t desc_ns(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+
+// instruction descriptor: TF32 x TF32 -> F32, M = 128
+__host__ __device__ constexpr uint32_t idesc_tf32(int N, bool b_mn_major) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((b_mn_major ? 1u : 0u) << 16) | ((uint32_t)(N >> 3) << 17) |
+           ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+          "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+          "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+        "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]),
+        "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v) & kTf32Mask; }
+
+template <int NH>
+__global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
+    constexpr int NEW = 4 * NH;  // epilogue warps
+    constexpr BtcSmem L = btc_smem(NH);
+    extern __shared__ __align__(1024) unsigned char sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
+    uint64_t* raw_full = bars;
+    uint64_t* raw_empty = raw_full + kXR;
+    uint64_t* xf_full = raw_empty + kXR;
+    uint64_t* xf_empty = xf_full + kXFS;
+    uint64_t* xc_full = xf_empty + kXFS;
+    uint64_t* xc_empty = xc_full + kXS;
+    uint64_t* z_full = xc_empty + kXS;
+    uint64_t* dh_ready = z_full + 2;
+    uint64_t* bwd_done = dh_ready + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bwd_done + 1);
+    float* tgt = reinterpret_cast<float*>(sm + L.tgt);
+    float* opart = reinterpret_cast<float*>(sm + L.opart);
+    float* dob = reinterpret_cast<float*>(sm + L.dob);
+    float* stat = reinterpret_cast<float*>(sm + L.stat);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nt = (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA (>= 1)
+    const int D = a.D, LD = a.LD, DP = a.DP;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kXR; s++) {
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&raw_empty[s], 2);
+        }
+        for (int s = 0; s < kXFS; s++) {
+            mbar_init(&xf_full[s], 2);
+            mbar_init(&xf_empty[s], 1);
+        }
+        for (int s = 0; s < kXS; s++) {
+            mbar_init(&xc_full[s], 2);
+            mbar_init(&xc_empty[s], 1);
+        }
+        mbar_init(&z_full[0], 1);
+        mbar_init(&z_full[1], 1);
+        mbar_init(dh_ready, NEW);
+        mbar_init(bwd_done, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    // weights -> hi/lo core-matrix copies (K-major A operand of the forward MMA)
+    for (int e = threadIdx.x; e < NH * 128 * kFC; e += blockDim.x) {
+        const int j = e / kFC, q = e - (e / kFC) * kFC;  // unit, 4-feature chunk
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int k = 4 * q + i;
+            v[i] = (k <= D) ? a.Wk[(int64_t)j * DP + k] : 0.f;
+        }
+        const int hf = j >> 7, jj = j & 127;
+        const int off = hf * kWT + (jj >> 3) * (kFC * 128) + q * 128 + (jj & 7) * 16;
+        uint4 hi, lo;
+        hi.x = tf32_hi(v[0]);
+        hi.y = tf32_hi(v[1]);
+        hi.z = tf32_hi(v[2]);
+        hi.w = tf32_hi(v[3]);
+        lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
+        lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
+        lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
+        lo.w = __float_as_uint(v[3] - __uint_as_float(hi.w));
+        *reinterpret_cast<uint4*>(sm + L.w + off) = hi;
+        *reinterpret_cast<uint4*>(sm + L.w + NH * kWT + off) = lo;
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            for (int64_t lt = 0; lt < nt; lt++) {
+                const int rs = (int)(lt % kXR);
+                if (lt >= kXR) mbar_wait(&raw_empty[rs], (uint32_t)((lt / kXR) - 1) & 1);
+                const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
+                const int64_t rem = a.N - row0;
+                const int nr = rem < kR ? (int)rem : kR;
+                const uint32_t bytes = (uint32_t)(nr * LD * 4);
+                mbar_arrive_expect_tx(&raw_full[rs], bytes);
+                bulk_g2s(sm + L.raw + rs * kRawBytes, a.Xp + row0 * LD, bytes, &raw_full[rs]);
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idf = idesc_tf32(kR, false);
+            constexpr uint32_t idb = idesc_tf32(kNB, false);
+            const uint32_t w_hi = smem_u32(sm + L.w), w_lo = w_hi + NH * kWT;
+            auto backward = [&](int64_t lt) {
+                const int cs = (int)(lt % kXS), zb = (int)(lt & 1);
+                mbar_wait(dh_ready, (uint32_t)lt & 1);
+                mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);
+                tc_fence_after();
+                const uint32_t x_hi = smem_u32(sm + L.xc + cs * 2 * kXT), x_lo = x_hi + kXT;
+#pragma unroll 1
+                for (int hf = 0; hf < NH; hf++) {
+                    const uint32_t d = tmem + kColW + 48 * hf;
+                    const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf, alo = tmem + kColLo + 64 * hf;
+#pragma unroll 1
+                    for (int s = 0; s < kR / 8; s++) {
+                        const uint64_t bh = desc_ns(x_hi + s * 256, 128, kR / 4 * 128);
+                        const uint64_t bl = desc_ns(x_lo + s * 256, 128, kR / 4 * 128);
+                        mma_ts(d, alo + 8 * s, bh, idb, (lt % kDrain) != 0 || s != 0);
+                        mma_ts(d, ahi + 8 * s, bl, idb, 1);
+                        mma_ts(d, ahi + 8 * s, bh, idb, 1);
+                    }
+                }
+                commit(&xc_empty[cs]);
+                commit(bwd_done);
+            };
+            for (int64_t lt = 0; lt < nt; lt++) {
+                const int fs = (int)(lt % kXFS), zb = (int)(lt & 1);
+                mbar_wait(&xf_full[fs], (uint32_t)(lt / kXFS) & 1);
+                tc_fence_after();
+                const uint32_t x_hi = smem_u32(sm + L.xf + fs * 2 * kXF), x_lo = x_hi + kXF;
+#pragma unroll 1
+                for (int hf = 0; hf < NH; hf++) {
+                    const uint32_t d = tmem + kColZ + 128 * zb + 64 * hf;
+                    const uint32_t wh = w_hi + hf * kWT, wl = w_lo + hf * kWT;
+#pragma unroll
+                    for (int s = 0; s < kFC / 2; s++) {
+                        mma_ss(d, desc_ns(wl + s * 256, 128, kFC * 128), desc_ns(x_hi + s * 256, 128, kFC * 128), idf,
+                               s != 0);
+                        mma_ss(d, desc_ns(wh + s * 256, 128, kFC * 128), desc_ns(x_lo + s * 256, 128, kFC * 128), idf,
+                               1);
+                    }
+#pragma unroll
+                    for (int s = 0; s < kFC / 2; s++)
+                        mma_ss(d, desc_ns(wh + s * 256, 128, kFC * 128), desc_ns(x_hi + s * 256, 128, kFC * 128), idf,
+                               1);
+                }
+                commit(&xf_empty[fs]);
+                commit(&z_full[zb]);
+                if (lt >= 1) backward(lt - 1);
+            }
+            backward(nt - 1);
+        }
+    } else if (warp < 4) {
+        // ------------------------------------------------------------ converters
+        const int r = threadIdx.x - 64;  // row within the tile (forward copy); item base (transposed copy)
+        for (int64_t lt = 0; lt < nt; lt++) {
+            const int rs = (int)(lt % kXR), cs = (int)(lt % kXS), fs = (int)(lt % kXFS);
+            mbar_wait(&raw_full[rs], (uint32_t)(lt / kXR) & 1);
+            const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
+            const int64_t rem = a.N - row0;
+            const int nr = rem < kR ? (int)rem : kR;
+            const float* rawt = reinterpret_cast<const float*>(sm + L.raw + rs * kRawBytes);
+            // forward copy [r/8][k/4][r%8][k%4] (hi, lo)
+            if (lt >= kXFS) mbar_wait(&xf_empty[fs], (uint32_t)((lt / kXFS) - 1) & 1);
+            {
+                const float* raw = rawt + r * LD;
+                unsigned char* xh = sm + L.xf + fs * 2 * kXF + (r >> 3) * (kFC * 128) + (r & 7) * 16;
+#pragma unroll
+                for (int q = 0; q < kFC; q++) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (r < nr && 4 * q < LD) v = *reinterpret_cast<const float4*>(raw + 4 * q);
+                    uint4 hi, lo;
+                    hi.x = tf32_hi(v.x);
+                    hi.y = tf32_hi(v.y);
+                    hi.z = tf32_hi(v.z);
+                    hi.w = tf32_hi(v.w);
+                    lo.x = __float_as_uint(v.x - __uint_as_float(hi.x));
+                    lo.y = __float_as_uint(v.y - __uint_as_float(hi.y));
+                    lo.z = __float_as_uint(v.z - __uint_as_float(hi.z));
+                    lo.w = __float_as_uint(v.w - __uint_as_float(hi.w));
+                    *reinterpret_cast<uint4*>(xh + q * 128) = hi;
+                    *reinterpret_cast<uint4*>(xh + kXF + q * 128) = lo;
+                }
+            }
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xf_full[fs]);
+            // transposed copy [k/8][r/4][k%8][r%4]: one 16-byte core-matrix row (4 rows of
+            // feature k) per item; 8 consecutive items fill one 128-byte core matrix
+            if (lt >= kXS) mbar_wait(&xc_empty[cs], (uint32_t)((lt / kXS) - 1) & 1);
+            unsigned char* xt = sm + L.xc + cs * 2 * kXT;
+#pragma unroll 4
+            for (int it = r; it < kNB * kR / 4; it += 64) {
+                const int k = ((it >> 3) % (kNB / 8)) * 8 + (it & 7);
+                const int rq = (it >> 3) / (kNB / 8);
+                float v[4];
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int rr = 4 * rq + i;
+                    v[i] = (rr < nr && k < LD) ? rawt[rr * LD + k] : 0.f;
+                }
+                uint4 hi, lo;
+                hi.x = tf32_hi(v[0]);
+                hi.y = tf32_hi(v[1]);
+                hi.z = tf32_hi(v[2]);
+                hi.w = tf32_hi(v[3]);
+                lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
+                lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
+                lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
+                lo.w = __float_as_uint(v[3] - __uint_as_float(hi.w));
+                const int off = (k >> 3) * (kR / 4 * 128) + rq * 128 + (k & 7) * 16;
+                *reinterpret_cast<uint4*>(xt + off) = hi;
+                *reinterpret_cast<uint4*>(xt + kXT + off) = lo;
+            }
+            tgt[cs * kR + r] = (r < nr) ? rawt[r * LD + D + 1] : 0.f;
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&xc_full[cs]);
+                mbar_arrive(&raw_empty[rs]);
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ epilogue
+        const int ew = warp - 4, quad = warp & 3, hf = ew >> 2;
+        const int j = hf * 128 + quad * 32 + lane;  // this thread's hidden unit
+        const int et = ew * 32 + lane;              // epilogue thread index; < kR: also owns row et
+        const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
+        const float w2s = a.Wk[a.H * DP + j];
+        const float b2s = a.Wk[a.H * DP + a.H];
+        float2 acc2 = make_float2(0.f, 0.f);
+        float* out = a.part + (int64_t)blockIdx.x * a.PS;
+        const uint32_t wcol = tmem + lanebase + kColW + 48 * hf;
+        float acc1[kD1];
+#pragma unroll
+        for (int k = 0; k < kD1; k++) acc1[k] = 0.f;
+        auto drain = [&]() {  // dW1 TMEM partial (this thread's unit) -> registers
+            uint32_t r0[32], r1[16];
+            ld32(wcol, r0);
+            ld16(wcol + 32, r1);
+            tmem_ld_wait();
+#pragma unroll
+            for (int k = 0; k < 32; k++) acc1[k] += __uint_as_float(r0[k]);
+#pragma unroll
+            for (int k = 32; k < kD1; k++) acc1[k] += __uint_as_float(r1[k - 32]);
+        };
+        float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+        for (int64_t lt = 0; lt < nt; lt++) {
+            const int cs = (int)(lt % kXS), zb = (int)(lt & 1);
+            const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
+            mbar_wait(&z_full[zb], (uint32_t)(lt >> 1) & 1);
+            mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);  // orders the converters' tgt writes
+            tc_fence_after();
+            const uint32_t zcol = tmem + lanebase + kColZ + 128 * zb + 64 * hf;
+            float h[kR];
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                uint32_t r0[32];
+                ld32(zcol + 32 * c, r0);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 32; i++) h[32 * c + i] = __uint_as_float(r0[i]);
+            }
+            // pass 1: h = sigmoid(z) (z prescaled by -log2 e)
+#pragma unroll
+            for (int i = 0; i < kR; i += 2) {
+                const float2 den = __fadd2_rn(make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1])), bcast2(1.0f));
+                h[i] = rcp_approx(den.x);
+                h[i + 1] = rcp_approx(den.y);
+            }
+            // output partials w2s_j h_j, reduce-scattered over the warp's 32 units per
+            // 32-row half: lane l ends with row 32 c + l
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                float p[32];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const float2 pp = __fmul2_rn(bcast2(w2s), make_float2(h[32 * c + i], h[32 * c + i + 1]));
+                    p[i] = pp.x;
+                    p[i + 1] = pp.y;
+                }
+#pragma unroll
+                for (int st = 0; st < 5; st++) {
+                    const int half = 16 >> st;
+                    const bool up = (lane >> (4 - st)) & 1;
+#pragma unroll
+                    for (int i = 0; i < half; i++) {
+                        const float send = up ? p[i] : p[i + half];
+                        const float keep = up ? p[i + half] : p[i];
+                        p[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+                    }
+                }
+                opart[ew * kR + 32 * c + lane] = p[0];
+            }
+            bar_sync(kEpiBar, NEW * 32);
+            if (et < kR) {  // per row: o, delta_o, loss, confusion (kernels.py:352-375)
+                float zo = 0.f;
+#pragma unroll
+                for (int w = 0; w < NEW; w++) zo += opart[w * kR + et];
+                float d = 0.f;
+                if (row0 + et < a.N) {
+                    const float o = sigmoid_scaled(zo + b2s);
+                    const float tt = tgt[cs * kR + et];
+                    d = (o - tt) * o * (1.0f - o);
+                    loss = fmaf(0.5f * (tt - o), (tt - o), loss);
+                    const bool pred = o >= 0.5f, pos = tt >= 0.5f;
+                    c0 += (pred && pos) ? 1.f : 0.f;
+                    c1 += (!pred && !pos) ? 1.f : 0.f;
+                    c2 += (pred && !pos) ? 1.f : 0.f;
+                    c3 += (!pred && pos) ? 1.f : 0.f;
+                }
+                dob[et] = d;
+                dsum += d;
+            }
+            bar_sync(kEpiBar, NEW * 32);
+            // the backward MMA of the previous tile still reads the single dh lo buffer
+            if (lt >= 1) {
+                mbar_wait(bwd_done, (uint32_t)(lt - 1) & 1);
+                tc_fence_after();
+                if (lt % kDrain == 0) drain();  // the next backward restarts the accumulator
+            }
+            // pass 2: dh = delta_o h (1 - h) -> TMEM as tf32 hi / lo; dW2 += delta_o h
+            const uint32_t locol = tmem + lanebase + kColLo + 64 * hf;
+#pragma unroll
+            for (int c = 0; c < 2; c++) {
+                uint32_t rh[32], rl[32];
+#pragma unroll
+                for (int i = 0; i < 32; i += 2) {
+                    const int r = 32 * c + i;
+                    const float2 d2 = *reinterpret_cast<const float2*>(dob + r);
+                    const float2 hp = make_float2(h[r], h[r + 1]);
+                    const float2 v = __fmul2_rn(d2, hp);
+                    acc2 = __fadd2_rn(acc2, v);
+                    const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
+                    rh[i] = tf32_hi(s2.x);
+                    rh[i + 1] = tf32_hi(s2.y);
+                    rl[i] = __float_as_uint(s2.x - __uint_as_float(rh[i]));
+                    rl[i + 1] = __float_as_uint(s2.y - __uint_as_float(rh[i + 1]));
+                }
+                st32(zcol + 32 * c, rh);
+                st32(locol + 32 * c, rl);
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(dh_ready);
+        }
+        // ---------------------------------------------- per-CTA partial record
+        mbar_wait(bwd_done, (uint32_t)(nt - 1) & 1);
+        tc_fence_after();
+        drain();  // tiles since the last drain (>= 1)
+        {
+            float* o1 = out + (int64_t)j * (D + 1);
+#pragma unroll
+            for (int k = 0; k < kD1; k++)
+                if (k <= D) o1[k] = acc1[k];
+        }
+        out[a.P1 + j] = acc2.x + acc2.y;
+        if (et < kR) {
+            stat[et * 6 + 0] = loss;
+            stat[et * 6 + 1] = c0;
+            stat[et * 6 + 2] = c1;
+            stat[et * 6 + 3] = c2;
+            stat[et * 6 + 4] = c3;
+            stat[et * 6 + 5] = dsum;
+        }
+        bar_sync(kEpiBar, NEW * 32);
+        if (et < 6) {
+            float s = 0.f;
+            for (int r = 0; r < kR; r++) s += stat[r * 6 + et];
+            if (et == 5) out[a.P1 + a.H] = s;
+            else out[a.P1 + a.H + 1 + et] = s;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+    }
+}
+
+int a4(int x) { return (x + 3) / 4 * 4; }
+
+}  // namespace
+
+bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
+    if (N < 1 || D < 1 || D > 33 || (H != 128 && H != 256)) return false;
+    BatchGeom g{};
+    g.D = D;
+    g.H = H;
+    g.N = N;
+    g.DP = D + 1 <= 8 ? 8 : D + 1 <= 16 ? 16 : 34;
+    g.LD = a4(std::max(D + 2, g.DP));
+    if (g.LD > kMaxLD) return false;
+    g.MT = 0;
+    g.HP = H;
+    g.P1 = H * (D + 1);
+    g.PS = a4(g.P1 + H + 6);
+    g.WKS = a4(H * g.DP + 2 * H + 1);
+    g.R = kR;
+    g.ntiles = (N + kR - 1) / kR;
+    g.grid = (int)std::min<int64_t>(g.ntiles, n_sms);
+    g.smem = (size_t)btc_smem(H / 128).total;
+    *out = g;
+    return true;
+}
+
+template <int NH>
+static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t st) {
+    auto k = batchtc_kernel<NH>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "glx: batchtc_kernel<%d> smem=%zu: %s\n", NH, g.smem, cudaGetErrorString(e));
+        return e;
+    }
+    k<<<g.grid, btc_threads(NH), g.smem, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) fprintf(stderr, "glx: batchtc_kernel<%d> launch: %s\n", NH, cudaGetErrorString(e));
+    return e;
+}
+
+cudaError_t launch_batchtc_epoch(const BatchGeom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st) {
+    BtcArgs a;
+    a.Xp = Xp;
+    a.Wk = Wk;
+    a.part = part;
+    a.N = g.N;
+    a.ntiles = g.ntiles;
+    a.D = g.D;
+    a.DP = g.DP;
+    a.LD = g.LD;
+    a.H = g.H;
+    a.P1 = g.P1;
+    a.PS = g.PS;
+    return g.H == 256 ? launch_btc<2>(g, a, st) : launch_btc<1>(g, a, st);
+}
+
+}  // namespace glx

@@ -102,6 +102,9 @@ cudaError_t launch_batch_update(const BatchGeom& g, const float* part, float* W1
 // three-role (forward / activation / backward) epoch kernel; same partial record
 bool batch3_geometry(int64_t N, int D, int H, int n_sms, Batch3Geom* g);
 cudaError_t launch_batch3_epoch(const Batch3Geom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st);
+// tcgen05 epoch kernel (glx_batchtc.cu): H = 128 or 256, D <= 33; same partial record as batch3
+bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* g);
+cudaError_t launch_batchtc_epoch(const BatchGeom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st);
 
 // ------------------------------------------------------------ exact eval
 cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,
