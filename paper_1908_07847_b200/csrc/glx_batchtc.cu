@@ -61,10 +61,25 @@ constexpr int kEpiBar = 1;
 // ~10^5 rows per CTA drifted by ~1e-3 relative at 64Mi rows; short partials keep
 // the sum at the fp32 CUDA-core kernel's accuracy (tests/test_gpu_fullsize.py)
 #ifndef GLX_BTC_DRAIN
-#define GLX_BTC_DRAIN 1
+#define GLX_BTC_DRAIN 4
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
-constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
+constexpr int kD1 = 34;
+#ifndef GLX_BTC_EXP
+#define GLX_BTC_EXP 0  // diagnostic builds only: 1 no MUFU sigmoid, 2 no backward MMAs, 3 no forward MMAs
+#endif  // dW1 columns kept per unit (D + 1 <= 34)
+
+#ifdef GLX_BTC_TIMING
+__device__ unsigned long long g_btc_dbg[4096];
+#define BTT(slot)                                                                                      \
+    do {                                                                                               \
+        if (blockIdx.x == 0 && lane == 0 && lt >= 8 && lt < 24) g_btc_dbg[((lt - 8) * 16 + (slot)) * 2 + (warp == 4 ? 0 : 1)] = clock64(); \
+    } while (0)
+#else
+#define BTT(slot) \
+    do {          \
+    } while (0)
+#endif
 
 struct BtcArgs {
     const float* Xp;
@@ -79,7 +94,7 @@ struct BtcSmem {  // byte offsets
     int total;
 };
 
-__host__ __device__ constexpr int btc_threads(int NH) { return (4 + 4 * NH) * 32; }
+__host__ __device__ constexpr int btc_threads(int NH) { return (4 + 8 * NH) * 32; }
 
 __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
     BtcSmem s{};
@@ -89,7 +104,7 @@ __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
     s.raw = s.xc + kXS * 2 * kXT;
     s.tgt = s.raw + kXR * kRawBytes;
     s.opart = s.tgt + kXS * kR * 4;
-    s.dob = s.opart + 4 * NH * kR * 4;
+    s.dob = s.opart + 8 * NH * 32 * 4;
     s.stat = s.dob + kR * 4;
     s.bars = s.stat + kR * 6 * 4;
     s.total = s.bars + 256;
@@ -110,27 +125,42 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int N, bool b_mn_major) {
            ((uint32_t)(128 >> 4) << 24);
 }
 
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+// The MMA warp runs its loop converged (warp-uniform operands stay in uniform
+// registers); `e` is the elect.sync flag: one lane issues each instruction.
+__device__ __forceinline__ uint32_t elect_one() {
+    uint32_t e;
+    asm volatile("{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.b32 %0, 1, 0, P;\n\t}" : "=r"(e));
+    return e;
+}
+
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc, uint32_t e) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, q;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        "setp.ne.b32 q, %5, 0;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc), "r"(e)
         : "memory");
 }
 
-__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc,
+                                       uint32_t e) {
     asm volatile(
-        "{\n\t.reg .pred p;\n\t"
+        "{\n\t.reg .pred p, q;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
-        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+        "setp.ne.b32 q, %5, 0;\n\t"
+        "@q tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc), "r"(e)
         : "memory");
 }
 
-__device__ __forceinline__ void commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
+__device__ __forceinline__ void commit(uint64_t* bar, uint32_t e) {
+    asm volatile(
+        "{\n\t.reg .pred q;\n\t"
+        "setp.ne.b32 q, %1, 0;\n\t"
+        "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(e)
+        : "memory");
 }
 
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -157,6 +187,21 @@ __device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&r)[16]) {
         : "memory");
 }
 
+__device__ __forceinline__ void ld1(uint32_t taddr, uint32_t& r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void ld2(uint32_t taddr, uint32_t (&r)[2]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(taddr) : "memory");
+}
+__device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
+        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -175,7 +220,7 @@ __device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v)
 
 template <int NH>
 __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
-    constexpr int NEW = 4 * NH;  // epilogue warps
+    constexpr int NEW = 8 * NH;  // epilogue warps: 4 lane quadrants x NH unit halves x 2 row blocks
     constexpr BtcSmem L = btc_smem(NH);
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
@@ -268,55 +313,73 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
-        if (lane == 0) {
+        {
+            const uint32_t el = elect_one();
             constexpr uint32_t idf = idesc_tf32(kR, false);
             constexpr uint32_t idb = idesc_tf32(kNB, false);
-            const uint32_t w_hi = smem_u32(sm + L.w), w_lo = w_hi + NH * kWT;
+            // descriptors are built once and advanced by (byte offset >> 4) in the start
+            // field (shared addresses < 256 KB: no carry out of the 14-bit field)
+            const uint64_t dwh = desc_ns(smem_u32(sm + L.w), 128, kFC * 128);
+            const uint64_t dwl = desc_ns(smem_u32(sm + L.w + NH * kWT), 128, kFC * 128);
             auto backward = [&](int64_t lt) {
                 const int cs = (int)(lt % kXS), zb = (int)(lt & 1);
+                BTT(8);
                 mbar_wait(dh_ready, (uint32_t)lt & 1);
                 mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);
                 tc_fence_after();
-                const uint32_t x_hi = smem_u32(sm + L.xc + cs * 2 * kXT), x_lo = x_hi + kXT;
-#pragma unroll 1
+                BTT(9);
+                const uint64_t dth = desc_ns(smem_u32(sm + L.xc + cs * 2 * kXT), 128, kR / 4 * 128);
+                const uint64_t dtl = dth + (kXT >> 4);
+#pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColW + 48 * hf;
                     const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf, alo = tmem + kColLo + 64 * hf;
-#pragma unroll 1
+#pragma unroll
                     for (int s = 0; s < kR / 8; s++) {
-                        const uint64_t bh = desc_ns(x_hi + s * 256, 128, kR / 4 * 128);
-                        const uint64_t bl = desc_ns(x_lo + s * 256, 128, kR / 4 * 128);
-                        mma_ts(d, alo + 8 * s, bh, idb, (lt % kDrain) != 0 || s != 0);
-                        mma_ts(d, ahi + 8 * s, bl, idb, 1);
-                        mma_ts(d, ahi + 8 * s, bh, idb, 1);
+                        const uint64_t bh = dth + (s * 256 >> 4);
+                        const uint64_t bl = dtl + (s * 256 >> 4);
+#if GLX_BTC_EXP == 2
+                        if (s == 0) mma_ts(d, alo + 8 * s, bh, idb, 0, el);
+#else
+                        mma_ts(d, alo + 8 * s, bh, idb, (lt % kDrain) != 0 || s != 0, el);
+                        mma_ts(d, ahi + 8 * s, bl, idb, 1, el);
+                        mma_ts(d, ahi + 8 * s, bh, idb, 1, el);
+#endif
                     }
                 }
-                commit(&xc_empty[cs]);
-                commit(bwd_done);
+                commit(&xc_empty[cs], el);
+                commit(bwd_done, el);
+                BTT(10);
             };
             for (int64_t lt = 0; lt < nt; lt++) {
                 const int fs = (int)(lt % kXFS), zb = (int)(lt & 1);
+                BTT(11);
                 mbar_wait(&xf_full[fs], (uint32_t)(lt / kXFS) & 1);
                 tc_fence_after();
-                const uint32_t x_hi = smem_u32(sm + L.xf + fs * 2 * kXF), x_lo = x_hi + kXF;
-#pragma unroll 1
+                BTT(12);
+                const uint64_t dxh = desc_ns(smem_u32(sm + L.xf + fs * 2 * kXF), 128, kFC * 128);
+                const uint64_t dxl = dxh + (kXF >> 4);
+#pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColZ + 128 * zb + 64 * hf;
-                    const uint32_t wh = w_hi + hf * kWT, wl = w_lo + hf * kWT;
+                    const uint64_t wh = dwh + (hf * kWT >> 4), wl = dwl + (hf * kWT >> 4);
+#if GLX_BTC_EXP == 3
+                    mma_ss(d, wl, dxh, idf, 0, el);
+                    if (false)
+#endif
 #pragma unroll
                     for (int s = 0; s < kFC / 2; s++) {
-                        mma_ss(d, desc_ns(wl + s * 256, 128, kFC * 128), desc_ns(x_hi + s * 256, 128, kFC * 128), idf,
-                               s != 0);
-                        mma_ss(d, desc_ns(wh + s * 256, 128, kFC * 128), desc_ns(x_lo + s * 256, 128, kFC * 128), idf,
-                               1);
+                        mma_ss(d, wl + (s * 256 >> 4), dxh + (s * 256 >> 4), idf, s != 0, el);
+                        mma_ss(d, wh + (s * 256 >> 4), dxl + (s * 256 >> 4), idf, 1, el);
                     }
+#if GLX_BTC_EXP != 3
 #pragma unroll
-                    for (int s = 0; s < kFC / 2; s++)
-                        mma_ss(d, desc_ns(wh + s * 256, 128, kFC * 128), desc_ns(x_hi + s * 256, 128, kFC * 128), idf,
-                               1);
+                    for (int s = 0; s < kFC / 2; s++) mma_ss(d, wh + (s * 256 >> 4), dxh + (s * 256 >> 4), idf, 1, el);
+#endif
                 }
-                commit(&xf_empty[fs]);
-                commit(&z_full[zb]);
+                commit(&xf_empty[fs], el);
+                commit(&z_full[zb], el);
+                BTT(13);
                 if (lt >= 1) backward(lt - 1);
             }
             backward(nt - 1);
@@ -393,7 +456,9 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         }
     } else {
         // ------------------------------------------------------------ epilogue
-        const int ew = warp - 4, quad = warp & 3, hf = ew >> 2;
+        // warp ew: TMEM lane quadrant quad = warp % 4 -> units 32 quad .. + 31 of half hf;
+        // row block rb -> rows 32 rb .. 32 rb + 31 of the tile
+        const int ew = warp - 4, quad = warp & 3, hf = (ew >> 2) % NH, rb = ew / (4 * NH);
         const int j = hf * 128 + quad * 32 + lane;  // this thread's hidden unit
         const int et = ew * 32 + lane;              // epilogue thread index; < kR: also owns row et
         const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
@@ -402,51 +467,67 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         float2 acc2 = make_float2(0.f, 0.f);
         float* out = a.part + (int64_t)blockIdx.x * a.PS;
         const uint32_t wcol = tmem + lanebase + kColW + 48 * hf;
-        float acc1[kD1];
+        constexpr int kDH = kD1 / 2;  // dW1 columns drained by each row block (0..16 | 17..33)
+        float acc1[kDH];
 #pragma unroll
-        for (int k = 0; k < kD1; k++) acc1[k] = 0.f;
+        for (int k = 0; k < kDH; k++) acc1[k] = 0.f;
         auto drain = [&]() {  // dW1 TMEM partial (this thread's unit) -> registers
-            uint32_t r0[32], r1[16];
-            ld32(wcol, r0);
-            ld16(wcol + 32, r1);
-            tmem_ld_wait();
+            if (rb == 0) {
+                uint32_t r0[16], r1;
+                ld16(wcol, r0);
+                ld1(wcol + 16, r1);
+                tmem_ld_wait();
 #pragma unroll
-            for (int k = 0; k < 32; k++) acc1[k] += __uint_as_float(r0[k]);
+                for (int k = 0; k < 16; k++) acc1[k] += __uint_as_float(r0[k]);
+                acc1[16] += __uint_as_float(r1);
+            } else {
+                uint32_t r0[16], r1[2];
+                ld16(wcol + 16, r0);
+                ld2(wcol + 32, r1);
+                tmem_ld_wait();
 #pragma unroll
-            for (int k = 32; k < kD1; k++) acc1[k] += __uint_as_float(r1[k - 32]);
+                for (int k = 0; k < 15; k++) acc1[k] += __uint_as_float(r0[k + 1]);
+                acc1[15] += __uint_as_float(r1[0]);
+                acc1[16] += __uint_as_float(r1[1]);
+            }
         };
         float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
         for (int64_t lt = 0; lt < nt; lt++) {
             const int cs = (int)(lt % kXS), zb = (int)(lt & 1);
             const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
+            BTT(0);
             mbar_wait(&z_full[zb], (uint32_t)(lt >> 1) & 1);
             mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);  // orders the converters' tgt writes
             tc_fence_after();
-            const uint32_t zcol = tmem + lanebase + kColZ + 128 * zb + 64 * hf;
-            float h[kR];
-#pragma unroll
-            for (int c = 0; c < 2; c++) {
+            BTT(1);
+            const uint32_t zcol = tmem + lanebase + kColZ + 128 * zb + 64 * hf + 32 * rb;
+            float h[32];
+            {
                 uint32_t r0[32];
-                ld32(zcol + 32 * c, r0);
+                ld32(zcol, r0);
                 tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 32; i++) h[32 * c + i] = __uint_as_float(r0[i]);
+                for (int i = 0; i < 32; i++) h[i] = __uint_as_float(r0[i]);
             }
             // pass 1: h = sigmoid(z) (z prescaled by -log2 e)
 #pragma unroll
-            for (int i = 0; i < kR; i += 2) {
+            for (int i = 0; i < 32; i += 2) {
+#if GLX_BTC_EXP == 1
+                h[i] = h[i] * 0.01f + 0.5f;
+                h[i + 1] = h[i + 1] * 0.01f + 0.5f;
+#else
                 const float2 den = __fadd2_rn(make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1])), bcast2(1.0f));
                 h[i] = rcp_approx(den.x);
                 h[i + 1] = rcp_approx(den.y);
+#endif
             }
-            // output partials w2s_j h_j, reduce-scattered over the warp's 32 units per
-            // 32-row half: lane l ends with row 32 c + l
-#pragma unroll
-            for (int c = 0; c < 2; c++) {
+            // output partials w2s_j h_j reduce-scattered over the warp's 32 units: lane l
+            // ends with row 32 rb + l
+            {
                 float p[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
-                    const float2 pp = __fmul2_rn(bcast2(w2s), make_float2(h[32 * c + i], h[32 * c + i + 1]));
+                    const float2 pp = __fmul2_rn(bcast2(w2s), make_float2(h[i], h[i + 1]));
                     p[i] = pp.x;
                     p[i + 1] = pp.y;
                 }
@@ -461,13 +542,20 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                         p[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
                     }
                 }
-                opart[ew * kR + 32 * c + lane] = p[0];
+                opart[ew * 32 + lane] = p[0];
             }
+            BTT(2);
             bar_sync(kEpiBar, NEW * 32);
+            BTT(3);
             if (et < kR) {  // per row: o, delta_o, loss, confusion (kernels.py:352-375)
-                float zo = 0.f;
+                const float* op = opart + (et >> 5) * (4 * NH * 32) + (et & 31);
+                float z0 = 0.f, z1 = 0.f;
 #pragma unroll
-                for (int w = 0; w < NEW; w++) zo += opart[w * kR + et];
+                for (int w = 0; w < 4 * NH; w += 2) {
+                    z0 += op[w * 32];
+                    z1 += op[(w + 1) * 32];
+                }
+                const float zo = z0 + z1;
                 float d = 0.f;
                 if (row0 + et < a.N) {
                     const float o = sigmoid_scaled(zo + b2s);
@@ -484,21 +572,24 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 dsum += d;
             }
             bar_sync(kEpiBar, NEW * 32);
+            BTT(4);
             // the backward MMA of the previous tile still reads the single dh lo buffer
             if (lt >= 1) {
                 mbar_wait(bwd_done, (uint32_t)(lt - 1) & 1);
                 tc_fence_after();
+                BTT(5);
                 if (lt % kDrain == 0) drain();  // the next backward restarts the accumulator
             }
+            BTT(6);
             // pass 2: dh = delta_o h (1 - h) -> TMEM as tf32 hi / lo; dW2 += delta_o h
-            const uint32_t locol = tmem + lanebase + kColLo + 64 * hf;
+            const uint32_t locol = tmem + lanebase + kColLo + 64 * hf + 32 * rb;
 #pragma unroll
             for (int c = 0; c < 2; c++) {
-                uint32_t rh[32], rl[32];
+                uint32_t rh[16], rl[16];
 #pragma unroll
-                for (int i = 0; i < 32; i += 2) {
-                    const int r = 32 * c + i;
-                    const float2 d2 = *reinterpret_cast<const float2*>(dob + r);
+                for (int i = 0; i < 16; i += 2) {
+                    const int r = 16 * c + i;
+                    const float2 d2 = *reinterpret_cast<const float2*>(dob + 32 * rb + r);
                     const float2 hp = make_float2(h[r], h[r + 1]);
                     const float2 v = __fmul2_rn(d2, hp);
                     acc2 = __fadd2_rn(acc2, v);
@@ -508,25 +599,27 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     rl[i] = __float_as_uint(s2.x - __uint_as_float(rh[i]));
                     rl[i + 1] = __float_as_uint(s2.y - __uint_as_float(rh[i + 1]));
                 }
-                st32(zcol + 32 * c, rh);
-                st32(locol + 32 * c, rl);
+                st16(zcol + 16 * c, rh);
+                st16(locol + 16 * c, rl);
             }
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(dh_ready);
+            BTT(7);
         }
         // ---------------------------------------------- per-CTA partial record
         mbar_wait(bwd_done, (uint32_t)(nt - 1) & 1);
         tc_fence_after();
         drain();  // tiles since the last drain (>= 1)
         {
-            float* o1 = out + (int64_t)j * (D + 1);
+            float* o1 = out + (int64_t)j * (D + 1) + kDH * rb;
 #pragma unroll
-            for (int k = 0; k < kD1; k++)
-                if (k <= D) o1[k] = acc1[k];
+            for (int k = 0; k < kDH; k++)
+                if (kDH * rb + k <= D) o1[k] = acc1[k];
         }
-        out[a.P1 + j] = acc2.x + acc2.y;
+        bar_sync(kEpiBar, NEW * 32);  // opart is free: exchange the dW2 partials of the two row blocks
+        if (rb == 1) opart[j] = acc2.x + acc2.y;
         if (et < kR) {
             stat[et * 6 + 0] = loss;
             stat[et * 6 + 1] = c0;
@@ -536,6 +629,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             stat[et * 6 + 5] = dsum;
         }
         bar_sync(kEpiBar, NEW * 32);
+        if (rb == 0) out[a.P1 + j] = (acc2.x + acc2.y) + opart[j];
         if (et < 6) {
             float s = 0.f;
             for (int r = 0; r < kR; r++) s += stat[r * 6 + et];
@@ -552,6 +646,26 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 }
 
 int a4(int x) { return (x + 3) / 4 * 4; }
+#ifdef GLX_BTC_TIMING
+}  // namespace
+}  // namespace glx
+extern "C" void glx_btc_timing_dump(void) {
+    unsigned long long h[4096];
+    cudaMemcpyFromSymbol(h, glx::g_btc_dbg, sizeof(h));
+    // per tile lt (8..23): epilogue slots 0-7 (warp 4), MMA slots 8-13 (warp 1; lt of the backward for 8-10)
+    for (int t = 0; t < 16; t++) {
+        const unsigned long long* e = h + t * 32;
+        printf("lt %2d epi: wait_z %6lld pass1 %6lld bar1 %6lld rows+bar2 %6lld wait_bwd %6lld drain %6lld pass2 %6lld | "
+               "mma: wait_dh %6lld bwd_issue %6lld wait_xf %6lld fwd_issue %6lld | t0 %lld\n",
+               t + 8, (long long)(e[2] - e[0]), (long long)(e[4] - e[2]), (long long)(e[6] - e[4]),
+               (long long)(e[8] - e[6]), (long long)(e[10] - e[8]), (long long)(e[12] - e[10]),
+               (long long)(e[14] - e[12]), (long long)(e[19] - e[17]), (long long)(e[21] - e[19]),
+               (long long)(e[25] - e[23]), (long long)(e[27] - e[25]), (long long)(e[0] - h[0]));
+    }
+}
+namespace glx {
+namespace {
+#endif
 
 }  // namespace
 
