@@ -296,16 +296,37 @@ def run_gpu(args):
     tr_file = ROOT / "profiles" / "traffic.json"
     if tr_file.exists():
         traffic = json.loads(tr_file.read_text()).get("batch_epoch_kernel_bytes_per_launch")
-    roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": traffic,
-                "kernel": "batch3_kernel<34,4,4> (three warp-specialised roles)", "kernel_ms_per_launch": k_ms,
-                "kernel_share_of_step": k_ms / (elapsed / args.steps) if elapsed else None,
-                "kernel_timing": kernel_timing,
-                "algorithmic_flops_per_launch": flops_per_launch,
-                "algorithmic_hbm_bytes_per_launch": ROWS_PER_GPU * (4 * D + 1),
-                "hbm_frac": ROWS_PER_GPU * (4 * D + 1) / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6545.9),
-                "peak_source": "glx_fp32_peak FFMA2 microbenchmark on this GPU in this run (MEASURED_PEAKS.json "
-                               "has no FP32 figure)"}
+    kind = int(L.glx_batch_kernel_kind(ROWS_PER_GPU, D, H))
+    common = {"traffic": traffic, "kernel_ms_per_launch": k_ms,
+              "kernel_share_of_step": k_ms / (elapsed / args.steps) if elapsed else None,
+              "kernel_timing": kernel_timing, "algorithmic_flops_per_launch": flops_per_launch,
+              "algorithmic_hbm_bytes_per_launch": ROWS_PER_GPU * (4 * D + 1),
+              "hbm_frac": ROWS_PER_GPU * (4 * D + 1) / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6545.9),
+              "fp32_peak_tflops": fp32_peak, "fp32_frac": achieved / fp32_peak}
+    if kind == 2:
+        # tcgen05 kind::tf32, 3xTF32: per 64-row tile 30 forward MMAs (M=128 units, N=64 rows,
+        # K=8) and 48 backward MMAs (M=128, N=48 features, K=8 rows) per 128-unit half pair
+        tf32_peak = peaks().get("bf16_tflops_sustained", 1355.8) / 2
+        tiles = -(-ROWS_PER_GPU // 64)
+        mma_flops = tiles * (H // 128) * (15 * 2 * 128 * 64 * 8 + 24 * 2 * 128 * 48 * 8)
+        mufu_peak = 148 * 16 * clk_mhz_for_peak(local) * 1e6
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / tf32_peak,
+                    "kernel": "batchtc_kernel<2> (tcgen05 kind::tf32, 3xTF32, deltas in TMEM)",
+                    "executed_mma_flops_per_launch": mma_flops,
+                    "executed_mma_frac": mma_flops / (k_ms * 1e-3) / 1e12 / tf32_peak,
+                    "mufu_frac": 2 * ROWS_PER_GPU * H / (k_ms * 1e-3) / mufu_peak,
+                    "peak_source": "dense TF32 = half of MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, "
+                                   "back to back); executed_mma_frac counts the 3xTF32 MMA work incl. K/N padding; "
+                                   "mufu_frac = 2 MUFU ops per hidden activation / (148 SMs x 16/clk x SM clock)",
+                    **common}
+    else:
+        roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": achieved / fp32_peak,
+                    "kernel": "batch3_kernel<34,4,4> (three warp-specialised roles)" if kind == 1 else
+                              "batch_epoch_kernel (two roles)",
+                    "peak_source": "glx_fp32_peak FFMA2 microbenchmark on this GPU in this run (MEASURED_PEAKS.json "
+                                   "has no FP32 figure)", **common}
 
     # end-to-end through the public API, inputs in pinned host memory: the host
     # segment API on one GPU, the data-parallel engine (every rank) on N
@@ -386,6 +407,16 @@ def run_e2e_dp(g, torch, dp, feats, targets, n_total, world, reps=3):
             "d2h_bytes_per_step": int(w_bytes + 5 * 8 * E_E2E), "epochs_per_step": E_E2E, "seconds_per_step": dt,
             "per_rank": True, "ranks": world,
             "api": "dp.DeviceEngine + dp.train_data_parallel (glx_batch_grad, NCCL all-reduce, glx_batch_apply)"}
+
+
+def clk_mhz_for_peak(dev) -> float:
+    """SM clock (MHz) for the MUFU peak: the max SM clock nvidia-smi reports, else MEASURED_PEAKS."""
+    try:
+        out = subprocess.run(["nvidia-smi", "-i", str(dev), "--query-gpu=clocks.max.sm", "--format=csv,noheader,nounits"],
+                             capture_output=True, text=True, timeout=20).stdout.strip()
+        return float(out.splitlines()[0])
+    except Exception:
+        return float(peaks().get("sm_max_mhz", 1965.0))
 
 
 def peaks():

@@ -152,6 +152,13 @@ int glx_minmax_apply(const float* X, int64_t N, int32_t D, const float* col_min,
 int glx_train_batch(float* w_ih, float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H, int64_t epochs,
                     double lr, double* stats_hist, int32_t* nonfinite, void* stream);
 
+/* Which full-batch epoch kernel glx_train_batch / glx_batch_grad run for this
+ * shape: 2 = tcgen05 3xTF32 kernel (H = 128 or 256, D <= 33), 1 = three-role
+ * FP32 kernel, 0 = two-role FP32 kernel, -1 = unsupported shape. Selection
+ * only (no device work); GLX_BATCH_KERNEL=3 / =2 cap the choice at 1 / 0.
+ * No reference counterpart (diagnostic). */
+int glx_batch_kernel_kind(int64_t N, int32_t D, int32_t H);
+
 /* Data-parallel split of one epoch (config 4): glx_batch_grad writes this
  * rank's gradient SUM over its N rows (not divided by N) into grad (device
  * double[glx_batch_grad_len]), laid out as [dW1 (H(D+1)) | dW2 (H+1) | loss,

@@ -54,6 +54,7 @@ SIGNATURES = {
     "glx_pack_rows": (_int, [_vp, _vp, _vp, _i64, _i32, _vp, _vp]),
     "glx_train_batch": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i64, _dbl, _vp, _vp, _vp]),
     "glx_batch_grad_len": (_i64, [_i32, _i32]),
+    "glx_batch_kernel_kind": (_i32, [_i64, _i32, _i32]),
     "glx_batch_grad": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _vp, _vp]),
     "glx_batch_apply": (_int, [_vp, _vp, _vp, _i32, _i32, _dbl, _vp, _vp]),
     "glx_eval": (_int, [_vp, _vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),

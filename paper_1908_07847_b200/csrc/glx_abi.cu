@@ -484,6 +484,13 @@ int glx_train_batch(float* w_ih, float* w_ho, const float* Xp, int64_t N, int32_
 
 int64_t glx_batch_grad_len(int32_t D, int32_t H) { return (int64_t)H * (D + 1) + H + 1 + 5; }
 
+int glx_batch_kernel_kind(int64_t N, int32_t D, int32_t H) {
+    BatchGeom g;
+    int kind = -1;
+    if (N < 1 || D < 1 || H < 1 || !train_geometry(N, D, H, &g, &kind)) return -1;
+    return kind;
+}
+
 int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int32_t D, int32_t H,
                    double* grad, void* stream) {
     int rc = check_dims(N, D, H);

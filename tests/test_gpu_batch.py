@@ -20,6 +20,8 @@ def _case(N, D, H, seed, signal="planted-linear"):
 @pytest.mark.parametrize("N,D,H", [
     (2, 33, 33), (65, 33, 33), (1000, 33, 33), (1000, 33, 256), (777, 33, 512), (500, 33, 19),
     (300, 7, 5), (301, 15, 16), (250, 30, 30), (4099, 33, 64), (130, 1, 1), (513, 32, 36),
+    # tcgen05 kernel shapes (H = 128 / 256): exact tile, one row past a tile, D < 33
+    (64, 33, 128), (65, 33, 256), (129, 33, 128), (1000, 33, 128), (3001, 7, 256), (2000, 16, 128),
 ])
 def test_batch_vs_oracle(gpu, N, D, H):
     x, l, t, net0 = _case(N, D, H, seed=N % 97)
@@ -36,6 +38,19 @@ def test_batch_vs_oracle(gpu, N, D, H):
     assert stats[0, 1:].sum() == N
     assert abs(stats[0, 0] - loss) <= 1e-4 * max(1.0, loss)
     assert np.abs(stats[0, 1:] - np.array([tp, tn, fp, fn])).sum() <= 2  # |o-0.5| < 1e-6 rows may flip
+
+
+def test_tcgen05_kernel_selected_for_headline_shapes(gpu):
+    """configs 2 and 4 (33 -> 128 / 256 -> 1) run the tcgen05 3xTF32 epoch kernel; other
+    widths fall back to the FP32 CUDA-core kernels (glx_batch_kernel_kind)."""
+    import paper_1908_07847_b200._lib as L
+
+    lib = L.load()
+    assert lib.glx_batch_kernel_kind(1 << 20, 33, 256) == 2
+    assert lib.glx_batch_kernel_kind(1 << 26, 33, 256) == 2
+    assert lib.glx_batch_kernel_kind(1000, 33, 128) == 2
+    assert lib.glx_batch_kernel_kind(1000, 33, 64) in (0, 1)
+    assert lib.glx_batch_kernel_kind(1000, 40, 256) == -1
 
 
 def test_batch_is_deterministic(gpu):
