@@ -171,8 +171,18 @@ def config4_1gpu(L, peak, cpu=None, rows=67_108_864, epochs=5):
     return {"config": "4 (1 GPU): 64Mi rows synthetic_matrix(...,33,0,planted-linear), 33->256->1 full batch",
             "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
             "tflops": flops / (ms * 1e-3) / 1e12, "frac_fp32_peak": flops / (ms * 1e-3) / 1e12 / peak,
+            "kernel": ["two-role FP32", "batch3 FP32", "batchtc tcgen05 3xTF32"][L.glx_batch_kernel_kind(rows, D, H)],
+            "frac_tf32_dense_sustained": flops / (ms * 1e-3) / 1e12 / (_peaks().get("bf16_tflops_sustained", 1355.8) / 2),
             "data_gen_and_pack_s": gen_s,
             "data_gen_note": "device generation + packing (host numpy generation + upload of the same rows: 19.4 s)"}
+
+
+def _peaks():
+    import json
+    from pathlib import Path
+
+    p = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    return json.loads(p.read_text()) if p.exists() else {}
 
 
 def config5(L, peak, cpu=None, rows=16_777_216, epochs=3):
