@@ -104,9 +104,9 @@ __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
     s.raw = s.xc + kXS * 2 * kXT;
     s.tgt = s.raw + kXR * kRawBytes;
     s.opart = s.tgt + kXS * kR * 4;
-    s.dob = s.opart + 8 * NH * 32 * 4;
-    s.stat = s.dob + kR * 4;
-    s.bars = s.stat + kR * 6 * 4;
+    s.dob = s.opart + 2 * 8 * NH * 32 * 4;  // output partials, double-buffered by tile parity
+    s.stat = s.dob + 8 * NH * 32 * 4;  // dob: one 32-row slot per epilogue warp
+    s.bars = s.stat;                   // (the row statistics reuse the partials buffer at the end)
     s.total = s.bars + 256;
     return s;
 }
@@ -237,7 +237,6 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
     float* tgt = reinterpret_cast<float*>(sm + L.tgt);
     float* opart = reinterpret_cast<float*>(sm + L.opart);
     float* dob = reinterpret_cast<float*>(sm + L.dob);
-    float* stat = reinterpret_cast<float*>(sm + L.stat);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nt = (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA (>= 1)
@@ -542,13 +541,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                         p[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
                     }
                 }
-                opart[ew * 32 + lane] = p[0];
+                opart[(int)(lt & 1) * NEW * 32 + ew * 32 + lane] = p[0];
             }
             BTT(2);
             bar_sync(kEpiBar, NEW * 32);
             BTT(3);
-            if (et < kR) {  // per row: o, delta_o, loss, confusion (kernels.py:352-375)
-                const float* op = opart + (et >> 5) * (4 * NH * 32) + (et & 31);
+            {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);
+               // every warp computes its own rows' delta_o, one warp per block keeps the statistics
+                const int r = 32 * rb + lane;
+                const float* op = opart + (int)(lt & 1) * NEW * 32 + rb * (4 * NH * 32) + lane;
                 float z0 = 0.f, z1 = 0.f;
 #pragma unroll
                 for (int w = 0; w < 4 * NH; w += 2) {
@@ -557,21 +558,23 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 }
                 const float zo = z0 + z1;
                 float d = 0.f;
-                if (row0 + et < a.N) {
+                if (row0 + r < a.N) {
                     const float o = sigmoid_scaled(zo + b2s);
-                    const float tt = tgt[cs * kR + et];
+                    const float tt = tgt[cs * kR + r];
                     d = (o - tt) * o * (1.0f - o);
-                    loss = fmaf(0.5f * (tt - o), (tt - o), loss);
-                    const bool pred = o >= 0.5f, pos = tt >= 0.5f;
-                    c0 += (pred && pos) ? 1.f : 0.f;
-                    c1 += (!pred && !pos) ? 1.f : 0.f;
-                    c2 += (pred && !pos) ? 1.f : 0.f;
-                    c3 += (!pred && pos) ? 1.f : 0.f;
+                    if (hf == 0 && quad == 0) {
+                        loss = fmaf(0.5f * (tt - o), (tt - o), loss);
+                        const bool pred = o >= 0.5f, pos = tt >= 0.5f;
+                        c0 += (pred && pos) ? 1.f : 0.f;
+                        c1 += (!pred && !pos) ? 1.f : 0.f;
+                        c2 += (pred && !pos) ? 1.f : 0.f;
+                        c3 += (!pred && pos) ? 1.f : 0.f;
+                        dsum += d;
+                    }
                 }
-                dob[et] = d;
-                dsum += d;
+                dob[ew * 32 + lane] = d;
+                __syncwarp();
             }
-            bar_sync(kEpiBar, NEW * 32);
             BTT(4);
             // the backward MMA of the previous tile still reads the single dh lo buffer
             if (lt >= 1) {
@@ -589,7 +592,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
                     const int r = 16 * c + i;
-                    const float2 d2 = *reinterpret_cast<const float2*>(dob + 32 * rb + r);
+                    const float2 d2 = *reinterpret_cast<const float2*>(dob + ew * 32 + r);
                     const float2 hp = make_float2(h[r], h[r + 1]);
                     const float2 v = __fmul2_rn(d2, hp);
                     acc2 = __fadd2_rn(acc2, v);
@@ -620,13 +623,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         }
         bar_sync(kEpiBar, NEW * 32);  // opart is free: exchange the dW2 partials of the two row blocks
         if (rb == 1) opart[j] = acc2.x + acc2.y;
-        if (et < kR) {
-            stat[et * 6 + 0] = loss;
-            stat[et * 6 + 1] = c0;
-            stat[et * 6 + 2] = c1;
-            stat[et * 6 + 3] = c2;
-            stat[et * 6 + 4] = c3;
-            stat[et * 6 + 5] = dsum;
+        float* stat = opart + 2 * NEW * 32 - kR * 6;  // behind the dW2 exchange slots (H <= 256 floats)
+        if (hf == 0 && quad == 0) {  // the statistics warps: rows 32 rb + lane
+            const int r = 32 * rb + lane;
+            stat[r * 6 + 0] = loss;
+            stat[r * 6 + 1] = c0;
+            stat[r * 6 + 2] = c1;
+            stat[r * 6 + 3] = c2;
+            stat[r * 6 + 4] = c3;
+            stat[r * 6 + 5] = dsum;
         }
         bar_sync(kEpiBar, NEW * 32);
         if (rb == 0) out[a.P1 + j] = (acc2.x + acc2.y) + opart[j];
