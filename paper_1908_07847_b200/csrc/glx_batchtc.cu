@@ -218,6 +218,28 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 
 __device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v) & kTf32Mask; }
 
+// 2^x for a pair on the FMA/ALU pipes (pass 1 is MUFU-bound): round-to-nearest by
+// the 1.5 * 2^23 magic add, degree-5 polynomial on [-1/2, 1/2] (max rel. error 2.3e-7
+// in fp32 Horner, on par with ex2.approx), exponent inserted with an integer add;
+// |x| clamped to 125 (1 + 2^-125 == 1 and 1 / (1 + 2^125) ~ 0 in fp32 either way)
+#ifndef GLX_BTC_POLY
+#define GLX_BTC_POLY 1  // element pairs per 4 that take the polynomial (0: all MUFU)
+#endif
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+    x.x = fminf(fmaxf(x.x, -125.f), 125.f);
+    x.y = fminf(fmaxf(x.y, -125.f), 125.f);
+    const float2 t = __fadd2_rn(x, bcast2(12582912.0f));
+    const float2 fi = __fadd2_rn(t, bcast2(-12582912.0f));
+    const float2 f = __fadd2_rn(x, make_float2(-fi.x, -fi.y));
+    float2 p = ffma2(bcast2(0.001327646430581808f), f, bcast2(0.009675540961325169f));
+    p = ffma2(p, f, bcast2(0.05550713464617729f));
+    p = ffma2(p, f, bcast2(0.24022120237350464f));
+    p = ffma2(p, f, bcast2(0.6931469440460205f));
+    p = ffma2(p, f, bcast2(1.0000001192092896f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
 template <int NH>
 __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
     constexpr int NEW = 8 * NH;  // epilogue warps: 4 lane quadrants x NH unit halves x 2 row blocks
@@ -515,7 +537,9 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 h[i] = h[i] * 0.01f + 0.5f;
                 h[i + 1] = h[i + 1] * 0.01f + 0.5f;
 #else
-                const float2 den = __fadd2_rn(make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1])), bcast2(1.0f));
+                const float2 e2 = ((i >> 1) % 4 < GLX_BTC_POLY) ? exp2_poly2(make_float2(h[i], h[i + 1]))
+                                                                 : make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
+                const float2 den = __fadd2_rn(e2, bcast2(1.0f));
                 h[i] = rcp_approx(den.x);
                 h[i + 1] = rcp_approx(den.y);
 #endif
