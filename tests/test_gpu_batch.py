@@ -21,7 +21,8 @@ def _case(N, D, H, seed, signal="planted-linear"):
     (2, 33, 33), (65, 33, 33), (1000, 33, 33), (1000, 33, 256), (777, 33, 512), (500, 33, 19),
     (300, 7, 5), (301, 15, 16), (250, 30, 30), (4099, 33, 64), (130, 1, 1), (513, 32, 36),
     # tcgen05 kernel shapes (H = 128 / 256): exact tile, one row past a tile, D < 33
-    (64, 33, 128), (65, 33, 256), (129, 33, 128), (1000, 33, 128), (3001, 7, 256), (2000, 16, 128),
+    (2, 33, 256), (63, 33, 128), (64, 33, 128), (65, 33, 256), (129, 33, 128), (1000, 33, 128), (3001, 7, 256),
+    (2000, 16, 128),
 ])
 def test_batch_vs_oracle(gpu, N, D, H):
     x, l, t, net0 = _case(N, D, H, seed=N % 97)
