@@ -313,11 +313,15 @@ def run_gpu(args):
         roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": achieved / tf32_peak,
                     "kernel": "batchtc_kernel<2> (tcgen05 kind::tf32, 3xTF32, deltas in TMEM)",
+                    "fp32_accurate_peak": tf32_peak / 3,
+                    "frac_of_fp32_accurate_peak": achieved / (tf32_peak / 3),
                     "executed_mma_flops_per_launch": mma_flops,
                     "executed_mma_frac": mma_flops / (k_ms * 1e-3) / 1e12 / tf32_peak,
                     "mufu_frac": 2 * ROWS_PER_GPU * H / (k_ms * 1e-3) / mufu_peak,
                     "peak_source": "dense TF32 = half of MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, "
-                                   "back to back); executed_mma_frac counts the 3xTF32 MMA work incl. K/N padding; "
+                                   "back to back); fp32_accurate_peak = TF32 / 3 (3xTF32 spends three TF32 MMAs "
+                                   "per fp32-accurate product); executed_mma_frac counts the 3xTF32 MMA work incl. "
+                                   "K/N padding; "
                                    "mufu_frac = 2 MUFU ops per hidden activation / (148 SMs x 16/clk x SM clock)",
                     **common}
     else:
