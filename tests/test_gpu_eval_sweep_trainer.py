@@ -187,6 +187,28 @@ def test_fused_checkpoint_equals_segment_plus_eval(gpu, mode):
         assert r.train_loss == pytest.approx(l_tr, rel=1e-12) and r.test_loss == pytest.approx(l_te, rel=1e-12)
 
 
+def test_fused_checkpoint_batch_on_the_tcgen05_kernel(gpu):
+    """33 -> 256 -> 1 (the tcgen05 epoch kernel): fused checkpoint segments of 1, 9 and
+    90 epochs give the same bytes as the unfused segment loop, and both track the
+    oracle batch restatement."""
+    import paper_1908_07847_b200._lib as L
+    from paper_1908_07847_b200.backend import run_train_segment_eval
+
+    c = load_case("paper_33_33_1")
+    x, y, vx, vy = c["train_x"], c["train_y"], c["test_x"], c["test_y"]
+    assert L.load().glx_batch_kernel_kind(x.shape[0], 33, 256) == 2
+    t = y.astype(np.float32)
+    cfg = g.NetworkConfig(input_dim=33, hidden_dim=256, seed=11)
+    a, b, ref = g.init_weights(cfg), g.init_weights(cfg), g.init_weights(cfg)
+    for n in (1, 9, 90):
+        r = run_train_segment_eval(a.w_ih2d, a.w_ho2d, x, t, y, vx, vy, n, 0.5, g.cuda(), mode="batch")
+        g.run_train_segment_batch(b.w_ih2d, b.w_ho2d, x, t, n, 0.5, g.cuda())
+        assert a.w_ih.tobytes() == b.w_ih.tobytes() and a.w_ho.tobytes() == b.w_ho.tobytes()
+        assert r.finite and r.train_counts == g.eval_counts(b.w_ih2d, b.w_ho2d, x, y)
+    O.train_batch(ref.w_ih2d, ref.w_ho2d, x, t, 100, 0.5, x.shape[0])
+    assert max(rel_err(a.w_ih, ref.w_ih), rel_err(a.w_ho, ref.w_ho)) <= 1e-5
+
+
 def test_fused_checkpoint_flags_nonfinite(gpu):
     from paper_1908_07847_b200.backend import run_train_segment_eval
 
