@@ -441,22 +441,24 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
 // 8 lanes per parameter: lane l sums CTA partials l, l+8, ... in f64, the 8
 // lane sums combine through a fixed xor tree -> deterministic for a fixed grid.
 // f64 sum of one record slot over the per-CTA partial records: a block is
-// 8 warps x 32 consecutive slots (coalesced 128-byte rows), warp l takes records
-// l, l+8, ...; the 8 sums are added in a fixed order (deterministic)
+// kRedW warps x 32 consecutive slots (coalesced 128-byte rows), warp l takes
+// records l, l+kRedW, ... (about ten independent loads per thread for 148
+// records); the kRedW sums are added in a fixed order (deterministic)
+constexpr int kRedW = 16;
 __device__ __forceinline__ double reduce_partials(const float* __restrict__ part, int nparts, int PS, int idx,
                                                   int nidx, double* red) {
     const int l = threadIdx.x >> 5, i = threadIdx.x & 31;
     double s = 0.0;
     if (idx < nidx) {
-#pragma unroll 4
-        for (int c = l; c < nparts; c += 8) s += (double)part[(int64_t)c * PS + idx];
+#pragma unroll 10
+        for (int c = l; c < nparts; c += kRedW) s += (double)part[(int64_t)c * PS + idx];
     }
     red[l * 32 + i] = s;
     __syncthreads();
     if (l != 0) return 0.0;
     double t = red[i];
 #pragma unroll
-    for (int k = 1; k < 8; k++) t += red[k * 32 + i];
+    for (int k = 1; k < kRedW; k++) t += red[k * 32 + i];
     return t;
 }
 
@@ -464,7 +466,7 @@ __global__ void batch_update_kernel(const float* __restrict__ part, int nparts, 
                                     float* __restrict__ W1, float* __restrict__ W2, const float* __restrict__ Wk_cur,
                                     float* __restrict__ Wk_next, double lr_over_n, int train,
                                     double* __restrict__ stats, int* __restrict__ nonfinite) {
-    __shared__ double red[256];
+    __shared__ double red[kRedW * 32];
     const int P1 = H * (D + 1);
     const int nidx = P1 + H + 1 + 5;
     const int idx = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -537,7 +539,7 @@ __global__ void pack_rows_kernel(const float* __restrict__ X, const float* __res
 // w2_j factor folded into the dW1 rows so that apply is a plain axpy.
 __global__ void batch_grad_kernel(const float* __restrict__ part, int nparts, int PS, int D, int H, int DP,
                                   const float* __restrict__ Wk, double* __restrict__ grad) {
-    __shared__ double red[256];
+    __shared__ double red[kRedW * 32];
     const int P1 = H * (D + 1);
     const int nidx = P1 + H + 1 + 5;
     const int idx = blockIdx.x * 32 + (threadIdx.x & 31);
@@ -563,7 +565,7 @@ __global__ void batch_apply_kernel(int D, int H, float* __restrict__ W1, float* 
 
 cudaError_t launch_batch_grad(const BatchGeom& g, const float* part, const float* Wk, double* grad, cudaStream_t st) {
     const int nidx = g.P1 + g.H + 1 + 5;
-    batch_grad_kernel<<<(nidx + 31) / 32, 256, 0, st>>>(part, g.grid, g.PS, g.D, g.H, g.DP, Wk, grad);
+    batch_grad_kernel<<<(nidx + 31) / 32, kRedW * 32, 0, st>>>(part, g.grid, g.PS, g.D, g.H, g.DP, Wk, grad);
     return cudaGetLastError();
 }
 
@@ -697,7 +699,7 @@ cudaError_t launch_batch_update(const BatchGeom& g, const float* part, float* W1
                                 cudaStream_t st) {
     const int nidx = g.P1 + g.H + 1 + 5;
     const int blocks = (nidx + 31) / 32;
-    batch_update_kernel<<<blocks, 256, 0, st>>>(part, g.grid, g.PS, g.D, g.H, g.DP, W1, W2, Wk_cur, Wk_next,
+    batch_update_kernel<<<blocks, kRedW * 32, 0, st>>>(part, g.grid, g.PS, g.D, g.H, g.DP, W1, W2, Wk_cur, Wk_next,
                                                 lr_over_n, train ? 1 : 0, stats, nonfinite);
     return cudaGetLastError();
 }
