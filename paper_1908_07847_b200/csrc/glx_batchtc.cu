@@ -61,7 +61,7 @@ constexpr int kEpiBar = 1;
 // ~10^5 rows per CTA drifted by ~1e-3 relative at 64Mi rows; short partials keep
 // the sum at the fp32 CUDA-core kernel's accuracy (tests/test_gpu_fullsize.py)
 #ifndef GLX_BTC_DRAIN
-#define GLX_BTC_DRAIN 4
+#define GLX_BTC_DRAIN 8
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
 constexpr int kD1 = 34;
@@ -223,7 +223,10 @@ __device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v)
 // in fp32 Horner, on par with ex2.approx), exponent inserted with an integer add;
 // |x| clamped to 125 (1 + 2^-125 == 1 and 1 / (1 + 2^125) ~ 0 in fp32 either way)
 #ifndef GLX_BTC_POLY
-#define GLX_BTC_POLY 1  // element pairs per 4 that take the polynomial (0: all MUFU)
+#define GLX_BTC_POLY 3  // element pairs per GLX_BTC_POLY_DEN that take the polynomial (0: all MUFU)
+#endif
+#ifndef GLX_BTC_POLY_DEN
+#define GLX_BTC_POLY_DEN 8
 #endif
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
     x.x = fminf(fmaxf(x.x, -125.f), 125.f);
@@ -537,7 +540,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 h[i] = h[i] * 0.01f + 0.5f;
                 h[i + 1] = h[i + 1] * 0.01f + 0.5f;
 #else
-                const float2 e2 = ((i >> 1) % 4 < GLX_BTC_POLY) ? exp2_poly2(make_float2(h[i], h[i + 1]))
+                const float2 e2 = ((i >> 1) % GLX_BTC_POLY_DEN < GLX_BTC_POLY) ? exp2_poly2(make_float2(h[i], h[i + 1]))
                                                                  : make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
                 const float2 den = __fadd2_rn(e2, bcast2(1.0f));
                 h[i] = rcp_approx(den.x);
