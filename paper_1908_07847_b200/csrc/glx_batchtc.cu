@@ -626,8 +626,9 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
                     rh[i] = tf32_hi(s2.x);
                     rh[i + 1] = tf32_hi(s2.y);
-                    rl[i] = __float_as_uint(s2.x - __uint_as_float(rh[i]));
-                    rl[i + 1] = __float_as_uint(s2.y - __uint_as_float(rh[i + 1]));
+                    const float2 lo2 = __fadd2_rn(s2, make_float2(-__uint_as_float(rh[i]), -__uint_as_float(rh[i + 1])));
+                    rl[i] = __float_as_uint(lo2.x);
+                    rl[i + 1] = __float_as_uint(lo2.y);
                 }
                 st16(zcol + 16 * c, rh);
                 st16(locol + 16 * c, rl);
