@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 opart[(int)(lt & 1) * NEW * 32 + ew * 32 + lane] = p[0];
             }
             BTT(2);
-            bar_sync(kEpiBar, NEW * 32);
+            bar_sync(kEpiBar + rb, NEW * 16);  // the warps of this row block (they cover all units of its rows)
             BTT(3);
             {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);
                // every warp computes its own rows' delta_o, one warp per block keeps the statistics
@@ -649,7 +649,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             for (int k = 0; k < kDH; k++)
                 if (kDH * rb + k <= D) o1[k] = acc1[k];
         }
-        bar_sync(kEpiBar, NEW * 32);  // opart is free: exchange the dW2 partials of the two row blocks
+        bar_sync(kEpiBar + 2, NEW * 32);  // opart is free: exchange the dW2 partials of the two row blocks
         if (rb == 1) opart[j] = acc2.x + acc2.y;
         float* stat = opart + 2 * NEW * 32 - kR * 6;  // behind the dW2 exchange slots (H <= 256 floats)
         if (hf == 0 && quad == 0) {  // the statistics warps: rows 32 rb + lane
@@ -661,7 +661,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             stat[r * 6 + 4] = c3;
             stat[r * 6 + 5] = dsum;
         }
-        bar_sync(kEpiBar, NEW * 32);
+        bar_sync(kEpiBar + 2, NEW * 32);
         if (rb == 0) out[a.P1 + j] = (acc2.x + acc2.y) + opart[j];
         if (et < 6) {
             float s = 0.f;
