@@ -22,13 +22,17 @@
 // accumulator: the dropped lo.lo term is 2^-22 relative, so results track the
 // fp32 CUDA-core kernel (tests/test_gpu_batch.py, 1e-5 against the f64 oracle).
 //
-// Per 64-row tile the epilogue warps (thread = hidden unit) read Z^T from
-// TMEM, apply the MUFU sigmoid, reduce the output partial w2s_j h_j over the
-// units with a warp reduce-scatter plus one shared-memory pass, compute
-// delta_o per row, and write dh = delta_o h (1 - h) back to TMEM as hi/lo for
-// the backward MMA. Z^T is double-buffered so the forward MMA of tile t+1
-// overlaps the epilogue of tile t, and the backward of tile t overlaps the
-// epilogue of tile t+1.
+// Per 64-row tile, 16 epilogue warps (4 TMEM lane quadrants x 2 unit halves x
+// 2 row blocks; thread = hidden unit, 32 rows) read Z^T from TMEM, apply the
+// sigmoid (MUFU, with 3 of 8 exponential pairs on the FMA pipe), reduce the
+// output partials w2s_j h_j with a warp reduce-scatter plus one shared-memory
+// pass per row block, compute delta_o for their own rows, and write
+// dh = delta_o h (1 - h) back to TMEM as tf32 hi/lo for the backward MMA. Z^T is
+// double-buffered so the forward MMA of tile t+1 overlaps the epilogue of tile
+// t, and the backward of tile t overlaps the epilogue of tile t+1. Warp 0 bulk-
+// copies the packed rows, warps 2-3 convert them into the two operand layouts,
+// warp 1 issues the MMAs (converged, one elect.sync lane). DESIGN.md §4 has the
+// measured path and the per-phase timeline.
 #include "glx_common.cuh"
 #include "glx_kernels.h"
 
@@ -64,10 +68,10 @@ constexpr int kEpiBar = 1;
 #define GLX_BTC_DRAIN 8
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
-constexpr int kD1 = 34;
+constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
 #ifndef GLX_BTC_EXP
 #define GLX_BTC_EXP 0  // diagnostic builds only: 1 no MUFU sigmoid, 2 no backward MMAs, 3 no forward MMAs
-#endif  // dW1 columns kept per unit (D + 1 <= 34)
+#endif
 
 #ifdef GLX_BTC_TIMING
 __device__ unsigned long long g_btc_dbg[4096];
