@@ -54,6 +54,36 @@ def test_tcgen05_kernel_selected_for_headline_shapes(gpu):
     assert lib.glx_batch_kernel_kind(1000, 40, 256) == -1
 
 
+def test_tcgen05_kernel_matches_fp32_kernel(gpu, tmp_path):
+    """The same 100k-row, 33-256-1 problem through the tcgen05 3xTF32 kernel (this
+    process) and the FP32 three-role kernel (a subprocess with GLX_BATCH_KERNEL=3):
+    weights agree within the parity tolerance and the epoch statistics' counts match."""
+    import os
+    import subprocess
+    import sys
+
+    x, l, t, net0 = _case(100_003, 33, 256, seed=6)
+    np.savez(tmp_path / "case.npz", x=x, t=t, w1=net0.w_ih2d, w2=net0.w_ho2d)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]); import paper_1908_07847_b200 as g\n"
+        "d = np.load(sys.argv[2]); w1, w2 = d['w1'].copy(), d['w2'].copy(); st = np.zeros((5, 5))\n"
+        "g.run_train_segment_batch(w1, w2, d['x'], d['t'], 5, 0.5, g.cuda(), st)\n"
+        "np.savez(sys.argv[3], w1=w1, w2=w2, st=st)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, GLX_BATCH_KERNEL="3")
+    subprocess.run([sys.executable, "-c", code, root, str(tmp_path / "case.npz"), str(tmp_path / "fp32.npz")],
+                   check=True, env=env, timeout=600)
+    other = np.load(tmp_path / "fp32.npz")
+    net = net0.copy()
+    st = np.zeros((5, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 5, 0.5, g.cuda(), st)
+    assert rel_err(net.w_ih2d, other["w1"]) <= 1e-5 and rel_err(net.w_ho2d, other["w2"]) <= 1e-5
+    assert (st[:, 1:].sum(axis=1) == x.shape[0]).all()
+    assert np.abs(st[:, 1:] - other["st"][:, 1:]).sum(axis=1).max() <= 4  # |o - 0.5| ~ 0 rows may flip
+    assert np.allclose(st[:, 0], other["st"][:, 0], rtol=1e-5)
+
+
 def test_batch_is_deterministic(gpu):
     x, l, t, net0 = _case(100_003, 33, 256, seed=4)
     a, b = net0.copy(), net0.copy()
