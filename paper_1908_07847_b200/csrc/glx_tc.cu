@@ -58,6 +58,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
            ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
+// MN-major operand (M contiguous): 128-byte swizzled rows of 64 M-elements, one
+// row per K index; LBO = byte stride between 64-element M atoms, SBO = 1024
+// (8 K rows) -- the A operand of dW2 read straight from row-major H
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr, uint32_t lbo) {
+    return (uint64_t)((smem_addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 // instruction descriptor: BF16 x BF16 -> F32, both K-major, M x N
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
@@ -227,6 +235,7 @@ struct TcGemm {
     int64_t lda, ldb;
     int splits;         // split-K: blockIdx.z takes K / splits
     int a_blk, b_blk;   // 0: row-major; R > 0: K-blocked [K/64][R][64] (lda/ldb unused)
+    int a_mn = 0;       // 1: A stored [K][M] (M contiguous, row stride lda): MN-major operand
 };
 
 // lane = row, pk[e] = columns 2e, 2e+1 of that row; stored transposed
@@ -421,7 +430,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
                     unsigned char* st = sm + s * kStage;
                     mbar_arrive_expect_tx(&full[s], kStage);
-                    if (flags & 1) tma_load_3d(st, &map_a, 0, m0, kb0 + kb, &full[s]);
+                    if (flags & 8) {  // MN-major A: two 64 (M) x 64 (K) swizzled atoms
+                        tma_load_2d(st, &map_a, m0, (kb0 + kb) * kTcBK, &full[s]);
+                        tma_load_2d(st + kABytes / 2, &map_a, m0 + 64, (kb0 + kb) * kTcBK, &full[s]);
+                    } else if (flags & 1) tma_load_3d(st, &map_a, 0, m0, kb0 + kb, &full[s]);
                     else tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
                     if (flags & 2) tma_load_3d(st + kABytes, &map_b, 0, n0, kb0 + kb, &full[s]);
                     else tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
@@ -430,7 +442,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            constexpr uint32_t idesc = umma_idesc_bf16(kTcBM, BN);
+            const bool a_mn = (flags & 8) != 0;
+            const uint32_t idesc = umma_idesc_bf16(kTcBM, BN) | (a_mn ? (1u << 15) : 0u);
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
                 int z, m0, n0, kb0, nk;
@@ -447,8 +460,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     const uint32_t b_addr = a_addr + kABytes;
 #pragma unroll
                     for (int kk = 0; kk < kTcBK / 16; kk++)
-                        umma_bf16(dcol, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
-                                  (kb | kk) != 0);
+                        umma_bf16(dcol,
+                                  a_mn ? umma_desc_sw128_mn(a_addr + kk * 16 * 128, kABytes / 2)
+                                       : umma_desc_sw128(a_addr + kk * 32),
+                                  umma_desc_sw128(b_addr + kk * 32), idesc, (kb | kk) != 0);
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
@@ -567,8 +582,9 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
     memset(&md, 0, sizeof(md));
     memset(&mt, 0, sizeof(mt));
     const int64_t nkb = g.K / kTcBK;
-    const bool oka = g.a_blk ? make_map_blk(&ma, g.A, g.a_blk, nkb, kTcBM, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
-                             : make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM);
+    const bool oka = g.a_mn    ? make_map_bf16(&ma, g.A, g.K, g.lda, g.lda, kTcBK, 64, CU_TENSOR_MAP_SWIZZLE_128B)
+                     : g.a_blk ? make_map_blk(&ma, g.A, g.a_blk, nkb, kTcBM, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
+                               : make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM);
     const bool okb = g.b_blk ? make_map_blk(&mb, g.B, g.b_blk, nkb, BN, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
                              : make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN);
     if (!oka || !okb) return cudaErrorInvalidValue;
@@ -581,7 +597,7 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
                                  : make_map_bf16(&mt, tdst, g.N, g.M, ep.ldt, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
         if (!ok) return cudaErrorInvalidValue;
     }
-    const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0);
+    const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0) | (g.a_mn ? 8 : 0);
     const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 256 + kTcStgBytes;
     auto k = tc_gemm_kernel<BN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -712,11 +728,6 @@ __global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __
 }
 
 // row `row` of a K-blocked [n/64][R][64] bf16 matrix = 1.0 (the bias row of H^T)
-__global__ void fill_ones_row_kernel(__nv_bfloat16* __restrict__ M, int R, int row, int64_t n) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) M[kblk_index(i, row, R)] = __float2bfloat16_rn(1.f);
-}
-
 // grad (f64, reference layout: dW1 [1024][1025] then dW2 [16][1025]) = the
 // split-K partial sums reduced in fixed slab order (dW1^T: [split][1152][1024],
 // dW2^T: [split][1152][32], row 1024 = bias)
@@ -763,6 +774,16 @@ cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint
 }
 
 constexpr int kWSplits2 = 16;  // split-K of the dW2 GEMM (9 M tiles x 16 = 144 CTAs)
+constexpr int kWHL = 1088;     // row stride of H: 1024 units, the bias column, zero padding to 64
+
+// H columns 1024.. of every row: 1 (the bias input of dW2), then zeros
+__global__ void h_bias_cols_kernel(__nv_bfloat16* __restrict__ H, int64_t C) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= C * (kWHL - kWH)) return;
+    const int64_t r = i / (kWHL - kWH);
+    const int c = (int)(i - r * (kWHL - kWH));
+    H[r * kWHL + kWH + c] = __float2bfloat16_rn(c == 0 ? 1.f : 0.f);
+}
 
 struct WideWork {
     void* W1b;
@@ -770,8 +791,7 @@ struct WideWork {
     void* W2b;
     float* b2;
     void* W2T;
-    void* Hb;   // [C][1024] bf16
-    void* HT;   // [H,1]^T, K-blocked [C/64][1025][64] bf16, row 1024 = 1 (bias input of dW2)
+    void* Hb;   // [C][kWHL] bf16: h in columns 0..1023, column 1024 = 1 (bias input of dW2), 1025.. = 0
     void* dob;  // [C][64] bf16
     void* doT;  // delta_o^T, K-blocked [C/64][32][64] bf16, rows >= 16 zero
     void* dht;  // dH^T, K-blocked [C/64][1024][64] bf16
@@ -795,8 +815,7 @@ static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
     t.W2b = take(32 * kWH * 2);
     t.b2 = (float*)take(64);
     t.W2T = take((size_t)kWH * 64 * 2);
-    t.Hb = take((size_t)C * kWH * 2);
-    t.HT = take((size_t)(kWH + 1) * C * 2);
+    t.Hb = take((size_t)C * kWHL * 2);
     t.dob = take((size_t)C * 64 * 2);
     t.doT = take((size_t)32 * C * 2);
     t.dht = take((size_t)kWH * C * 2);
@@ -833,7 +852,7 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
     if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)kWSplits2 * zstride2 * 4, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 64 * 2, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.doT, 0, (size_t)32 * C * 2, st)) != cudaSuccess) return e;
-    fill_ones_row_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.HT, kWH + 1, kWH, C);
+    h_bias_cols_kernel<<<(unsigned)((C * (kWHL - kWH) + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.Hb, C);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     for (int64_t r0 = 0; r0 < N; r0 += C) {
         const int Cc = (int)std::min<int64_t>(C, N - r0);
@@ -844,14 +863,12 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             TcEpilogue ep{};
             ep.kind = 1;
             ep.d_bf16 = (__nv_bfloat16*)w.Hb;
-            ep.d_t = (__nv_bfloat16*)w.HT;
-            ep.t_blk = kWH + 1;
             ep.bias = w.b1;
-            ep.ldd = kWH;
+            ep.ldd = kWHL;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
         {  // 2. output layer -> delta_o, loss, accuracy
-            TcGemm g{w.Hb, w.W2b, Cc, 32, kWH, kWH, kWH, 1};
+            TcGemm g{w.Hb, w.W2b, Cc, 32, kWH, kWHL, kWH, 1};
             TcEpilogue ep{};
             ep.kind = 2;
             ep.bias = w.b2;
@@ -867,7 +884,7 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             TcEpilogue ep{};
             ep.kind = 3;
             ep.h = (const __nv_bfloat16*)w.Hb;
-            ep.ldh = kWH;
+            ep.ldh = kWHL;
             ep.dht = (__nv_bfloat16*)w.dht;
             ep.t_blk = kWH;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
@@ -882,8 +899,9 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             ep.zstride = zstride;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32 with delta_o^T rows >= 16 zero)
-            TcGemm g{w.HT, w.doT, kWH + 1, 32, Cc, 0, 0, kWSplits2, kWH + 1, 32};
+        {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32 with delta_o^T rows >= 16 zero); A = H read
+           //    MN-major (rows = K), the bias column supplies the "1" input
+            TcGemm g{w.Hb, w.doT, kWH + 1, 32, Cc, kWHL, 0, kWSplits2, 0, 32, 1};
             TcEpilogue ep{};
             ep.kind = 4;
             ep.d_f32 = w.dW2T;
