@@ -236,6 +236,7 @@ struct TcGemm {
     int splits;         // split-K: blockIdx.z takes K / splits
     int a_blk, b_blk;   // 0: row-major; R > 0: K-blocked [K/64][R][64] (lda/ldb unused)
     int a_mn = 0;       // 1: A stored [K][M] (M contiguous, row stride lda): MN-major operand
+    int b_mn = 0;       // 1: B stored [K][N] (N contiguous, row stride ldb): MN-major operand
 };
 
 // lane = row, pk[e] = columns 2e, 2e+1 of that row; stored transposed
@@ -350,7 +351,8 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
                 pall[q4 * 4 + e] = *reinterpret_cast<const uint32_t*>(&d2);
             }
         }
-        store_cols_bf16(sg, pall, row - lane, n0 + c, lane);
+        if (ep.d_bf16) store_rows_cols_bf16(sg, pall, row - lane, n0 + c, lane, false);  // row-major dH
+        else store_cols_bf16(sg, pall, row - lane, n0 + c, lane);                         // transposed dH^T
     }
 }
 
@@ -435,15 +437,19 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         tma_load_2d(st + kABytes / 2, &map_a, m0 + 64, (kb0 + kb) * kTcBK, &full[s]);
                     } else if (flags & 1) tma_load_3d(st, &map_a, 0, m0, kb0 + kb, &full[s]);
                     else tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
-                    if (flags & 2) tma_load_3d(st + kABytes, &map_b, 0, n0, kb0 + kb, &full[s]);
+                    if (flags & 16) {  // MN-major B: BN / 64 atoms of 64 (N) x 64 (K)
+#pragma unroll
+                        for (int i = 0; i < BN / 64; i++)
+                            tma_load_2d(st + kABytes + i * 8192, &map_b, n0 + 64 * i, (kb0 + kb) * kTcBK, &full[s]);
+                    } else if (flags & 2) tma_load_3d(st + kABytes, &map_b, 0, n0, kb0 + kb, &full[s]);
                     else tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            const bool a_mn = (flags & 8) != 0;
-            const uint32_t idesc = umma_idesc_bf16(kTcBM, BN) | (a_mn ? (1u << 15) : 0u);
+            const bool a_mn = (flags & 8) != 0, b_mn = (flags & 16) != 0;
+            const uint32_t idesc = umma_idesc_bf16(kTcBM, BN) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
                 int z, m0, n0, kb0, nk;
@@ -463,7 +469,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         umma_bf16(dcol,
                                   a_mn ? umma_desc_sw128_mn(a_addr + kk * 16 * 128, kABytes / 2)
                                        : umma_desc_sw128(a_addr + kk * 32),
-                                  umma_desc_sw128(b_addr + kk * 32), idesc, (kb | kk) != 0);
+                                  b_mn ? umma_desc_sw128_mn(b_addr + kk * 16 * 128, 8192)
+                                       : umma_desc_sw128(b_addr + kk * 32),
+                                  idesc, (kb | kk) != 0);
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
@@ -585,10 +593,13 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
     const bool oka = g.a_mn    ? make_map_bf16(&ma, g.A, g.K, g.lda, g.lda, kTcBK, 64, CU_TENSOR_MAP_SWIZZLE_128B)
                      : g.a_blk ? make_map_blk(&ma, g.A, g.a_blk, nkb, kTcBM, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
                                : make_map_bf16(&ma, g.A, g.M, g.K, g.lda, kTcBM);
-    const bool okb = g.b_blk ? make_map_blk(&mb, g.B, g.b_blk, nkb, BN, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
-                             : make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN);
+    const bool okb = g.b_mn    ? (BN % 64 == 0 && make_map_bf16(&mb, g.B, g.K, g.ldb, g.ldb, kTcBK, 64,
+                                                               CU_TENSOR_MAP_SWIZZLE_128B))
+                     : g.b_blk ? make_map_blk(&mb, g.B, g.b_blk, nkb, BN, kTcBK, CU_TENSOR_MAP_SWIZZLE_128B)
+                               : make_map_bf16(&mb, g.B, g.N, g.K, g.ldb, BN);
     if (!oka || !okb) return cudaErrorInvalidValue;
-    if (ep.kind == 1 && !make_map_bf16(&md, ep.d_bf16, g.M, g.N, ep.ldd, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
+    if ((ep.kind == 1 || (ep.kind == 3 && ep.d_bf16)) &&
+        !make_map_bf16(&md, ep.d_bf16, g.M, g.N, ep.ldd, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE))
         return cudaErrorInvalidValue;
     __nv_bfloat16* tdst = ep.kind == 1 ? ep.d_t : ep.kind == 3 ? ep.dht : nullptr;
     if (tdst) {
@@ -597,7 +608,7 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
                                  : make_map_bf16(&mt, tdst, g.N, g.M, ep.ldt, 32, 32, CU_TENSOR_MAP_SWIZZLE_NONE);
         if (!ok) return cudaErrorInvalidValue;
     }
-    const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0) | (g.a_mn ? 8 : 0);
+    const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0) | (g.a_mn ? 8 : 0) | (g.b_mn ? 16 : 0);
     const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 256 + kTcStgBytes;
     auto k = tc_gemm_kernel<BN>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -794,7 +805,7 @@ struct WideWork {
     void* Hb;   // [C][kWHL] bf16: h in columns 0..1023, column 1024 = 1 (bias input of dW2), 1025.. = 0
     void* dob;  // [C][64] bf16
     void* doT;  // delta_o^T, K-blocked [C/64][32][64] bf16, rows >= 16 zero
-    void* dht;  // dH^T, K-blocked [C/64][1024][64] bf16
+    void* dht;  // dH, row-major [C][1024] bf16 (read MN-major by the dW1 GEMM)
     float* dW1T;
     float* dW2T;
     double* grad;  // [kWP + 3]: gradient sums, then loss, correct, wrong
@@ -885,13 +896,13 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             ep.kind = 3;
             ep.h = (const __nv_bfloat16*)w.Hb;
             ep.ldh = kWHL;
-            ep.dht = (__nv_bfloat16*)w.dht;
-            ep.t_blk = kWH;
+            ep.d_bf16 = (__nv_bfloat16*)w.dht;  // dH row-major [C][1024]
+            ep.ldd = kWH;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
         {  // 4. dW1^T += [X,1]^T dH (split-K over the chunk's rows)
             const __nv_bfloat16* XTc = reinterpret_cast<const __nv_bfloat16*>(XT) + r0 * (kWD + 1);
-            TcGemm g{XTc, w.dht, kWD + 1, kWH, Cc, 0, 0, splits, kWD + 1, kWH};
+            TcGemm g{XTc, w.dht, kWD + 1, kWH, Cc, 0, kWH, splits, kWD + 1, 0, 0, 1};  // B = dH read MN-major
             TcEpilogue ep{};
             ep.kind = 4;
             ep.d_f32 = w.dW1T;
