@@ -289,6 +289,69 @@ int orc_train_batch_par(float *w_ih, float *w_ho, const float *feats, const floa
     return 0;
 }
 
+/* One epoch's gradient SUM at fixed weights (the quantity glx_batch_grad
+ * returns): grad = [sum_r dh_r (x) [x_r, 1] (H(D+1)) | sum_r d_o,r (x) [h_r, 1]
+ * (K(H+1)) | loss | tp tn fp fn], deltas as in orc_train_batch with lr/B = 1
+ * (kernels.py:125-129 op order), rows split over nw OpenMP threads, f64
+ * partials combined in thread order. K == 1 counts as in orc_eval. */
+int orc_batch_grad_par(const float *w_ih, const float *w_ho, const float *feats, const float *T,
+                       int64_t rows, int D, int H, int K, double *grad, int nw) {
+    if (nw < 1) nw = 1;
+    const int64_t P1 = (int64_t)H * (D + 1), P2 = (int64_t)K * (H + 1), P = P1 + P2 + 5;
+    double *acc = (double *)calloc((size_t)nw * (size_t)P, sizeof(double));
+    if (!acc) return -1;
+#ifdef _OPENMP
+#pragma omp parallel num_threads(nw)
+#endif
+    {
+#ifdef _OPENMP
+        int w = omp_get_thread_num();
+        int nwr = omp_get_num_threads();
+#else
+        int w = 0, nwr = 1;
+#endif
+        float *h = (float *)malloc(sizeof(float) * (size_t)H);
+        float *o = (float *)malloc(sizeof(float) * (size_t)K);
+        double *d_o = (double *)malloc(sizeof(double) * (size_t)K);
+        double *g1 = acc + (int64_t)w * P, *g2 = g1 + P1, *st = g2 + P2;
+        int64_t r0 = rows * w / nwr, r1 = rows * (w + 1) / nwr;
+        for (int64_t r = r0; r < r1; r++) {
+            const float *x = feats + r * D;
+            orc_forward_row(w_ih, w_ho, x, D, H, K, h, o);
+            for (int k = 0; k < K; k++) {
+                d_o[k] = delta_from_error((double)o[k] - (double)T[r * K + k], o[k]);
+                double e = (double)T[r * K + k] - (double)o[k];
+                st[0] += 0.5 * e * e;
+            }
+            if (K == 1) {
+                int pred = o[0] >= 0.5f, pos = T[r] >= 0.5f;
+                st[pred && pos ? 1 : !pred && !pos ? 2 : pred ? 3 : 4] += 1.0;
+            }
+            for (int j = 0; j < H; j++) {
+                double err = 0.0;
+                for (int k = 0; k < K; k++) err += (double)w_ho[(int64_t)k * (H + 1) + j] * d_o[k];
+                double s = delta_from_error(err, h[j]);
+                double *g = g1 + (int64_t)j * (D + 1);
+                for (int i = 0; i < D; i++) g[i] += s * (double)x[i];
+                g[D] += s;
+            }
+            for (int k = 0; k < K; k++) {
+                double *g = g2 + (int64_t)k * (H + 1);
+                for (int j = 0; j < H; j++) g[j] += d_o[k] * (double)h[j];
+                g[H] += d_o[k];
+            }
+        }
+        free(h); free(o); free(d_o);
+    }
+    for (int64_t p = 0; p < P; p++) {
+        double s = 0.0;
+        for (int w = 0; w < nw; w++) s += acc[(int64_t)w * P + p];
+        grad[p] = s;
+    }
+    free(acc);
+    return 0;
+}
+
 /* kernels.py:352-375 eval_counts, plus the K>1 and loss extensions.
  * K == 1: counts = (tp, tn, fp, fn), poor (label 1) positive, pred = o >= 0.5f.
  * K  > 1: counts = (correct, wrong, 0, 0), pred = argmax (lowest index on ties).

@@ -22,6 +22,7 @@ _lib = None
 _f32p = np.ctypeslib.ndpointer(dtype=np.float32, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
+_f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
 _i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 _i64 = ctypes.c_int64
 _int = ctypes.c_int
@@ -45,6 +46,7 @@ def lib():
     L.orc_train_online_par.argtypes = [_f32p, _f32p, _f32p, _f32p, _i64, _int, _int, _i64, _dbl, _int]
     L.orc_train_batch.argtypes = [_f32p, _f32p, _f32p, _f32p, _i64, _int, _int, _int, _i64, _i64, _dbl]
     L.orc_train_batch_par.argtypes = [_f32p, _f32p, _f32p, _f32p, _i64, _int, _int, _int, _i64, _dbl, _int]
+    L.orc_batch_grad_par.argtypes = [_f32p, _f32p, _f32p, _f32p, _i64, _int, _int, _int, _f64p, _int]
     L.orc_eval.argtypes = [_f32p, _f32p, _f32p, _u8p, _i64, _int, _int, _int, _i64p,
                            ctypes.POINTER(ctypes.c_double)]
     L.orc_eval.restype = None
@@ -55,7 +57,7 @@ def lib():
     L.orc_train_sweep.argtypes = [_i64, _i32p, _i64p, _f32p, _f32p, _f32p, _i64, _int, _i64, _dbl, _int]
     L.orc_max_threads.restype = _int
     for name in ("orc_train_online_seq", "orc_train_online_par", "orc_train_batch",
-                 "orc_train_batch_par", "orc_train_sweep"):
+                 "orc_train_batch_par", "orc_train_sweep", "orc_batch_grad_par"):
         getattr(L, name).restype = _int
     _lib = L
     return L
@@ -107,6 +109,18 @@ def train_batch_par(w_ih2d, w_ho2d, feats2d, T2d, epochs, lr, workers=None):
     nw = workers or (os.cpu_count() or 1)
     _check(lib().orc_train_batch_par(w_ih2d, w_ho2d, np.ascontiguousarray(feats2d), T,
                                      feats2d.shape[0], D, H, K, int(epochs), float(lr), int(nw)))
+
+
+def batch_grad_par(w_ih2d, w_ho2d, feats2d, T2d, workers=None):
+    """One epoch's f64 gradient SUM at fixed weights, laid out like glx_batch_grad:
+    [dW1 | dW2 | loss, tp, tn, fp, fn] (K == 1 counts; restatement of kernels.py:102-139)."""
+    D, H, K = _dims(w_ih2d, w_ho2d)
+    T = np.ascontiguousarray(np.asarray(T2d, dtype=np.float32).reshape(feats2d.shape[0], K))
+    nw = workers or (os.cpu_count() or 1)
+    out = np.zeros(H * (D + 1) + K * (H + 1) + 5, np.float64)
+    _check(lib().orc_batch_grad_par(np.ascontiguousarray(w_ih2d), np.ascontiguousarray(w_ho2d),
+                                    np.ascontiguousarray(feats2d), T, feats2d.shape[0], D, H, K, out, int(nw)))
+    return out
 
 
 def eval_counts(w_ih2d, w_ho2d, feats2d, labels):

@@ -12,18 +12,21 @@ Reference counterparts (/root/reference/pkg/src/glycemlp/):
 plus run_train_segment_batch (full-batch GD) and
 run_train_segment_eval (one trainer checkpoint in one device call, 8(f)1).
 
-The engine name is "cuda" (the reference rejects any other name than its two
-CPU engines, test_backend.py:24-25, so the device engine has its own name).
-numerics="ref64" reproduces the reference's float64 operation order (the
-result the reference's sequential and parallel engines both produce);
-numerics="fp32" runs packed-FP32 FMA with a MUFU sigmoid, within the
-1e-4 max(1,|w|)-relative tolerance of SURVEY.md 8(c). sequential() and
-parallel() return the "ref64" device engine so reference call sites keep
-their exact semantics; there is no CPU engine in this package.
+Engine names. The reference's two names are accepted with their meaning kept:
+"sequential" and "parallel" (with a worker count, validated as the reference
+does) both select the device engine in the reference's float64 operation
+order ("ref64"), which is the result the reference's two CPU engines both
+produce bit for bit; the worker count is recorded (effective_workers) but the
+device has no host thread pool to size. "cuda" is the device engine with a
+choice of numerics: "fp32" (default; packed-FP32 FMA, MUFU sigmoid, within
+the 1e-4 max(1,|w|)-relative tolerance of SURVEY.md 8(c)) or "ref64". Any
+other name raises ValidationError (test_backend.py:24-25). There is no CPU
+engine in this package.
 """
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -32,31 +35,41 @@ from . import _lib
 from .errors import ShapeError, ValidationError
 
 CUDA = "cuda"
+SEQUENTIAL = "sequential"
+PARALLEL = "parallel"
+ENGINES = (SEQUENTIAL, PARALLEL, CUDA)
 ONLINE = "online"
 BATCH = "batch"
 
 
+def hardware_parallelism() -> int:
+    """backend.py:34-35: the host's core count (the default parallel() worker count)."""
+    return os.cpu_count() or 1
+
+
 @dataclass(frozen=True)
 class BackendKind:
-    """Device engine selector.
+    """Engine selector (backend.py:44-62).
 
-    name      always "cuda"
-    workers   GPUs used by the sharded entry points (sweep, data parallel);
-              a single training segment runs on `device`
-    numerics  "fp32" (default) or "ref64"
+    name      "sequential" | "parallel" (reference-exact device engine) | "cuda"
+    workers   the reference's worker-pool size (>= 1); for "cuda", the GPUs used by
+              the sharded entry points (sweep, data parallel)
+    numerics  "fp32" or "ref64"; forced to "ref64" for the reference's two names
     device    CUDA device ordinal for the host-pointer entry points
     """
 
-    name: str = CUDA
+    name: str
     workers: int = 1
     numerics: str = "fp32"
     device: int = 0
 
     def __post_init__(self) -> None:
-        if self.name != CUDA:
-            raise ValidationError(f"backend must be {CUDA!r}, got {self.name!r}")
-        if self.workers < 1:
+        if self.name not in ENGINES:
+            raise ValidationError(f"backend must be {SEQUENTIAL}, {PARALLEL} or {CUDA}, got {self.name!r}")
+        if not isinstance(self.workers, (int, np.integer)) or self.workers < 1:
             raise ValidationError(f"worker_count must be >= 1, got {self.workers}")
+        if self.name != CUDA:
+            object.__setattr__(self, "numerics", "ref64")
         if self.numerics not in _lib.NUMERICS:
             raise ValidationError(f"numerics must be one of {tuple(_lib.NUMERICS)}, got {self.numerics!r}")
         if self.device < 0:
@@ -64,7 +77,8 @@ class BackendKind:
 
     @property
     def effective_workers(self) -> int:
-        return self.workers
+        """backend.py:57-62: 1 for sequential; the requested pool otherwise."""
+        return 1 if self.name == SEQUENTIAL else int(self.workers)
 
 
 def cuda(device: int = 0, numerics: str = "fp32", workers: int = 1) -> BackendKind:
@@ -72,13 +86,14 @@ def cuda(device: int = 0, numerics: str = "fp32", workers: int = 1) -> BackendKi
 
 
 def sequential() -> BackendKind:
-    """Reference-exact numerics on the device (replaces the CPU sequential engine)."""
-    return BackendKind(CUDA, 1, "ref64", 0)
+    """The reference's sequential engine: reference-exact (ref64) numerics on the device."""
+    return BackendKind(SEQUENTIAL, 1)
 
 
 def parallel(workers: int | None = None) -> BackendKind:
-    """Reference-exact numerics on the device (replaces the CPU neuron-parallel engine)."""
-    return BackendKind(CUDA, 1, "ref64", 0)
+    """The reference's neuron-parallel engine (bit-identical to sequential by contract,
+    SPEC.md:301): the same reference-exact device engine; `workers` validated and kept."""
+    return BackendKind(PARALLEL, hardware_parallelism() if workers is None else workers)
 
 
 def _f32c(a: np.ndarray) -> np.ndarray:

@@ -62,3 +62,8 @@ def rel_err(a, b):
     if a.size == 0:
         return 0.0
     return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+
+
+PKG_SRC = ROOT / "pkg" / "src"
+if str(PKG_SRC) not in sys.path:
+    sys.path.insert(0, str(PKG_SRC))

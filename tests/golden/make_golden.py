@@ -167,6 +167,114 @@ def normalize_cases():
     print("normalize_cases: ok", sorted({k.split("_")[0] for k in out}))
 
 
+def protocol_cases():
+    """The paper protocol's long runs (cli.py:34-36: 100k epochs, lr 0.1): the
+    reference's weights and confusion counts at 10k and 100k epochs for the
+    paper 33-33-1 split and the two 30-30-1 cohorts (train_segment_seq)."""
+    out = {}
+    for name, pair, hidden, seed in (("paper", matrix_split(120, 33, 7), 33, 7),
+                                     ("male", record_split(120, 7, "planted-linear", "male"), 30, 7),
+                                     ("female", record_split(120, 7, "random", "female"), 30, 7)):
+        cfg = g.NetworkConfig(input_dim=pair.train.columns, hidden_dim=hidden, seed=seed)
+        net = g.init_weights(cfg)
+        feats = pair.train.matrix()
+        targets = pair.train.labels.astype(np.float32)
+        out[f"{name}_train_x"] = np.ascontiguousarray(feats)
+        out[f"{name}_train_y"] = pair.train.labels.copy()
+        out[f"{name}_test_x"] = np.ascontiguousarray(pair.test.matrix())
+        out[f"{name}_test_y"] = pair.test.labels.copy()
+        out[f"{name}_meta"] = np.array([pair.train.columns, hidden, 1, seed], dtype=np.int64)
+        prev = 0
+        for cp in (10_000, 100_000):
+            B.run_train_segment(net.w_ih2d, net.w_ho2d, feats, targets, cp - prev, 0.1, g.sequential())
+            prev = cp
+            out[f"{name}_w_ih_{cp}"] = net.w_ih.copy()
+            out[f"{name}_w_ho_{cp}"] = net.w_ho.copy()
+            out[f"{name}_train_counts_{cp}"] = np.array(
+                Kr.eval_counts(net.w_ih2d, net.w_ho2d, feats, pair.train.labels), np.int64)
+            out[f"{name}_test_counts_{cp}"] = np.array(
+                Kr.eval_counts(net.w_ih2d, net.w_ho2d, pair.test.matrix(), pair.test.labels), np.int64)
+        print(f"protocol {name}: 100k epochs, counts {out[f'{name}_train_counts_100000']} "
+              f"{out[f'{name}_test_counts_100000']}")
+    np.savez_compressed(OUT / "protocol_100k.npz", **out)
+
+
+def acceptance_cases():
+    """Acceptance criteria 4 and 5 (test_acceptance.py:80-115): ten seeds each of a
+    planted-signal 61-row and a weak-signal 59-row record cohort (conftest.py:7-11
+    make_record_split), trained by the reference's trainer for 100k epochs; the
+    normalised splits, final weights, counts and accuracies per seed."""
+    for crit, rows, signal in ((4, 61, "planted-linear"), (5, 59, "random")):
+        out = {}
+        finals = []
+        for seed in range(10):
+            records = g.synth_dataset(rows, seed, signal)
+            pair = g.normalize_split(g.train_test_split(g.build_dataset(records, "synthetic"), 0.75, seed))
+            cfg = g.NetworkConfig(input_dim=pair.train.columns, seed=seed, learning_rate=0.1)
+            rep = g.train(TrainSpec(config=cfg, epochs=100_000, backend=g.sequential(), checkpoints=(100_000,)),
+                          pair)
+            row = rep.rows[-1]
+            out[f"s{seed}_train_x"] = np.ascontiguousarray(pair.train.matrix())
+            out[f"s{seed}_train_y"] = pair.train.labels.copy()
+            out[f"s{seed}_test_x"] = np.ascontiguousarray(pair.test.matrix())
+            out[f"s{seed}_test_y"] = pair.test.labels.copy()
+            out[f"s{seed}_w_ih"] = rep.network.w_ih.copy()
+            out[f"s{seed}_w_ho"] = rep.network.w_ho.copy()
+            out[f"s{seed}_acc"] = np.array([row.train_accuracy, row.test_accuracy])
+            out[f"s{seed}_train_counts"] = np.array([row.train_confusion[k] for k in ("tp", "tn", "fp", "fn")],
+                                                    np.int64)
+            out[f"s{seed}_test_counts"] = np.array([row.test_confusion[k] for k in ("tp", "tn", "fp", "fn")],
+                                                   np.int64)
+            finals.append((round(row.train_accuracy, 3), round(row.test_accuracy, 3)))
+        np.savez_compressed(OUT / f"acceptance_c{crit}.npz", **out)
+        print(f"criterion {crit}: {finals}")
+
+
+def dropin_cases():
+    """The reference trainer tests' splits and the reference's own results on them
+    (test_trainer.py:50-121, test_acceptance.py:48-67): normalised features, labels,
+    row ids and norm stats of each SplitPair, plus every checkpoint row and the final
+    weights of g.train(spec, pair) with the sequential engine."""
+    def spec_of(columns, epochs, checkpoints, seed):
+        return TrainSpec(config=g.NetworkConfig(input_dim=columns, seed=seed), epochs=epochs,
+                         backend=g.sequential(), checkpoints=checkpoints)
+
+    runs = {
+        "m30_6_2": (matrix_split(30, 6, 2), [(40, (1, 10, 40), 1)]),
+        "m24_5_4": (matrix_split(24, 5, 4), [(32, (1, 2, 4, 8, 16, 32), 2), (32, (32,), 2)]),
+        "r40_6": (record_split(40, 6, "planted-linear"), [(100, (1, 10, 100), 0)]),
+        "m20_4_0": (matrix_split(20, 4, 0), []),
+        "m20_4_1": (matrix_split(20, 4, 1), []),
+        "r30_1": (record_split(30, 1, "planted-linear"), [(5, (5,), 0)]),
+        "m26_5_9": (matrix_split(26, 5, 9), [(60, (60,), 3)]),
+        "m24_4_5": (matrix_split(24, 4, 5), [(30, (1, 10, 30), 1), (20, (1, 20), 2)]),
+        "r30_3": (record_split(30, 3, "planted-linear"), [(10, (10,), 0)]),
+        "m24_4_7": (matrix_split(24, 4, 7), [(15, (5, 15), 4)]),
+    }
+    out = {}
+    for name, (pair, specs) in runs.items():
+        for part in ("train", "test"):
+            d = getattr(pair, part)
+            out[f"{name}_{part}_x"] = np.ascontiguousarray(d.matrix())
+            out[f"{name}_{part}_y"] = d.labels.copy()
+            out[f"{name}_{part}_ids"] = np.array([str(r) for r in d.row_ids])
+            out[f"{name}_{part}_tag"] = np.array([d.subset_tag])
+        out[f"{name}_col_min"] = pair.train.norm_stats.col_min.copy()
+        out[f"{name}_col_max"] = pair.train.norm_stats.col_max.copy()
+        out[f"{name}_split"] = np.array([pair.seed, pair.fraction])
+        for k, (epochs, cps, seed) in enumerate(specs):
+            rep = g.train(spec_of(pair.train.columns, epochs, cps, seed), pair)
+            out[f"{name}_run{k}_spec"] = np.array([epochs, seed, *cps], np.int64)
+            out[f"{name}_run{k}_rows"] = np.array(
+                [[r.epoch, r.train_accuracy, r.test_accuracy,
+                  *[r.train_confusion[c] for c in ("tp", "tn", "fp", "fn")],
+                  *[r.test_confusion[c] for c in ("tp", "tn", "fp", "fn")]] for r in rep.rows], np.float64)
+            out[f"{name}_run{k}_w_ih"] = rep.network.w_ih.copy()
+            out[f"{name}_run{k}_w_ho"] = rep.network.w_ho.copy()
+    np.savez_compressed(OUT / "dropin_splits.npz", **out)
+    print("dropin_splits:", ", ".join(runs))
+
+
 CASES = {
     "online": lambda: (
         online_case("paper_33_33_1", matrix_split(120, 33, 7), 33, 7, [1, 10, 100, 1000]),
@@ -177,6 +285,9 @@ CASES = {
     "trainer": trainer_case,
     "generators": generator_digests,
     "normalize": normalize_cases,
+    "protocol": protocol_cases,
+    "acceptance": acceptance_cases,
+    "dropin": dropin_cases,
 }
 
 if __name__ == "__main__":

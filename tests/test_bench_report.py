@@ -112,7 +112,7 @@ class TestRunCPU:
 @pytest.mark.gpu
 def test_device_cells_and_device_speedups(gpu):
     rep = B.run_bench(tiny_spec(rows=90, columns=33, config=g.NetworkConfig(input_dim=33, hidden_dim=33, seed=7),
-                                epochs_grid=(10, 100), repetitions=2, backends=(g.cuda(), g.sequential()),
+                                epochs_grid=(10, 100), repetitions=2, backends=(g.cuda(), g.cuda(numerics="ref64")),
                                 baselines=(("sequential", seq_engine),), fp32_peak_tflops=72.5))
     names = {c.backend for c in rep.cells}
     assert names == {"sequential", "cuda-fp32", "cuda-ref64"}

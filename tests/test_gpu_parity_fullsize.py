@@ -1,0 +1,149 @@
+"""Full-batch parity at the benchmark sizes (north_star:
+"predicted classes and accuracy identical, weights within a stated relative
+tolerance after N epochs").
+
+* config 2 at its full size (1M rows x 33 -> 256 -> 1, the bench workload) for 20
+  epochs on the tcgen05 kernel against the f64 oracle restatement
+  (oracle.train_batch_par, the reference's kernels.py:102-139 op order);
+* 100k rows for 200 epochs;
+* config 4's full 64Mi rows: one epoch's gradient sum (glx_batch_grad: fp32
+  tensor-core partials drained every 512 rows, f64 across tiles and CTAs)
+  against the oracle's f64 gradient over the same rows.
+
+Class agreement: both trained networks are evaluated with the exact
+reference-order forward (glx_forward, byte-identical to the oracle,
+tests/test_gpu_instance.py). A row may only change class when the oracle net's
+output is within the perturbation bound the weight difference allows,
+|o - 0.5| <= B with B = 1/4 (|dw2|_1 + sum_j |w2_j| 1/4 |dw1_j|_1) for inputs in
+[0, 1] (sigmoid' <= 1/4); the number of such rows is reported and the
+accuracy must agree to that many rows.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import rel_err
+
+import paper_1908_07847_b200 as g
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def _outputs(net, x):
+    from paper_1908_07847_b200.network import _device_forward
+
+    (_, _, _, _, out), _ = _device_forward(net, x)
+    return out[:, 0].cpu().numpy()
+
+
+def _flip_bound(a, b):
+    dw1 = np.abs(a.w_ih2d.astype(np.float64) - b.w_ih2d)
+    dw2 = np.abs(a.w_ho2d.astype(np.float64) - b.w_ho2d)[0]
+    w2 = np.abs(b.w_ho2d[0, :-1].astype(np.float64))
+    return 0.25 * (dw2.sum() + float((w2 * 0.25 * dw1.sum(axis=1)).sum()))
+
+
+def _class_agreement(net, ref, x, labels):
+    o_gpu, o_ref = _outputs(net, x), _outputs(ref, x)
+    p_gpu, p_ref = o_gpu >= np.float32(0.5), o_ref >= np.float32(0.5)
+    flips = np.nonzero(p_gpu != p_ref)[0]
+    bound = _flip_bound(net, ref)
+    if flips.size:
+        assert np.abs(o_ref[flips].astype(np.float64) - 0.5).max() <= bound, (
+            f"{flips.size} rows changed class beyond the weight-difference bound {bound:.3e}")
+    acc_gpu = float((p_gpu == (labels == 1)).mean())
+    acc_ref = float((p_ref == (labels == 1)).mean())
+    assert abs(acc_gpu - acc_ref) * x.shape[0] <= flips.size + 1e-9
+    return flips.size, bound, acc_gpu, acc_ref
+
+
+def _case(N, H, seed):
+    x, l = g.synthetic_arrays(N, 33, seed, "planted-linear")
+    return x, l, l.astype(np.float32), g.init_weights(g.NetworkConfig(input_dim=33, hidden_dim=H, seed=seed))
+
+
+@pytest.mark.timeout(900)
+def test_headline_1M_rows_20_epochs_vs_oracle(gpu):
+    """The bench workload (config 2, 1M x 33-256-1) through the product API for 20
+    epochs: weights within 1e-5 of the f64 oracle, classes identical up to the
+    bounded near-threshold rows, per-epoch confusion counts consistent."""
+    epochs, lr = 20, 0.1
+    x, l, t, net0 = _case(1_000_000, 256, seed=0)
+    net = net0.copy()
+    stats = np.zeros((epochs, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, epochs, lr, g.cuda(), stats)
+    ref = net0.copy()
+    O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, t, epochs, lr)
+    err = max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho))
+    print(f"1M x 33-256-1, {epochs} epochs: max rel weight err {err:.3e}")
+    assert err <= 1e-5
+    assert (stats[:, 1:].sum(axis=1) == x.shape[0]).all()
+    nflip, bound, acc, acc_ref = _class_agreement(net, ref, x, l)
+    print(f"class flips {nflip} (bound {bound:.2e}), accuracy {acc:.6f} vs oracle {acc_ref:.6f}")
+    assert nflip <= 50  # ~1e6 rows: only rows with |o - 0.5| below the bound may differ
+    # the epoch statistics are the exact evaluation of each epoch's start weights up to the
+    # same near-threshold rows: epoch 0 against the oracle evaluation of the initial net
+    (tp, tn, fp, fn), loss = O.eval_counts(net0.w_ih2d, net0.w_ho2d, x[:200_000], l[:200_000])
+    sub = np.zeros((1, 5))
+    g.run_train_segment_batch(net0.copy().w_ih2d, net0.copy().w_ho2d, x[:200_000], t[:200_000], 1, lr, g.cuda(), sub)
+    assert np.abs(sub[0, 1:] - np.array([tp, tn, fp, fn])).sum() <= 4
+    assert abs(sub[0, 0] - loss) <= 1e-5 * loss
+
+
+@pytest.mark.timeout(900)
+def test_100k_rows_200_epochs_vs_oracle(gpu):
+    epochs, lr = 200, 0.1
+    x, l, t, net0 = _case(100_000, 256, seed=3)
+    net = net0.copy()
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, epochs, lr, g.cuda())
+    ref = net0.copy()
+    O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, t, epochs, lr)
+    err = max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho))
+    print(f"100k x 33-256-1, {epochs} epochs: max rel weight err {err:.3e}")
+    assert err <= 1e-5
+    nflip, bound, acc, acc_ref = _class_agreement(net, ref, x, l)
+    print(f"class flips {nflip} (bound {bound:.2e}), accuracy {acc:.6f} vs oracle {acc_ref:.6f}")
+    assert nflip <= 10
+
+
+@pytest.mark.timeout(1200)
+def test_64Mi_rows_one_epoch_gradient_vs_f64_oracle(gpu):
+    """Config 4 at 64Mi rows: the device gradient sum (fp32 tensor-core partials of 512
+    rows, f64 across partials and CTAs) against the oracle's f64 sum over the same rows.
+    The mean gradient must agree to 1e-6 of its largest element, and the update it
+    implies (lr 0.1) within 1e-6 max(1,|w|) of the oracle's; loss and counts too."""
+    import torch
+
+    import paper_1908_07847_b200._lib as L
+
+    rows, D, H = 1 << 26, 33, 256
+    lib = L.load()
+    st = torch.cuda.current_stream().cuda_stream
+    X, lab = g.synthetic_arrays_device(rows, D, 0, "planted-linear")
+    ld = int(lib.glx_packed_ld(D))
+    Xp = torch.empty((rows, ld), device="cuda")
+    L.check(lib.glx_pack_rows(X.data_ptr(), None, lab.data_ptr(), rows, D, Xp.data_ptr(), st))
+    xh = X.cpu().numpy()
+    th = lab.cpu().numpy().astype(np.float32)
+    del X
+    net = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=5))
+    w1 = torch.from_numpy(net.w_ih).cuda()
+    w2 = torch.from_numpy(net.w_ho).cuda()
+    glen = int(lib.glx_batch_grad_len(D, H))
+    grad = torch.zeros(glen, dtype=torch.float64, device="cuda")
+    L.check(lib.glx_batch_grad(w1.data_ptr(), w2.data_ptr(), Xp.data_ptr(), rows, D, H, grad.data_ptr(), st))
+    gd = grad.cpu().numpy()
+    del Xp
+    go = O.batch_grad_par(net.w_ih2d, net.w_ho2d, xh, th)
+    P = H * (D + 1) + H + 1
+    mean_err = np.abs(gd[:P] - go[:P]).max() / np.abs(go[:P]).max()
+    upd_gpu = net.w_ih.astype(np.float64) - 0.1 / rows * gd[:H * (D + 1)]
+    upd_ref = net.w_ih.astype(np.float64) - 0.1 / rows * go[:H * (D + 1)]
+    werr = rel_err(upd_gpu.astype(np.float32), upd_ref.astype(np.float32))
+    print(f"64Mi rows: gradient err {mean_err:.3e} of max |g|, update err {werr:.3e}, "
+          f"counts {gd[P + 1:P + 5]} vs {go[P + 1:P + 5]}")
+    assert mean_err <= 1e-6
+    assert werr <= 1e-6
+    assert abs(gd[P] - go[P]) <= 1e-6 * go[P]
+    assert np.abs(gd[P + 1:P + 5] - go[P + 1:P + 5]).sum() <= 64  # rows with |o - 0.5| ~ 1e-7

@@ -1,6 +1,7 @@
 """Host-side logic of the product package (no GPU needed)."""
 
 import hashlib
+import os
 import json
 
 import numpy as np
@@ -77,9 +78,14 @@ def test_sigmoid_known_answers():
 
 
 def test_backend_kind_contract():
+    """The reference's names and validation (backend.py:44-70, test_backend.py:18-32) plus "cuda"."""
     assert g.cuda().name == "cuda"
     assert g.sequential().numerics == "ref64" and g.parallel(4).numerics == "ref64"
-    for bad in (("gpu", 1), ("sequential", 1), ("cuda", 0)):
+    assert B.BackendKind("sequential", 1) == g.sequential()
+    assert B.BackendKind("parallel", 3).effective_workers == 3 and g.sequential().effective_workers == 1
+    assert g.parallel().workers == (os.cpu_count() or 1)
+    assert B.BackendKind("parallel", 2, "fp32").numerics == "ref64"  # the reference engines are exact
+    for bad in (("gpu", 1), ("parallel", 0), ("cuda", 0), ("sequential", -1)):
         with pytest.raises(ValidationError):
             B.BackendKind(*bad)
     with pytest.raises(ValidationError):
