@@ -438,8 +438,6 @@ __global__ void __launch_bounds__(kFT + (TRAIN ? kBT : 0), 1) batch_epoch_kernel
 }
 
 // ------------------------------------------------------------- update kernel
-// 8 lanes per parameter: lane l sums CTA partials l, l+8, ... in f64, the 8
-// lane sums combine through a fixed xor tree -> deterministic for a fixed grid.
 // f64 sum of one record slot over the per-CTA partial records: a block is
 // kRedW warps x 32 consecutive slots (coalesced 128-byte rows), warp l takes
 // records l, l+kRedW, ... (about ten independent loads per thread for 148

@@ -132,7 +132,7 @@ __device__ __forceinline__ void tmem_ld32_async(uint32_t taddr, uint32_t (&r)[32
 __device__ __forceinline__ void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 struct TcEpilogue {
-    int kind;               // 0: f32 store; 1: bias+sigmoid -> bf16; 2: output layer; 3: delta_h^T; 4: f32 accumulate
+    int kind;               // 0: f32 store; 1: bias+sigmoid -> bf16; 2: output layer; 3: delta_h; 4: f32 accumulate
     float* d_f32;           // 0, 4 (4: + blockIdx.z * zstride)
     __nv_bfloat16* d_bf16;  // 1
     __nv_bfloat16* d_t;     // 1 (optional): transposed copy of the bf16 result, row stride ldt
@@ -145,7 +145,7 @@ struct TcEpilogue {
     __nv_bfloat16* do_b;  // [M][64] bf16, columns >= K stay zero
     __nv_bfloat16* do_t;  // delta_o transposed, K-blocked [M/64][32][64] bf16 (the dW2 GEMM operand)
     double* stats;        // [loss, correct, wrong]
-    // 3: delta_h = v * h (1 - h), written transposed
+    // 3: delta_h = v * h (1 - h), row-major into d_bf16 (or transposed into dht)
     const __nv_bfloat16* h;
     int ldh;
     __nv_bfloat16* dht;
@@ -332,7 +332,7 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
             atomicAdd(ep.stats + 2, (double)wrong);
         }
     } else {
-        // delta_h = (delta_o W2)_j * h (1 - h), stored transposed for the dW1 GEMM
+        // delta_h = (delta_o W2)_j * h (1 - h): row-major (the dW1 GEMM reads it MN-major)
         uint32_t pall[16];
         uint4 hv[4] = {};
         if (rv) {
@@ -641,9 +641,9 @@ cudaError_t launch_tc(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
 // full-batch GD. Per epoch, in row chunks of C rows:
 //   1. H     = sigmoid(X W1^T + b1)                 tcgen05, epilogue 1 -> bf16
 //   2. delta_o per row (one-hot targets, K outputs)  tcgen05 (N=32 padded), epilogue 2
-//   3. dH^T  = ((delta_o W2) * h(1-h))^T              tcgen05 (K=64 padded), epilogue 3
-//   4. dW1^T += [X,1]^T dH                            tcgen05 split-K, epilogue 4 (f32 accumulate)
-//   5. dW2^T += [H,1]^T delta_o                       tcgen05 split-K, epilogue 4 (H^T from epilogue 1)
+//   3. dH    = (delta_o W2) * h(1-h), row-major        tcgen05 (K=64 padded), epilogue 3
+//   4. dW1^T += [X,1]^T dH                            tcgen05 split-K, epilogue 4 (dH read MN-major)
+//   5. dW2^T += [H,1]^T delta_o                       tcgen05 split-K, epilogue 4 (H read MN-major)
 // then W <- f32(W - lr/N grad) on the f32 master weights (reference layout).
 constexpr int kWD = 1024, kWH = 1024, kWK = 16;
 constexpr int kWMi = 1152;
@@ -738,7 +738,6 @@ __global__ void wide_derive_kernel(const float* __restrict__ W1, const float* __
     if (e < kWK) b2[e] = W2[e * (kWH + 1) + kWH];
 }
 
-// row `row` of a K-blocked [n/64][R][64] bf16 matrix = 1.0 (the bias row of H^T)
 // grad (f64, reference layout: dW1 [1024][1025] then dW2 [16][1025]) = the
 // split-K partial sums reduced in fixed slab order (dW1^T: [split][1152][1024],
 // dW2^T: [split][1152][32], row 1024 = bias)
@@ -890,7 +889,7 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             ep.stats = stats;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 3. hidden deltas, transposed
+        {  // 3. hidden deltas, row-major
             TcGemm g{w.dob, w.W2T, Cc, kWH, 64, 64, 64, 1};
             TcEpilogue ep{};
             ep.kind = 3;

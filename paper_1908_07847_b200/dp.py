@@ -115,6 +115,8 @@ def train_data_parallel_graph(engine, epochs: int, lr: float, n_total: int, all_
     train_data_parallel."""
     import torch
 
+    if epochs <= 0:
+        return []
     P = getattr(engine, "P", None) or engine.H * (engine.D + 1) + engine.H + 1
     ns = getattr(engine, "n_stats", 5)
     key = float(lr) / n_total
@@ -122,27 +124,31 @@ def train_data_parallel_graph(engine, epochs: int, lr: float, n_total: int, all_
     if cache is None or cache[0] != key:
         side = torch.cuda.Stream(device=engine.grad.device)
         saved = engine.stream
+        side.wait_stream(torch.cuda.current_stream())
         try:
-            side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
                 engine.stream = side.cuda_stream
                 # one eager epoch on the capture stream: the library allocates its
-                # per-stream workspace on first use, which capture does not allow
+                # per-stream workspace on first use, which capture does not allow.
+                # Errors here are real (kernel / NCCL) and propagate.
                 first = train_data_parallel(engine, 1, lr, n_total, all_reduce)
                 graph = torch.cuda.CUDAGraph()
                 n0 = int(engine.L.glx_launch_count())
-                with torch.cuda.graph(graph, stream=side):
-                    g = engine.grad_sum()
-                    all_reduce(g)
-                    engine.apply(g, key)
+                try:
+                    with torch.cuda.graph(graph, stream=side):
+                        g = engine.grad_sum()
+                        all_reduce(g)
+                        engine.apply(g, key)
+                except RuntimeError as e:  # only a refused capture falls back to eager epochs
+                    if "captur" not in str(e).lower():
+                        raise
+                    graph = None
                 per_replay = int(engine.L.glx_launch_count()) - n0
-            torch.cuda.current_stream().wait_stream(side)
-        except Exception:  # capture unsupported here: eager epochs
-            engine.stream = saved
-            torch.cuda.current_stream().wait_stream(side)
-            return first + train_data_parallel(engine, epochs - 1, lr, n_total, all_reduce) if epochs > 1 else first
         finally:
             engine.stream = saved
+            torch.cuda.current_stream().wait_stream(side)
+        if graph is None:
+            return first + train_data_parallel(engine, epochs - 1, lr, n_total, all_reduce)
         engine._graph_cache = (key, graph, side, per_replay)
         done = first
         epochs -= 1

@@ -13,6 +13,7 @@ shared-memory copy of the rows.
 
 from __future__ import annotations
 
+import os
 import heapq
 from dataclasses import dataclass
 
@@ -139,7 +140,14 @@ def train_sweep(spec: SweepSpec, feats2d: np.ndarray, targets: np.ndarray, *, ra
     nets = [init_weights(c) for c in spec.configs()]
     shards = lpt_shards(spec.costs(), world_size)
     mine = shards[rank]
-    dev = rank if device is None else device
+    # the local GPU of this rank (a global rank can exceed the node's GPU count)
+    dev = int(os.environ.get("LOCAL_RANK", rank)) if device is None else device
+    if trainer is None:
+        import torch
+
+        if torch.cuda.is_available():
+            # gather_object over NCCL stages through torch.cuda.current_device()
+            torch.cuda.set_device(dev)
     (trainer or train_nets_on_device)([nets[i] for i in mine], feats2d, targets, spec.epochs, spec.learning_rate,
                                       spec.numerics, dev)
     if world_size == 1:
