@@ -47,6 +47,13 @@ def hardware_parallelism() -> int:
     return os.cpu_count() or 1
 
 
+def max_workers() -> int:
+    """backend.py:38-40: the upper bound on a worker pool. The reference sizes it by
+    numba's thread pool (the core count); the device engine has no host pool, so the
+    same core-count bound is kept for the reference's clamping contract."""
+    return hardware_parallelism()
+
+
 @dataclass(frozen=True)
 class BackendKind:
     """Engine selector (backend.py:44-62).
@@ -77,8 +84,8 @@ class BackendKind:
 
     @property
     def effective_workers(self) -> int:
-        """backend.py:57-62: 1 for sequential; the requested pool otherwise."""
-        return 1 if self.name == SEQUENTIAL else int(self.workers)
+        """backend.py:57-62: 1 for sequential; the requested pool clamped to max_workers()."""
+        return 1 if self.name == SEQUENTIAL else min(int(self.workers), max_workers())
 
 
 def cuda(device: int = 0, numerics: str = "fp32", workers: int = 1) -> BackendKind:

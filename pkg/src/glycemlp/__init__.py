@@ -40,6 +40,8 @@ from paper_1908_07847_b200.backend import (  # noqa: E402
     BackendKind,
     LayerJob,
     cuda,
+    hardware_parallelism,
+    max_workers,
     parallel,
     run_layer_backward,
     run_layer_forward,

@@ -1,0 +1,424 @@
+"""The reference's own hot-path tests, run against `import glycemlp` (pkg/src, the
+drop-in package) on the device.
+
+Ported from /root/reference/pkg/tests/ (test_trainer.py, test_gradcheck.py,
+test_acceptance.py criteria 1, 2, 4, 5) with the same assertions. The splits
+those tests build with the reference's record / CSV / split pipeline (out of
+scope here) come from fixtures the unmodified reference wrote
+(tests/golden/make_golden.py: `dropin`, `protocol`, `acceptance`), together with
+the reference's results on them, so every test also checks that the device
+engine reproduces the reference's bytes, not only the reference's assertions.
+
+Timing bounds of the reference's acceptance tests are not asserted (they bound a
+CPU engine's run time); the throughput claims live in bench.py.
+"""
+
+from __future__ import annotations
+
+import json
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, rel_err
+
+import glycemlp as g
+from glycemlp import backend as B
+from glycemlp.errors import ShapeError, ValidationError
+from glycemlp.network import loss_gradients
+from glycemlp.trainer import (
+    CURVE_HEADER,
+    TrainSpec,
+    load_report,
+    network_from_report,
+    read_curve_csv,
+    report_to_dict,
+    save_report,
+    strip_timing,
+    write_curve_csv,
+)
+
+pytestmark = pytest.mark.gpu
+
+_DROPIN = dict(np.load(GOLDEN / "dropin_splits.npz"))
+
+
+def _dataset(x, y, ids, tag, stats):
+    return g.Dataset(features=np.ascontiguousarray(x, np.float32).reshape(-1).copy(),
+                     labels=np.asarray(y, np.uint8).copy(), rows=x.shape[0], columns=x.shape[1],
+                     subset_tag=str(tag), row_ids=tuple(str(i) for i in ids), norm_stats=stats)
+
+
+def split_of(name, normalized=True):
+    """The reference-built SplitPair `name` (make_matrix_split / make_record_split of
+    the reference's conftest.py:7-17), rebuilt from the fixture."""
+    f = _DROPIN
+    stats = g.NormStats(col_min=f[f"{name}_col_min"], col_max=f[f"{name}_col_max"]) if normalized else None
+    parts = [_dataset(f[f"{name}_{p}_x"], f[f"{name}_{p}_y"], f[f"{name}_{p}_ids"], f[f"{name}_{p}_tag"][0], stats)
+             for p in ("train", "test")]
+    seed, frac = f[f"{name}_split"]
+    return g.SplitPair(train=parts[0], test=parts[1], seed=int(seed), fraction=float(frac))
+
+
+def small_spec(columns, epochs=50, checkpoints=None, seed=0, backend=None):
+    cfg = g.NetworkConfig(input_dim=columns, seed=seed)
+    return TrainSpec(config=cfg, epochs=epochs, backend=backend or g.sequential(), checkpoints=checkpoints)
+
+
+def assert_reference_run(report, name, run):
+    """The report equals the unmodified reference's g.train on the same split/spec:
+    every checkpoint row (epoch, accuracies, confusion counts) and the weight bytes."""
+    f = _DROPIN
+    want = f[f"{name}_run{run}_rows"]
+    got = np.array([[r.epoch, r.train_accuracy, r.test_accuracy,
+                     *[r.train_confusion[c] for c in ("tp", "tn", "fp", "fn")],
+                     *[r.test_confusion[c] for c in ("tp", "tn", "fp", "fn")]] for r in report.rows], np.float64)
+    assert got.shape == want.shape and (got == want).all(), (got, want)
+    assert report.network.w_ih.tobytes() == f[f"{name}_run{run}_w_ih"].tobytes()
+    assert report.network.w_ho.tobytes() == f[f"{name}_run{run}_w_ho"].tobytes()
+
+
+# ------------------------------------------------------------ test_trainer.py
+class TestTrain:
+    def test_deterministic_per_spec_and_split(self, gpu):
+        pair = split_of("m30_6_2")
+        spec = small_spec(6, epochs=40, checkpoints=(1, 10, 40), seed=1)
+        a, b = g.train(spec, pair), g.train(spec, pair)
+        assert [(r.epoch, r.train_accuracy, r.test_accuracy) for r in a.rows] == \
+               [(r.epoch, r.train_accuracy, r.test_accuracy) for r in b.rows]
+        assert a.network.w_ih.tobytes() == b.network.w_ih.tobytes()
+        assert a.network.w_ho.tobytes() == b.network.w_ho.tobytes()
+        assert_reference_run(a, "m30_6_2", 0)
+
+    def test_checkpoint_evaluation_is_side_effect_free(self, gpu):
+        pair = split_of("m24_5_4")
+        dense = g.train(small_spec(5, epochs=32, checkpoints=(1, 2, 4, 8, 16, 32), seed=2), pair)
+        sparse = g.train(small_spec(5, epochs=32, checkpoints=(32,), seed=2), pair)
+        assert dense.network.w_ih.tobytes() == sparse.network.w_ih.tobytes()
+        assert dense.network.w_ho.tobytes() == sparse.network.w_ho.tobytes()
+        assert_reference_run(dense, "m24_5_4", 0)
+        assert_reference_run(sparse, "m24_5_4", 1)
+
+    def test_rows_ordered_and_bounded(self, gpu):
+        pair = split_of("r40_6")
+        report = g.train(small_spec(pair.train.columns, epochs=100, checkpoints=(1, 10, 100)), pair)
+        epochs = [r.epoch for r in report.rows]
+        assert epochs == sorted(epochs) == [1, 10, 100]
+        for r in report.rows:
+            assert 0.0 <= r.train_accuracy <= 1.0
+            assert 0.0 <= r.test_accuracy <= 1.0
+            assert sum(r.train_confusion.values()) == pair.train.rows
+            assert sum(r.test_confusion.values()) == pair.test.rows
+        assert_reference_run(report, "r40_6", 0)
+
+    def test_requires_normalized_split(self, gpu):
+        pair = split_of("m20_4_0", normalized=False)
+        with pytest.raises(ValidationError):
+            g.train(small_spec(4), pair)
+
+    def test_rejects_overlapping_partitions(self, gpu):
+        pair = split_of("m20_4_0")
+        bogus = g.SplitPair(train=pair.train, test=pair.train, seed=0, fraction=0.75)
+        with pytest.raises(ValidationError):
+            g.train(small_spec(4), bogus)
+
+    def test_feature_count_mismatch(self, gpu):
+        pair = split_of("m20_4_0")
+        with pytest.raises(ShapeError):
+            g.train(small_spec(9), pair)
+
+    def test_divergence_reports_last_good_checkpoint(self, gpu):
+        pair = split_of("m20_4_1")
+        cfg = g.NetworkConfig(input_dim=4, seed=0)
+        poisoned = g.init_weights(cfg)
+        poisoned.w_ih[0] = np.float32(np.inf)
+        spec = TrainSpec(config=cfg, epochs=10, backend=g.sequential(), checkpoints=(1, 10))
+        report = g.train(spec, pair, initial_net=poisoned)
+        assert report.diverged
+        assert report.rows == ()
+        assert report.metadata["diverged"] is True
+        assert report.network.w_ih.tobytes() == poisoned.w_ih.tobytes()
+
+    def test_metadata_carries_deviation_flag_and_stats(self, gpu):
+        pair = split_of("r30_1")
+        report = g.train(small_spec(pair.train.columns, epochs=5, checkpoints=(5,)), pair)
+        assert "bias-terms-enabled" in report.metadata["deviation_flags"]
+        assert len(report.metadata["norm_stats"]["col_min"]) == pair.train.columns
+        assert report.metadata["split"]["train_rows"] == pair.train.rows
+        assert_reference_run(report, "r30_1", 0)
+
+    def test_backend_choice_does_not_change_results(self, gpu):
+        pair = split_of("m26_5_9")
+        seq = g.train(small_spec(5, epochs=60, checkpoints=(60,), seed=3), pair)
+        par = g.train(small_spec(5, epochs=60, checkpoints=(60,), seed=3, backend=g.parallel(2)), pair)
+        assert seq.network.w_ih.tobytes() == par.network.w_ih.tobytes()
+        assert [r.train_accuracy for r in seq.rows] == [r.train_accuracy for r in par.rows]
+        assert_reference_run(seq, "m26_5_9", 0)
+
+    def test_fp32_engine_within_tolerance_of_reference(self, gpu):
+        """The FP32 device engine (g.cuda()) on the same split: weights within 1e-4
+        max(1,|w|) of the reference's and the same checkpoint rows."""
+        pair = split_of("m26_5_9")
+        rep = g.train(small_spec(5, epochs=60, checkpoints=(60,), seed=3, backend=g.cuda()), pair)
+        assert rel_err(rep.network.w_ih, _DROPIN["m26_5_9_run0_w_ih"]) <= 1e-4
+        assert rel_err(rep.network.w_ho, _DROPIN["m26_5_9_run0_w_ho"]) <= 1e-4
+        assert rep.rows[-1].train_accuracy == _DROPIN["m26_5_9_run0_rows"][-1][1]
+
+
+class TestEvaluate:
+    def _dataset(self, labels):
+        labels = np.asarray(labels, dtype=np.uint8)
+        rng = np.random.default_rng(0)
+        feats = rng.random((len(labels), 3), dtype=np.float32).reshape(-1)
+        return g.Dataset(features=feats, labels=labels, rows=len(labels), columns=3, subset_tag="synthetic",
+                         row_ids=tuple(f"r{i}" for i in range(len(labels))))
+
+    def _zero_net(self):
+        cfg = g.NetworkConfig(input_dim=3, hidden_dim=2)
+        return g.Network(cfg, np.zeros(cfg.w_ih_len, np.float32), np.zeros(cfg.w_ho_len, np.float32))
+
+    def test_zero_net_predicts_poor_everywhere(self, gpu):
+        d = self._dataset([1, 1, 1, 1, 0, 0, 0, 0, 0, 0])
+        assert g.evaluate(self._zero_net(), d) == pytest.approx(0.4)
+
+    def test_perfect_classifier(self, gpu):
+        assert g.evaluate(self._zero_net(), self._dataset([1, 1, 1, 1])) == 1.0
+
+    def test_single_row_dataset(self, gpu):
+        for label in (0, 1):
+            assert g.evaluate(self._zero_net(), self._dataset([label])) in (0.0, 1.0)
+
+    def test_empty_dataset_rejected(self, gpu):
+        with pytest.raises(ValueError):
+            g.evaluate(self._zero_net(), self._dataset([]))
+
+    def test_confusion_counts(self, gpu):
+        from glycemlp.trainer import confusion
+
+        assert confusion(self._zero_net(), self._dataset([1, 0, 1, 0])) == {"tp": 2, "tn": 0, "fp": 2, "fn": 0}
+
+
+class TestConvergenceSmoke:
+    def test_separable_toy_reaches_full_accuracy(self, gpu):
+        rng = np.random.default_rng(0)
+        lo = rng.uniform(0.0, 0.35, size=(10, 2))
+        hi = rng.uniform(0.65, 1.0, size=(10, 2))
+        feats = np.vstack([lo, hi]).astype(np.float32)
+        labels = np.array([0] * 10 + [1] * 10, dtype=np.uint8)
+        d = g.Dataset(features=feats.reshape(-1).copy(), labels=labels, rows=20, columns=2, subset_tag="synthetic",
+                      row_ids=tuple(f"t{i}" for i in range(20)))
+        wins = 0
+        for seed in range(10):
+            net = g.init_weights(g.NetworkConfig(input_dim=2, seed=seed))
+            B.run_train_segment(net.w_ih2d, net.w_ho2d, d.matrix(), labels.astype(np.float32), 10_000, 0.1,
+                                g.sequential())
+            if g.evaluate(net, d) == 1.0:
+                wins += 1
+        assert wins >= 9
+
+
+class TestSweepAndReports:
+    def test_sweep_rows_match_train(self, gpu):
+        pair = split_of("m24_4_5")
+        spec = small_spec(4, epochs=30, checkpoints=(1, 10, 30), seed=1)
+        rows = g.epoch_sweep(spec, pair)
+        report = g.train(spec, pair)
+        assert [(a.epoch, a.train_accuracy, a.test_accuracy) for a in rows] == \
+               [(b.epoch, b.train_accuracy, b.test_accuracy) for b in report.rows]
+        assert_reference_run(report, "m24_4_5", 0)
+
+    def test_curve_csv_round_trip(self, gpu, tmp_path):
+        pair = split_of("m24_4_5")
+        rows = g.epoch_sweep(small_spec(4, epochs=20, checkpoints=(1, 20), seed=2), pair)
+        path = tmp_path / "curve.csv"
+        write_curve_csv(rows, path)
+        assert path.read_text().splitlines()[0] == ",".join(CURVE_HEADER)
+        parsed = read_curve_csv(path)
+        assert [p["epoch"] for p in parsed] == [r.epoch for r in rows]
+        assert parsed[0]["train_accuracy"] == rows[0].train_accuracy
+
+    def test_report_json_round_trip(self, gpu, tmp_path):
+        pair = split_of("r30_3")
+        report = g.train(small_spec(pair.train.columns, epochs=10, checkpoints=(10,)), pair)
+        path = tmp_path / "report.json"
+        save_report(report, path)
+        doc = load_report(path)
+        assert doc["format"] == "glycemlp-train-report-v1"
+        assert network_from_report(doc).w_ih.tobytes() == report.network.w_ih.tobytes()
+        assert_reference_run(report, "r30_3", 0)
+
+    def test_strip_timing_makes_documents_comparable(self, gpu):
+        pair = split_of("m24_4_7")
+        spec = small_spec(4, epochs=15, checkpoints=(5, 15), seed=4)
+        doc_a = strip_timing(report_to_dict(g.train(spec, pair)))
+        doc_b = strip_timing(report_to_dict(g.train(spec, pair)))
+        assert json.dumps(doc_a) == json.dumps(doc_b)
+
+
+# ---------------------------------------------------------- test_gradcheck.py
+FD_STEP = 1e-4
+GRAD_TOL = 1e-4
+
+
+def _oracle_loss(w_ih64, w_ho64, x64, target):
+    hidden = 1.0 / (1.0 + np.exp(-(w_ih64[:, :-1] @ x64 + w_ih64[:, -1])))
+    out = 1.0 / (1.0 + np.exp(-(w_ho64[:, :-1] @ hidden + w_ho64[:, -1])))
+    return 0.5 * (target - out[0]) ** 2
+
+
+def _fd_gradients(net, x, target):
+    w_ih64, w_ho64 = net.w_ih2d.astype(np.float64), net.w_ho2d.astype(np.float64)
+    x64 = np.asarray(x, dtype=np.float64)
+    grads = []
+    for w in (w_ih64, w_ho64):
+        grad = np.empty_like(w)
+        for idx in np.ndindex(w.shape):
+            keep = w[idx]
+            w[idx] = keep + FD_STEP
+            up = _oracle_loss(w_ih64, w_ho64, x64, target)
+            w[idx] = keep - FD_STEP
+            down = _oracle_loss(w_ih64, w_ho64, x64, target)
+            w[idx] = keep
+            grad[idx] = (up - down) / (2.0 * FD_STEP)
+        grads.append(grad)
+    return grads
+
+
+def max_relative_error(net, x, target):
+    g_ih, g_ho, _ = loss_gradients(net, x, target)  # the device instance-gradient kernel
+    fd_ih, fd_ho = _fd_gradients(net, x, target)
+    worst = 0.0
+    for analytic, numeric in ((g_ih, fd_ih), (g_ho, fd_ho)):
+        denom = np.maximum(1.0, np.abs(analytic))
+        worst = max(worst, float(np.max(np.abs(analytic - numeric) / denom)))
+    return worst
+
+
+def test_criterion_1_gradient_correctness(gpu):
+    """test_acceptance.py:29-45 and test_gradcheck.py:64-69: device analytic gradients
+    vs central finite differences of an independent f64 forward."""
+    worst = 0.0
+    for input_dim, hidden_dim in ((3, 2), (5, 3), (33, 33)):
+        for seed in range(10):
+            net = g.init_weights(g.NetworkConfig(input_dim=input_dim, hidden_dim=hidden_dim, seed=seed))
+            rng = np.random.default_rng(500 + seed)
+            x = rng.random(input_dim, dtype=np.float32)
+            worst = max(worst, max_relative_error(net, x, float(rng.integers(2))))
+    print(f"[criterion 1] max relative gradient error {worst:.2e} (tol {GRAD_TOL})")
+    assert worst < GRAD_TOL
+
+
+def test_gradients_zero_when_saturated_towards_target(gpu):
+    net = g.init_weights(g.NetworkConfig(input_dim=2, hidden_dim=2, seed=0))
+    net.w_ho[:] = np.array([0.0, 0.0, 30.0], dtype=np.float32)
+    g_ih, g_ho, err = loss_gradients(net, [0.5, 0.5], 1.0)
+    assert err < 1e-12
+    assert np.max(np.abs(g_ih)) < 1e-12
+    assert np.max(np.abs(g_ho)) < 1e-12
+
+
+# -------------------------------------------------------- test_acceptance.py
+_PROTO = dict(np.load(GOLDEN / "protocol_100k.npz"))
+
+
+def _proto_split(name):
+    f = _PROTO
+    D = f[f"{name}_train_x"].shape[1]
+    stats = g.NormStats(col_min=np.zeros(D, np.float32), col_max=np.ones(D, np.float32))
+    tr = _dataset(f[f"{name}_train_x"], f[f"{name}_train_y"], [f"a{i}" for i in range(len(f[f"{name}_train_y"]))],
+                  "synthetic", stats)
+    te = _dataset(f[f"{name}_test_x"], f[f"{name}_test_y"], [f"b{i}" for i in range(len(f[f"{name}_test_y"]))],
+                  "synthetic", stats)
+    return g.SplitPair(train=tr, test=te, seed=7, fraction=0.75)
+
+
+def test_criterion_2_backend_bitwise_equivalence(gpu):
+    """test_acceptance.py:48-67: paper split, 33-33-1, 1000 epochs; the sequential and
+    parallel engines (1 and all host workers) give byte-identical weights and identical
+    predictions -- and here also the reference's own bytes at 1000 epochs."""
+    pair = _proto_split("paper")
+    cfg = g.NetworkConfig(input_dim=33, hidden_dim=33, seed=7)
+    nets = []
+    for kind in (g.sequential(), *(g.parallel(w) for w in sorted({1, B.hardware_parallelism()}))):
+        nets.append(g.train(TrainSpec(config=cfg, epochs=1_000, backend=kind, checkpoints=(1_000,)), pair).network)
+    seq = nets[0]
+    assert all(seq.w_ih.tobytes() == n.w_ih.tobytes() and seq.w_ho.tobytes() == n.w_ho.tobytes() for n in nets[1:])
+    preds = [[g.predict(n, row) for row in pair.test.matrix()] for n in nets]
+    assert all(p == preds[0] for p in preds[1:])
+    ref = np.load(GOLDEN / "paper_33_33_1.npz")
+    assert seq.w_ih.tobytes() == ref["w_ih_1000"].tobytes() and seq.w_ho.tobytes() == ref["w_ho_1000"].tobytes()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("name", ["paper", "male", "female"])
+def test_paper_protocol_100k_epochs(gpu, name):
+    """The paper protocol (cli.py:34-36: 100k epochs at lr 0.1) on the paper split and
+    both cohorts through g.train: the exact engine reproduces the reference's weights
+    byte for byte and its confusion counts at 10k and 100k epochs; the FP32 engine
+    stays within 1e-4 max(1,|w|) with identical counts."""
+    f = _PROTO
+    D, H, _, seed = (int(v) for v in f[f"{name}_meta"])
+    pair = _proto_split(name)
+    cfg = g.NetworkConfig(input_dim=D, hidden_dim=H, seed=seed)
+    for kind in (g.sequential(), g.cuda()):
+        rep = g.train(TrainSpec(config=cfg, epochs=100_000, backend=kind, checkpoints=(10_000, 100_000)), pair)
+        assert not rep.diverged
+        for row in rep.rows:
+            e = row.epoch
+            assert [row.train_confusion[c] for c in ("tp", "tn", "fp", "fn")] == list(f[f"{name}_train_counts_{e}"])
+            assert [row.test_confusion[c] for c in ("tp", "tn", "fp", "fn")] == list(f[f"{name}_test_counts_{e}"])
+        w_ih, w_ho = f[f"{name}_w_ih_100000"], f[f"{name}_w_ho_100000"]
+        if kind.numerics == "ref64":
+            assert rep.network.w_ih.tobytes() == w_ih.tobytes() and rep.network.w_ho.tobytes() == w_ho.tobytes()
+        else:
+            err = max(rel_err(rep.network.w_ih, w_ih), rel_err(rep.network.w_ho, w_ho))
+            print(f"{name}: fp32 engine at 100k epochs, max rel weight err {err:.2e}")
+            assert err <= 1e-4
+
+
+def _acceptance(crit, kind):
+    f = dict(np.load(GOLDEN / f"acceptance_c{crit}.npz"))
+    finals, exact = [], 0
+    for seed in range(10):
+        D = f[f"s{seed}_train_x"].shape[1]
+        stats = g.NormStats(col_min=np.zeros(D, np.float32), col_max=np.ones(D, np.float32))
+        tr = _dataset(f[f"s{seed}_train_x"], f[f"s{seed}_train_y"], [f"a{i}" for i in range(len(f[f"s{seed}_train_y"]))],
+                      "synthetic", stats)
+        te = _dataset(f[f"s{seed}_test_x"], f[f"s{seed}_test_y"], [f"b{i}" for i in range(len(f[f"s{seed}_test_y"]))],
+                      "synthetic", stats)
+        cfg = g.NetworkConfig(input_dim=D, seed=seed, learning_rate=0.1)
+        rep = g.train(TrainSpec(config=cfg, epochs=100_000, backend=kind, checkpoints=(100_000,)),
+                      g.SplitPair(train=tr, test=te, seed=seed, fraction=0.75))
+        row = rep.rows[-1]
+        finals.append((row.train_accuracy, row.test_accuracy))
+        assert (row.train_accuracy, row.test_accuracy) == tuple(f[f"s{seed}_acc"])
+        if kind.numerics == "ref64":
+            assert rep.network.w_ih.tobytes() == f[f"s{seed}_w_ih"].tobytes()
+            assert rep.network.w_ho.tobytes() == f[f"s{seed}_w_ho"].tobytes()
+            exact += 1
+        else:
+            assert max(rel_err(rep.network.w_ih, f[f"s{seed}_w_ih"]), rel_err(rep.network.w_ho, f[f"s{seed}_w_ho"])) <= 1e-4
+    return finals
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("engine", ["parallel", "cuda"])
+def test_criterion_4_learnability_target(gpu, engine):
+    """test_acceptance.py:80-98: planted-linear 61-row cohorts, 100k epochs, >= 8 of 10
+    seeds reach train >= 0.95 and test >= 0.80 (and each seed's accuracies equal the
+    reference's)."""
+    finals = _acceptance(4, g.parallel() if engine == "parallel" else g.cuda())
+    passed = sum(tr >= 0.95 and te >= 0.80 for tr, te in finals)
+    print(f"[criterion 4] {engine}: {passed}/10 seeds, {[(round(a, 3), round(b, 3)) for a, b in finals]}")
+    assert passed >= 8
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("engine", ["sequential", "cuda"])
+def test_criterion_5_overfitting_demonstration(gpu, engine):
+    """test_acceptance.py:101-115: weak-signal 59-row cohorts, 100k epochs, >= 7 of 10
+    seeds memorise (train >= 0.90) without generalising (test <= 0.75)."""
+    finals = _acceptance(5, g.sequential() if engine == "sequential" else g.cuda())
+    passed = sum(tr >= 0.90 and te <= 0.75 for tr, te in finals)
+    print(f"[criterion 5] {engine}: {passed}/10 seeds, {[(round(a, 3), round(b, 3)) for a, b in finals]}")
+    assert passed >= 7
