@@ -170,6 +170,36 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
 int glx_batch_apply(float* w_ih, float* w_ho, const double* grad, int32_t D, int32_t H, double lr_over_n,
                     int32_t* nonfinite, void* stream);
 
+/* ------------------------------------------------ data-parallel data plane
+ * SURVEY.md 8(b) (glx_dp_init) and 8(e): the per-epoch gradient exchange of the
+ * data-parallel batch configurations (C2/C4 across GPUs) over NCCL, owned by
+ * this library (no reference counterpart: the reference has no multi-process
+ * or multi-GPU path). One communicator per rank (one process
+ * per GPU). glx_dp_unique_id fills the 128-byte ncclUniqueId on one rank; the
+ * caller ships it to the others by any channel; every rank then calls
+ * glx_dp_init (ncclCommInitRank, collective: all ranks must call it).
+ * glx_dp_allreduce_f64: in-place all-reduce of n doubles (op 0 sum, 1 max) on
+ * `stream`. glx_dp_train_batch: `epochs` full-batch epochs over this rank's N
+ * packed rows (glx_packed_ld layout) with the global row count N_total; every
+ * epoch = the epoch kernel, the f64 gradient sum, ncclAllReduce(sum) of the
+ * P + 5 doubles, and the update W <- f32(f64(W) - lr/N_total * grad) applied
+ * identically on every rank; captured once into a CUDA graph and replayed
+ * (GLX_DP_GRAPH=0: eager). N may be 0 (the rank still joins the all-reduce).
+ * stats_hist (device, may be NULL): 5 doubles per epoch, loss, tp, tn, fp, fn
+ * over ALL ranks' rows at the epoch-start weights. Collective: all ranks call
+ * it with the same D, H, epochs, lr, N_total.
+ * glx_dp_run_train_segment_batch: the same from host buffers (the rank's
+ * shard), with glx_run_train_segment_batch's copy-in/copy-out contract. */
+int glx_dp_unique_id(uint8_t* id128);
+int glx_dp_init(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id128, void** comm);
+int glx_dp_finalize(void* comm);
+int glx_dp_allreduce_f64(void* comm, double* buf, int64_t n, int32_t op, void* stream);
+int glx_dp_train_batch(void* comm, float* w_ih, float* w_ho, const float* Xp, int64_t N, int64_t N_total, int32_t D,
+                       int32_t H, int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream);
+int glx_dp_run_train_segment_batch(void* comm, float* w_ih, float* w_ho, const float* feats, const float* targets,
+                                   int64_t rows, int64_t rows_total, int32_t input_dim, int32_t hidden_dim,
+                                   int64_t epochs, double lr, double* stats_hist, int32_t flags);
+
 /* Evaluation on device buffers; results land in device memory
  * (counts4: uint64[4] accumulated, so zero it first; loss: double[1]). */
 int glx_eval(const float* w_ih, const float* w_ho, const float* X, const uint8_t* labels, int64_t N, int32_t D,

@@ -19,6 +19,9 @@ BUILD = ROOT / "build"
 LIB = PKG / "libglycemlp_cuda.so"
 SOURCES = ("glx_online.cu", "glx_batch.cu", "glx_batch3.cu", "glx_batchtc.cu", "glx_eval.cu", "glx_tc.cu", "glx_data.cu", "glx_abi.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# NCCL: the image's libnccl.so.2 (soname-compatible with the copy torch loads, which
+# the dynamic linker reuses when torch is imported first)
+LINK = ["-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 
 
@@ -62,7 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
                 if verbose:
                     print(f"compiled {src}")
     if force or jobs or _stale(LIB, objs):
-        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs)]
+        cmd = [nvcc(), *ARCH, "-shared", "-o", str(LIB), *map(str, objs), *LINK]
         p = subprocess.run(cmd, capture_output=True, text=True)
         if p.returncode != 0:
             raise RuntimeError(f"link failed:\n{p.stderr[-4000:]}")

@@ -78,6 +78,13 @@ SIGNATURES = {
     "glx_wide_grad_len": (_i64, []),
     "glx_wide_grad": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "glx_wide_apply": (_int, [_vp, _vp, _vp, _dbl, _vp, _vp]),
+    "glx_dp_unique_id": (_int, [_vp]),
+    "glx_dp_init": (_int, [_i32, _i32, _i32, _vp, _vp]),
+    "glx_dp_finalize": (_int, [_vp]),
+    "glx_dp_allreduce_f64": (_int, [_vp, _vp, _i64, _i32, _vp]),
+    "glx_dp_train_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i64, _dbl, _vp, _vp, _vp]),
+    "glx_dp_run_train_segment_batch": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i64, _dbl, _vp,
+                                              _i32]),
     "glx_launch_count": (_u64, []),
     "glx_profile_enable": (None, [_i32]),
     "glx_profile_read": (_int, [_vp, _vp]),

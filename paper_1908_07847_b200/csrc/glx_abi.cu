@@ -7,6 +7,7 @@
 // gradient partials, kernel weight copies, descriptors) is cached per
 // (device, stream) and only ever grows.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -347,6 +348,144 @@ cudaError_t launch_batch_grad(const BatchGeom& g, const float* part, const float
 cudaError_t launch_batch_apply(int D, int H, float* W1, float* W2, const double* grad, double lr_over_n,
                                int* nonfinite, cudaStream_t st);
 }  // namespace glx
+
+namespace {
+// ------------------------------------------------------------------------------
+// Data plane of the data-parallel configurations (SURVEY.md 8(b) glx_dp_init,
+// 8(e)): one NCCL communicator per rank, owned here. A DP epoch is
+//   epoch kernel (this rank's rows) -> f64 gradient sum (batch_grad_kernel)
+//   -> ncclAllReduce(sum, f64, P + 5 doubles) -> update + next weight copy
+// and is captured once into CUDA graphs (one per parity of the double-buffered
+// pre-scaled weight copy), replayed every epoch on a library-owned stream that
+// is joined to the caller's stream by events.
+struct DpComm {
+    ncclComm_t comm = nullptr;
+    int dev = 0, nranks = 1, rank = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+    DevBuf grad, slot;
+    // graph cache: the captured epoch is valid for these arguments
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    const void* key[6] = {};
+    int64_t key_n = -1;
+    int key_d = 0, key_h = 0;
+    double key_lr = 0.0;
+    int per_replay = 0;
+    void drop_graphs() {
+        for (auto& e : exec)
+            if (e) {
+                cudaGraphExecDestroy(e);
+                e = nullptr;
+            }
+        key_n = -1;
+    }
+};
+
+bool dp_graphs_enabled() {  // GLX_DP_GRAPH=0: eager epochs (read per call, for A/B tests)
+    const char* e = getenv("GLX_DP_GRAPH");
+    return !(e && e[0] == '0');
+}
+
+#define GLX_NCCL(expr)                                                                                          \
+    do {                                                                                                        \
+        ncclResult_t r_ = (expr);                                                                               \
+        if (r_ != ncclSuccess)                                                                                  \
+            return set_err(GLX_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, ncclGetErrorString(r_), __FILE__, __LINE__); \
+    } while (0)
+
+// one epoch on dp->st: kernels of this rank's rows, the all-reduce, the update
+// (profile: per-launch events around the epoch kernel, eager epochs only)
+int dp_epoch_enqueue(DpComm* dp, const BatchGeom& g, int kind, bool have_rows, const float* Xp, float* part,
+                     float* wk_cur, float* wk_nxt, float* w_ih, float* w_ho, double lr_over_n, int32_t* nonfinite,
+                     bool profile) {
+    cudaStream_t st = dp->st;
+    const int64_t glen = (int64_t)g.P1 + g.H + 1 + 5;
+    double* grad = dp->grad.as<double>();
+    if (have_rows) {
+        cudaEvent_t pe = nullptr;
+        if (profile) GLX_CK(prof_begin(st, &pe));
+        GLX_CK(launch_train_epoch(g, kind, Xp, wk_cur, part, st));
+        if (pe) GLX_CK(cudaEventRecord(pe, st));
+        GLX_CK(launch_batch_grad(g, part, wk_cur, grad, st));
+    } else {
+        GLX_CK(cudaMemsetAsync(grad, 0, glen * sizeof(double), st));
+    }
+    GLX_NCCL(ncclAllReduce(grad, grad, (size_t)glen, ncclDouble, ncclSum, dp->comm, st));
+    GLX_CK(launch_batch_dp_update(g, w_ih, w_ho, wk_nxt, grad, lr_over_n, dp->slot.as<double>(), nonfinite, st));
+    return GLX_OK;
+}
+
+int dp_train_batch(DpComm* dp, float* w_ih, float* w_ho, const float* Xp, int64_t N, int64_t N_total, int D, int H,
+                   int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, cudaStream_t caller) {
+    BatchGeom g;
+    int kind = 0;
+    if (!train_geometry(std::max<int64_t>(N, 1), D, H, &g, &kind))
+        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d", D, H);
+    GLX_CK(cudaSetDevice(dp->dev));
+    Workspace* ws = workspace(dp->st);
+    GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
+    GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
+    GLX_CK(dp->grad.ensure(((size_t)g.P1 + H + 1 + 5) * sizeof(double)));
+    GLX_CK(dp->slot.ensure(5 * sizeof(double)));
+    float* wk0 = ws->wk.as<float>();
+    float* wk1 = wk0 + g.WKS;
+    float* part = ws->part.as<float>();
+    const double lr_over_n = lr / (double)N_total;
+    const bool rows = N > 0;
+    GLX_CK(cudaEventRecord(dp->ev_in, caller));
+    GLX_CK(cudaStreamWaitEvent(dp->st, dp->ev_in, 0));
+    GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk1, dp->st));
+    const int per_epoch = rows ? 3 : 1;
+    if (dp_graphs_enabled()) {
+        const void* key[6] = {w_ih, w_ho, Xp, nonfinite, ws->wk.p, ws->part.p};
+        const bool hit = dp->exec[0] && dp->key_n == N && dp->key_d == D && dp->key_h == H &&
+                         dp->key_lr == lr_over_n && std::equal(key, key + 6, dp->key);
+        if (!hit) {
+            dp->drop_graphs();
+            for (int par = 0; par < 2; par++) {
+                cudaGraph_t graph = nullptr;
+                GLX_CK(cudaStreamBeginCapture(dp->st, cudaStreamCaptureModeThreadLocal));
+                int rc = dp_epoch_enqueue(dp, g, kind, rows, Xp, part, par ? wk1 : wk0, par ? wk0 : wk1, w_ih, w_ho,
+                                          lr_over_n, nonfinite, false);
+                cudaError_t ec = cudaStreamEndCapture(dp->st, &graph);
+                if (rc) {
+                    if (graph) cudaGraphDestroy(graph);
+                    return rc;
+                }
+                GLX_CK(ec);
+                cudaError_t ei = cudaGraphInstantiate(&dp->exec[par], graph, 0);
+                cudaGraphDestroy(graph);
+                GLX_CK(ei);
+            }
+            std::copy(key, key + 6, dp->key);
+            dp->key_n = N;
+            dp->key_d = D;
+            dp->key_h = H;
+            dp->key_lr = lr_over_n;
+        }
+        for (int64_t e = 0; e < epochs; e++) {
+            GLX_CK(cudaGraphLaunch(dp->exec[e & 1], dp->st));
+            g_launches.fetch_add(per_epoch);
+            if (stats_hist)
+                GLX_CK(cudaMemcpyAsync(stats_hist + 5 * e, dp->slot.p, 5 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       dp->st));
+        }
+    } else {
+        for (int64_t e = 0; e < epochs; e++) {
+            int rc = dp_epoch_enqueue(dp, g, kind, rows, Xp, part, (e & 1) ? wk1 : wk0, (e & 1) ? wk0 : wk1, w_ih,
+                                      w_ho, lr_over_n, nonfinite, true);
+            if (rc) return rc;
+            g_launches.fetch_add(per_epoch);
+            if (stats_hist)
+                GLX_CK(cudaMemcpyAsync(stats_hist + 5 * e, dp->slot.p, 5 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       dp->st));
+        }
+    }
+    GLX_CK(cudaEventRecord(dp->ev_out, dp->st));
+    GLX_CK(cudaStreamWaitEvent(caller, dp->ev_out, 0));
+    return GLX_OK;
+}
+}  // namespace
 
 extern "C" {
 
@@ -950,6 +1089,106 @@ int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, con
         GLX_CK(perr);
         g_launches.fetch_add(4 + 5 * (uint64_t)((N + C - 1) / C));
     }
+    return GLX_OK;
+}
+
+// ------------------------------------------------------------ data parallel
+int glx_dp_unique_id(uint8_t* id128) {
+    if (!id128) return set_err(GLX_ERR_INVALID, "id buffer is NULL");
+    ncclUniqueId id;
+    GLX_NCCL(ncclGetUniqueId(&id));
+    static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
+    memcpy(id128, &id, sizeof(id));
+    return GLX_OK;
+}
+
+int glx_dp_init(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id128, void** comm_out) {
+    if (!id128 || !comm_out) return set_err(GLX_ERR_INVALID, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks)
+        return set_err(GLX_ERR_INVALID, "rank %d of %d out of range", rank, nranks);
+    GLX_CK(cudaSetDevice(device));
+    DpComm* dp = new DpComm();
+    dp->dev = device;
+    dp->nranks = nranks;
+    dp->rank = rank;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&dp->comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        delete dp;
+        return set_err(GLX_ERR_CUDA, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+    }
+    GLX_CK(cudaStreamCreateWithFlags(&dp->st, cudaStreamNonBlocking));
+    GLX_CK(cudaEventCreateWithFlags(&dp->ev_in, cudaEventDisableTiming));
+    GLX_CK(cudaEventCreateWithFlags(&dp->ev_out, cudaEventDisableTiming));
+    *comm_out = dp;
+    return GLX_OK;
+}
+
+int glx_dp_finalize(void* comm) {
+    DpComm* dp = (DpComm*)comm;
+    if (!dp) return GLX_OK;
+    cudaSetDevice(dp->dev);
+    cudaStreamSynchronize(dp->st);
+    dp->drop_graphs();
+    ncclResult_t r = ncclCommDestroy(dp->comm);
+    cudaEventDestroy(dp->ev_in);
+    cudaEventDestroy(dp->ev_out);
+    cudaStreamDestroy(dp->st);
+    if (dp->grad.p) cudaFree(dp->grad.p);
+    if (dp->slot.p) cudaFree(dp->slot.p);
+    delete dp;
+    if (r != ncclSuccess) return set_err(GLX_ERR_CUDA, "ncclCommDestroy failed: %s", ncclGetErrorString(r));
+    return GLX_OK;
+}
+
+int glx_dp_allreduce_f64(void* comm, double* buf, int64_t n, int32_t op, void* stream) {
+    DpComm* dp = (DpComm*)comm;
+    if (!dp) return set_err(GLX_ERR_INVALID, "communicator is NULL");
+    if (n < 0 || (op != 0 && op != 1)) return set_err(GLX_ERR_INVALID, "bad count or op");
+    GLX_CK(cudaSetDevice(dp->dev));
+    GLX_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, op ? ncclMax : ncclSum, dp->comm, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_dp_train_batch(void* comm, float* w_ih, float* w_ho, const float* Xp, int64_t N, int64_t N_total, int32_t D,
+                       int32_t H, int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream) {
+    DpComm* dp = (DpComm*)comm;
+    if (!dp) return set_err(GLX_ERR_INVALID, "communicator is NULL");
+    int rc = check_dims(N, D, H);
+    if (rc) return rc;
+    if (N_total < N || N_total < 1) return set_err(GLX_ERR_SHAPE, "total rows %lld < local rows %lld",
+                                                   (long long)N_total, (long long)N);
+    if (epochs <= 0) return GLX_OK;
+    return dp_train_batch(dp, w_ih, w_ho, Xp, N, N_total, D, H, epochs, lr, stats_hist, nonfinite,
+                          (cudaStream_t)stream);
+}
+
+int glx_dp_run_train_segment_batch(void* comm, float* w_ih, float* w_ho, const float* feats, const float* targets,
+                                   int64_t rows, int64_t rows_total, int32_t input_dim, int32_t hidden_dim,
+                                   int64_t epochs, double lr, double* stats_hist, int32_t flags) {
+    DpComm* dp = (DpComm*)comm;
+    if (!dp) return set_err(GLX_ERR_INVALID, "communicator is NULL");
+    int rc = check_dims(rows, input_dim, hidden_dim);
+    if (rc) return rc;
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0, got %lld", (long long)epochs);
+    if (rows_total < rows || rows_total < 1)
+        return set_err(GLX_ERR_SHAPE, "total rows %lld < local rows %lld", (long long)rows_total, (long long)rows);
+    if (epochs == 0) return GLX_OK;
+    HOST_PROLOGUE(dp->dev);
+    const size_t n1 = (size_t)hidden_dim * (input_dim + 1), n2 = (size_t)hidden_dim + 1;
+    rc = batch_segment_dev(hs, w_ih, w_ho, feats, targets, rows, input_dim, hidden_dim, 0, lr, false, flags, st);
+    if (rc) return rc;
+    GLX_CK(hs->stats.ensure((size_t)5 * epochs * sizeof(double)));
+    rc = dp_train_batch(dp, hs->w1.as<float>(), hs->w2.as<float>(), hs->xp.as<float>(), rows, rows_total, input_dim,
+                        hidden_dim, epochs, lr, stats_hist ? hs->stats.as<double>() : nullptr, hs->flag.as<int>(), st);
+    if (rc) return rc;
+    GLX_CK(cudaMemcpyAsync(w_ih, hs->w1.p, n1 * 4, cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaMemcpyAsync(w_ho, hs->w2.p, n2 * 4, cudaMemcpyDeviceToHost, st));
+    if (stats_hist)
+        GLX_CK(cudaMemcpyAsync(stats_hist, hs->stats.p, (size_t)5 * epochs * sizeof(double), cudaMemcpyDeviceToHost,
+                               st));
+    GLX_CK(cudaStreamSynchronize(st));
     return GLX_OK;
 }
 

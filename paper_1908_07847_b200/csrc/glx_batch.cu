@@ -561,6 +561,47 @@ __global__ void batch_apply_kernel(int D, int H, float* __restrict__ W1, float* 
     if (!isfinite(wnew) && nonfinite) atomicOr(nonfinite, 1);
 }
 
+// DP epoch tail (config 4, after the all-reduce of grad): the update of
+// batch_apply_kernel plus the next epoch's pre-scaled weight copy (as
+// batch_update_kernel writes it) and the epoch statistics into stats_slot.
+__global__ void batch_dp_update_kernel(int D, int H, int DP, float* __restrict__ W1, float* __restrict__ W2,
+                                       float* __restrict__ Wk_next, const double* __restrict__ grad, double lr_over_n,
+                                       double* __restrict__ stats_slot, int* __restrict__ nonfinite) {
+    const int P1 = H * (D + 1);
+    const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+    const float kScale = (float)(-GLX_LOG2E);
+    if (idx >= P1 + H + 1) {
+        if (idx < P1 + H + 6 && stats_slot) stats_slot[idx - (P1 + H + 1)] = grad[idx];
+        return;
+    }
+    float wnew;
+    if (idx < P1) {
+        const int j = idx / (D + 1), i = idx - j * (D + 1);
+        wnew = __double2float_rn((double)W1[idx] - lr_over_n * grad[idx]);
+        W1[idx] = wnew;
+        Wk_next[j * DP + i] = kScale * wnew;
+    } else if (idx < P1 + H) {
+        const int j = idx - P1;
+        wnew = __double2float_rn((double)W2[j] - lr_over_n * grad[idx]);
+        W2[j] = wnew;
+        Wk_next[H * DP + j] = kScale * wnew;
+        Wk_next[H * DP + H + 1 + j] = wnew;
+    } else {
+        wnew = __double2float_rn((double)W2[H] - lr_over_n * grad[idx]);
+        W2[H] = wnew;
+        Wk_next[H * DP + H] = kScale * wnew;
+    }
+    if (!isfinite(wnew) && nonfinite) atomicOr(nonfinite, 1);
+}
+
+cudaError_t launch_batch_dp_update(const BatchGeom& g, float* W1, float* W2, float* Wk_next, const double* grad,
+                                   double lr_over_n, double* stats_slot, int* nonfinite, cudaStream_t st) {
+    const int n = g.P1 + g.H + 1 + 5;
+    batch_dp_update_kernel<<<(n + 255) / 256, 256, 0, st>>>(g.D, g.H, g.DP, W1, W2, Wk_next, grad, lr_over_n,
+                                                            stats_slot, nonfinite);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_batch_grad(const BatchGeom& g, const float* part, const float* Wk, double* grad, cudaStream_t st) {
     const int nidx = g.P1 + g.H + 1 + 5;
     batch_grad_kernel<<<(nidx + 31) / 32, kRedW * 32, 0, st>>>(part, g.grid, g.PS, g.D, g.H, g.DP, Wk, grad);

@@ -92,6 +92,8 @@ cudaError_t launch_batch_epoch(const BatchGeom& g, const float* Xp, const float*
                                cudaStream_t st);
 // reduce the per-CTA partials; if train, apply the SGD update to W1/W2 and
 // write the next kernel weight copy. stats (may be null): [loss, c0, c1, c2, c3]
+cudaError_t launch_batch_dp_update(const BatchGeom& g, float* W1, float* W2, float* Wk_next, const double* grad,
+                                   double lr_over_n, double* stats_slot, int* nonfinite, cudaStream_t st);
 cudaError_t launch_batch_update(const BatchGeom& g, const float* part, float* W1, float* W2, const float* Wk_cur,
                                 float* Wk_next, double lr_over_n, bool train, double* stats, int* nonfinite,
                                 cudaStream_t st);

@@ -1,17 +1,21 @@
-"""Data-parallel full-batch training over torch.distributed (configs 4 and 5).
+"""Data-parallel full-batch training (configs 2/4 across GPUs, config 5).
 
 SURVEY.md 8(e): the rows are sharded contiguously over the ranks (one
 process per GPU), every epoch each rank computes the gradient SUM of its
-shard with the fused streaming kernel (glx_batch_grad), the P-element f64
-vector (P = H(D+1) + H + 1, plus loss and confusion counts) is summed with
-one NCCL all-reduce over NVLink, and every rank applies the identical
-update W <- f32(f64(W) - lr/N_total * grad) (glx_batch_apply). Summing in
-float64 keeps 1/2/4/8-GPU results equal to ~1e-15 of each other.
+shard with the fused streaming kernel, the P-element f64 vector (P = H(D+1) +
+H + 1, plus loss and confusion counts) is summed with one NCCL all-reduce
+over NVLink, and every rank applies the identical update
+W <- f32(f64(W) - lr/N_total * grad). Summing in float64 keeps 1/2/4/8-GPU
+results equal to ~1e-15 of each other.
 
-The epoch loop is written against a small engine interface so the
-orchestration (sharding, all-reduce, update, statistics) is exercised on CPU
-with gloo and a test engine (tests/test_dp_cpu.py); DeviceEngine is the
-product engine.
+The NCCL communicator belongs to the C library (NcclComm: glx_dp_init /
+glx_dp_allreduce_f64 / glx_dp_train_batch); torch.distributed
+is only the control plane that ships the ncclUniqueId and runs barriers. The
+product epoch loop is train_data_parallel_nccl (one library call, the epoch
+captured in a CUDA graph with the all-reduce inside). train_data_parallel is
+the same loop written against a small engine interface so the orchestration
+(sharding, all-reduce, update, statistics) is exercised on CPU with gloo and a
+test engine (tests/test_dp_cpu.py), and drives the wide engine.
 """
 
 from __future__ import annotations
@@ -101,76 +105,74 @@ def train_data_parallel(engine, epochs: int, lr: float, n_total: int, all_reduce
     return stats
 
 
-# kernels of this library launched by CUDA-graph replays (the library's own
-# glx_launch_count only sees launches issued through its C entry points)
-graph_kernel_launches = 0
+class NcclComm:
+    """This rank's NCCL communicator, owned by the C library (glx_dp_init ->
+    ncclCommInitRank). Rank 0 makes the 128-byte ncclUniqueId
+    (glx_dp_unique_id) and the control group (any torch.distributed group that can
+    broadcast_object_list, e.g. gloo) ships it to the other ranks; with one rank
+    no group is needed. The data plane -- the per-epoch gradient all-reduce --
+    never goes through torch."""
+
+    def __init__(self, rank: int = 0, world_size: int = 1, device: int = 0, group=None):
+        import ctypes
+
+        self.L = _lib.load()
+        self.rank, self.world_size, self.device = rank, world_size, device
+        uid = np.zeros(128, np.uint8)
+        if rank == 0:
+            _lib.check(self.L.glx_dp_unique_id(_lib.ptr(uid)))
+        if world_size > 1:
+            import torch.distributed as dist
+
+            box = [uid.tobytes()]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = np.frombuffer(box[0], np.uint8).copy()
+        h = ctypes.c_void_p()
+        _lib.check(self.L.glx_dp_init(device, world_size, rank, _lib.ptr(uid), ctypes.byref(h)))
+        self.handle = h.value
+
+    def all_reduce(self, t, op: str = "sum", stream=None) -> None:
+        """In-place all-reduce of a float64 device tensor (sum or max)."""
+        import torch
+
+        assert t.dtype == torch.float64 and t.is_contiguous()
+        st = stream if stream is not None else torch.cuda.current_stream(t.device).cuda_stream
+        _lib.check(self.L.glx_dp_allreduce_f64(self.handle, t.data_ptr(), t.numel(), 1 if op == "max" else 0, st))
+
+    def close(self) -> None:
+        if getattr(self, "handle", None):
+            _lib.check(self.L.glx_dp_finalize(self.handle))
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
 
 
-def train_data_parallel_graph(engine, epochs: int, lr: float, n_total: int, all_reduce) -> list[EpochStats]:
-    """train_data_parallel with one epoch (gradient kernels, all-reduce, update)
-    captured in a CUDA graph and replayed, removing the per-epoch host launch
-    overhead. The graph is cached on the engine (keyed on the step size), so only
-    the first call captures. NCCL collectives are graph-capturable; if capture
-    fails the eager loop runs instead. Same arithmetic and results as
-    train_data_parallel."""
+def train_data_parallel_nccl(engine: DeviceEngine, comm: NcclComm, epochs: int, lr: float,
+                             n_total: int) -> list[EpochStats]:
+    """`epochs` data-parallel epochs in ONE library call (glx_dp_train_batch): the
+    epoch kernel over this rank's rows, the f64 gradient sum, the NCCL all-reduce
+    and the update, captured once into a CUDA graph by the library and replayed.
+    Same arithmetic as train_data_parallel with an all-reduce; returns the
+    per-epoch statistics over all ranks' rows."""
     import torch
 
     if epochs <= 0:
         return []
-    P = getattr(engine, "P", None) or engine.H * (engine.D + 1) + engine.H + 1
-    ns = getattr(engine, "n_stats", 5)
-    key = float(lr) / n_total
-    cache = getattr(engine, "_graph_cache", None)
-    if cache is None or cache[0] != key:
-        side = torch.cuda.Stream(device=engine.grad.device)
-        saved = engine.stream
-        side.wait_stream(torch.cuda.current_stream())
-        try:
-            with torch.cuda.stream(side):
-                engine.stream = side.cuda_stream
-                # one eager epoch on the capture stream: the library allocates its
-                # per-stream workspace on first use, which capture does not allow.
-                # Errors here are real (kernel / NCCL) and propagate.
-                first = train_data_parallel(engine, 1, lr, n_total, all_reduce)
-                graph = torch.cuda.CUDAGraph()
-                n0 = int(engine.L.glx_launch_count())
-                try:
-                    with torch.cuda.graph(graph, stream=side):
-                        g = engine.grad_sum()
-                        all_reduce(g)
-                        engine.apply(g, key)
-                except RuntimeError as e:  # only a refused capture falls back to eager epochs
-                    if "captur" not in str(e).lower():
-                        raise
-                    graph = None
-                per_replay = int(engine.L.glx_launch_count()) - n0
-        finally:
-            engine.stream = saved
-            torch.cuda.current_stream().wait_stream(side)
-        if graph is None:
-            return first + train_data_parallel(engine, epochs - 1, lr, n_total, all_reduce)
-        engine._graph_cache = (key, graph, side, per_replay)
-        done = first
-        epochs -= 1
-    else:
-        done = []
-    global graph_kernel_launches
-    _, graph, side, per_replay = engine._graph_cache
-    graph_kernel_launches += per_replay * epochs
-    hist = torch.zeros((max(epochs, 1), ns), dtype=torch.float64, device=engine.grad.device)
-    side.wait_stream(torch.cuda.current_stream())
-    with torch.cuda.stream(side):
-        for e in range(epochs):
-            graph.replay()
-            hist[e].copy_(engine.grad[P:P + ns])
-    torch.cuda.current_stream().wait_stream(side)
-    out = list(done)
-    for s in hist[:epochs].tolist():
-        out.append(EpochStats(float(s[0]), tuple(int(round(v)) for v in s[1:ns])))
-    return out
+    hist = torch.zeros((epochs, 5), dtype=torch.float64, device=engine.dev)
+    _lib.check(engine.L.glx_dp_train_batch(comm.handle, engine.w1.data_ptr(), engine.w2.data_ptr(),
+                                           engine.Xp.data_ptr(), engine.N, int(n_total), engine.D, engine.H,
+                                           int(epochs), float(lr), hist.data_ptr(), engine.flag.data_ptr(),
+                                           engine.stream))
+    return [EpochStats(float(s[0]), tuple(int(round(v)) for v in s[1:5])) for s in hist.tolist()]
 
 
-def nccl_all_reduce(group=None):
+def torch_all_reduce(group=None):
+    """all_reduce(tensor) over a torch.distributed group (the CPU/gloo tests' stand-in
+    for NcclComm.all_reduce)."""
     import torch.distributed as dist
 
     def _ar(t):

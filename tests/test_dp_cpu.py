@@ -68,7 +68,7 @@ def _worker(rank, world, port, out_q):
     x, t, w1, w2 = _data()
     r0, r1 = dp.shard_bounds(x.shape[0], world, rank)
     eng = NumpyEngine(x[r0:r1], t[r0:r1], w1, w2)
-    stats = dp.train_data_parallel(eng, 25, 2.0, x.shape[0], dp.nccl_all_reduce())
+    stats = dp.train_data_parallel(eng, 25, 2.0, x.shape[0], dp.torch_all_reduce())
     out_q.put((rank, eng.w1.copy(), eng.w2.copy(), [(s.loss_sum, s.counts) for s in stats]))
     dist.barrier()
     dist.destroy_process_group()
@@ -177,7 +177,7 @@ def _kworker(rank, world, port, out_q):
     x, y, w1, w2 = _kdata()
     r0, r1 = wide.shard_rows(x.shape[0], world, rank)  # 64-row aligned shards, as the wide path uses
     eng = NumpyKEngine(x[r0:r1], y[r0:r1], w1, w2, 6, 4)
-    stats = dp.train_data_parallel(eng, 10, 1.5, x.shape[0], dp.nccl_all_reduce())
+    stats = dp.train_data_parallel(eng, 10, 1.5, x.shape[0], dp.torch_all_reduce())
     out_q.put((rank, eng.w1.copy(), eng.w2.copy(), [(s.loss_sum, s.counts) for s in stats]))
     dist.barrier()
     dist.destroy_process_group()

@@ -146,61 +146,63 @@ def test_unsupported_shape_raises(gpu):
         g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, np.zeros(10, np.float32), 1, 0.1, g.cuda())
 
 
-def test_dp_path_over_nccl_one_rank(gpu):
-    """The torch.distributed NCCL all-reduce path of dp.py (world size 1) matches the fused loop."""
-    import socket
-
-    import torch
-    import torch.distributed as dist
+def test_dp_path_over_library_nccl_one_rank(gpu):
+    """The library-owned NCCL data plane (glx_dp_init, glx_dp_train_batch: epoch kernel,
+    f64 gradient, ncclAllReduce, update, captured in a CUDA graph) with one rank
+    matches the fused single-GPU loop; eager (GLX_DP_GRAPH=0) and graph replays are
+    byte-identical, including across calls (cached graphs) and the epoch statistics."""
+    import os
 
     from paper_1908_07847_b200 import dp
 
     x, l, t, net0 = _case(50_000, 33, 256, seed=2)
     fused = net0.copy()
-    g.run_train_segment_batch(fused.w_ih2d, fused.w_ho2d, x, t, 5, 0.5, g.cuda())
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
-    try:
-        eng = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
-        stats = dp.train_data_parallel(eng, 5, 0.5, x.shape[0], dp.nccl_all_reduce())
-        w1, w2 = eng.weights()
-    finally:
-        dist.destroy_process_group()
-    assert rel_err(w1, fused.w_ih) <= 1e-6 and rel_err(w2, fused.w_ho) <= 1e-6
-    assert all(sum(st.counts) == x.shape[0] for st in stats)
-
-
-def test_dp_graph_replay_equals_eager_over_nccl_one_rank(gpu):
-    """dp.train_data_parallel_graph (the epoch captured in a CUDA graph, NCCL all-reduce
-    inside) gives the same weights and statistics as the eager data-parallel loop."""
-    import socket
-
-    import torch
-    import torch.distributed as dist
-
-    from paper_1908_07847_b200 import dp
-
-    x, l, t, net0 = _case(40_000, 33, 256, seed=3)
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
-    try:
+    fstats = np.zeros((7, 5))
+    g.run_train_segment_batch(fused.w_ih2d, fused.w_ho2d, x, t, 7, 0.5, g.cuda(), fstats)
+    with dp.NcclComm(0, 1, 0) as comm:
         a = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
-        sa = dp.train_data_parallel(a, 7, 0.5, x.shape[0], dp.nccl_all_reduce())
-        b = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
-        sb = dp.train_data_parallel_graph(b, 3, 0.5, x.shape[0], dp.nccl_all_reduce())
-        sb += dp.train_data_parallel_graph(b, 4, 0.5, x.shape[0], dp.nccl_all_reduce())  # cached graph replays
-        assert getattr(b, "_graph_cache", None) is not None  # capture succeeded (no eager fallback)
-        torch.cuda.synchronize()
-        wa, wb = a.weights(), b.weights()
-    finally:
-        dist.destroy_process_group()
-    assert wa[0].tobytes() == wb[0].tobytes() and wa[1].tobytes() == wb[1].tobytes()
-    assert [(s.loss_sum, s.counts) for s in sa] == [(s.loss_sum, s.counts) for s in sb]
+        sa = dp.train_data_parallel_nccl(a, comm, 3, 0.5, x.shape[0])
+        sa += dp.train_data_parallel_nccl(a, comm, 4, 0.5, x.shape[0])  # cached graphs
+        os.environ["GLX_DP_GRAPH"] = "0"
+        try:
+            b = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
+            sb = dp.train_data_parallel_nccl(b, comm, 7, 0.5, x.shape[0])
+        finally:
+            del os.environ["GLX_DP_GRAPH"]
+        # the generic loop with the library all-reduce as its collective
+        c = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
+        sc = dp.train_data_parallel(c, 7, 0.5, x.shape[0], comm.all_reduce)
+        wa, wb, wc = a.weights(), b.weights(), c.weights()
+    assert wa[0].tobytes() == wb[0].tobytes() == wc[0].tobytes()
+    assert wa[1].tobytes() == wb[1].tobytes() == wc[1].tobytes()
+    assert [(s.loss_sum, s.counts) for s in sa] == [(s.loss_sum, s.counts) for s in sb] == \
+           [(s.loss_sum, s.counts) for s in sc]
+    assert rel_err(wa[0], fused.w_ih) <= 1e-6 and rel_err(wa[1], fused.w_ho) <= 1e-6
+    assert all(sum(st.counts) == x.shape[0] for st in sa)
+    assert np.abs(np.array([[s.loss_sum, *s.counts] for s in sa]) - fstats).max() <= 1e-6 * fstats[:, 0].max()
+
+
+def test_dp_rank_without_rows_and_host_api(gpu):
+    """A rank with no rows still joins the all-reduce (zero gradient: weights
+    unchanged when it is the only rank); the host-buffer DP entry point
+    (glx_dp_run_train_segment_batch) equals the device one."""
+    from paper_1908_07847_b200 import _lib, dp
+
+    x, l, t, net0 = _case(30_000, 33, 128, seed=4)
+    with dp.NcclComm(0, 1, 0) as comm:
+        e0 = dp.DeviceEngine(x[:0], t[:0], net0.w_ih, net0.w_ho)
+        s0 = dp.train_data_parallel_nccl(e0, comm, 2, 0.5, 1000)
+        w1, w2 = e0.weights()
+        assert w1.tobytes() == net0.w_ih.tobytes() and w2.tobytes() == net0.w_ho.tobytes()
+        assert all(s.loss_sum == 0 and sum(s.counts) == 0 for s in s0)
+        dev = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho)
+        dp.train_data_parallel_nccl(dev, comm, 5, 0.3, x.shape[0])
+        host = net0.copy()
+        st = np.zeros((5, 5))
+        L = _lib.load()
+        _lib.check(L.glx_dp_run_train_segment_batch(comm.handle, _lib.ptr(host.w_ih), _lib.ptr(host.w_ho),
+                                                     _lib.ptr(x), _lib.ptr(t), x.shape[0], x.shape[0], 33, 128, 5,
+                                                     0.3, _lib.ptr(st), 0))
+        v1, v2 = dev.weights()
+    assert host.w_ih.tobytes() == v1.tobytes() and host.w_ho.tobytes() == v2.tobytes()
+    assert (st[:, 1:].sum(axis=1) == x.shape[0]).all()

@@ -115,12 +115,9 @@ def test_wide_dp_split_equals_fused(gpu):
     assert rel_err(a1, fused1) <= 1e-6 and rel_err(a2, fused2) <= 1e-6
 
 
-def test_wide_dp_over_nccl_one_rank(gpu):
-    import socket
-
-    import torch
-    import torch.distributed as dist
-
+def test_wide_dp_over_library_nccl_one_rank(gpu):
+    """The wide engine's data-parallel loop with the library's NCCL all-reduce
+    (glx_dp_allreduce_f64) as the collective, one rank, equals the fused epochs."""
     from conftest import rel_err
     from paper_1908_07847_b200 import dp, wide
 
@@ -129,18 +126,10 @@ def test_wide_dp_over_nccl_one_rank(gpu):
     data = wide.WideData(N, seed=9)
     st = np.zeros((epochs, 3))
     f1, f2 = wide.train_wide(data, w1, w2, epochs, lr, st)
-    s = socket.socket()
-    s.bind(("127.0.0.1", 0))
-    port = s.getsockname()[1]
-    s.close()
-    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                            device_id=torch.device("cuda", 0))
-    try:
+    with dp.NcclComm(0, 1, 0) as comm:
         eng = wide.WideEngine(data, w1, w2)
-        stats = dp.train_data_parallel(eng, epochs, lr, N, dp.nccl_all_reduce())
+        stats = dp.train_data_parallel(eng, epochs, lr, N, comm.all_reduce)
         g1, g2 = eng.weights()
-    finally:
-        dist.destroy_process_group()
     assert rel_err(g1, f1) <= 1e-7 and rel_err(g2, f2) <= 1e-7
     for s_, row in zip(stats, st):
         assert s_.counts == (int(row[1]), int(row[2]))
