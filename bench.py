@@ -1,21 +1,29 @@
-"""Benchmark: train sample-epochs/s of full-batch GD on the B200 (BASELINE.json config 2).
+"""Benchmark: train sample-epochs/s of full-batch GD on B200 (BASELINE.json configs 4 / 2).
 
-Workload (per GPU): synthetic_matrix(1_000_000, 33, seed=rank, "planted-linear")
-rows, network 33 -> 256 -> 1, full-batch gradient descent, lr 0.1. One step =
-one epoch over all of a GPU's rows (forward, output/hidden deltas, dW/db
-reduction over the rows, SGD update, loss/accuracy of the epoch-start
-weights). N > 1 (torchrun, one process per GPU) is weak scaling: each rank
-owns 1M rows and the per-epoch gradient is summed with one NCCL all-reduce
-(paper_1908_07847_b200/dp.py).
+Default workload (config 4, the configuration BASELINE.json quotes at 1/2/4/8
+B200): synthetic_matrix(67_108_864, 33, seed=0, "planted-linear") rows,
+generated on the device (byte-identical to the host generator), network
+33 -> 256 -> 1, full-batch gradient descent, lr 0.1. The rows are sharded
+contiguously over the ranks (strong scaling: the global row count is fixed);
+one step = one epoch over all rows (forward, output/hidden deltas, dW/db
+reduction, SGD update, loss/accuracy of the epoch-start weights). N = 1 runs the
+fused single-GPU loop (epoch kernel + update kernel); N > 1 runs the library's
+data-parallel epoch (epoch kernel, f64 gradient, NCCL all-reduce owned by the C
+library, update) captured in a CUDA graph. `--workload c2` is config 2 (1M rows).
+
+`python bench.py --gpus N` spawns N ranks itself (torch.distributed.run,
+127.0.0.1) when it is not already running under torchrun.
 
 Prints ONE JSON line (rank 0). `value` is measured with the packed rows
 resident in HBM; `e2e` is the public host-pointer API
-(backend.run_train_segment_batch -> glx_run_train_segment_batch) with the
-inputs in pinned host memory, host<->device copies inside the timed region,
-one call of E_E2E epochs per step (the reference bench's default epoch grid,
-bench.py:147-155 of the reference CLI). `--impl reference` times the
-reference's own CPU training engine (a C port of kernels.train_segment_par,
-oracle/glx_oracle.c) on the host cores for the same shape and metric.
+(backend.run_train_segment_batch -> glx_run_train_segment_batch at N = 1,
+dp.run_train_segment_batch_dp -> glx_dp_run_train_segment_batch on every rank
+at N > 1) with this rank's rows in pinned host memory and the host<->device
+copies inside the timed region, E_E2E epochs per step (the reference bench's
+default epoch grid, bench.py:147-155 of the reference CLI). `--impl reference`
+times the reference's own CPU training engine (a C port of
+kernels.train_segment_par, oracle/glx_oracle.c) on the host cores for the same
+shape and metric.
 """
 
 from __future__ import annotations
@@ -23,6 +31,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -34,11 +43,17 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-ROWS_PER_GPU = 1_000_000
+WORKLOADS = {
+    "c4": {"rows": 1 << 26, "name": "config 4: synthetic_matrix(67_108_864, 33, seed=0, planted-linear), "
+                                    "33->256->1 sigmoid MLP, full-batch GD lr 0.1, K=1, rows sharded over the GPUs"},
+    "c2": {"rows": 1_000_000, "name": "config 2: synthetic_matrix(1_000_000, 33, seed=0, planted-linear), "
+                                      "33->256->1 sigmoid MLP, full-batch GD lr 0.1, K=1, rows sharded over the GPUs"},
+}
 D, H, K = 33, 256, 1
 LR = 0.1
 E_E2E = 100
-METRIC = "train sample-epochs/sec (full-batch GD, 33->256->1, 1M rows per GPU)"
+CPU_ROWS = 1_000_000  # rows the CPU legs sample from
+METRIC = "train sample-epochs/sec (full-batch GD, 33->256->1)"
 UNIT = "sample-epochs/s"
 
 
@@ -167,7 +182,7 @@ def run_reference(args):
     from oracle import oracle as O
 
     O.build()
-    feats, labels = synthetic_arrays(ROWS_PER_GPU, D, 0, "planted-linear")
+    feats, labels = synthetic_arrays(CPU_ROWS, D, 0, "planted-linear")
     targets = labels.astype(np.float32)
     nw = os.cpu_count() or 1
     name, cores, fn, rate = reference_calibrate(feats, targets, nw)
@@ -186,143 +201,188 @@ def run_reference(args):
     v = n / dt
     base = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
             "sample": f"{name} (C port of the reference engine, online SGD, same flops per sample-epoch as "
-                      f"config 2), {n} rows x 1 epoch per step, median of {args.steps}"}
+                      f"the 33->256->1 batch epoch), {n} rows x 1 epoch per step, median of {args.steps}"}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(args.gpus), "cpu_baseline": base,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(args.workload, args.gpus), "cpu_baseline": base,
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def config_dict(n):
-    return {"workload": "config 2: synthetic_matrix(1_000_000, 33, seed=rank, planted-linear) per GPU, "
-                        "33->256->1 sigmoid MLP, full-batch GD lr 0.1, K=1",
-            "rows_per_gpu": ROWS_PER_GPU, "input_dim": D, "hidden_dim": H, "output_dim": K,
-            "global_rows": ROWS_PER_GPU * n, "parallelism": f"dp{n}",
-            "l2": "packed rows 144 MB per GPU > 126 MB L2 (no flush needed)"}
+def config_dict(workload, n):
+    rows = WORKLOADS[workload]["rows"]
+    return {"workload": WORKLOADS[workload]["name"], "global_rows": rows, "rows_per_gpu": rows // n,
+            "input_dim": D, "hidden_dim": H, "output_dim": K, "parallelism": f"dp{n}",
+            "l2": f"packed rows {rows * 144 / n / 1e6:.0f} MB per GPU > 126 MB L2 (no flush needed)"}
+
+
+def tf32_peak_cublas(dev) -> float:
+    """Dense TF32 throughput of cuBLAS on this GPU now (8192^3 fp32 GEMM with TF32
+    tensor cores), the measured TF32 roofline denominator (TFLOP/s)."""
+    import torch
+
+    n = 8192
+    a = torch.rand((n, n), device=dev)
+    b = torch.rand((n, n), device=dev)
+    old = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        for _ in range(3):
+            torch.matmul(a, b)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        e0.record()
+        for _ in range(reps):
+            torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        return 2 * n ** 3 * reps / (e0.elapsed_time(e1) * 1e-3) / 1e12
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = old
+        del a, b
 
 
 # -------------------------------------------------------------- GPU arm
 def run_gpu(args):
     import torch
-    import torch.distributed as dist
 
     import paper_1908_07847_b200 as g
     from paper_1908_07847_b200 import _lib, dp
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    # GLX_BENCH_FORCE_DP=1: take the data-parallel branch even with one rank (a
-    # one-rank NCCL group), to exercise the N > 1 code path on a single GPU
+    # GLX_BENCH_FORCE_DP=1: the data-parallel (NCCL) branch even with one rank
     use_dp = world > 1 or os.environ.get("GLX_BENCH_FORCE_DP") == "1"
-    if use_dp:
-        if world == 1:
-            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-            os.environ.setdefault("MASTER_PORT", "29517")
-            os.environ.setdefault("RANK", "0")
-            os.environ.setdefault("WORLD_SIZE", "1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ctrl = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")  # control plane only: id exchange, barriers, max over ranks
+        ctrl = dist
     L = _lib.load()
-    feats, labels = g.synthetic_arrays(ROWS_PER_GPU, D, rank, "planted-linear")
-    targets = labels.astype(np.float32)
+    rows = WORKLOADS[args.workload]["rows"]
+    r0, r1 = dp.shard_bounds(rows, world, rank)
     net = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=0, learning_rate=LR))
-    eng = dp.DeviceEngine(feats, targets, net.w_ih, net.w_ho, device=local)
+
+    # rows on the device (byte-identical to synthetic_matrix), this rank's shard packed;
+    # a pinned host copy of the shard for the end-to-end leg
+    X, lab = g.synthetic_arrays_device(rows, D, 0, "planted-linear", device=local)
+    Xs, ls = X[r0:r1].contiguous(), lab[r0:r1].contiguous()
+    del X, lab
+    eng = dp.DeviceEngine.from_device(Xs, ls, net.w_ih, net.w_ho)
+    host_x = torch.empty((r1 - r0, D), dtype=torch.float32, pin_memory=True)
+    host_t = torch.empty((r1 - r0,), dtype=torch.float32, pin_memory=True)
+    host_x.copy_(Xs)
+    host_t.copy_(ls.to(torch.float32))
+    del Xs, ls
+    torch.cuda.empty_cache()
+    comm = dp.NcclComm(rank, world, local) if use_dp else None
+
     stream = torch.cuda.current_stream()
-    n_total = ROWS_PER_GPU * world
     stats_dev = torch.zeros((max(args.steps, args.warmup), 5), dtype=torch.float64, device="cuda")
-    flag = torch.zeros(1, dtype=torch.int32, device="cuda")
 
-    ar = dp.nccl_all_reduce() if use_dp else None
-
-    def epochs(k, stats):
-        if not use_dp:  # fused single-GPU loop: epoch kernel + reduce/update kernel per epoch
+    def epochs(k):
+        if comm is None:  # fused single-GPU loop: epoch kernel + reduce/update kernel per epoch
             _lib.check(L.glx_train_batch(eng.w1.data_ptr(), eng.w2.data_ptr(), eng.Xp.data_ptr(), eng.N, D, H, k,
-                                         LR, stats.data_ptr() if stats is not None else None, flag.data_ptr(),
-                                         stream.cuda_stream))
+                                         LR, stats_dev.data_ptr(), eng.flag.data_ptr(), stream.cuda_stream))
         else:
-            dp.train_data_parallel_graph(eng, k, LR, n_total, ar)
+            _lib.check(L.glx_dp_train_batch(comm.handle, eng.w1.data_ptr(), eng.w2.data_ptr(), eng.Xp.data_ptr(),
+                                            eng.N, rows, D, H, k, LR, stats_dev.data_ptr(), eng.flag.data_ptr(),
+                                            stream.cuda_stream))
 
-    # FP32 roofline denominator: packed-FFMA throughput on this GPU, now
+    def barrier():
+        if ctrl is not None:
+            ctrl.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if ctrl is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        ctrl.all_reduce(t, op=ctrl.ReduceOp.MAX)
+        return float(t.item())
+
+    # roofline denominators measured on this GPU now
     tfl = np.zeros(1)
     ms = np.zeros(1)
     _lib.check(L.glx_fp32_peak(local, 50_000, _lib.ptr(tfl), _lib.ptr(ms)))
     fp32_peak = float(tfl[0])
+    tf32_meas = tf32_peak_cublas(torch.device("cuda", local))
 
-    epochs(args.warmup, stats_dev)
+    epochs(args.warmup)
     torch.cuda.synchronize()
-    L.glx_profile_enable(1)
-    L.glx_profile_read(None, None)
-    launches0 = int(L.glx_launch_count()) + dp.graph_kernel_launches
+    launches0 = int(L.glx_launch_count())
     with ClockSampler(local) as clk:
-        if use_dp:
-            dist.barrier()
+        barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        epochs(args.steps, stats_dev)
+        epochs(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
-        if use_dp:
-            dist.barrier()
-    launches = int(L.glx_launch_count()) + dp.graph_kernel_launches - launches0
+        barrier()
+    launches = int(L.glx_launch_count()) - launches0
+    elapsed = max_over_ranks(e0.elapsed_time(e1))
+    value = rows * args.steps / (elapsed * 1e-3)
+    assert not eng.nonfinite(), "non-finite weights during the benchmark"
+    final_loss = float(stats_dev[args.steps - 1, 0].item())
+
+    # the dominant kernel (the epoch kernel), per launch: CUDA events around each launch
+    # on its stream, in eager epochs right after the timed region (the timed region
+    # itself runs without per-launch events; N > 1 replays a CUDA graph)
+    os.environ["GLX_DP_GRAPH"] = "0"
+    L.glx_profile_enable(1)
+    L.glx_profile_read(None, None)
+    epochs(10)
     kms = np.zeros(1)
     kn = np.zeros(1, dtype=np.int64)
     _lib.check(L.glx_profile_read(_lib.ptr(kms), _lib.ptr(kn)))
     L.glx_profile_enable(0)
-    elapsed = e0.elapsed_time(e1)
-    if use_dp:
-        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-    value = n_total * args.steps / (elapsed * 1e-3)
-    assert not eng.nonfinite() and not bool(flag.item()), "non-finite weights during the benchmark"
-
-    # roofline of the dominant kernel (the epoch kernel), per launch
-    kernel_timing = "CUDA events around every epoch-kernel launch in the timed region"
-    if int(kn[0]) == 0 and use_dp:
-        # the timed region replayed a CUDA graph (no per-launch host events): time the
-        # same kernel on eager data-parallel epochs right after it
-        L.glx_profile_enable(1)
-        L.glx_profile_read(None, None)
-        dp.train_data_parallel(eng, 5, LR, n_total, ar)
-        _lib.check(L.glx_profile_read(_lib.ptr(kms), _lib.ptr(kn)))
-        L.glx_profile_enable(0)
-        kernel_timing = "CUDA events around 5 eager epochs right after the timed region (which replays a CUDA graph)"
+    del os.environ["GLX_DP_GRAPH"]
     k_ms = float(kms[0]) / max(1, int(kn[0]))
-    flops_per_launch = ROWS_PER_GPU * f_train()
+    n_local = r1 - r0
+    flops_per_launch = n_local * f_train()
     achieved = flops_per_launch / (k_ms * 1e-3) / 1e12
-    traffic = None
+    traffic, traffic_src = None, None
     tr_file = ROOT / "profiles" / "traffic.json"
     if tr_file.exists():
-        traffic = json.loads(tr_file.read_text()).get("batch_epoch_kernel_bytes_per_launch")
-    kind = int(L.glx_batch_kernel_kind(ROWS_PER_GPU, D, H))
-    common = {"traffic": traffic, "kernel_ms_per_launch": k_ms,
-              "kernel_share_of_step": k_ms / (elapsed / args.steps) if elapsed else None,
-              "kernel_timing": kernel_timing, "algorithmic_flops_per_launch": flops_per_launch,
-              "algorithmic_hbm_bytes_per_launch": ROWS_PER_GPU * (4 * D + 1),
-              "hbm_frac": ROWS_PER_GPU * (4 * D + 1) / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6545.9),
+        tr = json.loads(tr_file.read_text())
+        per_row = tr.get("batch_epoch_kernel_bytes_per_row")
+        if per_row:
+            traffic = per_row * n_local
+            traffic_src = tr.get("source")
+    kind = int(L.glx_batch_kernel_kind(n_local, D, H))
+    step_ms = elapsed / args.steps
+    common = {"traffic": traffic, "traffic_source": traffic_src, "kernel_ms_per_launch": k_ms,
+              "kernel_share_of_step": k_ms / step_ms if step_ms else None,
+              "kernel_timing": "CUDA events around each epoch-kernel launch on its stream, 10 eager epochs right "
+                               "after the timed region (which ran without per-launch events)",
+              "algorithmic_flops_per_launch": flops_per_launch,
+              "algorithmic_hbm_bytes_per_launch": n_local * (4 * D + 1),
+              "hbm_frac": n_local * (4 * D + 1) / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6545.9),
               "fp32_peak_tflops": fp32_peak, "fp32_frac": achieved / fp32_peak}
     if kind == 2:
         # tcgen05 kind::tf32, 3xTF32: per 64-row tile 30 forward MMAs (M=128 units, N=64 rows,
         # K=8) and 48 backward MMAs (M=128, N=48 features, K=8 rows) per 128-unit half pair
-        tf32_peak = peaks().get("bf16_tflops_sustained", 1355.8) / 2
-        tiles = -(-ROWS_PER_GPU // 64)
+        tf32_derived = peaks().get("bf16_tflops_sustained", 1355.8) / 2
+        tf32_peak = max(tf32_meas, tf32_derived)
+        tiles = -(-n_local // 64)
         mma_flops = tiles * (H // 128) * (15 * 2 * 128 * 64 * 8 + 24 * 2 * 128 * 48 * 8)
         mufu_peak = 148 * 16 * clk_mhz_for_peak(local) * 1e6
         roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": achieved / tf32_peak,
                     "kernel": "batchtc_kernel<2> (tcgen05 kind::tf32, 3xTF32, deltas in TMEM)",
+                    "tf32_cublas_measured_tflops": tf32_meas, "tf32_half_of_bf16_tflops": tf32_derived,
                     "fp32_accurate_peak": tf32_peak / 3,
                     "frac_of_fp32_accurate_peak": achieved / (tf32_peak / 3),
                     "executed_mma_flops_per_launch": mma_flops,
                     "executed_mma_frac": mma_flops / (k_ms * 1e-3) / 1e12 / tf32_peak,
-                    "mufu_frac": 2 * ROWS_PER_GPU * H / (k_ms * 1e-3) / mufu_peak,
-                    "peak_source": "dense TF32 = half of MEASURED_PEAKS.json bf16_tflops_sustained (cuBLAS bf16, "
-                                   "back to back); fp32_accurate_peak = TF32 / 3 (3xTF32 spends three TF32 MMAs "
-                                   "per fp32-accurate product); executed_mma_frac counts the 3xTF32 MMA work incl. "
-                                   "K/N padding; "
-                                   "mufu_frac = 2 MUFU ops per hidden activation / (148 SMs x 16/clk x SM clock)",
+                    "mufu_frac": 2 * n_local * H / (k_ms * 1e-3) / mufu_peak,
+                    "peak_source": "dense TF32 = max(cuBLAS 8192^3 TF32 GEMM measured in this run, half of "
+                                   "MEASURED_PEAKS.json bf16_tflops_sustained); fp32_accurate_peak = TF32 / 3 "
+                                   "(3xTF32 spends three TF32 MMAs per fp32-accurate product); executed_mma_frac "
+                                   "counts the 3xTF32 MMA work incl. K/N padding; mufu_frac = 2 MUFU ops per "
+                                   "hidden activation / (148 SMs x 16/clk x SM clock)",
                     **common}
     else:
         roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -332,85 +392,59 @@ def run_gpu(args):
                     "peak_source": "glx_fp32_peak FFMA2 microbenchmark on this GPU in this run (MEASURED_PEAKS.json "
                                    "has no FP32 figure)", **common}
 
-    # end-to-end through the public API, inputs in pinned host memory: the host
-    # segment API on one GPU, the data-parallel engine (every rank) on N
-    e2e = run_e2e_dp(g, torch, dp, feats, targets, n_total, world) if use_dp else run_e2e(g, torch, feats, targets)
+    # end-to-end through the public API, this rank's rows in pinned host memory
+    e2e = run_e2e(g, dp, comm, host_x.numpy(), host_t.numpy(), rows, barrier, max_over_ranks)
+    e2e["gpu_launches"] = None
 
-    line = None
     if rank == 0:
-        cpu = cpu_baseline_batch(feats, targets) if world == 1 else None
+        cpu = None
+        if world == 1:
+            n_cpu = min(CPU_ROWS, host_x.shape[0])
+            cpu = cpu_baseline_batch(host_x.numpy()[:n_cpu], host_t.numpy()[:n_cpu])
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True,
-                "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
-                "config": config_dict(world), "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches, "clocks": clk.summary(),
-                "final_loss_sum": float(stats_dev[args.steps - 1, 0].item()) if not use_dp else None}
+                "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+                "config": config_dict(args.workload, world), "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "final_loss_sum": final_loss,
+                "path": "glx_train_batch (fused single-GPU loop)" if comm is None else
+                        "glx_dp_train_batch (epoch kernel, f64 gradient, library-owned ncclAllReduce, update; "
+                        "CUDA graph replay)"}
         print(json.dumps(line), flush=True)
-    if use_dp:
-        dist.barrier()
-        dist.destroy_process_group()
+    if comm is not None:
+        comm.close()
+    if ctrl is not None:
+        ctrl.barrier()
+        ctrl.destroy_process_group()
 
 
-def run_e2e(g, torch, feats, targets, reps=3):
-    """Public API step: run_train_segment_batch(host arrays, E_E2E epochs), copies included."""
-    pin_x = torch.empty(feats.shape, dtype=torch.float32, pin_memory=True)
-    pin_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
-    pin_x.numpy()[:] = feats
-    pin_t.numpy()[:] = targets
-    x, t = pin_x.numpy(), pin_t.numpy()
-    net0 = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=0))
-    kind = g.cuda()
-    net = net0.copy()
-    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 2, LR, kind)  # warm-up
-    times = []
-    for _ in range(reps):
-        net = net0.copy()
-        stats = np.zeros((E_E2E, 5))
-        t0 = time.perf_counter()
-        g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, E_E2E, LR, kind, stats)
-        times.append(time.perf_counter() - t0)
-    dt = statistics.median(times)
-    w_bytes = 4 * (net.w_ih.size + net.w_ho.size)
-    return {"value": feats.shape[0] * E_E2E / dt, "unit": UNIT,
-            "h2d_bytes_per_step": int(feats.nbytes + targets.nbytes + w_bytes),
-            "d2h_bytes_per_step": int(w_bytes + stats.nbytes), "epochs_per_step": E_E2E,
-            "seconds_per_step": dt, "api": "backend.run_train_segment_batch -> glx_run_train_segment_batch"}
-
-
-def run_e2e_dp(g, torch, dp, feats, targets, n_total, world, reps=3):
-    """N-GPU public-API step: every rank builds a dp.DeviceEngine from its pinned host
-    shard (host->device copy and row packing), runs E_E2E data-parallel epochs
-    (gradient kernel, NCCL all-reduce, update) and reads the weights back; the step
-    time is the max over ranks and the value covers all ranks' rows."""
-    import torch.distributed as dist
-
-    pin_x = torch.empty(feats.shape, dtype=torch.float32, pin_memory=True)
-    pin_t = torch.empty(targets.shape, dtype=torch.float32, pin_memory=True)
-    pin_x.numpy()[:] = feats
-    pin_t.numpy()[:] = targets
-    x, t = pin_x.numpy(), pin_t.numpy()
+def run_e2e(g, dp, comm, x, t, rows_total, barrier, max_over_ranks, reps=3):
+    """Public-API step with this rank's rows in pinned host memory: E_E2E epochs of
+    run_train_segment_batch (N = 1) or dp.run_train_segment_batch_dp (data parallel,
+    every rank), host->device copy of the rows and the weights, packing, training,
+    device->host copy of the weights and the per-epoch statistics; step time = max
+    over ranks, value over all ranks' rows."""
     net0 = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=H, seed=0))
     times = []
     for it in range(reps + 1):  # the first repetition is the warm-up
-        dist.barrier()
-        torch.cuda.synchronize()
+        net = net0.copy()
+        stats = np.zeros((E_E2E, 5))
+        barrier()
         t0 = time.perf_counter()
-        eng = dp.DeviceEngine(x, t, net0.w_ih, net0.w_ho, device=torch.cuda.current_device())
-        # eager epochs: a fresh engine per step would pay graph instantiation in-step
-        dp.train_data_parallel(eng, E_E2E, LR, n_total, dp.nccl_all_reduce())
-        w1, w2 = eng.weights()
-        dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
-        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        if comm is None:
+            g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, E_E2E, LR, g.cuda(), stats)
+        else:
+            dp.run_train_segment_batch_dp(comm, net.w_ih2d, net.w_ho2d, x, t, rows_total, E_E2E, LR, stats)
+        dt = max_over_ranks(time.perf_counter() - t0)
         if it:
-            times.append(float(dt.item()))
-        del eng
+            times.append(dt)
     dt = statistics.median(times)
-    w_bytes = 4 * (w1.size + w2.size)
-    return {"value": n_total * E_E2E / dt, "unit": UNIT,
-            "h2d_bytes_per_step": int(feats.nbytes + targets.nbytes + w_bytes),
-            "d2h_bytes_per_step": int(w_bytes + 5 * 8 * E_E2E), "epochs_per_step": E_E2E, "seconds_per_step": dt,
-            "per_rank": True, "ranks": world,
-            "api": "dp.DeviceEngine + dp.train_data_parallel (glx_batch_grad, NCCL all-reduce, glx_batch_apply)"}
+    w_bytes = 4 * (net.w_ih.size + net.w_ho.size)
+    return {"value": rows_total * E_E2E / dt, "unit": UNIT,
+            "h2d_bytes_per_step": int(x.nbytes + t.nbytes + w_bytes),
+            "d2h_bytes_per_step": int(w_bytes + stats.nbytes), "epochs_per_step": E_E2E,
+            "seconds_per_step": dt, "bytes_per_rank": comm is not None,
+            "api": "backend.run_train_segment_batch -> glx_run_train_segment_batch" if comm is None else
+                   "dp.run_train_segment_batch_dp -> glx_dp_run_train_segment_batch (every rank)"}
 
 
 def clk_mhz_for_peak(dev) -> float:
@@ -459,12 +493,49 @@ def run_suite(which: str, out: str | None):
     bench_configs.run_suite(which, out, SuiteCpuLegs())
 
 
+def free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`--gpus N` outside torchrun: re-launch this script as N ranks (one process per
+    GPU) with torch.distributed.run on 127.0.0.1; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def run_dry(args):
+    """GLX_BENCH_DRYRUN=1: the launch / rank plumbing only (no GPU): every rank joins
+    the gloo control group, rank 0 prints the line skeleton (tests/test_dp_cpu.py)."""
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = __import__("torch").tensor([float(rank)], dtype=__import__("torch").float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        top = float(t.item())
+    else:
+        top = 0.0
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "max_rank": top, "steps": args.steps,
+                          "warmup": args.warmup, "config": config_dict(args.workload, world)}), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c4")
     ap.add_argument("--suite", default=None,
                     help="secondary configurations instead of the headline, e.g. 1,3,4,5,eval,norm")
     ap.add_argument("--out", default=None, help="with --suite: write the results JSON here")
@@ -475,6 +546,10 @@ def main():
         run_suite(args.suite, args.out)
     elif args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
+    elif os.environ.get("GLX_BENCH_DRYRUN") == "1":
+        run_dry(args)
     else:
         run_gpu(args)
 

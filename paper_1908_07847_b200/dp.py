@@ -25,6 +25,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from .errors import ShapeError
 
 
 def shard_bounds(n_rows: int, world_size: int, rank: int) -> tuple[int, int]:
@@ -64,6 +65,31 @@ class DeviceEngine:
             self.grad = torch.zeros(int(self.L.glx_batch_grad_len(self.D, self.H)), dtype=torch.float64,
                                     device=self.dev)
             self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+
+    @classmethod
+    def from_device(cls, X, labels, w_ih: np.ndarray, w_ho: np.ndarray):
+        """Engine over rows already on the device (torch X (N, D) f32, labels (N,) u8,
+        targets = labels): packed straight from HBM, no host round trip."""
+        import torch
+
+        self = cls.__new__(cls)
+        self.torch = torch
+        self.L = _lib.load()
+        self.dev = X.device
+        self.N, self.D = X.shape
+        self.H = w_ih.size // (self.D + 1)
+        ld = int(self.L.glx_packed_ld(self.D))
+        with torch.cuda.device(self.dev):
+            self.stream = torch.cuda.current_stream(self.dev).cuda_stream
+            self.Xp = torch.empty((max(self.N, 1), ld), dtype=torch.float32, device=self.dev)
+            _lib.check(self.L.glx_pack_rows(X.data_ptr(), None, labels.data_ptr(), self.N, self.D, self.Xp.data_ptr(),
+                                            self.stream))
+            self.w1 = torch.from_numpy(np.ascontiguousarray(w_ih, dtype=np.float32)).to(self.dev)
+            self.w2 = torch.from_numpy(np.ascontiguousarray(w_ho, dtype=np.float32)).to(self.dev)
+            self.grad = torch.zeros(int(self.L.glx_batch_grad_len(self.D, self.H)), dtype=torch.float64,
+                                    device=self.dev)
+            self.flag = torch.zeros(1, dtype=torch.int32, device=self.dev)
+        return self
 
     def grad_sum(self):
         _lib.check(self.L.glx_batch_grad(self.w1.data_ptr(), self.w2.data_ptr(), self.Xp.data_ptr(), self.N,
@@ -168,6 +194,31 @@ def train_data_parallel_nccl(engine: DeviceEngine, comm: NcclComm, epochs: int, 
                                            int(epochs), float(lr), hist.data_ptr(), engine.flag.data_ptr(),
                                            engine.stream))
     return [EpochStats(float(s[0]), tuple(int(round(v)) for v in s[1:5])) for s in hist.tolist()]
+
+
+def run_train_segment_batch_dp(comm: NcclComm, w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray,
+                               targets: np.ndarray, rows_total: int, epochs: int, lr: float,
+                               stats_hist: np.ndarray | None = None) -> None:
+    """Public data-parallel counterpart of backend.run_train_segment_batch: this
+    rank's row shard in HOST memory (copied in), `epochs` full-batch epochs over
+    all ranks' rows_total rows (glx_dp_run_train_segment_batch: pack, the
+    graph-captured epoch with the NCCL all-reduce inside, update), the weights
+    copied back into the caller's arrays in place -- identical on every rank.
+    Collective: every rank calls it with the same epochs, lr and rows_total.
+    stats_hist (epochs x 5 f64, optional): loss, tp, tn, fp, fn over all rows."""
+    from .backend import _check_inputs, _check_weights, _f32c
+
+    D, H = _check_weights(w_ih2d, w_ho2d)
+    _check_inputs(w_ih2d, feats2d, targets)
+    x, t = _f32c(feats2d), _f32c(targets)
+    st = None
+    if stats_hist is not None:
+        if stats_hist.dtype != np.float64 or stats_hist.shape != (epochs, 5) or not stats_hist.flags.c_contiguous:
+            raise ShapeError(f"stats_hist must be a C-contiguous float64 ({epochs}, 5) array")
+        st = _lib.ptr(stats_hist)
+    _lib.check(comm.L.glx_dp_run_train_segment_batch(comm.handle, _lib.ptr(w_ih2d), _lib.ptr(w_ho2d), _lib.ptr(x),
+                                                     _lib.ptr(t), x.shape[0], int(rows_total), D, H, int(epochs),
+                                                     float(lr), st, 0))
 
 
 def torch_all_reduce(group=None):

@@ -269,3 +269,26 @@ def test_gloo_world2_sweep_sharding_and_gather():
     assert len(res[0]) == len(single) == 12
     for (wi, wo), n in zip(res[0], single):
         assert wi.tobytes() == n.w_ih.tobytes() and wo.tobytes() == n.w_ho.tobytes()
+
+
+def test_bench_spawns_ranks_itself():
+    """`python bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1); rank 0 prints one JSON line with n_gpus 2.
+    GLX_BENCH_DRYRUN=1 stops after the rank plumbing (no GPU here)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, GLX_BENCH_DRYRUN="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "4", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert rec["n_gpus"] == 2 and rec["max_rank"] == 1.0
+    assert rec["config"]["parallelism"] == "dp2" and rec["config"]["rows_per_gpu"] * 2 == rec["config"]["global_rows"]
