@@ -19,9 +19,9 @@ BUILD = ROOT / "build"
 LIB = PKG / "libglycemlp_cuda.so"
 SOURCES = ("glx_online.cu", "glx_batch.cu", "glx_batch3.cu", "glx_batchtc.cu", "glx_eval.cu", "glx_tc.cu", "glx_data.cu", "glx_abi.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-# NCCL: the image's libnccl.so.2 (soname-compatible with the copy torch loads, which
-# the dynamic linker reuses when torch is imported first)
-LINK = ["-L/usr/lib/x86_64-linux-gnu", "-lnccl"]
+# NCCL is bound at run time (dlopen in glx_abi.cu), so the library never pins a
+# libnccl.so.2 that could shadow the one torch loads
+LINK = ["-ldl"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v", f"-I{INCLUDE}", f"-I{CSRC}"]
 
 

@@ -100,6 +100,10 @@ def load(require_device: bool = True):
     global _lib
     with _lock:
         if _lib is None:
+            # torch first: its libnccl.so.2 must be the process's copy (the library binds
+            # NCCL at run time to whatever copy is loaded, glx_abi.cu)
+            import torch  # noqa: F401
+
             if not LIB_PATH.exists():
                 raise RuntimeError(
                     f"{LIB_PATH.name} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`"

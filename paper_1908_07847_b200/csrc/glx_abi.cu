@@ -7,6 +7,7 @@
 // gradient partials, kernel weight copies, descriptors) is cached per
 // (device, stream) and only ever grows.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -381,6 +382,48 @@ struct DpComm {
     }
 };
 
+// NCCL is bound lazily at the first glx_dp_* call (no link-time dependency):
+// the copy already loaded into the process when there is one (torch's bundled
+// libnccl, so one NCCL serves the process), else $GLX_NCCL_LIB, else the
+// image's libnccl.so.2. nccl.h supplies the types only.
+struct NcclApi {
+    decltype(&ncclGetUniqueId) GetUniqueId = nullptr;
+    decltype(&ncclCommInitRank) CommInitRank = nullptr;
+    decltype(&ncclCommDestroy) CommDestroy = nullptr;
+    decltype(&ncclAllReduce) AllReduce = nullptr;
+    decltype(&ncclGetErrorString) GetErrorString = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api = [] {
+        NcclApi a;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        const char* env = getenv("GLX_NCCL_LIB");
+        if (!h && env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("cannot load libnccl.so.2: ") + dlerror();
+            return a;
+        }
+        a.GetUniqueId = (decltype(a.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+        a.CommInitRank = (decltype(a.CommInitRank))dlsym(h, "ncclCommInitRank");
+        a.CommDestroy = (decltype(a.CommDestroy))dlsym(h, "ncclCommDestroy");
+        a.AllReduce = (decltype(a.AllReduce))dlsym(h, "ncclAllReduce");
+        a.GetErrorString = (decltype(a.GetErrorString))dlsym(h, "ncclGetErrorString");
+        a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.GetErrorString;
+        if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+        return a;
+    }();
+    return api;
+}
+
+#define GLX_NCCL_API()                                                             \
+    do {                                                                           \
+        if (!nccl().ok) return set_err(GLX_ERR_CUDA, "%s", nccl().why.c_str());    \
+    } while (0)
+
 bool dp_graphs_enabled() {  // GLX_DP_GRAPH=0: eager epochs (read per call, for A/B tests)
     const char* e = getenv("GLX_DP_GRAPH");
     return !(e && e[0] == '0');
@@ -390,7 +433,8 @@ bool dp_graphs_enabled() {  // GLX_DP_GRAPH=0: eager epochs (read per call, for 
     do {                                                                                                        \
         ncclResult_t r_ = (expr);                                                                               \
         if (r_ != ncclSuccess)                                                                                  \
-            return set_err(GLX_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, ncclGetErrorString(r_), __FILE__, __LINE__); \
+            return set_err(GLX_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, nccl().GetErrorString(r_), __FILE__,  \
+                           __LINE__);                                                                           \
     } while (0)
 
 // one epoch on dp->st: kernels of this rank's rows, the all-reduce, the update
@@ -410,7 +454,7 @@ int dp_epoch_enqueue(DpComm* dp, const BatchGeom& g, int kind, bool have_rows, c
     } else {
         GLX_CK(cudaMemsetAsync(grad, 0, glen * sizeof(double), st));
     }
-    GLX_NCCL(ncclAllReduce(grad, grad, (size_t)glen, ncclDouble, ncclSum, dp->comm, st));
+    GLX_NCCL(nccl().AllReduce(grad, grad, (size_t)glen, ncclDouble, ncclSum, dp->comm, st));
     GLX_CK(launch_batch_dp_update(g, w_ih, w_ho, wk_nxt, grad, lr_over_n, dp->slot.as<double>(), nonfinite, st));
     return GLX_OK;
 }
@@ -1095,8 +1139,9 @@ int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, con
 // ------------------------------------------------------------ data parallel
 int glx_dp_unique_id(uint8_t* id128) {
     if (!id128) return set_err(GLX_ERR_INVALID, "id buffer is NULL");
+    GLX_NCCL_API();
     ncclUniqueId id;
-    GLX_NCCL(ncclGetUniqueId(&id));
+    GLX_NCCL(nccl().GetUniqueId(&id));
     static_assert(sizeof(id) == 128, "ncclUniqueId is 128 bytes");
     memcpy(id128, &id, sizeof(id));
     return GLX_OK;
@@ -1106,6 +1151,7 @@ int glx_dp_init(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id1
     if (!id128 || !comm_out) return set_err(GLX_ERR_INVALID, "NULL argument");
     if (nranks < 1 || rank < 0 || rank >= nranks)
         return set_err(GLX_ERR_INVALID, "rank %d of %d out of range", rank, nranks);
+    GLX_NCCL_API();
     GLX_CK(cudaSetDevice(device));
     DpComm* dp = new DpComm();
     dp->dev = device;
@@ -1113,10 +1159,10 @@ int glx_dp_init(int32_t device, int32_t nranks, int32_t rank, const uint8_t* id1
     dp->rank = rank;
     ncclUniqueId id;
     memcpy(&id, id128, sizeof(id));
-    ncclResult_t r = ncclCommInitRank(&dp->comm, nranks, id, rank);
+    ncclResult_t r = nccl().CommInitRank(&dp->comm, nranks, id, rank);
     if (r != ncclSuccess) {
         delete dp;
-        return set_err(GLX_ERR_CUDA, "ncclCommInitRank failed: %s", ncclGetErrorString(r));
+        return set_err(GLX_ERR_CUDA, "ncclCommInitRank failed: %s", nccl().GetErrorString(r));
     }
     GLX_CK(cudaStreamCreateWithFlags(&dp->st, cudaStreamNonBlocking));
     GLX_CK(cudaEventCreateWithFlags(&dp->ev_in, cudaEventDisableTiming));
@@ -1131,14 +1177,14 @@ int glx_dp_finalize(void* comm) {
     cudaSetDevice(dp->dev);
     cudaStreamSynchronize(dp->st);
     dp->drop_graphs();
-    ncclResult_t r = ncclCommDestroy(dp->comm);
+    ncclResult_t r = nccl().CommDestroy(dp->comm);
     cudaEventDestroy(dp->ev_in);
     cudaEventDestroy(dp->ev_out);
     cudaStreamDestroy(dp->st);
     if (dp->grad.p) cudaFree(dp->grad.p);
     if (dp->slot.p) cudaFree(dp->slot.p);
     delete dp;
-    if (r != ncclSuccess) return set_err(GLX_ERR_CUDA, "ncclCommDestroy failed: %s", ncclGetErrorString(r));
+    if (r != ncclSuccess) return set_err(GLX_ERR_CUDA, "ncclCommDestroy failed: %s", nccl().GetErrorString(r));
     return GLX_OK;
 }
 
@@ -1147,7 +1193,7 @@ int glx_dp_allreduce_f64(void* comm, double* buf, int64_t n, int32_t op, void* s
     if (!dp) return set_err(GLX_ERR_INVALID, "communicator is NULL");
     if (n < 0 || (op != 0 && op != 1)) return set_err(GLX_ERR_INVALID, "bad count or op");
     GLX_CK(cudaSetDevice(dp->dev));
-    GLX_NCCL(ncclAllReduce(buf, buf, (size_t)n, ncclDouble, op ? ncclMax : ncclSum, dp->comm, (cudaStream_t)stream));
+    GLX_NCCL(nccl().AllReduce(buf, buf, (size_t)n, ncclDouble, op ? ncclMax : ncclSum, dp->comm, (cudaStream_t)stream));
     return GLX_OK;
 }
 

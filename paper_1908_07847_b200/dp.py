@@ -142,6 +142,8 @@ class NcclComm:
     def __init__(self, rank: int = 0, world_size: int = 1, device: int = 0, group=None):
         import ctypes
 
+        import torch  # noqa: F401  (loads torch's libnccl first: the library binds the loaded copy)
+
         self.L = _lib.load()
         self.rank, self.world_size, self.device = rank, world_size, device
         uid = np.zeros(128, np.uint8)

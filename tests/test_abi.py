@@ -51,3 +51,20 @@ def test_error_codes_map_to_reference_exceptions(built):
     assert rc == L.GLX_ERR_INVALID
     with pytest.raises(ValidationError):
         L.check(rc)
+
+
+def test_nccl_bound_at_run_time_to_the_loaded_copy(built):
+    """The library has no link-time libnccl dependency (a system libnccl loaded first
+    would shadow torch's newer one); glx_dp_unique_id binds the copy torch loaded."""
+    import subprocess
+
+    import numpy as np
+
+    ldd = subprocess.run(["ldd", str(L.LIB_PATH)], capture_output=True, text=True).stdout
+    assert "nccl" not in ldd
+    lib = L.load(require_device=False)
+    uid = np.zeros(128, np.uint8)
+    assert lib.glx_dp_unique_id(L.ptr(uid)) == 0 and uid.any()
+    maps = [l for l in open("/proc/self/maps").read().splitlines() if "libnccl" in l]
+    assert maps and all("nvidia/nccl" in l for l in maps), maps  # torch's bundled copy only
+    assert lib.glx_dp_train_batch(None, None, None, None, 10, 10, 33, 256, 1, 0.1, None, None, None) == L.GLX_ERR_INVALID
