@@ -46,17 +46,17 @@ namespace {
 constexpr int kR = 64;                      // rows per tile (forward MMA N)
 constexpr int kFC = 10;                     // 4-feature chunks of the forward operands (K = 40)
 constexpr int kNB = 48;                     // features in the backward (MMA N, multiple of 16)
-constexpr int kXF = kR / 8 * kFC * 128;     // bytes per forward x tile copy (hi or lo): [r/8][k/4][r%8][k%4]
-constexpr int kXT = kNB / 8 * kR / 4 * 128; // bytes per transposed tile copy: [k/8][r/4][k%8][r%4]
+constexpr int kXF = kR / 8 * kFC * 128;     // bytes per forward x tile (tf32): [r/8][k/4][r%8][k%4]
+constexpr int kXT = kNB / 8 * kR / 4 * 128; // bytes per transposed tile (tf32): [k/8][r/4][k%8][r%4]
 constexpr int kWT = 16 * kFC * 128;         // bytes per 128-unit weight copy (hi or lo)
-constexpr int kXFS = 2;                     // forward x stages (free once the forward MMA completes)
-constexpr int kXS = 3;                      // transposed x stages (free once the backward MMA completes)
-constexpr int kXR = 3;                      // raw x stages (TMA bulk targets)
+constexpr int kXFS = 4;                     // forward x stages (free once the forward MMA completes)
+constexpr int kXS = 4;                      // transposed x stages (free once the backward MMA completes)
+constexpr int kXR = 4;                      // raw x stages (TMA bulk targets)
 constexpr int kMaxLD = 36;
 constexpr int kRawBytes = kR * kMaxLD * 4;
 constexpr uint32_t kTf32Mask = 0xFFFFE000u;
-constexpr int kColZ = 0;     // Z^T / dh hi: buffer b at 128 b, half hf at + 64 hf
-constexpr int kColLo = 256;  // dh lo: half hf at + 64 hf
+constexpr int kZB = 3;       // Z^T buffers: the forward runs two tiles ahead of the epilogue
+constexpr int kColZ = 0;     // Z^T, then dh (tf32) in place: buffer b at 128 b, half hf at + 64 hf
 constexpr int kColW = 384;   // dW1 accumulators: half hf at + 48 hf
 constexpr uint32_t kTmemCols = 512;
 constexpr int kEpiBar = 1;
@@ -104,8 +104,8 @@ __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
     BtcSmem s{};
     s.w = 0;
     s.xf = s.w + 2 * NH * kWT;
-    s.xc = s.xf + kXFS * 2 * kXF;
-    s.raw = s.xc + kXS * 2 * kXT;
+    s.xc = s.xf + kXFS * kXF;
+    s.raw = s.xc + kXS * kXT;
     s.tgt = s.raw + kXR * kRawBytes;
     s.opart = s.tgt + kXS * kR * 4;
     s.dob = s.opart + 2 * 8 * NH * 32 * 4;  // output partials, double-buffered by tile parity
@@ -220,7 +220,10 @@ __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-__device__ __forceinline__ uint32_t tf32_hi(float v) { return __float_as_uint(v) & kTf32Mask; }
+// round-to-nearest (ties away from zero) tf32, as cvt.rna.tf32.f32: unbiased operand
+// rounding is what lets single-product terms meet the 1e-5 parity bar
+// (tools/tf32_split_error.py); the MMA ignores the 13 low bits of any operand
+__device__ __forceinline__ uint32_t tf32_rn(float v) { return (__float_as_uint(v) + 0x1000u) & kTf32Mask; }
 
 // 2^x for a pair on the FMA/ALU pipes (pass 1 is MUFU-bound): round-to-nearest by
 // the 1.5 * 2^23 magic add, degree-5 polynomial on [-1/2, 1/2] (max rel. error 2.3e-7
@@ -260,9 +263,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
     uint64_t* xc_full = xf_empty + kXFS;
     uint64_t* xc_empty = xc_full + kXS;
     uint64_t* z_full = xc_empty + kXS;
-    uint64_t* dh_ready = z_full + 2;
-    uint64_t* bwd_done = dh_ready + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bwd_done + 1);
+    uint64_t* dh_ready = z_full + kZB;
+    uint64_t* drain_bar = dh_ready + 1;  // the backward of the last tile before a dW1 drain completed
+    uint64_t* fin_bar = drain_bar + 1;   // the last backward completed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin_bar + 1);
     float* tgt = reinterpret_cast<float*>(sm + L.tgt);
     float* opart = reinterpret_cast<float*>(sm + L.opart);
     float* dob = reinterpret_cast<float*>(sm + L.dob);
@@ -284,10 +288,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             mbar_init(&xc_full[s], 2);
             mbar_init(&xc_empty[s], 1);
         }
-        mbar_init(&z_full[0], 1);
-        mbar_init(&z_full[1], 1);
+        for (int b = 0; b < kZB; b++) mbar_init(&z_full[b], 1);
         mbar_init(dh_ready, NEW);
-        mbar_init(bwd_done, 1);
+        mbar_init(drain_bar, 1);
+        mbar_init(fin_bar, 1);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -308,10 +312,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         const int hf = j >> 7, jj = j & 127;
         const int off = hf * kWT + (jj >> 3) * (kFC * 128) + q * 128 + (jj & 7) * 16;
         uint4 hi, lo;
-        hi.x = tf32_hi(v[0]);
-        hi.y = tf32_hi(v[1]);
-        hi.z = tf32_hi(v[2]);
-        hi.w = tf32_hi(v[3]);
+        hi.x = tf32_rn(v[0]);
+        hi.y = tf32_rn(v[1]);
+        hi.z = tf32_rn(v[2]);
+        hi.w = tf32_rn(v[3]);
         lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
         lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
         lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
@@ -349,68 +353,70 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             // field (shared addresses < 256 KB: no carry out of the 14-bit field)
             const uint64_t dwh = desc_ns(smem_u32(sm + L.w), 128, kFC * 128);
             const uint64_t dwl = desc_ns(smem_u32(sm + L.w + NH * kWT), 128, kFC * 128);
+            // backward of tile lt: dW1[j][k] += sum_r dh[j][r] x_r[k] (one tf32 product: the
+            // rounding errors of dh and x average out over the rows, tools/tf32_split_error.py)
             auto backward = [&](int64_t lt) {
-                const int cs = (int)(lt % kXS), zb = (int)(lt & 1);
+                const int cs = (int)(lt % kXS), zb = (int)(lt % kZB);
                 BTT(8);
                 mbar_wait(dh_ready, (uint32_t)lt & 1);
                 mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);
                 tc_fence_after();
                 BTT(9);
-                const uint64_t dth = desc_ns(smem_u32(sm + L.xc + cs * 2 * kXT), 128, kR / 4 * 128);
-                const uint64_t dtl = dth + (kXT >> 4);
+                const uint64_t dth = desc_ns(smem_u32(sm + L.xc + cs * kXT), 128, kR / 4 * 128);
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColW + 48 * hf;
-                    const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf, alo = tmem + kColLo + 64 * hf;
+                    const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf;
 #pragma unroll
                     for (int s = 0; s < kR / 8; s++) {
-                        const uint64_t bh = dth + (s * 256 >> 4);
-                        const uint64_t bl = dtl + (s * 256 >> 4);
 #if GLX_BTC_EXP == 2
-                        if (s == 0) mma_ts(d, alo + 8 * s, bh, idb, 0, el);
+                        if (s == 0) mma_ts(d, ahi, dth, idb, 0, el);
 #else
-                        mma_ts(d, alo + 8 * s, bh, idb, (lt % kDrain) != 0 || s != 0, el);
-                        mma_ts(d, ahi + 8 * s, bl, idb, 1, el);
-                        mma_ts(d, ahi + 8 * s, bh, idb, 1, el);
+                        mma_ts(d, ahi + 8 * s, dth + (s * 256 >> 4), idb, (lt % kDrain) != 0 || s != 0, el);
 #endif
                     }
                 }
                 commit(&xc_empty[cs], el);
-                commit(bwd_done, el);
+                if ((lt + 1) % kDrain == 0) commit(drain_bar, el);
+                if (lt == nt - 1) commit(fin_bar, el);
                 BTT(10);
             };
-            for (int64_t lt = 0; lt < nt; lt++) {
-                const int fs = (int)(lt % kXFS), zb = (int)(lt & 1);
+            // forward of tile lt: Z^T = W1s . x as tf32 hi(W) hi(x) + lo(W) hi(x) (the small
+            // term first); x is rounded once (the dropped hi(W) lo(x) term is unbiased)
+            auto forward = [&](int64_t lt) {
+                const int fs = (int)(lt % kXFS), zb = (int)(lt % kZB);
                 BTT(11);
                 mbar_wait(&xf_full[fs], (uint32_t)(lt / kXFS) & 1);
                 tc_fence_after();
                 BTT(12);
-                const uint64_t dxh = desc_ns(smem_u32(sm + L.xf + fs * 2 * kXF), 128, kFC * 128);
-                const uint64_t dxl = dxh + (kXF >> 4);
+                const uint64_t dx = desc_ns(smem_u32(sm + L.xf + fs * kXF), 128, kFC * 128);
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColZ + 128 * zb + 64 * hf;
                     const uint64_t wh = dwh + (hf * kWT >> 4), wl = dwl + (hf * kWT >> 4);
 #if GLX_BTC_EXP == 3
-                    mma_ss(d, wl, dxh, idf, 0, el);
+                    mma_ss(d, wh, dx, idf, 0, el);
                     if (false)
 #endif
+                    {
 #pragma unroll
-                    for (int s = 0; s < kFC / 2; s++) {
-                        mma_ss(d, wl + (s * 256 >> 4), dxh + (s * 256 >> 4), idf, s != 0, el);
-                        mma_ss(d, wh + (s * 256 >> 4), dxl + (s * 256 >> 4), idf, 1, el);
+                        for (int s = 0; s < kFC / 2; s++) mma_ss(d, wl + (s * 256 >> 4), dx + (s * 256 >> 4), idf, s != 0, el);
+#pragma unroll
+                        for (int s = 0; s < kFC / 2; s++) mma_ss(d, wh + (s * 256 >> 4), dx + (s * 256 >> 4), idf, 1, el);
                     }
-#if GLX_BTC_EXP != 3
-#pragma unroll
-                    for (int s = 0; s < kFC / 2; s++) mma_ss(d, wh + (s * 256 >> 4), dxh + (s * 256 >> 4), idf, 1, el);
-#endif
                 }
                 commit(&xf_empty[fs], el);
                 commit(&z_full[zb], el);
                 BTT(13);
-                if (lt >= 1) backward(lt - 1);
+            };
+            // Z^T is triple-buffered: forward(lt + 2) reuses the buffer of tile lt - 1, whose
+            // backward was issued (tensor-pipe order) in the previous iteration
+            forward(0);
+            if (nt > 1) forward(1);
+            for (int64_t lt = 0; lt < nt; lt++) {
+                backward(lt);
+                if (lt + 2 < nt) forward(lt + 2);
             }
-            backward(nt - 1);
         }
     } else if (warp < 4) {
         // ------------------------------------------------------------ converters
@@ -422,26 +428,21 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             const int64_t rem = a.N - row0;
             const int nr = rem < kR ? (int)rem : kR;
             const float* rawt = reinterpret_cast<const float*>(sm + L.raw + rs * kRawBytes);
-            // forward copy [r/8][k/4][r%8][k%4] (hi, lo)
+            // forward copy [r/8][k/4][r%8][k%4], tf32 (round to nearest)
             if (lt >= kXFS) mbar_wait(&xf_empty[fs], (uint32_t)((lt / kXFS) - 1) & 1);
             {
                 const float* raw = rawt + r * LD;
-                unsigned char* xh = sm + L.xf + fs * 2 * kXF + (r >> 3) * (kFC * 128) + (r & 7) * 16;
+                unsigned char* xh = sm + L.xf + fs * kXF + (r >> 3) * (kFC * 128) + (r & 7) * 16;
 #pragma unroll
                 for (int q = 0; q < kFC; q++) {
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (r < nr && 4 * q < LD) v = *reinterpret_cast<const float4*>(raw + 4 * q);
-                    uint4 hi, lo;
-                    hi.x = tf32_hi(v.x);
-                    hi.y = tf32_hi(v.y);
-                    hi.z = tf32_hi(v.z);
-                    hi.w = tf32_hi(v.w);
-                    lo.x = __float_as_uint(v.x - __uint_as_float(hi.x));
-                    lo.y = __float_as_uint(v.y - __uint_as_float(hi.y));
-                    lo.z = __float_as_uint(v.z - __uint_as_float(hi.z));
-                    lo.w = __float_as_uint(v.w - __uint_as_float(hi.w));
+                    uint4 hi;
+                    hi.x = tf32_rn(v.x);
+                    hi.y = tf32_rn(v.y);
+                    hi.z = tf32_rn(v.z);
+                    hi.w = tf32_rn(v.w);
                     *reinterpret_cast<uint4*>(xh + q * 128) = hi;
-                    *reinterpret_cast<uint4*>(xh + kXF + q * 128) = lo;
                 }
             }
             fence_proxy_async();
@@ -450,7 +451,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             // transposed copy [k/8][r/4][k%8][r%4]: one 16-byte core-matrix row (4 rows of
             // feature k) per item; 8 consecutive items fill one 128-byte core matrix
             if (lt >= kXS) mbar_wait(&xc_empty[cs], (uint32_t)((lt / kXS) - 1) & 1);
-            unsigned char* xt = sm + L.xc + cs * 2 * kXT;
+            unsigned char* xt = sm + L.xc + cs * kXT;
 #pragma unroll 4
             for (int it = r; it < kNB * kR / 4; it += 64) {
                 const int k = ((it >> 3) % (kNB / 8)) * 8 + (it & 7);
@@ -461,18 +462,13 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     const int rr = 4 * rq + i;
                     v[i] = (rr < nr && k < LD) ? rawt[rr * LD + k] : 0.f;
                 }
-                uint4 hi, lo;
-                hi.x = tf32_hi(v[0]);
-                hi.y = tf32_hi(v[1]);
-                hi.z = tf32_hi(v[2]);
-                hi.w = tf32_hi(v[3]);
-                lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
-                lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
-                lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
-                lo.w = __float_as_uint(v[3] - __uint_as_float(hi.w));
+                uint4 hi;
+                hi.x = tf32_rn(v[0]);
+                hi.y = tf32_rn(v[1]);
+                hi.z = tf32_rn(v[2]);
+                hi.w = tf32_rn(v[3]);
                 const int off = (k >> 3) * (kR / 4 * 128) + rq * 128 + (k & 7) * 16;
                 *reinterpret_cast<uint4*>(xt + off) = hi;
-                *reinterpret_cast<uint4*>(xt + kXT + off) = lo;
             }
             tgt[cs * kR + r] = (r < nr) ? rawt[r * LD + D + 1] : 0.f;
             fence_proxy_async();
@@ -521,10 +517,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         };
         float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
         for (int64_t lt = 0; lt < nt; lt++) {
-            const int cs = (int)(lt % kXS), zb = (int)(lt & 1);
+            const int cs = (int)(lt % kXS), zb = (int)(lt % kZB);
             const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
             BTT(0);
-            mbar_wait(&z_full[zb], (uint32_t)(lt >> 1) & 1);
+            mbar_wait(&z_full[zb], (uint32_t)(lt / kZB) & 1);
             mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);  // orders the converters' tgt writes
             tc_fence_after();
             BTT(1);
@@ -607,19 +603,19 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 __syncwarp();
             }
             BTT(4);
-            // the backward MMA of the previous tile still reads the single dh lo buffer
-            if (lt >= 1) {
-                mbar_wait(bwd_done, (uint32_t)(lt - 1) & 1);
+            // the backward of tile lt restarts the dW1 accumulator every kDrain tiles: add the
+            // finished partial (through the backward of tile lt - 1) into registers first
+            if (lt >= 1 && lt % kDrain == 0) {
+                mbar_wait(drain_bar, (uint32_t)((lt / kDrain) - 1) & 1);
                 tc_fence_after();
                 BTT(5);
-                if (lt % kDrain == 0) drain();  // the next backward restarts the accumulator
+                drain();
             }
             BTT(6);
-            // pass 2: dh = delta_o h (1 - h) -> TMEM as tf32 hi / lo; dW2 += delta_o h
-            const uint32_t locol = tmem + lanebase + kColLo + 64 * hf + 32 * rb;
+            // pass 2: dh = delta_o h (1 - h) -> TMEM (tf32, in place of Z); dW2 += delta_o h
 #pragma unroll
             for (int c = 0; c < 2; c++) {
-                uint32_t rh[16], rl[16];
+                uint32_t rh[16];
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
                     const int r = 16 * c + i;
@@ -628,14 +624,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     const float2 v = __fmul2_rn(d2, hp);
                     acc2 = __fadd2_rn(acc2, v);
                     const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
-                    rh[i] = tf32_hi(s2.x);
-                    rh[i + 1] = tf32_hi(s2.y);
-                    const float2 lo2 = __fadd2_rn(s2, make_float2(-__uint_as_float(rh[i]), -__uint_as_float(rh[i + 1])));
-                    rl[i] = __float_as_uint(lo2.x);
-                    rl[i + 1] = __float_as_uint(lo2.y);
+                    rh[i] = tf32_rn(s2.x);
+                    rh[i + 1] = tf32_rn(s2.y);
                 }
                 st16(zcol + 16 * c, rh);
-                st16(locol + 16 * c, rl);
             }
             tmem_st_wait();
             tc_fence_before();
@@ -644,7 +636,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             BTT(7);
         }
         // ---------------------------------------------- per-CTA partial record
-        mbar_wait(bwd_done, (uint32_t)(nt - 1) & 1);
+        mbar_wait(fin_bar, 0);
         tc_fence_after();
         drain();  // tiles since the last drain (>= 1)
         {
