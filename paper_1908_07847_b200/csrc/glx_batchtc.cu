@@ -37,6 +37,8 @@
 #include "glx_kernels.h"
 
 #include <algorithm>
+#include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 
 namespace glx {
@@ -49,14 +51,24 @@ constexpr int kNB = 48;                     // features in the backward (MMA N, 
 constexpr int kXF = kR / 8 * kFC * 128;     // bytes per forward x tile (tf32): [r/8][k/4][r%8][k%4]
 constexpr int kXT = kNB / 8 * kR / 4 * 128; // bytes per transposed tile (tf32): [k/8][r/4][k%8][r%4]
 constexpr int kWT = 16 * kFC * 128;         // bytes per 128-unit weight copy (hi or lo)
-constexpr int kXFS = 4;                     // forward x stages (free once the forward MMA completes)
-constexpr int kXS = 4;                      // transposed x stages (free once the backward MMA completes)
-constexpr int kXR = 4;                      // raw x stages (TMA bulk targets)
+// Two precisions (template FULL): FAST (large N) uses tf32(x) only, forward
+// hi(W) tf32(x) + lo(W) tf32(x), backward tf32(dh) tf32(x); FULL (small N, where
+// too few rows average the operand rounding out) is 3xTF32 on both GEMMs (x and dh
+// split into hi + lo as well), which needs the lo copies of x and a dh lo TMEM
+// buffer. Stage counts per precision (shared memory, TMEM):
+template <bool FULL>
+struct Pipe {
+    static constexpr int XFS = FULL ? 2 : 4;  // forward x stages (free once the forward MMA completes)
+    static constexpr int XS = FULL ? 3 : 4;   // transposed x stages (free once the backward MMA completes)
+    static constexpr int XR = FULL ? 3 : 4;   // raw x stages (TMA bulk targets)
+    static constexpr int ZB = FULL ? 2 : 3;   // Z^T buffers (FAST: the forward runs two tiles ahead)
+    static constexpr int NX = FULL ? 2 : 1;   // x operand copies: hi (+ lo)
+};
 constexpr int kMaxLD = 36;
 constexpr int kRawBytes = kR * kMaxLD * 4;
 constexpr uint32_t kTf32Mask = 0xFFFFE000u;
-constexpr int kZB = 3;       // Z^T buffers: the forward runs two tiles ahead of the epilogue
-constexpr int kColZ = 0;     // Z^T, then dh (tf32) in place: buffer b at 128 b, half hf at + 64 hf
+constexpr int kColZ = 0;     // Z^T, then dh (tf32 hi) in place: buffer b at 128 b, half hf at + 64 hf
+constexpr int kColLo = 256;  // FULL: dh lo, half hf at + 64 hf (Z uses buffers 0, 1)
 constexpr int kColW = 384;   // dW1 accumulators: half hf at + 48 hf
 constexpr uint32_t kTmemCols = 512;
 constexpr int kEpiBar = 1;
@@ -100,14 +112,16 @@ struct BtcSmem {  // byte offsets
 
 __host__ __device__ constexpr int btc_threads(int NH) { return (4 + 8 * NH) * 32; }
 
+template <bool FULL>
 __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
+    using P = Pipe<FULL>;
     BtcSmem s{};
     s.w = 0;
     s.xf = s.w + 2 * NH * kWT;
-    s.xc = s.xf + kXFS * kXF;
-    s.raw = s.xc + kXS * kXT;
-    s.tgt = s.raw + kXR * kRawBytes;
-    s.opart = s.tgt + kXS * kR * 4;
+    s.xc = s.xf + P::XFS * P::NX * kXF;
+    s.raw = s.xc + P::XS * P::NX * kXT;
+    s.tgt = s.raw + P::XR * kRawBytes;
+    s.opart = s.tgt + P::XS * kR * 4;
     s.dob = s.opart + 2 * 8 * NH * 32 * 4;  // output partials, double-buffered by tile parity
     s.stat = s.dob + 8 * NH * 32 * 4;  // dob: one 32-row slot per epilogue warp
     s.bars = s.stat;                   // (the row statistics reuse the partials buffer at the end)
@@ -250,10 +264,12 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <int NH>
+template <int NH, bool FULL>
 __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
     constexpr int NEW = 8 * NH;  // epilogue warps: 4 lane quadrants x NH unit halves x 2 row blocks
-    constexpr BtcSmem L = btc_smem(NH);
+    constexpr BtcSmem L = btc_smem<FULL>(NH);
+    constexpr int kXFS = Pipe<FULL>::XFS, kXS = Pipe<FULL>::XS, kXR = Pipe<FULL>::XR, kZB = Pipe<FULL>::ZB;
+    constexpr int kNX = Pipe<FULL>::NX;
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
     uint64_t* raw_full = bars;
@@ -266,7 +282,8 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
     uint64_t* dh_ready = z_full + kZB;
     uint64_t* drain_bar = dh_ready + 1;  // the backward of the last tile before a dW1 drain completed
     uint64_t* fin_bar = drain_bar + 1;   // the last backward completed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin_bar + 1);
+    uint64_t* bwd_done = fin_bar + 1;    // FULL: every backward completed (the single dh lo buffer is free)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bwd_done + 1);
     float* tgt = reinterpret_cast<float*>(sm + L.tgt);
     float* opart = reinterpret_cast<float*>(sm + L.opart);
     float* dob = reinterpret_cast<float*>(sm + L.dob);
@@ -292,6 +309,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         mbar_init(dh_ready, NEW);
         mbar_init(drain_bar, 1);
         mbar_init(fin_bar, 1);
+        mbar_init(bwd_done, 1);
         fence_mbar_init();
     }
     if (warp == 1) {
@@ -362,21 +380,30 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);
                 tc_fence_after();
                 BTT(9);
-                const uint64_t dth = desc_ns(smem_u32(sm + L.xc + cs * kXT), 128, kR / 4 * 128);
+                const uint64_t dth = desc_ns(smem_u32(sm + L.xc + cs * kNX * kXT), 128, kR / 4 * 128);
+                const uint64_t dtl = dth + (kXT >> 4);  // FULL: the lo copy follows the hi copy
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColW + 48 * hf;
-                    const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf;
+                    const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf, alo = tmem + kColLo + 64 * hf;
 #pragma unroll
                     for (int s = 0; s < kR / 8; s++) {
+                        const uint32_t acc = (lt % kDrain) != 0 || s != 0;
 #if GLX_BTC_EXP == 2
                         if (s == 0) mma_ts(d, ahi, dth, idb, 0, el);
 #else
-                        mma_ts(d, ahi + 8 * s, dth + (s * 256 >> 4), idb, (lt % kDrain) != 0 || s != 0, el);
+                        if constexpr (FULL) {
+                            mma_ts(d, alo + 8 * s, dth + (s * 256 >> 4), idb, acc, el);
+                            mma_ts(d, ahi + 8 * s, dtl + (s * 256 >> 4), idb, 1, el);
+                            mma_ts(d, ahi + 8 * s, dth + (s * 256 >> 4), idb, 1, el);
+                        } else {
+                            mma_ts(d, ahi + 8 * s, dth + (s * 256 >> 4), idb, acc, el);
+                        }
 #endif
                     }
                 }
                 commit(&xc_empty[cs], el);
+                if constexpr (FULL) commit(bwd_done, el);
                 if ((lt + 1) % kDrain == 0) commit(drain_bar, el);
                 if (lt == nt - 1) commit(fin_bar, el);
                 BTT(10);
@@ -389,7 +416,8 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 mbar_wait(&xf_full[fs], (uint32_t)(lt / kXFS) & 1);
                 tc_fence_after();
                 BTT(12);
-                const uint64_t dx = desc_ns(smem_u32(sm + L.xf + fs * kXF), 128, kFC * 128);
+                const uint64_t dx = desc_ns(smem_u32(sm + L.xf + fs * kNX * kXF), 128, kFC * 128);
+                const uint64_t dxl = dx + (kXF >> 4);  // FULL: lo copy
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColZ + 128 * zb + 64 * hf;
@@ -400,7 +428,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #endif
                     {
 #pragma unroll
-                        for (int s = 0; s < kFC / 2; s++) mma_ss(d, wl + (s * 256 >> 4), dx + (s * 256 >> 4), idf, s != 0, el);
+                        for (int s = 0; s < kFC / 2; s++) {
+                            mma_ss(d, wl + (s * 256 >> 4), dx + (s * 256 >> 4), idf, s != 0, el);
+                            if constexpr (FULL) mma_ss(d, wh + (s * 256 >> 4), dxl + (s * 256 >> 4), idf, 1, el);
+                        }
 #pragma unroll
                         for (int s = 0; s < kFC / 2; s++) mma_ss(d, wh + (s * 256 >> 4), dx + (s * 256 >> 4), idf, 1, el);
                     }
@@ -432,7 +463,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             if (lt >= kXFS) mbar_wait(&xf_empty[fs], (uint32_t)((lt / kXFS) - 1) & 1);
             {
                 const float* raw = rawt + r * LD;
-                unsigned char* xh = sm + L.xf + fs * kXF + (r >> 3) * (kFC * 128) + (r & 7) * 16;
+                unsigned char* xh = sm + L.xf + fs * kNX * kXF + (r >> 3) * (kFC * 128) + (r & 7) * 16;
 #pragma unroll
                 for (int q = 0; q < kFC; q++) {
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -443,6 +474,14 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     hi.z = tf32_rn(v.z);
                     hi.w = tf32_rn(v.w);
                     *reinterpret_cast<uint4*>(xh + q * 128) = hi;
+                    if constexpr (FULL) {
+                        uint4 lo;
+                        lo.x = __float_as_uint(v.x - __uint_as_float(hi.x));
+                        lo.y = __float_as_uint(v.y - __uint_as_float(hi.y));
+                        lo.z = __float_as_uint(v.z - __uint_as_float(hi.z));
+                        lo.w = __float_as_uint(v.w - __uint_as_float(hi.w));
+                        *reinterpret_cast<uint4*>(xh + kXF + q * 128) = lo;
+                    }
                 }
             }
             fence_proxy_async();
@@ -451,7 +490,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             // transposed copy [k/8][r/4][k%8][r%4]: one 16-byte core-matrix row (4 rows of
             // feature k) per item; 8 consecutive items fill one 128-byte core matrix
             if (lt >= kXS) mbar_wait(&xc_empty[cs], (uint32_t)((lt / kXS) - 1) & 1);
-            unsigned char* xt = sm + L.xc + cs * kXT;
+            unsigned char* xt = sm + L.xc + cs * kNX * kXT;
 #pragma unroll 4
             for (int it = r; it < kNB * kR / 4; it += 64) {
                 const int k = ((it >> 3) % (kNB / 8)) * 8 + (it & 7);
@@ -469,6 +508,14 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 hi.w = tf32_rn(v[3]);
                 const int off = (k >> 3) * (kR / 4 * 128) + rq * 128 + (k & 7) * 16;
                 *reinterpret_cast<uint4*>(xt + off) = hi;
+                if constexpr (FULL) {
+                    uint4 lo;
+                    lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
+                    lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
+                    lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
+                    lo.w = __float_as_uint(v[3] - __uint_as_float(hi.w));
+                    *reinterpret_cast<uint4*>(xt + kXT + off) = lo;
+                }
             }
             tgt[cs * kR + r] = (r < nr) ? rawt[r * LD + D + 1] : 0.f;
             fence_proxy_async();
@@ -605,6 +652,12 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             BTT(4);
             // the backward of tile lt restarts the dW1 accumulator every kDrain tiles: add the
             // finished partial (through the backward of tile lt - 1) into registers first
+            if constexpr (FULL) {  // the backward of the previous tile still reads the dh lo buffer
+                if (lt >= 1) {
+                    mbar_wait(bwd_done, (uint32_t)(lt - 1) & 1);
+                    tc_fence_after();
+                }
+            }
             if (lt >= 1 && lt % kDrain == 0) {
                 mbar_wait(drain_bar, (uint32_t)((lt / kDrain) - 1) & 1);
                 tc_fence_after();
@@ -612,10 +665,12 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 drain();
             }
             BTT(6);
-            // pass 2: dh = delta_o h (1 - h) -> TMEM (tf32, in place of Z); dW2 += delta_o h
+            // pass 2: dh = delta_o h (1 - h) -> TMEM (tf32 hi in place of Z, FULL: + lo);
+            // dW2 += delta_o h
+            const uint32_t locol = tmem + lanebase + kColLo + 64 * hf + 32 * rb;
 #pragma unroll
             for (int c = 0; c < 2; c++) {
-                uint32_t rh[16];
+                uint32_t rh[16], rl[16];
 #pragma unroll
                 for (int i = 0; i < 16; i += 2) {
                     const int r = 16 * c + i;
@@ -626,8 +681,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
                     rh[i] = tf32_rn(s2.x);
                     rh[i + 1] = tf32_rn(s2.y);
+                    if constexpr (FULL) {
+                        const float2 lo2 =
+                            __fadd2_rn(s2, make_float2(-__uint_as_float(rh[i]), -__uint_as_float(rh[i + 1])));
+                        rl[i] = __float_as_uint(lo2.x);
+                        rl[i + 1] = __float_as_uint(lo2.y);
+                    }
                 }
                 st16(zcol + 16 * c, rh);
+                if constexpr (FULL) st16(locol + 16 * c, rl);
             }
             tmem_st_wait();
             tc_fence_before();
@@ -675,6 +737,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 }
 
 int a4(int x) { return (x + 3) / 4 * 4; }
+
+// row count from which the FAST precision runs (GLX_BTC_PREC=full / fast override it,
+// read per launch for A/B tests)
+int64_t btc_full_rows() {
+    const char* e = getenv("GLX_BTC_PREC");
+    if (e && e[0] == 'f' && e[1] == 'u') return INT64_MAX;
+    if (e && e[0] == 'f' && e[1] == 'a') return 0;
+    return (int64_t)1 << 17;
+}
 #ifdef GLX_BTC_TIMING
 }  // namespace
 }  // namespace glx
@@ -707,7 +778,6 @@ bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
     g.DP = D + 1 <= 8 ? 8 : D + 1 <= 16 ? 16 : 34;
     g.LD = a4(std::max(D + 2, g.DP));
     if (g.LD > kMaxLD) return false;
-    g.MT = 0;
     g.HP = H;
     g.P1 = H * (D + 1);
     g.PS = a4(g.P1 + H + 6);
@@ -715,14 +785,17 @@ bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
     g.R = kR;
     g.ntiles = (N + kR - 1) / kR;
     g.grid = (int)std::min<int64_t>(g.ntiles, n_sms);
-    g.smem = (size_t)btc_smem(H / 128).total;
+    // FAST above btc_full_rows() rows (tests/test_gpu_batch.py: FULL keeps small row
+    // counts within 1e-5 of the oracle, where FAST's rounding has too few rows to average)
+    g.MT = N < btc_full_rows() ? 1 : 0;  // 1: FULL precision
+    g.smem = (size_t)(g.MT ? btc_smem<true>(H / 128).total : btc_smem<false>(H / 128).total);
     *out = g;
     return true;
 }
 
-template <int NH>
+template <int NH, bool FULL>
 static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t st) {
-    auto k = batchtc_kernel<NH>;
+    auto k = batchtc_kernel<NH, FULL>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e != cudaSuccess) {
         fprintf(stderr, "glx: batchtc_kernel<%d> smem=%zu: %s\n", NH, g.smem, cudaGetErrorString(e));
@@ -747,7 +820,8 @@ cudaError_t launch_batchtc_epoch(const BatchGeom& g, const float* Xp, const floa
     a.H = g.H;
     a.P1 = g.P1;
     a.PS = g.PS;
-    return g.H == 256 ? launch_btc<2>(g, a, st) : launch_btc<1>(g, a, st);
+    if (g.MT) return g.H == 256 ? launch_btc<2, true>(g, a, st) : launch_btc<1, true>(g, a, st);
+    return g.H == 256 ? launch_btc<2, false>(g, a, st) : launch_btc<1, false>(g, a, st);
 }
 
 }  // namespace glx

@@ -66,7 +66,7 @@ def epoch_grad(w1, w2, x1, t, mode, fwd_terms, bwd_terms):
     return g1, g2
 
 
-def run(rows=100_000, epochs=20, lr=0.1):
+def run(rows=100_000, epochs=20, lr=0.1, schemes=None):
     import paper_1908_07847_b200 as g
     from oracle import oracle as O
 
@@ -76,7 +76,7 @@ def run(rows=100_000, epochs=20, lr=0.1):
     net0 = g.init_weights(g.NetworkConfig(input_dim=33, hidden_dim=256, seed=3))
     ref = net0.copy()
     O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, l.astype(np.float32), epochs, lr)
-    schemes = [("trunc", "hl lh", "hl lh"), ("rn", "hl lh", "hl lh"), ("rn", "hl lh", "hl"),
+    schemes = schemes or [("trunc", "hl lh", "hl lh"), ("rn", "hl lh", "hl lh"), ("rn", "hl lh", "hl"),
                ("rn", "hl lh", "lh"), ("rn", "hl", "hl"), ("trunc", "hl lh", "hl"), ("rn", "", "hl"),
                ("rn", "hl", "")]
     for mode, ft, bt in schemes:
@@ -93,4 +93,4 @@ def run(rows=100_000, epochs=20, lr=0.1):
 
 
 if __name__ == "__main__":
-    run(*(int(a) for a in sys.argv[1:3]))
+    run(*(int(a) for a in sys.argv[1:3]), *(float(a) for a in sys.argv[3:4]))
