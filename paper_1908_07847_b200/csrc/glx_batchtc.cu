@@ -81,6 +81,9 @@ constexpr int kEpiBar = 1;
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
 constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
+#ifndef GLX_BTC_OFFSET
+#define GLX_BTC_OFFSET 1  // 0: the two row blocks start together
+#endif
 #ifndef GLX_BTC_EXP
 #define GLX_BTC_EXP 0  // diagnostic builds only: 1 no MUFU sigmoid, 2 no backward MMAs, 3 no forward MMAs
 #endif
@@ -563,6 +566,14 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             }
         };
         float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+        // The two row blocks are independent pipelines (own named barrier; they meet
+        // only at dh_ready, two tiles of slack behind the triple-buffered forward).
+        // Row block 1 starts half a tile late -- after row block 0's MUFU-bound pass 1
+        // of tile 0 -- so one block's sigmoid pass overlaps the other's shuffle / FMA
+        // phases instead of both contending for the MUFU pipe at once.
+#if GLX_BTC_OFFSET
+        if (rb == 1) bar_sync(kEpiBar + 3, NEW * 32);
+#endif
         for (int64_t lt = 0; lt < nt; lt++) {
             const int cs = (int)(lt % kXS), zb = (int)(lt % kZB);
             const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
@@ -618,6 +629,9 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 opart[(int)(lt & 1) * NEW * 32 + ew * 32 + lane] = p[0];
             }
             BTT(2);
+#if GLX_BTC_OFFSET
+            if (lt == 0 && rb == 0) bar_arrive(kEpiBar + 3, NEW * 32);
+#endif
             bar_sync(kEpiBar + rb, NEW * 16);  // the warps of this row block (they cover all units of its rows)
             BTT(3);
             {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);

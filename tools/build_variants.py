@@ -1,22 +1,34 @@
-"""Build libglycemlp_cuda.so variants with different batch-kernel knobs into variants/ (tuning only)."""
-import subprocess, sys, concurrent.futures as cf
+"""Build libglycemlp_cuda.so variants with different epoch-kernel knobs into variants/ (tuning only).
+
+    python tools/build_variants.py NAME="-DKNOB=1 ..." ...
+
+Only glx_batchtc.cu is recompiled per variant; the other objects come from build/
+(run the normal build first). Time a variant with
+GLX_LIB=variants/lib_NAME.so python tools/batch_epoch_time.py.
+"""
+import concurrent.futures as cf
+import subprocess
+import sys
 from pathlib import Path
+
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
-from paper_1908_07847_b200 import _build as B
+from paper_1908_07847_b200 import _build as B  # noqa: E402
 
 VARIANTS = {name: flags for name, flags in (a.split("=", 1) for a in sys.argv[1:])}
-out = ROOT / "variants"; out.mkdir(exist_ok=True)
+out = ROOT / "variants"
+out.mkdir(exist_ok=True)
+B.build()
+
 
 def one(name, flags):
-    objs = []
-    for src in B.SOURCES:
-        obj = out / f"{name}_{Path(src).stem}.o"
-        cmd = [B.nvcc(), *B.ARCH, *B.FLAGS, *flags.split(), "-c", str(B.CSRC / src), "-o", str(obj)]
-        subprocess.run(cmd, check=True, capture_output=True)
-        objs.append(str(obj))
-    subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(out / f"lib_{name}.so"), *objs], check=True)
+    obj = out / f"{name}_glx_batchtc.o"
+    cmd = [B.nvcc(), *B.ARCH, *B.FLAGS, *flags.split(), "-c", str(B.CSRC / "glx_batchtc.cu"), "-o", str(obj)]
+    subprocess.run(cmd, check=True, capture_output=True)
+    objs = [str(obj) if src == "glx_batchtc.cu" else str(B.BUILD / (Path(src).stem + ".o")) for src in B.SOURCES]
+    subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(out / f"lib_{name}.so"), *objs, *B.LINK], check=True)
     return name
+
 
 with cf.ThreadPoolExecutor(4) as ex:
     for n in ex.map(lambda kv: one(*kv), VARIANTS.items()):
