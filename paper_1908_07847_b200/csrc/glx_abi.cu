@@ -78,7 +78,7 @@ struct DevBuf {
 
 // scratch tied to one (device, stream): stream order serialises its reuse
 struct Workspace {
-    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm;
+    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm, tiles;
 };
 
 std::mutex g_ws_mu;
@@ -303,9 +303,24 @@ bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
     return batch_geometry(N, D, H, sm_count_current(), true, g);
 }
 
-cudaError_t launch_train_epoch(const BatchGeom& g, int kind, const float* Xp, const float* Wk, float* part,
+// what the epoch kernel reads: the packed rows (kinds 0, 1) or, for the tcgen05
+// kernel, their per-tile MMA operand layout, built here once per training call
+// into the stream's workspace (one pass over the rows)
+int epoch_input(Workspace* ws, const BatchGeom& g, int kind, const float* Xp, cudaStream_t st, const void** in) {
+    if (kind != 2) {
+        *in = Xp;
+        return GLX_OK;
+    }
+    GLX_CK(ws->tiles.ensure(batchtc_tile_bytes(g)));
+    GLX_LAUNCH(launch_batchtc_pack(g, Xp, ws->tiles.p, st));
+    *in = ws->tiles.p;
+    return GLX_OK;
+}
+
+cudaError_t launch_train_epoch(const BatchGeom& g, int kind, const void* in, const float* Wk, float* part,
                                cudaStream_t st) {
-    if (kind == 2) return launch_batchtc_epoch(g, Xp, Wk, part, st);
+    const float* Xp = (const float*)in;
+    if (kind == 2) return launch_batchtc_epoch(g, in, Wk, part, st);
     return kind == 1 ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
 }
 
@@ -322,13 +337,16 @@ int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D
     float* wk0 = ws->wk.as<float>();
     float* wk1 = wk0 + g.WKS;
     GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk1, st));
+    const void* in = nullptr;
+    int rc = epoch_input(ws, g, kind, Xp, st, &in);
+    if (rc) return rc;
     const double lr_over_n = lr / (double)N;
     for (int64_t e = 0; e < epochs; e++) {
         float* cur = (e & 1) ? wk1 : wk0;
         float* nxt = (e & 1) ? wk0 : wk1;
         cudaEvent_t pe = nullptr;
         GLX_CK(prof_begin(st, &pe));
-        GLX_LAUNCH(launch_train_epoch(g, kind, Xp, cur, ws->part.as<float>(), st));
+        GLX_LAUNCH(launch_train_epoch(g, kind, in, cur, ws->part.as<float>(), st));
         if (pe) GLX_CK(cudaEventRecord(pe, st));
         GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), w_ih, w_ho, cur, nxt, lr_over_n, true,
                                        stats_hist ? stats_hist + 5 * e : nullptr, nonfinite, st));
@@ -367,7 +385,7 @@ struct DpComm {
     DevBuf grad, slot;
     // graph cache: the captured epoch is valid for these arguments
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
-    const void* key[6] = {};
+    const void* key[7] = {};
     int64_t key_n = -1;
     int key_d = 0, key_h = 0;
     double key_lr = 0.0;
@@ -439,7 +457,7 @@ bool dp_graphs_enabled() {  // GLX_DP_GRAPH=0: eager epochs (read per call, for 
 
 // one epoch on dp->st: kernels of this rank's rows, the all-reduce, the update
 // (profile: per-launch events around the epoch kernel, eager epochs only)
-int dp_epoch_enqueue(DpComm* dp, const BatchGeom& g, int kind, bool have_rows, const float* Xp, float* part,
+int dp_epoch_enqueue(DpComm* dp, const BatchGeom& g, int kind, bool have_rows, const void* in, float* part,
                      float* wk_cur, float* wk_nxt, float* w_ih, float* w_ho, double lr_over_n, int32_t* nonfinite,
                      bool profile) {
     cudaStream_t st = dp->st;
@@ -448,7 +466,7 @@ int dp_epoch_enqueue(DpComm* dp, const BatchGeom& g, int kind, bool have_rows, c
     if (have_rows) {
         cudaEvent_t pe = nullptr;
         if (profile) GLX_CK(prof_begin(st, &pe));
-        GLX_CK(launch_train_epoch(g, kind, Xp, wk_cur, part, st));
+        GLX_CK(launch_train_epoch(g, kind, in, wk_cur, part, st));
         if (pe) GLX_CK(cudaEventRecord(pe, st));
         GLX_CK(launch_batch_grad(g, part, wk_cur, grad, st));
     } else {
@@ -479,17 +497,22 @@ int dp_train_batch(DpComm* dp, float* w_ih, float* w_ho, const float* Xp, int64_
     GLX_CK(cudaEventRecord(dp->ev_in, caller));
     GLX_CK(cudaStreamWaitEvent(dp->st, dp->ev_in, 0));
     GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk1, dp->st));
+    const void* in = Xp;
+    if (rows) {
+        int rc = epoch_input(ws, g, kind, Xp, dp->st, &in);
+        if (rc) return rc;
+    }
     const int per_epoch = rows ? 3 : 1;
     if (dp_graphs_enabled()) {
-        const void* key[6] = {w_ih, w_ho, Xp, nonfinite, ws->wk.p, ws->part.p};
+        const void* key[7] = {w_ih, w_ho, in, nonfinite, ws->wk.p, ws->part.p, dp->grad.p};
         const bool hit = dp->exec[0] && dp->key_n == N && dp->key_d == D && dp->key_h == H &&
-                         dp->key_lr == lr_over_n && std::equal(key, key + 6, dp->key);
+                         dp->key_lr == lr_over_n && std::equal(key, key + 7, dp->key);
         if (!hit) {
             dp->drop_graphs();
             for (int par = 0; par < 2; par++) {
                 cudaGraph_t graph = nullptr;
                 GLX_CK(cudaStreamBeginCapture(dp->st, cudaStreamCaptureModeThreadLocal));
-                int rc = dp_epoch_enqueue(dp, g, kind, rows, Xp, part, par ? wk1 : wk0, par ? wk0 : wk1, w_ih, w_ho,
+                int rc = dp_epoch_enqueue(dp, g, kind, rows, in, part, par ? wk1 : wk0, par ? wk0 : wk1, w_ih, w_ho,
                                           lr_over_n, nonfinite, false);
                 cudaError_t ec = cudaStreamEndCapture(dp->st, &graph);
                 if (rc) {
@@ -501,7 +524,7 @@ int dp_train_batch(DpComm* dp, float* w_ih, float* w_ho, const float* Xp, int64_
                 cudaGraphDestroy(graph);
                 GLX_CK(ei);
             }
-            std::copy(key, key + 6, dp->key);
+            std::copy(key, key + 7, dp->key);
             dp->key_n = N;
             dp->key_d = D;
             dp->key_h = H;
@@ -516,7 +539,7 @@ int dp_train_batch(DpComm* dp, float* w_ih, float* w_ho, const float* Xp, int64_
         }
     } else {
         for (int64_t e = 0; e < epochs; e++) {
-            int rc = dp_epoch_enqueue(dp, g, kind, rows, Xp, part, (e & 1) ? wk1 : wk0, (e & 1) ? wk0 : wk1, w_ih,
+            int rc = dp_epoch_enqueue(dp, g, kind, rows, in, part, (e & 1) ? wk1 : wk0, (e & 1) ? wk0 : wk1, w_ih,
                                       w_ho, lr_over_n, nonfinite, true);
             if (rc) return rc;
             g_launches.fetch_add(per_epoch);
@@ -692,9 +715,12 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
     GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
     float* wk0 = ws->wk.as<float>();
     GLX_LAUNCH(launch_batch_prep(g, w_ih, w_ho, wk0, wk0 + g.WKS, st));
+    const void* in = nullptr;
+    rc = epoch_input(ws, g, kind, Xp, st, &in);
+    if (rc) return rc;
     cudaEvent_t pe = nullptr;
     GLX_CK(prof_begin(st, &pe));
-    GLX_LAUNCH(launch_train_epoch(g, kind, Xp, wk0, ws->part.as<float>(), st));
+    GLX_LAUNCH(launch_train_epoch(g, kind, in, wk0, ws->part.as<float>(), st));
     if (pe) GLX_CK(cudaEventRecord(pe, st));
     GLX_LAUNCH(launch_batch_grad(g, ws->part.as<float>(), wk0, grad, st));
     return GLX_OK;

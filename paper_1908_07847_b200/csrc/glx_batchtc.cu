@@ -45,12 +45,22 @@ namespace glx {
 
 namespace {
 
-constexpr int kR = 64;                      // rows per tile (forward MMA N)
-constexpr int kFC = 10;                     // 4-feature chunks of the forward operands (K = 40)
-constexpr int kNB = 48;                     // features in the backward (MMA N, multiple of 16)
-constexpr int kXF = kR / 8 * kFC * 128;     // bytes per forward x tile (tf32): [r/8][k/4][r%8][k%4]
-constexpr int kXT = kNB / 8 * kR / 4 * 128; // bytes per transposed tile (tf32): [k/8][r/4][k%8][r%4]
-constexpr int kWT = 16 * kFC * 128;         // bytes per 128-unit weight copy (hi or lo)
+constexpr int kR = 64;    // rows per tile (forward MMA N)
+constexpr int kFC = 10;   // 4-feature chunks of the forward operands (K = 40)
+constexpr int kFCS = 9;   // chunks stored per tile (k < 36; chunk 9 is zero: LD <= 36)
+constexpr int kNB = 48;   // features in the backward (MMA N, multiple of 16)
+constexpr int kNBS = 40;  // feature rows stored per tile (k < 40; block 5 is zero)
+// Per 64-row tile the epoch reads the rows pre-laid-out for the MMAs (glx_tile_pack,
+// once per training call) -- tf32-rounded, no conversion inside the epoch:
+//   forward operand  [k/4][r/8][r%8][k%4]  (K-major core matrices, LBO 1024 B, SBO 128 B)
+//   backward operand [k/8][r/4][k%8][r%4]  (x transposed: K = rows; LBO 128 B, SBO 2048 B)
+// FAST stores the hi (tf32) copies, FULL also the lo copies. The target of row r
+// travels as feature D + 1 (a zero weight column), read back from the backward copy.
+constexpr int kXF = kFC * kR / 8 * 128;        // smem bytes, forward operand (10 KB)
+constexpr int kXT = kNB / 8 * kR / 4 * 128;    // smem bytes, backward operand (12 KB)
+constexpr int kXFG = kFCS * kR / 8 * 128;      // global bytes, forward operand (9 KB)
+constexpr int kXTG = kNBS / 8 * kR / 4 * 128;  // global bytes, backward operand (10 KB)
+constexpr int kWT = 16 * kFC * 128;            // bytes per 128-unit weight copy (hi or lo)
 // Two precisions (template FULL): FAST (large N) uses tf32(x) only, forward
 // hi(W) tf32(x) + lo(W) tf32(x), backward tf32(dh) tf32(x); FULL (small N, where
 // too few rows average the operand rounding out) is 3xTF32 on both GEMMs (x and dh
@@ -58,14 +68,12 @@ constexpr int kWT = 16 * kFC * 128;         // bytes per 128-unit weight copy (h
 // buffer. Stage counts per precision (shared memory, TMEM):
 template <bool FULL>
 struct Pipe {
-    static constexpr int XFS = FULL ? 2 : 4;  // forward x stages (free once the forward MMA completes)
-    static constexpr int XS = FULL ? 3 : 4;   // transposed x stages (free once the backward MMA completes)
-    static constexpr int XR = FULL ? 3 : 4;   // raw x stages (TMA bulk targets)
-    static constexpr int ZB = FULL ? 2 : 3;   // Z^T buffers (FAST: the forward runs two tiles ahead)
-    static constexpr int NX = FULL ? 2 : 1;   // x operand copies: hi (+ lo)
+    static constexpr int NX = FULL ? 2 : 1;                       // x operand copies: hi (+ lo)
+    static constexpr int STAGE = NX * (kXF + kXT);                 // smem bytes per tile stage
+    static constexpr int GTILE = NX * (kXFG + kXTG);               // global bytes per tile
+    static constexpr int S = FULL ? 3 : 6;                         // tile stages (free after the backward)
+    static constexpr int ZB = FULL ? 2 : 3;                        // Z^T buffers: the forward runs ZB tiles ahead
 };
-constexpr int kMaxLD = 36;
-constexpr int kRawBytes = kR * kMaxLD * 4;
 constexpr uint32_t kTf32Mask = 0xFFFFE000u;
 constexpr int kColZ = 0;     // Z^T, then dh (tf32 hi) in place: buffer b at 128 b, half hf at + 64 hf
 constexpr int kColLo = 256;  // FULL: dh lo, half hf at + 64 hf (Z uses buffers 0, 1)
@@ -89,10 +97,15 @@ constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
 #endif
 
 #ifdef GLX_BTC_TIMING
+// per-phase clock64 timeline of CTA 0 (diagnostic builds: tools/btc_timeline.py):
+// tiles 8..23, 16 slots per tile, for warp 4 (row block 0), warp 1 (MMA), warp 12
+// (row block 1 when NH = 2) and warp 0 (producer)
 __device__ unsigned long long g_btc_dbg[4096];
-#define BTT(slot)                                                                                      \
-    do {                                                                                               \
-        if (blockIdx.x == 0 && lane == 0 && lt >= 8 && lt < 24) g_btc_dbg[((lt - 8) * 16 + (slot)) * 2 + (warp == 4 ? 0 : 1)] = clock64(); \
+#define BTT(slot)                                                                                           \
+    do {                                                                                                    \
+        const int wi_ = warp == 4 ? 0 : warp == 1 ? 1 : warp == 12 ? 2 : warp == 0 ? 3 : -1;                \
+        if (blockIdx.x == 0 && lane == 0 && wi_ >= 0 && lt >= 8 && lt < 24)                                 \
+            g_btc_dbg[((lt - 8) * 16 + (slot)) * 4 + wi_] = clock64();                                      \
     } while (0)
 #else
 #define BTT(slot) \
@@ -101,30 +114,28 @@ __device__ unsigned long long g_btc_dbg[4096];
 #endif
 
 struct BtcArgs {
-    const float* Xp;
+    const unsigned char* tiles;  // glx_tile_pack output: ntiles x Pipe<FULL>::GTILE bytes
     const float* Wk;
     float* part;
     int64_t N, ntiles;
-    int D, DP, LD, H, P1, PS;
+    int D, DP, H, P1, PS;
 };
 
 struct BtcSmem {  // byte offsets
-    int w, xf, xc, raw, tgt, opart, dob, stat, bars;
+    int w, x, opart, dob, stat, bars;
     int total;
 };
 
-__host__ __device__ constexpr int btc_threads(int NH) { return (4 + 8 * NH) * 32; }
+// warp 0 producer, warp 1 MMA, warps 2 .. 2 + 8 NH - 1 epilogue
+__host__ __device__ constexpr int btc_threads(int NH) { return (2 + 8 * NH) * 32; }
 
 template <bool FULL>
 __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
     using P = Pipe<FULL>;
     BtcSmem s{};
     s.w = 0;
-    s.xf = s.w + 2 * NH * kWT;
-    s.xc = s.xf + P::XFS * P::NX * kXF;
-    s.raw = s.xc + P::XS * P::NX * kXT;
-    s.tgt = s.raw + P::XR * kRawBytes;
-    s.opart = s.tgt + P::XS * kR * 4;
+    s.x = s.w + 2 * NH * kWT;          // stage i at x + i * STAGE: [xf hi | xt hi (| xf lo | xt lo)]
+    s.opart = s.x + P::S * P::STAGE;
     s.dob = s.opart + 2 * 8 * NH * 32 * 4;  // output partials, double-buffered by tile parity
     s.stat = s.dob + 8 * NH * 32 * 4;  // dob: one 32-row slot per epilogue warp
     s.bars = s.stat;                   // (the row statistics reuse the partials buffer at the end)
@@ -270,43 +281,30 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 template <int NH, bool FULL>
 __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
     constexpr int NEW = 8 * NH;  // epilogue warps: 4 lane quadrants x NH unit halves x 2 row blocks
+    using P = Pipe<FULL>;
     constexpr BtcSmem L = btc_smem<FULL>(NH);
-    constexpr int kXFS = Pipe<FULL>::XFS, kXS = Pipe<FULL>::XS, kXR = Pipe<FULL>::XR, kZB = Pipe<FULL>::ZB;
-    constexpr int kNX = Pipe<FULL>::NX;
+    constexpr int kS = P::S, kZB = P::ZB;
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
-    uint64_t* raw_full = bars;
-    uint64_t* raw_empty = raw_full + kXR;
-    uint64_t* xf_full = raw_empty + kXR;
-    uint64_t* xf_empty = xf_full + kXFS;
-    uint64_t* xc_full = xf_empty + kXFS;
-    uint64_t* xc_empty = xc_full + kXS;
-    uint64_t* z_full = xc_empty + kXS;
-    uint64_t* dh_ready = z_full + kZB;
-    uint64_t* drain_bar = dh_ready + 1;  // the backward of the last tile before a dW1 drain completed
-    uint64_t* fin_bar = drain_bar + 1;   // the last backward completed
-    uint64_t* bwd_done = fin_bar + 1;    // FULL: every backward completed (the single dh lo buffer is free)
+    uint64_t* x_full = bars;                // tile stage loaded (bulk-copy bytes)
+    uint64_t* x_empty = x_full + kS;        // tile stage free (its backward completed)
+    uint64_t* z_full = x_empty + kS;        // Z^T buffer written by the forward
+    uint64_t* dh_ready = z_full + kZB;      // the epilogue wrote dh of the tile
+    uint64_t* drain_bar = dh_ready + 1;     // the backward of the last tile before a dW1 drain completed
+    uint64_t* fin_bar = drain_bar + 1;      // the last backward completed
+    uint64_t* bwd_done = fin_bar + 1;       // FULL: every backward completed (the dh lo buffer is free)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bwd_done + 1);
-    float* tgt = reinterpret_cast<float*>(sm + L.tgt);
     float* opart = reinterpret_cast<float*>(sm + L.opart);
     float* dob = reinterpret_cast<float*>(sm + L.dob);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nt = (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA (>= 1)
-    const int D = a.D, LD = a.LD, DP = a.DP;
+    const int D = a.D, DP = a.DP;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kXR; s++) {
-            mbar_init(&raw_full[s], 1);
-            mbar_init(&raw_empty[s], 2);
-        }
-        for (int s = 0; s < kXFS; s++) {
-            mbar_init(&xf_full[s], 2);
-            mbar_init(&xf_empty[s], 1);
-        }
-        for (int s = 0; s < kXS; s++) {
-            mbar_init(&xc_full[s], 2);
-            mbar_init(&xc_empty[s], 1);
+        for (int i = 0; i < kS; i++) {
+            mbar_init(&x_full[i], 1);
+            mbar_init(&x_empty[i], 1);
         }
         for (int b = 0; b < kZB; b++) mbar_init(&z_full[b], 1);
         mbar_init(dh_ready, NEW);
@@ -344,6 +342,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         *reinterpret_cast<uint4*>(sm + L.w + off) = hi;
         *reinterpret_cast<uint4*>(sm + L.w + NH * kWT + off) = lo;
     }
+    // the operand regions the bulk copies never write (forward chunk 9, backward
+    // feature block 5) stay zero for the whole launch
+    for (int i = threadIdx.x; i < kS * P::NX * (kXF - kXFG + kXT - kXTG) / 16; i += blockDim.x) {
+        const int per = (kXF - kXFG + kXT - kXTG) / 16, c = i / per, w = i - (i / per) * per;
+        const int st = c / P::NX, cp = c - st * P::NX;
+        unsigned char* base = sm + L.x + st * P::STAGE + cp * (kXF + kXT);
+        unsigned char* dst = w < (kXF - kXFG) / 16 ? base + kXFG + 16 * w : base + kXF + kXTG + 16 * (w - (kXF - kXFG) / 16);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+    }
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
@@ -354,14 +361,18 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         // ------------------------------------------------------------ producer
         if (lane == 0) {
             for (int64_t lt = 0; lt < nt; lt++) {
-                const int rs = (int)(lt % kXR);
-                if (lt >= kXR) mbar_wait(&raw_empty[rs], (uint32_t)((lt / kXR) - 1) & 1);
-                const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
-                const int64_t rem = a.N - row0;
-                const int nr = rem < kR ? (int)rem : kR;
-                const uint32_t bytes = (uint32_t)(nr * LD * 4);
-                mbar_arrive_expect_tx(&raw_full[rs], bytes);
-                bulk_g2s(sm + L.raw + rs * kRawBytes, a.Xp + row0 * LD, bytes, &raw_full[rs]);
+                const int xs = (int)(lt % kS);
+                if (lt >= kS) mbar_wait(&x_empty[xs], (uint32_t)((lt / kS) - 1) & 1);
+                BTT(14);
+                const unsigned char* src = a.tiles + (blockIdx.x + lt * gridDim.x) * (int64_t)P::GTILE;
+                unsigned char* dst = sm + L.x + xs * P::STAGE;
+                mbar_arrive_expect_tx(&x_full[xs], (uint32_t)P::GTILE);
+#pragma unroll
+                for (int cp = 0; cp < P::NX; cp++) {
+                    bulk_g2s(dst + cp * (kXF + kXT), src + cp * (kXFG + kXTG), kXFG, &x_full[xs]);
+                    bulk_g2s(dst + cp * (kXF + kXT) + kXF, src + cp * (kXFG + kXTG) + kXFG, kXTG, &x_full[xs]);
+                }
+                BTT(15);
             }
         }
     } else if (warp == 1) {
@@ -374,17 +385,18 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             // field (shared addresses < 256 KB: no carry out of the 14-bit field)
             const uint64_t dwh = desc_ns(smem_u32(sm + L.w), 128, kFC * 128);
             const uint64_t dwl = desc_ns(smem_u32(sm + L.w + NH * kWT), 128, kFC * 128);
-            // backward of tile lt: dW1[j][k] += sum_r dh[j][r] x_r[k] (one tf32 product: the
-            // rounding errors of dh and x average out over the rows, tools/tf32_split_error.py)
+            const uint64_t dx0 = desc_ns(smem_u32(sm + L.x), kR / 8 * 128, 128);
+            const uint64_t dt0 = desc_ns(smem_u32(sm + L.x + kXF), 128, kR / 4 * 128);
+            // backward of tile lt: dW1[j][k] += sum_r dh[j][r] x_r[k] (FAST: one tf32 product,
+            // the rounding of dh and x averages out over the rows, tools/tf32_split_error.py)
             auto backward = [&](int64_t lt) {
-                const int cs = (int)(lt % kXS), zb = (int)(lt % kZB);
+                const int xs = (int)(lt % kS), zb = (int)(lt % kZB);
                 BTT(8);
                 mbar_wait(dh_ready, (uint32_t)lt & 1);
-                mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);
                 tc_fence_after();
                 BTT(9);
-                const uint64_t dth = desc_ns(smem_u32(sm + L.xc + cs * kNX * kXT), 128, kR / 4 * 128);
-                const uint64_t dtl = dth + (kXT >> 4);  // FULL: the lo copy follows the hi copy
+                const uint64_t dth = dt0 + ((xs * P::STAGE) >> 4);
+                const uint64_t dtl = dth + ((kXF + kXT) >> 4);  // FULL: the lo copies follow
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColW + 48 * hf;
@@ -405,22 +417,22 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #endif
                     }
                 }
-                commit(&xc_empty[cs], el);
+                commit(&x_empty[xs], el);
                 if constexpr (FULL) commit(bwd_done, el);
                 if ((lt + 1) % kDrain == 0) commit(drain_bar, el);
                 if (lt == nt - 1) commit(fin_bar, el);
                 BTT(10);
             };
-            // forward of tile lt: Z^T = W1s . x as tf32 hi(W) hi(x) + lo(W) hi(x) (the small
-            // term first); x is rounded once (the dropped hi(W) lo(x) term is unbiased)
+            // forward of tile lt: Z^T = W1s . x as hi(W) x + lo(W) x (the small term first;
+            // FULL adds hi(W) lo(x))
             auto forward = [&](int64_t lt) {
-                const int fs = (int)(lt % kXFS), zb = (int)(lt % kZB);
+                const int xs = (int)(lt % kS), zb = (int)(lt % kZB);
                 BTT(11);
-                mbar_wait(&xf_full[fs], (uint32_t)(lt / kXFS) & 1);
+                mbar_wait(&x_full[xs], (uint32_t)(lt / kS) & 1);
                 tc_fence_after();
                 BTT(12);
-                const uint64_t dx = desc_ns(smem_u32(sm + L.xf + fs * kNX * kXF), 128, kFC * 128);
-                const uint64_t dxl = dx + (kXF >> 4);  // FULL: lo copy
+                const uint64_t dx = dx0 + ((xs * P::STAGE) >> 4);
+                const uint64_t dxl = dx + ((kXF + kXT) >> 4);  // FULL: lo copy
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColZ + 128 * zb + 64 * hf;
@@ -432,112 +444,38 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     {
 #pragma unroll
                         for (int s = 0; s < kFC / 2; s++) {
-                            mma_ss(d, wl + (s * 256 >> 4), dx + (s * 256 >> 4), idf, s != 0, el);
-                            if constexpr (FULL) mma_ss(d, wh + (s * 256 >> 4), dxl + (s * 256 >> 4), idf, 1, el);
+                            mma_ss(d, wl + (s * 256 >> 4), dx + (s * 2048 >> 4), idf, s != 0, el);
+                            if constexpr (FULL) mma_ss(d, wh + (s * 256 >> 4), dxl + (s * 2048 >> 4), idf, 1, el);
                         }
 #pragma unroll
-                        for (int s = 0; s < kFC / 2; s++) mma_ss(d, wh + (s * 256 >> 4), dx + (s * 256 >> 4), idf, 1, el);
+                        for (int s = 0; s < kFC / 2; s++)
+                            mma_ss(d, wh + (s * 256 >> 4), dx + (s * 2048 >> 4), idf, 1, el);
                     }
                 }
-                commit(&xf_empty[fs], el);
                 commit(&z_full[zb], el);
                 BTT(13);
             };
-            // Z^T is triple-buffered: forward(lt + 2) reuses the buffer of tile lt - 1, whose
-            // backward was issued (tensor-pipe order) in the previous iteration
-            forward(0);
-            if (nt > 1) forward(1);
+            // kZB Z^T buffers: the forward runs kZB tiles ahead; forward(lt + kZB) reuses the
+            // buffer of tile lt right after backward(lt) (the tensor pipe executes in order)
+            for (int64_t lt = 0; lt < kZB && lt < nt; lt++) forward(lt);
             for (int64_t lt = 0; lt < nt; lt++) {
                 backward(lt);
-                if (lt + 2 < nt) forward(lt + 2);
-            }
-        }
-    } else if (warp < 4) {
-        // ------------------------------------------------------------ converters
-        const int r = threadIdx.x - 64;  // row within the tile (forward copy); item base (transposed copy)
-        for (int64_t lt = 0; lt < nt; lt++) {
-            const int rs = (int)(lt % kXR), cs = (int)(lt % kXS), fs = (int)(lt % kXFS);
-            mbar_wait(&raw_full[rs], (uint32_t)(lt / kXR) & 1);
-            const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
-            const int64_t rem = a.N - row0;
-            const int nr = rem < kR ? (int)rem : kR;
-            const float* rawt = reinterpret_cast<const float*>(sm + L.raw + rs * kRawBytes);
-            // forward copy [r/8][k/4][r%8][k%4], tf32 (round to nearest)
-            if (lt >= kXFS) mbar_wait(&xf_empty[fs], (uint32_t)((lt / kXFS) - 1) & 1);
-            {
-                const float* raw = rawt + r * LD;
-                unsigned char* xh = sm + L.xf + fs * kNX * kXF + (r >> 3) * (kFC * 128) + (r & 7) * 16;
-#pragma unroll
-                for (int q = 0; q < kFC; q++) {
-                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if (r < nr && 4 * q < LD) v = *reinterpret_cast<const float4*>(raw + 4 * q);
-                    uint4 hi;
-                    hi.x = tf32_rn(v.x);
-                    hi.y = tf32_rn(v.y);
-                    hi.z = tf32_rn(v.z);
-                    hi.w = tf32_rn(v.w);
-                    *reinterpret_cast<uint4*>(xh + q * 128) = hi;
-                    if constexpr (FULL) {
-                        uint4 lo;
-                        lo.x = __float_as_uint(v.x - __uint_as_float(hi.x));
-                        lo.y = __float_as_uint(v.y - __uint_as_float(hi.y));
-                        lo.z = __float_as_uint(v.z - __uint_as_float(hi.z));
-                        lo.w = __float_as_uint(v.w - __uint_as_float(hi.w));
-                        *reinterpret_cast<uint4*>(xh + kXF + q * 128) = lo;
-                    }
-                }
-            }
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&xf_full[fs]);
-            // transposed copy [k/8][r/4][k%8][r%4]: one 16-byte core-matrix row (4 rows of
-            // feature k) per item; 8 consecutive items fill one 128-byte core matrix
-            if (lt >= kXS) mbar_wait(&xc_empty[cs], (uint32_t)((lt / kXS) - 1) & 1);
-            unsigned char* xt = sm + L.xc + cs * kNX * kXT;
-#pragma unroll 4
-            for (int it = r; it < kNB * kR / 4; it += 64) {
-                const int k = ((it >> 3) % (kNB / 8)) * 8 + (it & 7);
-                const int rq = (it >> 3) / (kNB / 8);
-                float v[4];
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const int rr = 4 * rq + i;
-                    v[i] = (rr < nr && k < LD) ? rawt[rr * LD + k] : 0.f;
-                }
-                uint4 hi;
-                hi.x = tf32_rn(v[0]);
-                hi.y = tf32_rn(v[1]);
-                hi.z = tf32_rn(v[2]);
-                hi.w = tf32_rn(v[3]);
-                const int off = (k >> 3) * (kR / 4 * 128) + rq * 128 + (k & 7) * 16;
-                *reinterpret_cast<uint4*>(xt + off) = hi;
-                if constexpr (FULL) {
-                    uint4 lo;
-                    lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
-                    lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
-                    lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
-                    lo.w = __float_as_uint(v[3] - __uint_as_float(hi.w));
-                    *reinterpret_cast<uint4*>(xt + kXT + off) = lo;
-                }
-            }
-            tgt[cs * kR + r] = (r < nr) ? rawt[r * LD + D + 1] : 0.f;
-            fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&xc_full[cs]);
-                mbar_arrive(&raw_empty[rs]);
+                if (lt + kZB < nt) forward(lt + kZB);
             }
         }
     } else {
         // ------------------------------------------------------------ epilogue
         // warp ew: TMEM lane quadrant quad = warp % 4 -> units 32 quad .. + 31 of half hf;
         // row block rb -> rows 32 rb .. 32 rb + 31 of the tile
-        const int ew = warp - 4, quad = warp & 3, hf = (ew >> 2) % NH, rb = ew / (4 * NH);
+        const int ew = warp - 2, quad = warp & 3, hf = (ew >> 2) % NH, rb = ew / (4 * NH);
         const int j = hf * 128 + quad * 32 + lane;  // this thread's hidden unit
         const int et = ew * 32 + lane;              // epilogue thread index; < kR: also owns row et
         const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
         const float w2s = a.Wk[a.H * DP + j];
         const float b2s = a.Wk[a.H * DP + a.H];
+        // the target of row r: feature D + 1 of the backward operand copy
+        const int tk = D + 1;
+        const int toff = kXF + (tk >> 3) * (kR / 4 * 128) + (tk & 7) * 16;
         float2 acc2 = make_float2(0.f, 0.f);
         float* out = a.part + (int64_t)blockIdx.x * a.PS;
         const uint32_t wcol = tmem + lanebase + kColW + 48 * hf;
@@ -567,19 +505,17 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         };
         float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
         // The two row blocks are independent pipelines (own named barrier; they meet
-        // only at dh_ready, two tiles of slack behind the triple-buffered forward).
-        // Row block 1 starts half a tile late -- after row block 0's MUFU-bound pass 1
-        // of tile 0 -- so one block's sigmoid pass overlaps the other's shuffle / FMA
-        // phases instead of both contending for the MUFU pipe at once.
+        // only at dh_ready, kZB tiles of slack behind the forward). Row block 1 starts
+        // half a tile late -- after row block 0's MUFU-bound pass 1 of tile 0 -- so one
+        // block's sigmoid pass overlaps the other's shuffle / FMA phases.
 #if GLX_BTC_OFFSET
         if (rb == 1) bar_sync(kEpiBar + 3, NEW * 32);
 #endif
         for (int64_t lt = 0; lt < nt; lt++) {
-            const int cs = (int)(lt % kXS), zb = (int)(lt % kZB);
+            const int xs = (int)(lt % kS), zb = (int)(lt % kZB);
             const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
             BTT(0);
             mbar_wait(&z_full[zb], (uint32_t)(lt / kZB) & 1);
-            mbar_wait(&xc_full[cs], (uint32_t)(lt / kXS) & 1);  // orders the converters' tgt writes
             tc_fence_after();
             BTT(1);
             const uint32_t zcol = tmem + lanebase + kColZ + 128 * zb + 64 * hf + 32 * rb;
@@ -648,7 +584,8 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 float d = 0.f;
                 if (row0 + r < a.N) {
                     const float o = sigmoid_scaled(zo + b2s);
-                    const float tt = tgt[cs * kR + r];
+                    const float tt = *reinterpret_cast<const float*>(sm + L.x + xs * P::STAGE + toff +
+                                                                     (r >> 2) * 128 + (r & 3) * 4);
                     d = (o - tt) * o * (1.0f - o);
                     if (hf == 0 && quad == 0) {
                         loss = fmaf(0.5f * (tt - o), (tt - o), loss);
@@ -664,19 +601,11 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 __syncwarp();
             }
             BTT(4);
-            // the backward of tile lt restarts the dW1 accumulator every kDrain tiles: add the
-            // finished partial (through the backward of tile lt - 1) into registers first
             if constexpr (FULL) {  // the backward of the previous tile still reads the dh lo buffer
                 if (lt >= 1) {
                     mbar_wait(bwd_done, (uint32_t)(lt - 1) & 1);
                     tc_fence_after();
                 }
-            }
-            if (lt >= 1 && lt % kDrain == 0) {
-                mbar_wait(drain_bar, (uint32_t)((lt / kDrain) - 1) & 1);
-                tc_fence_after();
-                BTT(5);
-                drain();
             }
             BTT(6);
             // pass 2: dh = delta_o h (1 - h) -> TMEM (tf32 hi in place of Z, FULL: + lo);
@@ -686,24 +615,37 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             for (int c = 0; c < 2; c++) {
                 uint32_t rh[16], rl[16];
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) {
+                for (int i = 0; i < 16; i += 4) {
                     const int r = 16 * c + i;
-                    const float2 d2 = *reinterpret_cast<const float2*>(dob + ew * 32 + r);
-                    const float2 hp = make_float2(h[r], h[r + 1]);
-                    const float2 v = __fmul2_rn(d2, hp);
-                    acc2 = __fadd2_rn(acc2, v);
-                    const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
-                    rh[i] = tf32_rn(s2.x);
-                    rh[i + 1] = tf32_rn(s2.y);
-                    if constexpr (FULL) {
-                        const float2 lo2 =
-                            __fadd2_rn(s2, make_float2(-__uint_as_float(rh[i]), -__uint_as_float(rh[i + 1])));
-                        rl[i] = __float_as_uint(lo2.x);
-                        rl[i + 1] = __float_as_uint(lo2.y);
+                    const float4 d4 = *reinterpret_cast<const float4*>(dob + ew * 32 + r);
+#pragma unroll
+                    for (int u = 0; u < 4; u += 2) {
+                        const float2 d2 = u ? make_float2(d4.z, d4.w) : make_float2(d4.x, d4.y);
+                        const float2 hp = make_float2(h[r + u], h[r + u + 1]);
+                        const float2 v = __fmul2_rn(d2, hp);
+                        acc2 = __fadd2_rn(acc2, v);
+                        const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
+                        rh[i + u] = tf32_rn(s2.x);
+                        rh[i + u + 1] = tf32_rn(s2.y);
+                        if constexpr (FULL) {
+                            const float2 lo2 = __fadd2_rn(
+                                s2, make_float2(-__uint_as_float(rh[i + u]), -__uint_as_float(rh[i + u + 1])));
+                            rl[i + u] = __float_as_uint(lo2.x);
+                            rl[i + u + 1] = __float_as_uint(lo2.y);
+                        }
                     }
                 }
                 st16(zcol + 16 * c, rh);
                 if constexpr (FULL) st16(locol + 16 * c, rl);
+            }
+            // the backward of tile lt restarts the dW1 accumulator every kDrain tiles: add the
+            // finished partial (through the backward of tile lt - 1, issued a tile ago) into
+            // registers before this tile's dh_ready releases that backward
+            if (lt >= 1 && lt % kDrain == 0) {
+                mbar_wait(drain_bar, (uint32_t)((lt / kDrain) - 1) & 1);
+                tc_fence_after();
+                BTT(5);
+                drain();
             }
             tmem_st_wait();
             tc_fence_before();
@@ -750,6 +692,42 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
     }
 }
 
+// rows -> the per-tile operand layouts (see kXF / kXT), tf32 round to nearest; FULL
+// also writes the lo remainders. One block per 64-row tile, the tile staged through
+// shared memory so both the row reads and the tile writes are coalesced.
+template <bool FULL>
+__global__ void __launch_bounds__(256) btc_pack_kernel(const float* __restrict__ Xp, int64_t N, int LD,
+                                                       unsigned char* __restrict__ tiles) {
+    using P = Pipe<FULL>;
+    __shared__ float t[kR * 37];
+    const int64_t tile = blockIdx.x;
+    const int64_t row0 = tile * kR;
+    const int nr = (int)((N - row0) < kR ? (N - row0) : kR);
+    for (int e = threadIdx.x; e < kR * 36; e += blockDim.x) {
+        const int r = e / 36, k = e - (e / 36) * 36;
+        t[r * 37 + k] = (r < nr && k < LD) ? Xp[(row0 + r) * LD + k] : 0.f;
+    }
+    __syncthreads();
+    uint32_t* out = reinterpret_cast<uint32_t*>(tiles + tile * (int64_t)P::GTILE);
+    // forward operand: word w = ((q * 8 + r / 8) * 8 + r % 8) * 4 + k % 4, k = 4 q + k % 4
+    for (int w = threadIdx.x; w < kXFG / 4; w += blockDim.x) {
+        const int e = w & 3, r8 = (w >> 2) & 7, ro = (w >> 5) & 7, q = w >> 8;
+        const float v = t[(ro * 8 + r8) * 37 + 4 * q + e];
+        const uint32_t hi = tf32_rn(v);
+        out[w] = hi;
+        if constexpr (FULL) out[(kXFG + kXTG) / 4 + w] = __float_as_uint(v - __uint_as_float(hi));
+    }
+    // backward operand: word w = ((kb * 16 + r / 4) * 8 + k % 8) * 4 + r % 4, k = 8 kb + k % 8
+    for (int w = threadIdx.x; w < kXTG / 4; w += blockDim.x) {
+        const int r4 = w & 3, k8 = (w >> 2) & 7, rq = (w >> 5) & 15, kb = w >> 9;
+        const int k = kb * 8 + k8;
+        const float v = k < 36 ? t[(rq * 4 + r4) * 37 + k] : 0.f;
+        const uint32_t hi = tf32_rn(v);
+        out[kXFG / 4 + w] = hi;
+        if constexpr (FULL) out[(kXFG + kXTG + kXFG) / 4 + w] = __float_as_uint(v - __uint_as_float(hi));
+    }
+}
+
 int a4(int x) { return (x + 3) / 4 * 4; }
 
 // row count from which the FAST precision runs (GLX_BTC_PREC=full / fast override it,
@@ -766,15 +744,20 @@ int64_t btc_full_rows() {
 extern "C" void glx_btc_timing_dump(void) {
     unsigned long long h[4096];
     cudaMemcpyFromSymbol(h, glx::g_btc_dbg, sizeof(h));
-    // per tile lt (8..23): epilogue slots 0-7 (warp 4), MMA slots 8-13 (warp 1; lt of the backward for 8-10)
+    auto at = [&](int t, int slot, int w) { return (long long)h[((t * 16) + slot) * 4 + w]; };
+    const long long t0 = at(0, 0, 0);
+    // epilogue slots 0-7 (rb0: warp 4, rb1: warp 12), MMA slots 8-13 (8-10 backward of tile
+    // t, 11-13 forward of tile t), producer slots 14-15; times relative to tile 8's start
     for (int t = 0; t < 16; t++) {
-        const unsigned long long* e = h + t * 32;
-        printf("lt %2d epi: wait_z %6lld pass1 %6lld bar1 %6lld rows+bar2 %6lld wait_bwd %6lld drain %6lld pass2 %6lld | "
-               "mma: wait_dh %6lld bwd_issue %6lld wait_xf %6lld fwd_issue %6lld | t0 %lld\n",
-               t + 8, (long long)(e[2] - e[0]), (long long)(e[4] - e[2]), (long long)(e[6] - e[4]),
-               (long long)(e[8] - e[6]), (long long)(e[10] - e[8]), (long long)(e[12] - e[10]),
-               (long long)(e[14] - e[12]), (long long)(e[19] - e[17]), (long long)(e[21] - e[19]),
-               (long long)(e[25] - e[23]), (long long)(e[27] - e[25]), (long long)(e[0] - h[0]));
+        printf("lt %2d", t + 8);
+        for (int w : {0, 2}) {
+            printf(" | rb%d start %7lld waitz %5lld p1 %5lld bar %5lld rows %5lld drain %5lld p2 %5lld", w / 2,
+                   at(t, 0, w) - t0, at(t, 1, w) - at(t, 0, w), at(t, 2, w) - at(t, 1, w), at(t, 3, w) - at(t, 2, w),
+                   at(t, 4, w) - at(t, 3, w), at(t, 6, w) - at(t, 4, w), at(t, 7, w) - at(t, 6, w));
+        }
+        printf(" | mma bwd: wait %5lld @%7lld issue %4lld | fwd: wait %5lld @%7lld issue %4lld | load @%7lld %5lld\n",
+               at(t, 9, 1) - at(t, 8, 1), at(t, 9, 1) - t0, at(t, 10, 1) - at(t, 9, 1), at(t, 12, 1) - at(t, 11, 1),
+               at(t, 12, 1) - t0, at(t, 13, 1) - at(t, 12, 1), at(t, 14, 3) - t0, at(t, 15, 3) - at(t, 14, 3));
     }
 }
 namespace glx {
@@ -791,7 +774,7 @@ bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
     g.N = N;
     g.DP = D + 1 <= 8 ? 8 : D + 1 <= 16 ? 16 : 34;
     g.LD = a4(std::max(D + 2, g.DP));
-    if (g.LD > kMaxLD) return false;
+    if (g.LD > 36) return false;
     g.HP = H;
     g.P1 = H * (D + 1);
     g.PS = a4(g.P1 + H + 6);
@@ -821,16 +804,25 @@ static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t
     return e;
 }
 
-cudaError_t launch_batchtc_epoch(const BatchGeom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st) {
+size_t batchtc_tile_bytes(const BatchGeom& g) {
+    return (size_t)g.ntiles * (g.MT ? Pipe<true>::GTILE : Pipe<false>::GTILE);
+}
+
+cudaError_t launch_batchtc_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st) {
+    if (g.MT) btc_pack_kernel<true><<<(unsigned)g.ntiles, 256, 0, st>>>(Xp, g.N, g.LD, (unsigned char*)tiles);
+    else btc_pack_kernel<false><<<(unsigned)g.ntiles, 256, 0, st>>>(Xp, g.N, g.LD, (unsigned char*)tiles);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st) {
     BtcArgs a;
-    a.Xp = Xp;
+    a.tiles = (const unsigned char*)tiles;
     a.Wk = Wk;
     a.part = part;
     a.N = g.N;
     a.ntiles = g.ntiles;
     a.D = g.D;
     a.DP = g.DP;
-    a.LD = g.LD;
     a.H = g.H;
     a.P1 = g.P1;
     a.PS = g.PS;

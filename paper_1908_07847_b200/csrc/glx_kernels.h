@@ -106,7 +106,12 @@ bool batch3_geometry(int64_t N, int D, int H, int n_sms, Batch3Geom* g);
 cudaError_t launch_batch3_epoch(const Batch3Geom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st);
 // tcgen05 epoch kernel (glx_batchtc.cu): H = 128 or 256, D <= 33; same partial record as batch3
 bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* g);
-cudaError_t launch_batchtc_epoch(const BatchGeom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st);
+// the tcgen05 epoch kernel reads the rows pre-laid-out per 64-row tile (tf32 MMA
+// operands): batchtc_tile_bytes of scratch filled once per training call from the
+// packed rows by launch_batchtc_pack
+size_t batchtc_tile_bytes(const BatchGeom& g);
+cudaError_t launch_batchtc_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st);
+cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st);
 
 // ------------------------------------------------------------ exact eval
 cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,
