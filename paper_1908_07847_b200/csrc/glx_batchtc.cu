@@ -89,8 +89,8 @@ constexpr int kEpiBar = 1;
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
 constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
-#ifndef GLX_BTC_OFFSET
-#define GLX_BTC_OFFSET 1  // 0: the two row blocks start together
+#ifndef GLX_BTC_TOKEN
+#define GLX_BTC_TOKEN 1  // 0: the two row blocks' sigmoid passes are not interleaved
 #endif
 #ifndef GLX_BTC_EXP
 #define GLX_BTC_EXP 0  // diagnostic builds only: 1 no MUFU sigmoid, 2 no backward MMAs, 3 no forward MMAs
@@ -258,7 +258,7 @@ __device__ __forceinline__ uint32_t tf32_rn(float v) { return (__float_as_uint(v
 // in fp32 Horner, on par with ex2.approx), exponent inserted with an integer add;
 // |x| clamped to 125 (1 + 2^-125 == 1 and 1 / (1 + 2^125) ~ 0 in fp32 either way)
 #ifndef GLX_BTC_POLY
-#define GLX_BTC_POLY 3  // element pairs per GLX_BTC_POLY_DEN that take the polynomial (0: all MUFU)
+#define GLX_BTC_POLY 2  // element pairs per GLX_BTC_POLY_DEN that take the polynomial (0: all MUFU)
 #endif
 #ifndef GLX_BTC_POLY_DEN
 #define GLX_BTC_POLY_DEN 8
@@ -289,8 +289,13 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
     uint64_t* x_full = bars;                // tile stage loaded (bulk-copy bytes)
     uint64_t* x_empty = x_full + kS;        // tile stage free (its backward completed)
     uint64_t* z_full = x_empty + kS;        // Z^T buffer written by the forward
-    uint64_t* dh_ready = z_full + kZB;      // the epilogue wrote dh of the tile
-    uint64_t* drain_bar = dh_ready + 1;     // the backward of the last tile before a dW1 drain completed
+    // dh_ready[rb * kZB + lt % kZB]: row block rb wrote dh of tile lt. Per row block:
+    // the blocks run up to kZB tiles apart, and a counter shared by both would complete
+    // a tile's phase on the leading block's arrivals for a later tile. Per Z buffer: a
+    // block cannot arrive for tile lt + kZB before backward(lt) was issued (it needs
+    // Z(lt + kZB)), so each barrier is at most one phase ahead of the MMA warp's wait.
+    uint64_t* dh_ready = z_full + kZB;
+    uint64_t* drain_bar = dh_ready + 2 * kZB;  // the backward of the last tile before a dW1 drain completed
     uint64_t* fin_bar = drain_bar + 1;      // the last backward completed
     uint64_t* bwd_done = fin_bar + 1;       // FULL: every backward completed (the dh lo buffer is free)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bwd_done + 1);
@@ -307,7 +312,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             mbar_init(&x_empty[i], 1);
         }
         for (int b = 0; b < kZB; b++) mbar_init(&z_full[b], 1);
-        mbar_init(dh_ready, NEW);
+        for (int b = 0; b < 2 * kZB; b++) mbar_init(&dh_ready[b], NEW / 2);
         mbar_init(drain_bar, 1);
         mbar_init(fin_bar, 1);
         mbar_init(bwd_done, 1);
@@ -392,7 +397,8 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             auto backward = [&](int64_t lt) {
                 const int xs = (int)(lt % kS), zb = (int)(lt % kZB);
                 BTT(8);
-                mbar_wait(dh_ready, (uint32_t)lt & 1);
+                mbar_wait(&dh_ready[zb], (uint32_t)(lt / kZB) & 1);
+                mbar_wait(&dh_ready[kZB + zb], (uint32_t)(lt / kZB) & 1);
                 tc_fence_after();
                 BTT(9);
                 const uint64_t dth = dt0 + ((xs * P::STAGE) >> 4);
@@ -505,12 +511,12 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         };
         float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
         // The two row blocks are independent pipelines (own named barrier; they meet
-        // only at dh_ready, kZB tiles of slack behind the forward). Row block 1 starts
-        // half a tile late -- after row block 0's MUFU-bound pass 1 of tile 0 -- so one
-        // block's sigmoid pass overlaps the other's shuffle / FMA phases.
-#if GLX_BTC_OFFSET
-        if (rb == 1) bar_sync(kEpiBar + 3, NEW * 32);
-#endif
+        // only at dh_ready, kZB tiles of slack behind the forward). Their MUFU-bound
+        // sigmoid passes take turns -- a token passed through two named barriers: block 0
+        // does tile lt's pass 1, then block 1 does its own, then block 0 tile lt + 1 --
+        // so each pass has the MUFU pipe to itself while the other block runs its
+        // shuffle / FMA phases, instead of both contending at once.
+        constexpr int kTok0 = kEpiBar + 4, kTok1 = kEpiBar + 5;  // block 1 -> 0, block 0 -> 1
         for (int64_t lt = 0; lt < nt; lt++) {
             const int xs = (int)(lt % kS), zb = (int)(lt % kZB);
             const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
@@ -527,6 +533,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #pragma unroll
                 for (int i = 0; i < 32; i++) h[i] = __uint_as_float(r0[i]);
             }
+#if GLX_BTC_TOKEN
+            if (rb == 1) bar_sync(kTok1, NEW * 32);           // block 0 finished its pass 1 of tile lt
+            else if (lt >= 1) bar_sync(kTok0, NEW * 32);      // block 1 finished its pass 1 of tile lt - 1
+#endif
             // pass 1: h = sigmoid(z) (z prescaled by -log2 e)
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
@@ -541,6 +551,9 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 h[i + 1] = rcp_approx(den.y);
 #endif
             }
+#if GLX_BTC_TOKEN
+            bar_arrive(rb == 0 ? kTok1 : kTok0, NEW * 32);  // the other block's turn on the MUFU pipe
+#endif
             // output partials w2s_j h_j reduce-scattered over the warp's 32 units: lane l
             // ends with row 32 rb + l
             {
@@ -565,9 +578,6 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 opart[(int)(lt & 1) * NEW * 32 + ew * 32 + lane] = p[0];
             }
             BTT(2);
-#if GLX_BTC_OFFSET
-            if (lt == 0 && rb == 0) bar_arrive(kEpiBar + 3, NEW * 32);
-#endif
             bar_sync(kEpiBar + rb, NEW * 16);  // the warps of this row block (they cover all units of its rows)
             BTT(3);
             {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);
@@ -650,10 +660,13 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(dh_ready);
+            if (lane == 0) mbar_arrive(&dh_ready[rb * kZB + zb]);
             BTT(7);
         }
         // ---------------------------------------------- per-CTA partial record
+#if GLX_BTC_TOKEN
+        if (rb == 0) bar_sync(kTok0, NEW * 32);  // block 1's last token
+#endif
         mbar_wait(fin_bar, 0);
         tc_fence_after();
         drain();  // tiles since the last drain (>= 1)
