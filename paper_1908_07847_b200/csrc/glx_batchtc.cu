@@ -89,6 +89,9 @@ constexpr int kEpiBar = 1;
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
 constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
+#ifndef GLX_BTC_RN2
+#define GLX_BTC_RN2 0  // 1: tf32 rounding of the hidden deltas on the FMA pipe (pairs)
+#endif
 #ifndef GLX_BTC_TOKEN
 #define GLX_BTC_TOKEN 1  // 0: the two row blocks' sigmoid passes are not interleaved
 #endif
@@ -252,6 +255,13 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // rounding is what lets single-product terms meet the 1e-5 parity bar
 // (tools/tf32_split_error.py); the MMA ignores the 13 low bits of any operand
 __device__ __forceinline__ uint32_t tf32_rn(float v) { return (__float_as_uint(v) + 0x1000u) & kTf32Mask; }
+// the same rounding for a pair on the FMA pipe (Veltkamp split: t = v (2^13 + 1),
+// hi = t - (t - v) keeps the leading 11 significant bits, round to nearest even;
+// |v| < 2^114 so t cannot overflow)
+__device__ __forceinline__ float2 tf32_rn2(float2 v) {
+    const float2 t = __fmul2_rn(v, bcast2(8193.0f));
+    return __fadd2_rn(t, make_float2(-(t.x - v.x), -(t.y - v.y)));
+}
 
 // 2^x for a pair on the FMA/ALU pipes (pass 1 is MUFU-bound): round-to-nearest by
 // the 1.5 * 2^23 magic add, degree-5 polynomial on [-1/2, 1/2] (max rel. error 2.3e-7
@@ -635,8 +645,14 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                         const float2 v = __fmul2_rn(d2, hp);
                         acc2 = __fadd2_rn(acc2, v);
                         const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
+#if GLX_BTC_RN2
+                        const float2 r2 = tf32_rn2(s2);
+                        rh[i + u] = __float_as_uint(r2.x);
+                        rh[i + u + 1] = __float_as_uint(r2.y);
+#else
                         rh[i + u] = tf32_rn(s2.x);
                         rh[i + u + 1] = tf32_rn(s2.y);
+#endif
                         if constexpr (FULL) {
                             const float2 lo2 = __fadd2_rn(
                                 s2, make_float2(-__uint_as_float(rh[i + u]), -__uint_as_float(rh[i + u + 1])));
