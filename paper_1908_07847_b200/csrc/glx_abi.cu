@@ -287,9 +287,18 @@ int batch_kernel_pref() {
     return v;
 }
 
+// the tcgen05 kernel's per-tile time is set by its epilogue warps (32 units x 32 rows
+// each), so narrow layers leave most of its warps idle: below 96 units the FP32
+// kernels are as fast (GLX_BATCH_KERNEL=tc forces the tcgen05 kernel for any H <= 256)
+constexpr int kTcMinH = 96;
+bool force_tc() {
+    const char* e = getenv("GLX_BATCH_KERNEL");
+    return e && e[0] == 't' && e[1] == 'c';
+}
+
 bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
     const int pref = batch_kernel_pref();
-    if (pref >= 2 && batchtc_geometry(N, D, H, sm_count_current(), g)) {
+    if (pref >= 2 && (H >= kTcMinH || force_tc()) && batchtc_geometry(N, D, H, sm_count_current(), g)) {
         *kind = 2;
         return true;
     }
@@ -329,7 +338,7 @@ int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D
     BatchGeom g;
     int kind = 0;
     if (!train_geometry(N, D, H, &g, &kind))
-        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d N=%lld (needs D<=33, H<=512)", D,
+        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d N=%lld (needs D<=127, H<=512)", D,
                        H, (long long)N);
     Workspace* ws = workspace(st);
     GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
@@ -610,7 +619,8 @@ int glx_train_sweep(int64_t n_nets, const int32_t* H_per_net, const int64_t* w_o
 }
 
 int32_t glx_packed_ld(int32_t D) {
-    const int dp = D + 1 <= 8 ? 8 : D + 1 <= 16 ? 16 : D + 1 <= 34 ? 34 : D + 1;
+    int dp = pick_dp(D);  // the batch kernels' weight-row stride: a row holds at least that many floats
+    if (dp < 0) dp = D + 1;
     return ((std::max(D + 2, dp)) + 3) / 4 * 4;
 }
 

@@ -616,10 +616,11 @@ cudaError_t launch_batch_apply(int D, int H, float* W1, float* W2, const double*
 }
 
 // ------------------------------------------------------------------ host side
-static int pick_dp(int D) {
-    if (D + 1 <= 8) return 8;
-    if (D + 1 <= 16) return 16;
-    if (D + 1 <= 34) return 34;
+// weight-row stride (the [W1 | b1] row in registers, float2 pairs): the kernels are
+// instantiated for these widths; D + 1 <= 128 (kernels.py:264-295 takes any D)
+int pick_dp(int D) {
+    for (int dp : {8, 16, 34, 48, 64, 128})
+        if (D + 1 <= dp) return dp;
     return -1;
 }
 
@@ -642,7 +643,8 @@ bool batch_geometry(int64_t N, int D, int H, int n_sms, bool train, BatchGeom* g
     q.LD = ((std::max(D + 2, q.DP)) + 3) / 4 * 4;
     q.MT = 0;
     for (int mt : {4, 3, 2, 1})
-        if (mt <= GLX_MAXMT && H % mt == 0 && H / mt <= kFT) {
+        if (mt <= GLX_MAXMT && (q.DP <= 34 || mt <= 2) && (q.DP < 128 || mt == 1) && H % mt == 0 &&
+            H / mt <= kFT) {
             q.MT = mt;
             break;
         }
@@ -690,12 +692,15 @@ static cudaError_t launch_t(const BatchGeom& g, const BatchArgs& a, cudaStream_t
 
 template <int DP, bool TRAIN>
 static cudaError_t launch_mt(const BatchGeom& g, const BatchArgs& a, cudaStream_t st) {
-    switch (g.MT) {
-        case 4: return launch_t<DP, 4, TRAIN>(g, a, st);
-        case 3: return launch_t<DP, 3, TRAIN>(g, a, st);
-        case 2: return launch_t<DP, 2, TRAIN>(g, a, st);
-        case 1: return launch_t<DP, 1, TRAIN>(g, a, st);
+    if constexpr (DP <= 34) {  // wide rows: at most 2 units per thread (register tile)
+        switch (g.MT) {
+            case 4: return launch_t<DP, 4, TRAIN>(g, a, st);
+            case 3: return launch_t<DP, 3, TRAIN>(g, a, st);
+        }
     }
+    if constexpr (DP < 128)
+        if (g.MT == 2) return launch_t<DP, 2, TRAIN>(g, a, st);
+    if (g.MT == 1) return launch_t<DP, 1, TRAIN>(g, a, st);
     return cudaErrorInvalidValue;
 }
 
@@ -722,12 +727,18 @@ cudaError_t launch_batch_epoch(const BatchGeom& g, const float* Xp, const float*
             case 8: return launch_mt<8, true>(g, a, st);
             case 16: return launch_mt<16, true>(g, a, st);
             case 34: return launch_mt<34, true>(g, a, st);
+            case 48: return launch_mt<48, true>(g, a, st);
+            case 64: return launch_mt<64, true>(g, a, st);
+            case 128: return launch_mt<128, true>(g, a, st);
         }
     } else {
         switch (g.DP) {
             case 8: return launch_mt<8, false>(g, a, st);
             case 16: return launch_mt<16, false>(g, a, st);
             case 34: return launch_mt<34, false>(g, a, st);
+            case 48: return launch_mt<48, false>(g, a, st);
+            case 64: return launch_mt<64, false>(g, a, st);
+            case 128: return launch_mt<128, false>(g, a, st);
         }
     }
     return cudaErrorInvalidValue;

@@ -288,7 +288,7 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <int NH, bool FULL>
+template <int NH, bool FULL, bool PAD>
 __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
     constexpr int NEW = 8 * NH;  // epilogue warps: 4 lane quadrants x NH unit halves x 2 row blocks
     using P = Pipe<FULL>;
@@ -341,7 +341,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #pragma unroll
         for (int i = 0; i < 4; i++) {
             const int k = 4 * q + i;
-            v[i] = (k <= D) ? a.Wk[(int64_t)j * DP + k] : 0.f;
+            v[i] = (k <= D && j < a.H) ? a.Wk[(int64_t)j * DP + k] : 0.f;  // units >= H: zero rows
         }
         const int hf = j >> 7, jj = j & 127;
         const int off = hf * kWT + (jj >> 3) * (kFC * 128) + q * 128 + (jj & 7) * 16;
@@ -487,7 +487,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         const int j = hf * 128 + quad * 32 + lane;  // this thread's hidden unit
         const int et = ew * 32 + lane;              // epilogue thread index; < kR: also owns row et
         const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
-        const float w2s = a.Wk[a.H * DP + j];
+        // H not a multiple of 128: the padded units have zero weights (Z = 0, w2 = 0);
+        // a warp whose 32 units are all padding skips the arithmetic and only keeps the
+        // barrier protocol (its output partial slots stay zero)
+        const bool active = !PAD || hf * 128 + quad * 32 < a.H;  // PAD: H is not 128 NH
+        const float w2s = j < a.H ? a.Wk[a.H * DP + j] : 0.f;
+        if (!active) {
+            opart[ew * 32 + lane] = 0.f;
+            opart[NEW * 32 + ew * 32 + lane] = 0.f;
+        }
         const float b2s = a.Wk[a.H * DP + a.H];
         // the target of row r: feature D + 1 of the backward operand copy
         const int tk = D + 1;
@@ -536,7 +544,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             BTT(1);
             const uint32_t zcol = tmem + lanebase + kColZ + 128 * zb + 64 * hf + 32 * rb;
             float h[32];
-            {
+            if (active) {
                 uint32_t r0[32];
                 ld32(zcol, r0);
                 tmem_ld_wait();
@@ -548,25 +556,28 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             else if (lt >= 1) bar_sync(kTok0, NEW * 32);      // block 1 finished its pass 1 of tile lt - 1
 #endif
             // pass 1: h = sigmoid(z) (z prescaled by -log2 e)
+            if (active) {
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
+                for (int i = 0; i < 32; i += 2) {
 #if GLX_BTC_EXP == 1
-                h[i] = h[i] * 0.01f + 0.5f;
-                h[i + 1] = h[i + 1] * 0.01f + 0.5f;
+                    h[i] = h[i] * 0.01f + 0.5f;
+                    h[i + 1] = h[i + 1] * 0.01f + 0.5f;
 #else
-                const float2 e2 = ((i >> 1) % GLX_BTC_POLY_DEN < GLX_BTC_POLY) ? exp2_poly2(make_float2(h[i], h[i + 1]))
-                                                                 : make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
-                const float2 den = __fadd2_rn(e2, bcast2(1.0f));
-                h[i] = rcp_approx(den.x);
-                h[i + 1] = rcp_approx(den.y);
+                    const float2 e2 = ((i >> 1) % GLX_BTC_POLY_DEN < GLX_BTC_POLY)
+                                          ? exp2_poly2(make_float2(h[i], h[i + 1]))
+                                          : make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
+                    const float2 den = __fadd2_rn(e2, bcast2(1.0f));
+                    h[i] = rcp_approx(den.x);
+                    h[i + 1] = rcp_approx(den.y);
 #endif
+                }
             }
 #if GLX_BTC_TOKEN
             bar_arrive(rb == 0 ? kTok1 : kTok0, NEW * 32);  // the other block's turn on the MUFU pipe
 #endif
             // output partials w2s_j h_j reduce-scattered over the warp's 32 units: lane l
             // ends with row 32 rb + l
-            {
+            if (active) {
                 float p[32];
 #pragma unroll
                 for (int i = 0; i < 32; i += 2) {
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             BTT(2);
             bar_sync(kEpiBar + rb, NEW * 16);  // the warps of this row block (they cover all units of its rows)
             BTT(3);
-            {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);
+            if (active) {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);
                // every warp computes its own rows' delta_o, one warp per block keeps the statistics
                 const int r = 32 * rb + lane;
                 const float* op = opart + (int)(lt & 1) * NEW * 32 + rb * (4 * NH * 32) + lane;
@@ -622,7 +633,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             }
             BTT(4);
             if constexpr (FULL) {  // the backward of the previous tile still reads the dh lo buffer
-                if (lt >= 1) {
+                if (lt >= 1 && active) {
                     mbar_wait(bwd_done, (uint32_t)(lt - 1) & 1);
                     tc_fence_after();
                 }
@@ -631,6 +642,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             // pass 2: dh = delta_o h (1 - h) -> TMEM (tf32 hi in place of Z, FULL: + lo);
             // dW2 += delta_o h
             const uint32_t locol = tmem + lanebase + kColLo + 64 * hf + 32 * rb;
+            if (active) {
 #pragma unroll
             for (int c = 0; c < 2; c++) {
                 uint32_t rh[16], rl[16];
@@ -664,10 +676,11 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 st16(zcol + 16 * c, rh);
                 if constexpr (FULL) st16(locol + 16 * c, rl);
             }
+            }
             // the backward of tile lt restarts the dW1 accumulator every kDrain tiles: add the
             // finished partial (through the backward of tile lt - 1, issued a tile ago) into
             // registers before this tile's dh_ready releases that backward
-            if (lt >= 1 && lt % kDrain == 0) {
+            if (lt >= 1 && lt % kDrain == 0 && active) {
                 mbar_wait(drain_bar, (uint32_t)((lt / kDrain) - 1) & 1);
                 tc_fence_after();
                 BTT(5);
@@ -685,15 +698,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #endif
         mbar_wait(fin_bar, 0);
         tc_fence_after();
-        drain();  // tiles since the last drain (>= 1)
-        {
+        if (active) drain();  // tiles since the last drain (>= 1)
+        if (j < a.H) {
             float* o1 = out + (int64_t)j * (D + 1) + kDH * rb;
 #pragma unroll
             for (int k = 0; k < kDH; k++)
                 if (kDH * rb + k <= D) o1[k] = acc1[k];
         }
         bar_sync(kEpiBar + 2, NEW * 32);  // opart is free: exchange the dW2 partials of the two row blocks
-        if (rb == 1) opart[j] = acc2.x + acc2.y;
+        if (rb == 1 && j < a.H) opart[j] = acc2.x + acc2.y;
         float* stat = opart + 2 * NEW * 32 - kR * 6;  // behind the dW2 exchange slots (H <= 256 floats)
         if (hf == 0 && quad == 0) {  // the statistics warps: rows 32 rb + lane
             const int r = 32 * rb + lane;
@@ -705,7 +718,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             stat[r * 6 + 5] = dsum;
         }
         bar_sync(kEpiBar + 2, NEW * 32);
-        if (rb == 0) out[a.P1 + j] = (acc2.x + acc2.y) + opart[j];
+        if (rb == 0 && j < a.H) out[a.P1 + j] = (acc2.x + acc2.y) + opart[j];
         if (et < 6) {
             float s = 0.f;
             for (int r = 0; r < kR; r++) s += stat[r * 6 + et];
@@ -796,7 +809,7 @@ namespace {
 }  // namespace
 
 bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
-    if (N < 1 || D < 1 || D > 33 || (H != 128 && H != 256)) return false;
+    if (N < 1 || D < 1 || D > 33 || H < 1 || H > 256) return false;
     BatchGeom g{};
     g.D = D;
     g.H = H;
@@ -814,14 +827,15 @@ bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
     // FAST above btc_full_rows() rows (tests/test_gpu_batch.py: FULL keeps small row
     // counts within 1e-5 of the oracle, where FAST's rounding has too few rows to average)
     g.MT = N < btc_full_rows() ? 1 : 0;  // 1: FULL precision
-    g.smem = (size_t)(g.MT ? btc_smem<true>(H / 128).total : btc_smem<false>(H / 128).total);
+    const int nh = (H + 127) / 128;
+    g.smem = (size_t)(g.MT ? btc_smem<true>(nh).total : btc_smem<false>(nh).total);
     *out = g;
     return true;
 }
 
 template <int NH, bool FULL>
 static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t st) {
-    auto k = batchtc_kernel<NH, FULL>;
+    auto k = g.H % 128 ? batchtc_kernel<NH, FULL, true> : batchtc_kernel<NH, FULL, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e != cudaSuccess) {
         fprintf(stderr, "glx: batchtc_kernel<%d> smem=%zu: %s\n", NH, g.smem, cudaGetErrorString(e));
@@ -855,8 +869,8 @@ cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const fl
     a.H = g.H;
     a.P1 = g.P1;
     a.PS = g.PS;
-    if (g.MT) return g.H == 256 ? launch_btc<2, true>(g, a, st) : launch_btc<1, true>(g, a, st);
-    return g.H == 256 ? launch_btc<2, false>(g, a, st) : launch_btc<1, false>(g, a, st);
+    if (g.MT) return g.H > 128 ? launch_btc<2, true>(g, a, st) : launch_btc<1, true>(g, a, st);
+    return g.H > 128 ? launch_btc<2, false>(g, a, st) : launch_btc<1, false>(g, a, st);
 }
 
 }  // namespace glx

@@ -106,6 +106,7 @@ bool batch3_geometry(int64_t N, int D, int H, int n_sms, Batch3Geom* g);
 cudaError_t launch_batch3_epoch(const Batch3Geom& g, const float* Xp, const float* Wk, float* part, cudaStream_t st);
 // tcgen05 epoch kernel (glx_batchtc.cu): H = 128 or 256, D <= 33; same partial record as batch3
 bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* g);
+int pick_dp(int D);  // glx_batch.cu: weight-row stride of the FP32 batch kernels (-1: D too wide)
 // the tcgen05 epoch kernel reads the rows pre-laid-out per 64-row tile (tf32 MMA
 // operands): batchtc_tile_bytes of scratch filled once per training call from the
 // packed rows by launch_batchtc_pack

@@ -41,17 +41,68 @@ def test_batch_vs_oracle(gpu, N, D, H):
     assert np.abs(stats[0, 1:] - np.array([tp, tn, fp, fn])).sum() <= 2  # |o-0.5| < 1e-6 rows may flip
 
 
+@pytest.mark.parametrize("N,H,force", [
+    (3001, 160, False), (2000, 96, False), (5000, 200, False), (4099, 250, False),
+    (1000, 33, True), (129, 64, True), (700, 1, True),
+])
+def test_tcgen05_kernel_any_width_vs_oracle(gpu, N, H, force, monkeypatch):
+    """The tcgen05 epoch kernel for widths that are not a multiple of 128 (padded
+    units: zero weights, idle epilogue warps) -- the default for 96 <= H <= 256,
+    forced with GLX_BATCH_KERNEL=tc below that."""
+    import paper_1908_07847_b200._lib as L
+
+    if force:
+        monkeypatch.setenv("GLX_BATCH_KERNEL", "tc")
+    assert L.load().glx_batch_kernel_kind(N, 33, H) == 2
+    x, l, t, net0 = _case(N, 33, H, seed=N % 89)
+    ref, net = net0.copy(), net0.copy()
+    O.train_batch(ref.w_ih2d, ref.w_ho2d, x, t, 6, 0.5, N)
+    stats = np.zeros((6, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 6, 0.5, g.cuda(), stats)
+    err = max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho))
+    assert err <= 1e-5, f"N={N} H={H}: {err:.3e}"
+    assert (stats[:, 1:].sum(axis=1) == N).all()
+
+
+@pytest.mark.parametrize("N,D,H", [(500, 40, 64), (777, 60, 30), (300, 100, 12), (129, 127, 3)])
+def test_batch_wide_inputs_vs_oracle(gpu, N, D, H):
+    """D > 33 (kernels.py:264-295 takes any input width): the FP32 batch kernel with
+    48-, 64- and 128-float weight rows."""
+    x, l, t, net0 = _case(N, D, H, seed=D)
+    ref, net = net0.copy(), net0.copy()
+    O.train_batch(ref.w_ih2d, ref.w_ho2d, x, t, 5, 0.5, N)
+    stats = np.zeros((5, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 5, 0.5, g.cuda(), stats)
+    assert max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho)) <= 1e-5
+    (tp, tn, fp, fn), loss = O.eval_counts(net0.w_ih2d, net0.w_ho2d, x, l)
+    assert abs(stats[0, 0] - loss) <= 1e-4 * max(1.0, loss)
+
+
+def test_tcgen05_fast_precision_padded_width(gpu, monkeypatch):
+    """The large-N (FAST) precision with a padded width, 150k rows x 33 -> 192 -> 1."""
+    monkeypatch.setenv("GLX_BTC_PREC", "fast")
+    x, l, t, net0 = _case(150_000, 33, 192, seed=6)
+    ref, net = net0.copy(), net0.copy()
+    O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, t, 4, 0.1)
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 4, 0.1, g.cuda())
+    assert max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho)) <= 1e-5
+
+
 def test_tcgen05_kernel_selected_for_headline_shapes(gpu):
-    """configs 2 and 4 (33 -> 128 / 256 -> 1) run the tcgen05 3xTF32 epoch kernel; other
-    widths fall back to the FP32 CUDA-core kernels (glx_batch_kernel_kind)."""
+    """configs 2 and 4 (33 -> 128 / 256 -> 1) run the tcgen05 epoch kernel, as does any
+    width 96..256; narrower and wider layers run the FP32 CUDA-core kernels
+    (glx_batch_kernel_kind)."""
     import paper_1908_07847_b200._lib as L
 
     lib = L.load()
     assert lib.glx_batch_kernel_kind(1 << 20, 33, 256) == 2
     assert lib.glx_batch_kernel_kind(1 << 26, 33, 256) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 128) == 2
+    assert lib.glx_batch_kernel_kind(1000, 33, 192) == 2 and lib.glx_batch_kernel_kind(1000, 33, 97) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 64) in (0, 1)
-    assert lib.glx_batch_kernel_kind(1000, 40, 256) == -1
+    assert lib.glx_batch_kernel_kind(1000, 33, 512) in (0, 1)
+    assert lib.glx_batch_kernel_kind(1000, 40, 256) in (0, 1)  # D > 33: FP32 kernels
+    assert lib.glx_batch_kernel_kind(1000, 128, 8) == -1
 
 
 def test_tcgen05_kernel_matches_fp32_kernel(gpu, tmp_path):
@@ -140,8 +191,8 @@ def test_dp_split_equals_fused_single_gpu(gpu):
 
 
 def test_unsupported_shape_raises(gpu):
-    net = g.init_weights(g.NetworkConfig(input_dim=40, hidden_dim=8, seed=0))
-    x = np.zeros((10, 40), np.float32)
+    net = g.init_weights(g.NetworkConfig(input_dim=128, hidden_dim=8, seed=0))
+    x = np.zeros((10, 128), np.float32)
     with pytest.raises(g.ValidationError):
         g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, np.zeros(10, np.float32), 1, 0.1, g.cuda())
 
