@@ -242,6 +242,19 @@ int glx_wide_apply(float* w_ih, float* w_ho, const double* grad, double lr_over_
 int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
                    int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream);
 
+/* The wide configuration with f32 rows on tcgen05 kind::tf32 (f32 storage of H and
+ * the deltas; SURVEY.md C5 "evaluated against the FP32 tolerance"): X f32 [N][1024]
+ * U[0,1) and [X,1]^T f32 K-blocked [N/32][1025][32] (element (i, r) at
+ * ((r/32)*1025 + i)*32 + r%32), labels as glx_wide_make_data; N % 32 == 0. The
+ * gradient and training calls mirror glx_wide_grad / glx_wide_train (the update is
+ * glx_wide_apply). */
+int glx_wide_make_shard_tf32(int64_t row0, int64_t N, uint64_t seed, float* X, float* XT, uint8_t* labels,
+                             void* stream);
+int glx_wide_grad_tf32(const float* w_ih, const float* w_ho, const float* X, const float* XT, const uint8_t* labels,
+                       int64_t N, double* grad, void* stream);
+int glx_wide_train_tf32(float* w_ih, float* w_ho, const float* X, const float* XT, const uint8_t* labels, int64_t N,
+                        int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream);
+
 /* ---------------------------------------------------- per-instance API */
 /* network.forward (network.py:128-135) for N rows, the reference's f64 order:
  * hidden (device, N x H f32) and out (device, N x K f32) activations. */

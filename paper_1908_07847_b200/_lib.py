@@ -85,6 +85,9 @@ SIGNATURES = {
     "glx_dp_train_batch": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i64, _dbl, _vp, _vp, _vp]),
     "glx_dp_run_train_segment_batch": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _i32, _i32, _i64, _dbl, _vp,
                                               _i32]),
+    "glx_wide_make_shard_tf32": (_int, [_i64, _i64, _u64, _vp, _vp, _vp, _vp]),
+    "glx_wide_grad_tf32": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    "glx_wide_train_tf32": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _dbl, _vp, _vp, _vp]),
     "glx_launch_count": (_u64, []),
     "glx_profile_enable": (None, [_i32]),
     "glx_profile_read": (_int, [_vp, _vp]),

@@ -1133,6 +1133,63 @@ int glx_wide_grad(const float* w_ih, const float* w_ho, const void* Xb, const vo
     return GLX_OK;
 }
 
+// ---------------------------------------------------------- wide, tf32 path
+int glx_wide_make_shard_tf32(int64_t row0, int64_t N, uint64_t seed, float* X, float* XT, uint8_t* labels,
+                             void* stream) {
+    if (N < 32 || N % 32) return set_err(GLX_ERR_SHAPE, "wide tf32 data needs N %% 32 == 0 (got %lld)", (long long)N);
+    if (row0 < 0) return set_err(GLX_ERR_INVALID, "row0 must be >= 0");
+    GLX_LAUNCH(launch_wide_gen_tf32(X, XT, labels, N, seed, row0, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+static int64_t wide32_chunk(int64_t N) { return std::min<int64_t>(N, (int64_t)1 << 19); }  // rows per chunk
+
+int glx_wide_grad_tf32(const float* w_ih, const float* w_ho, const float* X, const float* XT, const uint8_t* labels,
+                       int64_t N, double* grad, void* stream) {
+    if (N < 32 || N % 32) return set_err(GLX_ERR_SHAPE, "wide tf32 gradient needs N %% 32 == 0 (got %lld)", (long long)N);
+    if (!grad) return set_err(GLX_ERR_INVALID, "grad must be a device buffer of glx_wide_grad_len() doubles");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t C = wide32_chunk(N);
+    const int splits = 8;
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->wide.ensure(wide32_work_bytes(C, splits)));
+    GLX_CK(wide_grad_tf32(w_ih, w_ho, X, XT, labels, N, ws->wide.as<unsigned char>(), C, splits, grad, st,
+                          [](bool) {}));
+    g_launches.fetch_add(3 + 5 * (uint64_t)((N + C - 1) / C));
+    return GLX_OK;
+}
+
+int glx_wide_train_tf32(float* w_ih, float* w_ho, const float* X, const float* XT, const uint8_t* labels, int64_t N,
+                        int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, void* stream) {
+    if (N < 32 || N % 32) return set_err(GLX_ERR_SHAPE, "wide tf32 training needs N %% 32 == 0 (got %lld)", (long long)N);
+    if (epochs < 0) return set_err(GLX_ERR_INVALID, "epochs must be >= 0");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t C = wide32_chunk(N);
+    const int splits = 8;
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->wide.ensure(wide32_work_bytes(C, splits)));
+    for (int64_t e = 0; e < epochs; e++) {
+        double* stats = stats_hist ? stats_hist + 3 * e : nullptr;
+        cudaEvent_t pe = nullptr;
+        cudaError_t perr = cudaSuccess;
+        auto prof = [&](bool begin) {
+            if (begin) {
+                cudaError_t r = prof_begin(st, &pe);
+                if (r != cudaSuccess) perr = r;
+            } else if (pe) {
+                cudaError_t r = cudaEventRecord(pe, st);
+                if (r != cudaSuccess) perr = r;
+                pe = nullptr;
+            }
+        };
+        GLX_CK(wide_epoch_tf32(w_ih, w_ho, X, XT, labels, N, lr, ws->wide.as<unsigned char>(), C, splits, stats,
+                               nonfinite, st, prof));
+        GLX_CK(perr);
+        g_launches.fetch_add(4 + 5 * (uint64_t)((N + C - 1) / C));
+    }
+    return GLX_OK;
+}
+
 int glx_wide_apply(float* w_ih, float* w_ho, const double* grad, double lr_over_n, int32_t* nonfinite, void* stream) {
     if (!grad) return set_err(GLX_ERR_INVALID, "grad must not be NULL");
     GLX_CK(wide_apply(w_ih, w_ho, grad, lr_over_n, nonfinite, (cudaStream_t)stream));

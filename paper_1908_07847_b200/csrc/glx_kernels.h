@@ -155,6 +155,16 @@ cudaError_t wide_apply(float* W1, float* W2, const double* grad, double lr_over_
 cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, const uint8_t* labels, int64_t N,
                        double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
                        cudaStream_t st, const std::function<void(bool)>& prof);
+// the tf32 variant: f32 rows X [N][1024] and [X,1]^T K-blocked [N/32][1025][32]
+cudaError_t launch_wide_gen_tf32(float* X, float* XT, uint8_t* labels, int64_t N, uint64_t seed, int64_t row0,
+                                 cudaStream_t st);
+size_t wide32_work_bytes(int64_t C, int splits);
+cudaError_t wide_grad_tf32(const float* W1, const float* W2, const float* X, const float* XT, const uint8_t* labels,
+                           int64_t N, unsigned char* work, int64_t C, int splits, double* grad, cudaStream_t st,
+                           const std::function<void(bool)>& prof);
+cudaError_t wide_epoch_tf32(float* W1, float* W2, const float* X, const float* XT, const uint8_t* labels, int64_t N,
+                            double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
+                            cudaStream_t st, const std::function<void(bool)>& prof);
 
 // ------------------------------------------------------------ diagnostics
 cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st);

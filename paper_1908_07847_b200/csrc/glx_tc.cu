@@ -71,6 +71,12 @@ __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
+// instruction descriptor: TF32 x TF32 -> F32, both K-major, M x N (tf32 MMAs take no
+// MN-major operands: every operand of the tf32 path is stored K-major)
+__host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
@@ -93,6 +99,15 @@ __device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t da, uint64_t
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc)
+        : "memory");
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(da), "l"(db), "r"(idesc), "r"(acc)
         : "memory");
 }
@@ -151,6 +166,13 @@ struct TcEpilogue {
     __nv_bfloat16* dht;
     int64_t ldt;  // row stride of the transposed outputs (d_t, dht) when t_blk == 0
     int t_blk;    // R > 0: transposed outputs K-blocked [M/64][R][64]
+    // tf32 path (f32 storage; transposed outputs K-blocked [M/32][t_blk][32], written
+    // with plain coalesced stores: a warp's 32 lanes are the 32 rows of one K block)
+    float* h32;         // 1: sigmoid(v + bias) row-major, row stride ldd (may be null)
+    float* t32;         // 1: the same transposed; 3: delta_h transposed
+    const float* hin32; // 3: h row-major, row stride ldh
+    float* do32;        // 2: delta_o row-major [M][32] (columns >= K zero)
+    float* doT32;       // 2: delta_o transposed [M/32][32][32]
 };
 
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* src, int c0, int c1) {
@@ -248,6 +270,95 @@ __device__ __forceinline__ void store_cols_bf16(EpiStage& sg, const uint32_t (&p
         b[(2 * e + 1) * 32 + lane] = (uint16_t)(pk[e] >> 16);
     }
     sg.release(sg.map_t, b, row0, col0, lane, sg.t_blocked);
+}
+
+// tf32 path epilogues (f32 results): lane = row, v = 32 consecutive columns n0 + c ..
+__device__ __forceinline__ void tc_epilogue_chunk_f32(const TcEpilogue& ep, const float (&v)[32], int M, int row,
+                                                      int n0, int c, int lane) {
+    const bool rv = row < M;
+    const int64_t kb = (int64_t)(row >> 5) * ep.t_blk;  // K block of this row (transposed outputs)
+    if (ep.kind == 0 || ep.kind == 4) {
+        if (rv) {
+            float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (int64_t)row * ep.ldd + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; q++) {
+                float4 o = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                if (ep.kind == 4) {
+                    const float4 p = dst[q];
+                    o.x += p.x;
+                    o.y += p.y;
+                    o.z += p.z;
+                    o.w += p.w;
+                }
+                dst[q] = o;
+            }
+        }
+    } else if (ep.kind == 1) {
+        float h[32];
+        const float4* b4 = reinterpret_cast<const float4*>(ep.bias + n0 + c);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const float4 b = __ldg(b4 + q);
+            const float bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++) h[4 * q + e] = 1.0f / (1.0f + __expf(-(v[4 * q + e] + bv[e])));
+        }
+        if (rv && ep.h32) {
+            float4* dst = reinterpret_cast<float4*>(ep.h32 + (int64_t)row * ep.ldd + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; q++) dst[q] = make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+        }
+        if (rv && ep.t32) {
+#pragma unroll
+            for (int j = 0; j < 32; j++) ep.t32[(kb + n0 + c + j) * 32 + (row & 31)] = h[j];
+        }
+    } else if (ep.kind == 2) {
+        // output neuron (kernels.py:352-375 generalised to K outputs)
+        float loss = 0.f, correct = 0.f, wrong = 0.f;
+        if (rv) {
+            const int lab = ep.labels[row];
+            float best = -1.f;
+            int arg = 0;
+#pragma unroll
+            for (int k = 0; k < 32; k++) {
+                if (k >= ep.K) break;
+                const float o = 1.0f / (1.0f + __expf(-(v[k] + ep.bias[k])));
+                const float t = (k == lab) ? 1.f : 0.f;
+                const float d = (o - t) * o * (1.0f - o);
+                loss = fmaf(0.5f * (t - o), t - o, loss);
+                if (o > best) {
+                    best = o;
+                    arg = k;
+                }
+                ep.do32[(int64_t)row * 32 + k] = d;
+                ep.doT32[((int64_t)(row >> 5) * 32 + k) * 32 + (row & 31)] = d;
+            }
+            correct = arg == lab ? 1.f : 0.f;
+            wrong = 1.f - correct;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            loss += __shfl_xor_sync(0xffffffffu, loss, o);
+            correct += __shfl_xor_sync(0xffffffffu, correct, o);
+            wrong += __shfl_xor_sync(0xffffffffu, wrong, o);
+        }
+        if (lane == 0 && ep.stats) {
+            atomicAdd(ep.stats + 0, (double)loss);
+            atomicAdd(ep.stats + 1, (double)correct);
+            atomicAdd(ep.stats + 2, (double)wrong);
+        }
+    } else if (rv) {
+        // delta_h = (delta_o W2)_j * h (1 - h), transposed (the dW1 GEMM's K-major B operand)
+        const float4* hp = reinterpret_cast<const float4*>(ep.hin32 + (int64_t)row * ep.ldh + n0 + c);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            const float4 h4 = hp[q];
+            const float hv[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+            for (int e = 0; e < 4; e++)
+                ep.t32[(kb + n0 + c + 4 * q + e) * 32 + (row & 31)] = v[4 * q + e] * hv[e] * (1.f - hv[e]);
+        }
+    }
 }
 
 template <int BN>
@@ -361,7 +472,9 @@ __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const fl
 // (2 x BN columns), so the epilogue of tile i overlaps the MMAs of tile i+1.
 // Tiles are walked (split z, M, N) with N fastest, so concurrently running
 // CTAs share their A tile through L2.
-template <int BN>
+// TF: the tf32 variant (f32 operands, kind::tf32, 32 K-elements per 128-byte row, f32
+// epilogues); same stage bytes, same 4 MMAs (32 bytes of K each) per k-block.
+template <int BN, bool TF>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
                                                                   const __grid_constant__ CUtensorMap map_b,
                                                                   const __grid_constant__ CUtensorMap map_d,
@@ -369,8 +482,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                                                                   int M,
                                                                   int N, int K, int kb_per_split, int n_mt, int n_nt,
                                                                   int n_zt, TcEpilogue ep) {
-    constexpr uint32_t kABytes = kTcBM * kTcBK * 2;
-    constexpr uint32_t kBBytes = BN * kTcBK * 2;
+    constexpr int kBKe = TF ? 32 : kTcBK;  // K elements per 128-byte row
+    constexpr uint32_t kABytes = kTcBM * 128;
+    constexpr uint32_t kBBytes = BN * 128;
     constexpr uint32_t kStage = kABytes + kBBytes;
     constexpr int kTcStages = tc_stages(BN);
     constexpr uint32_t kCols = 2 * BN < 32 ? 32 : 2 * BN;  // two accumulators
@@ -385,7 +499,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     uint16_t* stg_all = reinterpret_cast<uint16_t*>(sm + kTcStages * kStage + 256);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nkt = K / kTcBK;
+    const int nkt = K / kBKe;
     const int tiles = n_mt * n_nt * n_zt;
 
     if (warp == 0 && lane == 0) {
@@ -432,24 +546,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
                     unsigned char* st = sm + s * kStage;
                     mbar_arrive_expect_tx(&full[s], kStage);
-                    if (flags & 8) {  // MN-major A: two 64 (M) x 64 (K) swizzled atoms
-                        tma_load_2d(st, &map_a, m0, (kb0 + kb) * kTcBK, &full[s]);
-                        tma_load_2d(st + kABytes / 2, &map_a, m0 + 64, (kb0 + kb) * kTcBK, &full[s]);
+                    if (!TF && (flags & 8)) {  // MN-major A: two 64 (M) x 64 (K) swizzled atoms
+                        tma_load_2d(st, &map_a, m0, (kb0 + kb) * kBKe, &full[s]);
+                        tma_load_2d(st + kABytes / 2, &map_a, m0 + 64, (kb0 + kb) * kBKe, &full[s]);
                     } else if (flags & 1) tma_load_3d(st, &map_a, 0, m0, kb0 + kb, &full[s]);
-                    else tma_load_2d(st, &map_a, (kb0 + kb) * kTcBK, m0, &full[s]);
-                    if (flags & 16) {  // MN-major B: BN / 64 atoms of 64 (N) x 64 (K)
+                    else tma_load_2d(st, &map_a, (kb0 + kb) * kBKe, m0, &full[s]);
+                    if (!TF && (flags & 16)) {  // MN-major B: BN / 64 atoms of 64 (N) x 64 (K)
 #pragma unroll
                         for (int i = 0; i < BN / 64; i++)
-                            tma_load_2d(st + kABytes + i * 8192, &map_b, n0 + 64 * i, (kb0 + kb) * kTcBK, &full[s]);
+                            tma_load_2d(st + kABytes + i * 8192, &map_b, n0 + 64 * i, (kb0 + kb) * kBKe, &full[s]);
                     } else if (flags & 2) tma_load_3d(st + kABytes, &map_b, 0, n0, kb0 + kb, &full[s]);
-                    else tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kTcBK, n0, &full[s]);
+                    else tma_load_2d(st + kABytes, &map_b, (kb0 + kb) * kBKe, n0, &full[s]);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer
-            const bool a_mn = (flags & 8) != 0, b_mn = (flags & 16) != 0;
-            const uint32_t idesc = umma_idesc_bf16(kTcBM, BN) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
+            const bool a_mn = !TF && (flags & 8) != 0, b_mn = !TF && (flags & 16) != 0;
+            const uint32_t idesc = TF ? umma_idesc_tf32(kTcBM, BN)
+                                      : umma_idesc_bf16(kTcBM, BN) | (a_mn ? (1u << 15) : 0u) | (b_mn ? (1u << 16) : 0u);
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < tiles; t += gridDim.x, lt++) {
                 int z, m0, n0, kb0, nk;
@@ -465,13 +580,18 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                     const uint32_t a_addr = smem_u32(sm + s * kStage);
                     const uint32_t b_addr = a_addr + kABytes;
 #pragma unroll
-                    for (int kk = 0; kk < kTcBK / 16; kk++)
-                        umma_bf16(dcol,
-                                  a_mn ? umma_desc_sw128_mn(a_addr + kk * 16 * 128, kABytes / 2)
-                                       : umma_desc_sw128(a_addr + kk * 32),
-                                  b_mn ? umma_desc_sw128_mn(b_addr + kk * 16 * 128, 8192)
-                                       : umma_desc_sw128(b_addr + kk * 32),
-                                  idesc, (kb | kk) != 0);
+                    for (int kk = 0; kk < 4; kk++) {  // 32 bytes of K per MMA
+                        if constexpr (TF)
+                            umma_tf32(dcol, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
+                                      idesc, (kb | kk) != 0);
+                        else
+                            umma_bf16(dcol,
+                                      a_mn ? umma_desc_sw128_mn(a_addr + kk * 16 * 128, kABytes / 2)
+                                           : umma_desc_sw128(a_addr + kk * 32),
+                                      b_mn ? umma_desc_sw128_mn(b_addr + kk * 16 * 128, 8192)
+                                           : umma_desc_sw128(b_addr + kk * 32),
+                                      idesc, (kb | kk) != 0);
+                    }
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&tfull[acc]);
@@ -509,7 +629,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __uint_as_float(ra[i]);
-                        tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane, sg);
+                        if constexpr (TF) tc_epilogue_chunk_f32(e2, v, M, row, n0, c, lane);
+                        else tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane, sg);
                     }
                     if (!more) break;
                     tmem_wait();
@@ -518,7 +639,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __uint_as_float(rb[i]);
-                        tc_epilogue_chunk<BN>(e2, v, M, row, n0, c + 32, lane, sg);
+                        if constexpr (TF) tc_epilogue_chunk_f32(e2, v, M, row, n0, c + 32, lane);
+                        else tc_epilogue_chunk<BN>(e2, v, M, row, n0, c + 32, lane, sg);
                     }
                     tmem_wait();
                 }
@@ -584,6 +706,68 @@ static bool make_map_blk(CUtensorMap* map, const void* base, int64_t R, int64_t 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// f32 (tf32 operand) maps: row-major [rows x cols] with 32-column 128-byte-swizzled
+// boxes, and the K-blocked [nkb][R][32] layout
+static bool make_map_f32(CUtensorMap* map, const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+    cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+static bool make_map_blk32(CUtensorMap* map, const void* base, int64_t R, int64_t nkb, int box_rows) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {32, (cuuint64_t)R, (cuuint64_t)nkb};
+    cuuint64_t strides[2] = {32 * 4, (cuuint64_t)R * 32 * 4};
+    cuuint32_t box[3] = {32, (cuuint32_t)box_rows, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+static cudaError_t tc_launch_tf32(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
+    CUtensorMap ma, mb, md, mt;
+    memset(&md, 0, sizeof(md));
+    memset(&mt, 0, sizeof(mt));
+    const int64_t nkb = g.K / 32;
+    const bool oka = g.a_blk ? make_map_blk32(&ma, g.A, g.a_blk, nkb, kTcBM) : make_map_f32(&ma, g.A, g.M, g.K, g.lda, kTcBM);
+    const bool okb = g.b_blk ? make_map_blk32(&mb, g.B, g.b_blk, nkb, BN) : make_map_f32(&mb, g.B, g.N, g.K, g.ldb, BN);
+    if (!oka || !okb || g.a_mn || g.b_mn) return cudaErrorInvalidValue;
+    const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0);
+    const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * 128 + 256 + kTcStgBytes;
+    auto k = tc_gemm_kernel<BN, true>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int nk = g.K / 32;
+    const int splits = g.splits < 1 ? 1 : g.splits;
+    const int kps = (nk + splits - 1) / splits;
+    const int n_nt = g.N / BN, n_mt = (g.M + kTcBM - 1) / kTcBM, n_zt = (nk + kps - 1) / kps;
+    int sms = 148;
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int tiles = n_nt * n_mt * n_zt;
+    const int grid = tiles < sms ? tiles : sms;
+    k<<<grid, kTcThreads, smem, st>>>(ma, mb, md, mt, flags, g.M, g.N, g.K, kps, n_mt, n_nt, n_zt, ep);
+    return cudaGetLastError();
+}
+
+// the tf32 GEMM: D = A . B^T with f32 operands rounded to tf32 by the tensor core
+cudaError_t launch_tc_tf32(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
+    if (g.K % 32 != 0) return cudaErrorInvalidValue;
+    if (GLX_TC_MAXBN >= 256 && g.N % 256 == 0 && ep.kind != 2) return tc_launch_tf32<256>(g, ep, st);
+    if (GLX_TC_MAXBN >= 128 && g.N % 128 == 0 && ep.kind != 2) return tc_launch_tf32<128>(g, ep, st);
+    if (g.N % 64 == 0 && ep.kind != 2) return tc_launch_tf32<64>(g, ep, st);
+    if (g.N % 32 == 0) return tc_launch_tf32<32>(g, ep, st);
+    return cudaErrorInvalidValue;
+}
+
 template <int BN>
 static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t st) {
     CUtensorMap ma, mb, md, mt;
@@ -610,7 +794,7 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
     }
     const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0) | (g.a_mn ? 8 : 0) | (g.b_mn ? 16 : 0);
     const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 256 + kTcStgBytes;
-    auto k = tc_gemm_kernel<BN>;
+    auto k = tc_gemm_kernel<BN, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     const int nk = g.K / kTcBK;
@@ -664,7 +848,8 @@ __device__ __forceinline__ float unit_u01(uint64_t seed, uint64_t idx) {
 // X[r][i] ~ U[0,1) (counter-based hash), bf16; labels = argmax_k of 16 planted
 // linear scores over 32 fixed columns (a K-class analogue of synthetic_matrix's
 // planted-linear labels)
-__global__ void wide_gen_kernel(__nv_bfloat16* __restrict__ X, uint8_t* __restrict__ labels, int64_t N,
+template <typename T>
+__global__ void wide_gen_kernel(T* __restrict__ X, uint8_t* __restrict__ labels, int64_t N,
                                 uint64_t seed, int64_t row0) {
     const int64_t r = (int64_t)blockIdx.x * blockDim.y + threadIdx.y;
     if (r >= N) return;
@@ -674,10 +859,17 @@ __global__ void wide_gen_kernel(__nv_bfloat16* __restrict__ X, uint8_t* __restri
     for (int k = 0; k < kWK; k++) score[k] = 0.f;
     for (int i = threadIdx.x; i < kWD; i += 32) {
         const float v = unit_u01(seed, (uint64_t)rg * kWD + i);
-        const __nv_bfloat16 b = __float2bfloat16_rn(v);
-        X[r * kWD + i] = b;
+        float xv;  // the stored value (bf16 path: rounded to bf16; tf32 path: the f32 U[0,1) draw)
+        if constexpr (sizeof(T) == 2) {
+            const __nv_bfloat16 b = __float2bfloat16_rn(v);
+            X[r * kWD + i] = b;
+            xv = __bfloat162float(b);
+        } else {
+            X[r * kWD + i] = v;
+            xv = v;
+        }
         if ((i & 31) == 7) {  // 32 planted columns
-            const float vb = __bfloat162float(b) - 0.5f;  // centred: classes come out balanced
+            const float vb = xv - 0.5f;  // centred: classes come out balanced
 #pragma unroll
             for (int k = 0; k < kWK; k++) score[k] += (unit_u01(seed ^ 0xABCDEFULL, (uint64_t)k * kWD + i) - 0.5f) * vb;
         }
@@ -773,8 +965,8 @@ __global__ void wide_apply_kernel(float* __restrict__ W1, float* __restrict__ W2
 cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, int64_t row0,
                             cudaStream_t st) {
     dim3 blk(32, 8);
-    wide_gen_kernel<<<(unsigned)((N + 7) / 8), blk, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(Xb), labels, N, seed,
-                                                            row0);
+    wide_gen_kernel<__nv_bfloat16><<<(unsigned)((N + 7) / 8), blk, 0, st>>>(reinterpret_cast<__nv_bfloat16*>(Xb),
+                                                                           labels, N, seed, row0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 grid((unsigned)((N + 31) / 32), kWD / 32);
@@ -939,6 +1131,206 @@ cudaError_t wide_epoch(float* W1, float* W2, const void* Xb, const void* XT, con
     WideWork w;
     carve(&w, work, C, splits);
     cudaError_t e = wide_grad(W1, W2, Xb, XT, labels, N, work, C, splits, w.grad, st, prof);
+    if (e != cudaSuccess) return e;
+    if (stats && (e = cudaMemcpyAsync(stats, w.grad + kWP, 3 * sizeof(double), cudaMemcpyDeviceToDevice, st)) !=
+                     cudaSuccess)
+        return e;
+    return wide_apply(W1, W2, w.grad, lr / (double)N, nonfinite, st);
+}
+
+// =============================================== wide config, tf32 path
+// The same five GEMMs on tcgen05 kind::tf32 with f32 storage, for f32 U[0,1) rows
+// (SURVEY.md C5 "evaluated against the FP32 tolerance"): every operand K-major
+// (tf32 MMAs take no MN-major operands), so the epilogues write the transposed,
+// K-blocked ([rows/32][R][32]) copies the split-K GEMMs read:
+//   1. H = sigmoid(X W1^T + b1)   -> H (f32 row-major) and [H,1]^T (K-blocked, R = 1025)
+//   2. output layer (N = 32)      -> delta_o row-major [C][32] and K-blocked [C/32][32][32]
+//   3. dH = (delta_o W2) h(1-h)   -> dH^T K-blocked [C/32][1024][32]
+//   4. dW1^T += [X,1]^T dH        (A = [X,1]^T K-blocked, stored with the data)
+//   5. dW2^T += [H,1]^T delta_o
+// Rows >= 1025 of a 128-row M tile of the [.,1]^T operands read as zero (TMA OOB).
+constexpr int kWR = kWD + 1;  // rows of the [X,1]^T and [H,1]^T operands
+
+// [X,1]^T, K-blocked by 32 rows: element (i, r) at ((r / 32) * 1025 + i) * 32 + r % 32
+__global__ void wide_transpose32_kernel(const float* __restrict__ X, float* __restrict__ XT, int64_t N) {
+    __shared__ float tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int i0 = blockIdx.y * 32;
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t r = r0 + dy;
+        tile[dy][threadIdx.x] = r < N ? X[r * kWD + i0 + threadIdx.x] : 0.f;
+    }
+    __syncthreads();
+    for (int dy = threadIdx.y; dy < 32; dy += blockDim.y) {
+        const int64_t r = r0 + threadIdx.x;
+        if (r < N) XT[((r >> 5) * kWR + i0 + dy) * 32 + (r & 31)] = tile[threadIdx.x][dy];
+    }
+    if (blockIdx.y == 0 && threadIdx.y == 0) {
+        const int64_t r = r0 + threadIdx.x;
+        if (r < N) XT[((r >> 5) * kWR + kWD) * 32 + (r & 31)] = 1.f;
+    }
+}
+
+cudaError_t launch_wide_gen_tf32(float* X, float* XT, uint8_t* labels, int64_t N, uint64_t seed, int64_t row0,
+                                 cudaStream_t st) {
+    wide_gen_kernel<float><<<(unsigned)((N + 7) / 8), dim3(32, 8), 0, st>>>(X, labels, N, seed, row0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 grid((unsigned)((N + 31) / 32), kWD / 32);
+    wide_transpose32_kernel<<<grid, dim3(32, 8), 0, st>>>(X, XT, N);
+    return cudaGetLastError();
+}
+
+// f32 operand copies of the master weights for this epoch: W1 without its bias
+// column (16-byte rows for TMA), W2 padded to 32 outputs, W2^T [1024][32]
+__global__ void wide_derive32_kernel(const float* __restrict__ W1, const float* __restrict__ W2,
+                                     float* __restrict__ W1p, float* __restrict__ b1, float* __restrict__ W2p,
+                                     float* __restrict__ b2, float* __restrict__ W2T) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < kWH * kWD) {
+        const int j = e / kWD, i = e % kWD;
+        W1p[e] = W1[(int64_t)j * kWR + i];
+    }
+    if (e < kWH) b1[e] = W1[(int64_t)e * kWR + kWD];
+    if (e < 32 * kWH) {
+        const int k = e / kWH, j = e % kWH;
+        W2p[e] = k < kWK ? W2[k * (kWH + 1) + j] : 0.f;
+        const int j2 = e / 32, k2 = e % 32;
+        W2T[e] = k2 < kWK ? W2[k2 * (kWH + 1) + j2] : 0.f;
+    }
+    if (e < kWK) b2[e] = W2[e * (kWH + 1) + kWH];
+}
+
+// row 1024 of the K-blocked [H,1]^T chunk buffer: the bias input 1
+__global__ void ht_bias_row_kernel(float* __restrict__ HT, int64_t C) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < C) HT[((r >> 5) * kWR + kWD) * 32 + (r & 31)] = 1.f;
+}
+
+struct WideWork32 {
+    float *W1p, *b1, *W2p, *b2, *W2T;
+    float* H;    // [C][1024]
+    float* HT;   // [C/32][1025][32]
+    float* dob;  // [C][32]
+    float* doT;  // [C/32][32][32]
+    float* dhT;  // [C/32][1024][32]
+    float* dW1T;
+    float* dW2T;
+    double* grad;
+};
+
+static size_t carve32(WideWork32* w, unsigned char* base, int64_t C, int splits) {
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        void* p = base ? base + o : nullptr;
+        o += (bytes + 255) / 256 * 256;
+        return (float*)p;
+    };
+    WideWork32 t;
+    t.W1p = take((size_t)kWH * kWD * 4);
+    t.b1 = take(kWH * 4);
+    t.W2p = take(32 * kWH * 4);
+    t.b2 = take(64 * 4);
+    t.W2T = take((size_t)kWH * 32 * 4);
+    t.H = take((size_t)C * kWH * 4);
+    t.HT = take((size_t)C * kWR * 4);
+    t.dob = take((size_t)C * 32 * 4);
+    t.doT = take((size_t)C * 32 * 4);
+    t.dhT = take((size_t)C * kWH * 4);
+    t.dW1T = take((size_t)splits * kWMi * kWH * 4);
+    t.dW2T = take((size_t)kWSplits2 * kWMi * 32 * 4);
+    t.grad = (double*)take((size_t)(kWP + 3) * 8);
+    if (w) *w = t;
+    return o;
+}
+
+size_t wide32_work_bytes(int64_t C, int splits) { return carve32(nullptr, nullptr, C, splits); }
+
+cudaError_t wide_grad_tf32(const float* W1, const float* W2, const float* X, const float* XT, const uint8_t* labels,
+                           int64_t N, unsigned char* work, int64_t C, int splits, double* grad, cudaStream_t st,
+                           const std::function<void(bool)>& prof) {
+    WideWork32 w;
+    carve32(&w, work, C, splits);
+    cudaError_t e;
+    if (!grad) grad = w.grad;
+    double* stats = grad + kWP;
+    if ((e = cudaMemsetAsync(stats, 0, 3 * sizeof(double), st)) != cudaSuccess) return e;
+    wide_derive32_kernel<<<(kWH * kWD + 255) / 256, 256, 0, st>>>(W1, W2, w.W1p, w.b1, w.W2p, w.b2, w.W2T);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    const int64_t zstride = (int64_t)kWMi * kWH, zstride2 = (int64_t)kWMi * 32;
+    if ((e = cudaMemsetAsync(w.dW1T, 0, (size_t)splits * zstride * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)kWSplits2 * zstride2 * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 32 * 4, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(w.doT, 0, (size_t)C * 32 * 4, st)) != cudaSuccess) return e;
+    ht_bias_row_kernel<<<(unsigned)((C + 255) / 256), 256, 0, st>>>(w.HT, C);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    for (int64_t r0 = 0; r0 < N; r0 += C) {
+        const int Cc = (int)std::min<int64_t>(C, N - r0);
+        prof(true);
+        {  // 1. hidden layer -> H, [H,1]^T
+            TcGemm g{X + r0 * kWD, w.W1p, Cc, kWH, kWD, kWD, kWD, 1};
+            TcEpilogue ep{};
+            ep.kind = 1;
+            ep.bias = w.b1;
+            ep.h32 = w.H;
+            ep.ldd = kWH;
+            ep.t32 = w.HT;
+            ep.t_blk = kWR;
+            if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 2. output layer -> delta_o, loss, accuracy
+            TcGemm g{w.H, w.W2p, Cc, 32, kWH, kWH, kWH, 1};
+            TcEpilogue ep{};
+            ep.kind = 2;
+            ep.bias = w.b2;
+            ep.labels = labels + r0;
+            ep.K = kWK;
+            ep.do32 = w.dob;
+            ep.doT32 = w.doT;
+            ep.stats = stats;
+            if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 3. hidden deltas -> dH^T (K-blocked)
+            TcGemm g{w.dob, w.W2T, Cc, kWH, 32, 32, 32, 1};
+            TcEpilogue ep{};
+            ep.kind = 3;
+            ep.hin32 = w.H;
+            ep.ldh = kWH;
+            ep.t32 = w.dhT;
+            ep.t_blk = kWH;
+            if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 4. dW1^T += [X,1]^T dH (split-K over the chunk's rows)
+            TcGemm g{XT + r0 * kWR, w.dhT, kWR, kWH, Cc, 0, 0, splits, kWR, kWH};
+            TcEpilogue ep{};
+            ep.kind = 4;
+            ep.d_f32 = w.dW1T;
+            ep.ldd = kWH;
+            ep.zstride = zstride;
+            if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
+        }
+        {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32, delta_o columns >= 16 zero)
+            TcGemm g{w.HT, w.doT, kWR, 32, Cc, 0, 0, kWSplits2, kWR, 32};
+            TcEpilogue ep{};
+            ep.kind = 4;
+            ep.d_f32 = w.dW2T;
+            ep.ldd = 32;
+            ep.zstride = zstride2;
+            if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
+        }
+        prof(false);
+    }
+    wide_reduce_kernel<<<(kWP + 255) / 256, 256, 0, st>>>(w.dW1T, splits, zstride, w.dW2T, kWSplits2, zstride2,
+                                                         grad);
+    return cudaGetLastError();
+}
+
+cudaError_t wide_epoch_tf32(float* W1, float* W2, const float* X, const float* XT, const uint8_t* labels, int64_t N,
+                            double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
+                            cudaStream_t st, const std::function<void(bool)>& prof) {
+    WideWork32 w;
+    carve32(&w, work, C, splits);
+    cudaError_t e = wide_grad_tf32(W1, W2, X, XT, labels, N, work, C, splits, w.grad, st, prof);
     if (e != cudaSuccess) return e;
     if (stats && (e = cudaMemcpyAsync(stats, w.grad + kWP, 3 * sizeof(double), cudaMemcpyDeviceToDevice, st)) !=
                      cudaSuccess)
