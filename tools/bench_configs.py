@@ -218,6 +218,32 @@ def config5(L, peak, cpu=None, rows=16_777_216, epochs=3):
                     "frac_bf16_peak is against MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"}
 
 
+def config5_tf32(L, peak, cpu=None, rows=16_777_216, epochs=2):
+    """Wide 1024 -> 1024 -> 16 on 16Mi f32 rows, full batch, tcgen05 kind::tf32 with f32 H and
+    deltas (the precision held to the 1e-4 FP32 tolerance, tests/test_gpu_tc.py)."""
+    from paper_1908_07847_b200 import wide
+
+    data = wide.WideData(rows, seed=0, precision="tf32")
+    w1, w2 = wide.init_wide_weights(seed=0)
+    dev = torch.device("cuda")
+    W1 = torch.from_numpy(w1).to(dev)
+    W2 = torch.from_numpy(w2).to(dev)
+    st = torch.cuda.current_stream().cuda_stream
+    run = lambda e: _lib.check(L.glx_wide_train_tf32(W1.data_ptr(), W2.data_ptr(), data.Xb.data_ptr(),
+                                                     data.XT.data_ptr(), data.labels.data_ptr(), rows, e, 0.1, None,
+                                                     None, st))
+    run(1)
+    ms = timed(lambda: run(epochs)) / epochs
+    flops = rows * f_train(1024, 1024, 16)
+    import bench as _bench
+
+    tf32 = _bench.tf32_peak_cublas(dev)
+    return {"config": "5 (tf32): wide 1024->1024->16, 16Mi f32 rows, full batch, tcgen05 kind::tf32, f32 H / deltas",
+            "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
+            "tflops_algorithmic": flops / (ms * 1e-3) / 1e12, "tf32_peak_tflops_cublas": tf32,
+            "frac_tf32_peak": flops / (ms * 1e-3) / 1e12 / tf32}
+
+
 def eval_rate(L, peak, cpu=None):
     x, l = g.synthetic_arrays(1_000_000, 33, 0, "planted-linear")
     out = {}
@@ -291,7 +317,8 @@ def norm_rate(L, peak, cpu=None, rows=67_108_864, D=33):
             "pack_rows_minmax_ms": t_packn, "pack_rows_minmax_gbs": pb / (t_packn * 1e-3) / 1e9}
 
 
-SUITE = {"1": config1, "3": config3, "4": config4_1gpu, "5": config5, "eval": eval_rate, "norm": norm_rate}
+SUITE = {"1": config1, "3": config3, "4": config4_1gpu, "5": config5, "5tf32": config5_tf32, "eval": eval_rate,
+         "norm": norm_rate}
 
 
 def run_suite(which: str, out: str | None = None, cpu=None) -> dict:
