@@ -89,6 +89,9 @@ constexpr int kEpiBar = 1;
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
 constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
+#ifndef GLX_BTC_RCP2
+#define GLX_BTC_RCP2 1  // 1: one MUFU reciprocal per element pair (0: one per element)
+#endif
 #ifndef GLX_BTC_RN2
 #define GLX_BTC_RN2 0  // 1: tf32 rounding of the hidden deltas on the FMA pipe (pairs)
 #endif
@@ -254,7 +257,18 @@ __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.
 // round-to-nearest (ties away from zero) tf32, as cvt.rna.tf32.f32: unbiased operand
 // rounding is what lets single-product terms meet the 1e-5 parity bar
 // (tools/tf32_split_error.py); the MMA ignores the 13 low bits of any operand
-__device__ __forceinline__ uint32_t tf32_rn(float v) { return (__float_as_uint(v) + 0x1000u) & kTf32Mask; }
+#ifndef GLX_BTC_CVT
+#define GLX_BTC_CVT 0  // 1: cvt.rn.satfinite.tf32.f32 (one F2FP: measured slower), 0: integer round-half-away
+#endif
+__device__ __forceinline__ uint32_t tf32_rn(float v) {
+#if GLX_BTC_CVT
+    uint32_t r;
+    asm("cvt.rn.satfinite.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return r;
+#else
+    return (__float_as_uint(v) + 0x1000u) & kTf32Mask;
+#endif
+}
 // the same rounding for a pair on the FMA pipe (Veltkamp split: t = v (2^13 + 1),
 // hi = t - (t - v) keeps the leading 11 significant bits, round to nearest even;
 // |v| < 2^114 so t cannot overflow)
@@ -268,11 +282,13 @@ __device__ __forceinline__ float2 tf32_rn2(float2 v) {
 // in fp32 Horner, on par with ex2.approx), exponent inserted with an integer add;
 // |x| clamped to 125 (1 + 2^-125 == 1 and 1 / (1 + 2^125) ~ 0 in fp32 either way)
 #ifndef GLX_BTC_POLY
-#define GLX_BTC_POLY 2  // element pairs per GLX_BTC_POLY_DEN that take the polynomial (0: all MUFU)
+#define GLX_BTC_POLY 0  // element pairs per GLX_BTC_POLY_DEN that take the polynomial (0: all MUFU)
 #endif
 #ifndef GLX_BTC_POLY_DEN
 #define GLX_BTC_POLY_DEN 8
 #endif
+__device__ __forceinline__ float2 fminf2(float2 a, float2 b) { return make_float2(fminf(a.x, b.x), fminf(a.y, b.y)); }
+
 __device__ __forceinline__ float2 exp2_poly2(float2 x) {
     x.x = fminf(fmaxf(x.x, -125.f), 125.f);
     x.y = fminf(fmaxf(x.y, -125.f), 125.f);
@@ -555,6 +571,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             if (rb == 1) bar_sync(kTok1, NEW * 32);           // block 0 finished its pass 1 of tile lt
             else if (lt >= 1) bar_sync(kTok0, NEW * 32);      // block 1 finished its pass 1 of tile lt - 1
 #endif
+            BTT(5);
             // pass 1: h = sigmoid(z) (z prescaled by -log2 e)
             if (active) {
 #pragma unroll
@@ -566,12 +583,23 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     const float2 e2 = ((i >> 1) % GLX_BTC_POLY_DEN < GLX_BTC_POLY)
                                           ? exp2_poly2(make_float2(h[i], h[i + 1]))
                                           : make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
+#if GLX_BTC_RCP2
+                    // one MUFU reciprocal per pair: 1/a = b / (ab), 1/b = a / (ab); e clamped to
+                    // 2^60 so ab stays finite (h < 2^-60 there either way)
+                    const float2 den = __fadd2_rn(fminf2(e2, bcast2(1.152921504606847e18f)), bcast2(1.0f));
+                    const float r = rcp_approx(den.x * den.y);
+                    const float2 hh = __fmul2_rn(make_float2(den.y, den.x), bcast2(r));
+                    h[i] = hh.x;
+                    h[i + 1] = hh.y;
+#else
                     const float2 den = __fadd2_rn(e2, bcast2(1.0f));
                     h[i] = rcp_approx(den.x);
                     h[i + 1] = rcp_approx(den.y);
 #endif
+#endif
                 }
             }
+            BTT(6);
 #if GLX_BTC_TOKEN
             bar_arrive(rb == 0 ? kTok1 : kTok0, NEW * 32);  // the other block's turn on the MUFU pipe
 #endif
@@ -638,7 +666,6 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                     tc_fence_after();
                 }
             }
-            BTT(6);
             // pass 2: dh = delta_o h (1 - h) -> TMEM (tf32 hi in place of Z, FULL: + lo);
             // dW2 += delta_o h
             const uint32_t locol = tmem + lanebase + kColLo + 64 * hf + 32 * rb;
@@ -683,7 +710,6 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             if (lt >= 1 && lt % kDrain == 0 && active) {
                 mbar_wait(drain_bar, (uint32_t)((lt / kDrain) - 1) & 1);
                 tc_fence_after();
-                BTT(5);
                 drain();
             }
             tmem_st_wait();
@@ -793,9 +819,10 @@ extern "C" void glx_btc_timing_dump(void) {
     for (int t = 0; t < 16; t++) {
         printf("lt %2d", t + 8);
         for (int w : {0, 2}) {
-            printf(" | rb%d start %7lld waitz %5lld p1 %5lld bar %5lld rows %5lld drain %5lld p2 %5lld", w / 2,
-                   at(t, 0, w) - t0, at(t, 1, w) - at(t, 0, w), at(t, 2, w) - at(t, 1, w), at(t, 3, w) - at(t, 2, w),
-                   at(t, 4, w) - at(t, 3, w), at(t, 6, w) - at(t, 4, w), at(t, 7, w) - at(t, 6, w));
+            printf(" | rb%d @%7lld z %4lld tok %4lld sig %4lld red %4lld bar %4lld rows %4lld p2 %4lld", w / 2,
+                   at(t, 0, w) - t0, at(t, 1, w) - at(t, 0, w), at(t, 5, w) - at(t, 1, w), at(t, 6, w) - at(t, 5, w),
+                   at(t, 2, w) - at(t, 6, w), at(t, 3, w) - at(t, 2, w), at(t, 4, w) - at(t, 3, w),
+                   at(t, 7, w) - at(t, 4, w));
         }
         printf(" | mma bwd: wait %5lld @%7lld issue %4lld | fwd: wait %5lld @%7lld issue %4lld | load @%7lld %5lld\n",
                at(t, 9, 1) - at(t, 8, 1), at(t, 9, 1) - t0, at(t, 10, 1) - at(t, 9, 1), at(t, 12, 1) - at(t, 11, 1),
