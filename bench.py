@@ -362,27 +362,30 @@ def run_gpu(args):
               "hbm_frac": n_local * (4 * D + 1) / (k_ms * 1e-3) / 1e9 / peaks().get("hbm_gbs", 6545.9),
               "fp32_peak_tflops": fp32_peak, "fp32_frac": achieved / fp32_peak}
     if kind == 2:
-        # tcgen05 kind::tf32, 3xTF32: per 64-row tile 30 forward MMAs (M=128 units, N=64 rows,
-        # K=8) and 48 backward MMAs (M=128, N=48 features, K=8 rows) per 128-unit half pair
+        # tcgen05 kind::tf32: per 64-row tile and 128-unit half, FAST precision
+        # (>= 2^17 rows) runs 10 forward MMAs (M=128 units, N=64 rows, K=8: hi(W) x + lo(W) x over
+        # K=40) and 8 backward MMAs (M=128, N=48 features, K=8 rows); FULL (3xTF32) 15 + 24
         tf32_derived = peaks().get("bf16_tflops_sustained", 1355.8) / 2
         tf32_peak = max(tf32_meas, tf32_derived)
         tiles = -(-n_local // 64)
-        mma_flops = tiles * (H // 128) * (15 * 2 * 128 * 64 * 8 + 24 * 2 * 128 * 48 * 8)
+        fast = n_local >= (1 << 17)
+        nf, nb = (10, 8) if fast else (15, 24)
+        mma_flops = tiles * (H // 128) * (nf * 2 * 128 * 64 * 8 + nb * 2 * 128 * 48 * 8)
         mufu_peak = 148 * 16 * clk_mhz_for_peak(local) * 1e6
         roofline = {"bound": "tensor", "achieved": achieved, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": achieved / tf32_peak,
-                    "kernel": "batchtc_kernel<2> (tcgen05 kind::tf32, 3xTF32, deltas in TMEM)",
+                    "kernel": f"batchtc_kernel<2, {'FAST' if fast else 'FULL'}> (tcgen05 kind::tf32, deltas in TMEM)",
                     "tf32_cublas_measured_tflops": tf32_meas, "tf32_half_of_bf16_tflops": tf32_derived,
-                    "fp32_accurate_peak": tf32_peak / 3,
-                    "frac_of_fp32_accurate_peak": achieved / (tf32_peak / 3),
                     "executed_mma_flops_per_launch": mma_flops,
                     "executed_mma_frac": mma_flops / (k_ms * 1e-3) / 1e12 / tf32_peak,
-                    "mufu_frac": 2 * n_local * H / (k_ms * 1e-3) / mufu_peak,
+                    "mufu_ops_per_launch": 1.5 * n_local * H,
+                    "mufu_frac": 1.5 * n_local * H / (k_ms * 1e-3) / mufu_peak,
+                    "binding_resource": "the epilogue (sigmoid on MUFU, shuffle/FMA row and delta passes), "
+                                        "not the tensor pipe: mufu_frac and the ncu capture in profiles/",
                     "peak_source": "dense TF32 = max(cuBLAS 8192^3 TF32 GEMM measured in this run, half of "
-                                   "MEASURED_PEAKS.json bf16_tflops_sustained); fp32_accurate_peak = TF32 / 3 "
-                                   "(3xTF32 spends three TF32 MMAs per fp32-accurate product); executed_mma_frac "
-                                   "counts the 3xTF32 MMA work incl. K/N padding; mufu_frac = 2 MUFU ops per "
-                                   "hidden activation / (148 SMs x 16/clk x SM clock)",
+                                   "MEASURED_PEAKS.json bf16_tflops_sustained); executed_mma_frac counts the MMA "
+                                   "work incl. K/N padding; mufu_frac = 1.5 MUFU ops per hidden activation (ex2 "
+                                   "+ one reciprocal per pair) / (148 SMs x 16/clk x max SM clock)",
                     **common}
     else:
         roofline = {"bound": "fp32", "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
