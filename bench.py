@@ -401,14 +401,20 @@ def run_gpu(args):
 
     if rank == 0:
         cpu = None
+        secondary = None
         if world == 1:
             n_cpu = min(CPU_ROWS, host_x.shape[0])
             cpu = cpu_baseline_batch(host_x.numpy()[:n_cpu], host_t.numpy()[:n_cpu])
+            if not args.no_secondary:
+                del eng, host_x, host_t
+                torch.cuda.empty_cache()
+                secondary = secondary_configs(L, fp32_peak)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
                 "config": config_dict(args.workload, world), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "final_loss_sum": final_loss,
+                "secondary_configs": secondary,
                 "path": "glx_train_batch (fused single-GPU loop)" if comm is None else
                         "glx_dp_train_batch (epoch kernel, f64 gradient, library-owned ncclAllReduce, update; "
                         "CUDA graph replay)"}
@@ -418,6 +424,51 @@ def run_gpu(args):
     if ctrl is not None:
         ctrl.barrier()
         ctrl.destroy_process_group()
+
+
+def secondary_configs(L, fp32_peak):
+    """The other named configurations measured in the same run on the same GPU (BASELINE.json
+    configs 1, 3, 5 and config 2 at the reference's default width H = 33), device-timed,
+    bounded to a few seconds each (tools/bench_configs.py; CPU legs: bench.py --suite)."""
+    import torch
+
+    import paper_1908_07847_b200 as g
+    from paper_1908_07847_b200 import _lib
+
+    sys.path.insert(0, str(ROOT / "tools"))
+    sys.path.insert(0, str(ROOT / "tests"))
+    import bench_configs as bc
+
+    out = {}
+    for name, fn in (("config1", lambda: bc.config1(L, fp32_peak)), ("config3", lambda: bc.config3(L, fp32_peak)),
+                     ("config5_bf16", lambda: bc.config5(L, fp32_peak))):
+        try:
+            out[name] = fn()
+        except Exception as e:  # reported, never fatal to the headline line
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+        torch.cuda.empty_cache()
+    # config 2 at the reference default width (33 -> 33 -> 1, 1M rows): the FP32 two-role kernel
+    rows, h33 = 1_000_000, 33
+    X, lab = g.synthetic_arrays_device(rows, D, 0, "planted-linear")
+    Xp = torch.empty((rows, int(L.glx_packed_ld(D))), device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.glx_pack_rows(X.data_ptr(), None, lab.data_ptr(), rows, D, Xp.data_ptr(), st))
+    net = g.init_weights(g.NetworkConfig(input_dim=D, hidden_dim=h33, seed=0))
+    w1, w2 = torch.from_numpy(net.w_ih).cuda(), torch.from_numpy(net.w_ho).cuda()
+    run = lambda k: _lib.check(L.glx_train_batch(w1.data_ptr(), w2.data_ptr(), Xp.data_ptr(), rows, D, h33, k, LR,
+                                                 None, None, st))
+    run(5)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run(200)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 200
+    out["config2_h33"] = {"config": "2 at H = 33: synthetic_matrix(1_000_000, 33, 0, planted-linear), 33->33->1",
+                          "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
+                          "kernel_kind": int(L.glx_batch_kernel_kind(rows, D, h33)),
+                          "frac_fp32_peak": rows * f_train(D, h33) / (ms * 1e-3) / 1e12 / fp32_peak}
+    return out
 
 
 def run_e2e(g, dp, comm, x, t, rows_total, barrier, max_over_ranks, reps=3):
@@ -539,6 +590,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
     ap.add_argument("--workload", choices=tuple(WORKLOADS), default="c4")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the other configurations measured after the headline (N = 1)")
     ap.add_argument("--suite", default=None,
                     help="secondary configurations instead of the headline, e.g. 1,3,4,5,eval,norm")
     ap.add_argument("--out", default=None, help="with --suite: write the results JSON here")
