@@ -304,7 +304,8 @@ bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
     }
     // the three-role kernel wins where its forward/backward tiles are 4 units wide
     // (H % 4 == 0); narrower tiles stay on the two-role kernel (profiles/r01_summary.md)
-    if (pref >= 1 && batch3_geometry(N, D, H, sm_count_current(), g) && g->MT == 4) {
+    static const bool any_mt = getenv("GLX_BATCH3_ANY_MT") != nullptr;  // diagnostic: MT < 4 tiles too
+    if (pref >= 1 && batch3_geometry(N, D, H, sm_count_current(), g) && (g->MT == 4 || any_mt)) {
         *kind = 1;
         return true;
     }
