@@ -287,10 +287,11 @@ int batch_kernel_pref() {
     return v;
 }
 
-// the tcgen05 kernel's per-tile time is set by its epilogue warps (32 units x 32 rows
-// each), so narrow layers leave most of its warps idle: below 96 units the FP32
-// kernels are as fast (GLX_BATCH_KERNEL=tc forces the tcgen05 kernel for any H <= 256)
-constexpr int kTcMinH = 96;
+// the tcgen05 kernel's per-tile time is set by its epilogue chain (32 units x 32 rows
+// per warp), so narrow layers cost about as much as 128 units (0.115-0.12 ms per 1M
+// rows for H <= 128, tools/batch_width_time.py); the FP32 kernels win below ~24 units
+// (H = 16: 0.090 vs 0.116 ms). GLX_BATCH_KERNEL=tc forces the tcgen05 kernel for any H <= 256
+constexpr int kTcMinH = 24;
 bool force_tc() {
     const char* e = getenv("GLX_BATCH_KERNEL");
     return e && e[0] == 't' && e[1] == 'c';

@@ -133,7 +133,11 @@ struct BtcSmem {  // byte offsets
 };
 
 // warp 0 producer, warp 1 MMA, warps 2 .. 2 + 8 NH - 1 epilogue
-__host__ __device__ constexpr int btc_threads(int NH) { return (2 + 8 * NH) * 32; }
+// epilogue groups: with one 128-unit half (NH = 1) the FAST kernel runs two groups of 8
+// warps on alternate tiles (the per-tile chain of a row block, not throughput, bounds
+// the narrow layer); NH = 2 and FULL run one group
+__host__ __device__ constexpr int btc_groups(int NH, bool FULL) { return (NH == 1 && !FULL) ? 2 : 1; }
+__host__ __device__ constexpr int btc_threads(int NH, bool FULL) { return (2 + 8 * NH * btc_groups(NH, FULL)) * 32; }
 
 template <bool FULL>
 __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
@@ -142,8 +146,9 @@ __host__ __device__ constexpr BtcSmem btc_smem(int NH) {
     s.w = 0;
     s.x = s.w + 2 * NH * kWT;          // stage i at x + i * STAGE: [xf hi | xt hi (| xf lo | xt lo)]
     s.opart = s.x + P::S * P::STAGE;
-    s.dob = s.opart + 2 * 8 * NH * 32 * 4;  // output partials, double-buffered by tile parity
-    s.stat = s.dob + 8 * NH * 32 * 4;  // dob: one 32-row slot per epilogue warp
+    const int nw = 8 * NH * btc_groups(NH, FULL);  // epilogue warps
+    s.dob = s.opart + 2 * nw * 32 * 4;  // output partials, double-buffered by tile parity
+    s.stat = s.dob + nw * 32 * 4;       // dob: one 32-row slot per epilogue warp
     s.bars = s.stat;                   // (the row statistics reuse the partials buffer at the end)
     s.total = s.bars + 256;
     return s;
@@ -305,11 +310,15 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
 }
 
 template <int NH, bool FULL, bool PAD>
-__global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcArgs a) {
-    constexpr int NEW = 8 * NH;  // epilogue warps: 4 lane quadrants x NH unit halves x 2 row blocks
+__global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const BtcArgs a) {
+    constexpr int G = btc_groups(NH, FULL);  // epilogue groups, on alternate tiles
+    constexpr int NEWG = 8 * NH;             // warps per group: 4 lane quadrants x NH unit halves x 2 row blocks
+    constexpr int NEW = NEWG * G;            // epilogue warps
     using P = Pipe<FULL>;
     constexpr BtcSmem L = btc_smem<FULL>(NH);
-    constexpr int kS = P::S, kZB = P::ZB;
+    constexpr int kS = P::S;
+    constexpr int kZB = FULL ? 2 : (G == 2 ? 4 : 3);  // Z^T buffers (64 NH columns each)
+    static_assert(kDrain % G == 0, "the drained tiles must all belong to group 0");
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
     uint64_t* x_full = bars;                // tile stage loaded (bulk-copy bytes)
@@ -338,7 +347,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             mbar_init(&x_empty[i], 1);
         }
         for (int b = 0; b < kZB; b++) mbar_init(&z_full[b], 1);
-        for (int b = 0; b < 2 * kZB; b++) mbar_init(&dh_ready[b], NEW / 2);
+        for (int b = 0; b < 2 * kZB; b++) mbar_init(&dh_ready[b], NEWG / 2);
         mbar_init(drain_bar, 1);
         mbar_init(fin_bar, 1);
         mbar_init(bwd_done, 1);
@@ -432,7 +441,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
                     const uint32_t d = tmem + kColW + 48 * hf;
-                    const uint32_t ahi = tmem + kColZ + 128 * zb + 64 * hf, alo = tmem + kColLo + 64 * hf;
+                    const uint32_t ahi = tmem + kColZ + 64 * NH * zb + 64 * hf, alo = tmem + kColLo + 64 * hf;
 #pragma unroll
                     for (int s = 0; s < kR / 8; s++) {
                         const uint32_t acc = (lt % kDrain) != 0 || s != 0;
@@ -467,7 +476,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 const uint64_t dxl = dx + ((kXF + kXT) >> 4);  // FULL: lo copy
 #pragma unroll
                 for (int hf = 0; hf < NH; hf++) {
-                    const uint32_t d = tmem + kColZ + 128 * zb + 64 * hf;
+                    const uint32_t d = tmem + kColZ + 64 * NH * zb + 64 * hf;
                     const uint64_t wh = dwh + (hf * kWT >> 4), wl = dwl + (hf * kWT >> 4);
 #if GLX_BTC_EXP == 3
                     mma_ss(d, wh, dx, idf, 0, el);
@@ -499,7 +508,9 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         // ------------------------------------------------------------ epilogue
         // warp ew: TMEM lane quadrant quad = warp % 4 -> units 32 quad .. + 31 of half hf;
         // row block rb -> rows 32 rb .. 32 rb + 31 of the tile
-        const int ew = warp - 2, quad = warp & 3, hf = (ew >> 2) % NH, rb = ew / (4 * NH);
+        // group gi takes tiles lt = gi, gi + G, ...
+        const int ew = warp - 2, quad = warp & 3, gi = ew / NEWG, ewg = ew - gi * NEWG;
+        const int hf = (ewg >> 2) % NH, rb = ewg / (4 * NH);
         const int j = hf * 128 + quad * 32 + lane;  // this thread's hidden unit
         const int et = ew * 32 + lane;              // epilogue thread index; < kR: also owns row et
         const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
@@ -550,15 +561,18 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         // does tile lt's pass 1, then block 1 does its own, then block 0 tile lt + 1 --
         // so each pass has the MUFU pipe to itself while the other block runs its
         // shuffle / FMA phases, instead of both contending at once.
-        constexpr int kTok0 = kEpiBar + 4, kTok1 = kEpiBar + 5;  // block 1 -> 0, block 0 -> 1
-        for (int64_t lt = 0; lt < nt; lt++) {
+        // named barriers of group gi: its two row blocks, then the token pair
+        const int kBarRb = 1 + 4 * gi, kTok0 = kBarRb + 2, kTok1 = kBarRb + 3;  // token: block 1 -> 0, 0 -> 1
+        constexpr int kBarAll = 1 + 4 * G;  // all epilogue warps (the final exchange)
+        for (int64_t lt = gi; lt < nt; lt += G) {
             const int xs = (int)(lt % kS), zb = (int)(lt % kZB);
+            const int par = (int)((lt / G) & 1);  // this group's tile parity (double-buffered output partials)
             const int64_t row0 = (blockIdx.x + lt * gridDim.x) * kR;
             BTT(0);
             mbar_wait(&z_full[zb], (uint32_t)(lt / kZB) & 1);
             tc_fence_after();
             BTT(1);
-            const uint32_t zcol = tmem + lanebase + kColZ + 128 * zb + 64 * hf + 32 * rb;
+            const uint32_t zcol = tmem + lanebase + kColZ + 64 * NH * zb + 64 * hf + 32 * rb;
             float h[32];
             if (active) {
                 uint32_t r0[32];
@@ -568,8 +582,8 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                 for (int i = 0; i < 32; i++) h[i] = __uint_as_float(r0[i]);
             }
 #if GLX_BTC_TOKEN
-            if (rb == 1) bar_sync(kTok1, NEW * 32);           // block 0 finished its pass 1 of tile lt
-            else if (lt >= 1) bar_sync(kTok0, NEW * 32);      // block 1 finished its pass 1 of tile lt - 1
+            if (rb == 1) bar_sync(kTok1, NEWG * 32);          // block 0 finished its pass 1 of tile lt
+            else if (lt >= G) bar_sync(kTok0, NEWG * 32);     // block 1 finished its pass 1 of tile lt - G
 #endif
             BTT(5);
             // pass 1: h = sigmoid(z) (z prescaled by -log2 e)
@@ -601,7 +615,7 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             }
             BTT(6);
 #if GLX_BTC_TOKEN
-            bar_arrive(rb == 0 ? kTok1 : kTok0, NEW * 32);  // the other block's turn on the MUFU pipe
+            bar_arrive(rb == 0 ? kTok1 : kTok0, NEWG * 32);  // the other block's turn on the MUFU pipe
 #endif
             // output partials w2s_j h_j reduce-scattered over the warp's 32 units: lane l
             // ends with row 32 rb + l
@@ -624,15 +638,15 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
                         p[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
                     }
                 }
-                opart[(int)(lt & 1) * NEW * 32 + ew * 32 + lane] = p[0];
+                opart[par * NEW * 32 + ew * 32 + lane] = p[0];
             }
             BTT(2);
-            bar_sync(kEpiBar + rb, NEW * 16);  // the warps of this row block (they cover all units of its rows)
+            bar_sync(kBarRb + rb, NEWG * 16);  // the warps of this row block (they cover all units of its rows)
             BTT(3);
             if (active) {  // per row of this warp's block (lane = row 32 rb + l): o, delta_o (kernels.py:352-375);
                // every warp computes its own rows' delta_o, one warp per block keeps the statistics
                 const int r = 32 * rb + lane;
-                const float* op = opart + (int)(lt & 1) * NEW * 32 + rb * (4 * NH * 32) + lane;
+                const float* op = opart + par * NEW * 32 + (gi * NEWG + rb * 4 * NH) * 32 + lane;
                 float z0 = 0.f, z1 = 0.f;
 #pragma unroll
                 for (int w = 0; w < 4 * NH; w += 2) {
@@ -720,22 +734,34 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
         }
         // ---------------------------------------------- per-CTA partial record
 #if GLX_BTC_TOKEN
-        if (rb == 0) bar_sync(kTok0, NEW * 32);  // block 1's last token
+        if (rb == 0 && gi < nt) bar_sync(kTok0, NEWG * 32);  // block 1's last token
 #endif
-        mbar_wait(fin_bar, 0);
-        tc_fence_after();
-        if (active) drain();  // tiles since the last drain (>= 1)
-        if (j < a.H) {
-            float* o1 = out + (int64_t)j * (D + 1) + kDH * rb;
+        // dW1: the TMEM accumulator sums every tile's backward; group 0 drains it (the
+        // drained tiles are all group 0's) and owns the dW1 partials
+        if (gi == 0) {
+            mbar_wait(fin_bar, 0);
+            tc_fence_after();
+            if (active) drain();  // tiles since the last drain (>= 1)
+            if (j < a.H) {
+                float* o1 = out + (int64_t)j * (D + 1) + kDH * rb;
 #pragma unroll
-            for (int k = 0; k < kDH; k++)
-                if (kDH * rb + k <= D) o1[k] = acc1[k];
+                for (int k = 0; k < kDH; k++)
+                    if (kDH * rb + k <= D) o1[k] = acc1[k];
+            }
         }
-        bar_sync(kEpiBar + 2, NEW * 32);  // opart is free: exchange the dW2 partials of the two row blocks
-        if (rb == 1 && j < a.H) opart[j] = acc2.x + acc2.y;
-        float* stat = opart + 2 * NEW * 32 - kR * 6;  // behind the dW2 exchange slots (H <= 256 floats)
-        if (hf == 0 && quad == 0) {  // the statistics warps: rows 32 rb + lane
-            const int r = 32 * rb + lane;
+        // dW2 and the row statistics: one slot per (group, row block), summed in fixed order
+        bar_sync(kBarAll, NEW * 32);  // opart is free
+        if (j < a.H) opart[(gi * 2 + rb) * 256 + j] = acc2.x + acc2.y;
+        bar_sync(kBarAll, NEW * 32);
+        if (gi == 0 && rb == 0 && j < a.H) {
+            float s2 = 0.f;
+            for (int q = 0; q < 2 * G; q++) s2 += opart[q * 256 + j];
+            out[a.P1 + j] = s2;
+        }
+        bar_sync(kBarAll, NEW * 32);
+        float* stat = opart;  // [G][64 rows][6]
+        if (hf == 0 && quad == 0) {  // the statistics warps: rows 32 rb + lane of this group's tiles
+            const int r = gi * kR + 32 * rb + lane;
             stat[r * 6 + 0] = loss;
             stat[r * 6 + 1] = c0;
             stat[r * 6 + 2] = c1;
@@ -743,11 +769,10 @@ __global__ void __launch_bounds__(btc_threads(NH), 1) batchtc_kernel(const BtcAr
             stat[r * 6 + 4] = c3;
             stat[r * 6 + 5] = dsum;
         }
-        bar_sync(kEpiBar + 2, NEW * 32);
-        if (rb == 0 && j < a.H) out[a.P1 + j] = (acc2.x + acc2.y) + opart[j];
+        bar_sync(kBarAll, NEW * 32);
         if (et < 6) {
             float s = 0.f;
-            for (int r = 0; r < kR; r++) s += stat[r * 6 + et];
+            for (int r = 0; r < G * kR; r++) s += stat[r * 6 + et];
             if (et == 5) out[a.P1 + a.H] = s;
             else out[a.P1 + a.H + 1 + et] = s;
         }
@@ -868,7 +893,7 @@ static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t
         fprintf(stderr, "glx: batchtc_kernel<%d> smem=%zu: %s\n", NH, g.smem, cudaGetErrorString(e));
         return e;
     }
-    k<<<g.grid, btc_threads(NH), g.smem, st>>>(a);
+    k<<<g.grid, btc_threads(NH, FULL), g.smem, st>>>(a);
     e = cudaGetLastError();
     if (e != cudaSuccess) fprintf(stderr, "glx: batchtc_kernel<%d> launch: %s\n", NH, cudaGetErrorString(e));
     return e;

@@ -43,12 +43,12 @@ def test_batch_vs_oracle(gpu, N, D, H):
 
 @pytest.mark.parametrize("N,H,force", [
     (3001, 160, False), (2000, 96, False), (5000, 200, False), (4099, 250, False),
-    (1000, 33, True), (129, 64, True), (700, 1, True),
+    (1000, 33, False), (129, 64, False), (700, 1, True), (50_000, 40, False),
 ])
 def test_tcgen05_kernel_any_width_vs_oracle(gpu, N, H, force, monkeypatch):
     """The tcgen05 epoch kernel for widths that are not a multiple of 128 (padded
-    units: zero weights, idle epilogue warps) -- the default for 96 <= H <= 256,
-    forced with GLX_BATCH_KERNEL=tc below that."""
+    units: zero weights, idle epilogue warps) -- the default for 24 <= H <= 256,
+    forced with GLX_BATCH_KERNEL=tc below that; H <= 128 runs two epilogue groups."""
     import paper_1908_07847_b200._lib as L
 
     if force:
@@ -89,8 +89,8 @@ def test_tcgen05_fast_precision_padded_width(gpu, monkeypatch):
 
 
 def test_tcgen05_kernel_selected_for_headline_shapes(gpu):
-    """configs 2 and 4 (33 -> 128 / 256 -> 1) run the tcgen05 epoch kernel, as does any
-    width 96..256; narrower and wider layers run the FP32 CUDA-core kernels
+    """configs 2 and 4 (33 -> 33 / 128 / 256 -> 1) run the tcgen05 epoch kernel, as does any
+    width 24..256; narrower and wider layers run the FP32 CUDA-core kernels
     (glx_batch_kernel_kind)."""
     import paper_1908_07847_b200._lib as L
 
@@ -99,7 +99,8 @@ def test_tcgen05_kernel_selected_for_headline_shapes(gpu):
     assert lib.glx_batch_kernel_kind(1 << 26, 33, 256) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 128) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 192) == 2 and lib.glx_batch_kernel_kind(1000, 33, 97) == 2
-    assert lib.glx_batch_kernel_kind(1000, 33, 64) in (0, 1)
+    assert lib.glx_batch_kernel_kind(1000, 33, 33) == 2 and lib.glx_batch_kernel_kind(1000, 33, 64) == 2
+    assert lib.glx_batch_kernel_kind(1000, 33, 16) in (0, 1)
     assert lib.glx_batch_kernel_kind(1000, 33, 512) in (0, 1)
     assert lib.glx_batch_kernel_kind(1000, 40, 256) in (0, 1)  # D > 33: FP32 kernels
     assert lib.glx_batch_kernel_kind(1000, 128, 8) == -1
