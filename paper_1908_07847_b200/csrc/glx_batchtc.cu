@@ -1,6 +1,6 @@
 // glx_batchtc.cu -- full-batch gradient-descent epoch (configs 2 and 4:
-// D <= 33 inputs -> H = 128 or 256 sigmoid units -> 1 output) on the
-// 5th-generation tensor cores, fp32-accurate through 3xTF32.
+// D <= 33 inputs -> 24 <= H <= 256 sigmoid units -> 1 output) on the
+// 5th-generation tensor cores (tcgen05 kind::tf32).
 //
 // Same contract as batch3_kernel (glx_batch3.cu): one persistent CTA per SM
 // walks row tiles and writes one per-CTA partial record
@@ -8,31 +8,27 @@
 // that batch_update_kernel reduces in f64 and applies (kernels.py:264-295
 // batch semantics).
 //
-// Both GEMMs of the epoch run on tcgen05 with the hidden units on the TMEM
-// lanes (M = 128 units per half):
-//   forward   Z^T[j][r]  = W1s[j][:] . x_r            (SS: A = W1s, B = x tile, K-major)
-//   backward  dW1[j][k] += sum_r dh[j][r] x_r[k]       (TS: A = dh^T from TMEM, B = x tile, MN-major)
-// so the delta of every hidden unit stays in TMEM between the two MMAs. Both
-// shared-memory operands are K-major no-swizzle core matrices (8 rows x 16 B):
-// the forward reads the x tile as [rows x features], the backward a transposed
-// copy [features x rows] written by the converter warps (tf32 MMAs with an
-// MN-major B operand return zeros on sm_100a, tools/umma_probe.cu).
-// Each operand is split hi = tf32(v) (bit truncation), lo = v - hi and the
-// products are accumulated as lo.hi + hi.lo + hi.hi in the fp32 TMEM
-// accumulator: the dropped lo.lo term is 2^-22 relative, so results track the
-// fp32 CUDA-core kernel (tests/test_gpu_batch.py, 1e-5 against the f64 oracle).
+// Both GEMMs of the epoch run with the hidden units on the TMEM lanes (M = 128
+// units per half; units past H are zero-weight padding):
+//   forward   Z^T[j][r]  = W1s[j][:] . x_r            (SS: A = W1s, B = x tile)
+//   backward  dW1[j][k] += sum_r dh[j][r] x_r[k]       (TS: A = dh^T from TMEM, B = x^T tile)
+// so the delta of every hidden unit stays in TMEM between the two MMAs. The rows
+// arrive as per-tile MMA operands built once per training call (btc_pack_kernel:
+// tf32-rounded forward and transposed copies, K-major no-swizzle core matrices);
+// warp 0 bulk-copies them, warp 1 issues the MMAs (converged, one elect.sync
+// lane). Precision (M4b): FULL = 3xTF32 below 2^17 rows,
+// FAST = x and the deltas rounded once to tf32 (round to nearest) above.
 //
-// Per 64-row tile, 16 epilogue warps (4 TMEM lane quadrants x 2 unit halves x
-// 2 row blocks; thread = hidden unit, 32 rows) read Z^T from TMEM, apply the
-// sigmoid (MUFU, with 3 of 8 exponential pairs on the FMA pipe), reduce the
-// output partials w2s_j h_j with a warp reduce-scatter plus one shared-memory
-// pass per row block, compute delta_o for their own rows, and write
-// dh = delta_o h (1 - h) back to TMEM as tf32 hi/lo for the backward MMA. Z^T is
-// double-buffered so the forward MMA of tile t+1 overlaps the epilogue of tile
-// t, and the backward of tile t overlaps the epilogue of tile t+1. Warp 0 bulk-
-// copies the packed rows, warps 2-3 convert them into the two operand layouts,
-// warp 1 issues the MMAs (converged, one elect.sync lane). DESIGN.md §4 has the
-// measured path and the per-phase timeline.
+// Per 64-row tile, the epilogue warps (4 TMEM lane quadrants x NH unit halves x 2
+// row blocks; thread = hidden unit, 32 rows; two such groups on alternate tiles
+// when NH = 1) read Z^T from TMEM, apply the sigmoid (MUFU ex2, one reciprocal
+// per element pair), reduce the output partials w2s_j h_j with a warp
+// reduce-scatter plus one shared-memory pass per row block, compute delta_o for
+// their own rows, and write dh = delta_o h (1 - h) back over Z^T for the backward
+// MMA. Z^T has 3-4 buffers (the forward runs ahead of the epilogue); the two row
+// blocks are independent pipelines whose sigmoid passes alternate through a
+// named-barrier token. DESIGN.md section 4 has the measured path and the per-phase
+// timeline (GLX_BTC_TIMING builds, tools/btc_timeline.py).
 #include "glx_common.cuh"
 #include "glx_kernels.h"
 
