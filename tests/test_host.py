@@ -180,3 +180,53 @@ def test_post_feature_generator_matches_reference_draws(rows, cols, seed):
     assert (gen.normal(0.0, 1.0, size=pick.shape[0]) == coef).all()
     hi, lo = _split128((1 << 127) + 5)
     assert hi == 1 << 63 and lo == 5
+
+
+def test_parallel_workers_validated_and_clamped():
+    """backend.py:45-62: workers >= 1, effective_workers clamped to max_workers()."""
+    import pytest
+
+    from paper_1908_07847_b200 import backend as B
+    from paper_1908_07847_b200.errors import ValidationError
+
+    assert B.max_workers() == B.hardware_parallelism()
+    assert B.parallel(10 ** 6).effective_workers == B.max_workers()
+    assert B.sequential().effective_workers == 1
+    with pytest.raises(ValidationError):
+        B.parallel(0)
+    with pytest.raises(ValidationError):
+        B.BackendKind("numba")
+
+
+def test_wide_shard_rows_block_alignment():
+    from paper_1908_07847_b200 import wide
+    from paper_1908_07847_b200.errors import ShapeError
+
+    for block in (32, 64):
+        n = block * 37
+        bounds = [wide.shard_rows(n, 4, r, block) for r in range(4)]
+        assert bounds[0][0] == 0 and bounds[-1][1] == n
+        assert all(a % block == 0 and b % block == 0 and a <= b for a, b in bounds)
+        assert all(bounds[i][1] == bounds[i + 1][0] for i in range(3))
+    import pytest
+
+    with pytest.raises(ShapeError):
+        wide.shard_rows(100, 2, 0, 32)
+
+
+def test_glycemlp_import_surface():
+    """pkg/src/glycemlp re-exports the reference's hot-path names
+    (/root/reference/pkg/src/glycemlp/__init__.py:5-106) on this engine."""
+    import glycemlp as G
+
+    for name in ("train", "evaluate", "TrainSpec", "NetworkConfig", "init_weights", "sequential", "parallel",
+                 "BackendKind", "forward", "predict", "backprop_update", "normalize_split", "synthetic_matrix",
+                 "save_checkpoint", "load_checkpoint", "run_bench", "max_workers", "hardware_parallelism"):
+        assert hasattr(G, name), name
+    from glycemlp import kernels
+
+    assert callable(kernels.train_segment_seq) and callable(kernels.eval_counts)
+    import pytest
+
+    with pytest.raises(AttributeError):
+        G.parse_csv  # out of scope: host CSV plumbing
