@@ -153,10 +153,11 @@ int glx_train_batch(float* w_ih, float* w_ho, const float* Xp, int64_t N, int32_
                     double lr, double* stats_hist, int32_t* nonfinite, void* stream);
 
 /* Which full-batch epoch kernel glx_train_batch / glx_batch_grad run for this
- * shape: 2 = tcgen05 3xTF32 kernel (H = 128 or 256, D <= 33), 1 = three-role
- * FP32 kernel, 0 = two-role FP32 kernel, -1 = unsupported shape. Selection
- * only (no device work); GLX_BATCH_KERNEL=3 / =2 cap the choice at 1 / 0.
- * No reference counterpart (diagnostic). */
+ * shape: 3 = tcgen05 rows-on-lanes kernel (24 <= H <= 64, D <= 33, from 2^17
+ * rows), 2 = tcgen05 units-on-lanes kernel (24 <= H <= 256, D <= 33), 1 =
+ * three-role FP32 kernel, 0 = two-role FP32 kernel (D <= 127), -1 = unsupported
+ * shape. Selection only (no device work); GLX_BATCH_KERNEL=3 / =2 cap the choice
+ * at 1 / 0, =tc / =rt force a tcgen05 kernel. No reference counterpart (diagnostic). */
 int glx_batch_kernel_kind(int64_t N, int32_t D, int32_t H);
 
 /* Data-parallel split of one epoch (config 4): glx_batch_grad writes this

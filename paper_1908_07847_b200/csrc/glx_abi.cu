@@ -297,8 +297,19 @@ bool force_tc() {
     return e && e[0] == 't' && e[1] == 'c';
 }
 
+bool force_rt() {
+    const char* e = getenv("GLX_BATCH_KERNEL");
+    return e && e[0] == 'r' && e[1] == 't';
+}
+
 bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
     const int pref = batch_kernel_pref();
+    // narrow layers with enough rows for the FAST precision: rows on the TMEM lanes
+    // (glx_batchtc.cu batchrt_kernel); GLX_BATCH_KERNEL=tc keeps the unit-on-lanes kernel
+    if (pref >= 2 && !force_tc() && (H >= kTcMinH || force_rt()) && batchrt_geometry(N, D, H, sm_count_current(), g)) {
+        *kind = 3;
+        return true;
+    }
     if (pref >= 2 && (H >= kTcMinH || force_tc()) && batchtc_geometry(N, D, H, sm_count_current(), g)) {
         *kind = 2;
         return true;
@@ -318,12 +329,13 @@ bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
 // kernel, their per-tile MMA operand layout, built here once per training call
 // into the stream's workspace (one pass over the rows)
 int epoch_input(Workspace* ws, const BatchGeom& g, int kind, const float* Xp, cudaStream_t st, const void** in) {
-    if (kind != 2) {
+    if (kind != 2 && kind != 3) {
         *in = Xp;
         return GLX_OK;
     }
-    GLX_CK(ws->tiles.ensure(batchtc_tile_bytes(g)));
-    GLX_LAUNCH(launch_batchtc_pack(g, Xp, ws->tiles.p, st));
+    GLX_CK(ws->tiles.ensure(kind == 3 ? batchrt_tile_bytes(g) : batchtc_tile_bytes(g)));
+    if (kind == 3) GLX_LAUNCH(launch_batchrt_pack(g, Xp, ws->tiles.p, st));
+    else GLX_LAUNCH(launch_batchtc_pack(g, Xp, ws->tiles.p, st));
     *in = ws->tiles.p;
     return GLX_OK;
 }
@@ -331,6 +343,7 @@ int epoch_input(Workspace* ws, const BatchGeom& g, int kind, const float* Xp, cu
 cudaError_t launch_train_epoch(const BatchGeom& g, int kind, const void* in, const float* Wk, float* part,
                                cudaStream_t st) {
     const float* Xp = (const float*)in;
+    if (kind == 3) return launch_batchrt_epoch(g, in, Wk, part, st);
     if (kind == 2) return launch_batchtc_epoch(g, in, Wk, part, st);
     return kind == 1 ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
 }

@@ -817,6 +817,470 @@ __global__ void __launch_bounds__(256) btc_pack_kernel(const float* __restrict__
     }
 }
 
+// =================================================== narrow layers: rows on the lanes
+// For H <= 64 (the reference's default width is 33) the unit-on-lanes kernel above
+// leaves most of its epilogue idle and pays a cross-lane reduction per row. Here the
+// forward puts the ROWS on the TMEM lanes (M = 128 rows, N = HP units), so each
+// epilogue thread owns one row: the output dot, delta_o and the statistics are
+// per-thread sums. The backward contracts over rows, so the hidden deltas go to
+// shared memory as the K-major A operand dh^T [128 units][128 rows] (128-byte
+// swizzle: a warp's 32 rows of one unit are one conflict-free 128-byte row) and
+//   dW1[j][k] += sum_r dh[j][r] x_r[k]      (SS: A = dh^T, B = x^T tile, M = 128 units)
+// accumulates in TMEM, drained every kRDrain tiles into the per-CTA record.
+// FAST precision only (x and dh rounded once to tf32, forward hi(W) x + lo(W) x);
+// rows arrive as 128-row tiles built once per call by btr_pack_kernel:
+//   forward A  [k/4][r/8][r%8][k%4]   (LBO 2048 B, SBO 128 B; 9 chunks stored, 18 KB)
+//   backward B [f/8][r/4][f%8][r%4]   (LBO 128 B, SBO 4096 B; features < 40, 20 KB)
+constexpr int kRR = 128;                      // rows per tile (forward M)
+constexpr int kRXF = kFC * kRR / 8 * 128;     // smem bytes, forward operand (20 KB)
+constexpr int kRXT = kNB / 8 * kRR / 4 * 128;  // smem bytes, backward operand (24 KB)
+constexpr int kRXFG = kFCS * kRR / 8 * 128;   // global bytes, forward operand (18 KB)
+constexpr int kRXTG = kNBS / 8 * kRR / 4 * 128;  // global bytes, backward operand (20 KB)
+constexpr int kRGT = kRXFG + kRXTG;           // global bytes per tile
+constexpr int kRS = 3;                        // stages of each ring: forward operands (freed by the
+                                              // forward MMA) and backward operands (freed by the backward)
+constexpr int kRZB = 3;                       // Z buffers (forward kRZB tiles ahead)
+// epilogue groups of 4 warps on alternate tiles: 3 (registers: h and the dW2 partials
+// are 2 HP per thread), 2 for HP = 64
+__host__ __device__ constexpr int btr_groups(int HP) { return HP <= 48 ? 3 : 2; }
+// dW1 drain period (a multiple of the group count: group 0's tiles); a drain holds up the
+// dh^T hand-off chain for its global read-modify-write, so it is rare: 48 tiles = 6144
+// rows per TMEM fp32 partial
+constexpr int kRDrain = 48;
+constexpr int kRColW = 256;                   // dW1 accumulator columns (48)
+__host__ __device__ constexpr int btr_threads(int HP) { return (2 + 4 * btr_groups(HP)) * 32; }
+
+template <int HP>
+struct BtrSmem {  // byte offsets
+    static constexpr int wt = HP / 8 * kFC * 128;       // one W1 copy (hi or lo): [j/8][k/4][j%8][k%4]
+    static constexpr int w = 0;
+    static constexpr int x = 1024 * ((2 * wt + 1023) / 1024);
+    // dh^T, two buffers of 4 planes x 64 unit-rows x 128 B (1024-aligned swizzle atoms). The
+    // backward MMA reads M = 128 unit-rows per plane; rows >= 64 fall in the next plane /
+    // buffer / the backward ring (valid shared memory; their D rows are units >= HP, which
+    // the drain never reads)
+    static constexpr int dh = x + kRS * kRXF;
+    static constexpr int xt = dh + 2 * 4 * 8192;        // backward-operand ring
+    static constexpr int w2 = xt + kRS * kRXT;          // w2s (HP floats), b2s
+    static constexpr int red = w2 + (HP + 4) * 4;        // final reductions: [warps][HP + 8]
+    static constexpr int bars = red + 4 * btr_groups(HP) * (HP + 8) * 4;
+    static constexpr int total = bars + 256;
+};
+
+#ifdef GLX_BTR_TIMING
+__device__ unsigned long long g_btr_dbg[4096];
+// clock64 timeline of CTA 0, tiles 6..37: slot s of tile t at [(t - 6) * 8 + s] (per-tile
+// slots: 0 epilogue start, 1 Z loaded, 2 deltas computed, 3 dh buffer free, 4 dh_ready
+// arrived (warp 2); 5 MMA saw dh_ready, 6 backward issued (warp 1); 7 tile loaded (warp 0))
+#define BTR_T(slot, lt)                                                                                     \
+    do {                                                                                                    \
+        if (blockIdx.x == 0 && lane == 0 && (lt) >= 6 && (lt) < 38) g_btr_dbg[((lt) - 6) * 8 + (slot)] = clock64(); \
+    } while (0)
+#else
+#define BTR_T(slot, lt) \
+    do {                \
+    } while (0)
+#endif
+#ifdef GLX_BTR_DEBUG
+// diagnostic builds: a bounded wait that reports which barrier never completed
+__device__ __forceinline__ void btr_wait(uint64_t* bar, uint32_t parity, int tag, int64_t lt) {
+    uint32_t ok = 0;
+    const long long t0 = clock64();
+    while (!ok && clock64() - t0 < 4000000000ll)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    if (!ok) {
+        printf("btr hang: block %d warp %d lane %d tag %d lt %lld parity %u\n", blockIdx.x, threadIdx.x / 32,
+               threadIdx.x % 32, tag, (long long)lt, parity);
+        __trap();
+    }
+}
+#define BTR_WAIT(bar, par, tag, lt) btr_wait(bar, par, tag, lt)
+#else
+#define BTR_WAIT(bar, par, tag, lt) mbar_wait(bar, par)
+#endif
+
+template <int HP>
+__global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcArgs a) {
+    using L = BtrSmem<HP>;
+    constexpr int kRG = btr_groups(HP);
+    static_assert(kRDrain % kRG == 0, "the drained tiles must all belong to group 0");
+    extern __shared__ __align__(1024) unsigned char sm[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::bars);
+    uint64_t* x_full = bars;            // forward operand of a tile loaded
+    uint64_t* x_empty = x_full + kRS;   // forward-operand stage free (its forward completed)
+    uint64_t* t_full = x_empty + kRS;   // backward operand of a tile loaded
+    uint64_t* t_empty = t_full + kRS;   // backward-operand stage free (its backward completed)
+    uint64_t* z_full = t_empty + kRS;   // Z buffer written by the forward
+    uint64_t* z_free = z_full + kRZB;   // Z buffer read by the epilogue
+    // dh_ready[lt % 2]: tile lt's dh^T is in buffer lt % 2 (4 warps); per buffer, since the
+    // next tile's group may arrive before the MMA warp consumed this tile's phase
+    uint64_t* dh_ready = z_free + kRZB;
+    // dh_free[k % kRG]: backward(k) completed. Tile lt waits for backward(lt - 2) (the last
+    // reader of its buffer); its group knows backward(lt - 2 - kRG) completed (its own
+    // previous tile waited for it), so with kRG slots the barrier is never two phases behind
+    uint64_t* dh_free = dh_ready + 2;
+    uint64_t* fin_bar = dh_free + 3;    // the last backward completed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin_bar + 1);
+    float* w2s = reinterpret_cast<float*>(sm + L::w2);
+    float* red = reinterpret_cast<float*>(sm + L::red);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nt = (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const int D = a.D, DP = a.DP, H = a.H;
+    float* out = a.part + (int64_t)blockIdx.x * a.PS;
+#ifdef GLX_BTR_DEBUG
+    if (blockIdx.x == 0 && threadIdx.x == 0) printf("btr start: nt %lld N %lld D %d H %d HP %d\n", (long long)nt, (long long)a.N, D, H, HP);
+#endif
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kRS; i++) {
+            mbar_init(&x_full[i], 1);
+            mbar_init(&x_empty[i], 1);
+            mbar_init(&t_full[i], 1);
+            mbar_init(&t_empty[i], 1);
+        }
+        for (int b = 0; b < kRZB; b++) {
+            mbar_init(&z_full[b], 1);
+            mbar_init(&z_free[b], 4);
+        }
+        mbar_init(&dh_ready[0], 4);
+        mbar_init(&dh_ready[1], 4);
+        for (int b = 0; b < kRG; b++) mbar_init(&dh_free[b], 1);
+        mbar_init(fin_bar, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(kTmemCols)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    // W1 (B operand of the forward: N = HP units, K = 40) as tf32 hi + lo; units >= H zero
+    for (int e = threadIdx.x; e < HP * kFC; e += blockDim.x) {
+        const int j = e / kFC, q = e - (e / kFC) * kFC;
+        float v[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+            const int k = 4 * q + i;
+            v[i] = (k <= D && j < H) ? a.Wk[(int64_t)j * DP + k] : 0.f;
+        }
+        const int off = (j >> 3) * (kFC * 128) + q * 128 + (j & 7) * 16;
+        uint4 hi, lo;
+        hi.x = tf32_rn(v[0]);
+        hi.y = tf32_rn(v[1]);
+        hi.z = tf32_rn(v[2]);
+        hi.w = tf32_rn(v[3]);
+        lo.x = __float_as_uint(v[0] - __uint_as_float(hi.x));
+        lo.y = __float_as_uint(v[1] - __uint_as_float(hi.y));
+        lo.z = __float_as_uint(v[2] - __uint_as_float(hi.z));
+        lo.w = __float_as_uint(v[3] - __uint_as_float(hi.w));
+        *reinterpret_cast<uint4*>(sm + L::w + off) = hi;
+        *reinterpret_cast<uint4*>(sm + L::w + L::wt + off) = lo;
+    }
+    for (int j = threadIdx.x; j < HP + 4; j += blockDim.x)
+        w2s[j] = j < H ? a.Wk[(int64_t)H * DP + j] : (j == HP ? a.Wk[(int64_t)H * DP + H] : 0.f);
+    // zero: the padding regions of every stage, the dh^T operand (units >= HP stay zero),
+    // and this CTA's dW1 record (the drains accumulate into it)
+    for (int i = threadIdx.x; i < kRS * (kRXF - kRXFG + kRXT - kRXTG) / 16; i += blockDim.x) {
+        const int per = (kRXF - kRXFG + kRXT - kRXTG) / 16, st = i / per, w = i - (i / per) * per;
+        unsigned char* dst = w < (kRXF - kRXFG) / 16 ? sm + L::x + st * kRXF + kRXFG + 16 * w
+                                                      : sm + L::xt + st * kRXT + kRXTG + 16 * (w - (kRXF - kRXFG) / 16);
+        *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    for (int i = threadIdx.x; i < 2 * 4 * 8192 / 16; i += blockDim.x)  // units HP..63 stay zero
+        reinterpret_cast<uint4*>(sm + L::dh)[i] = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = threadIdx.x; i < a.P1; i += blockDim.x) out[i] = 0.f;
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        // the forward operand of tile lt as soon as its stage frees (forward(lt - kRS) done);
+        // the backward operand of tile lt - 2 behind it (needed a few tiles later, by
+        // backward(lt - 2); its stage freed by backward(lt - 2 - kRS), long done)
+        if (lane == 0) {
+            auto load_t = [&](int64_t k) {
+                const int ts = (int)(k % kRS);
+                if (k >= kRS) BTR_WAIT(&t_empty[ts], (uint32_t)((k / kRS) - 1) & 1, 8, k);
+                const unsigned char* src = a.tiles + (blockIdx.x + k * gridDim.x) * (int64_t)kRGT + kRXFG;
+                mbar_arrive_expect_tx(&t_full[ts], (uint32_t)kRXTG);
+                bulk_g2s(sm + L::xt + ts * kRXT, src, kRXTG, &t_full[ts]);
+            };
+            for (int64_t lt = 0; lt < nt; lt++) {
+                const int xs = (int)(lt % kRS);
+                if (lt >= kRS) BTR_WAIT(&x_empty[xs], (uint32_t)((lt / kRS) - 1) & 1, 1, lt);
+                const unsigned char* src = a.tiles + (blockIdx.x + lt * gridDim.x) * (int64_t)kRGT;
+                mbar_arrive_expect_tx(&x_full[xs], (uint32_t)kRXFG);
+                bulk_g2s(sm + L::x + xs * kRXF, src, kRXFG, &x_full[xs]);
+                BTR_T(7, lt);
+                if (lt >= 2) load_t(lt - 2);
+            }
+            for (int64_t k = nt >= 2 ? nt - 2 : 0; k < nt; k++) load_t(k);
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        const uint32_t el = elect_one();
+        constexpr uint32_t idf = idesc_tf32(HP, false);   // M = 128 rows, N = HP units
+        constexpr uint32_t idb = idesc_tf32(kNB, false);  // M = 128 units, N = 48 features
+        const uint64_t dwh = desc_ns(smem_u32(sm + L::w), 128, kFC * 128);
+        const uint64_t dwl = desc_ns(smem_u32(sm + L::w + L::wt), 128, kFC * 128);
+        const uint64_t dx0 = desc_ns(smem_u32(sm + L::x), kRR / 8 * 128, 128);
+        const uint64_t dt0 = desc_ns(smem_u32(sm + L::xt), 128, kRR / 4 * 128);
+        // dh^T: 128-byte-swizzled K-major (4 planes of 32 rows x 128 units, atoms 1 KB)
+        const uint64_t dd0 = (uint64_t)((smem_u32(sm + L::dh) >> 4) & 0x3FFF) | ((uint64_t)1 << 16) |
+                             ((uint64_t)(1024 >> 4) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+        auto forward = [&](int64_t lt) {
+            const int xs = (int)(lt % kRS), zb = (int)(lt % kRZB);
+            BTR_WAIT(&x_full[xs], (uint32_t)(lt / kRS) & 1, 2, lt);
+            tc_fence_after();
+            const uint32_t d = tmem + HP * zb;
+            const uint64_t dx = dx0 + ((xs * kRXF) >> 4);
+#pragma unroll
+            for (int s = 0; s < kFC / 2; s++) mma_ss(d, dx + (s * 4096 >> 4), dwl + (s * 256 >> 4), idf, s != 0, el);
+#pragma unroll
+            for (int s = 0; s < kFC / 2; s++) mma_ss(d, dx + (s * 4096 >> 4), dwh + (s * 256 >> 4), idf, 1, el);
+            commit(&x_empty[xs], el);
+            commit(&z_full[zb], el);
+        };
+        auto backward = [&](int64_t lt) {
+            const int ts = (int)(lt % kRS);
+            BTR_WAIT(&dh_ready[lt & 1], (uint32_t)(lt >> 1) & 1, 3, lt);
+            BTR_WAIT(&t_full[ts], (uint32_t)(lt / kRS) & 1, 9, lt);
+            tc_fence_after();
+            BTR_T(5, lt);
+            const uint64_t dt = dt0 + ((ts * kRXT) >> 4);
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+#pragma unroll
+                for (int kk = 0; kk < 4; kk++) {
+                    const uint32_t acc = (lt % kRDrain) != 0 || c != 0 || kk != 0;
+                    mma_ss(tmem + kRColW, dd0 + (((int)(lt & 1) * 32768 + c * 8192 + kk * 32) >> 4),
+                           dt + (((4 * c + kk) * 256) >> 4), idb, acc, el);
+                }
+            }
+            commit(&t_empty[ts], el);
+            commit(&dh_free[lt % kRG], el);
+            if (lt == nt - 1) commit(fin_bar, el);
+            BTR_T(6, lt);
+        };
+        for (int64_t lt = 0; lt < kRZB && lt < nt; lt++) forward(lt);
+        for (int64_t lt = 0; lt < nt; lt++) {
+            backward(lt);
+            if (lt + kRZB < nt) {
+                BTR_WAIT(&z_free[lt % kRZB], (uint32_t)(lt / kRZB) & 1, 4, lt);  // the epilogue read Z(lt)
+                forward(lt + kRZB);
+            }
+        }
+#ifdef GLX_BTR_DEBUG
+        if (blockIdx.x == 0 && lane == 0) printf("btr mma: all %lld backwards issued\n", (long long)nt);
+#endif
+    } else {
+        // ------------------------------------------------------------ epilogue
+        // group gi (4 warps) takes tiles gi, gi + kRG, ...; warp quadrant q -> rows 32 q ..
+        const int ew = warp - 2, gi = ew / 4, quad = warp & 3;
+        const int r = quad * 32 + lane;  // this thread's row within the tile
+        const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
+        const int tk = D + 1;            // the target travels as feature D + 1
+        // its word in the tile's forward operand in global memory: [k/4][r/8][r%8][k%4]
+        const int twd = (((tk >> 2) * 16 + (r >> 3)) * 8 + (r & 7)) * 4 + (tk & 3);
+        const float b2s = w2s[HP];
+        float acc2[HP];
+#pragma unroll
+        for (int j = 0; j < HP; j++) acc2[j] = 0.f;
+        float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
+        // dW1 drain: the TMEM accumulator (lanes = units) added into the per-CTA record by
+        // the warps whose quadrant holds units (unit j = lane of quadrant j / 32)
+        auto drain = [&]() {
+            const int j = quad * 32 + lane;
+            if (quad * 32 < HP) {
+                uint32_t v0[32], v1[2];
+                ld32(tmem + lanebase + kRColW, v0);
+                ld2(tmem + lanebase + kRColW + 32, v1);
+                tmem_ld_wait();
+                if (j < H) {
+                    float* o1 = out + (int64_t)j * (D + 1);
+                    float cur[34];
+#pragma unroll
+                    for (int k = 0; k < 34; k++) cur[k] = k <= D ? o1[k] : 0.f;  // all loads in flight
+#pragma unroll
+                    for (int k = 0; k < 34; k++)
+                        if (k <= D) o1[k] = cur[k] + __uint_as_float(k < 32 ? v0[k] : v1[k - 32]);
+                }
+            }
+        };
+        for (int64_t lt = gi; lt < nt; lt += kRG) {
+            const int zb = (int)(lt % kRZB);
+            const int64_t row = (blockIdx.x + lt * gridDim.x) * kRR + r;
+            // the target, read early from global memory (the tile's smem stages are freed
+            // by the MMAs before this epilogue needs it)
+            const float tt = __ldg(reinterpret_cast<const float*>(a.tiles + (blockIdx.x + lt * gridDim.x) * (int64_t)kRGT) + twd);
+            if (quad == 2) BTR_T(0, lt);
+            BTR_WAIT(&z_full[zb], (uint32_t)(lt / kRZB) & 1, 5, lt);
+            tc_fence_after();
+            float h[HP];
+            {
+                uint32_t v[32];
+#pragma unroll
+                for (int c = 0; c < HP; c += 32) {
+                    if (HP - c >= 32) {
+                        ld32(tmem + lanebase + HP * zb + c, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 32; i++) h[c + i] = __uint_as_float(v[i]);
+                    } else {
+                        uint32_t v16[16];
+                        ld16(tmem + lanebase + HP * zb + c, v16);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; i++) h[c + i] = __uint_as_float(v16[i]);
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&z_free[zb]);
+            if (quad == 2) BTR_T(1, lt);
+            // h = sigmoid(z) (z prescaled by -log2 e), one reciprocal per pair
+#pragma unroll
+            for (int i = 0; i < HP; i += 2) {
+                const float2 e2 = make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
+                const float2 den = __fadd2_rn(fminf2(e2, bcast2(1.152921504606847e18f)), bcast2(1.0f));
+                const float rc = rcp_approx(den.x * den.y);
+                const float2 hh = __fmul2_rn(make_float2(den.y, den.x), bcast2(rc));
+                h[i] = hh.x;
+                h[i + 1] = hh.y;
+            }
+            // the output neuron: a per-thread dot (w2s prescaled by -log2 e)
+            float2 zo2 = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < HP; i += 4) {
+                const float4 w4 = *reinterpret_cast<const float4*>(w2s + i);
+                zo2 = ffma2(make_float2(w4.x, w4.y), make_float2(h[i], h[i + 1]), zo2);
+                zo2 = ffma2(make_float2(w4.z, w4.w), make_float2(h[i + 2], h[i + 3]), zo2);
+            }
+            float d = 0.f;
+            if (row < a.N) {
+                const float o = sigmoid_scaled(zo2.x + zo2.y + b2s);
+                d = (o - tt) * o * (1.0f - o);
+                loss = fmaf(0.5f * (tt - o), tt - o, loss);
+                const bool pred = o >= 0.5f, pos = tt >= 0.5f;
+                c0 += (pred && pos) ? 1.f : 0.f;
+                c1 += (!pred && !pos) ? 1.f : 0.f;
+                c2 += (pred && !pos) ? 1.f : 0.f;
+                c3 += (!pred && pos) ? 1.f : 0.f;
+                dsum += d;
+            }
+            // dW2 += delta_o h; dh = delta_o h (1 - h) -> tf32 (h reused as dh)
+#pragma unroll
+            for (int i = 0; i < HP; i += 2) {
+                const float2 hp = make_float2(h[i], h[i + 1]);
+                const float2 v = __fmul2_rn(bcast2(d), hp);
+                const float2 a2 = __fadd2_rn(make_float2(acc2[i], acc2[i + 1]), v);
+                acc2[i] = a2.x;
+                acc2[i + 1] = a2.y;
+                const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
+                h[i] = __uint_as_float(tf32_rn(s2.x));
+                h[i + 1] = __uint_as_float(tf32_rn(s2.y));
+            }
+            if (quad == 2) BTR_T(2, lt);
+            // dh^T buffer lt % 2: backward(lt - 2) read it last. A drain tile also needs
+            // backward(lt - 1) (the end of the accumulation it takes)
+            if (lt >= 2) {
+                BTR_WAIT(&dh_free[(lt - 2) % kRG], (uint32_t)((lt - 2) / kRG) & 1, 6, lt);
+                tc_fence_after();
+            }
+            if (quad == 2) BTR_T(3, lt);
+            if (lt >= 1 && lt % kRDrain == 0) {  // group 0's tile: the backward of lt restarts
+                BTR_WAIT(&dh_free[(lt - 1) % kRG], (uint32_t)((lt - 1) / kRG) & 1, 6, lt);
+                tc_fence_after();
+                drain();
+            }
+            {
+                unsigned char* plane = sm + L::dh + (int)(lt & 1) * 32768 + quad * 8192;
+#pragma unroll
+                for (int j = 0; j < HP; j++)
+                    *reinterpret_cast<float*>(plane + (j >> 3) * 1024 + (j & 7) * 128 +
+                                              ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4) = h[j];
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&dh_ready[lt & 1]);
+            if (quad == 2) BTR_T(4, lt);
+        }
+        // ---------------------------------------------- per-CTA partial record
+        if (gi == 0) {
+#ifdef GLX_BTR_DEBUG
+            BTR_WAIT(&dh_free[(nt - 1) % kRG], (uint32_t)((nt - 1) / kRG) & 1, 8, nt);
+#endif
+            BTR_WAIT(fin_bar, 0, 7, nt);
+            tc_fence_after();
+            drain();  // tiles since the last drain
+        }
+        // dW2 and the statistics: warp sums, then a fixed-order sum over the warps
+        float* slot = red + ew * (HP + 8);
+#pragma unroll
+        for (int j = 0; j < HP; j++) {
+            float v = acc2[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) slot[j] = v;
+        }
+        float st[6] = {loss, c0, c1, c2, c3, dsum};
+#pragma unroll
+        for (int q = 0; q < 6; q++) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) st[q] += __shfl_xor_sync(0xffffffffu, st[q], o);
+            if (lane == 0) slot[HP + q] = st[q];
+        }
+        bar_sync(kEpiBar, 4 * kRG * 32);
+        const int et = ew * 32 + lane;
+        if (et < HP + 6) {
+            float sum = 0.f;
+            for (int w = 0; w < 4 * kRG; w++) sum += red[w * (HP + 8) + et];
+            if (et < H) out[a.P1 + et] = sum;
+            else if (et == HP + 5) out[a.P1 + H] = sum;                   // dsum
+            else if (et >= HP && et < HP + 5) out[a.P1 + H + 1 + (et - HP)] = sum;  // loss, counts
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+    }
+}
+
+// rows -> 128-row tiles in the two operand layouts of batchrt_kernel (tf32, round to nearest)
+__global__ void __launch_bounds__(256) btr_pack_kernel(const float* __restrict__ Xp, int64_t N, int LD,
+                                                       unsigned char* __restrict__ tiles) {
+    __shared__ float t[kRR * 37];
+    const int64_t tile = blockIdx.x;
+    const int64_t row0 = tile * kRR;
+    const int nr = (int)((N - row0) < kRR ? (N - row0) : kRR);
+    for (int e = threadIdx.x; e < kRR * 36; e += blockDim.x) {
+        const int rr = e / 36, k = e - (e / 36) * 36;
+        t[rr * 37 + k] = (rr < nr && k < LD) ? Xp[(row0 + rr) * LD + k] : 0.f;
+    }
+    __syncthreads();
+    uint32_t* out = reinterpret_cast<uint32_t*>(tiles + tile * (int64_t)kRGT);
+    // forward: word w = ((q * 16 + r / 8) * 8 + r % 8) * 4 + k % 4, k = 4 q + k % 4
+    for (int w = threadIdx.x; w < kRXFG / 4; w += blockDim.x) {
+        const int e = w & 3, ro = (w >> 2) & 7, r8 = (w >> 5) & 15, q = w >> 9;
+        out[w] = tf32_rn(t[(r8 * 8 + ro) * 37 + 4 * q + e]);
+    }
+    // backward: word w = ((fb * 32 + r / 4) * 8 + f % 8) * 4 + r % 4, f = 8 fb + f % 8
+    for (int w = threadIdx.x; w < kRXTG / 4; w += blockDim.x) {
+        const int r4 = w & 3, f8 = (w >> 2) & 7, rq = (w >> 5) & 31, fb = w >> 10;
+        const int f = fb * 8 + f8;
+        out[kRXFG / 4 + w] = tf32_rn(f < 36 ? t[(rq * 4 + r4) * 37 + f] : 0.f);
+    }
+}
+
 int a4(int x) { return (x + 3) / 4 * 4; }
 
 // row count from which the FAST precision runs (GLX_BTC_PREC=full / fast override it,
@@ -827,6 +1291,22 @@ int64_t btc_full_rows() {
     if (e && e[0] == 'f' && e[1] == 'a') return 0;
     return (int64_t)1 << 17;
 }
+#ifdef GLX_BTR_TIMING
+}  // namespace
+}  // namespace glx
+extern "C" void glx_btr_timing_dump(void) {
+    unsigned long long h[4096];
+    cudaMemcpyFromSymbol(h, glx::g_btr_dbg, sizeof(h));
+    auto at = [&](int t, int s) { return (long long)h[t * 8 + s]; };
+    const long long t0 = at(0, 0);
+    for (int t = 0; t < 32; t++)
+        printf("lt %2d epi @%7lld z %5lld sig %5lld free %5lld dhw %5lld | mma ready @%7lld issue %4lld | load @%7lld\n",
+               t + 6, at(t, 0) - t0, at(t, 1) - at(t, 0), at(t, 2) - at(t, 1), at(t, 3) - at(t, 2), at(t, 4) - at(t, 3),
+               at(t, 5) - t0, at(t, 6) - at(t, 5), at(t, 7) - t0);
+}
+namespace glx {
+namespace {
+#endif
 #ifdef GLX_BTC_TIMING
 }  // namespace
 }  // namespace glx
@@ -879,6 +1359,64 @@ bool batchtc_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
     g.smem = (size_t)(g.MT ? btc_smem<true>(nh).total : btc_smem<false>(nh).total);
     *out = g;
     return true;
+}
+
+// narrow layers (rows on the lanes): FAST precision, D <= 33, H <= 64
+bool batchrt_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* out) {
+    if (N < btc_full_rows() || N < 1 || D < 1 || D > 33 || H < 1 || H > 64) return false;
+    BatchGeom g{};
+    g.D = D;
+    g.H = H;
+    g.N = N;
+    g.DP = D + 1 <= 8 ? 8 : D + 1 <= 16 ? 16 : 34;
+    g.LD = a4(std::max(D + 2, g.DP));
+    if (g.LD > 36) return false;
+    g.HP = H <= 32 ? 32 : H <= 48 ? 48 : 64;
+    g.P1 = H * (D + 1);
+    g.PS = a4(g.P1 + H + 6);
+    g.WKS = a4(H * g.DP + 2 * H + 1);
+    g.R = kRR;
+    g.ntiles = (N + kRR - 1) / kRR;
+    g.grid = (int)std::min<int64_t>(g.ntiles, n_sms);
+    g.MT = 0;
+    g.smem = g.HP == 32 ? BtrSmem<32>::total : g.HP == 48 ? BtrSmem<48>::total : BtrSmem<64>::total;
+    *out = g;
+    return true;
+}
+
+size_t batchrt_tile_bytes(const BatchGeom& g) { return (size_t)g.ntiles * kRGT; }
+
+cudaError_t launch_batchrt_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st) {
+    btr_pack_kernel<<<(unsigned)g.ntiles, 256, 0, st>>>(Xp, g.N, g.LD, (unsigned char*)tiles);
+    return cudaGetLastError();
+}
+
+template <int HP>
+static cudaError_t launch_btr(const BatchGeom& g, const BtcArgs& a, cudaStream_t st) {
+    auto k = batchrt_kernel<HP>;
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "glx: batchrt_kernel<%d> smem=%zu: %s\n", HP, g.smem, cudaGetErrorString(e));
+        return e;
+    }
+    k<<<g.grid, btr_threads(HP), g.smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_batchrt_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part,
+                                 cudaStream_t st) {
+    BtcArgs a;
+    a.tiles = (const unsigned char*)tiles;
+    a.Wk = Wk;
+    a.part = part;
+    a.N = g.N;
+    a.ntiles = g.ntiles;
+    a.D = g.D;
+    a.DP = g.DP;
+    a.H = g.H;
+    a.P1 = g.P1;
+    a.PS = g.PS;
+    return g.HP == 32 ? launch_btr<32>(g, a, st) : g.HP == 48 ? launch_btr<48>(g, a, st) : launch_btr<64>(g, a, st);
 }
 
 template <int NH, bool FULL>

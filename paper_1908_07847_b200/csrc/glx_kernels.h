@@ -113,6 +113,11 @@ int pick_dp(int D);  // glx_batch.cu: weight-row stride of the FP32 batch kernel
 size_t batchtc_tile_bytes(const BatchGeom& g);
 cudaError_t launch_batchtc_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st);
 cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st);
+// narrow layers (H <= 64, FAST precision): rows on the TMEM lanes, 128-row tiles
+bool batchrt_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* g);
+size_t batchrt_tile_bytes(const BatchGeom& g);
+cudaError_t launch_batchrt_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st);
+cudaError_t launch_batchrt_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st);
 
 // ------------------------------------------------------------ exact eval
 cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,

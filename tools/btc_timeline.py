@@ -14,7 +14,7 @@ import paper_1908_07847_b200 as g  # noqa: E402
 import paper_1908_07847_b200._lib as L  # noqa: E402
 
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 1 << 20
-D, H = 33, 256
+D, H = 33, int(sys.argv[2]) if len(sys.argv) > 2 else 256
 lib = L.load()
 st = torch.cuda.current_stream().cuda_stream
 X, lab = g.synthetic_arrays_device(rows, D, 0, "planted-linear")
@@ -25,4 +25,4 @@ w1, w2 = torch.from_numpy(net.w_ih).cuda(), torch.from_numpy(net.w_ho).cuda()
 for _ in range(2):
     L.check(lib.glx_train_batch(w1.data_ptr(), w2.data_ptr(), Xp.data_ptr(), rows, D, H, 1, 0.1, None, None, st))
 torch.cuda.synchronize()
-ctypes.CDLL(str(L.LIB_PATH)).glx_btc_timing_dump()
+fn = getattr(ctypes.CDLL(str(L.LIB_PATH)), sys.argv[3] if len(sys.argv) > 3 else "glx_btc_timing_dump"); fn()
