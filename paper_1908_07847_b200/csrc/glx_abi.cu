@@ -292,6 +292,9 @@ int batch_kernel_pref() {
 // rows for H <= 128, tools/batch_width_time.py); the FP32 kernels win below ~24 units
 // (H = 16: 0.090 vs 0.116 ms). GLX_BATCH_KERNEL=tc forces the tcgen05 kernel for any H <= 256
 constexpr int kTcMinH = 24;
+// the rows-on-lanes kernel (H <= 64, from 2^17 rows) is flat at ~0.065 ms per 1M rows up
+// to 32 units; the three-role FP32 kernel is level at H = 8 and slower above
+constexpr int kRtMinH = 12;
 bool force_tc() {
     const char* e = getenv("GLX_BATCH_KERNEL");
     return e && e[0] == 't' && e[1] == 'c';
@@ -306,7 +309,7 @@ bool train_geometry(int64_t N, int D, int H, BatchGeom* g, int* kind) {
     const int pref = batch_kernel_pref();
     // narrow layers with enough rows for the FAST precision: rows on the TMEM lanes
     // (glx_batchtc.cu batchrt_kernel); GLX_BATCH_KERNEL=tc keeps the unit-on-lanes kernel
-    if (pref >= 2 && !force_tc() && (H >= kTcMinH || force_rt()) && batchrt_geometry(N, D, H, sm_count_current(), g)) {
+    if (pref >= 2 && !force_tc() && (H >= kRtMinH || force_rt()) && batchrt_geometry(N, D, H, sm_count_current(), g)) {
         *kind = 3;
         return true;
     }

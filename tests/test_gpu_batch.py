@@ -78,6 +78,25 @@ def test_batch_wide_inputs_vs_oracle(gpu, N, D, H):
     assert abs(stats[0, 0] - loss) <= 1e-4 * max(1.0, loss)
 
 
+@pytest.mark.parametrize("N,H", [(200_000, 33), (150_001, 64), (131_072, 12), (300_000, 48)])
+def test_rows_on_lanes_kernel_vs_oracle(gpu, N, H):
+    """The narrow-layer kernel (rows on the TMEM lanes, kind 3; FAST precision from 2^17
+    rows) against the f64 oracle: weights within 1e-5 after 4 epochs, epoch-0
+    statistics equal to the oracle evaluation."""
+    import paper_1908_07847_b200._lib as L
+
+    assert L.load().glx_batch_kernel_kind(N, 33, H) == 3
+    x, l, t, net0 = _case(N, 33, H, seed=H)
+    ref, net = net0.copy(), net0.copy()
+    O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, t, 4, 0.1)
+    stats = np.zeros((4, 5))
+    g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 4, 0.1, g.cuda(), stats)
+    assert max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho)) <= 1e-5
+    (tp, tn, fp, fn), loss = O.eval_counts(net0.w_ih2d, net0.w_ho2d, x, l)
+    assert np.abs(stats[0, 1:] - np.array([tp, tn, fp, fn])).sum() <= 4
+    assert abs(stats[0, 0] - loss) <= 1e-5 * loss
+
+
 def test_tcgen05_fast_precision_padded_width(gpu, monkeypatch):
     """The large-N (FAST) precision with a padded width, 150k rows x 33 -> 192 -> 1."""
     monkeypatch.setenv("GLX_BTC_PREC", "fast")
@@ -100,6 +119,9 @@ def test_tcgen05_kernel_selected_for_headline_shapes(gpu):
     assert lib.glx_batch_kernel_kind(1000, 33, 128) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 192) == 2 and lib.glx_batch_kernel_kind(1000, 33, 97) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 33) == 2 and lib.glx_batch_kernel_kind(1000, 33, 64) == 2
+    # from 2^17 rows, narrow layers run the rows-on-lanes kernel (kind 3)
+    assert lib.glx_batch_kernel_kind(1 << 20, 33, 33) == 3 and lib.glx_batch_kernel_kind(1 << 20, 33, 64) == 3
+    assert lib.glx_batch_kernel_kind(1 << 20, 33, 12) == 3 and lib.glx_batch_kernel_kind(1 << 20, 33, 65) == 2
     assert lib.glx_batch_kernel_kind(1000, 33, 16) in (0, 1)
     assert lib.glx_batch_kernel_kind(1000, 33, 512) in (0, 1)
     assert lib.glx_batch_kernel_kind(1000, 40, 256) in (0, 1)  # D > 33: FP32 kernels
