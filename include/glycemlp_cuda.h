@@ -99,7 +99,10 @@ void glx_cache_clear(void);
 
 /* ---------------------------------------------------------------- device API */
 
-/* Online SGD on device buffers (single network). X: N x D, T: N. */
+/* Online SGD on device buffers (single network). X: N x D, T: N. Any D and H:
+ * D <= 63 and H <= 512 run the register-tiled kernels, wider networks the
+ * any-shape engine (weights in global memory; fails with GLX_ERR_INVALID when
+ * 2D + H floats of row and activations exceed its ~200 KB of shared memory). */
 int glx_train_online(float* w_ih, float* w_ho, const float* X, const float* T, int64_t N, int32_t D, int32_t H,
                      int64_t epochs, double lr, int32_t numerics, void* stream);
 
@@ -155,8 +158,9 @@ int glx_train_batch(float* w_ih, float* w_ho, const float* Xp, int64_t N, int32_
 /* Which full-batch epoch kernel glx_train_batch / glx_batch_grad run for this
  * shape: 3 = tcgen05 rows-on-lanes kernel (24 <= H <= 64, D <= 33, from 2^17
  * rows), 2 = tcgen05 units-on-lanes kernel (24 <= H <= 256, D <= 33), 1 =
- * three-role FP32 kernel, 0 = two-role FP32 kernel (D <= 127), -1 = unsupported
- * shape. Selection only (no device work); GLX_BATCH_KERNEL=3 / =2 cap the choice
+ * three-role FP32 kernel, 0 = two-role FP32 kernel (D <= 127, H <= 512), 4 =
+ * the any-shape FP32 engine (tiled GEMM-shaped kernels, glx_generic.cu), -1 =
+ * invalid arguments. Selection only (no device work); GLX_BATCH_KERNEL=3 / =2 cap the choice
  * at 1 / 0, =tc / =rt force a tcgen05 kernel. No reference counterpart (diagnostic). */
 int glx_batch_kernel_kind(int64_t N, int32_t D, int32_t H);
 

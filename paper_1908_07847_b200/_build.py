@@ -17,7 +17,7 @@ CSRC = PKG / "csrc"
 INCLUDE = ROOT / "include"
 BUILD = ROOT / "build"
 LIB = PKG / "libglycemlp_cuda.so"
-SOURCES = ("glx_online.cu", "glx_batch.cu", "glx_batch3.cu", "glx_batchtc.cu", "glx_eval.cu", "glx_tc.cu", "glx_data.cu", "glx_abi.cu")
+SOURCES = ("glx_online.cu", "glx_batch.cu", "glx_batch3.cu", "glx_batchtc.cu", "glx_eval.cu", "glx_tc.cu", "glx_data.cu", "glx_generic.cu", "glx_abi.cu")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 # NCCL is bound at run time (dlopen in glx_abi.cu), so the library never pins a
 # libnccl.so.2 that could shadow the one torch loads

@@ -78,7 +78,7 @@ struct DevBuf {
 
 // scratch tied to one (device, stream): stream order serialises its reuse
 struct Workspace {
-    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm, tiles;
+    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm, tiles, gen;
 };
 
 std::mutex g_ws_mu;
@@ -173,12 +173,33 @@ int online_mt(size_t n_nets, bool ref64, int dp, int max_h, double big_frac) {
     return mt;
 }
 
+// widths outside the register-tiled kernels (D > 63 or H > 512): one CTA per
+// network, weights in global memory (glx_generic.cu)
+int run_online_generic(const std::vector<NetReq>& nets, const float* X, const float* T, int64_t N, int D,
+                       int64_t epochs, double lr, bool ref64, cudaStream_t st) {
+    std::vector<GenNet> g(nets.size());
+    int max_h = 0;
+    for (size_t n = 0; n < nets.size(); n++) {
+        g[n] = GenNet{nets[n].w_ih, nets[n].w_ho, nets[n].H, 0};
+        max_h = std::max(max_h, nets[n].H);
+    }
+    if (online_generic_smem(D, max_h) > kGenMaxSmem)
+        return set_err(GLX_ERR_INVALID, "online engine: input_dim %d with hidden_dim %d exceeds the shared-memory row "
+                       "and activation buffers (%zu bytes > %zu)", D, max_h, online_generic_smem(D, max_h),
+                       kGenMaxSmem);
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->desc.ensure(g.size() * sizeof(GenNet)));
+    GLX_CK(cudaMemcpyAsync(ws->desc.p, g.data(), g.size() * sizeof(GenNet), cudaMemcpyHostToDevice, st));
+    GLX_LAUNCH(launch_online_generic(ws->desc.as<GenNet>(), (int)g.size(), max_h, X, T, N, D, epochs, lr, ref64, st));
+    return GLX_OK;
+}
+
 int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t N, int D, int64_t epochs, double lr,
                bool ref64, cudaStream_t st) {
     const int dp = online_dp_for(D);
-    if (dp < 0) return set_err(GLX_ERR_INVALID, "online kernel supports input_dim <= 63, got %d", D);
-    for (auto& n : nets)
-        if (n.H < 1 || n.H > 512) return set_err(GLX_ERR_INVALID, "online kernel supports 1 <= hidden_dim <= 512, got %d", n.H);
+    int max_h = 0;
+    for (auto& n : nets) max_h = std::max(max_h, n.H);
+    if (dp < 0 || max_h > 512) return run_online_generic(nets, X, T, N, D, epochs, lr, ref64, st);
     // exact path, one paper-size network: the f64-resident small kernel
     if (ref64 && nets.size() == 1 && nets[0].H <= 64 && dp <= 34 && online_ref64_small_smem(N, D) <= 160 * 1024 &&
         getenv("GLX_ONLINE_REF64_SMALL") == nullptr) {
@@ -188,10 +209,8 @@ int run_online(std::vector<NetReq> nets, const float* X, const float* T, int64_t
     // staged rows [N][dp], targets [N], lookahead dots [N] (glx_online.cu)
     const size_t xbytes = ((size_t)N * ((dp + 3) & ~3) * 4 + (size_t)N * 8 + 15) / 16 * 16;  // rows padded to 4
     const bool x_in_smem = xbytes <= 160 * 1024;
-    int max_h = 0;
     double units = 0, big_units = 0;
     for (auto& n : nets) {
-        max_h = std::max(max_h, n.H);
         units += n.H;
         if (n.H >= 128) big_units += n.H;
     }
@@ -351,13 +370,49 @@ cudaError_t launch_train_epoch(const BatchGeom& g, int kind, const void* in, con
     return kind == 1 ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
 }
 
+}  // namespace
+namespace glx {
+cudaError_t launch_batch_grad(const BatchGeom& g, const float* part, const float* Wk, double* grad, cudaStream_t st);
+cudaError_t launch_batch_apply(int D, int H, float* W1, float* W2, const double* grad, double lr_over_n,
+                               int* nonfinite, cudaStream_t st);
+}  // namespace glx
+namespace {
+
+// any shape outside the batch kernels (kind 4, glx_generic.cu): this rank's f64
+// gradient sum in the glx_batch_grad layout
+int generic_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_t N, int D, int H, double* grad,
+                 cudaStream_t st) {
+    Workspace* ws = workspace(st);
+    GLX_CK(ws->gen.ensure(generic_work_bytes(N, D, H)));
+    const int64_t nlaunch = 4 * ((N + (int64_t)generic_chunk_rows(N, H) - 1) / (int64_t)generic_chunk_rows(N, H));
+    GLX_CK(generic_batch_grad(w_ih, w_ho, Xp, N, D, H, glx_packed_ld(D), ws->gen.p, grad, st));
+    g_launches.fetch_add(nlaunch);
+    return GLX_OK;
+}
+
+int generic_train(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, int H, int64_t epochs, double lr,
+                  double* stats_hist, int32_t* nonfinite, cudaStream_t st) {
+    Workspace* ws = workspace(st);
+    const int64_t glen = (int64_t)H * (D + 1) + H + 1 + 5;
+    GLX_CK(ws->grad.ensure((size_t)glen * sizeof(double)));
+    double* grad = ws->grad.as<double>();
+    for (int64_t e = 0; e < epochs; e++) {
+        int rc = generic_grad(w_ih, w_ho, Xp, N, D, H, grad, st);
+        if (rc) return rc;
+        GLX_LAUNCH(launch_batch_apply(D, H, w_ih, w_ho, grad, lr / (double)N, nonfinite, st));
+        if (stats_hist)  // loss, tp, tn, fp, fn at this epoch's starting weights
+            GLX_CK(cudaMemcpyAsync(stats_hist + 5 * e, grad + glen - 5, 5 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   st));
+    }
+    return GLX_OK;
+}
+
 int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, int H, int64_t epochs, double lr,
                      double* stats_hist, int32_t* nonfinite, cudaStream_t st) {
     BatchGeom g;
     int kind = 0;
-    if (!train_geometry(N, D, H, &g, &kind))
-        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d N=%lld (needs D<=127, H<=512)", D,
-                       H, (long long)N);
+    if (!train_geometry(N, D, H, &g, &kind)) return generic_train(w_ih, w_ho, Xp, N, D, H, epochs, lr, stats_hist,
+                                                                  nonfinite, st);
     Workspace* ws = workspace(st);
     GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
     GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
@@ -389,10 +444,6 @@ size_t online_scratch_bytes(int H, bool ref64) {
     const int nb = (H + 15) / 16;
     return (size_t)(nb * 17 + 2) * sizeof(double);
 }
-// defined in glx_batch.cu
-cudaError_t launch_batch_grad(const BatchGeom& g, const float* part, const float* Wk, double* grad, cudaStream_t st);
-cudaError_t launch_batch_apply(int D, int H, float* W1, float* W2, const double* grad, double lr_over_n,
-                               int* nonfinite, cudaStream_t st);
 }  // namespace glx
 
 namespace {
@@ -504,12 +555,40 @@ int dp_epoch_enqueue(DpComm* dp, const BatchGeom& g, int kind, bool have_rows, c
     return GLX_OK;
 }
 
+// shapes outside the batch kernels: eager epochs of the any-shape gradient, the
+// all-reduce and the plain update
+int dp_train_generic(DpComm* dp, float* w_ih, float* w_ho, const float* Xp, int64_t N, int64_t N_total, int D, int H,
+                     int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, cudaStream_t caller) {
+    GLX_CK(cudaSetDevice(dp->dev));
+    const int64_t glen = (int64_t)H * (D + 1) + H + 1 + 5;
+    GLX_CK(dp->grad.ensure((size_t)glen * sizeof(double)));
+    double* grad = dp->grad.as<double>();
+    GLX_CK(cudaEventRecord(dp->ev_in, caller));
+    GLX_CK(cudaStreamWaitEvent(dp->st, dp->ev_in, 0));
+    for (int64_t e = 0; e < epochs; e++) {
+        if (N > 0) {
+            int rc = generic_grad(w_ih, w_ho, Xp, N, D, H, grad, dp->st);
+            if (rc) return rc;
+        } else {
+            GLX_CK(cudaMemsetAsync(grad, 0, glen * sizeof(double), dp->st));
+        }
+        GLX_NCCL(nccl().AllReduce(grad, grad, (size_t)glen, ncclDouble, ncclSum, dp->comm, dp->st));
+        GLX_LAUNCH(launch_batch_apply(D, H, w_ih, w_ho, grad, lr / (double)N_total, nonfinite, dp->st));
+        if (stats_hist)
+            GLX_CK(cudaMemcpyAsync(stats_hist + 5 * e, grad + glen - 5, 5 * sizeof(double), cudaMemcpyDeviceToDevice,
+                                   dp->st));
+    }
+    GLX_CK(cudaEventRecord(dp->ev_out, dp->st));
+    GLX_CK(cudaStreamWaitEvent(caller, dp->ev_out, 0));
+    return GLX_OK;
+}
+
 int dp_train_batch(DpComm* dp, float* w_ih, float* w_ho, const float* Xp, int64_t N, int64_t N_total, int D, int H,
                    int64_t epochs, double lr, double* stats_hist, int32_t* nonfinite, cudaStream_t caller) {
     BatchGeom g;
     int kind = 0;
     if (!train_geometry(std::max<int64_t>(N, 1), D, H, &g, &kind))
-        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d", D, H);
+        return dp_train_generic(dp, w_ih, w_ho, Xp, N, N_total, D, H, epochs, lr, stats_hist, nonfinite, caller);
     GLX_CK(cudaSetDevice(dp->dev));
     Workspace* ws = workspace(dp->st);
     GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
@@ -721,7 +800,8 @@ int64_t glx_batch_grad_len(int32_t D, int32_t H) { return (int64_t)H * (D + 1) +
 int glx_batch_kernel_kind(int64_t N, int32_t D, int32_t H) {
     BatchGeom g;
     int kind = -1;
-    if (N < 1 || D < 1 || H < 1 || !train_geometry(N, D, H, &g, &kind)) return -1;
+    if (N < 1 || D < 1 || H < 1) return -1;
+    if (!train_geometry(N, D, H, &g, &kind)) return 4;  // the any-shape engine (glx_generic.cu)
     return kind;
 }
 
@@ -736,8 +816,7 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
     }
     BatchGeom g;
     int kind = 0;
-    if (!train_geometry(N, D, H, &g, &kind))
-        return set_err(GLX_ERR_INVALID, "batch kernel: unsupported shape D=%d H=%d", D, H);
+    if (!train_geometry(N, D, H, &g, &kind)) return generic_grad(w_ih, w_ho, Xp, N, D, H, grad, st);
     Workspace* ws = workspace(st);
     GLX_CK(ws->part.ensure((size_t)g.grid * g.PS * 4));
     GLX_CK(ws->wk.ensure((size_t)2 * g.WKS * 4));
@@ -999,7 +1078,9 @@ int glx_eval_counts(const float* w_ih, const float* w_ho, const float* feats, co
     GLX_CK(cudaMemcpyAsync(xb->p, feats, xbytes, cudaMemcpyHostToDevice, st));
     uint64_t hc[4] = {0, 0, 0, 0};
     double hl[5] = {0, 0, 0, 0, 0};
-    if (numerics == GLX_REF64 || output_dim > 1) {
+    BatchGeom eg;
+    const bool fused_eval = batch_geometry(rows, input_dim, hidden_dim, sm_count_current(), false, &eg);
+    if (numerics == GLX_REF64 || output_dim > 1 || !fused_eval) {  // exact kernel (any shape)
         GLX_CK(cudaMemsetAsync(hs->cnt.p, 0, 4 * sizeof(uint64_t), st));
         rc = glx_eval(hs->w1.as<float>(), hs->w2.as<float>(), xb->as<float>(), hs->lab.as<uint8_t>(), rows, input_dim,
                       hidden_dim, output_dim, hs->cnt.as<uint64_t>(), hs->loss.as<double>(), st);

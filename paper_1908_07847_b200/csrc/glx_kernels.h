@@ -171,6 +171,25 @@ cudaError_t wide_epoch_tf32(float* W1, float* W2, const float* X, const float* X
                             double lr, unsigned char* work, int64_t C, int splits, double* stats, int* nonfinite,
                             cudaStream_t st, const std::function<void(bool)>& prof);
 
+// any-shape engines (glx_generic.cu): online SGD for D > 63 or H > 512, the
+// full-batch gradient for shapes outside the batch kernels' register tiles
+struct GenNet {
+    float* w_ih;  // H x (D+1)
+    float* w_ho;  // H + 1
+    int H;
+    int pad;
+};
+constexpr size_t kGenMaxSmem = 200 * 1024;
+size_t online_generic_smem(int D, int H);
+cudaError_t launch_online_generic(const GenNet* nets, int n_nets, int max_h, const float* X, const float* T, int64_t N,
+                                  int D, int64_t epochs, double lr, bool ref64, cudaStream_t st);
+size_t generic_chunk_rows(int64_t N, int H);
+size_t generic_work_bytes(int64_t N, int D, int H);
+// grad (f64, glx_batch_grad layout: H(D+1) dW1 sums, H + 1 dW2 sums, loss, tp,
+// tn, fp, fn) of the packed rows Xp [N][LD] under (W1, W2)
+cudaError_t generic_batch_grad(const float* W1, const float* W2, const float* Xp, int64_t N, int D, int H, int LD,
+                               void* work, double* grad, cudaStream_t st);
+
 // ------------------------------------------------------------ diagnostics
 cudaError_t launch_fp32_peak(float* out, int iters, int blocks, cudaStream_t st);
 
