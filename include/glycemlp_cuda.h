@@ -39,11 +39,17 @@ extern "C" {
 #define GLX_ERR_NUMERIC (-3) /* NumericError     (errors.py:24) */
 #define GLX_ERR_CUDA (-4)    /* RuntimeError: CUDA / NCCL failure */
 #define GLX_ERR_NOMEM (-5)   /* MemoryError */
+#define GLX_ERR_RACE (-6)    /* RuntimeError: a debug run's pipeline check failed (backend.py:130-132) */
 
 #define GLX_FP32 0
 #define GLX_REF64 1
 
 #define GLX_FLAG_CACHE_INPUTS 1 /* host API: keep feats/targets resident keyed by host pointer */
+/* host API, full batch: check the tcgen05 epoch kernels' pipelines every epoch (tile
+ * hand-off stamps and per-tile visit counts; GLX_ERR_RACE on a violation) -- the
+ * device analogue of the reference's debug=True instrumentation (backend.py:122-133,
+ * 237-284). Costs one host sync per epoch. */
+#define GLX_FLAG_DEBUG 2
 
 const char* glx_last_error(void);
 int glx_version(void);
@@ -286,6 +292,25 @@ uint64_t glx_launch_count(void);
  * enabled, an event pair is recorded on the launching stream around every
  * launch; glx_profile_read synchronises, returns the summed kernel time and
  * launch count since the last read, and resets. */
+/* Debug instrumentation of the layer-level API (backend.py:122-133, 237-284).
+ * write_counts (device int32[N*n] / [n], zeroed by the caller): every output
+ * slot adds 1 when written; the caller requires all ones. glx_forward_pair_debug:
+ * `workers` warps write the hidden activations and stamp each slot; after the
+ * layer barrier the output pass checks every stamp (status: device int32, 0 = ok,
+ * 1 + j = hidden slot j read before it was written; stamps: device int32[H],
+ * zeroed by the caller). */
+int glx_layer_forward_checked(const float* W, const float* X, int64_t N, int32_t m, int32_t n, float* out,
+                              int32_t* write_counts, void* stream);
+int glx_layer_backward_checked(const float* x, const float* acts, const double* err, int32_t n, int32_t m,
+                               double* deltas, double* grads, int32_t* write_counts, void* stream);
+int glx_forward_pair_debug(const float* w_ih, const float* w_ho, const float* x, int32_t D, int32_t H, int32_t K,
+                           float* hidden, float* out, int32_t* stamps, int32_t* status, int32_t workers,
+                           void* stream);
+
+/* Process-wide debug switch: every full-batch training call (host and device API)
+ * runs the GLX_FLAG_DEBUG pipeline checks, as does glx_batch_grad. */
+void glx_set_debug(int32_t on);
+
 void glx_profile_enable(int32_t on);
 int glx_profile_read(double* total_ms, int64_t* launches);
 /* FFMA2 throughput microbenchmark on `device`: returns TFLOP/s. */

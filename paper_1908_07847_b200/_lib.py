@@ -23,6 +23,8 @@ GLX_ERR_INVALID = -2
 GLX_ERR_NUMERIC = -3
 GLX_ERR_CUDA = -4
 GLX_ERR_NOMEM = -5
+GLX_ERR_RACE = -6  # a debug run's pipeline check failed -> RuntimeError
+GLX_FLAG_DEBUG = 2
 
 GLX_FP32 = 0
 GLX_REF64 = 1
@@ -67,6 +69,9 @@ SIGNATURES = {
     "glx_forward": (_int, [_vp, _vp, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp]),
     "glx_layer_forward": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _vp]),
     "glx_layer_backward": (_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp]),
+    "glx_layer_forward_checked": (_int, [_vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp]),
+    "glx_layer_backward_checked": (_int, [_vp, _vp, _vp, _i32, _i32, _vp, _vp, _vp, _vp]),
+    "glx_forward_pair_debug": (_int, [_vp, _vp, _vp, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _i32, _vp]),
     "glx_backprop_error": (_int, [_vp, _vp, _i32, _i32, _vp, _vp]),
     "glx_instance_gradients": (_int, [_vp, _vp, _vp, _vp, _dbl, _i32, _i32, _vp, _vp, _vp]),
     "glx_pcg64_uniform_f32": (_int, [_u64, _u64, _u64, _u64, _i64, _i64, _vp, _vp]),
@@ -90,6 +95,7 @@ SIGNATURES = {
     "glx_wide_train_tf32": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _i64, _dbl, _vp, _vp, _vp]),
     "glx_launch_count": (_u64, []),
     "glx_profile_enable": (None, [_i32]),
+    "glx_set_debug": (None, [_i32]),
     "glx_profile_read": (_int, [_vp, _vp]),
     "glx_fp32_peak": (_int, [_i32, _i32, _vp, _vp]),
 }

@@ -154,12 +154,15 @@ def run_train_segment(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarra
 
 def run_train_segment_batch(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.ndarray, targets: np.ndarray,
                             epochs: int, lr: float, kind: BackendKind, stats: np.ndarray | None = None, *,
-                            cache_inputs: bool = False) -> None:
+                            cache_inputs: bool = False, debug: bool = False) -> None:
     """`epochs` of full-batch gradient descent (mean gradient over all rows), in place.
 
     SURVEY.md 8(a) a13 (no reference implementation; parity against the
     oracle restatement). `stats`, if given, is a float64 (epochs, 5) array
     receiving loss sum, tp, tn, fp, fn at each epoch's starting weights.
+    `debug` checks the tcgen05 epoch kernels' pipelines every epoch (tile hand-off
+    stamps, one visit per row tile; RuntimeError on a violation) -- the device
+    analogue of the reference's debug instrumentation (backend.py:122-133, 237-284).
     """
     _check_inputs(w_ih2d, feats2d, targets)
     D, H = _check_weights(w_ih2d, w_ho2d)
@@ -173,7 +176,7 @@ def run_train_segment_batch(w_ih2d: np.ndarray, w_ho2d: np.ndarray, feats2d: np.
         sp = _lib.ptr(stats)
     _lib.check(L.glx_run_train_segment_batch(
         _lib.ptr(w_ih2d), _lib.ptr(w_ho2d), _lib.ptr(X), _lib.ptr(T), X.shape[0], D, H, int(epochs), float(lr),
-        sp, kind.device, _cache_flag(cache_inputs, X, T)))
+        sp, kind.device, _cache_flag(cache_inputs, X, T) | (_lib.GLX_FLAG_DEBUG if debug else 0)))
 
 
 @dataclass(frozen=True)
@@ -287,11 +290,19 @@ def _dev(kind: BackendKind | None):
     return torch.device("cuda", (kind or sequential()).device)
 
 
+def _check_written_once(counts) -> None:
+    """The reference's write-once shadow check (backend.py:122-133)."""
+    c = counts.cpu().numpy()
+    if not (c == 1).all():
+        bad = np.flatnonzero(c != 1)
+        raise RuntimeError(f"output slots written != once: indices {bad.tolist()}")
+
+
 def run_layer_forward(job: LayerJob, kind: BackendKind | None = None, debug: bool = False) -> np.ndarray:
     """outputs[j] = sigmoid(dot(weights row j, inputs) + bias_j), filled in place
-    (backend.py:134-144), on the device in the reference's f64 order. `debug`
-    (the reference's write-once check of its thread pool) has no device analogue:
-    each neuron is one thread's single store."""
+    (backend.py:134-144), on the device in the reference's f64 order. `debug`: every
+    output slot counts its writes on the device (glx_layer_forward_checked) and
+    each must be written exactly once (backend.py:122-133)."""
     import torch
 
     L = _lib.load()
@@ -300,8 +311,14 @@ def run_layer_forward(job: LayerJob, kind: BackendKind | None = None, debug: boo
     W = torch.from_numpy(np.ascontiguousarray(job.weights)).to(dev)
     x = torch.from_numpy(np.ascontiguousarray(job.inputs)).to(dev)
     out = torch.empty(n, dtype=torch.float32, device=dev)
-    _lib.check(L.glx_layer_forward(W.data_ptr(), x.data_ptr(), 1, m1 - 1, n, out.data_ptr(),
-                                   torch.cuda.current_stream(dev).cuda_stream))
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if debug:
+        counts = torch.zeros(n, dtype=torch.int32, device=dev)
+        _lib.check(L.glx_layer_forward_checked(W.data_ptr(), x.data_ptr(), 1, m1 - 1, n, out.data_ptr(),
+                                               counts.data_ptr(), st))
+        _check_written_once(counts)
+    else:
+        _lib.check(L.glx_layer_forward(W.data_ptr(), x.data_ptr(), 1, m1 - 1, n, out.data_ptr(), st))
     job.outputs[:] = out.cpu().numpy()
     return job.outputs
 
@@ -324,9 +341,50 @@ def run_layer_backward(job: LayerJob, upstream_error: np.ndarray, kind: BackendK
     e = torch.from_numpy(err).to(dev)
     deltas = torch.empty(n, dtype=torch.float64, device=dev)
     grads = torch.empty((n, m1), dtype=torch.float64, device=dev)
-    _lib.check(L.glx_layer_backward(x.data_ptr(), a.data_ptr(), e.data_ptr(), n, m1 - 1, deltas.data_ptr(),
-                                    grads.data_ptr(), torch.cuda.current_stream(dev).cuda_stream))
+    st = torch.cuda.current_stream(dev).cuda_stream
+    if debug:  # each neuron's delta and gradient row written exactly once
+        counts = torch.zeros(n, dtype=torch.int32, device=dev)
+        _lib.check(L.glx_layer_backward_checked(x.data_ptr(), a.data_ptr(), e.data_ptr(), n, m1 - 1,
+                                                deltas.data_ptr(), grads.data_ptr(), counts.data_ptr(), st))
+        _check_written_once(counts)
+    else:
+        _lib.check(L.glx_layer_backward(x.data_ptr(), a.data_ptr(), e.data_ptr(), n, m1 - 1, deltas.data_ptr(),
+                                        grads.data_ptr(), st))
     return deltas.cpu().numpy(), grads.cpu().numpy()
+
+
+def forward_pair_debug(w_ih2d: np.ndarray, w_ho2d: np.ndarray, instance: np.ndarray, workers: int = 2,
+                       kind: BackendKind | None = None) -> tuple[np.ndarray, np.ndarray]:
+    """Instrumented two-layer forward proving the inter-layer barrier
+    (backend.py:237-284) on the device: `workers` warps write and generation-stamp
+    the hidden slots, and past the layer barrier the output pass requires every
+    stamp to be current (RuntimeError naming the stale slots otherwise)."""
+    import torch
+
+    if w_ih2d.ndim != 2 or w_ho2d.ndim != 2 or w_ho2d.shape[1] != w_ih2d.shape[0] + 1:
+        raise ShapeError(f"weight shapes {w_ih2d.shape} / {w_ho2d.shape} do not chain")
+    H, D = w_ih2d.shape[0], w_ih2d.shape[1] - 1
+    K = w_ho2d.shape[0]
+    x = np.ascontiguousarray(instance, dtype=np.float32).ravel()
+    if x.shape[0] != D:
+        raise ShapeError(f"instance has {x.shape[0]} features, network expects {D}")
+    L = _lib.load()
+    dev = _dev(kind)
+    W1 = torch.from_numpy(_f32c(w_ih2d)).to(dev)
+    W2 = torch.from_numpy(_f32c(w_ho2d)).to(dev)
+    xd = torch.from_numpy(x).to(dev)
+    hidden = torch.empty(H, dtype=torch.float32, device=dev)
+    out = torch.empty(K, dtype=torch.float32, device=dev)
+    stamps = torch.zeros(H, dtype=torch.int32, device=dev)
+    status = torch.full((1,), -1, dtype=torch.int32, device=dev)
+    _lib.check(L.glx_forward_pair_debug(W1.data_ptr(), W2.data_ptr(), xd.data_ptr(), D, H, K, hidden.data_ptr(),
+                                        out.data_ptr(), stamps.data_ptr(), status.data_ptr(), int(workers),
+                                        torch.cuda.current_stream(dev).cuda_stream))
+    s = int(status.item())
+    if s != 0:
+        stale = np.flatnonzero(stamps.cpu().numpy() != 1)
+        raise RuntimeError(f"hidden slots read before write: {stale.tolist()}")
+    return hidden.cpu().numpy(), out.cpu().numpy()
 
 
 def backpropagate_error(weights: np.ndarray, deltas: np.ndarray, kind: BackendKind | None = None) -> np.ndarray:

@@ -78,7 +78,7 @@ struct DevBuf {
 
 // scratch tied to one (device, stream): stream order serialises its reuse
 struct Workspace {
-    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm, tiles, gen;
+    DevBuf part, wk, desc, ctan, losspart, grad, wide, norm, tiles, gen, dbg;
 };
 
 std::mutex g_ws_mu;
@@ -363,10 +363,10 @@ int epoch_input(Workspace* ws, const BatchGeom& g, int kind, const float* Xp, cu
 }
 
 cudaError_t launch_train_epoch(const BatchGeom& g, int kind, const void* in, const float* Wk, float* part,
-                               cudaStream_t st) {
+                               cudaStream_t st, int* dbg = nullptr) {
     const float* Xp = (const float*)in;
-    if (kind == 3) return launch_batchrt_epoch(g, in, Wk, part, st);
-    if (kind == 2) return launch_batchtc_epoch(g, in, Wk, part, st);
+    if (kind == 3) return launch_batchrt_epoch(g, in, Wk, part, st, dbg);
+    if (kind == 2) return launch_batchtc_epoch(g, in, Wk, part, st, dbg);
     return kind == 1 ? launch_batch3_epoch(g, Xp, Wk, part, st) : launch_batch_epoch(g, Xp, Wk, part, true, st);
 }
 
@@ -407,8 +407,46 @@ int generic_train(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, i
     return GLX_OK;
 }
 
+// debug runs (GLX_FLAG_DEBUG, glx_set_debug): the tcgen05 epoch kernels stamp every
+// tile hand-off between their roles and count the tiles each role handled
+// (glx_batchtc.cu dbg_expect); after each epoch the host requires no stale stamp,
+// one forward issue per row tile and one dh hand-off per row group of it
+std::atomic<int> g_debug{0};
+
+int pipeline_verify(const BatchGeom& g, int kind, const int* dbg, int64_t epoch, cudaStream_t st) {
+    constexpr int kHdr = 16;  // glx_batchtc.cu kDbgHdr
+    std::vector<int> h(kHdr + 2 * (size_t)g.ntiles);
+    GLX_CK(cudaMemcpyAsync(h.data(), dbg, h.size() * sizeof(int), cudaMemcpyDeviceToHost, st));
+    GLX_CK(cudaStreamSynchronize(st));
+    if (h[0])
+        return set_err(GLX_ERR_RACE, "epoch kernel pipeline check (kind %d), epoch %lld: %d stale hand-off(s); first: "
+                       "check %d in CTA %d expected tile stamp %d, saw %d", kind, (long long)epoch, h[0], h[1], h[2],
+                       h[3], h[4]);
+    const int want_b = kind == 2 ? 2 : 4;  // row blocks (kind 2) / row quadrants (kind 3) per tile
+    for (int64_t t = 0; t < g.ntiles; t++) {
+        const int f = h[kHdr + t], b = h[kHdr + g.ntiles + t];
+        if (f != 1 || b != want_b)
+            return set_err(GLX_ERR_RACE, "epoch kernel pipeline check (kind %d), epoch %lld: row tile %lld had %d "
+                           "forward issue(s) and %d dh hand-off(s), want 1 and %d", kind, (long long)epoch,
+                           (long long)t, f, b, want_b);
+    }
+    return GLX_OK;
+}
+
+// GLX_DEBUG_INJECT_TILE=t (tests): the producer stamps row tile t wrongly, so a debug
+// run must fail -- proof that the checker observes the hand-offs
+int pipeline_inject(int* dbg, cudaStream_t st) {
+    const char* e = getenv("GLX_DEBUG_INJECT_TILE");
+    if (!e) return GLX_OK;
+    static thread_local int v;
+    v = atoi(e) + 1;
+    GLX_CK(cudaMemcpyAsync(dbg + 6, &v, sizeof(int), cudaMemcpyHostToDevice, st));
+    GLX_CK(cudaStreamSynchronize(st));
+    return GLX_OK;
+}
+
 int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D, int H, int64_t epochs, double lr,
-                     double* stats_hist, int32_t* nonfinite, cudaStream_t st) {
+                     double* stats_hist, int32_t* nonfinite, cudaStream_t st, bool debug = false) {
     BatchGeom g;
     int kind = 0;
     if (!train_geometry(N, D, H, &g, &kind)) return generic_train(w_ih, w_ho, Xp, N, D, H, epochs, lr, stats_hist,
@@ -423,13 +461,28 @@ int batch_train_impl(float* w_ih, float* w_ho, const float* Xp, int64_t N, int D
     int rc = epoch_input(ws, g, kind, Xp, st, &in);
     if (rc) return rc;
     const double lr_over_n = lr / (double)N;
+    const bool check = (debug || g_debug.load()) && (kind == 2 || kind == 3);
+    int* dbg = nullptr;
+    if (check) {
+        GLX_CK(ws->dbg.ensure(pipeline_check_ints(g) * sizeof(int)));
+        dbg = ws->dbg.as<int>();
+    }
     for (int64_t e = 0; e < epochs; e++) {
         float* cur = (e & 1) ? wk1 : wk0;
         float* nxt = (e & 1) ? wk0 : wk1;
+        if (check) {
+            GLX_CK(cudaMemsetAsync(dbg, 0, pipeline_check_ints(g) * sizeof(int), st));
+            int rc = pipeline_inject(dbg, st);
+            if (rc) return rc;
+        }
         cudaEvent_t pe = nullptr;
         GLX_CK(prof_begin(st, &pe));
-        GLX_LAUNCH(launch_train_epoch(g, kind, in, cur, ws->part.as<float>(), st));
+        GLX_LAUNCH(launch_train_epoch(g, kind, in, cur, ws->part.as<float>(), st, dbg));
         if (pe) GLX_CK(cudaEventRecord(pe, st));
+        if (check) {
+            int rc = pipeline_verify(g, kind, dbg, e, st);
+            if (rc) return rc;
+        }
         GLX_LAUNCH(launch_batch_update(g, ws->part.as<float>(), w_ih, w_ho, cur, nxt, lr_over_n, true,
                                        stats_hist ? stats_hist + 5 * e : nullptr, nonfinite, st));
     }
@@ -825,10 +878,21 @@ int glx_batch_grad(const float* w_ih, const float* w_ho, const float* Xp, int64_
     const void* in = nullptr;
     rc = epoch_input(ws, g, kind, Xp, st, &in);
     if (rc) return rc;
+    const bool check = g_debug.load() && (kind == 2 || kind == 3);
+    int* dbg = nullptr;
+    if (check) {
+        GLX_CK(ws->dbg.ensure(pipeline_check_ints(g) * sizeof(int)));
+        dbg = ws->dbg.as<int>();
+        GLX_CK(cudaMemsetAsync(dbg, 0, pipeline_check_ints(g) * sizeof(int), st));
+    }
     cudaEvent_t pe = nullptr;
     GLX_CK(prof_begin(st, &pe));
-    GLX_LAUNCH(launch_train_epoch(g, kind, in, wk0, ws->part.as<float>(), st));
+    GLX_LAUNCH(launch_train_epoch(g, kind, in, wk0, ws->part.as<float>(), st, dbg));
     if (pe) GLX_CK(cudaEventRecord(pe, st));
+    if (check) {
+        rc = pipeline_verify(g, kind, dbg, 0, st);
+        if (rc) return rc;
+    }
     GLX_LAUNCH(launch_batch_grad(g, ws->part.as<float>(), wk0, grad, st));
     return GLX_OK;
 }
@@ -882,6 +946,35 @@ int glx_layer_backward(const float* x, const float* acts, const double* err, int
                        double* grads, void* stream) {
     if (m < 0 || n < 1) return set_err(GLX_ERR_SHAPE, "bad layer shape (m=%d n=%d)", m, n);
     GLX_LAUNCH(launch_layer_backward(x, acts, err, n, m, deltas, grads, (cudaStream_t)stream));
+    return GLX_OK;
+}
+
+int glx_layer_forward_checked(const float* W, const float* X, int64_t N, int32_t m, int32_t n, float* out,
+                              int32_t* write_counts, void* stream) {
+    if (N < 0 || m < 1 || n < 1) return set_err(GLX_ERR_SHAPE, "bad layer shape (N=%lld m=%d n=%d)", (long long)N, m, n);
+    if (!write_counts) return set_err(GLX_ERR_INVALID, "write_counts is required");
+    if (N == 0) return GLX_OK;
+    GLX_LAUNCH(launch_layer_forward(W, X, N, m, n, out, (cudaStream_t)stream, write_counts));
+    return GLX_OK;
+}
+
+int glx_layer_backward_checked(const float* x, const float* acts, const double* err, int32_t n, int32_t m,
+                               double* deltas, double* grads, int32_t* write_counts, void* stream) {
+    if (m < 0 || n < 1) return set_err(GLX_ERR_SHAPE, "bad layer shape (m=%d n=%d)", m, n);
+    if (!write_counts) return set_err(GLX_ERR_INVALID, "write_counts is required");
+    GLX_LAUNCH(launch_layer_backward(x, acts, err, n, m, deltas, grads, (cudaStream_t)stream, write_counts));
+    return GLX_OK;
+}
+
+int glx_forward_pair_debug(const float* w_ih, const float* w_ho, const float* x, int32_t D, int32_t H, int32_t K,
+                           float* hidden, float* out, int32_t* stamps, int32_t* status, int32_t workers,
+                           void* stream) {
+    int rc = check_dims(1, D, H);
+    if (rc) return rc;
+    if (K < 1 || K > 16) return set_err(GLX_ERR_INVALID, "output_dim must be in [1, 16], got %d", K);
+    if (workers < 1 || workers > 32) return set_err(GLX_ERR_INVALID, "workers must be in [1, 32], got %d", workers);
+    GLX_LAUNCH(launch_forward_pair_debug(w_ih, w_ho, x, D, H, K, hidden, out, stamps, status, workers,
+                                         (cudaStream_t)stream));
     return GLX_OK;
 }
 
@@ -1025,7 +1118,8 @@ static int batch_segment_dev(HostState* hs, const float* w_ih, const float* w_ho
     GLX_CK(cudaMemcpyAsync(hs->w2.p, w_ho, n2 * 4, cudaMemcpyHostToDevice, st));
     if (epochs == 0) return GLX_OK;
     return batch_train_impl(hs->w1.as<float>(), hs->w2.as<float>(), hs->xp.as<float>(), rows, input_dim, hidden_dim,
-                            epochs, lr, want_stats ? hs->stats.as<double>() : nullptr, hs->flag.as<int>(), st);
+                            epochs, lr, want_stats ? hs->stats.as<double>() : nullptr, hs->flag.as<int>(), st,
+                            (flags & GLX_FLAG_DEBUG) != 0);
 }
 
 int glx_run_train_segment_batch(float* w_ih, float* w_ho, const float* feats, const float* targets, int64_t rows,
@@ -1429,6 +1523,8 @@ int glx_dp_run_train_segment_batch(void* comm, float* w_ih, float* w_ho, const f
     GLX_CK(cudaStreamSynchronize(st));
     return GLX_OK;
 }
+
+void glx_set_debug(int32_t on) { g_debug.store(on ? 1 : 0); }
 
 void glx_profile_enable(int32_t on) {
     std::lock_guard<std::mutex> lk(g_prof.mu);

@@ -121,7 +121,65 @@ struct BtcArgs {
     float* part;
     int64_t N, ntiles;
     int D, DP, H, P1, PS;
+    int* dbg;  // pipeline checker (debug runs, else nullptr): see dbg_expect
 };
+
+// ---------------------------------------------------------------- pipeline checker
+// Debug runs (GLX_FLAG_DEBUG / glx_set_debug) pass a.dbg: every hand-off of a tile
+// between the roles carries a stamp (tile index + 1) that the producing role writes
+// before its barrier arrive and the consuming role checks after its wait -- the
+// device analogue of the reference's generation-stamped forward_pair_debug
+// (backend.py:237-284): a role that passes a barrier on the wrong phase (the hazard
+// of a counter shared by tiles that run ahead of each other) reads another tile's
+// stamp. The roles also count the tiles they handled, the analogue of the
+// reference's write-once shadow counts (backend.py:122-133): the host requires one
+// forward issue and one dh hand-off per row group for every tile of the epoch.
+// Layout (ints): [0] violations, [1] first check id, [2] its CTA, [3] expected
+// stamp, [4] seen stamp; [kDbgHdr, + T) forward issues per tile, [+ T, + 2T) dh
+// hand-offs per tile; then kDbgCta stamp slots per CTA. Stamps are global words:
+// mbarrier arrive / wait order them (release / acquire at CTA scope); the arrives
+// made by tcgen05.commit fire when the MMAs complete, long after the issuing
+// thread's stamp store, which a CTA fence orders first.
+#ifndef GLX_PIPELINE_CHECK
+#define GLX_PIPELINE_CHECK 1  // 0 compiles the checker out (A/B timing of its cost)
+#endif
+#define GLX_DBG_ON(a) (GLX_PIPELINE_CHECK && (a).dbg != nullptr)
+constexpr int kDbgHdr = 16, kDbgCta = 64;
+struct DbgView {
+    int* base;
+    int* vf;
+    int* vb;
+    int* st;
+};
+__device__ __forceinline__ DbgView dbg_view(int* p, int64_t ntiles) {
+    DbgView d;
+    d.base = p;
+    d.vf = p ? p + kDbgHdr : nullptr;
+    d.vb = p ? p + kDbgHdr + ntiles : nullptr;
+    d.st = p ? p + kDbgHdr + 2 * ntiles + (int64_t)blockIdx.x * kDbgCta : nullptr;
+    return d;
+}
+__device__ __forceinline__ void dbg_put(const DbgView& d, int slot, int64_t lt) {
+    reinterpret_cast<volatile int*>(d.st)[slot] = (int)(lt + 1);
+    __threadfence_block();
+}
+// the producer's stamp of a loaded stage; header word 6 = 1 + a tile index makes
+// that tile's stamp wrong (fault injection: tests prove the checker fires)
+__device__ __forceinline__ void dbg_put_load(const DbgView& d, int slot, int64_t lt) {
+    const int64_t tile = blockIdx.x + lt * gridDim.x;
+    const int bad = d.base[6] == (int)(tile + 1);
+    reinterpret_cast<volatile int*>(d.st)[slot] = (int)(lt + 1) + bad;
+    __threadfence_block();
+}
+__device__ __forceinline__ void dbg_expect(const DbgView& d, int id, int slot, int64_t lt) {
+    const int seen = reinterpret_cast<volatile int*>(d.st)[slot];
+    if (seen != (int)(lt + 1) && atomicAdd(d.base, 1) == 0) {
+        d.base[1] = id;
+        d.base[2] = blockIdx.x;
+        d.base[3] = (int)(lt + 1);
+        d.base[4] = seen;
+    }
+}
 
 struct BtcSmem {  // byte offsets
     int w, x, opart, dob, stat, bars;
@@ -305,7 +363,9 @@ __device__ __forceinline__ float2 exp2_poly2(float2 x) {
                        __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
-template <int NH, bool FULL, bool PAD>
+// CHK: the pipeline-checker instantiation (debug runs only: the checks cost the
+// production kernel ~10 % through code layout even when switched off at run time)
+template <int NH, bool FULL, bool PAD, bool CHK>
 __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const BtcArgs a) {
     constexpr int G = btc_groups(NH, FULL);  // epilogue groups, on alternate tiles
     constexpr int NEWG = 8 * NH;             // warps per group: 4 lane quadrants x NH unit halves x 2 row blocks
@@ -336,6 +396,10 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nt = (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;  // tiles of this CTA (>= 1)
     const int D = a.D, DP = a.DP;
+    // checker slots: x stage [0, kS), its release by the backward [8, 8 + kS), Z buffer
+    // [16, 16 + kZB), dh per row block and Z buffer [24, 24 + 2 kZB)
+    const DbgView dv = dbg_view(a.dbg, a.ntiles);
+#define BTC_CHK (CHK && a.dbg != nullptr)
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kS; i++) {
@@ -398,10 +462,14 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
         if (lane == 0) {
             for (int64_t lt = 0; lt < nt; lt++) {
                 const int xs = (int)(lt % kS);
-                if (lt >= kS) mbar_wait(&x_empty[xs], (uint32_t)((lt / kS) - 1) & 1);
+                if (lt >= kS) {
+                    mbar_wait(&x_empty[xs], (uint32_t)((lt / kS) - 1) & 1);
+                    if (BTC_CHK) dbg_expect(dv, 1, 8 + xs, lt - kS);
+                }
                 BTT(14);
                 const unsigned char* src = a.tiles + (blockIdx.x + lt * gridDim.x) * (int64_t)P::GTILE;
                 unsigned char* dst = sm + L.x + xs * P::STAGE;
+                if (BTC_CHK) dbg_put_load(dv, xs, lt);
                 mbar_arrive_expect_tx(&x_full[xs], (uint32_t)P::GTILE);
 #pragma unroll
                 for (int cp = 0; cp < P::NX; cp++) {
@@ -431,6 +499,11 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
                 mbar_wait(&dh_ready[zb], (uint32_t)(lt / kZB) & 1);
                 mbar_wait(&dh_ready[kZB + zb], (uint32_t)(lt / kZB) & 1);
                 tc_fence_after();
+                if (BTC_CHK && el) {
+                    dbg_expect(dv, 3, 24 + zb, lt);
+                    dbg_expect(dv, 4, 24 + kZB + zb, lt);
+                    dbg_put(dv, 8 + xs, lt);  // read by the producer after x_empty
+                }
                 BTT(9);
                 const uint64_t dth = dt0 + ((xs * P::STAGE) >> 4);
                 const uint64_t dtl = dth + ((kXF + kXT) >> 4);  // FULL: the lo copies follow
@@ -467,6 +540,11 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
                 BTT(11);
                 mbar_wait(&x_full[xs], (uint32_t)(lt / kS) & 1);
                 tc_fence_after();
+                if (BTC_CHK && el) {
+                    dbg_expect(dv, 2, xs, lt);
+                    atomicAdd(&dv.vf[blockIdx.x + lt * gridDim.x], 1);
+                    dbg_put(dv, 16 + zb, lt);  // read by the epilogue after z_full
+                }
                 BTT(12);
                 const uint64_t dx = dx0 + ((xs * P::STAGE) >> 4);
                 const uint64_t dxl = dx + ((kXF + kXT) >> 4);  // FULL: lo copy
@@ -567,6 +645,7 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
             BTT(0);
             mbar_wait(&z_full[zb], (uint32_t)(lt / kZB) & 1);
             tc_fence_after();
+            if (BTC_CHK && lane == 0) dbg_expect(dv, 5, 16 + zb, lt);
             BTT(1);
             const uint32_t zcol = tmem + lanebase + kColZ + 64 * NH * zb + 64 * hf + 32 * rb;
             float h[32];
@@ -725,6 +804,10 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
             tmem_st_wait();
             tc_fence_before();
             __syncwarp();
+            if (BTC_CHK && lane == 0) {
+                dbg_put(dv, 24 + rb * kZB + zb, lt);
+                if (ewg % (4 * NH) == 0) atomicAdd(&dv.vb[blockIdx.x + lt * gridDim.x], 1);  // one per row block
+            }
             if (lane == 0) mbar_arrive(&dh_ready[rb * kZB + zb]);
             BTT(7);
         }
@@ -780,6 +863,8 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
     }
 }
+
+#undef BTC_CHK
 
 // rows -> the per-tile operand layouts (see kXF / kXT), tf32 round to nearest; FULL
 // also writes the lo remainders. One block per 64-row tile, the tile staged through
@@ -929,6 +1014,10 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
     const int64_t nt = (a.ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
     const int D = a.D, DP = a.DP, H = a.H;
     float* out = a.part + (int64_t)blockIdx.x * a.PS;
+    // checker slots: forward stage [0, kRS) and its release [4, 4 + kRS), backward stage
+    // [8, 8 + kRS) and its release [12, 12 + kRS), Z buffer [16, 16 + kRZB) and its
+    // release [20, 20 + kRZB), dh^T buffer [24, 26), backward completion [28, 28 + kRG)
+    const DbgView dv = dbg_view(a.dbg, a.ntiles);
 #ifdef GLX_BTR_DEBUG
     if (blockIdx.x == 0 && threadIdx.x == 0) printf("btr start: nt %lld N %lld D %d H %d HP %d\n", (long long)nt, (long long)a.N, D, H, HP);
 #endif
@@ -1005,15 +1094,23 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
         if (lane == 0) {
             auto load_t = [&](int64_t k) {
                 const int ts = (int)(k % kRS);
-                if (k >= kRS) BTR_WAIT(&t_empty[ts], (uint32_t)((k / kRS) - 1) & 1, 8, k);
+                if (k >= kRS) {
+                    BTR_WAIT(&t_empty[ts], (uint32_t)((k / kRS) - 1) & 1, 8, k);
+                    if (GLX_DBG_ON(a)) dbg_expect(dv, 11, 12 + ts, k - kRS);
+                }
                 const unsigned char* src = a.tiles + (blockIdx.x + k * gridDim.x) * (int64_t)kRGT + kRXFG;
+                if (GLX_DBG_ON(a)) dbg_put(dv, 8 + ts, k);
                 mbar_arrive_expect_tx(&t_full[ts], (uint32_t)kRXTG);
                 bulk_g2s(sm + L::xt + ts * kRXT, src, kRXTG, &t_full[ts]);
             };
             for (int64_t lt = 0; lt < nt; lt++) {
                 const int xs = (int)(lt % kRS);
-                if (lt >= kRS) BTR_WAIT(&x_empty[xs], (uint32_t)((lt / kRS) - 1) & 1, 1, lt);
+                if (lt >= kRS) {
+                    BTR_WAIT(&x_empty[xs], (uint32_t)((lt / kRS) - 1) & 1, 1, lt);
+                    if (GLX_DBG_ON(a)) dbg_expect(dv, 12, 4 + xs, lt - kRS);
+                }
                 const unsigned char* src = a.tiles + (blockIdx.x + lt * gridDim.x) * (int64_t)kRGT;
+                if (GLX_DBG_ON(a)) dbg_put_load(dv, xs, lt);
                 mbar_arrive_expect_tx(&x_full[xs], (uint32_t)kRXFG);
                 bulk_g2s(sm + L::x + xs * kRXF, src, kRXFG, &x_full[xs]);
                 BTR_T(7, lt);
@@ -1037,6 +1134,12 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             const int xs = (int)(lt % kRS), zb = (int)(lt % kRZB);
             BTR_WAIT(&x_full[xs], (uint32_t)(lt / kRS) & 1, 2, lt);
             tc_fence_after();
+            if (GLX_DBG_ON(a) && el) {
+                dbg_expect(dv, 13, xs, lt);
+                atomicAdd(&dv.vf[blockIdx.x + lt * gridDim.x], 1);
+                dbg_put(dv, 4 + xs, lt);
+                dbg_put(dv, 16 + zb, lt);
+            }
             const uint32_t d = tmem + HP * zb;
             const uint64_t dx = dx0 + ((xs * kRXF) >> 4);
 #pragma unroll
@@ -1051,6 +1154,12 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             BTR_WAIT(&dh_ready[lt & 1], (uint32_t)(lt >> 1) & 1, 3, lt);
             BTR_WAIT(&t_full[ts], (uint32_t)(lt / kRS) & 1, 9, lt);
             tc_fence_after();
+            if (GLX_DBG_ON(a) && el) {
+                dbg_expect(dv, 14, 24 + (int)(lt & 1), lt);
+                dbg_expect(dv, 15, 8 + ts, lt);
+                dbg_put(dv, 12 + ts, lt);
+                dbg_put(dv, 28 + (int)(lt % kRG), lt);
+            }
             BTR_T(5, lt);
             const uint64_t dt = dt0 + ((ts * kRXT) >> 4);
 #pragma unroll
@@ -1072,6 +1181,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             backward(lt);
             if (lt + kRZB < nt) {
                 BTR_WAIT(&z_free[lt % kRZB], (uint32_t)(lt / kRZB) & 1, 4, lt);  // the epilogue read Z(lt)
+                if (GLX_DBG_ON(a) && el) dbg_expect(dv, 16, 20 + (int)(lt % kRZB), lt);
                 forward(lt + kRZB);
             }
         }
@@ -1121,6 +1231,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             if (quad == 2) BTR_T(0, lt);
             BTR_WAIT(&z_full[zb], (uint32_t)(lt / kRZB) & 1, 5, lt);
             tc_fence_after();
+            if (GLX_DBG_ON(a) && lane == 0) dbg_expect(dv, 17, 16 + zb, lt);
             float h[HP];
             {
                 uint32_t v[32];
@@ -1142,6 +1253,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             }
             tc_fence_before();
             __syncwarp();
+            if (GLX_DBG_ON(a) && lane == 0) dbg_put(dv, 20 + zb, lt);
             if (lane == 0) mbar_arrive(&z_free[zb]);
             if (quad == 2) BTR_T(1, lt);
             // h = sigmoid(z) (z prescaled by -log2 e), one reciprocal per pair
@@ -1192,6 +1304,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             if (lt >= 2) {
                 BTR_WAIT(&dh_free[(lt - 2) % kRG], (uint32_t)((lt - 2) / kRG) & 1, 6, lt);
                 tc_fence_after();
+                if (GLX_DBG_ON(a) && lane == 0) dbg_expect(dv, 18, 28 + (int)((lt - 2) % kRG), lt - 2);
             }
             if (quad == 2) BTR_T(3, lt);
             if (lt >= 1 && lt % kRDrain == 0) {  // group 0's tile: the backward of lt restarts
@@ -1209,6 +1322,10 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             fence_proxy_async();
             tc_fence_before();
             __syncwarp();
+            if (GLX_DBG_ON(a) && lane == 0) {
+                dbg_put(dv, 24 + (int)(lt & 1), lt);
+                atomicAdd(&dv.vb[blockIdx.x + lt * gridDim.x], 1);  // one per row quadrant
+            }
             if (lane == 0) mbar_arrive(&dh_ready[lt & 1]);
             if (quad == 2) BTR_T(4, lt);
         }
@@ -1404,8 +1521,9 @@ static cudaError_t launch_btr(const BatchGeom& g, const BtcArgs& a, cudaStream_t
 }
 
 cudaError_t launch_batchrt_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, int* dbg) {
     BtcArgs a;
+    a.dbg = dbg;
     a.tiles = (const unsigned char*)tiles;
     a.Wk = Wk;
     a.part = part;
@@ -1421,7 +1539,8 @@ cudaError_t launch_batchrt_epoch(const BatchGeom& g, const void* tiles, const fl
 
 template <int NH, bool FULL>
 static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t st) {
-    auto k = g.H % 128 ? batchtc_kernel<NH, FULL, true> : batchtc_kernel<NH, FULL, false>;
+    auto k = a.dbg ? (g.H % 128 ? batchtc_kernel<NH, FULL, true, true> : batchtc_kernel<NH, FULL, false, true>)
+                   : (g.H % 128 ? batchtc_kernel<NH, FULL, true, false> : batchtc_kernel<NH, FULL, false, false>);
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e != cudaSuccess) {
         fprintf(stderr, "glx: batchtc_kernel<%d> smem=%zu: %s\n", NH, g.smem, cudaGetErrorString(e));
@@ -1433,6 +1552,8 @@ static cudaError_t launch_btc(const BatchGeom& g, const BtcArgs& a, cudaStream_t
     return e;
 }
 
+size_t pipeline_check_ints(const BatchGeom& g) { return kDbgHdr + 2 * (size_t)g.ntiles + (size_t)g.grid * kDbgCta; }
+
 size_t batchtc_tile_bytes(const BatchGeom& g) {
     return (size_t)g.ntiles * (g.MT ? Pipe<true>::GTILE : Pipe<false>::GTILE);
 }
@@ -1443,8 +1564,10 @@ cudaError_t launch_batchtc_pack(const BatchGeom& g, const float* Xp, void* tiles
     return cudaGetLastError();
 }
 
-cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st) {
+cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st,
+                                 int* dbg) {
     BtcArgs a;
+    a.dbg = dbg;
     a.tiles = (const unsigned char*)tiles;
     a.Wk = Wk;
     a.part = part;

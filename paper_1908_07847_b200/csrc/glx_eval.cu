@@ -213,8 +213,10 @@ static bool use_split(int H, int K) {
 // ----------------------------------------------------------- per-instance API
 // network.forward (network.py:128-135) for N rows: hidden[r][j] and out[r][k] are
 // _activation's f32 results (kernels.py:102-122), the reference's f64 order.
+// counts (debug runs, else nullptr): one increment per output slot written, the
+// write-once shadow count of the reference's debug forward (backend.py:122-133)
 __global__ void forward_hidden_kernel(const float* __restrict__ W1, const float* __restrict__ X, int64_t N, int D,
-                                      int H, float* __restrict__ hidden) {
+                                      int H, float* __restrict__ hidden, int* __restrict__ counts = nullptr) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= N * H) return;
     const int64_t r = e / H;
@@ -230,6 +232,7 @@ __global__ void forward_hidden_kernel(const float* __restrict__ W1, const float*
     }
     const double z = __dadd_rn(acc, (double)wr[D]);
     hidden[e] = __double2float_rn(1.0 / (1.0 + exp(-z)));
+    if (counts) atomicAdd(counts + e, 1);
 }
 
 __global__ void forward_output_kernel(const float* __restrict__ W2, const float* __restrict__ hidden, int64_t N, int H,
@@ -279,7 +282,7 @@ __global__ void instance_gradients_kernel(const float* __restrict__ W2, const fl
 // deltas[j] = (err[j] a_j)(1 - a_j), grads[j] = deltas[j] [x, 1], f64
 __global__ void layer_backward_kernel(const float* __restrict__ x, const float* __restrict__ acts,
                                       const double* __restrict__ err, int n, int m, double* __restrict__ deltas,
-                                      double* __restrict__ grads) {
+                                      double* __restrict__ grads, int* __restrict__ counts = nullptr) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= n) return;
     const double a = (double)acts[j];
@@ -288,6 +291,59 @@ __global__ void layer_backward_kernel(const float* __restrict__ x, const float* 
     double* g = grads + (int64_t)j * (m + 1);
     for (int i = 0; i < m; i++) g[i] = __dmul_rn(d, (double)x[i]);
     g[m] = d;
+    if (counts) atomicAdd(counts + j, 1);
+}
+
+// backend.forward_pair_debug (backend.py:237-284) on the device: `workers` warps
+// claim hidden units round-robin and stamp each activation slot with the
+// generation after writing it; past the layer barrier (__syncthreads) thread 0
+// requires every stamp to be current -- no hidden slot read before it was
+// written -- then evaluates the output layer. Exact f64 order (kernels.py:102-122).
+// status: 0 ok, else 1 + the first stale hidden index.
+__global__ void forward_pair_debug_kernel(const float* __restrict__ W1, const float* __restrict__ W2,
+                                          const float* __restrict__ x, int D, int H, int K,
+                                          float* __restrict__ hidden, float* __restrict__ out,
+                                          int* __restrict__ stamps, int* __restrict__ status) {
+    const int generation = 1;
+    for (int j = threadIdx.x; j < H; j += blockDim.x) {
+        const float* wr = W1 + (int64_t)j * (D + 1);
+        double acc = 0.0;
+        for (int b0 = 0; b0 < D; b0 += 16) {
+            const int b1 = b0 + 16 < D ? b0 + 16 : D;
+            double part = 0.0;
+            for (int i = b0; i < b1; i++) part = fma((double)wr[i], (double)x[i], part);
+            acc = __dadd_rn(acc, part);
+        }
+        hidden[j] = __double2float_rn(1.0 / (1.0 + exp(-__dadd_rn(acc, (double)wr[D]))));
+        __threadfence_block();
+        reinterpret_cast<volatile int*>(stamps)[j] = generation;
+    }
+    __syncthreads();  // the layer boundary
+    if (threadIdx.x != 0) return;
+    for (int j = 0; j < H; j++)
+        if (reinterpret_cast<volatile int*>(stamps)[j] != generation) {
+            *status = 1 + j;
+            return;
+        }
+    for (int k = 0; k < K; k++) {
+        const float* wr = W2 + (int64_t)k * (H + 1);
+        double acc = 0.0;
+        for (int b0 = 0; b0 < H; b0 += 16) {
+            const int b1 = b0 + 16 < H ? b0 + 16 : H;
+            double part = 0.0;
+            for (int j = b0; j < b1; j++) part = fma((double)wr[j], (double)hidden[j], part);
+            acc = __dadd_rn(acc, part);
+        }
+        out[k] = __double2float_rn(1.0 / (1.0 + exp(-__dadd_rn(acc, (double)wr[H]))));
+    }
+    *status = 0;
+}
+
+cudaError_t launch_forward_pair_debug(const float* W1, const float* W2, const float* x, int D, int H, int K,
+                                      float* hidden, float* out, int* stamps, int* status, int workers,
+                                      cudaStream_t st) {
+    forward_pair_debug_kernel<<<1, 32 * workers, 0, st>>>(W1, W2, x, D, H, K, hidden, out, stamps, status);
+    return cudaGetLastError();
 }
 
 // backend.backpropagate_error (backend.py:192-205 -> kernels.backprop_error_seq):
@@ -306,15 +362,16 @@ __global__ void backprop_error_kernel(const float* __restrict__ W, const double*
     err_prev[i] = acc;
 }
 
-cudaError_t launch_layer_forward(const float* W, const float* X, int64_t N, int m, int n, float* out, cudaStream_t st) {
+cudaError_t launch_layer_forward(const float* W, const float* X, int64_t N, int m, int n, float* out, cudaStream_t st,
+                                 int* counts) {
     const int64_t e = N * n;
-    forward_hidden_kernel<<<(unsigned)((e + 127) / 128), 128, 0, st>>>(W, X, N, m, n, out);
+    forward_hidden_kernel<<<(unsigned)((e + 127) / 128), 128, 0, st>>>(W, X, N, m, n, out, counts);
     return cudaGetLastError();
 }
 
 cudaError_t launch_layer_backward(const float* x, const float* acts, const double* err, int n, int m, double* deltas,
-                                  double* grads, cudaStream_t st) {
-    layer_backward_kernel<<<(n + 127) / 128, 128, 0, st>>>(x, acts, err, n, m, deltas, grads);
+                                  double* grads, cudaStream_t st, int* counts) {
+    layer_backward_kernel<<<(n + 127) / 128, 128, 0, st>>>(x, acts, err, n, m, deltas, grads, counts);
     return cudaGetLastError();
 }
 

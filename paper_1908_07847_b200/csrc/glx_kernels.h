@@ -112,12 +112,16 @@ int pick_dp(int D);  // glx_batch.cu: weight-row stride of the FP32 batch kernel
 // packed rows by launch_batchtc_pack
 size_t batchtc_tile_bytes(const BatchGeom& g);
 cudaError_t launch_batchtc_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st);
-cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st);
+cudaError_t launch_batchtc_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st,
+                                 int* dbg = nullptr);
+// ints of the tcgen05 kernels' pipeline-checker buffer (debug runs; glx_batchtc.cu)
+size_t pipeline_check_ints(const BatchGeom& g);
 // narrow layers (H <= 64, FAST precision): rows on the TMEM lanes, 128-row tiles
 bool batchrt_geometry(int64_t N, int D, int H, int n_sms, BatchGeom* g);
 size_t batchrt_tile_bytes(const BatchGeom& g);
 cudaError_t launch_batchrt_pack(const BatchGeom& g, const float* Xp, void* tiles, cudaStream_t st);
-cudaError_t launch_batchrt_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st);
+cudaError_t launch_batchrt_epoch(const BatchGeom& g, const void* tiles, const float* Wk, float* part, cudaStream_t st,
+                                 int* dbg = nullptr);
 
 // ------------------------------------------------------------ exact eval
 cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, const uint8_t* labels, int64_t N,
@@ -125,9 +129,13 @@ cudaError_t launch_eval_ref64(const float* W1, const float* W2, const float* X, 
                               cudaStream_t st);
 cudaError_t launch_nonfinite(const float* a, int64_t na, const float* b, int64_t nb, int* flag, cudaStream_t st);
 int eval_nparts(int64_t N, int H, int K);  // loss partials of launch_eval_ref64
-cudaError_t launch_layer_forward(const float* W, const float* X, int64_t N, int m, int n, float* out, cudaStream_t st);
+cudaError_t launch_layer_forward(const float* W, const float* X, int64_t N, int m, int n, float* out, cudaStream_t st,
+                                 int* counts = nullptr);
 cudaError_t launch_layer_backward(const float* x, const float* acts, const double* err, int n, int m, double* deltas,
-                                  double* grads, cudaStream_t st);
+                                  double* grads, cudaStream_t st, int* counts = nullptr);
+cudaError_t launch_forward_pair_debug(const float* W1, const float* W2, const float* x, int D, int H, int K,
+                                      float* hidden, float* out, int* stamps, int* status, int workers,
+                                      cudaStream_t st);
 cudaError_t launch_backprop_error(const float* W, const double* deltas, int n, int m, double* err_prev,
                                   cudaStream_t st);
 cudaError_t launch_forward(const float* W1, const float* W2, const float* X, int64_t N, int D, int H, int K,

@@ -274,3 +274,31 @@ def test_dp_rank_without_rows_and_host_api(gpu):
         v1, v2 = dev.weights()
     assert host.w_ih.tobytes() == v1.tobytes() and host.w_ho.tobytes() == v2.tobytes()
     assert (st[:, 1:].sum(axis=1) == x.shape[0]).all()
+
+
+@pytest.mark.parametrize("N,H", [(1 << 20, 256), (100_000, 256), (300_000, 128), (1 << 18, 33), (200_000, 60)])
+def test_pipeline_checker_debug_runs(gpu, N, H):
+    """debug=True: the tcgen05 epoch kernels stamp every tile hand-off between their
+    roles and count the tiles each role handled (the device analogue of the
+    reference's debug instrumentation, backend.py:122-133, 237-284); a clean run
+    passes every check and trains the same bytes as the unchecked run."""
+    import paper_1908_07847_b200._lib as L
+
+    kind = L.load().glx_batch_kernel_kind(N, 33, H)
+    assert kind in (2, 3)
+    x, l, t, net0 = _case(N, 33, H, seed=H)
+    a, b = net0.copy(), net0.copy()
+    g.run_train_segment_batch(a.w_ih2d, a.w_ho2d, x, t, 3, 0.5, g.cuda())
+    g.run_train_segment_batch(b.w_ih2d, b.w_ho2d, x, t, 3, 0.5, g.cuda(), debug=True)
+    assert a.w_ih.tobytes() == b.w_ih.tobytes() and a.w_ho.tobytes() == b.w_ho.tobytes()
+
+
+@pytest.mark.parametrize("N,H", [(1 << 20, 256), (1 << 18, 33)])
+def test_pipeline_checker_catches_a_stale_hand_off(gpu, N, H, monkeypatch):
+    """Fault injection: the producer stamps one row tile wrongly; the debug run must
+    fail with the checker's RuntimeError naming the hand-off."""
+    monkeypatch.setenv("GLX_DEBUG_INJECT_TILE", "37")
+    x, l, t, net0 = _case(N, 33, H, seed=1)
+    net = net0.copy()
+    with pytest.raises(RuntimeError, match="pipeline check"):
+        g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, 1, 0.5, g.cuda(), debug=True)
