@@ -2,11 +2,12 @@
 
     python tools/build_variants.py NAME="-DKNOB=1 ..." ...
 
-Only glx_batchtc.cu is recompiled per variant; the other objects come from build/
-(run the normal build first). Time a variant with
+Only one source is recompiled per variant (glx_batchtc.cu, or GLX_VARIANT_SRC);
+the other objects come from build/ (run the normal build first). Time a variant with
 GLX_LIB=variants/lib_NAME.so python tools/batch_epoch_time.py.
 """
 import concurrent.futures as cf
+import os
 import subprocess
 import sys
 from pathlib import Path
@@ -21,11 +22,14 @@ out.mkdir(exist_ok=True)
 B.build()
 
 
+SRC = os.environ.get("GLX_VARIANT_SRC", "glx_batchtc.cu")
+
+
 def one(name, flags):
-    obj = out / f"{name}_glx_batchtc.o"
-    cmd = [B.nvcc(), *B.ARCH, *B.FLAGS, *flags.split(), "-c", str(B.CSRC / "glx_batchtc.cu"), "-o", str(obj)]
+    obj = out / f"{name}_{Path(SRC).stem}.o"
+    cmd = [B.nvcc(), *B.ARCH, *B.FLAGS, *flags.split(), "-c", str(B.CSRC / SRC), "-o", str(obj)]
     subprocess.run(cmd, check=True, capture_output=True)
-    objs = [str(obj) if src == "glx_batchtc.cu" else str(B.BUILD / (Path(src).stem + ".o")) for src in B.SOURCES]
+    objs = [str(obj) if src == SRC else str(B.BUILD / (Path(src).stem + ".o")) for src in B.SOURCES]
     subprocess.run([B.nvcc(), *B.ARCH, "-shared", "-o", str(out / f"lib_{name}.so"), *objs, *B.LINK], check=True)
     return name
 
