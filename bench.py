@@ -583,6 +583,38 @@ def run_dry(args):
         dist.destroy_process_group()
 
 
+def run_scaling(args) -> None:
+    """`--scaling 1,2,4,8`: the headline at each GPU count, each a separate
+    `bench.py --gpus N` run (its own ranks), and one JSON line of scaling rows
+    (n_gpus, value, ms_per_step, speedup over the first N, efficiency) -- the
+    report-side 1/2/4/8 rows of SURVEY.md 8(f)3. The driver's SCALE run computes
+    its own efficiency from the per-N lines; this is the builder-side table."""
+    rows = []
+    for n in [int(v) for v in args.scaling.split(",") if v]:
+        cmd = [sys.executable, str(Path(__file__).resolve()), "--gpus", str(n), "--steps", str(args.steps),
+               "--warmup", str(args.warmup), "--workload", args.workload, "--no-secondary"]
+        env = dict(os.environ)
+        for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK"):
+            env.pop(k, None)
+        out = subprocess.run(cmd, capture_output=True, text=True, env=env)
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        if out.returncode != 0 or not lines:
+            rows.append({"n_gpus": n, "failed": True, "error": (out.stderr or out.stdout)[-400:]})
+            continue
+        rec = json.loads(lines[-1])
+        rows.append({"n_gpus": rec.get("n_gpus", n), "value": rec.get("value"), "ms_per_step": rec.get("ms_per_step"),
+                     "e2e": (rec.get("e2e") or {}).get("value"), "scaling": rec.get("scaling")})
+    base = next((r for r in rows if r.get("value")), None)
+    for r in rows:
+        if base and r.get("value"):
+            r["speedup"] = r["value"] / base["value"]
+            r["efficiency"] = r["speedup"] * base["n_gpus"] / r["n_gpus"]
+    line = {"metric": METRIC, "unit": "sample-epochs/s", "workload": args.workload, "scaling_rows": rows}
+    if args.out:
+        Path(args.out).write_text(json.dumps(line, indent=1))
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -594,12 +626,16 @@ def main():
                     help="skip the other configurations measured after the headline (N = 1)")
     ap.add_argument("--suite", default=None,
                     help="secondary configurations instead of the headline, e.g. 1,3,4,5,eval,norm")
-    ap.add_argument("--out", default=None, help="with --suite: write the results JSON here")
+    ap.add_argument("--out", default=None, help="with --suite / --scaling: write the results JSON here")
+    ap.add_argument("--scaling", default=None, help="GPU counts, e.g. 1,2,4,8: one headline run per count and "
+                    "a table of scaling rows")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     if args.suite:
         run_suite(args.suite, args.out)
+    elif args.scaling:
+        run_scaling(args)
     elif args.impl == "reference":
         run_reference(args)
     elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:

@@ -129,3 +129,21 @@ def test_batch_mode_device_cells(gpu):
                                 epochs_grid=(5,), repetitions=2, backends=(g.cuda(),), baselines=(), mode="batch"))
     (c,) = rep.cells
     assert c.backend == "cuda-fp32" and not c.failed and c.sample_epochs_per_s > 0
+
+
+@pytest.mark.gpu
+def test_bench_front_end_artifacts(gpu, tmp_path):
+    """The reference's `glycemlp bench` command (cli.py:147-155, 266-288) as
+    `python -m paper_1908_07847_b200.bench_report`: same arguments, same artifacts."""
+    import csv
+
+    rc = B.bench_main(["--rows", "300", "--columns", "33", "--hidden-dim", "16", "--epochs-grid", "2,4",
+                       "--repetitions", "1", "--workers", "2", "--device", "--out", str(tmp_path)])
+    assert rc == 0
+    doc = json.loads((tmp_path / "bench_report.json").read_text())
+    assert doc["format"] == "glycemlp-bench-report-v1"
+    assert {c["backend"] for c in doc["cells"]} == {"sequential", "parallel", "cuda-fp32"}
+    assert [s["epochs"] for s in doc["speedups"]] == [2, 4]
+    rows = list(csv.reader((tmp_path / "speedup.csv").open()))
+    assert rows[0] == list(B.SPEEDUP_HEADER) and len(rows) == 3
+    assert (tmp_path / "device_speedup.csv").exists()

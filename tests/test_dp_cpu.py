@@ -292,3 +292,25 @@ def test_bench_spawns_ranks_itself():
     rec = json.loads(lines[0])
     assert rec["n_gpus"] == 2 and rec["max_rank"] == 1.0
     assert rec["config"]["parallelism"] == "dp2" and rec["config"]["rows_per_gpu"] * 2 == rec["config"]["global_rows"]
+
+
+def test_bench_scaling_rows():
+    """`python bench.py --scaling 1,2` runs the headline once per GPU count (each its
+    own ranks) and prints one line of scaling rows (GLX_BENCH_DRYRUN=1: plumbing only)."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    env = dict(os.environ, GLX_BENCH_DRYRUN="1")
+    env.pop("WORLD_SIZE", None)
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--scaling", "1,2", "--steps", "4", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    rec = json.loads(lines[0])
+    assert [r["n_gpus"] for r in rec["scaling_rows"]] == [1, 2]
+    assert not any(r.get("failed") for r in rec["scaling_rows"]), rec
