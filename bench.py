@@ -398,6 +398,8 @@ def run_gpu(args):
     # end-to-end through the public API, this rank's rows in pinned host memory
     e2e = run_e2e(g, dp, comm, host_x.numpy(), host_t.numpy(), rows, barrier, max_over_ranks)
     e2e["gpu_launches"] = None
+    # config 3 sharded the way it scales: every rank its LPT share of the 4096 networks
+    sweep = run_sweep_sharded(L, rank, world, barrier, max_over_ranks)
 
     if rank == 0:
         cpu = None
@@ -414,7 +416,7 @@ def run_gpu(args):
                 "scaling": "strong", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
                 "config": config_dict(args.workload, world), "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary(), "final_loss_sum": final_loss,
-                "secondary_configs": secondary,
+                "secondary_configs": secondary, "sweep_sharded": sweep,
                 "path": "glx_train_batch (fused single-GPU loop)" if comm is None else
                         "glx_dp_train_batch (epoch kernel, f64 gradient, library-owned ncclAllReduce, update; "
                         "CUDA graph replay)"}
@@ -440,14 +442,8 @@ def secondary_configs(L, fp32_peak):
     import bench_configs as bc
 
     out = {}
-    for name, fn in (("config1", lambda: bc.config1(L, fp32_peak)), ("config3", lambda: bc.config3(L, fp32_peak)),
-                     ("config5_bf16", lambda: bc.config5(L, fp32_peak))):
-        try:
-            out[name] = fn()
-        except Exception as e:  # reported, never fatal to the headline line
-            out[name] = {"error": f"{type(e).__name__}: {e}"}
-        torch.cuda.empty_cache()
-    # config 2 at the reference default width (33 -> 33 -> 1, 1M rows): the FP32 two-role kernel
+    # config 2 at the reference default width (33 -> 33 -> 1, 1M rows; the rows-on-lanes
+    # tcgen05 kernel), first: after config 5's BF16 GEMMs the power cap lowers the clocks
     rows, h33 = 1_000_000, 33
     X, lab = g.synthetic_arrays_device(rows, D, 0, "planted-linear")
     Xp = torch.empty((rows, int(L.glx_packed_ld(D))), device="cuda")
@@ -468,7 +464,64 @@ def secondary_configs(L, fp32_peak):
                           "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
                           "kernel_kind": int(L.glx_batch_kernel_kind(rows, D, h33)),
                           "frac_fp32_peak": rows * f_train(D, h33) / (ms * 1e-3) / 1e12 / fp32_peak}
+    del X, lab, Xp, w1, w2
+    torch.cuda.empty_cache()
+    for name, fn in (("config1", lambda: bc.config1(L, fp32_peak)), ("config3", lambda: bc.config3(L, fp32_peak)),
+                     ("config5_bf16", lambda: bc.config5(L, fp32_peak))):
+        try:
+            out[name] = fn()
+        except Exception as e:  # reported, never fatal to the headline line
+            out[name] = {"error": f"{type(e).__name__}: {e}"}
+        torch.cuda.empty_cache()
     return out
+
+
+def run_sweep_sharded(L, rank, world, barrier, max_over_ranks, epochs=200, reps=3):
+    """Config 3 at this GPU count: 4096 networks 33 -> {8..512} -> 1 (64 widths x 64 seeds)
+    on the paper's 90-row split, online fp32; the networks are LPT-sharded over the ranks
+    by cost (sweep.lpt_shards, no communication), every rank trains its share with
+    glx_train_sweep, time = max over ranks of the median device time; value = all
+    networks' sample-epochs / that time."""
+    import torch
+
+    import paper_1908_07847_b200 as g
+    from paper_1908_07847_b200 import _lib
+    from paper_1908_07847_b200.sweep import lpt_shards, pack_pool
+
+    sys.path.insert(0, str(ROOT / "tests"))
+    from conftest import load_case
+
+    c = load_case("paper_33_33_1")
+    x, t = c["train_x"], c["train_y"].astype(np.float32)
+    N, Dx = x.shape
+    hs, ss = g.sweep_grid(range(8, 513, 8), range(64))
+    spec = g.SweepSpec(input_dim=Dx, hidden_dims=hs, seeds=ss, epochs=epochs)
+    mine = lpt_shards(spec.costs(), world)[rank]
+    nets = [g.init_weights(g.NetworkConfig(input_dim=Dx, hidden_dim=hs[i], seed=ss[i])) for i in mine]
+    pool, Hs, off = pack_pool(nets)
+    wp = torch.from_numpy(pool).cuda()
+    X = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    T = torch.from_numpy(t).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    run = lambda: _lib.check(L.glx_train_sweep(len(nets), _lib.ptr(Hs), _lib.ptr(off), wp.data_ptr(), X.data_ptr(),
+                                               T.data_ptr(), N, Dx, epochs, 0.1, _lib.NUMERICS["fp32"], st))
+    run()
+    times = []
+    for _ in range(reps):
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        run()
+        e1.record()
+        torch.cuda.synchronize()
+        times.append(max_over_ranks(e0.elapsed_time(e1)))
+    ms = statistics.median(times)
+    flops = sum(f_train(Dx, h) for h in hs) * N * epochs
+    return {"config": "3: sweep 4096 nets 33->{8..512}->1, 90 rows, online fp32, LPT-sharded over the GPUs",
+            "n_gpus": world, "epochs": epochs, "ms": ms, "nets_this_rank": len(nets),
+            "net_sample_epochs_per_s": len(hs) * N * epochs / (ms * 1e-3),
+            "tflops": flops / (ms * 1e-3) / 1e12, "scaling": "strong",
+            "timing": "CUDA events per rank, max over ranks, median of 3"}
 
 
 def run_e2e(g, dp, comm, x, t, rows_total, barrier, max_over_ranks, reps=3):
@@ -602,13 +655,18 @@ def run_scaling(args) -> None:
             rows.append({"n_gpus": n, "failed": True, "error": (out.stderr or out.stdout)[-400:]})
             continue
         rec = json.loads(lines[-1])
+        sw = rec.get("sweep_sharded") or {}
         rows.append({"n_gpus": rec.get("n_gpus", n), "value": rec.get("value"), "ms_per_step": rec.get("ms_per_step"),
-                     "e2e": (rec.get("e2e") or {}).get("value"), "scaling": rec.get("scaling")})
+                     "e2e": (rec.get("e2e") or {}).get("value"), "scaling": rec.get("scaling"),
+                     "sweep_net_sample_epochs_per_s": sw.get("net_sample_epochs_per_s")})
     base = next((r for r in rows if r.get("value")), None)
+    sbase = next((r for r in rows if r.get("sweep_net_sample_epochs_per_s")), None)
     for r in rows:
         if base and r.get("value"):
             r["speedup"] = r["value"] / base["value"]
             r["efficiency"] = r["speedup"] * base["n_gpus"] / r["n_gpus"]
+        if sbase and r.get("sweep_net_sample_epochs_per_s"):
+            r["sweep_speedup"] = r["sweep_net_sample_epochs_per_s"] / sbase["sweep_net_sample_epochs_per_s"]
     line = {"metric": METRIC, "unit": "sample-epochs/s", "workload": args.workload, "scaling_rows": rows}
     if args.out:
         Path(args.out).write_text(json.dumps(line, indent=1))
