@@ -64,19 +64,25 @@ def _case(N, H, seed):
 
 
 @pytest.mark.timeout(900)
-def test_headline_1M_rows_20_epochs_vs_oracle(gpu):
+@pytest.mark.parametrize("H,kind", [(256, 2), (128, 2), (33, 3)])
+def test_headline_1M_rows_20_epochs_vs_oracle(gpu, H, kind):
     """The bench workload (config 2, 1M x 33-256-1) through the product API for 20
-    epochs: weights within 1e-5 of the f64 oracle, classes identical up to the
-    bounded near-threshold rows, per-epoch confusion counts consistent."""
+    epochs -- and the same at H = 128 (the two-group tcgen05 kernel) and at the
+    reference's default H = 33 (the rows-on-lanes kernel): weights within 1e-5 of
+    the f64 oracle, classes identical up to the bounded near-threshold rows,
+    per-epoch confusion counts consistent."""
+    import paper_1908_07847_b200._lib as L
+
     epochs, lr = 20, 0.1
-    x, l, t, net0 = _case(1_000_000, 256, seed=0)
+    assert L.load().glx_batch_kernel_kind(1_000_000, 33, H) == kind
+    x, l, t, net0 = _case(1_000_000, H, seed=0)
     net = net0.copy()
     stats = np.zeros((epochs, 5))
     g.run_train_segment_batch(net.w_ih2d, net.w_ho2d, x, t, epochs, lr, g.cuda(), stats)
     ref = net0.copy()
     O.train_batch_par(ref.w_ih2d, ref.w_ho2d, x, t, epochs, lr)
     err = max(rel_err(net.w_ih, ref.w_ih), rel_err(net.w_ho, ref.w_ho))
-    print(f"1M x 33-256-1, {epochs} epochs: max rel weight err {err:.3e}")
+    print(f"1M x 33-{H}-1, {epochs} epochs: max rel weight err {err:.3e}")
     assert err <= 1e-5
     assert (stats[:, 1:].sum(axis=1) == x.shape[0]).all()
     nflip, bound, acc, acc_ref = _class_agreement(net, ref, x, l)
