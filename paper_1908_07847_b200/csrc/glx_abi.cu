@@ -1322,7 +1322,7 @@ int glx_wide_grad(const float* w_ih, const float* w_ho, const void* Xb, const vo
     GLX_CK(ws->wide.ensure(wide_work_bytes(C, splits)));
     GLX_CK(wide_grad(w_ih, w_ho, Xb, XT, labels, N, ws->wide.as<unsigned char>(), C, splits, grad, st,
                      [](bool) {}));
-    g_launches.fetch_add(3 + 5 * (uint64_t)((N + C - 1) / C));
+    g_launches.fetch_add(3 + wide_launches_per_chunk() * (uint64_t)((N + C - 1) / C));
     return GLX_OK;
 }
 
@@ -1417,7 +1417,7 @@ int glx_wide_train(float* w_ih, float* w_ho, const void* Xb, const void* XT, con
         GLX_CK(wide_epoch(w_ih, w_ho, Xb, XT, labels, N, lr, ws->wide.as<unsigned char>(), C, splits, stats,
                           nonfinite, st, prof));
         GLX_CK(perr);
-        g_launches.fetch_add(4 + 5 * (uint64_t)((N + C - 1) / C));
+        g_launches.fetch_add(4 + wide_launches_per_chunk() * (uint64_t)((N + C - 1) / C));
     }
     return GLX_OK;
 }

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 
@@ -987,6 +988,351 @@ __global__ void h_bias_cols_kernel(__nv_bfloat16* __restrict__ H, int64_t C) {
     H[r * kWHL + kWH + c] = __float2bfloat16_rn(c == 0 ? 1.f : 0.f);
 }
 
+// ------------------------------------------------ wide tail: GEMMs 2, 3, 5 fused
+// One persistent kernel per row chunk takes the chain that follows the hidden
+// layer, so H is read from HBM once (GEMMs 2, 3 and 5 read it three times) and
+// delta_o never leaves the SM. Per 128-row tile:
+//   A  D_o[128 rows][16]  = H . W2b^T             (SS, M=128 N=16, K = 1024: 16 H k-blocks)
+//   B  epilogue: o = sigmoid(D_o + b2), delta_o, loss, argmax, sum delta_o (the
+//      dW2 bias row); delta_o -> shared memory as the A operand of C and the B
+//      operand of E (bf16, no-swizzle core-matrix layouts)
+//   C  D_h[128 rows][64 units] = delta_o . W2^T    (SS, M=128 N=64 K=16), per 64-unit chunk
+//   E  dW2^T[128 units][16] += H^T . delta_o       (SS, A = the H k-block pair read MN-major,
+//      M=128 units N=16 K=128 rows), accumulated in TMEM over the CTA's tiles
+//   D  epilogue: dH = D_h * h (1 - h) with h from the k-block still in shared memory,
+//      written over h in place (same 128-byte swizzle) and TMA-stored row-major
+// The H k-blocks of a tile are streamed twice through an 8-stage ring: pass 1
+// (from HBM) for A, pass 2 (L2-hot, the tile was just read) for C/D/E, so a
+// tile's 256 KB of H never has to stay resident. TMEM: D_o [0,16), dW2^T
+// [32,160) (8 unit blocks x 16 outputs), D_h 4 x 64 columns at 256.
+constexpr int kTlS = 8;                 // ring stages (one H k-block of 128 rows x 64 units each)
+constexpr int kTlKB = kWH / 64;         // 16 k-blocks per pass
+constexpr int kTlSlabs = 160;           // per-CTA dW2 partial slabs (>= the SM count)
+constexpr uint32_t kTlStage = 128 * 128;
+constexpr uint32_t kTlRing = kTlS * kTlStage;
+constexpr uint32_t kTlW2b = kTlKB * 16 * 128;  // W2 rows 0..15, 16 k-blocks of 2 KB (128-byte swizzle)
+constexpr uint32_t kTlW2t = kWH * 16 * 2;      // W2^T [1024 units][16], no-swizzle core matrices
+constexpr uint32_t kTlDo = 128 * 16 * 2;       // delta_o tile, one layout
+constexpr size_t kTlSmem = 1024 + kTlRing + kTlW2b + kTlW2t + 2 * kTlDo + 512;
+
+// UMMA descriptor, no swizzle: core matrices of 8 rows x 16 B; LBO = K-direction
+// stride, SBO = M/N-direction stride
+__device__ __forceinline__ uint64_t umma_desc_ns(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
+}
+
+__device__ __forceinline__ void tmem_ld16_async(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+// W2^T as the C operand image: element (u, k) at (k/8) 16384 + (u/8) 128 + (u%8) 16 + (k%8) 2 bytes
+__global__ void wide_tail_w2t_kernel(const float* __restrict__ W2, __nv_bfloat16* __restrict__ img) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= kWH * 16) return;
+    const int u = e >> 4, k = e & 15;
+    img[((k >> 3) * 16384 + (u >> 3) * 128 + (u & 7) * 16 + (k & 7) * 2) / 2] =
+        __float2bfloat16_rn(W2[k * (kWH + 1) + u]);
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_constant__ CUtensorMap map_h,
+                                                                    const __grid_constant__ CUtensorMap map_w2,
+                                                                    const __grid_constant__ CUtensorMap map_dh,
+                                                                    const __nv_bfloat16* __restrict__ w2t_img,
+                                                                    const float* __restrict__ b2,
+                                                                    const uint8_t* __restrict__ labels, int M,
+                                                                    float* __restrict__ slabs,
+                                                                    double* __restrict__ stats) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* ring = sm;
+    unsigned char* w2b = ring + kTlRing;
+    unsigned char* w2t = w2b + kTlW2b;
+    unsigned char* doa = w2t + kTlW2t;  // delta_o [128 rows][K = 16]: (k/8) 2048 + (r/8) 128 + (r%8) 16 + (k%8) 2
+    unsigned char* dot = doa + kTlDo;   // delta_o^T [16][K = 128 rows]: (r/8) 256 + (k/8) 128 + (k%8) 16 + (r%8) 2
+    uint64_t* full = reinterpret_cast<uint64_t*>(dot + kTlDo);
+    uint64_t* empty = full + kTlS;      // pass 1: 4 MMA commits; pass 2: one arrival per row quadrant (store read)
+    uint64_t* ofull = empty + kTlS;     // D_o written
+    uint64_t* ofree = ofull + 1;        // D_o read (4 warps)
+    uint64_t* doready = ofree + 1;      // delta_o in shared memory (4 warps)
+    uint64_t* dhfull = doready + 1;     // [4] D_h buffer written (and every earlier MMA done)
+    uint64_t* dhfree = dhfull + 4;      // [4] D_h buffer read (8 warps)
+    uint64_t* wbar = dhfree + 4;        // constant operands loaded
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+    float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4 quadrants][16] bias-row partials
+
+    constexpr uint32_t kColO = 0, kColW2 = 32, kColDH = 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = (M + 127) / 128;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kTlS; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 4);
+        }
+        mbar_init(ofull, 1);
+        mbar_init(ofree, 4);
+        mbar_init(doready, 4);
+        for (int b = 0; b < 4; b++) {
+            mbar_init(&dhfull[b], 1);
+            mbar_init(&dhfree[b], 8);
+        }
+        mbar_init(wbar, 1);
+        fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_h) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(&map_dh) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(512)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer: constants, then per tile pass 1 and pass 2 (16 k-blocks each)
+            mbar_arrive_expect_tx(wbar, kTlW2b + kTlW2t);
+            for (int kb = 0; kb < kTlKB; kb++) tma_load_2d(w2b + kb * 2048, &map_w2, kb * 64, 0, wbar);
+            bulk_g2s(w2t, w2t_img, kTlW2t, wbar);
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                for (int j = 0; j < 2 * kTlKB; j++, it++) {
+                    const int s = it % kTlS;
+                    if (it >= kTlS) mbar_wait(&empty[s], ((it / kTlS) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], kTlStage);
+                    tma_load_2d(ring + s * kTlStage, &map_h, (j % kTlKB) * 64, t * 128, &full[s]);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            mbar_wait(wbar, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t idO = umma_idesc_bf16(128, 16);
+            const uint32_t idC = umma_idesc_bf16(128, 64);
+            const uint32_t idE = umma_idesc_bf16(128, 16) | (1u << 15);  // A (H^T) MN-major
+            const uint32_t ring_a = smem_u32(ring), w2b_a = smem_u32(w2b), w2t_a = smem_u32(w2t);
+            const uint32_t doa_a = smem_u32(doa), dot_a = smem_u32(dot);
+            int it = 0, ct = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                if (lt > 0) {
+                    mbar_wait(ofree, (lt - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                for (int kb = 0; kb < kTlKB; kb++, it++) {  // A: output layer
+                    const int s = it % kTlS;
+                    mbar_wait(&full[s], (it / kTlS) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        umma_bf16(tmem + kColO, umma_desc_sw128(ring_a + s * kTlStage + kk * 32),
+                                  umma_desc_sw128(w2b_a + kb * 2048 + kk * 32), idO, (kb | kk) != 0);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) umma_commit(&empty[s]);
+                }
+                umma_commit(ofull);
+                mbar_wait(doready, lt & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int p = 0; p < kTlKB / 2; p++, it += 2) {
+                    const int s0 = it % kTlS;  // even: the pair (s0, s0 + 1) is contiguous
+                    mbar_wait(&full[s0], (it / kTlS) & 1);
+                    mbar_wait(&full[s0 + 1], ((it + 1) / kTlS) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int kk = 0; kk < 8; kk++)  // E: dW2^T for units 128p .. 128p + 127
+                        umma_bf16(tmem + kColW2 + 16 * p, umma_desc_sw128_mn(ring_a + s0 * kTlStage + kk * 2048, kTlStage),
+                                  umma_desc_ns(dot_a + kk * 512, 256, 128), idE, (lt > 0 || kk > 0) ? 1u : 0u);
+#pragma unroll
+                    for (int c2 = 0; c2 < 2; c2++, ct++) {  // C: hidden-delta pre-activations, units 64c ..
+                        const int c = 2 * p + c2, b = ct & 3;
+                        if (ct >= 4) {
+                            mbar_wait(&dhfree[b], ((ct >> 2) - 1) & 1);
+                            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                        }
+                        umma_bf16(tmem + kColDH + 64 * b, umma_desc_ns(doa_a, 2048, 128),
+                                  umma_desc_ns(w2t_a + c * 1024, 16384, 128), idC, 0u);
+                        umma_commit(&dhfull[b]);
+                    }
+                }
+            }
+        }
+    } else {
+        // epilogue warps 2..9: TMEM lane quadrant = warp % 4 (rows 32 quad ..), column half hlf
+        const int ew = warp - 2, quad = warp & 3, hlf = ew >> 2;
+        const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
+        const int r = quad * 32 + lane;  // row within the tile
+        float bk[kWK];
+#pragma unroll
+        for (int k = 0; k < kWK; k++) bk[k] = b2[k];
+        float dbias[kWK];
+#pragma unroll
+        for (int k = 0; k < kWK; k++) dbias[k] = 0.f;
+        float loss = 0.f, correct = 0.f, valid = 0.f;
+        int ct = 0, lt = 0, pend = -1;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+            const int row = t * 128 + r;
+            if (hlf == 0) {  // B: output neuron per row (kernels.py:352-375 generalised to K outputs)
+                const int lab = row < M ? labels[row] : 0;
+                mbar_wait(ofull, lt & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                uint32_t ro[16];
+                tmem_ld16_async(tmem + lanebase + kColO, ro);
+                tmem_wait();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(ofree);
+                uint32_t pk[8];
+                if (row < M) {
+                    float best = -1.f;
+                    int arg = 0;
+                    float d[kWK];
+#pragma unroll
+                    for (int k = 0; k < kWK; k++) {
+                        const float o = 1.0f / (1.0f + __expf(-(__uint_as_float(ro[k]) + bk[k])));
+                        const float tk = (k == lab) ? 1.f : 0.f;
+                        d[k] = (o - tk) * o * (1.0f - o);
+                        loss = fmaf(0.5f * (tk - o), tk - o, loss);
+                        if (o > best) {
+                            best = o;
+                            arg = k;
+                        }
+                    }
+                    correct += arg == lab ? 1.f : 0.f;
+                    valid += 1.f;
+#pragma unroll
+                    for (int e = 0; e < 8; e++) pk[e] = pack_bf16x2(d[2 * e], d[2 * e + 1]);
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 8; e++) pk[e] = 0u;
+                }
+#pragma unroll
+                for (int e = 0; e < 8; e++) {  // the dW2 bias row sums the bf16 delta_o the MMAs use
+                    dbias[2 * e] += __uint_as_float(pk[e] << 16);
+                    dbias[2 * e + 1] += __uint_as_float(pk[e] & 0xFFFF0000u);
+                }
+                *reinterpret_cast<uint4*>(doa + (r >> 3) * 128 + (r & 7) * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+                *reinterpret_cast<uint4*>(doa + 2048 + (r >> 3) * 128 + (r & 7) * 16) =
+                    make_uint4(pk[4], pk[5], pk[6], pk[7]);
+                uint16_t* dt = reinterpret_cast<uint16_t*>(dot + (r >> 3) * 256 + (r & 7) * 2);
+#pragma unroll
+                for (int k = 0; k < kWK; k++)
+                    dt[((k >> 3) * 128 + (k & 7) * 16) / 2] = (uint16_t)((k & 1) ? (pk[k >> 1] >> 16) : (pk[k >> 1] & 0xFFFFu));
+                fence_proxy_async();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(doready);
+            }
+            // D: dH = D_h * h (1 - h), 16 chunks of 64 units; this warp takes 32 of them
+            for (int c = 0; c < kTlKB; c++, ct++) {
+                const int b = ct & 3;
+                mbar_wait(&dhfull[b], (ct >> 2) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                uint32_t v[32];
+                tmem_ld32_async(tmem + lanebase + kColDH + 64 * b + 32 * hlf, v);
+                tmem_wait();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&dhfree[b]);
+                const int it = lt * 2 * kTlKB + kTlKB + c, s = it % kTlS;
+                mbar_wait(&full[s], (it / kTlS) & 1);  // complete already (the MMAs read it)
+                unsigned char* rowp = ring + s * kTlStage + r * 128;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    uint4* p16 = reinterpret_cast<uint4*>(rowp + (((4 * hlf + q) ^ (r & 7)) << 4));
+                    uint4 hv = *p16;
+                    uint32_t* hw = reinterpret_cast<uint32_t*>(&hv);
+#pragma unroll
+                    for (int e = 0; e < 4; e++) {
+                        const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[e]));
+                        hw[e] = pack_bf16x2(__uint_as_float(v[8 * q + 2 * e]) * hf.x * (1.f - hf.x),
+                                            __uint_as_float(v[8 * q + 2 * e + 1]) * hf.y * (1.f - hf.y));
+                    }
+                    *p16 = hv;
+                }
+                fence_proxy_async();
+                bar_sync(1 + quad, 64);  // both column halves of these 32 rows are written
+                if (hlf == 0 && lane == 0) {
+                    tma_store_2d(&map_dh, ring + s * kTlStage + quad * 32 * 128, c * 64, t * 128 + quad * 32);
+                    // a stage is released once its store has read it, one chunk late; the
+                    // tile's last stage at once (the producer refills it with pass 1 of the
+                    // next tile, which this warp's next store depends on)
+                    if (c + 1 < kTlKB) {
+                        asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        if (pend >= 0) mbar_arrive(&empty[pend]);
+                        pend = s;
+                    } else {
+                        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                        if (pend >= 0) mbar_arrive(&empty[pend]);
+                        mbar_arrive(&empty[s]);
+                        pend = -1;
+                    }
+                }
+            }
+        }
+        if (hlf == 0 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        // dW2^T partials (TMEM lanes = units) into this CTA's slab: units 128p + 32 quad + lane
+        float* slab = slabs + (int64_t)blockIdx.x * kWMi * 32;
+        for (int p = 4 * hlf; p < 4 * hlf + 4; p++) {
+            uint32_t w[16];
+            tmem_ld16_async(tmem + lanebase + kColW2 + 16 * p, w);
+            tmem_wait();
+            float4* dst = reinterpret_cast<float4*>(slab + (int64_t)(128 * p + r) * 32);
+#pragma unroll
+            for (int q = 0; q < 4; q++) {
+                float4 a = dst[q];
+                a.x += __uint_as_float(w[4 * q]);
+                a.y += __uint_as_float(w[4 * q + 1]);
+                a.z += __uint_as_float(w[4 * q + 2]);
+                a.w += __uint_as_float(w[4 * q + 3]);
+                dst[q] = a;
+            }
+        }
+        if (hlf == 0) {  // bias row (unit 1024) and the statistics
+#pragma unroll
+            for (int k = 0; k < kWK; k++)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) dbias[k] += __shfl_xor_sync(0xffffffffu, dbias[k], o);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                loss += __shfl_xor_sync(0xffffffffu, loss, o);
+                correct += __shfl_xor_sync(0xffffffffu, correct, o);
+                valid += __shfl_xor_sync(0xffffffffu, valid, o);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int k = 0; k < kWK; k++) red[quad * kWK + k] = dbias[k];
+                if (stats) {
+                    atomicAdd(stats + 0, (double)loss);
+                    atomicAdd(stats + 1, (double)correct);
+                    atomicAdd(stats + 2, (double)(valid - correct));
+                }
+            }
+            bar_sync(5, 128);
+            if (quad == 0 && lane < kWK)
+                slab[kWH * 32 + lane] += red[lane] + red[kWK + lane] + red[2 * kWK + lane] + red[3 * kWK + lane];
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+    }
+}
+
 struct WideWork {
     void* W1b;
     float* b1;
@@ -997,6 +1343,7 @@ struct WideWork {
     void* dob;  // [C][64] bf16
     void* doT;  // delta_o^T, K-blocked [C/64][32][64] bf16, rows >= 16 zero
     void* dht;  // dH, row-major [C][1024] bf16 (read MN-major by the dW1 GEMM)
+    void* w2tl; // W2^T in the tail kernel's operand layout (32 KB)
     float* dW1T;
     float* dW2T;
     double* grad;  // [kWP + 3]: gradient sums, then loss, correct, wrong
@@ -1021,8 +1368,9 @@ static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
     t.dob = take((size_t)C * 64 * 2);
     t.doT = take((size_t)32 * C * 2);
     t.dht = take((size_t)kWH * C * 2);
+    t.w2tl = take(kTlW2t);
     t.dW1T = (float*)take((size_t)splits * kWMi * kWH * 4);
-    t.dW2T = (float*)take((size_t)kWSplits2 * kWMi * 32 * 4);
+    t.dW2T = (float*)take((size_t)std::max(kWSplits2, kTlSlabs) * kWMi * 32 * 4);
     t.grad = (double*)take((size_t)(kWP + 3) * 8);
     t.C = C;
     t.splits = splits;
@@ -1031,6 +1379,36 @@ static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
 }
 
 size_t wide_work_bytes(int64_t C, int splits) { return carve(nullptr, nullptr, C, splits); }
+
+// GLX_WIDE_TAIL=0 selects the unfused GEMMs 2, 3, 5 (A/B measurements)
+bool wide_tail_enabled() {
+    const char* v = getenv("GLX_WIDE_TAIL");
+    return !(v && v[0] == '0');
+}
+
+static int sm_count() {
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+// the fused tail over the Cc rows of a chunk: dH -> dht, dW2^T partials -> slabs[blockIdx],
+// stats += loss, correct, wrong
+static cudaError_t launch_wide_tail(const WideWork& w, int Cc, const uint8_t* labels, double* stats, cudaStream_t st) {
+    CUtensorMap mh, mw, md;
+    if (!make_map_bf16(&mh, w.Hb, Cc, kWH, kWHL, 128) || !make_map_bf16(&mw, w.W2b, 32, kWH, kWH, 16) ||
+        !make_map_bf16(&md, w.dht, Cc, kWH, kWH, 32, 64, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(wide_tail_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTlSmem);
+    if (e != cudaSuccess) return e;
+    const int ntiles = (Cc + 127) / 128;
+    const int grid = std::min(std::min(sm_count(), kTlSlabs), ntiles);
+    wide_tail_kernel<<<grid, kTcThreads, kTlSmem, st>>>(mh, mw, md, (const __nv_bfloat16*)w.w2tl, w.b2, labels, Cc,
+                                                        w.dW2T, stats);
+    return cudaGetLastError();
+}
+
+int wide_launches_per_chunk() { return wide_tail_enabled() ? 3 : 5; }
 
 // one epoch; stats (device, may be null): [loss, correct, wrong] accumulated
 // gradient SUM over the N rows at the current weights -> grad[0, kWP) (f64),
@@ -1051,7 +1429,13 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
     const int64_t zstride = (int64_t)kWMi * kWH;
     if ((e = cudaMemsetAsync(w.dW1T, 0, (size_t)splits * zstride * 4, st)) != cudaSuccess) return e;
     const int64_t zstride2 = (int64_t)kWMi * 32;
-    if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)kWSplits2 * zstride2 * 4, st)) != cudaSuccess) return e;
+    const bool tail = wide_tail_enabled();
+    const int slabs2 = tail ? kTlSlabs : kWSplits2;
+    if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)slabs2 * zstride2 * 4, st)) != cudaSuccess) return e;
+    if (tail) {
+        wide_tail_w2t_kernel<<<kWH * 16 / 256, 256, 0, st>>>(W2, (__nv_bfloat16*)w.w2tl);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 64 * 2, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.doT, 0, (size_t)32 * C * 2, st)) != cudaSuccess) return e;
     h_bias_cols_kernel<<<(unsigned)((C * (kWHL - kWH) + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.Hb, C);
@@ -1069,7 +1453,10 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             ep.ldd = kWHL;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 2. output layer -> delta_o, loss, accuracy
+        if (tail) {  // 2, 3, 5 fused: delta_o, loss, accuracy, dH, dW2 partials
+            if ((e = launch_wide_tail(w, Cc, labels + r0, stats, st)) != cudaSuccess) return e;
+        }
+        if (!tail) {  // 2. output layer -> delta_o, loss, accuracy
             TcGemm g{w.Hb, w.W2b, Cc, 32, kWH, kWHL, kWH, 1};
             TcEpilogue ep{};
             ep.kind = 2;
@@ -1081,7 +1468,7 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             ep.stats = stats;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 3. hidden deltas, row-major
+        if (!tail) {  // 3. hidden deltas, row-major
             TcGemm g{w.dob, w.W2T, Cc, kWH, 64, 64, 64, 1};
             TcEpilogue ep{};
             ep.kind = 3;
@@ -1101,7 +1488,7 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
             ep.zstride = zstride;
             if ((e = launch_tc(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32 with delta_o^T rows >= 16 zero); A = H read
+        if (!tail) {  // 5. dW2^T += [H,1]^T delta_o (split-K; N = 32 with delta_o^T rows >= 16 zero); A = H read
            //    MN-major (rows = K), the bias column supplies the "1" input
             TcGemm g{w.Hb, w.doT, kWH + 1, 32, Cc, kWHL, 0, kWSplits2, 0, 32, 1};
             TcEpilogue ep{};
@@ -1113,8 +1500,7 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
         }
         prof(false);
     }
-    wide_reduce_kernel<<<(kWP + 255) / 256, 256, 0, st>>>(w.dW1T, splits, zstride, w.dW2T, kWSplits2, zstride2,
-                                                         grad);
+    wide_reduce_kernel<<<(kWP + 255) / 256, 256, 0, st>>>(w.dW1T, splits, zstride, w.dW2T, slabs2, zstride2, grad);
     return cudaGetLastError();
 }
 
