@@ -992,28 +992,43 @@ __global__ void h_bias_cols_kernel(__nv_bfloat16* __restrict__ H, int64_t C) {
 // One persistent kernel per row chunk takes the chain that follows the hidden
 // layer, so H is read from HBM once (GEMMs 2, 3 and 5 read it three times) and
 // delta_o never leaves the SM. Per 128-row tile:
-//   A  D_o[128 rows][16]  = H . W2b^T             (SS, M=128 N=16, K = 1024: 16 H k-blocks)
+//   A  D_o[128 rows][16]  = H . W2^T              (SS, M=128 N=16, K = 1024: 16 H k-blocks)
 //   B  epilogue: o = sigmoid(D_o + b2), delta_o, loss, argmax, sum delta_o (the
 //      dW2 bias row); delta_o -> shared memory as the A operand of C and the B
 //      operand of E (bf16, no-swizzle core-matrix layouts)
-//   C  D_h[128 rows][64 units] = delta_o . W2^T    (SS, M=128 N=64 K=16), per 64-unit chunk
+//   C  D_h[128 rows][64 units] = delta_o . W2      (SS, M=128 N=64 K=16, W2 read MN-major), per 64-unit chunk
 //   E  dW2^T[128 units][16] += H^T . delta_o       (SS, A = the H k-block pair read MN-major,
 //      M=128 units N=16 K=128 rows), accumulated in TMEM over the CTA's tiles
 //   D  epilogue: dH = D_h * h (1 - h) with h from the k-block still in shared memory,
 //      written over h in place (same 128-byte swizzle) and TMA-stored row-major
-// The H k-blocks of a tile are streamed twice through an 8-stage ring: pass 1
-// (from HBM) for A, pass 2 (L2-hot, the tile was just read) for C/D/E, so a
-// tile's 256 KB of H never has to stay resident. TMEM: D_o [0,16), dW2^T
-// [32,160) (8 unit blocks x 16 outputs), D_h 4 x 64 columns at 256.
-constexpr int kTlS = 8;                 // ring stages (one H k-block of 128 rows x 64 units each)
+// The H k-blocks of a tile are streamed twice: pass 1 (from HBM) through ring 1
+// for A, pass 2 (L2-hot: the tile was just read) through ring 2 for C/D/E, so a
+// tile's 256 KB of H never has to stay resident. Each ring has its own producer
+// thread and A and C/E their own MMA-issuing threads (tcgen05 operations of
+// different threads touch disjoint TMEM columns and shared memory here), so the
+// next tile's output layer streams in from HBM while this tile's deltas are
+// written. TMEM: D_o [0,16), dW2^T [32,160) (8 unit blocks x 16 outputs), D_h
+// 4 x 64 columns at 256.
+#ifndef GLX_TL_S1
+#define GLX_TL_S1 3
+#endif
+#ifndef GLX_TL_S2
+#define GLX_TL_S2 8
+#endif
+#ifndef GLX_TL_GATE
+#define GLX_TL_GATE 1  // pass 2 of a tile waits for its pass 1 (L2 reuse)
+#endif
+constexpr int kTlS1 = GLX_TL_S1;        // ring 1 stages (one H k-block of 128 rows x 64 units each)
+constexpr int kTlS2 = GLX_TL_S2;        // ring 2 stages (even: E reads contiguous stage pairs)
+static_assert(kTlS2 % 2 == 0, "ring 2 holds stage pairs");
 constexpr int kTlKB = kWH / 64;         // 16 k-blocks per pass
 constexpr int kTlSlabs = 160;           // per-CTA dW2 partial slabs (>= the SM count)
+constexpr int kTlThreads = 384;         // P1 producer, A issuer, 8 epilogue warps, P2 producer, C/E issuer
 constexpr uint32_t kTlStage = 128 * 128;
-constexpr uint32_t kTlRing = kTlS * kTlStage;
-constexpr uint32_t kTlW2b = kTlKB * 16 * 128;  // W2 rows 0..15, 16 k-blocks of 2 KB (128-byte swizzle)
-constexpr uint32_t kTlW2t = kWH * 16 * 2;      // W2^T [1024 units][16], no-swizzle core matrices
+constexpr uint32_t kTlW2b = kTlKB * 16 * 128;  // W2 rows 0..15 as 16 k-blocks of 2 KB (128-byte swizzle)
 constexpr uint32_t kTlDo = 128 * 16 * 2;       // delta_o tile, one layout
-constexpr size_t kTlSmem = 1024 + kTlRing + kTlW2b + kTlW2t + 2 * kTlDo + 512;
+constexpr size_t kTlSmem = 1024 + (kTlS1 + kTlS2) * kTlStage + kTlW2b + 2 * kTlDo + 512;
+static_assert(kTlSmem <= 232448, "wide tail shared memory");
 
 // UMMA descriptor, no swizzle: core matrices of 8 rows x 16 B; LBO = K-direction
 // stride, SBO = M/N-direction stride
@@ -1036,39 +1051,80 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-// W2^T as the C operand image: element (u, k) at (k/8) 16384 + (u/8) 128 + (u%8) 16 + (k%8) 2 bytes
-__global__ void wide_tail_w2t_kernel(const float* __restrict__ W2, __nv_bfloat16* __restrict__ img) {
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= kWH * 16) return;
-    const int u = e >> 4, k = e & 15;
-    img[((k >> 3) * 16384 + (u >> 3) * 128 + (u & 7) * 16 + (k & 7) * 2) / 2] =
-        __float2bfloat16_rn(W2[k * (kWH + 1) + u]);
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void sts16(uint32_t a, uint16_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(v) : "memory");
 }
 
-__global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_constant__ CUtensorMap map_h,
+// TMA with an L2 cache policy (createpolicy): pass 1 keeps its lines for pass 2
+// (evict_last), pass 2 and the dH stores let theirs go first
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ void tma_load_2d_hint(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar,
+                                                 uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, "
+        "%3}], [%4], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d_hint(const CUtensorMap* map, const void* src, int c0, int c1, uint64_t pol) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group.L2::cache_hint [%0, {%2, %3}], [%1], %4;" ::"l"(
+                     map),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "l"(pol)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+#ifndef GLX_TL_HINTS
+#define GLX_TL_HINTS 1
+#endif
+
+__global__ void __launch_bounds__(kTlThreads, 1) wide_tail_kernel(const __grid_constant__ CUtensorMap map_h,
                                                                     const __grid_constant__ CUtensorMap map_w2,
                                                                     const __grid_constant__ CUtensorMap map_dh,
-                                                                    const __nv_bfloat16* __restrict__ w2t_img,
                                                                     const float* __restrict__ b2,
                                                                     const uint8_t* __restrict__ labels, int M,
                                                                     float* __restrict__ slabs,
                                                                     double* __restrict__ stats) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
-    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    unsigned char* ring = sm;
-    unsigned char* w2b = ring + kTlRing;
-    unsigned char* w2t = w2b + kTlW2b;
-    unsigned char* doa = w2t + kTlW2t;  // delta_o [128 rows][K = 16]: (k/8) 2048 + (r/8) 128 + (r%8) 16 + (k%8) 2
+    // 1024-byte aligned base, kept as an offset into the shared array (shared-space accesses)
+    unsigned char* sm = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
+    unsigned char* ring1 = sm;
+    unsigned char* ring2 = ring1 + kTlS1 * kTlStage;
+    unsigned char* w2b = ring2 + kTlS2 * kTlStage;
+    unsigned char* doa = w2b + kTlW2b;  // delta_o [128 rows][K = 16]: (k/8) 2048 + (r/8) 128 + (r%8) 16 + (k%8) 2
     unsigned char* dot = doa + kTlDo;   // delta_o^T [16][K = 128 rows]: (r/8) 256 + (k/8) 128 + (k%8) 16 + (r%8) 2
-    uint64_t* full = reinterpret_cast<uint64_t*>(dot + kTlDo);
-    uint64_t* empty = full + kTlS;      // pass 1: 4 MMA commits; pass 2: one arrival per row quadrant (store read)
-    uint64_t* ofull = empty + kTlS;     // D_o written
+    uint64_t* full1 = reinterpret_cast<uint64_t*>(dot + kTlDo);
+    uint64_t* empty1 = full1 + kTlS1;   // A's MMAs read the stage
+    uint64_t* full2 = empty1 + kTlS1;
+    uint64_t* empty2 = full2 + kTlS2;   // one arrival per row quadrant (its dH store read the stage)
+    uint64_t* ofull = empty2 + kTlS2;   // D_o written
     uint64_t* ofree = ofull + 1;        // D_o read (4 warps)
     uint64_t* doready = ofree + 1;      // delta_o in shared memory (4 warps)
-    uint64_t* dhfull = doready + 1;     // [4] D_h buffer written (and every earlier MMA done)
+    uint64_t* dhfull = doready + 1;     // [4] D_h buffer written (and every earlier C/E MMA done)
     uint64_t* dhfree = dhfull + 4;      // [4] D_h buffer read (8 warps)
-    uint64_t* wbar = dhfree + 4;        // constant operands loaded
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+    uint64_t* wbar = dhfree + 4;        // W2 loaded
+    // pass 2 of a tile is issued only after its pass 1 landed (p1land), so it hits L2;
+    // p2got (the pass-2 producer saw p1land) keeps A at most one tile ahead of it
+    uint64_t* p1land = wbar + 1;
+    uint64_t* p2got = p1land + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p2got + 1);
     float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [4 quadrants][16] bias-row partials
 
     constexpr uint32_t kColO = 0, kColW2 = 32, kColDH = 256;
@@ -1076,9 +1132,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_c
     const int ntiles = (M + 127) / 128;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kTlS; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 4);
+        for (int s = 0; s < kTlS1; s++) {
+            mbar_init(&full1[s], 1);
+            mbar_init(&empty1[s], 1);
+        }
+        for (int s = 0; s < kTlS2; s++) {
+            mbar_init(&full2[s], 1);
+            mbar_init(&empty2[s], 4);
         }
         mbar_init(ofull, 1);
         mbar_init(ofree, 4);
@@ -1088,6 +1148,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_c
             mbar_init(&dhfree[b], 8);
         }
         mbar_init(wbar, 1);
+        mbar_init(p1land, 1);
+        mbar_init(p2got, 1);
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_h) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(&map_dh) : "memory");
@@ -1102,69 +1164,96 @@ __global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_c
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    const uint32_t w2b_a = smem_u32(w2b), doa_a = smem_u32(doa), dot_a = smem_u32(dot);
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer: constants, then per tile pass 1 and pass 2 (16 k-blocks each)
-            mbar_arrive_expect_tx(wbar, kTlW2b + kTlW2t);
+        if (lane == 0) {  // pass-1 producer (HBM): W2, then the tiles' k-blocks
+            const uint64_t pol = l2_policy_evict_last();
+            mbar_arrive_expect_tx(wbar, kTlW2b);
             for (int kb = 0; kb < kTlKB; kb++) tma_load_2d(w2b + kb * 2048, &map_w2, kb * 64, 0, wbar);
-            bulk_g2s(w2t, w2t_img, kTlW2t, wbar);
             int it = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                for (int j = 0; j < 2 * kTlKB; j++, it++) {
-                    const int s = it % kTlS;
-                    if (it >= kTlS) mbar_wait(&empty[s], ((it / kTlS) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], kTlStage);
-                    tma_load_2d(ring + s * kTlStage, &map_h, (j % kTlKB) * 64, t * 128, &full[s]);
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+                for (int kb = 0; kb < kTlKB; kb++, it++) {
+                    const int s = it % kTlS1;
+                    if (it >= kTlS1) mbar_wait(&empty1[s], ((it / kTlS1) - 1) & 1);
+                    mbar_arrive_expect_tx(&full1[s], kTlStage);
+                    if (GLX_TL_HINTS) tma_load_2d_hint(ring1 + s * kTlStage, &map_h, kb * 64, t * 128, &full1[s], pol);
+                    else tma_load_2d(ring1 + s * kTlStage, &map_h, kb * 64, t * 128, &full1[s]);
+                }
+        }
+    } else if (warp == 10) {
+        if (lane == 0) {  // pass-2 producer (L2)
+            const uint64_t pol = l2_policy_evict_first();
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                if (GLX_TL_GATE) {
+                    mbar_wait(p1land, lt & 1);
+                    mbar_arrive(p2got);
+                }
+                for (int kb = 0; kb < kTlKB; kb++, it++) {
+                    const int s = it % kTlS2;
+                    if (it >= kTlS2) mbar_wait(&empty2[s], ((it / kTlS2) - 1) & 1);
+                    mbar_arrive_expect_tx(&full2[s], kTlStage);
+                    if (GLX_TL_HINTS) tma_load_2d_hint(ring2 + s * kTlStage, &map_h, kb * 64, t * 128, &full2[s], pol);
+                    else tma_load_2d(ring2 + s * kTlStage, &map_h, kb * 64, t * 128, &full2[s]);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
+        if (lane == 0) {  // A issuer: the output layer of each tile
             mbar_wait(wbar, 0);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t idO = umma_idesc_bf16(128, 16);
-            const uint32_t idC = umma_idesc_bf16(128, 64);
-            const uint32_t idE = umma_idesc_bf16(128, 16) | (1u << 15);  // A (H^T) MN-major
-            const uint32_t ring_a = smem_u32(ring), w2b_a = smem_u32(w2b), w2t_a = smem_u32(w2t);
-            const uint32_t doa_a = smem_u32(doa), dot_a = smem_u32(dot);
-            int it = 0, ct = 0, lt = 0;
+            const uint32_t r1 = smem_u32(ring1);
+            int it = 0, lt = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
                 if (lt > 0) {
                     mbar_wait(ofree, (lt - 1) & 1);
+                    if (GLX_TL_GATE) mbar_wait(p2got, (lt - 1) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 }
-                for (int kb = 0; kb < kTlKB; kb++, it++) {  // A: output layer
-                    const int s = it % kTlS;
-                    mbar_wait(&full[s], (it / kTlS) & 1);
+                for (int kb = 0; kb < kTlKB; kb++, it++) {
+                    const int s = it % kTlS1;
+                    mbar_wait(&full1[s], (it / kTlS1) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                     for (int kk = 0; kk < 4; kk++)
-                        umma_bf16(tmem + kColO, umma_desc_sw128(ring_a + s * kTlStage + kk * 32),
+                        umma_bf16(tmem + kColO, umma_desc_sw128(r1 + s * kTlStage + kk * 32),
                                   umma_desc_sw128(w2b_a + kb * 2048 + kk * 32), idO, (kb | kk) != 0);
-#pragma unroll
-                    for (int q = 0; q < 4; q++) umma_commit(&empty[s]);
+                    umma_commit(&empty1[s]);
                 }
+                mbar_arrive(p1land);  // every pass-1 k-block of this tile has landed
                 umma_commit(ofull);
+            }
+        }
+    } else if (warp == 11) {
+        if (lane == 0) {  // C/E issuer: hidden-delta pre-activations and dW2 of each tile
+            mbar_wait(wbar, 0);
+            const uint32_t idC = umma_idesc_bf16(128, 64) | (1u << 16);  // B (W2, [k][units]) MN-major
+            const uint32_t idE = umma_idesc_bf16(128, 16) | (1u << 15);  // A (H^T) MN-major
+            const uint32_t r2 = smem_u32(ring2);
+            int it = 0, ct = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
                 mbar_wait(doready, lt & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 for (int p = 0; p < kTlKB / 2; p++, it += 2) {
-                    const int s0 = it % kTlS;  // even: the pair (s0, s0 + 1) is contiguous
-                    mbar_wait(&full[s0], (it / kTlS) & 1);
-                    mbar_wait(&full[s0 + 1], ((it + 1) / kTlS) & 1);
+                    const int s0 = it % kTlS2;  // even: the pair (s0, s0 + 1) is contiguous
+                    mbar_wait(&full2[s0], (it / kTlS2) & 1);
+                    mbar_wait(&full2[s0 + 1], ((it + 1) / kTlS2) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
                     for (int kk = 0; kk < 8; kk++)  // E: dW2^T for units 128p .. 128p + 127
-                        umma_bf16(tmem + kColW2 + 16 * p, umma_desc_sw128_mn(ring_a + s0 * kTlStage + kk * 2048, kTlStage),
+                        umma_bf16(tmem + kColW2 + 16 * p, umma_desc_sw128_mn(r2 + s0 * kTlStage + kk * 2048, kTlStage),
                                   umma_desc_ns(dot_a + kk * 512, 256, 128), idE, (lt > 0 || kk > 0) ? 1u : 0u);
 #pragma unroll
-                    for (int c2 = 0; c2 < 2; c2++, ct++) {  // C: hidden-delta pre-activations, units 64c ..
+                    for (int c2 = 0; c2 < 2; c2++, ct++) {  // C: units 64c .. 64c + 63
                         const int c = 2 * p + c2, b = ct & 3;
                         if (ct >= 4) {
                             mbar_wait(&dhfree[b], ((ct >> 2) - 1) & 1);
                             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                         }
                         umma_bf16(tmem + kColDH + 64 * b, umma_desc_ns(doa_a, 2048, 128),
-                                  umma_desc_ns(w2t_a + c * 1024, 16384, 128), idC, 0u);
+                                  umma_desc_sw128_mn(w2b_a + c * 2048, 2048), idC, 0u);
                         umma_commit(&dhfull[b]);
                     }
                 }
@@ -1175,6 +1264,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_c
         const int ew = warp - 2, quad = warp & 3, hlf = ew >> 2;
         const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
         const int r = quad * 32 + lane;  // row within the tile
+        const uint32_t r2 = smem_u32(ring2);
         float bk[kWK];
 #pragma unroll
         for (int k = 0; k < kWK; k++) bk[k] = b2[k];
@@ -1224,13 +1314,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_c
                     dbias[2 * e] += __uint_as_float(pk[e] << 16);
                     dbias[2 * e + 1] += __uint_as_float(pk[e] & 0xFFFF0000u);
                 }
-                *reinterpret_cast<uint4*>(doa + (r >> 3) * 128 + (r & 7) * 16) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-                *reinterpret_cast<uint4*>(doa + 2048 + (r >> 3) * 128 + (r & 7) * 16) =
-                    make_uint4(pk[4], pk[5], pk[6], pk[7]);
-                uint16_t* dt = reinterpret_cast<uint16_t*>(dot + (r >> 3) * 256 + (r & 7) * 2);
+                sts128(doa_a + (r >> 3) * 128 + (r & 7) * 16, make_uint4(pk[0], pk[1], pk[2], pk[3]));
+                sts128(doa_a + 2048 + (r >> 3) * 128 + (r & 7) * 16, make_uint4(pk[4], pk[5], pk[6], pk[7]));
+                const uint32_t dt = dot_a + (r >> 3) * 256 + (r & 7) * 2;
 #pragma unroll
                 for (int k = 0; k < kWK; k++)
-                    dt[((k >> 3) * 128 + (k & 7) * 16) / 2] = (uint16_t)((k & 1) ? (pk[k >> 1] >> 16) : (pk[k >> 1] & 0xFFFFu));
+                    sts16(dt + (k >> 3) * 128 + (k & 7) * 16,
+                          (uint16_t)((k & 1) ? (pk[k >> 1] >> 16) : (pk[k >> 1] & 0xFFFFu)));
                 fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(doready);
@@ -1242,41 +1332,45 @@ __global__ void __launch_bounds__(kTcThreads, 1) wide_tail_kernel(const __grid_c
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 uint32_t v[32];
                 tmem_ld32_async(tmem + lanebase + kColDH + 64 * b + 32 * hlf, v);
+                const int it = lt * kTlKB + c, s = it % kTlS2;
+                mbar_wait(&full2[s], (it / kTlS2) & 1);  // complete already (the MMAs read it)
+                const uint32_t rowa = r2 + s * kTlStage + r * 128;
+                uint4 hv[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) hv[q] = lds128(rowa + (((4 * hlf + q) ^ (r & 7)) << 4));
                 tmem_wait();
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&dhfree[b]);
-                const int it = lt * 2 * kTlKB + kTlKB + c, s = it % kTlS;
-                mbar_wait(&full[s], (it / kTlS) & 1);  // complete already (the MMAs read it)
-                unsigned char* rowp = ring + s * kTlStage + r * 128;
 #pragma unroll
                 for (int q = 0; q < 4; q++) {
-                    uint4* p16 = reinterpret_cast<uint4*>(rowp + (((4 * hlf + q) ^ (r & 7)) << 4));
-                    uint4 hv = *p16;
-                    uint32_t* hw = reinterpret_cast<uint32_t*>(&hv);
+                    uint32_t* hw = reinterpret_cast<uint32_t*>(&hv[q]);
 #pragma unroll
                     for (int e = 0; e < 4; e++) {
                         const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&hw[e]));
                         hw[e] = pack_bf16x2(__uint_as_float(v[8 * q + 2 * e]) * hf.x * (1.f - hf.x),
                                             __uint_as_float(v[8 * q + 2 * e + 1]) * hf.y * (1.f - hf.y));
                     }
-                    *p16 = hv;
+                    sts128(rowa + (((4 * hlf + q) ^ (r & 7)) << 4), hv[q]);
                 }
                 fence_proxy_async();
                 bar_sync(1 + quad, 64);  // both column halves of these 32 rows are written
                 if (hlf == 0 && lane == 0) {
-                    tma_store_2d(&map_dh, ring + s * kTlStage + quad * 32 * 128, c * 64, t * 128 + quad * 32);
+                    if (GLX_TL_HINTS)
+                        tma_store_2d_hint(&map_dh, ring2 + s * kTlStage + quad * 32 * 128, c * 64, t * 128 + quad * 32,
+                                          l2_policy_evict_first());
+                    else
+                        tma_store_2d(&map_dh, ring2 + s * kTlStage + quad * 32 * 128, c * 64, t * 128 + quad * 32);
                     // a stage is released once its store has read it, one chunk late; the
-                    // tile's last stage at once (the producer refills it with pass 1 of the
-                    // next tile, which this warp's next store depends on)
+                    // tile's last stage at once (keeps the release independent of the next tile)
                     if (c + 1 < kTlKB) {
                         asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-                        if (pend >= 0) mbar_arrive(&empty[pend]);
+                        if (pend >= 0) mbar_arrive(&empty2[pend]);
                         pend = s;
                     } else {
                         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-                        if (pend >= 0) mbar_arrive(&empty[pend]);
-                        mbar_arrive(&empty[s]);
+                        if (pend >= 0) mbar_arrive(&empty2[pend]);
+                        mbar_arrive(&empty2[s]);
                         pend = -1;
                     }
                 }
@@ -1343,7 +1437,6 @@ struct WideWork {
     void* dob;  // [C][64] bf16
     void* doT;  // delta_o^T, K-blocked [C/64][32][64] bf16, rows >= 16 zero
     void* dht;  // dH, row-major [C][1024] bf16 (read MN-major by the dW1 GEMM)
-    void* w2tl; // W2^T in the tail kernel's operand layout (32 KB)
     float* dW1T;
     float* dW2T;
     double* grad;  // [kWP + 3]: gradient sums, then loss, correct, wrong
@@ -1368,7 +1461,6 @@ static size_t carve(WideWork* w, unsigned char* base, int64_t C, int splits) {
     t.dob = take((size_t)C * 64 * 2);
     t.doT = take((size_t)32 * C * 2);
     t.dht = take((size_t)kWH * C * 2);
-    t.w2tl = take(kTlW2t);
     t.dW1T = (float*)take((size_t)splits * kWMi * kWH * 4);
     t.dW2T = (float*)take((size_t)std::max(kWSplits2, kTlSlabs) * kWMi * 32 * 4);
     t.grad = (double*)take((size_t)(kWP + 3) * 8);
@@ -1403,8 +1495,7 @@ static cudaError_t launch_wide_tail(const WideWork& w, int Cc, const uint8_t* la
     if (e != cudaSuccess) return e;
     const int ntiles = (Cc + 127) / 128;
     const int grid = std::min(std::min(sm_count(), kTlSlabs), ntiles);
-    wide_tail_kernel<<<grid, kTcThreads, kTlSmem, st>>>(mh, mw, md, (const __nv_bfloat16*)w.w2tl, w.b2, labels, Cc,
-                                                        w.dW2T, stats);
+    wide_tail_kernel<<<grid, kTlThreads, kTlSmem, st>>>(mh, mw, md, w.b2, labels, Cc, w.dW2T, stats);
     return cudaGetLastError();
 }
 
@@ -1432,14 +1523,12 @@ cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const vo
     const bool tail = wide_tail_enabled();
     const int slabs2 = tail ? kTlSlabs : kWSplits2;
     if ((e = cudaMemsetAsync(w.dW2T, 0, (size_t)slabs2 * zstride2 * 4, st)) != cudaSuccess) return e;
-    if (tail) {
-        wide_tail_w2t_kernel<<<kWH * 16 / 256, 256, 0, st>>>(W2, (__nv_bfloat16*)w.w2tl);
-        if ((e = cudaGetLastError()) != cudaSuccess) return e;
-    }
     if ((e = cudaMemsetAsync(w.dob, 0, (size_t)C * 64 * 2, st)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(w.doT, 0, (size_t)32 * C * 2, st)) != cudaSuccess) return e;
-    h_bias_cols_kernel<<<(unsigned)((C * (kWHL - kWH) + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.Hb, C);
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (!tail) {  // the bias input column of H (only GEMM 5 reads it)
+        h_bias_cols_kernel<<<(unsigned)((C * (kWHL - kWH) + 255) / 256), 256, 0, st>>>((__nv_bfloat16*)w.Hb, C);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    }
     for (int64_t r0 = 0; r0 < N; r0 += C) {
         const int Cc = (int)std::min<int64_t>(C, N - r0);
         const __nv_bfloat16* Xc = reinterpret_cast<const __nv_bfloat16*>(Xb) + r0 * kWD;

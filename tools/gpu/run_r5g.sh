@@ -1,0 +1,7 @@
+set -x
+timeout 240 python -m pytest tests/test_gpu_tc.py -q -k "fused_tail" -s > gpurun_out/r5g_tail.log 2>&1; echo "rc=$?" >> gpurun_out/r5g_tail.log
+grep -E "fused|passed|failed|Error" gpurun_out/r5g_tail.log | tail -12
+grep -q "rc=0" gpurun_out/r5g_tail.log || exit 1
+for v in 0 1; do GLX_WIDE_TAIL=$v timeout 200 python tools/wide_time.py 4194304; done > gpurun_out/r5g_time.log 2>&1
+cat gpurun_out/r5g_time.log
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:wide_tail -c 6 --csv --log-file gpurun_out/r5g_tail_launches.csv python tools/wide_time.py 4194304 > gpurun_out/r5g_ncu1.log 2>&1
