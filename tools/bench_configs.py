@@ -213,9 +213,10 @@ def config5(L, peak, cpu=None, rows=16_777_216, epochs=3):
             "ms_per_epoch": ms, "sample_epochs_per_s": rows / (ms * 1e-3),
             "tflops_algorithmic": flops / (ms * 1e-3) / 1e12, "frac_bf16_peak": flops / (ms * 1e-3) / 1e12 / bf16,
             "tc_gemm_ms_per_epoch": float(kms[0]) / epochs, "bf16_peak_tflops": bf16,
-            "note": "tc_gemm_ms covers the five tcgen05 GEMM launches per 1Mi-row chunk (hidden layer, output layer, "
-                    "hidden deltas, split-K dW1, split-K dW2); the remainder is the per-epoch derive/update kernels. "
-                    "frac_bf16_peak is against MEASURED_PEAKS.json bf16_tflops (cuBLAS burst)"}
+            "note": "tc_gemm_ms covers the three tcgen05 launches per 1Mi-row chunk (hidden-layer GEMM, the fused tail "
+                    "kernel: output layer + delta_o + dH + dW2 in one pass over H, split-K dW1 GEMM); the remainder is "
+                    "the per-epoch derive/reduce/update kernels. frac_bf16_peak is against MEASURED_PEAKS.json "
+                    "bf16_tflops (cuBLAS burst)"}
 
 
 def config5_tf32(L, peak, cpu=None, rows=16_777_216, epochs=2):
