@@ -1348,7 +1348,7 @@ int glx_wide_grad_tf32(const float* w_ih, const float* w_ho, const float* X, con
     GLX_CK(ws->wide.ensure(wide32_work_bytes(C, splits)));
     GLX_CK(wide_grad_tf32(w_ih, w_ho, X, XT, labels, N, ws->wide.as<unsigned char>(), C, splits, grad, st,
                           [](bool) {}));
-    g_launches.fetch_add(3 + 5 * (uint64_t)((N + C - 1) / C));
+    g_launches.fetch_add(3 + wide32_launches_per_chunk() * (uint64_t)((N + C - 1) / C));
     return GLX_OK;
 }
 
@@ -1378,7 +1378,7 @@ int glx_wide_train_tf32(float* w_ih, float* w_ho, const float* X, const float* X
         GLX_CK(wide_epoch_tf32(w_ih, w_ho, X, XT, labels, N, lr, ws->wide.as<unsigned char>(), C, splits, stats,
                                nonfinite, st, prof));
         GLX_CK(perr);
-        g_launches.fetch_add(4 + 5 * (uint64_t)((N + C - 1) / C));
+        g_launches.fetch_add(4 + wide32_launches_per_chunk() * (uint64_t)((N + C - 1) / C));
     }
     return GLX_OK;
 }

@@ -161,7 +161,8 @@ constexpr int64_t kWideP = 1024 * 1025 + 16 * 1025;  // weights of the wide netw
 cudaError_t launch_wide_gen(void* Xb, void* XT, uint8_t* labels, int64_t N, uint64_t seed, int64_t row0,
                             cudaStream_t st);
 size_t wide_work_bytes(int64_t C, int splits);
-int wide_launches_per_chunk();  // tcgen05 launches per row chunk of the bf16 wide epoch (3 fused, 5 unfused)
+int wide_launches_per_chunk();
+int wide32_launches_per_chunk();  // the tf32 wide epoch (4 fused, 5 unfused)  // tcgen05 launches per row chunk of the bf16 wide epoch (3 fused, 5 unfused)
 cudaError_t wide_grad(const float* W1, const float* W2, const void* Xb, const void* XT, const uint8_t* labels,
                       int64_t N, unsigned char* work, int64_t C, int splits, double* grad, cudaStream_t st,
                       const std::function<void(bool)>& prof);

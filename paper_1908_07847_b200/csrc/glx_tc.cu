@@ -1500,6 +1500,7 @@ static cudaError_t launch_wide_tail(const WideWork& w, int Cc, const uint8_t* la
 }
 
 int wide_launches_per_chunk() { return wide_tail_enabled() ? 3 : 5; }
+int wide32_launches_per_chunk() { return wide_tail_enabled() ? 4 : 5; }
 
 // one epoch; stats (device, may be null): [loss, correct, wrong] accumulated
 // gradient SUM over the N rows at the current weights -> grad[0, kWP) (f64),
@@ -1694,6 +1695,203 @@ struct WideWork32 {
     double* grad;
 };
 
+// ------------------------------------------- wide tail, tf32 path (CUDA cores)
+// GEMMs 2 and 3 of the tf32 epoch fused into one streaming pass per 128-row tile. Both
+// contractions are 16 wide (the K = 16 outputs), and tf32 MMAs take no MN-major
+// operands (a second, transposed W2 copy would be needed), so this runs on the FP32
+// pipe: 32 FMA per H element against 8 bytes of HBM traffic (H in, dH^T out).
+//   pass 1 (H from HBM): o_pre[r][k] = sum_j H[r][j] W2[k][j] (fp32, more exact than the
+//          tf32 GEMM it replaces); o = sigmoid(o_pre + b2), delta_o, loss, argmax;
+//          delta_o -> the K-blocked delta_o^T operand of the dW2 GEMM
+//   pass 2 (H again, L2-hot): dH[r][j] = (sum_k delta_o[r][k] W2[k][j]) h (1 - h) ->
+//          dH^T K-blocked [rows/32][1024][32] (the dW1 GEMM's operand; a warp's lanes are
+//          32 consecutive rows: one 128-byte store per unit)
+// Thread (row r, half) takes 16 of each k-block's 32 units; W2^T sits in shared memory
+// ([1024][16], read as broadcasts).
+#ifndef GLX_T3_TPR
+#define GLX_T3_TPR 4  // threads per row (2: 8 compute warps, 4: 16)
+#endif
+constexpr int kT3S = 8;                     // H k-block stages (128 rows x 32 f32 each)
+constexpr int kT3KB = kWH / 32;             // 32 k-blocks per pass
+constexpr int kT3P = GLX_T3_TPR;            // threads per row
+constexpr int kT3U = 32 / kT3P;             // units per thread per k-block
+constexpr uint32_t kT3Stage = 128 * 128;
+constexpr int kT3Threads = 32 + 128 * kT3P;  // producer warp + compute warps
+constexpr size_t kT3Smem = 1024 + kT3S * kT3Stage + kWH * 16 * 4 + kT3P * 128 * 16 * 4 + 64 + 256;
+static_assert(kT3Smem <= 232448, "tf32 tail shared memory");
+
+__global__ void __launch_bounds__(kT3Threads, 1) wide_tail32_kernel(const __grid_constant__ CUtensorMap map_h,
+                                                                     const float* __restrict__ W2T,
+                                                                     const float* __restrict__ b2,
+                                                                     const uint8_t* __restrict__ labels, int M,
+                                                                     float* __restrict__ doT, float* __restrict__ dhT,
+                                                                     double* __restrict__ stats) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
+    unsigned char* ring = sm;
+    float* w2t = reinterpret_cast<float*>(ring + kT3S * kT3Stage);  // [1024 units][16]
+    float* xo = w2t + kWH * 16;                                      // [kT3P - 1][128][16] pass-1 partials
+    float* dob = xo + (kT3P - 1) * 128 * 16;                         // [128][16] delta_o
+    float* b2s = dob + 128 * 16;                                     // [16]
+    uint64_t* full = reinterpret_cast<uint64_t*>(b2s + 16);
+    uint64_t* empty = full + kT3S;
+    constexpr int kCW = 4 * kT3P;  // compute warps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = (M + 127) / 128;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < kT3S; i++) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kCW);
+        }
+        fence_mbar_init();
+    }
+    for (int e = threadIdx.x; e < kWH * 16; e += blockDim.x) w2t[e] = W2T[(e >> 4) * 32 + (e & 15)];
+    if (threadIdx.x < 16) b2s[threadIdx.x] = b2[threadIdx.x];
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {  // producer: pass 1 then pass 2 of each tile through one ring
+            const uint64_t keep = l2_policy_evict_last(), drop = l2_policy_evict_first();
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x)
+                for (int j = 0; j < 2 * kT3KB; j++, it++) {
+                    const int s = it % kT3S;
+                    if (it >= kT3S) mbar_wait(&empty[s], ((it / kT3S) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], kT3Stage);
+                    tma_load_2d_hint(ring + s * kT3Stage, &map_h, (j % kT3KB) * 32, t * 128, &full[s],
+                                     j < kT3KB ? keep : drop);
+                }
+        }
+        return;
+    }
+    // thread (row r, part): units kT3U part .. of every 32-unit k-block
+    const int c = threadIdx.x - 32, r = c & 127, part = c >> 7;
+    const uint32_t ring_a = smem_u32(ring);
+    float loss = 0.f, correct = 0.f, valid = 0.f;
+    int it = 0;
+    auto load_h = [&](int s, float (&hv)[kT3U]) {
+        const uint32_t rowa = ring_a + s * kT3Stage + r * 128;
+#pragma unroll
+        for (int q = 0; q < kT3U / 4; q++) {
+            const uint4 v = lds128(rowa + ((((kT3U / 4) * part + q) ^ (r & 7)) << 4));
+            hv[4 * q] = __uint_as_float(v.x);
+            hv[4 * q + 1] = __uint_as_float(v.y);
+            hv[4 * q + 2] = __uint_as_float(v.z);
+            hv[4 * q + 3] = __uint_as_float(v.w);
+        }
+    };
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int row = t * 128 + r;
+        const int lab = (part == 0 && row < M) ? labels[row] : 0;
+        // pass 1: output-layer pre-activations over this thread's units
+        float2 acc[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) acc[k] = make_float2(0.f, 0.f);
+        for (int kb = 0; kb < kT3KB; kb++, it++) {
+            const int s = it % kT3S;
+            mbar_wait(&full[s], (it / kT3S) & 1);
+            float hv[kT3U];
+            load_h(s, hv);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            const float4* wj = reinterpret_cast<const float4*>(w2t + (kb * 32 + kT3U * part) * 16);
+#pragma unroll
+            for (int u = 0; u < kT3U; u++) {
+                const float2 h2 = bcast2(hv[u]);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const float4 w = wj[u * 4 + q];
+                    acc[2 * q] = ffma2(h2, make_float2(w.x, w.y), acc[2 * q]);
+                    acc[2 * q + 1] = ffma2(h2, make_float2(w.z, w.w), acc[2 * q + 1]);
+                }
+            }
+        }
+        // the parts of each row meet; part 0 owns the output neuron of its row
+        if (part > 0) {
+#pragma unroll
+            for (int k = 0; k < 8; k++) *reinterpret_cast<float2*>(xo + ((part - 1) * 128 + r) * 16 + 2 * k) = acc[k];
+        }
+        bar_sync(1, kCW * 32);
+        if (part == 0) {
+#pragma unroll
+            for (int p = 1; p < kT3P; p++)
+#pragma unroll
+                for (int k = 0; k < 8; k++) {
+                    const float2 o2 = *reinterpret_cast<const float2*>(xo + ((p - 1) * 128 + r) * 16 + 2 * k);
+                    acc[k].x += o2.x;
+                    acc[k].y += o2.y;
+                }
+            float d[kWK];
+            if (row < M) {
+                float best = -1.f;
+                int arg = 0;
+#pragma unroll
+                for (int k = 0; k < kWK; k++) {
+                    const float pre = k & 1 ? acc[k >> 1].y : acc[k >> 1].x;
+                    const float o = 1.0f / (1.0f + __expf(-(pre + b2s[k])));
+                    const float tk = (k == lab) ? 1.f : 0.f;
+                    d[k] = (o - tk) * o * (1.0f - o);
+                    loss = fmaf(0.5f * (tk - o), tk - o, loss);
+                    if (o > best) {
+                        best = o;
+                        arg = k;
+                    }
+                }
+                correct += arg == lab ? 1.f : 0.f;
+                valid += 1.f;
+#pragma unroll
+                for (int k = 0; k < kWK; k++) doT[((int64_t)(row >> 5) * 32 + k) * 32 + (row & 31)] = d[k];
+            } else {
+#pragma unroll
+                for (int k = 0; k < kWK; k++) d[k] = 0.f;
+            }
+#pragma unroll
+            for (int k = 0; k < kWK; k += 4)
+                *reinterpret_cast<float4*>(dob + r * 16 + k) = make_float4(d[k], d[k + 1], d[k + 2], d[k + 3]);
+        }
+        bar_sync(1, kCW * 32);
+        float2 dd[8];
+#pragma unroll
+        for (int k = 0; k < 8; k++) dd[k] = *reinterpret_cast<const float2*>(dob + r * 16 + 2 * k);
+        // pass 2: dH = (delta_o W2) h (1 - h) -> dH^T
+        float* dst = dhT + (int64_t)(row >> 5) * kWH * 32 + (row & 31);
+        for (int kb = 0; kb < kT3KB; kb++, it++) {
+            const int s = it % kT3S;
+            mbar_wait(&full[s], (it / kT3S) & 1);
+            float hv[kT3U];
+            load_h(s, hv);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            const int j0 = kb * 32 + kT3U * part;
+            const float4* wj = reinterpret_cast<const float4*>(w2t + j0 * 16);
+#pragma unroll
+            for (int u = 0; u < kT3U; u++) {
+                float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const float4 w = wj[u * 4 + q];
+                    p = ffma2(dd[2 * q], make_float2(w.x, w.y), p);
+                    p = ffma2(dd[2 * q + 1], make_float2(w.z, w.w), p);
+                }
+                const float h = hv[u];
+                if (row < M) dst[(int64_t)(j0 + u) * 32] = (p.x + p.y) * h * (1.f - h);
+            }
+        }
+    }
+    if (part == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            loss += __shfl_xor_sync(0xffffffffu, loss, o);
+            correct += __shfl_xor_sync(0xffffffffu, correct, o);
+            valid += __shfl_xor_sync(0xffffffffu, valid, o);
+        }
+        if (lane == 0 && stats) {
+            atomicAdd(stats + 0, (double)loss);
+            atomicAdd(stats + 1, (double)correct);
+            atomicAdd(stats + 2, (double)(valid - correct));
+        }
+    }
+}
+
 static size_t carve32(WideWork32* w, unsigned char* base, int64_t C, int splits) {
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -1730,6 +1928,7 @@ cudaError_t wide_grad_tf32(const float* W1, const float* W2, const float* X, con
     if (!grad) grad = w.grad;
     double* stats = grad + kWP;
     if ((e = cudaMemsetAsync(stats, 0, 3 * sizeof(double), st)) != cudaSuccess) return e;
+    const bool tail = wide_tail_enabled();
     wide_derive32_kernel<<<(kWH * kWD + 255) / 256, 256, 0, st>>>(W1, W2, w.W1p, w.b1, w.W2p, w.b2, w.W2T);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int64_t zstride = (int64_t)kWMi * kWH, zstride2 = (int64_t)kWMi * 32;
@@ -1753,7 +1952,18 @@ cudaError_t wide_grad_tf32(const float* W1, const float* W2, const float* X, con
             ep.t_blk = kWR;
             if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 2. output layer -> delta_o, loss, accuracy
+        if (tail) {  // 2 + 3 fused (CUDA cores): delta_o, loss, accuracy, dH^T
+            CUtensorMap mh;
+            if (!make_map_f32(&mh, w.H, Cc, kWH, kWH, 128)) return cudaErrorInvalidValue;
+            if ((e = cudaFuncSetAttribute(wide_tail32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kT3Smem)) != cudaSuccess)
+                return e;
+            const int grid = std::min(sm_count(), (Cc + 127) / 128);
+            wide_tail32_kernel<<<grid, kT3Threads, kT3Smem, st>>>(mh, w.W2T, w.b2, labels + r0, Cc, w.doT, w.dhT,
+                                                                  stats);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        if (!tail) {  // 2. output layer -> delta_o, loss, accuracy
             TcGemm g{w.H, w.W2p, Cc, 32, kWH, kWH, kWH, 1};
             TcEpilogue ep{};
             ep.kind = 2;
@@ -1765,7 +1975,7 @@ cudaError_t wide_grad_tf32(const float* W1, const float* W2, const float* X, con
             ep.stats = stats;
             if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
         }
-        {  // 3. hidden deltas -> dH^T (K-blocked)
+        if (!tail) {  // 3. hidden deltas -> dH^T (K-blocked)
             TcGemm g{w.dob, w.W2T, Cc, kWH, 32, 32, 32, 1};
             TcEpilogue ep{};
             ep.kind = 3;

@@ -79,8 +79,9 @@ def test_wide_config_vs_oracle(gpu, init_range, lr, tol):
     assert abs(stats[0, 1] - correct) <= 20
 
 
+@pytest.mark.parametrize("tail", ["1", "0"])
 @pytest.mark.parametrize("lr", [0.1, 0.5])
-def test_wide_tf32_vs_oracle_f32_rows(gpu, lr):
+def test_wide_tf32_vs_oracle_f32_rows(gpu, lr, tail, monkeypatch):
     """Config 5 shape on tcgen05 kind::tf32 with f32 U[0,1) rows (not bf16-valued),
     f32 H and deltas: after 10 epochs the weights are within SURVEY.md 8(c)'s 1e-4
     max(1,|w|) of the f64 oracle run on the same f32 rows, at the reference's lr 0.1
@@ -93,6 +94,7 @@ def test_wide_tf32_vs_oracle_f32_rows(gpu, lr):
     from oracle import oracle as O
     from paper_1908_07847_b200 import wide
 
+    monkeypatch.setenv("GLX_WIDE_TAIL", tail)  # fused CUDA-core tail (default) or tf32 GEMMs 2, 3
     N, epochs = 2048, 10
     data = wide.WideData(N, seed=5, precision="tf32")
     x, y = data.host_rows()
@@ -293,4 +295,34 @@ def test_wide_fused_tail_vs_unfused_and_f64(gpu, N, monkeypatch):
     assert abs(gb[P].item() - loss) <= 1e-4 * loss  # loss sum
     assert abs(ga[P].item() - gb[P].item()) <= 1e-6 * ga[P].item()
     assert ga[P + 1].item() == gb[P + 1].item() and ga[P + 2].item() == gb[P + 2].item()
+    assert gb[P + 1].item() + gb[P + 2].item() == N
+
+
+@pytest.mark.parametrize("N", [4096 + 32, (1 << 19) + 32])
+def test_wide_tf32_fused_tail_vs_unfused(gpu, N, monkeypatch):
+    """tf32 path: the fused CUDA-core tail (output layer + dH in fp32, glx_tc.cu
+    wide_tail32_kernel) against the tf32 GEMMs 2 and 3 it replaces, on the same f32 rows
+    (one tile with a partial second, and a partial second chunk). The fused output layer
+    is exact fp32 where the GEMM rounds H and W2 to tf32, so the gradients agree to that
+    rounding, and the statistics count the same rows."""
+    import torch
+
+    from paper_1908_07847_b200 import wide
+
+    data = wide.WideData(N, seed=13, precision="tf32")
+    w1, w2 = wide.init_wide_weights(seed=6)
+    monkeypatch.setenv("GLX_WIDE_TAIL", "0")
+    ga = wide.WideEngine(data, w1, w2).grad_sum().clone()
+    monkeypatch.setenv("GLX_WIDE_TAIL", "1")
+    gb = wide.WideEngine(data, w1, w2).grad_sum().clone()
+    torch.cuda.synchronize()
+    P = wide.WideEngine.P
+    P1 = 1024 * 1025
+    e1 = (ga[:P1] - gb[:P1]).abs().max().item() / ga[:P1].abs().max().item()
+    e2 = (ga[P1:P] - gb[P1:P]).abs().max().item() / ga[P1:P].abs().max().item()
+    el = abs(ga[P].item() - gb[P].item()) / ga[P].item()
+    print(f"N={N}: tf32 fused vs unfused: dW1 {e1:.2e}, dW2 {e2:.2e}, loss {el:.2e}, "
+          f"correct {ga[P + 1].item()} vs {gb[P + 1].item()}")
+    assert e1 <= 1e-3 and e2 <= 1e-3 and el <= 1e-4, (e1, e2, el)
+    assert abs(ga[P + 1].item() - gb[P + 1].item()) <= 4
     assert gb[P + 1].item() + gb[P + 2].item() == N
