@@ -1892,6 +1892,264 @@ __global__ void __launch_bounds__(kT3Threads, 1) wide_tail32_kernel(const __grid
     }
 }
 
+// tf32 tail with the output layer on the tensor cores: pass 1 is an SS kind::tf32 MMA
+// chain (D_o[128 rows][16] = H . W2^T over 32 k-blocks, as in the bf16 tail's phase A),
+// so the CUDA cores only run pass 2. Pass 1 streams H from HBM through ring 1 (its own
+// producer, MMA-issuing thread and TMEM accumulator); pass 2 re-reads the tile from L2
+// through ring 2 once pass 1 landed (p1land / p2got as in wide_tail_kernel).
+#ifndef GLX_T4_P1HINT
+#define GLX_T4_P1HINT 1  // pass-1 loads evict_last (0: default policy)
+#endif
+#ifndef GLX_T4_DHCS
+#define GLX_T4_DHCS 0    // 1: dH^T / delta_o^T stores with the streaming (evict-first) cache operator
+#endif
+#ifndef GLX_T4_LAG
+#define GLX_T4_LAG 0     // > 0: pass 1 of tile t + 1 starts once pass 2 of tile t issued this many k-blocks
+#endif
+constexpr int kT4S1 = 3, kT4S2 = 2;
+constexpr int kT4CW = 16;                        // compute warps (4 per row, 8 units each per k-block)
+constexpr int kT4Threads = 32 * (3 + kT4CW);     // P1 producer, MMA, compute warps, P2 producer
+constexpr size_t kT4Smem = 1024 + (kT4S1 + kT4S2) * kT3Stage + kT3KB * 2048 + kWH * 16 * 4 + 128 * 16 * 4 + 64 + 512;
+static_assert(kT4Smem <= 232448, "tf32 tc tail shared memory");
+
+__global__ void __launch_bounds__(kT4Threads, 1) wide_tail32tc_kernel(const __grid_constant__ CUtensorMap map_h,
+                                                                       const __grid_constant__ CUtensorMap map_w2,
+                                                                       const float* __restrict__ W2T,
+                                                                       const float* __restrict__ b2,
+                                                                       const uint8_t* __restrict__ labels, int M,
+                                                                       float* __restrict__ doT, float* __restrict__ dhT,
+                                                                       double* __restrict__ stats) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* sm = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
+    unsigned char* ring1 = sm;
+    unsigned char* ring2 = ring1 + kT4S1 * kT3Stage;
+    unsigned char* w2m = ring2 + kT4S2 * kT3Stage;                  // W2 [16][1024] as 32 sw128 k-blocks of 2 KB
+    float* w2t = reinterpret_cast<float*>(w2m + kT3KB * 2048);      // [1024 units][16]
+    float* dob = w2t + kWH * 16;                                     // [128][16] delta_o
+    float* b2s = dob + 128 * 16;                                     // [16]
+    uint64_t* full1 = reinterpret_cast<uint64_t*>(b2s + 16);
+    uint64_t* empty1 = full1 + kT4S1;
+    uint64_t* full2 = empty1 + kT4S1;
+    uint64_t* empty2 = full2 + kT4S2;
+    uint64_t* wbar = empty2 + kT4S2;
+    uint64_t* ofull = wbar + 1;
+    uint64_t* ofree = ofull + 1;
+    uint64_t* p1land = ofree + 1;
+    uint64_t* p2got = p1land + 1;
+    uint64_t* p2lag = p2got + 1;  // GLX_T4_LAG: pass 2 of a tile issued its first GLX_T4_LAG k-blocks
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(p2lag + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = (M + 127) / 128;
+    if (threadIdx.x == 0) {
+        mbar_init(p2lag, 1);
+        for (int i = 0; i < kT4S1; i++) {
+            mbar_init(&full1[i], 1);
+            mbar_init(&empty1[i], 1);
+        }
+        for (int i = 0; i < kT4S2; i++) {
+            mbar_init(&full2[i], 1);
+            mbar_init(&empty2[i], kT4CW);
+        }
+        mbar_init(wbar, 1);
+        mbar_init(ofull, 1);
+        mbar_init(ofree, 4);
+        mbar_init(p1land, 1);
+        mbar_init(p2got, 1);
+        fence_mbar_init();
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(32)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    for (int e = threadIdx.x; e < kWH * 16; e += blockDim.x) w2t[e] = W2T[(e >> 4) * 32 + (e & 15)];
+    if (threadIdx.x < 16) b2s[threadIdx.x] = b2[threadIdx.x];
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // pass-1 producer (HBM): W2, then the tiles' k-blocks
+            const uint64_t keep = l2_policy_evict_last();
+            mbar_arrive_expect_tx(wbar, kT3KB * 2048);
+            for (int kb = 0; kb < kT3KB; kb++) tma_load_2d(w2m + kb * 2048, &map_w2, kb * 32, 0, wbar);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                if (GLX_T4_LAG > 0 && lt > 0) mbar_wait(p2lag, (lt - 1) & 1);
+                for (int kb = 0; kb < kT3KB; kb++, it++) {
+                    const int s = it % kT4S1;
+                    if (it >= kT4S1) mbar_wait(&empty1[s], ((it / kT4S1) - 1) & 1);
+                    mbar_arrive_expect_tx(&full1[s], kT3Stage);
+                    if (GLX_T4_P1HINT) tma_load_2d_hint(ring1 + s * kT3Stage, &map_h, kb * 32, t * 128, &full1[s], keep);
+                    else tma_load_2d(ring1 + s * kT3Stage, &map_h, kb * 32, t * 128, &full1[s]);
+                }
+            }
+        }
+    } else if (warp == 2 + kT4CW) {
+        if (lane == 0) {  // pass-2 producer (L2)
+            const uint64_t drop = l2_policy_evict_first();
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                mbar_wait(p1land, lt & 1);
+                mbar_arrive(p2got);
+                for (int kb = 0; kb < kT3KB; kb++, it++) {
+                    const int s = it % kT4S2;
+                    if (it >= kT4S2) mbar_wait(&empty2[s], ((it / kT4S2) - 1) & 1);
+                    mbar_arrive_expect_tx(&full2[s], kT3Stage);
+                    tma_load_2d_hint(ring2 + s * kT3Stage, &map_h, kb * 32, t * 128, &full2[s], drop);
+                    if (GLX_T4_LAG > 0 && kb + 1 == GLX_T4_LAG) mbar_arrive(p2lag);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // output-layer MMAs
+            mbar_wait(wbar, 0);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t idO = umma_idesc_tf32(128, 16);
+            const uint32_t r1 = smem_u32(ring1), wa = smem_u32(w2m);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                if (lt > 0) {
+                    mbar_wait(ofree, (lt - 1) & 1);
+                    mbar_wait(p2got, (lt - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                }
+                for (int kb = 0; kb < kT3KB; kb++, it++) {
+                    const int s = it % kT4S1;
+                    mbar_wait(&full1[s], (it / kT4S1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int kk = 0; kk < 4; kk++)
+                        umma_tf32(tmem, umma_desc_sw128(r1 + s * kT3Stage + kk * 32), umma_desc_sw128(wa + kb * 2048 + kk * 32),
+                                  idO, (kb | kk) != 0);
+                    umma_commit(&empty1[s]);
+                }
+                mbar_arrive(p1land);
+                umma_commit(ofull);
+            }
+        }
+    } else {
+        // compute warps 2 .. 17: TMEM lane quadrant = warp % 4 -> rows 32 quad ..; part = (warp - 2) / 4
+        const int quad = warp & 3, part = (warp - 2) >> 2;
+        const int r = quad * 32 + lane;
+        const uint32_t lanebase = (uint32_t)(quad * 32) << 16;
+        const uint32_t r2 = smem_u32(ring2);
+        constexpr int kU = 8;  // units per thread per k-block
+        float loss = 0.f, correct = 0.f, valid = 0.f;
+        int it = 0, lt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+            const int row = t * 128 + r;
+            if (part == 0) {
+                const int lab = row < M ? labels[row] : 0;
+                mbar_wait(ofull, lt & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                uint32_t ro[16];
+                tmem_ld16_async(tmem + lanebase, ro);
+                tmem_wait();
+                asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(ofree);
+                float d[kWK];
+                if (row < M) {
+                    float best = -1.f;
+                    int arg = 0;
+#pragma unroll
+                    for (int k = 0; k < kWK; k++) {
+                        const float o = 1.0f / (1.0f + __expf(-(__uint_as_float(ro[k]) + b2s[k])));
+                        const float tk = (k == lab) ? 1.f : 0.f;
+                        d[k] = (o - tk) * o * (1.0f - o);
+                        loss = fmaf(0.5f * (tk - o), tk - o, loss);
+                        if (o > best) {
+                            best = o;
+                            arg = k;
+                        }
+                    }
+                    correct += arg == lab ? 1.f : 0.f;
+                    valid += 1.f;
+#pragma unroll
+                    for (int k = 0; k < kWK; k++) {
+                        float* q = doT + ((int64_t)(row >> 5) * 32 + k) * 32 + (row & 31);
+                        if (GLX_T4_DHCS) __stcs(q, d[k]);
+                        else *q = d[k];
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < kWK; k++) d[k] = 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < kWK; k += 4)
+                    *reinterpret_cast<float4*>(dob + r * 16 + k) = make_float4(d[k], d[k + 1], d[k + 2], d[k + 3]);
+            }
+            bar_sync(1, kT4CW * 32);
+            float2 dd[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) dd[k] = *reinterpret_cast<const float2*>(dob + r * 16 + 2 * k);
+            // pass 2: dH = (delta_o W2) h (1 - h) -> dH^T
+            float* dst = dhT + (int64_t)(row >> 5) * kWH * 32 + (row & 31);
+            for (int kb = 0; kb < kT3KB; kb++, it++) {
+                const int s = it % kT4S2;
+                mbar_wait(&full2[s], (it / kT4S2) & 1);
+                const uint32_t rowa = r2 + s * kT3Stage + r * 128;
+                float hv[kU];
+#pragma unroll
+                for (int q = 0; q < kU / 4; q++) {
+                    const uint4 v = lds128(rowa + ((((kU / 4) * part + q) ^ (r & 7)) << 4));
+                    hv[4 * q] = __uint_as_float(v.x);
+                    hv[4 * q + 1] = __uint_as_float(v.y);
+                    hv[4 * q + 2] = __uint_as_float(v.z);
+                    hv[4 * q + 3] = __uint_as_float(v.w);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty2[s]);
+                const int j0 = kb * 32 + kU * part;
+                const float4* wj = reinterpret_cast<const float4*>(w2t + j0 * 16);
+#pragma unroll
+                for (int u = 0; u < kU; u++) {
+                    float2 p = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const float4 w = wj[u * 4 + q];
+                        p = ffma2(dd[2 * q], make_float2(w.x, w.y), p);
+                        p = ffma2(dd[2 * q + 1], make_float2(w.z, w.w), p);
+                    }
+                    const float h = hv[u];
+                    if (row < M) {
+                        if (GLX_T4_DHCS) __stcs(dst + (int64_t)(j0 + u) * 32, (p.x + p.y) * h * (1.f - h));
+                        else dst[(int64_t)(j0 + u) * 32] = (p.x + p.y) * h * (1.f - h);
+                    }
+                }
+            }
+        }
+        if (part == 0) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                loss += __shfl_xor_sync(0xffffffffu, loss, o);
+                correct += __shfl_xor_sync(0xffffffffu, correct, o);
+                valid += __shfl_xor_sync(0xffffffffu, valid, o);
+            }
+            if (lane == 0 && stats) {
+                atomicAdd(stats + 0, (double)loss);
+                atomicAdd(stats + 1, (double)correct);
+                atomicAdd(stats + 2, (double)(valid - correct));
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(32) : "memory");
+    }
+}
+
+// GLX_WIDE_TAIL32=cuda selects the CUDA-core tf32 tail (output layer on the FP32 pipe too)
+static bool wide_tail32_tc() {
+    const char* v = getenv("GLX_WIDE_TAIL32");
+    return !(v && v[0] == 'c');
+}
+
 static size_t carve32(WideWork32* w, unsigned char* base, int64_t C, int splits) {
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -1952,7 +2210,18 @@ cudaError_t wide_grad_tf32(const float* W1, const float* W2, const float* X, con
             ep.t_blk = kWR;
             if ((e = launch_tc_tf32(g, ep, st)) != cudaSuccess) return e;
         }
-        if (tail) {  // 2 + 3 fused (CUDA cores): delta_o, loss, accuracy, dH^T
+        if (tail && wide_tail32_tc()) {  // 2 + 3 fused, output layer on tcgen05: delta_o, loss, accuracy, dH^T
+            CUtensorMap mh, mw;
+            if (!make_map_f32(&mh, w.H, Cc, kWH, kWH, 128) || !make_map_f32(&mw, w.W2p, 32, kWH, kWH, 16))
+                return cudaErrorInvalidValue;
+            if ((e = cudaFuncSetAttribute(wide_tail32tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kT4Smem)) != cudaSuccess)
+                return e;
+            const int grid = std::min(sm_count(), (Cc + 127) / 128);
+            wide_tail32tc_kernel<<<grid, kT4Threads, kT4Smem, st>>>(mh, mw, w.W2T, w.b2, labels + r0, Cc, w.doT,
+                                                                    w.dhT, stats);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        } else if (tail) {  // 2 + 3 fused (CUDA cores): delta_o, loss, accuracy, dH^T
             CUtensorMap mh;
             if (!make_map_f32(&mh, w.H, Cc, kWH, kWH, 128)) return cudaErrorInvalidValue;
             if ((e = cudaFuncSetAttribute(wide_tail32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -298,8 +298,9 @@ def test_wide_fused_tail_vs_unfused_and_f64(gpu, N, monkeypatch):
     assert gb[P + 1].item() + gb[P + 2].item() == N
 
 
+@pytest.mark.parametrize("variant", ["tc", "cuda"])
 @pytest.mark.parametrize("N", [4096 + 32, (1 << 19) + 32])
-def test_wide_tf32_fused_tail_vs_unfused(gpu, N, monkeypatch):
+def test_wide_tf32_fused_tail_vs_unfused(gpu, N, variant, monkeypatch):
     """tf32 path: the fused CUDA-core tail (output layer + dH in fp32, glx_tc.cu
     wide_tail32_kernel) against the tf32 GEMMs 2 and 3 it replaces, on the same f32 rows
     (one tile with a partial second, and a partial second chunk). The fused output layer
@@ -314,6 +315,7 @@ def test_wide_tf32_fused_tail_vs_unfused(gpu, N, monkeypatch):
     monkeypatch.setenv("GLX_WIDE_TAIL", "0")
     ga = wide.WideEngine(data, w1, w2).grad_sum().clone()
     monkeypatch.setenv("GLX_WIDE_TAIL", "1")
+    monkeypatch.setenv("GLX_WIDE_TAIL32", variant)  # output layer on tcgen05 (default) or the FP32 pipe
     gb = wide.WideEngine(data, w1, w2).grad_sum().clone()
     torch.cuda.synchronize()
     P = wide.WideEngine.P
@@ -321,7 +323,7 @@ def test_wide_tf32_fused_tail_vs_unfused(gpu, N, monkeypatch):
     e1 = (ga[:P1] - gb[:P1]).abs().max().item() / ga[:P1].abs().max().item()
     e2 = (ga[P1:P] - gb[P1:P]).abs().max().item() / ga[P1:P].abs().max().item()
     el = abs(ga[P].item() - gb[P].item()) / ga[P].item()
-    print(f"N={N}: tf32 fused vs unfused: dW1 {e1:.2e}, dW2 {e2:.2e}, loss {el:.2e}, "
+    print(f"N={N} {variant}: tf32 fused vs unfused: dW1 {e1:.2e}, dW2 {e2:.2e}, loss {el:.2e}, "
           f"correct {ga[P + 1].item()} vs {gb[P + 1].item()}")
     assert e1 <= 1e-3 and e2 <= 1e-3 and el <= 1e-4, (e1, e2, el)
     assert abs(ga[P + 1].item() - gb[P + 1].item()) <= 4
