@@ -922,7 +922,14 @@ constexpr int kRXT = kNB / 8 * kRR / 4 * 128;  // smem bytes, backward operand (
 constexpr int kRXFG = kFCS * kRR / 8 * 128;   // global bytes, forward operand (18 KB)
 constexpr int kRXTG = kNBS / 8 * kRR / 4 * 128;  // global bytes, backward operand (20 KB)
 constexpr int kRGT = kRXFG + kRXTG;           // global bytes per tile
-constexpr int kRS = 3;                        // stages of each ring: forward operands (freed by the
+#ifndef GLX_BTR_RS
+#define GLX_BTR_RS 2  // operand ring stages (3: 0.112 ms per 1M rows at H = 33, 2: 0.106)
+#endif
+#ifndef GLX_BTR_NB
+#define GLX_BTR_NB 2  // dh^T buffers (tile lt uses buffer lt % NB and waits for backward(lt - NB))
+#endif
+constexpr int kRNB = GLX_BTR_NB;
+constexpr int kRS = GLX_BTR_RS;                        // stages of each ring: forward operands (freed by the
                                               // forward MMA) and backward operands (freed by the backward)
 constexpr int kRZB = 3;                       // Z buffers (forward kRZB tiles ahead)
 // epilogue groups of 4 warps on alternate tiles: 3 (registers: h and the dW2 partials
@@ -945,7 +952,7 @@ struct BtrSmem {  // byte offsets
     // buffer / the backward ring (valid shared memory; their D rows are units >= HP, which
     // the drain never reads)
     static constexpr int dh = x + kRS * kRXF;
-    static constexpr int xt = dh + 2 * 4 * 8192;        // backward-operand ring
+    static constexpr int xt = dh + kRNB * 4 * 8192;     // backward-operand ring
     static constexpr int w2 = xt + kRS * kRXT;          // w2s (HP floats), b2s
     static constexpr int red = w2 + (HP + 4) * 4;        // final reductions: [warps][HP + 8]
     static constexpr int bars = red + 4 * btr_groups(HP) * (HP + 8) * 4;
@@ -990,6 +997,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
     using L = BtrSmem<HP>;
     constexpr int kRG = btr_groups(HP);
     static_assert(kRDrain % kRG == 0, "the drained tiles must all belong to group 0");
+    static_assert(kRNB <= kRG, "dh_free slots alias beyond one dh buffer per group (hangs at HP = 64 with 3 buffers)");
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::bars);
     uint64_t* x_full = bars;            // forward operand of a tile loaded
@@ -1004,8 +1012,8 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
     // dh_free[k % kRG]: backward(k) completed. Tile lt waits for backward(lt - 2) (the last
     // reader of its buffer); its group knows backward(lt - 2 - kRG) completed (its own
     // previous tile waited for it), so with kRG slots the barrier is never two phases behind
-    uint64_t* dh_free = dh_ready + 2;
-    uint64_t* fin_bar = dh_free + 3;    // the last backward completed
+    uint64_t* dh_free = dh_ready + kRNB;
+    uint64_t* fin_bar = dh_free + kRG;  // the last backward completed
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fin_bar + 1);
     float* w2s = reinterpret_cast<float*>(sm + L::w2);
     float* red = reinterpret_cast<float*>(sm + L::red);
@@ -1033,8 +1041,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             mbar_init(&z_full[b], 1);
             mbar_init(&z_free[b], 4);
         }
-        mbar_init(&dh_ready[0], 4);
-        mbar_init(&dh_ready[1], 4);
+        for (int b = 0; b < kRNB; b++) mbar_init(&dh_ready[b], 4);
         for (int b = 0; b < kRG; b++) mbar_init(&dh_free[b], 1);
         mbar_init(fin_bar, 1);
         fence_mbar_init();
@@ -1077,7 +1084,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
                                                       : sm + L::xt + st * kRXT + kRXTG + 16 * (w - (kRXF - kRXFG) / 16);
         *reinterpret_cast<uint4*>(dst) = make_uint4(0u, 0u, 0u, 0u);
     }
-    for (int i = threadIdx.x; i < 2 * 4 * 8192 / 16; i += blockDim.x)  // units HP..63 stay zero
+    for (int i = threadIdx.x; i < kRNB * 4 * 8192 / 16; i += blockDim.x)  // units HP..63 stay zero
         reinterpret_cast<uint4*>(sm + L::dh)[i] = make_uint4(0u, 0u, 0u, 0u);
     for (int i = threadIdx.x; i < a.P1; i += blockDim.x) out[i] = 0.f;
     fence_proxy_async();
@@ -1151,11 +1158,11 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
         };
         auto backward = [&](int64_t lt) {
             const int ts = (int)(lt % kRS);
-            BTR_WAIT(&dh_ready[lt & 1], (uint32_t)(lt >> 1) & 1, 3, lt);
+            BTR_WAIT(&dh_ready[lt % kRNB], (uint32_t)(lt / kRNB) & 1, 3, lt);
             BTR_WAIT(&t_full[ts], (uint32_t)(lt / kRS) & 1, 9, lt);
             tc_fence_after();
             if (GLX_DBG_ON(a) && el) {
-                dbg_expect(dv, 14, 24 + (int)(lt & 1), lt);
+                dbg_expect(dv, 14, 24 + (int)(lt % kRNB), lt);
                 dbg_expect(dv, 15, 8 + ts, lt);
                 dbg_put(dv, 12 + ts, lt);
                 dbg_put(dv, 28 + (int)(lt % kRG), lt);
@@ -1167,7 +1174,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
 #pragma unroll
                 for (int kk = 0; kk < 4; kk++) {
                     const uint32_t acc = (lt % kRDrain) != 0 || c != 0 || kk != 0;
-                    mma_ss(tmem + kRColW, dd0 + (((int)(lt & 1) * 32768 + c * 8192 + kk * 32) >> 4),
+                    mma_ss(tmem + kRColW, dd0 + (((int)(lt % kRNB) * 32768 + c * 8192 + kk * 32) >> 4),
                            dt + (((4 * c + kk) * 256) >> 4), idb, acc, el);
                 }
             }
@@ -1301,10 +1308,10 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             if (quad == 2) BTR_T(2, lt);
             // dh^T buffer lt % 2: backward(lt - 2) read it last. A drain tile also needs
             // backward(lt - 1) (the end of the accumulation it takes)
-            if (lt >= 2) {
-                BTR_WAIT(&dh_free[(lt - 2) % kRG], (uint32_t)((lt - 2) / kRG) & 1, 6, lt);
+            if (lt >= kRNB) {
+                BTR_WAIT(&dh_free[(lt - kRNB) % kRG], (uint32_t)((lt - kRNB) / kRG) & 1, 6, lt);
                 tc_fence_after();
-                if (GLX_DBG_ON(a) && lane == 0) dbg_expect(dv, 18, 28 + (int)((lt - 2) % kRG), lt - 2);
+                if (GLX_DBG_ON(a) && lane == 0) dbg_expect(dv, 18, 28 + (int)((lt - kRNB) % kRG), lt - kRNB);
             }
             if (quad == 2) BTR_T(3, lt);
             if (lt >= 1 && lt % kRDrain == 0) {  // group 0's tile: the backward of lt restarts
@@ -1313,7 +1320,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
                 drain();
             }
             {
-                unsigned char* plane = sm + L::dh + (int)(lt & 1) * 32768 + quad * 8192;
+                unsigned char* plane = sm + L::dh + (int)(lt % kRNB) * 32768 + quad * 8192;
 #pragma unroll
                 for (int j = 0; j < HP; j++)
                     *reinterpret_cast<float*>(plane + (j >> 3) * 1024 + (j & 7) * 128 +
@@ -1323,10 +1330,10 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             tc_fence_before();
             __syncwarp();
             if (GLX_DBG_ON(a) && lane == 0) {
-                dbg_put(dv, 24 + (int)(lt & 1), lt);
+                dbg_put(dv, 24 + (int)(lt % kRNB), lt);
                 atomicAdd(&dv.vb[blockIdx.x + lt * gridDim.x], 1);  // one per row quadrant
             }
-            if (lane == 0) mbar_arrive(&dh_ready[lt & 1]);
+            if (lane == 0) mbar_arrive(&dh_ready[lt % kRNB]);
             if (quad == 2) BTR_T(4, lt);
         }
         // ---------------------------------------------- per-CTA partial record
