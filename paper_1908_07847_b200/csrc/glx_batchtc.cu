@@ -940,6 +940,10 @@ __host__ __device__ constexpr int btr_groups(int HP) { return HP <= 48 ? 3 : 2; 
 // rows per TMEM fp32 partial
 constexpr int kRDrain = 48;
 constexpr int kRColW = 256;                   // dW1 accumulator columns (48)
+constexpr int kRColA = 304;                   // dW2 partials, HP columns per epilogue group
+#ifndef GLX_BTR_ACC_TMEM
+#define GLX_BTR_ACC_TMEM 1
+#endif
 __host__ __device__ constexpr int btr_threads(int HP) { return (2 + 4 * btr_groups(HP)) * 32; }
 
 template <int HP>
@@ -998,6 +1002,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
     constexpr int kRG = btr_groups(HP);
     static_assert(kRDrain % kRG == 0, "the drained tiles must all belong to group 0");
     static_assert(kRNB <= kRG, "dh_free slots alias beyond one dh buffer per group (hangs at HP = 64 with 3 buffers)");
+    static_assert(kRColA + HP * kRG <= (int)kTmemCols, "dW2 partial columns");
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::bars);
     uint64_t* x_full = bars;            // forward operand of a tile loaded
@@ -1205,9 +1210,24 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
         // its word in the tile's forward operand in global memory: [k/4][r/8][r%8][k%4]
         const int twd = (((tk >> 2) * 16 + (r >> 3)) * 8 + (r & 7)) * 4 + (tk & 3);
         const float b2s = w2s[HP];
+#if GLX_BTR_ACC_TMEM
+        // dW2 partials of this thread's row slot in TMEM (columns kRColA + HP gi ..), not
+        // registers: held across the whole tile loop they pushed the row statistics and
+        // themselves into local memory
+        const uint32_t acol = tmem + lanebase + kRColA + HP * gi;
+        {
+            uint32_t z[16];
+#pragma unroll
+            for (int i = 0; i < 16; i++) z[i] = 0u;
+#pragma unroll
+            for (int c = 0; c < HP; c += 16) st16(acol + c, z);
+            tmem_st_wait();
+        }
+#else
         float acc2[HP];
 #pragma unroll
         for (int j = 0; j < HP; j++) acc2[j] = 0.f;
+#endif
         float dsum = 0.f, loss = 0.f, c0 = 0.f, c1 = 0.f, c2 = 0.f, c3 = 0.f;
         // dW1 drain: the TMEM accumulator (lanes = units) added into the per-CTA record by
         // the warps whose quadrant holds units (unit j = lane of quadrant j / 32)
@@ -1294,6 +1314,27 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
                 dsum += d;
             }
             // dW2 += delta_o h; dh = delta_o h (1 - h) -> tf32 (h reused as dh)
+#if GLX_BTR_ACC_TMEM
+#pragma unroll
+            for (int c = 0; c < HP; c += 16) {
+                uint32_t av[16];
+                ld16(acol + c, av);
+                tmem_ld_wait();
+#pragma unroll
+                for (int i = 0; i < 16; i += 2) {
+                    const float2 hp = make_float2(h[c + i], h[c + i + 1]);
+                    const float2 v = __fmul2_rn(bcast2(d), hp);
+                    const float2 a2 = __fadd2_rn(make_float2(__uint_as_float(av[i]), __uint_as_float(av[i + 1])), v);
+                    av[i] = __float_as_uint(a2.x);
+                    av[i + 1] = __float_as_uint(a2.y);
+                    const float2 s2 = ffma2(make_float2(-v.x, -v.y), hp, v);
+                    h[c + i] = __uint_as_float(tf32_rn(s2.x));
+                    h[c + i + 1] = __uint_as_float(tf32_rn(s2.y));
+                }
+                st16(acol + c, av);
+            }
+            tmem_st_wait();  // the next tile's loads of these columns follow the stores
+#else
 #pragma unroll
             for (int i = 0; i < HP; i += 2) {
                 const float2 hp = make_float2(h[i], h[i + 1]);
@@ -1305,6 +1346,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
                 h[i] = __uint_as_float(tf32_rn(s2.x));
                 h[i + 1] = __uint_as_float(tf32_rn(s2.y));
             }
+#endif
             if (quad == 2) BTR_T(2, lt);
             // dh^T buffer lt % 2: backward(lt - 2) read it last. A drain tile also needs
             // backward(lt - 1) (the end of the accumulation it takes)
@@ -1347,6 +1389,17 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
         }
         // dW2 and the statistics: warp sums, then a fixed-order sum over the warps
         float* slot = red + ew * (HP + 8);
+#if GLX_BTR_ACC_TMEM
+        float acc2[HP];
+#pragma unroll
+        for (int c = 0; c < HP; c += 16) {
+            uint32_t av[16];
+            ld16(acol + c, av);
+            tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; i++) acc2[c + i] = __uint_as_float(av[i]);
+        }
+#endif
 #pragma unroll
         for (int j = 0; j < HP; j++) {
             float v = acc2[j];
