@@ -299,6 +299,10 @@ __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&r)[16]) {
         : "memory");
 }
 
+__device__ __forceinline__ void st2(uint32_t taddr, const uint32_t (&r)[2]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(r[0]), "r"(r[1]) : "memory");
+}
+
 __device__ __forceinline__ void st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
@@ -996,8 +1000,12 @@ __device__ __forceinline__ void btr_wait(uint64_t* bar, uint32_t parity, int tag
 #define BTR_WAIT(bar, par, tag, lt) mbar_wait(bar, par)
 #endif
 
-template <int HP>
+// HE: units the epilogue computes (H rounded up to even; HP = H padded to the MMA's N
+// granularity of 16). The padded units HE .. HP - 1 have zero weights: their dh^T rows
+// stay zero and their dW2 partials are never formed.
+template <int HP, int HE = HP>
 __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcArgs a) {
+    static_assert(HE % 2 == 0 && HE <= HP && (HE % 16 == 0 || HE % 16 == 2), "epilogue width");
     using L = BtrSmem<HP>;
     constexpr int kRG = btr_groups(HP);
     static_assert(kRDrain % kRG == 0, "the drained tiles must all belong to group 0");
@@ -1259,22 +1267,28 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             BTR_WAIT(&z_full[zb], (uint32_t)(lt / kRZB) & 1, 5, lt);
             tc_fence_after();
             if (GLX_DBG_ON(a) && lane == 0) dbg_expect(dv, 17, 16 + zb, lt);
-            float h[HP];
+            float h[HE];
             {
                 uint32_t v[32];
 #pragma unroll
-                for (int c = 0; c < HP; c += 32) {
-                    if (HP - c >= 32) {
+                for (int c = 0; c < HE; c += 32) {
+                    if (HE - c >= 32) {
                         ld32(tmem + lanebase + HP * zb + c, v);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 32; i++) h[c + i] = __uint_as_float(v[i]);
-                    } else {
+                    } else if (HE - c >= 16) {
                         uint32_t v16[16];
                         ld16(tmem + lanebase + HP * zb + c, v16);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 16; i++) h[c + i] = __uint_as_float(v16[i]);
+                    } else {
+                        uint32_t v2[2];
+                        ld2(tmem + lanebase + HP * zb + c, v2);
+                        tmem_ld_wait();
+                        h[c] = __uint_as_float(v2[0]);
+                        h[c + 1] = __uint_as_float(v2[1]);
                     }
                 }
             }
@@ -1285,7 +1299,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             if (quad == 2) BTR_T(1, lt);
             // h = sigmoid(z) (z prescaled by -log2 e), one reciprocal per pair
 #pragma unroll
-            for (int i = 0; i < HP; i += 2) {
+            for (int i = 0; i < HE; i += 2) {
                 const float2 e2 = make_float2(ex2_approx(h[i]), ex2_approx(h[i + 1]));
                 const float2 den = __fadd2_rn(fminf2(e2, bcast2(1.152921504606847e18f)), bcast2(1.0f));
                 const float rc = rcp_approx(den.x * den.y);
@@ -1295,11 +1309,17 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             }
             // the output neuron: a per-thread dot (w2s prescaled by -log2 e)
             float2 zo2 = make_float2(0.f, 0.f);
+            if constexpr (HE % 4 == 0) {
 #pragma unroll
-            for (int i = 0; i < HP; i += 4) {
-                const float4 w4 = *reinterpret_cast<const float4*>(w2s + i);
-                zo2 = ffma2(make_float2(w4.x, w4.y), make_float2(h[i], h[i + 1]), zo2);
-                zo2 = ffma2(make_float2(w4.z, w4.w), make_float2(h[i + 2], h[i + 3]), zo2);
+                for (int i = 0; i < HE; i += 4) {
+                    const float4 w4 = *reinterpret_cast<const float4*>(w2s + i);
+                    zo2 = ffma2(make_float2(w4.x, w4.y), make_float2(h[i], h[i + 1]), zo2);
+                    zo2 = ffma2(make_float2(w4.z, w4.w), make_float2(h[i + 2], h[i + 3]), zo2);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < HE; i += 2)
+                    zo2 = ffma2(*reinterpret_cast<const float2*>(w2s + i), make_float2(h[i], h[i + 1]), zo2);
             }
             float d = 0.f;
             if (row < a.N) {
@@ -1316,12 +1336,13 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             // dW2 += delta_o h; dh = delta_o h (1 - h) -> tf32 (h reused as dh)
 #if GLX_BTR_ACC_TMEM
 #pragma unroll
-            for (int c = 0; c < HP; c += 16) {
+            for (int c = 0; c < HE; c += 16) {
                 uint32_t av[16];
-                ld16(acol + c, av);
+                if (HE - c >= 16) ld16(acol + c, av);
+                else ld2(acol + c, reinterpret_cast<uint32_t(&)[2]>(av));
                 tmem_ld_wait();
 #pragma unroll
-                for (int i = 0; i < 16; i += 2) {
+                for (int i = 0; i < (HE - c >= 16 ? 16 : HE - c); i += 2) {
                     const float2 hp = make_float2(h[c + i], h[c + i + 1]);
                     const float2 v = __fmul2_rn(bcast2(d), hp);
                     const float2 a2 = __fadd2_rn(make_float2(__uint_as_float(av[i]), __uint_as_float(av[i + 1])), v);
@@ -1331,7 +1352,8 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
                     h[c + i] = __uint_as_float(tf32_rn(s2.x));
                     h[c + i + 1] = __uint_as_float(tf32_rn(s2.y));
                 }
-                st16(acol + c, av);
+                if (HE - c >= 16) st16(acol + c, av);
+                else st2(acol + c, reinterpret_cast<const uint32_t(&)[2]>(av));
             }
             tmem_st_wait();  // the next tile's loads of these columns follow the stores
 #else
@@ -1364,7 +1386,7 @@ __global__ void __launch_bounds__(btr_threads(HP), 1) batchrt_kernel(const BtcAr
             {
                 unsigned char* plane = sm + L::dh + (int)(lt % kRNB) * 32768 + quad * 8192;
 #pragma unroll
-                for (int j = 0; j < HP; j++)
+                for (int j = 0; j < HE; j++)
                     *reinterpret_cast<float*>(plane + (j >> 3) * 1024 + (j & 7) * 128 +
                                               ((((lane >> 2) ^ (j & 7))) << 4) + (lane & 3) * 4) = h[j];
             }
@@ -1568,9 +1590,12 @@ cudaError_t launch_batchrt_pack(const BatchGeom& g, const float* Xp, void* tiles
     return cudaGetLastError();
 }
 
+#ifndef GLX_BTR_NARROW34
+#define GLX_BTR_NARROW34 1  // H <= 34 at HP = 48 (the reference's default H = 33): a 34-unit epilogue
+#endif
 template <int HP>
 static cudaError_t launch_btr(const BatchGeom& g, const BtcArgs& a, cudaStream_t st) {
-    auto k = batchrt_kernel<HP>;
+    auto k = (HP == 48 && GLX_BTR_NARROW34 && g.H <= 34) ? batchrt_kernel<HP, (HP == 48 ? 34 : HP)> : batchrt_kernel<HP>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e != cudaSuccess) {
         fprintf(stderr, "glx: batchrt_kernel<%d> smem=%zu: %s\n", HP, g.smem, cudaGetErrorString(e));
