@@ -85,6 +85,14 @@ constexpr int kEpiBar = 1;
 #endif
 constexpr int kDrain = GLX_BTC_DRAIN;
 constexpr int kD1 = 34;  // dW1 columns kept per unit (D + 1 <= 34)
+#ifndef GLX_BTC_ZB
+#define GLX_BTC_ZB 2  // FAST, two unit halves: Z^T buffers (the forward runs this many tiles ahead; 2 frees the
+                      // TMEM columns of the drain sums: 0.234 -> 0.224 ms per 1M rows at H = 256, 3 without: 0.234)
+#endif
+#ifndef GLX_BTC_ACC_TMEM
+#define GLX_BTC_ACC_TMEM 1  // FAST dW1 drain sums in TMEM instead of 17 registers per thread (0: registers)
+#endif
+constexpr int kColA1 = 256;  // FAST: dW1 drain sums (needs the Z buffers below column 256)
 #ifndef GLX_BTC_RCP2
 #define GLX_BTC_RCP2 1  // 1: one MUFU reciprocal per element pair (0: one per element)
 #endif
@@ -299,6 +307,9 @@ __device__ __forceinline__ void st16(uint32_t taddr, const uint32_t (&r)[16]) {
         : "memory");
 }
 
+__device__ __forceinline__ void st1(uint32_t taddr, const uint32_t (&r)[1]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(r[0]) : "memory");
+}
 __device__ __forceinline__ void st2(uint32_t taddr, const uint32_t (&r)[2]) {
     asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(taddr), "r"(r[0]), "r"(r[1]) : "memory");
 }
@@ -377,7 +388,10 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
     using P = Pipe<FULL>;
     constexpr BtcSmem L = btc_smem<FULL>(NH);
     constexpr int kS = P::S;
-    constexpr int kZB = FULL ? 2 : (G == 2 ? 4 : 3);  // Z^T buffers (64 NH columns each)
+    constexpr int kZB = FULL ? 2 : (G == 2 ? 4 : GLX_BTC_ZB);  // Z^T buffers (64 NH columns each)
+    // FAST: the dW1 drain sums in TMEM columns kColA1 .. (17 per unit half and row block),
+    // free when the Z buffers end below them
+    constexpr bool kAccT = GLX_BTC_ACC_TMEM && !FULL && 64 * NH * kZB <= kColA1;
     static_assert(kDrain % G == 0, "the drained tiles must all belong to group 0");
     extern __shared__ __align__(1024) unsigned char sm[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L.bars);
@@ -609,10 +623,45 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
         float* out = a.part + (int64_t)blockIdx.x * a.PS;
         const uint32_t wcol = tmem + lanebase + kColW + 48 * hf;
         constexpr int kDH = kD1 / 2;  // dW1 columns drained by each row block (0..16 | 17..33)
-        float acc1[kDH];
+        const uint32_t acol1 = tmem + lanebase + kColA1 + kDH * (2 * hf + rb);
+        if constexpr (kAccT) {
+            if (gi == 0 && active) {
+                uint32_t z[16] = {}, z1[1] = {0u};
+                st16(acol1, z);
+                st1(acol1 + 16, z1);
+                tmem_st_wait();
+            }
+        }
+        float acc1[kAccT ? 1 : kDH];
 #pragma unroll
-        for (int k = 0; k < kDH; k++) acc1[k] = 0.f;
+        for (int k = 0; k < (kAccT ? 1 : kDH); k++) acc1[k] = 0.f;
         auto drain = [&]() {  // dW1 TMEM partial (this thread's unit) -> registers
+            if constexpr (kAccT) {  // ... -> the TMEM sums: add the partial to them
+                uint32_t q0[16], q1, s0[16], s1;
+                if (rb == 0) {
+                    ld16(wcol, q0);
+                    ld1(wcol + 16, q1);
+                } else {
+                    uint32_t t0[16], t1[2];
+                    ld16(wcol + 16, t0);
+                    ld2(wcol + 32, t1);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 15; k++) q0[k] = t0[k + 1];
+                    q0[15] = t1[0];
+                    q1 = t1[1];
+                }
+                ld16(acol1, s0);
+                ld1(acol1 + 16, s1);
+                tmem_ld_wait();
+#pragma unroll
+                for (int k = 0; k < 16; k++) s0[k] = __float_as_uint(__uint_as_float(s0[k]) + __uint_as_float(q0[k]));
+                uint32_t s1a[1] = {__float_as_uint(__uint_as_float(s1) + __uint_as_float(q1))};
+                st16(acol1, s0);
+                st1(acol1 + 16, s1a);
+                tmem_st_wait();
+                return;
+            }
             if (rb == 0) {
                 uint32_t r0[16], r1;
                 ld16(wcol, r0);
@@ -825,7 +874,20 @@ __global__ void __launch_bounds__(btc_threads(NH, FULL), 1) batchtc_kernel(const
             mbar_wait(fin_bar, 0);
             tc_fence_after();
             if (active) drain();  // tiles since the last drain (>= 1)
-            if (j < a.H) {
+            if constexpr (kAccT) {
+                if (active) {
+                    uint32_t s0[16], s1;
+                    ld16(acol1, s0);
+                    ld1(acol1 + 16, s1);
+                    tmem_ld_wait();
+                    if (j < a.H) {
+                        float* o1 = out + (int64_t)j * (D + 1) + kDH * rb;
+#pragma unroll
+                        for (int k = 0; k < kDH; k++)
+                            if (kDH * rb + k <= D) o1[k] = __uint_as_float(k < 16 ? s0[k] : s1);
+                    }
+                }
+            } else if (j < a.H) {
                 float* o1 = out + (int64_t)j * (D + 1) + kDH * rb;
 #pragma unroll
                 for (int k = 0; k < kDH; k++)
