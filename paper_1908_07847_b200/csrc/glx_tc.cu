@@ -273,12 +273,28 @@ __device__ __forceinline__ void store_cols_bf16(EpiStage& sg, const uint32_t (&p
     sg.release(sg.map_t, b, row0, col0, lane, sg.t_blocked);
 }
 
+// f32 accumulate into global memory without the load round trip: one writer per element
+// per launch (split-K slab), so the sum is the same a + b as a read-modify-write
+__device__ __forceinline__ void red_add_v4(float* dst, float4 v) {
+    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+#ifndef GLX_TC_RED
+#define GLX_TC_RED 1  // kind 4 (split-K accumulate) with vector reductions (0: load + add + store)
+#endif
+
 // tf32 path epilogues (f32 results): lane = row, v = 32 consecutive columns n0 + c ..
 __device__ __forceinline__ void tc_epilogue_chunk_f32(const TcEpilogue& ep, const float (&v)[32], int M, int row,
                                                       int n0, int c, int lane) {
     const bool rv = row < M;
     const int64_t kb = (int64_t)(row >> 5) * ep.t_blk;  // K block of this row (transposed outputs)
-    if (ep.kind == 0 || ep.kind == 4) {
+    if (GLX_TC_RED && ep.kind == 4) {
+        if (rv) {
+            float* dst = ep.d_f32 + (int64_t)row * ep.ldd + n0 + c;
+#pragma unroll
+            for (int q = 0; q < 8; q++) red_add_v4(dst + 4 * q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        }
+    } else if (ep.kind == 0 || ep.kind == 4) {
         if (rv) {
             float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (int64_t)row * ep.ldd + n0 + c);
 #pragma unroll
@@ -366,7 +382,13 @@ template <int BN>
 __device__ __forceinline__ void tc_epilogue_chunk(const TcEpilogue& ep, const float (&v)[32], int M, int row, int n0,
                                                   int c, int lane, EpiStage& sg) {
     const bool rv = row < M;
-    if (ep.kind == 0 || ep.kind == 4) {
+    if (GLX_TC_RED && ep.kind == 4) {
+        if (rv) {
+            float* dst = ep.d_f32 + (int64_t)row * ep.ldd + n0 + c;
+#pragma unroll
+            for (int q = 0; q < 8; q++) red_add_v4(dst + 4 * q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
+        }
+    } else if (ep.kind == 0 || ep.kind == 4) {
         if (rv) {
             float4* dst = reinterpret_cast<float4*>(ep.d_f32 + (int64_t)row * ep.ldd +
                                                     n0 + c);
