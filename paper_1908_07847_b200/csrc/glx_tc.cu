@@ -279,13 +279,16 @@ __device__ __forceinline__ void red_add_v4(float* dst, float4 v) {
     asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                  : "memory");
 }
+#ifndef GLX_TC_F32_TMA_H
+#define GLX_TC_F32_TMA_H 1  // tf32 hidden layer: H rows leave through staged TMA stores (0: per-lane float4 stores)
+#endif
 #ifndef GLX_TC_RED
 #define GLX_TC_RED 1  // kind 4 (split-K accumulate) with vector reductions (0: load + add + store)
 #endif
 
 // tf32 path epilogues (f32 results): lane = row, v = 32 consecutive columns n0 + c ..
 __device__ __forceinline__ void tc_epilogue_chunk_f32(const TcEpilogue& ep, const float (&v)[32], int M, int row,
-                                                      int n0, int c, int lane) {
+                                                      int n0, int c, int lane, EpiStage& sg) {
     const bool rv = row < M;
     const int64_t kb = (int64_t)(row >> 5) * ep.t_blk;  // K block of this row (transposed outputs)
     if (GLX_TC_RED && ep.kind == 4) {
@@ -320,10 +323,29 @@ __device__ __forceinline__ void tc_epilogue_chunk_f32(const TcEpilogue& ep, cons
 #pragma unroll
             for (int e = 0; e < 4; e++) h[4 * q + e] = 1.0f / (1.0f + __expf(-(v[4 * q + e] + bv[e])));
         }
-        if (rv && ep.h32) {
-            float4* dst = reinterpret_cast<float4*>(ep.h32 + (int64_t)row * ep.ldd + n0 + c);
+        if (ep.h32) {
+#if GLX_TC_F32_TMA_H
+            // the warp's 32 rows x 32 columns through a 128-byte-swizzled staging block and one
+            // TMA store (per-lane row stores were 32 half-sector writes per instruction);
+            // the block is reused once the previous chunk's store has read it
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+            const uint32_t b = smem_u32(sg.buf) + lane * 128;
 #pragma unroll
-            for (int q = 0; q < 8; q++) dst[q] = make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+            for (int q = 0; q < 8; q++)
+                asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(b + ((q ^ (lane & 7)) << 4)),
+                             "f"(h[4 * q]), "f"(h[4 * q + 1]), "f"(h[4 * q + 2]), "f"(h[4 * q + 3])
+                             : "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tma_store_2d(sg.map_d, sg.buf, n0 + c, row - lane);  // clips rows >= M
+#else
+            if (rv) {
+                float4* dst = reinterpret_cast<float4*>(ep.h32 + (int64_t)row * ep.ldd + n0 + c);
+#pragma unroll
+                for (int q = 0; q < 8; q++) dst[q] = make_float4(h[4 * q], h[4 * q + 1], h[4 * q + 2], h[4 * q + 3]);
+            }
+#endif
         }
         if (rv && ep.t32) {
 #pragma unroll
@@ -519,7 +541,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
     uint64_t* tfull = empty + kTcStages;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    uint16_t* stg_all = reinterpret_cast<uint16_t*>(sm + kTcStages * kStage + 256);
+    // staging blocks start 1024-aligned (the tf32 path's 128-byte-swizzled TMA stores)
+    uint16_t* stg_all = reinterpret_cast<uint16_t*>(sm + kTcStages * kStage + 1024);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nkt = K / kBKe;
@@ -652,7 +675,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __uint_as_float(ra[i]);
-                        if constexpr (TF) tc_epilogue_chunk_f32(e2, v, M, row, n0, c, lane);
+                        if constexpr (TF) tc_epilogue_chunk_f32(e2, v, M, row, n0, c, lane, sg);
                         else tc_epilogue_chunk<BN>(e2, v, M, row, n0, c, lane, sg);
                     }
                     if (!more) break;
@@ -662,7 +685,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const __grid_con
                         float v[32];
 #pragma unroll
                         for (int i = 0; i < 32; i++) v[i] = __uint_as_float(rb[i]);
-                        if constexpr (TF) tc_epilogue_chunk_f32(e2, v, M, row, n0, c + 32, lane);
+                        if constexpr (TF) tc_epilogue_chunk_f32(e2, v, M, row, n0, c + 32, lane, sg);
                         else tc_epilogue_chunk<BN>(e2, v, M, row, n0, c + 32, lane, sg);
                     }
                     tmem_wait();
@@ -763,8 +786,19 @@ static cudaError_t tc_launch_tf32(const TcGemm& g, const TcEpilogue& ep, cudaStr
     const bool oka = g.a_blk ? make_map_blk32(&ma, g.A, g.a_blk, nkb, kTcBM) : make_map_f32(&ma, g.A, g.M, g.K, g.lda, kTcBM);
     const bool okb = g.b_blk ? make_map_blk32(&mb, g.B, g.b_blk, nkb, BN) : make_map_f32(&mb, g.B, g.N, g.K, g.ldb, BN);
     if (!oka || !okb || g.a_mn || g.b_mn) return cudaErrorInvalidValue;
+    if (GLX_TC_F32_TMA_H && ep.kind == 1 && ep.h32) {  // H (f32, row-major) stores: 32 x 32 boxes, 128-byte swizzle
+        EncodeTiledFn fn = encode_fn();
+        cuuint64_t dims[2] = {(cuuint64_t)g.N, (cuuint64_t)g.M};
+        cuuint64_t strides[1] = {(cuuint64_t)ep.ldd * 4};
+        cuuint32_t box[2] = {32, 32};
+        cuuint32_t estr[2] = {1, 1};
+        if (!fn || fn(&md, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, ep.h32, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
     const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0);
-    const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * 128 + 256 + kTcStgBytes;
+    const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * 128 + 1024 + kTcStgBytes;
     auto k = tc_gemm_kernel<BN, true>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -816,7 +850,7 @@ static cudaError_t tc_launch(const TcGemm& g, const TcEpilogue& ep, cudaStream_t
         if (!ok) return cudaErrorInvalidValue;
     }
     const int flags = (g.a_blk ? 1 : 0) | (g.b_blk ? 2 : 0) | (ep.t_blk ? 4 : 0) | (g.a_mn ? 8 : 0) | (g.b_mn ? 16 : 0);
-    const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 256 + kTcStgBytes;
+    const size_t smem = 1024 + (size_t)tc_stages(BN) * (kTcBM + BN) * kTcBK * 2 + 1024 + kTcStgBytes;
     auto k = tc_gemm_kernel<BN, false>;
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
