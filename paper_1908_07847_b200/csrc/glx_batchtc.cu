@@ -62,12 +62,15 @@ constexpr int kWT = 16 * kFC * 128;            // bytes per 128-unit weight copy
 // too few rows average the operand rounding out) is 3xTF32 on both GEMMs (x and dh
 // split into hi + lo as well), which needs the lo copies of x and a dh lo TMEM
 // buffer. Stage counts per precision (shared memory, TMEM):
+#ifndef GLX_BTC_S
+#define GLX_BTC_S 6  // FAST tile-ring stages
+#endif
 template <bool FULL>
 struct Pipe {
     static constexpr int NX = FULL ? 2 : 1;                       // x operand copies: hi (+ lo)
     static constexpr int STAGE = NX * (kXF + kXT);                 // smem bytes per tile stage
     static constexpr int GTILE = NX * (kXFG + kXTG);               // global bytes per tile
-    static constexpr int S = FULL ? 3 : 6;                         // tile stages (free after the backward)
+    static constexpr int S = FULL ? 3 : GLX_BTC_S;                 // tile stages (free after the backward)
     static constexpr int ZB = FULL ? 2 : 3;                        // Z^T buffers: the forward runs ZB tiles ahead
 };
 constexpr uint32_t kTf32Mask = 0xFFFFE000u;
